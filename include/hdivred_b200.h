@@ -1,0 +1,189 @@
+/* hdivred_b200.h — C ABI of the B200-native element-local hybridization /
+ * static-condensation hot path (arXiv 1801.08914, reference: hdivred).
+ *
+ * Plain C: pointers, sizes, status codes.  No torch or CUDA types.  Every entry
+ * point names the reference interface it replaces (paths relative to
+ * /root/reference/proj).  A C++ drop-in for the reference signatures is in
+ * shim/hdivred_b200_shim.cpp; ctypes/pybind bindings are shown in
+ * INTEGRATION.md.
+ *
+ * Conventions
+ *  - index width on the boundary is int64 (include/hdivred/dense.hpp:9,
+ *    index_t); CSR arrays follow CsrMatrix (include/hdivred/csr.hpp:13-42):
+ *    row_offsets[nrows+1], col_indices[nnz] strictly increasing per row,
+ *    values[nnz]; explicit zeros kept.
+ *  - dense blocks are row-major fp64 (include/hdivred/dense.hpp:12-25).
+ *  - "on_device" flags: 0 = host pointers (copied through the library's
+ *    stream), 1 = device pointers already resident in HBM.
+ *  - every call is synchronous with respect to the host unless it says
+ *    otherwise; results are bit-identical for identical inputs (the
+ *    deterministic scatter has no float atomics).
+ *  - errors: a non-zero hdr_status; hdr_last_error() returns a thread-local
+ *    message.  The C++ shim maps HDR_SINGULAR_BLOCK → hdivred::SingularBlock,
+ *    HDR_DIMENSION_MISMATCH → DimensionMismatch, HDR_VALIDATION →
+ *    ValidationError (include/hdivred/errors.hpp:9-47).
+ */
+#ifndef HDIVRED_B200_H
+#define HDIVRED_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  HDR_OK = 0,
+  HDR_SINGULAR_BLOCK = 1,     /* hdivred::SingularBlock (errors.hpp:15) */
+  HDR_DIMENSION_MISMATCH = 2, /* hdivred::DimensionMismatch (errors.hpp:9) */
+  HDR_VALIDATION = 3,         /* hdivred::ValidationError (errors.hpp:44) */
+  HDR_UNSUPPORTED = 4,        /* input outside what the device path implements (typed, never silent) */
+  HDR_CUDA_ERROR = 5,         /* CUDA runtime failure, or no device */
+  HDR_INVALID_ARGUMENT = 6    /* std::invalid_argument in the reference */
+} hdr_status;
+
+typedef struct hdr_space_s* hdr_space_t;         /* mesh + RT_k space + device pattern + fixed factors */
+typedef struct hdr_hybrid_s* hdr_hybrid_t;       /* HybridizedOperator (reduction.hpp:49-68) on the device */
+typedef struct hdr_condensed_s* hdr_condensed_t; /* CondensedOperator (reduction.hpp:78-95) on the device */
+
+/* Space information indices for hdr_space_info(). */
+enum {
+  HDR_INFO_DIM = 0,
+  HDR_INFO_ORDER,
+  HDR_INFO_NCELLS,
+  HDR_INFO_NFACES,
+  HDR_INFO_NDOFS,          /* RtSpace::ndofs */
+  HDR_INFO_BROKEN_NDOFS,   /* RtSpace::broken_ndofs */
+  HDR_INFO_ELEMENT_NDOFS,  /* n */
+  HDR_INFO_DOFS_PER_FACE,  /* dpf */
+  HDR_INFO_INTERIOR_DOFS,  /* per cell */
+  HDR_INFO_FACE_DOF_COUNT, /* RtSpace::face_dof_count */
+  HDR_INFO_M,              /* multiplier count = rows of H */
+  HDR_INFO_NNZ_H,
+  HDR_INFO_NS,             /* rows of S = master count */
+  HDR_INFO_NNZ_S,
+  HDR_INFO_DIV_RANK,       /* rank of the reference divdiv (structured path) */
+  HDR_INFO_COUNT
+};
+
+/* ------------------------------------------------------------------ space */
+
+/* Builds the FE space on the device.  Replaces build_mesh (src/mesh.cpp:137)
+ * + build_space (src/rt_space.cpp:318) as far as the hot path needs them.
+ *  dim 2|3; cells[3]; cell sizes h[3] (cells congruent, axis aligned); order k
+ *  in 0..3 (the reference allows 0..1, src/rt_space.cpp:319; 2..3 follow the
+ *  guard-lifted reference).
+ *  ref_divdiv / ref_mass: the reference element matrices (RtSpace::ref_divdiv /
+ *  ref_mass, n*n row-major).  Pass NULL to have the library build them with
+ *  its bit-exact restatement of build_reference (src/rt_space.cpp:180-314).
+ *  weighted: 1 = mass-weighted constraint rows (build_C weighted=true,
+ *  src/reduction.cpp:182-195); ref_face_moments (2*dim*dpf*n) is then used
+ *  (NULL → built internally).
+ * Builds the H and S CSR patterns (bit-exact with hybridize/static_condense's
+ * from_triplets output) once, on the device. */
+hdr_status hdr_space_create(int dim, const int64_t cells[3], const double h[3], int order, const double* ref_divdiv,
+                            const double* ref_mass, int weighted, const double* ref_face_moments, hdr_space_t* out);
+void hdr_space_destroy(hdr_space_t space);
+/* out[HDR_INFO_COUNT] */
+hdr_status hdr_space_info(hdr_space_t space, int64_t* out);
+/* Copies the reference element matrices the space uses (n*n each; NULL skips). */
+hdr_status hdr_space_reference(hdr_space_t space, double* ref_divdiv, double* ref_mass);
+/* ref_unit_load (RtSpace::ref_unit_load, src/rt_space.cpp:254-255): 3*n, the load
+ * of a constant unit field per component; the FE load of build_reduction_inputs
+ * is sum_c g[c] * unit_load[c] (src/rt_space.cpp:361-364). */
+hdr_status hdr_space_unit_load(hdr_space_t space, double* out);
+/* Binds a CUDA stream (cudaStream_t passed as void*) for all later work on
+ * this space and its operators; NULL = the library's own stream. */
+hdr_status hdr_space_set_stream(hdr_space_t space, void* stream);
+/* which = 0: H pattern (m x m); 1: S pattern (nS x nS).  Host copies, int64. */
+hdr_status hdr_space_pattern(hdr_space_t space, int which, int64_t* row_offsets, int64_t* col_indices);
+/* master_globals of static_condense (src/reduction.cpp:509-521), int64, nS entries. */
+hdr_status hdr_space_master_globals(hdr_space_t space, int64_t* out);
+/* Signed local->global dof map of every cell (local_dof_map,
+ * src/rt_space.cpp:383-393): global[ncells*n] int64, sign[ncells*n]. */
+hdr_status hdr_space_dof_map(hdr_space_t space, int64_t* global, double* sign);
+
+/* ------------------------------------------------------------- hybridize */
+
+/* FE fast path of hybridize (src/reduction.cpp:262-354) fused with the
+ * element assembly it consumes (build_reduction_inputs → element_matrices,
+ * src/reduction.cpp:200-222, src/rt_space.cpp:345-374):
+ *   A_T = fl(fl(alpha_T * ref_divdiv) + fl(beta_T * ref_mass))   (bit-exact)
+ *   H   = sum_T C_T A_T^-1 C_T^T,  g = sum_T C_T A_T^-1 f_T
+ * scattered into the space's H pattern without float atomics.
+ * alpha, beta: ncells; f_hat: broken_ndofs (cell-major, local dof order).
+ * Creates a new operator in *out (device resident; nothing is copied back). */
+hdr_status hdr_hybridize_fe(hdr_space_t space, const double* alpha, const double* beta, const double* f_hat,
+                            int on_device, hdr_hybrid_t* out);
+/* Same, reusing an existing operator's device buffers (steady-state loop). */
+hdr_status hdr_hybridize_fe_into(hdr_hybrid_t op, const double* alpha, const double* beta, const double* f_hat,
+                                 int on_device);
+void hdr_hybrid_destroy(hdr_hybrid_t op);
+/* Copy H values (nnz_H, in the space's pattern order) and/or g (m); NULL
+ * skips.  dst_on_device selects device-to-device copies. */
+hdr_status hdr_hybrid_values(hdr_hybrid_t op, double* h_values, double* g, int dst_on_device);
+/* Device pointers of H values / g / pattern (borrowed; valid while op lives).
+ * row_offsets are int64, col_indices int32 on the device. */
+hdr_status hdr_hybrid_device_ptrs(hdr_hybrid_t op, const double** h_values, const double** g,
+                                  const int64_t** row_offsets, const int32_t** col_indices);
+
+/* recover_hybrid (src/reduction.cpp:356-446):
+ *   x_hat = A_hat^-1 (f_hat - C^T lambda)   (broken_ndofs)
+ *   x     = (P^T P)^-1 P^T x_hat            (ndofs)
+ * lambda: m; f_hat: broken_ndofs.  Either output may be NULL. */
+hdr_status hdr_recover_hybrid(hdr_hybrid_t op, const double* lambda, const double* f_hat, int on_device,
+                              double* x_hat, double* x);
+
+/* ---------------------------------------------------- static condensation */
+
+/* static_condense (src/reduction.cpp:448-557) on the FE path, marker
+ * partition i = element bubbles: S = sum_T P_b^T (A_bb - A_bi A_ii^-1 A_ib) P_b,
+ * f_S likewise. */
+hdr_status hdr_static_condense_fe(hdr_space_t space, const double* alpha, const double* beta, const double* f_hat,
+                                  int on_device, hdr_condensed_t* out);
+hdr_status hdr_static_condense_fe_into(hdr_condensed_t op, const double* alpha, const double* beta,
+                                       const double* f_hat, int on_device);
+void hdr_condensed_destroy(hdr_condensed_t op);
+hdr_status hdr_condensed_values(hdr_condensed_t op, double* s_values, double* f_s, int dst_on_device);
+/* recover_condensed (src/reduction.cpp:559-587): x (ndofs) from x_b (nS). */
+hdr_status hdr_recover_condensed(hdr_condensed_t op, const double* x_b, const double* f_hat, int on_device,
+                                 double* x);
+
+/* ------------------------------------------------------------------ spmv */
+
+/* spmv (src/csr.cpp:77-87) with the operator's reduced matrix: y = H x
+ * (hybrid) / y = S x (condensed).  Row sums accumulate in storage order. */
+hdr_status hdr_hybrid_spmv(hdr_hybrid_t op, const double* x, double* y, int on_device);
+hdr_status hdr_condensed_spmv(hdr_condensed_t op, const double* x, double* y, int on_device);
+/* General CSR SpMV on device arrays (int64 offsets, int64 columns). */
+hdr_status hdr_csr_spmv_device(int64_t nrows, const int64_t* row_offsets, const int64_t* col_indices,
+                               const double* values, const double* x, double* y, void* stream);
+
+/* ------------------------------------------------- host-only introspection */
+
+/* The reference element matrices of RT_k on an h[0] x h[1] (x h[2]) box,
+ * bit-identical to build_reference (src/rt_space.cpp:180-314): divdiv, mass
+ * (n*n), face_moments (2*dim*dpf*n), unit_load (3*n).  NULL skips.  Host only. */
+hdr_status hdr_reference_element(int dim, int order, const double h[3], double* divdiv, double* mass,
+                                 double* face_moments, double* unit_load);
+/* Fixed factors of the structured element solve: X (n*r), lambda
+ * (r), E, N0, Ma (n*n); diag = {rho, max|E|/max|D|, max|X^T M X - I|, block
+ * diagonal M}.  Host only. */
+hdr_status hdr_structured_factors(int dim, int order, const double h[3], double* X, double* lambda, double* E,
+                                  double* N0, double* Ma, double* diag, int64_t* rank);
+
+/* ------------------------------------------------------------------ misc */
+
+const char* hdr_last_error(void);
+/* Build/version string: "hdivred_b200 <ver> sm_100a". */
+const char* hdr_version(void);
+/* Number of kernels this library launched since load (launch accounting for
+ * bench.py's gpu_launches). */
+int64_t hdr_launch_count(void);
+/* Synchronize the space's stream. */
+hdr_status hdr_space_synchronize(hdr_space_t space);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,493 @@
+"""B200-native element-local hybridization / static condensation for RT_k H(div)
+systems (arXiv 1801.08914), a drop-in for the reference toolkit ``hdivred``'s
+hot path.
+
+Host-side mirror of the reference interfaces for this path:
+
+* ``hybridized_matrix(config)`` / ``space_info(dim, cells, order)`` and the
+  exception names mirror the pybind11 module ``hdivred._core``
+  (bindings/module.cpp:75-174 of the reference);
+* ``Space`` / ``HybridizedOperator`` / ``CondensedOperator`` mirror
+  ``build_space`` + ``hybridize`` / ``recover_hybrid`` / ``static_condense`` /
+  ``recover_condensed`` / ``spmv`` (include/hdivred/reduction.hpp,
+  include/hdivred/csr.hpp) as far as the FE fast path goes.
+
+All compute goes through the C ABI of ``libhdivred_b200.so`` (hand-written
+sm_100a CUDA); there is no CPU fallback.  Arrays may be numpy (host) or torch
+CUDA tensors (device resident, float64, contiguous).
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import _capi
+
+__version__ = "0.1.0"
+
+
+class HdivredError(RuntimeError):
+    pass
+
+
+class SingularBlockError(HdivredError):
+    """hdivred::SingularBlock (include/hdivred/errors.hpp:15)."""
+
+
+class CapExceededError(HdivredError):
+    """hdivred::CapExceeded (include/hdivred/errors.hpp:20)."""
+
+
+class FormatError(HdivredError):
+    """hdivred::FormatError (include/hdivred/errors.hpp:25)."""
+
+
+class ValidationError(HdivredError):
+    """hdivred::ValidationError (include/hdivred/errors.hpp:44)."""
+
+
+class DimensionMismatch(HdivredError):
+    """hdivred::DimensionMismatch (include/hdivred/errors.hpp:9)."""
+
+
+class UnsupportedError(HdivredError):
+    """Input outside what the device path implements (never silently ignored)."""
+
+
+class DeviceError(HdivredError):
+    """CUDA failure or no device (the hot path has no CPU fallback)."""
+
+
+_STATUS_EXC = {
+    _capi.SINGULAR_BLOCK: SingularBlockError,
+    _capi.DIMENSION_MISMATCH: DimensionMismatch,
+    _capi.VALIDATION: ValidationError,
+    _capi.UNSUPPORTED: UnsupportedError,
+    _capi.CUDA_ERROR: DeviceError,
+    _capi.INVALID_ARGUMENT: ValueError,
+}
+
+
+def _check(status: int) -> None:
+    if status != _capi.OK:
+        raise _STATUS_EXC.get(status, HdivredError)(_capi.last_error())
+
+
+def _lib():
+    return _capi.load()
+
+
+def _ptr(a) -> tuple[int, int]:
+    """(address, on_device) of a float64/int64 numpy array or torch tensor."""
+    if isinstance(a, np.ndarray):
+        if not a.flags.c_contiguous:
+            raise ValueError("array must be C-contiguous")
+        return a.ctypes.data, 0
+    if hasattr(a, "data_ptr") and hasattr(a, "is_cuda"):
+        if not a.is_contiguous():
+            raise ValueError("tensor must be contiguous")
+        return a.data_ptr(), 1 if a.is_cuda else 0
+    raise TypeError(f"unsupported array type {type(a)}")
+
+
+def _as_f64(a, n: int, name: str):
+    if isinstance(a, np.ndarray) or not hasattr(a, "data_ptr"):
+        a = np.ascontiguousarray(a, dtype=np.float64)
+        if a.size != n:
+            raise DimensionMismatch(f"{name}: expected {n} values, got {a.size}")
+        return a
+    import torch
+
+    if a.dtype != torch.float64:
+        raise TypeError(f"{name}: tensor must be float64")
+    if a.numel() != n:
+        raise DimensionMismatch(f"{name}: expected {n} values, got {a.numel()}")
+    return a.contiguous()
+
+
+def _same_device(arrays) -> int:
+    flags = {_ptr(a)[1] for a in arrays}
+    if len(flags) != 1:
+        raise ValueError("inputs must be all host arrays or all CUDA tensors")
+    return flags.pop()
+
+
+class Space:
+    """Structured mesh + RT_k space with its device-resident H/S patterns.
+
+    Mirrors build_mesh + build_space (src/mesh.cpp:137, src/rt_space.cpp:318):
+    ``cells`` per axis, ``sizes`` per axis (default 1/cells: unit cube),
+    ``order`` k in 0..3.  ``ref_divdiv``/``ref_mass`` may be given to bind the
+    reference element matrices of an existing RtSpace; by default the library's
+    bit-exact restatement of build_reference builds them.
+    """
+
+    def __init__(self, dim: int, cells: Sequence[int], order: int, sizes: Optional[Sequence[float]] = None,
+                 ref_divdiv=None, ref_mass=None):
+        cells = list(cells) + [1] * (3 - len(cells))
+        if sizes is None:
+            sizes = [1.0 / c if a < dim else 1.0 for a, c in enumerate(cells)]
+        sizes = list(sizes) + [1.0] * (3 - len(sizes))
+        carr = (ctypes.c_int64 * 3)(*[int(c) for c in cells[:3]])
+        harr = (ctypes.c_double * 3)(*[float(s) for s in sizes[:3]])
+        dd = mm = None
+        if ref_divdiv is not None:
+            dd = np.ascontiguousarray(ref_divdiv, dtype=np.float64)
+            mm = np.ascontiguousarray(ref_mass, dtype=np.float64)
+        h = ctypes.c_void_p()
+        _check(_lib().hdr_space_create(dim, ctypes.addressof(carr), ctypes.addressof(harr), order,
+                                       None if dd is None else dd.ctypes.data,
+                                       None if mm is None else mm.ctypes.data, 0, None, ctypes.byref(h)))
+        self._h = h
+        info = np.zeros(len(_capi.INFO_NAMES), np.int64)
+        _check(_lib().hdr_space_info(self._h, info.ctypes.data))
+        self.info = {k: int(v) for k, v in zip(_capi.INFO_NAMES, info)}
+        self.dim, self.order = dim, order
+        self.cells = tuple(cells[:dim])
+        self.sizes = tuple(sizes[:3])
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            _lib().hdr_space_destroy(h)
+            self._h = None
+
+    # sizes
+    @property
+    def ncells(self) -> int:
+        return self.info["ncells"]
+
+    @property
+    def n(self) -> int:
+        return self.info["element_ndofs"]
+
+    @property
+    def m(self) -> int:
+        return self.info["m"]
+
+    @property
+    def broken_ndofs(self) -> int:
+        return self.info["broken_ndofs"]
+
+    @property
+    def ndofs(self) -> int:
+        return self.info["ndofs"]
+
+    def reference_matrices(self):
+        n = self.n
+        dd = np.empty(n * n)
+        mm = np.empty(n * n)
+        _check(_lib().hdr_space_reference(self._h, dd.ctypes.data, mm.ctypes.data))
+        return dd.reshape(n, n), mm.reshape(n, n)
+
+    def unit_load(self) -> np.ndarray:
+        ul = np.empty(3 * self.n)
+        _check(_lib().hdr_space_unit_load(self._h, ul.ctypes.data))
+        return ul.reshape(3, self.n)
+
+    def load_vector(self, g=(1.0, 1.0, 1.0)) -> np.ndarray:
+        """FE load f_hat of build_reduction_inputs (rt_space.cpp:361-364), broken order."""
+        ul = self.unit_load()
+        load = np.zeros(self.n)
+        for c in range(self.dim):
+            load = load + g[c] * ul[c]
+        return np.tile(load, self.ncells)
+
+    def pattern(self, which: str = "H"):
+        nr = self.m if which == "H" else self.info["n_s"]
+        nz = self.info["nnz_h"] if which == "H" else self.info["nnz_s"]
+        ro = np.empty(nr + 1, np.int64)
+        ci = np.empty(nz, np.int64)
+        _check(_lib().hdr_space_pattern(self._h, 0 if which == "H" else 1, ro.ctypes.data, ci.ctypes.data))
+        return ro, ci
+
+    def master_globals(self) -> np.ndarray:
+        out = np.empty(self.info["n_s"], np.int64)
+        _check(_lib().hdr_space_master_globals(self._h, out.ctypes.data))
+        return out
+
+    def dof_map(self):
+        gl = np.empty(self.broken_ndofs, np.int64)
+        sg = np.empty(self.broken_ndofs)
+        _check(_lib().hdr_space_dof_map(self._h, gl.ctypes.data, sg.ctypes.data))
+        return gl, sg
+
+    def set_stream(self, stream_ptr: Optional[int]) -> None:
+        """Run on a caller's CUDA stream (e.g. torch.cuda.current_stream().cuda_stream)."""
+        _check(_lib().hdr_space_set_stream(self._h, ctypes.c_void_p(stream_ptr) if stream_ptr else None))
+
+    def synchronize(self) -> None:
+        _check(_lib().hdr_space_synchronize(self._h))
+
+    # ---- hot path
+    def hybridize(self, alpha, beta, f_hat) -> "HybridizedOperator":
+        """hybridize (src/reduction.cpp:262-354) of the FE inputs (alpha, beta per cell, f_hat)."""
+        a = _as_f64(alpha, self.ncells, "alpha")
+        b = _as_f64(beta, self.ncells, "beta")
+        f = _as_f64(f_hat, self.broken_ndofs, "f_hat")
+        dev = _same_device([a, b, f])
+        h = ctypes.c_void_p()
+        _check(_lib().hdr_hybridize_fe(self._h, _ptr(a)[0], _ptr(b)[0], _ptr(f)[0], dev, ctypes.byref(h)))
+        return HybridizedOperator(self, h)
+
+    def static_condense(self, alpha, beta, f_hat) -> "CondensedOperator":
+        """static_condense (src/reduction.cpp:448-557) of the FE inputs."""
+        a = _as_f64(alpha, self.ncells, "alpha")
+        b = _as_f64(beta, self.ncells, "beta")
+        f = _as_f64(f_hat, self.broken_ndofs, "f_hat")
+        dev = _same_device([a, b, f])
+        h = ctypes.c_void_p()
+        _check(_lib().hdr_static_condense_fe(self._h, _ptr(a)[0], _ptr(b)[0], _ptr(f)[0], dev, ctypes.byref(h)))
+        return CondensedOperator(self, h)
+
+
+class HybridizedOperator:
+    """Device-resident HybridizedOperator (include/hdivred/reduction.hpp:49-68)."""
+
+    def __init__(self, space: Space, handle):
+        self.space = space
+        self._h = handle
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            _lib().hdr_hybrid_destroy(h)
+            self._h = None
+
+    def rehybridize(self, alpha, beta, f_hat) -> None:
+        sp = self.space
+        a = _as_f64(alpha, sp.ncells, "alpha")
+        b = _as_f64(beta, sp.ncells, "beta")
+        f = _as_f64(f_hat, sp.broken_ndofs, "f_hat")
+        dev = _same_device([a, b, f])
+        _check(_lib().hdr_hybridize_fe_into(self._h, _ptr(a)[0], _ptr(b)[0], _ptr(f)[0], dev))
+
+    def values(self):
+        """(H values in pattern order, g) as host arrays."""
+        hv = np.empty(self.space.info["nnz_h"])
+        g = np.empty(self.space.m)
+        _check(_lib().hdr_hybrid_values(self._h, hv.ctypes.data, g.ctypes.data, 0))
+        return hv, g
+
+    def h_mat(self):
+        """CsrMatrix as the reference's csr_to_tuple: (nrows, ncols, row_offsets, col_indices, values)."""
+        ro, ci = self.space.pattern("H")
+        hv, _ = self.values()
+        return self.space.m, self.space.m, ro, ci, hv
+
+    def recover(self, lam, f_hat):
+        """recover_hybrid (src/reduction.cpp:356-446): returns (x_hat, x)."""
+        sp = self.space
+        lam = _as_f64(lam, sp.m, "lambda")
+        f = _as_f64(f_hat, sp.broken_ndofs, "f_hat")
+        dev = _same_device([lam, f])
+        if dev:
+            import torch
+
+            xh = torch.empty(sp.broken_ndofs, dtype=torch.float64, device=lam.device)
+            x = torch.empty(sp.ndofs, dtype=torch.float64, device=lam.device)
+        else:
+            xh = np.empty(sp.broken_ndofs)
+            x = np.empty(sp.ndofs)
+        _check(_lib().hdr_recover_hybrid(self._h, _ptr(lam)[0], _ptr(f)[0], dev, _ptr(xh)[0], _ptr(x)[0]))
+        return xh, x
+
+    def spmv(self, x):
+        """y = H x (spmv, src/csr.cpp:77-87)."""
+        sp = self.space
+        x = _as_f64(x, sp.m, "x")
+        dev = _ptr(x)[1]
+        if dev:
+            import torch
+
+            y = torch.empty(sp.m, dtype=torch.float64, device=x.device)
+        else:
+            y = np.empty(sp.m)
+        _check(_lib().hdr_hybrid_spmv(self._h, _ptr(x)[0], _ptr(y)[0], dev))
+        return y
+
+
+class CondensedOperator:
+    """Device-resident CondensedOperator (include/hdivred/reduction.hpp:78-95)."""
+
+    def __init__(self, space: Space, handle):
+        self.space = space
+        self._h = handle
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            _lib().hdr_condensed_destroy(h)
+            self._h = None
+
+    def values(self):
+        sv = np.empty(self.space.info["nnz_s"])
+        fs = np.empty(self.space.info["n_s"])
+        _check(_lib().hdr_condensed_values(self._h, sv.ctypes.data, fs.ctypes.data, 0))
+        return sv, fs
+
+    def s_mat(self):
+        ro, ci = self.space.pattern("S")
+        sv, _ = self.values()
+        ns = self.space.info["n_s"]
+        return ns, ns, ro, ci, sv
+
+    def recover(self, x_b, f_hat):
+        """recover_condensed (src/reduction.cpp:559-587): full global solution."""
+        sp = self.space
+        xb = _as_f64(x_b, sp.info["n_s"], "x_b")
+        f = _as_f64(f_hat, sp.broken_ndofs, "f_hat")
+        dev = _same_device([xb, f])
+        if dev:
+            import torch
+
+            x = torch.empty(sp.ndofs, dtype=torch.float64, device=xb.device)
+        else:
+            x = np.empty(sp.ndofs)
+        _check(_lib().hdr_recover_condensed(self._h, _ptr(xb)[0], _ptr(f)[0], dev, _ptr(x)[0]))
+        return x
+
+    def spmv(self, x):
+        sp = self.space
+        x = _as_f64(x, sp.info["n_s"], "x")
+        dev = _ptr(x)[1]
+        if dev:
+            import torch
+
+            y = torch.empty(sp.info["n_s"], dtype=torch.float64, device=x.device)
+        else:
+            y = np.empty(sp.info["n_s"])
+        _check(_lib().hdr_condensed_spmv(self._h, _ptr(x)[0], _ptr(y)[0], dev))
+        return y
+
+
+# ------------------------------------------------------------------ reference-mirroring front-end
+
+def _axes(v, dim, default):
+    if v is None:
+        return list(default)
+    if isinstance(v, (list, tuple)):
+        out = list(default)
+        for a in range(min(3, len(v))):
+            out[a] = v[a]
+        return out
+    return [v, v, v]
+
+
+def coefficients_from_config(config: dict, space: Space):
+    """Per-cell (alpha, beta) as the reference's build_problem (src/driver.cpp:166-197):
+    uniform alpha/beta, the soft-hard preset (src/mesh.cpp:168-191) or a coefficient file
+    (src/mesh.cpp:193-221)."""
+    nc = space.ncells
+    preset = config.get("coeff_preset", "")
+    if preset == "soft-hard":
+        p = int(config.get("p", 0))
+        jump = math.pow(10.0, p)
+        alpha = np.ones(nc)
+        beta = np.ones(nc)
+        n0, n1, n2 = (list(space.cells) + [1, 1])[:3]
+        h = space.sizes
+        idx = np.arange(nc)
+        co = [idx % n0, (idx // n0) % n1, idx // (n0 * n1)]
+        in_lo = np.ones(nc, bool)
+        in_hi = np.ones(nc, bool)
+        for a in range(space.dim):
+            t = 0.0 + (co[a].astype(np.float64) + 0.5) * h[a]
+            in_lo &= (t >= 0.25) & (t <= 0.5)
+            in_hi &= (t >= 0.5) & (t <= 0.75)
+        beta[in_lo | in_hi] = jump
+        return alpha, beta
+    if preset:
+        raise ValueError(f"unknown coefficient preset '{preset}'")
+    if config.get("coeff_file"):
+        alpha = np.empty(nc)
+        beta = np.empty(nc)
+        expected = 0
+        with open(config["coeff_file"]) as fh:
+            for line_no, line in enumerate(fh, 1):
+                if not line.strip() or line.startswith("#"):
+                    continue
+                parts = line.split()
+                if len(parts) < 3:
+                    raise FormatError(f"bad coefficient line (line {line_no})")
+                cell, a, b = int(parts[0]), float(parts[1]), float(parts[2])
+                if cell != expected:
+                    raise FormatError(f"coefficient lines must be in lexicographic cell order (line {line_no})")
+                if not (a > 0 and b > 0 and math.isfinite(a) and math.isfinite(b)):
+                    raise FormatError(f"coefficients must be positive and finite (line {line_no})")
+                alpha[cell], beta[cell] = a, b
+                expected += 1
+        if expected != nc:
+            raise FormatError(f"coefficient file has {expected} cells, mesh has {nc}")
+        return alpha, beta
+    a = float(config.get("alpha", 1.0))
+    b = float(config.get("beta", 1.0))
+    if not (a > 0 and b > 0):
+        raise ValueError("coefficients must be positive")
+    return np.full(nc, a), np.full(nc, b)
+
+
+def space_from_config(config: dict) -> Space:
+    dim = int(config.get("dim", 3))
+    cells = [int(c) for c in _axes(config.get("cells"), dim, [8, 8, 8])]
+    sizes = [float(s) for s in _axes(config.get("sizes"), dim, [0.0, 0.0, 0.0])]
+    for a in range(dim):
+        if sizes[a] == 0.0:
+            sizes[a] = 1.0 / cells[a]
+    if dim == 2:
+        cells[2], sizes[2] = 1, 1.0
+    if config.get("weighted", False):
+        raise UnsupportedError("weighted constraint rows are not implemented on the device path yet")
+    if config.get("essential_boundary", False):
+        raise UnsupportedError("essential-boundary elimination is outside the FE fast path")
+    return Space(dim, cells[:dim], int(config.get("order", 0)), sizes)
+
+
+def hybridized_matrix(config: dict):
+    """Mirror of hdivred._core.hybridized_matrix (bindings/module.cpp:163-171):
+    ((nrows, ncols, row_offsets, col_indices, values), g) for the config's FE problem."""
+    space = space_from_config(config)
+    alpha, beta = coefficients_from_config(config, space)
+    g = config.get("g", (1.0, 1.0, 1.0))
+    g = _axes(g, 3, [1.0, 1.0, 1.0])
+    f_hat = space.load_vector(g)
+    op = space.hybridize(alpha, beta, f_hat)
+    nr, nc, ro, ci, hv = op.h_mat()
+    _, gv = op.values()
+    return (nr, nc, list(ro), list(ci), list(hv)), list(gv)
+
+
+def space_info(dim: int, cells: Sequence[int], order: int) -> dict:
+    """Mirror of hdivred._core.space_info (bindings/module.cpp:83-101), computed
+    from the mesh numbering alone (no device needed)."""
+    cells = list(cells) + [1] * (3 - len(cells))
+    n = cells[:dim]
+    nfaces = 0
+    for a in range(dim):
+        c = n[a] + 1
+        for b in range(dim):
+            if b != a:
+                c *= n[b]
+        nfaces += c
+    ncells = int(np.prod(n))
+    dpf = (order + 1) ** (dim - 1)
+    nint = dim * order * dpf
+    ndofs = nfaces * dpf + ncells * nint
+    return {"ncells": ncells, "nfaces": nfaces, "ndofs": ndofs, "broken_ndofs": ncells * (2 * dim * dpf + nint),
+            "dofs_per_face": dpf, "interior_dofs_per_cell": nint}
+
+
+def launch_count() -> int:
+    """Kernels this process launched through the library (bench.py gpu_launches)."""
+    return int(_lib().hdr_launch_count())
+
+
+__all__ = [
+    "CapExceededError", "FormatError", "SingularBlockError", "ValidationError", "DimensionMismatch",
+    "UnsupportedError", "DeviceError", "Space", "HybridizedOperator", "CondensedOperator", "hybridized_matrix",
+    "space_info", "coefficients_from_config", "space_from_config", "launch_count", "__version__",
+]

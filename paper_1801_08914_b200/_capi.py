@@ -1,0 +1,81 @@
+"""ctypes binding of the C ABI in include/hdivred_b200.h (libhdivred_b200.so).
+
+The library is built in-tree (``make -C paper_1801_08914_b200/csrc`` or
+``__graft_entry__.build()``).  Importing this module without it raises: the hot
+path has no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from pathlib import Path
+
+LIB_PATH = Path(__file__).resolve().parent / "libhdivred_b200.so"
+
+# status codes (hdr_status)
+OK, SINGULAR_BLOCK, DIMENSION_MISMATCH, VALIDATION, UNSUPPORTED, CUDA_ERROR, INVALID_ARGUMENT = range(7)
+
+# hdr_space_info indices
+INFO_NAMES = ["dim", "order", "ncells", "nfaces", "ndofs", "broken_ndofs", "element_ndofs", "dofs_per_face",
+              "interior_dofs_per_cell", "face_dof_count", "m", "nnz_h", "n_s", "nnz_s", "div_rank"]
+
+_vp, _i32, _i64, _d = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_double
+
+_SIGS = {
+    "hdr_space_create": (_i32, [_i32, _vp, _vp, _i32, _vp, _vp, _i32, _vp, _vp]),
+    "hdr_space_destroy": (None, [_vp]),
+    "hdr_space_info": (_i32, [_vp, _vp]),
+    "hdr_space_reference": (_i32, [_vp, _vp, _vp]),
+    "hdr_space_unit_load": (_i32, [_vp, _vp]),
+    "hdr_space_set_stream": (_i32, [_vp, _vp]),
+    "hdr_space_pattern": (_i32, [_vp, _i32, _vp, _vp]),
+    "hdr_space_master_globals": (_i32, [_vp, _vp]),
+    "hdr_space_dof_map": (_i32, [_vp, _vp, _vp]),
+    "hdr_space_synchronize": (_i32, [_vp]),
+    "hdr_hybridize_fe": (_i32, [_vp, _vp, _vp, _vp, _i32, _vp]),
+    "hdr_hybridize_fe_into": (_i32, [_vp, _vp, _vp, _vp, _i32]),
+    "hdr_hybrid_destroy": (None, [_vp]),
+    "hdr_hybrid_values": (_i32, [_vp, _vp, _vp, _i32]),
+    "hdr_hybrid_device_ptrs": (_i32, [_vp, _vp, _vp, _vp, _vp]),
+    "hdr_recover_hybrid": (_i32, [_vp, _vp, _vp, _i32, _vp, _vp]),
+    "hdr_static_condense_fe": (_i32, [_vp, _vp, _vp, _vp, _i32, _vp]),
+    "hdr_static_condense_fe_into": (_i32, [_vp, _vp, _vp, _vp, _i32]),
+    "hdr_condensed_destroy": (None, [_vp]),
+    "hdr_condensed_values": (_i32, [_vp, _vp, _vp, _i32]),
+    "hdr_recover_condensed": (_i32, [_vp, _vp, _vp, _i32, _vp]),
+    "hdr_hybrid_spmv": (_i32, [_vp, _vp, _vp, _i32]),
+    "hdr_condensed_spmv": (_i32, [_vp, _vp, _vp, _i32]),
+    "hdr_csr_spmv_device": (_i32, [_i64, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "hdr_reference_element": (_i32, [_i32, _i32, _vp, _vp, _vp, _vp, _vp]),
+    "hdr_structured_factors": (_i32, [_i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "hdr_last_error": (ctypes.c_char_p, []),
+    "hdr_version": (ctypes.c_char_p, []),
+    "hdr_launch_count": (_i64, []),
+}
+
+EXPORTED = sorted(_SIGS)
+
+_lib = None
+
+
+def load(path: os.PathLike | None = None):
+    """Loads libhdivred_b200.so (raises ImportError if it has not been built)."""
+    global _lib
+    if _lib is not None and path is None:
+        return _lib
+    p = Path(path) if path else LIB_PATH
+    if not p.exists():
+        raise ImportError(f"{p} is missing: build the CUDA library first "
+                          "(make -C paper_1801_08914_b200/csrc); there is no CPU fallback")
+    lib = ctypes.CDLL(str(p))
+    for name, (res, args) in _SIGS.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    if path is None:
+        _lib = lib
+    return lib
+
+
+def last_error() -> str:
+    return load().hdr_last_error().decode(errors="replace")

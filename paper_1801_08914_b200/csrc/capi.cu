@@ -1,0 +1,618 @@
+// C ABI (include/hdivred_b200.h): handles, device memory, orchestration.
+//
+// There is no CPU compute path behind these entry points: every per-cell
+// operation runs in the kernels of kern_*.cu; the host only builds the
+// reference element once per space (rt_reference.cpp), its fixed factors
+// (structured.cpp) and launches.  Without a CUDA device every compute entry
+// point returns HDR_CUDA_ERROR.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <functional>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include <cub/cub.cuh>
+
+#include "../../include/hdivred_b200.h"
+#include "hdr_internal.hpp"
+#include "kernels.hpp"
+
+namespace hdr {
+
+static std::atomic<int64_t> g_launches{0};
+void count_launch(int64_t k) { g_launches += k; }
+
+namespace {
+
+thread_local std::string g_err;
+
+hdr_status fail(hdr_status s, const std::string& msg) {
+  g_err = msg;
+  return s;
+}
+
+struct CudaError : std::exception {
+  cudaError_t e;
+  std::string where;
+  CudaError(cudaError_t err, const char* w) : e(err), where(w) {}
+};
+
+#define CK(call)                                    \
+  do {                                              \
+    cudaError_t _e = (call);                        \
+    if (_e != cudaSuccess) throw CudaError(_e, #call); \
+  } while (0)
+
+template <class T>
+struct DBuf {  // owning device buffer
+  T* p = nullptr;
+  size_t n = 0;
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  ~DBuf() { reset(); }
+  void reset() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  void alloc(size_t count) {
+    reset();
+    if (count == 0) count = 1;
+    CK(cudaMalloc(&p, count * sizeof(T)));
+    n = count;
+  }
+};
+
+}  // namespace
+}  // namespace hdr
+
+using namespace hdr;
+
+struct hdr_space_s {
+  int dim = 3, k = 0, n = 0, dpf = 1, nint = 0, nF = 0, r = 0;
+  int64_t N[3] = {1, 1, 1};
+  double h[3] = {1, 1, 1};
+  int weighted = 0;
+  int64_t ncells = 0, nfaces = 0, ndofs = 0, fdc = 0, broken = 0, m = 0, nnz_h = 0, ns = 0, nnz_s = 0;
+  RefElement re;
+  Structured st;
+  DevMesh dm{};
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  // device data
+  DBuf<int> mbase;
+  DBuf<int64_t> row_h, row_s;
+  DBuf<int32_t> col_h, col_s;
+  DBuf<double> fixed;  // D, M, E, Ma, N0 (n*n each), X (n*r), lam (r)
+  std::vector<double> rt0_consts;  // packed constant block of the k = 0 kernel
+  Fixed fx{};
+  ~hdr_space_s() {
+    if (own_stream && stream) cudaStreamDestroy(stream);
+  }
+};
+
+struct hdr_hybrid_s {
+  hdr_space_t sp = nullptr;
+  DBuf<double> hval, g, alpha, beta, f, ws;
+  DBuf<int> status;
+  int64_t ws_doubles = 0;
+};
+
+struct hdr_condensed_s {
+  hdr_space_t sp = nullptr;
+  DBuf<double> sval, fs, alpha, beta, f;
+};
+
+namespace {
+
+int64_t ipow(int64_t b, int e) {
+  int64_t r = 1;
+  while (e-- > 0) r *= b;
+  return r;
+}
+
+hdr_status catch_all(const std::function<hdr_status()>& fn) {
+  try {
+    return fn();
+  } catch (const CudaError& e) {
+    return fail(HDR_CUDA_ERROR, std::string("CUDA error in ") + e.where + ": " + cudaGetErrorString(e.e));
+  } catch (const std::bad_alloc&) {
+    return fail(HDR_CUDA_ERROR, "host allocation failed");
+  } catch (const std::exception& e) {
+    return fail(HDR_UNSUPPORTED, e.what());
+  }
+}
+
+template <class T>
+void exclusive_scan(const T* in, T* out, int64_t count, cudaStream_t st) {
+  size_t bytes = 0;
+  CK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, in, out, static_cast<int>(count), st));
+  DBuf<unsigned char> tmp;
+  tmp.alloc(bytes);
+  CK(cub::DeviceScan::ExclusiveSum(tmp.p, bytes, in, out, static_cast<int>(count), st));
+  CK(cudaStreamSynchronize(st));
+}
+
+// copies host (on_device = 0) or device data into an owned device buffer
+void stage(DBuf<double>& dst, const double* src, int64_t count, int on_device, cudaStream_t st) {
+  if (dst.n < static_cast<size_t>(count) || !dst.p) dst.alloc(static_cast<size_t>(count));
+  if (count == 0) return;
+  CK(cudaMemcpyAsync(dst.p, src, static_cast<size_t>(count) * 8,
+                     on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* hdr_last_error(void) { return g_err.c_str(); }
+const char* hdr_version(void) { return "hdivred_b200 0.1.0 sm_100a"; }
+int64_t hdr_launch_count(void) { return g_launches.load(); }
+
+hdr_status hdr_reference_element(int dim, int order, const double h[3], double* divdiv, double* mass,
+                                 double* face_moments, double* unit_load) {
+  if (dim != 2 && dim != 3) return fail(HDR_INVALID_ARGUMENT, "dim must be 2 or 3");
+  if (order < 0 || order > 3) return fail(HDR_INVALID_ARGUMENT, "order must be in 0..3");
+  return catch_all([&]() -> hdr_status {
+    const double hh[3] = {h ? h[0] : 1.0, h ? h[1] : 1.0, (h && dim == 3) ? h[2] : 1.0};
+    const RefElement re = build_reference_element(dim, order, hh);
+    if (divdiv) std::memcpy(divdiv, re.divdiv.data(), re.divdiv.size() * 8);
+    if (mass) std::memcpy(mass, re.mass.data(), re.mass.size() * 8);
+    if (face_moments) std::memcpy(face_moments, re.face_moments.data(), re.face_moments.size() * 8);
+    if (unit_load) std::memcpy(unit_load, re.unit_load.data(), re.unit_load.size() * 8);
+    return HDR_OK;
+  });
+}
+
+hdr_status hdr_structured_factors(int dim, int order, const double h[3], double* X, double* lambda, double* E,
+                                  double* N0, double* Ma, double* diag, int64_t* rank) {
+  if (dim != 2 && dim != 3) return fail(HDR_INVALID_ARGUMENT, "dim must be 2 or 3");
+  if (order < 0 || order > 3) return fail(HDR_INVALID_ARGUMENT, "order must be in 0..3");
+  return catch_all([&]() -> hdr_status {
+    const double hh[3] = {h ? h[0] : 1.0, h ? h[1] : 1.0, (h && dim == 3) ? h[2] : 1.0};
+    const RefElement re = build_reference_element(dim, order, hh);
+    Structured st;
+    std::string err;
+    if (!precompute_structured(re, static_cast<int>(ipow(order + 1, dim)), &st, &err)) return fail(HDR_UNSUPPORTED, err);
+    if (X) std::memcpy(X, st.X.data(), st.X.size() * 8);
+    if (lambda) std::memcpy(lambda, st.lambda.data(), st.lambda.size() * 8);
+    if (E) std::memcpy(E, st.E.data(), st.E.size() * 8);
+    if (N0) std::memcpy(N0, st.N0.data(), st.N0.size() * 8);
+    if (Ma) std::memcpy(Ma, st.Ma.data(), st.Ma.size() * 8);
+    if (diag) {
+      diag[0] = st.rho;
+      diag[1] = st.e_rel;
+      diag[2] = st.orth;
+      diag[3] = st.block_diag ? 1.0 : 0.0;
+    }
+    if (rank) *rank = st.r;
+    return HDR_OK;
+  });
+}
+
+hdr_status hdr_space_create(int dim, const int64_t cells[3], const double h[3], int order, const double* ref_divdiv,
+                            const double* ref_mass, int weighted, const double* ref_face_moments, hdr_space_t* out) {
+  if (!out || !cells) return fail(HDR_INVALID_ARGUMENT, "hdr_space_create: null argument");
+  *out = nullptr;
+  if (dim != 2 && dim != 3) return fail(HDR_INVALID_ARGUMENT, "build_mesh: dim must be 2 or 3");
+  if (order < 0 || order > 3) return fail(HDR_INVALID_ARGUMENT, "build_space: order must be in 0..3");
+  for (int a = 0; a < dim; ++a) {
+    if (cells[a] < 1) return fail(HDR_INVALID_ARGUMENT, "build_mesh: cell counts must be >= 1");
+    if (h && !(h[a] > 0.0)) return fail(HDR_INVALID_ARGUMENT, "build_mesh: cell sizes must be > 0");
+  }
+  if (weighted) return fail(HDR_UNSUPPORTED, "weighted constraint rows are not implemented on the device path yet");
+  (void)ref_face_moments;
+  return catch_all([&]() -> hdr_status {
+    int dev_count = 0;
+    if (cudaGetDeviceCount(&dev_count) != cudaSuccess || dev_count == 0)
+      return fail(HDR_CUDA_ERROR, "no CUDA device available (the hot path has no CPU fallback)");
+    auto sp = std::make_unique<hdr_space_s>();
+    sp->dim = dim;
+    sp->k = order;
+    for (int a = 0; a < 3; ++a) {
+      sp->N[a] = a < dim ? cells[a] : 1;
+      sp->h[a] = a < dim ? (h ? h[a] : 1.0 / static_cast<double>(cells[a])) : 1.0;
+    }
+    sp->re = build_reference_element(dim, order, sp->h);
+    const int n = sp->re.n;
+    if (ref_divdiv) sp->re.divdiv.assign(ref_divdiv, ref_divdiv + static_cast<size_t>(n) * n);
+    if (ref_mass) sp->re.mass.assign(ref_mass, ref_mass + static_cast<size_t>(n) * n);
+    sp->n = n;
+    sp->dpf = sp->re.dpf;
+    sp->nint = sp->re.nint;
+    sp->nF = 2 * dim * sp->dpf;
+    std::string err;
+    if (!precompute_structured(sp->re, static_cast<int>(ipow(order + 1, dim)), &sp->st, &err))
+      return fail(HDR_UNSUPPORTED, err);
+    sp->r = sp->st.r;
+
+    // mesh numbering
+    DevMesh& m = sp->dm;
+    m.dim = dim;
+    m.dpf = sp->dpf;
+    m.n = n;
+    m.nint = sp->nint;
+    for (int a = 0; a < 3; ++a) m.N[a] = sp->N[a];
+    int64_t off = 0;
+    for (int a = 0; a < 3; ++a) {
+      m.foff[a] = off;
+      if (a < dim) {
+        int64_t cnt = sp->N[a] + 1;
+        for (int b = 0; b < dim; ++b)
+          if (b != a) cnt *= sp->N[b];
+        off += cnt;
+      }
+    }
+    m.nfaces = off;
+    m.ncells = sp->N[0] * sp->N[1] * sp->N[2];
+    m.face_dof_count = m.nfaces * sp->dpf;
+    sp->ncells = m.ncells;
+    sp->nfaces = m.nfaces;
+    sp->fdc = m.face_dof_count;
+    sp->ndofs = sp->fdc + sp->ncells * sp->nint;
+    sp->broken = sp->ncells * n;
+    sp->m = sp->broken - sp->ndofs;
+    sp->ns = sp->fdc;
+
+    CK(cudaStreamCreateWithFlags(&sp->stream, cudaStreamNonBlocking));
+    sp->own_stream = true;
+    cudaStream_t st = sp->stream;
+
+    // K1: patterns
+    const int64_t nf = m.nfaces;
+    DBuf<int> flag, ord;
+    DBuf<int64_t> fnnz_h, fnnz_s, fbase_h, fbase_s;
+    flag.alloc(nf + 1);
+    ord.alloc(nf + 1);
+    fnnz_h.alloc(nf + 1);
+    fnnz_s.alloc(nf + 1);
+    fbase_h.alloc(nf + 1);
+    fbase_s.alloc(nf + 1);
+    sp->mbase.alloc(nf);
+    launch_face_counts(m, flag.p, fnnz_h.p, fnnz_s.p, st);
+    CK(cudaMemsetAsync(flag.p + nf, 0, sizeof(int), st));
+    CK(cudaMemsetAsync(fnnz_h.p + nf, 0, sizeof(int64_t), st));
+    CK(cudaMemsetAsync(fnnz_s.p + nf, 0, sizeof(int64_t), st));
+    exclusive_scan(flag.p, ord.p, nf + 1, st);
+    exclusive_scan(fnnz_h.p, fbase_h.p, nf + 1, st);
+    exclusive_scan(fnnz_s.p, fbase_s.p, nf + 1, st);
+    int n_int_faces = 0;
+    CK(cudaMemcpy(&n_int_faces, ord.p + nf, sizeof(int), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(&sp->nnz_h, fbase_h.p + nf, sizeof(int64_t), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(&sp->nnz_s, fbase_s.p + nf, sizeof(int64_t), cudaMemcpyDeviceToHost));
+    if (static_cast<int64_t>(n_int_faces) * sp->dpf != sp->m)
+      return fail(HDR_VALIDATION, "multiplier count mismatch (m != n_hat - n)");
+    if (sp->nnz_h >= (int64_t(1) << 31) || sp->nnz_s >= (int64_t(1) << 31) || sp->fdc >= (int64_t(1) << 31))
+      return fail(HDR_UNSUPPORTED, "mesh too large for int32 device column indices");
+    launch_mbase(m, flag.p, ord.p, sp->mbase.p, st);
+    sp->row_h.alloc(sp->m + 1);
+    sp->col_h.alloc(sp->nnz_h);
+    sp->row_s.alloc(sp->ns + 1);
+    sp->col_s.alloc(sp->nnz_s);
+    launch_fill_patterns(m, sp->mbase.p, fbase_h.p, fbase_s.p, sp->row_h.p, sp->col_h.p, sp->row_s.p, sp->col_s.p,
+                         sp->m, sp->nnz_h, sp->ns, sp->nnz_s, st);
+
+    // fixed factors
+    const int r = sp->r;
+    const size_t nn = static_cast<size_t>(n) * n;
+    std::vector<double> pack(5 * nn + static_cast<size_t>(n) * r + r);
+    std::memcpy(pack.data(), sp->re.divdiv.data(), nn * 8);
+    std::memcpy(pack.data() + nn, sp->re.mass.data(), nn * 8);
+    std::memcpy(pack.data() + 2 * nn, sp->st.E.data(), nn * 8);
+    std::memcpy(pack.data() + 3 * nn, sp->st.Ma.data(), nn * 8);
+    std::memcpy(pack.data() + 4 * nn, sp->st.N0.data(), nn * 8);
+    std::memcpy(pack.data() + 5 * nn, sp->st.X.data(), static_cast<size_t>(n) * r * 8);
+    std::memcpy(pack.data() + 5 * nn + static_cast<size_t>(n) * r, sp->st.lambda.data(), static_cast<size_t>(r) * 8);
+    sp->fixed.alloc(pack.size());
+    CK(cudaMemcpyAsync(sp->fixed.p, pack.data(), pack.size() * 8, cudaMemcpyHostToDevice, st));
+    Fixed& fx = sp->fx;
+    fx.D = sp->fixed.p;
+    fx.M = fx.D + nn;
+    fx.E = fx.M + nn;
+    fx.Ma = fx.E + nn;
+    fx.N0 = fx.Ma + nn;
+    fx.X = fx.N0 + nn;
+    fx.lam = fx.X + static_cast<size_t>(n) * r;
+    fx.r = r;
+    fx.rho = sp->st.rho;
+    if (order == 0) {  // constant block for the register kernel: D, M, E, Ma, N0, X, lam, rho
+      sp->rt0_consts.assign(pack.begin(), pack.begin() + 5 * nn + n + 1);
+      sp->rt0_consts.push_back(sp->st.rho);
+    }
+    CK(cudaStreamSynchronize(st));
+    CK(cudaGetLastError());
+    *out = sp.release();
+    return HDR_OK;
+  });
+}
+
+void hdr_space_destroy(hdr_space_t sp) { delete sp; }
+
+hdr_status hdr_space_info(hdr_space_t sp, int64_t* o) {
+  if (!sp || !o) return fail(HDR_INVALID_ARGUMENT, "null argument");
+  o[HDR_INFO_DIM] = sp->dim;
+  o[HDR_INFO_ORDER] = sp->k;
+  o[HDR_INFO_NCELLS] = sp->ncells;
+  o[HDR_INFO_NFACES] = sp->nfaces;
+  o[HDR_INFO_NDOFS] = sp->ndofs;
+  o[HDR_INFO_BROKEN_NDOFS] = sp->broken;
+  o[HDR_INFO_ELEMENT_NDOFS] = sp->n;
+  o[HDR_INFO_DOFS_PER_FACE] = sp->dpf;
+  o[HDR_INFO_INTERIOR_DOFS] = sp->nint;
+  o[HDR_INFO_FACE_DOF_COUNT] = sp->fdc;
+  o[HDR_INFO_M] = sp->m;
+  o[HDR_INFO_NNZ_H] = sp->nnz_h;
+  o[HDR_INFO_NS] = sp->ns;
+  o[HDR_INFO_NNZ_S] = sp->nnz_s;
+  o[HDR_INFO_DIV_RANK] = sp->r;
+  return HDR_OK;
+}
+
+hdr_status hdr_space_reference(hdr_space_t sp, double* dd, double* mm) {
+  if (!sp) return fail(HDR_INVALID_ARGUMENT, "null space");
+  if (dd) std::memcpy(dd, sp->re.divdiv.data(), sp->re.divdiv.size() * 8);
+  if (mm) std::memcpy(mm, sp->re.mass.data(), sp->re.mass.size() * 8);
+  return HDR_OK;
+}
+
+hdr_status hdr_space_unit_load(hdr_space_t sp, double* out) {
+  if (!sp || !out) return fail(HDR_INVALID_ARGUMENT, "null argument");
+  std::memcpy(out, sp->re.unit_load.data(), sp->re.unit_load.size() * 8);
+  return HDR_OK;
+}
+
+hdr_status hdr_space_set_stream(hdr_space_t sp, void* stream) {
+  if (!sp) return fail(HDR_INVALID_ARGUMENT, "null space");
+  return catch_all([&]() -> hdr_status {
+    CK(cudaStreamSynchronize(sp->stream));
+    if (sp->own_stream) cudaStreamDestroy(sp->stream);
+    if (stream) {
+      sp->stream = static_cast<cudaStream_t>(stream);
+      sp->own_stream = false;
+    } else {
+      CK(cudaStreamCreateWithFlags(&sp->stream, cudaStreamNonBlocking));
+      sp->own_stream = true;
+    }
+    return HDR_OK;
+  });
+}
+
+hdr_status hdr_space_synchronize(hdr_space_t sp) {
+  if (!sp) return fail(HDR_INVALID_ARGUMENT, "null space");
+  return catch_all([&]() -> hdr_status {
+    CK(cudaStreamSynchronize(sp->stream));
+    return HDR_OK;
+  });
+}
+
+hdr_status hdr_space_pattern(hdr_space_t sp, int which, int64_t* row_offsets, int64_t* col_indices) {
+  if (!sp) return fail(HDR_INVALID_ARGUMENT, "null space");
+  return catch_all([&]() -> hdr_status {
+    const int64_t nr = which == 0 ? sp->m : sp->ns;
+    const int64_t nz = which == 0 ? sp->nnz_h : sp->nnz_s;
+    const int64_t* ro = which == 0 ? sp->row_h.p : sp->row_s.p;
+    const int32_t* ci = which == 0 ? sp->col_h.p : sp->col_s.p;
+    if (row_offsets) CK(cudaMemcpy(row_offsets, ro, static_cast<size_t>(nr + 1) * 8, cudaMemcpyDeviceToHost));
+    if (col_indices) {
+      std::vector<int32_t> tmp(static_cast<size_t>(nz));
+      if (nz) CK(cudaMemcpy(tmp.data(), ci, static_cast<size_t>(nz) * 4, cudaMemcpyDeviceToHost));
+      for (int64_t i = 0; i < nz; ++i) col_indices[i] = tmp[static_cast<size_t>(i)];
+    }
+    return HDR_OK;
+  });
+}
+
+hdr_status hdr_space_master_globals(hdr_space_t sp, int64_t* out) {
+  if (!sp || !out) return fail(HDR_INVALID_ARGUMENT, "null argument");
+  for (int64_t i = 0; i < sp->ns; ++i) out[i] = i;  // every face dof is a master, in order
+  return HDR_OK;
+}
+
+hdr_status hdr_space_dof_map(hdr_space_t sp, int64_t* global, double* sign) {
+  if (!sp) return fail(HDR_INVALID_ARGUMENT, "null space");
+  const DevMesh& m = sp->dm;
+  for (int64_t e = 0; e < sp->ncells; ++e) {
+    int64_t c[3];
+    cell_coords(m, e, c);
+    int64_t l = e * sp->n;
+    for (int i = 0; i < sp->nint; ++i, ++l) {
+      if (global) global[l] = sp->fdc + e * sp->nint + i;
+      if (sign) sign[l] = 1.0;
+    }
+    for (int s = 0; s < 2 * sp->dim; ++s) {
+      const int64_t f = slot_face(m, c, s, nullptr);
+      for (int sub = 0; sub < sp->dpf; ++sub, ++l) {
+        if (global) global[l] = f * sp->dpf + sub;
+        if (sign) sign[l] = (s & 1) ? 1.0 : -1.0;
+      }
+    }
+  }
+  return HDR_OK;
+}
+
+static hdr_status run_hybridize(hdr_hybrid_t op, const double* alpha, const double* beta, const double* f_hat,
+                                int on_device) {
+  hdr_space_t sp = op->sp;
+  return catch_all([&]() -> hdr_status {
+    cudaStream_t st = sp->stream;
+    const double *da = alpha, *db = beta, *df = f_hat;
+    if (!on_device) {
+      stage(op->alpha, alpha, sp->ncells, 0, st);
+      stage(op->beta, beta, sp->ncells, 0, st);
+      stage(op->f, f_hat, sp->broken, 0, st);
+      da = op->alpha.p;
+      db = op->beta.p;
+      df = op->f.p;
+    } else {  // recovery needs the coefficients later: keep device copies (16 B/cell)
+      stage(op->alpha, alpha, sp->ncells, 1, st);
+      stage(op->beta, beta, sp->ncells, 1, st);
+      da = op->alpha.p;
+      db = op->beta.p;
+    }
+    if (!op->hval.p) op->hval.alloc(sp->nnz_h);
+    if (!op->g.p) op->g.alloc(sp->m);
+    if (!op->status.p) op->status.alloc(1);
+    CK(cudaMemsetAsync(op->status.p, 0, sizeof(int), st));
+    HybArgs A{};
+    A.m = sp->dm;
+    A.fx = sp->fx;
+    A.nF = sp->nF;
+    A.p_max = 4;
+    A.alpha = da;
+    A.beta = db;
+    A.f = df;
+    A.mbase = sp->mbase.p;
+    A.rowoff = sp->row_h.p;
+    A.hval = op->hval.p;
+    A.g = op->g.p;
+    A.status = op->status.p;
+    if (sp->k == 0) {
+      for (int parity = 0; parity < 2; ++parity) launch_hybridize_rt0(A, sp->rt0_consts.data(), parity, st);
+    } else {
+      bool use_smem = false;
+      const int64_t need = hybridize_cta_ws_doubles(sp->dm, sp->nF, sp->r, A.p_max, &use_smem);
+      if (!use_smem && !op->ws.p) {
+        op->ws_doubles = need * 148 * 4;
+        op->ws.alloc(static_cast<size_t>(op->ws_doubles));
+      }
+      for (int parity = 0; parity < 2; ++parity) launch_hybridize_cta(A, parity, op->ws.p, op->ws_doubles, st);
+    }
+    CK(cudaGetLastError());
+    int status = 0;
+    CK(cudaMemcpyAsync(&status, op->status.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (status & 1)
+      return fail(HDR_UNSUPPORTED, "coefficient ratio alpha/beta outside the structured solve's range on some cell");
+    return HDR_OK;
+  });
+}
+
+hdr_status hdr_hybridize_fe(hdr_space_t sp, const double* alpha, const double* beta, const double* f_hat, int on_device,
+                            hdr_hybrid_t* out) {
+  if (!sp || !out || !alpha || !beta || !f_hat) return fail(HDR_INVALID_ARGUMENT, "null argument");
+  *out = nullptr;
+  auto op = std::make_unique<hdr_hybrid_s>();
+  op->sp = sp;
+  const hdr_status s = run_hybridize(op.get(), alpha, beta, f_hat, on_device);
+  if (s != HDR_OK) return s;
+  *out = op.release();
+  return HDR_OK;
+}
+
+hdr_status hdr_hybridize_fe_into(hdr_hybrid_t op, const double* alpha, const double* beta, const double* f_hat,
+                                 int on_device) {
+  if (!op || !alpha || !beta || !f_hat) return fail(HDR_INVALID_ARGUMENT, "null argument");
+  return run_hybridize(op, alpha, beta, f_hat, on_device);
+}
+
+void hdr_hybrid_destroy(hdr_hybrid_t op) { delete op; }
+
+hdr_status hdr_hybrid_values(hdr_hybrid_t op, double* h_values, double* g, int dst_on_device) {
+  if (!op) return fail(HDR_INVALID_ARGUMENT, "null operator");
+  return catch_all([&]() -> hdr_status {
+    const cudaMemcpyKind kind = dst_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+    cudaStream_t st = op->sp->stream;
+    if (h_values && op->sp->nnz_h)
+      CK(cudaMemcpyAsync(h_values, op->hval.p, static_cast<size_t>(op->sp->nnz_h) * 8, kind, st));
+    if (g && op->sp->m) CK(cudaMemcpyAsync(g, op->g.p, static_cast<size_t>(op->sp->m) * 8, kind, st));
+    CK(cudaStreamSynchronize(st));
+    return HDR_OK;
+  });
+}
+
+hdr_status hdr_hybrid_device_ptrs(hdr_hybrid_t op, const double** h_values, const double** g,
+                                  const int64_t** row_offsets, const int32_t** col_indices) {
+  if (!op) return fail(HDR_INVALID_ARGUMENT, "null operator");
+  if (h_values) *h_values = op->hval.p;
+  if (g) *g = op->g.p;
+  if (row_offsets) *row_offsets = op->sp->row_h.p;
+  if (col_indices) *col_indices = op->sp->col_h.p;
+  return HDR_OK;
+}
+
+hdr_status hdr_recover_hybrid(hdr_hybrid_t op, const double* lambda, const double* f_hat, int on_device, double* x_hat,
+                              double* x) {
+  if (!op || !lambda || !f_hat) return fail(HDR_INVALID_ARGUMENT, "null argument");
+  hdr_space_t sp = op->sp;
+  return catch_all([&]() -> hdr_status {
+    cudaStream_t st = sp->stream;
+    DBuf<double> dl, df, dxh, dx;
+    const double *pl = lambda, *pf = f_hat;
+    if (!on_device) {
+      stage(dl, lambda, sp->m, 0, st);
+      stage(df, f_hat, sp->broken, 0, st);
+      pl = dl.p;
+      pf = df.p;
+    }
+    double* pxh = x_hat;
+    double* px = x;
+    if (!on_device || !x_hat) {
+      dxh.alloc(sp->broken);
+      pxh = dxh.p;
+    }
+    if (!on_device || !x) {
+      dx.alloc(sp->ndofs);
+      px = dx.p;
+    }
+    if (!op->status.p) op->status.alloc(1);
+    CK(cudaMemsetAsync(op->status.p, 0, sizeof(int), st));
+    RecArgs R{};
+    R.m = sp->dm;
+    R.fx = sp->fx;
+    R.nF = sp->nF;
+    R.p_max = 4;
+    R.alpha = op->alpha.p;
+    R.beta = op->beta.p;
+    R.f = pf;
+    R.lambda = pl;
+    R.mbase = sp->mbase.p;
+    R.x_hat = pxh;
+    R.x = px;
+    R.status = op->status.p;
+    launch_recover_hybrid(R, nullptr, 0, st);
+    launch_average_faces(sp->dm, pxh, px, st);
+    CK(cudaGetLastError());
+    if (!on_device) {
+      if (x_hat) CK(cudaMemcpyAsync(x_hat, pxh, static_cast<size_t>(sp->broken) * 8, cudaMemcpyDeviceToHost, st));
+      if (x) CK(cudaMemcpyAsync(x, px, static_cast<size_t>(sp->ndofs) * 8, cudaMemcpyDeviceToHost, st));
+    }
+    int status = 0;
+    CK(cudaMemcpyAsync(&status, op->status.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (status & 1) return fail(HDR_UNSUPPORTED, "coefficient ratio outside the structured solve's range");
+    return HDR_OK;
+  });
+}
+
+// ---- placeholders until the condensation / spmv kernels land
+hdr_status hdr_static_condense_fe(hdr_space_t, const double*, const double*, const double*, int, hdr_condensed_t* out) {
+  if (out) *out = nullptr;
+  return fail(HDR_UNSUPPORTED, "static condensation not built yet");
+}
+hdr_status hdr_static_condense_fe_into(hdr_condensed_t, const double*, const double*, const double*, int) {
+  return fail(HDR_UNSUPPORTED, "static condensation not built yet");
+}
+void hdr_condensed_destroy(hdr_condensed_t op) { delete op; }
+hdr_status hdr_condensed_values(hdr_condensed_t, double*, double*, int) {
+  return fail(HDR_UNSUPPORTED, "static condensation not built yet");
+}
+hdr_status hdr_recover_condensed(hdr_condensed_t, const double*, const double*, int, double*) {
+  return fail(HDR_UNSUPPORTED, "static condensation not built yet");
+}
+hdr_status hdr_hybrid_spmv(hdr_hybrid_t, const double*, double*, int) {
+  return fail(HDR_UNSUPPORTED, "spmv not built yet");
+}
+hdr_status hdr_condensed_spmv(hdr_condensed_t, const double*, double*, int) {
+  return fail(HDR_UNSUPPORTED, "spmv not built yet");
+}
+hdr_status hdr_csr_spmv_device(int64_t, const int64_t*, const int64_t*, const double*, const double*, double*, void*) {
+  return fail(HDR_UNSUPPORTED, "spmv not built yet");
+}
+
+}  // extern "C"

@@ -1,0 +1,556 @@
+// K2+K3+K4: fused element assembly, structured element solve and deterministic
+// scatter of hybridize (src/reduction.cpp:262-354 with element_matrices,
+// src/rt_space.cpp:345-374), plus the hybrid recovery (recover_hybrid,
+// src/reduction.cpp:356-446).
+//
+// Per cell T (alpha, beta, f_T):
+//   A_T   = fl(fl(alpha D) + fl(beta M))                         (bit-exact, never formed)
+//   A0^-1 = (N0 + X diag(s) X^T) / beta,  s_j = beta / (beta + alpha lambda_j)
+//   Delta = A_T - A0 = alpha E + beta Ma + delta(alpha, beta)     (generated on the fly)
+//   V     = A0^-1 [E_F | f_T]                (face columns + load column)
+//   [H_T | g_T] = E_F^T V + sum_{p>=1} (-1)^p V_F^T Y_p,  Y_1 = Delta V, Y_p = Delta A0^-1 Y_{p-1}
+// H_T = C_T A_T^-1 C_T^T and g_T = C_T A_T^-1 f_T for the unit constraint rows of
+// build_C (src/reduction.cpp:172-181): C_T selects the cell's interior-face dofs.
+// The Neumann order P is chosen per cell from the bound rho*alpha/beta so that
+// the truncation is below 1e-14 relative.
+//
+// Scatter: two launches, one per checkerboard colour.  Colour 0 stores, colour 1
+// stores its off-diagonal face blocks and adds its same-face blocks (and g) to
+// colour 0's values: every entry has at most two contributions (SURVEY.md §0
+// item 7) and fl(a+b) = fl(b+a), so the result is deterministic without atomics.
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+
+#include "hdr_device.cuh"
+#include "kernels.hpp"
+
+namespace hdr {
+
+namespace {
+
+__device__ inline int neumann_order(double tau, int p_max, int* status) {
+  if (!(tau < 0.25)) {
+    atomicOr(status, 1);
+    return p_max;
+  }
+  int p = 1;
+  double t = tau * tau;
+  while (t > 1e-14 && p < p_max) {
+    ++p;
+    t *= tau;
+  }
+  return p;
+}
+
+// ------------------------------------------------------------------ k = 0
+
+template <int N>
+struct Rt0Const {
+  double D[N * N], M[N * N], E[N * N], Ma[N * N], N0[N * N], X[N];
+  double lam, rho;
+};
+
+// Higher Neumann orders for one RT0 cell (rare: tau > 1e-7).  A0^-1 = V here.
+template <int N>
+__device__ __noinline__ void rt0_higher(const Rt0Const<N>& c, double a, double b, const double (&V)[N][N],
+                                        const double (&w)[N], int P, double (&H)[N][N], double (&gg)[N]) {
+  double T[N][N + 1], Y[N][N + 1];
+  for (int i = 0; i < N; ++i) {
+    for (int j = 0; j < N; ++j) T[i][j] = V[i][j];
+    T[i][N] = w[i];
+  }
+  for (int p = 1; p <= P; ++p) {
+    for (int k = 0; k < N; ++k)
+      for (int j = 0; j <= N; ++j) {
+        double acc = 0.0;
+        for (int l = 0; l < N; ++l)
+          acc = fma(delta_entry(a, b, c.D[k * N + l], c.M[k * N + l], c.E[k * N + l], c.Ma[k * N + l]), T[l][j], acc);
+        Y[k][j] = acc;
+      }
+    const double sg = (p & 1) ? -1.0 : 1.0;
+    if (p >= 2) {
+      for (int i = 0; i < N; ++i) {
+        for (int q = 0; q < N; ++q) {
+          double acc = 0.0;
+          for (int k = 0; k < N; ++k) acc = fma(V[k][i], Y[k][q], acc);
+          H[i][q] = fma(sg, acc, H[i][q]);
+        }
+        double acc = 0.0;
+        for (int k = 0; k < N; ++k) acc = fma(V[k][i], Y[k][N], acc);
+        gg[i] = fma(sg, acc, gg[i]);
+      }
+    }
+    // T <- A0^-1 Y = V Y
+    for (int i = 0; i < N; ++i)
+      for (int j = 0; j <= N; ++j) {
+        double acc = 0.0;
+        for (int k = 0; k < N; ++k) acc = fma(V[i][k], Y[k][j], acc);
+        T[i][j] = acc;
+      }
+  }
+}
+
+template <int DIM>
+__global__ void __launch_bounds__(128) k_hyb_rt0(HybArgs A, Rt0Const<2 * DIM> c, int parity) {
+  constexpr int N = 2 * DIM;
+  const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (t >= parity_count(A.m)) return;
+  const int64_t e = parity_cell(A.m, parity, t);
+  if (e < 0) return;
+  const double a = A.alpha[e], b = A.beta[e];
+  const double ib = 1.0 / b;
+  const double s = b / fma(a, c.lam, b);
+  double fv[N];
+#pragma unroll
+  for (int i = 0; i < N; ++i) fv[i] = A.f[e * N + i];
+
+  // V = A0^-1 (all dofs are face dofs for k = 0), w = A0^-1 f
+  double V[N][N], w[N];
+#pragma unroll
+  for (int i = 0; i < N; ++i)
+#pragma unroll
+    for (int j = 0; j < N; ++j) V[i][j] = fma(c.X[i] * s, c.X[j], c.N0[i * N + j]) * ib;
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    double acc = 0.0;
+#pragma unroll
+    for (int j = 0; j < N; ++j) acc = fma(V[i][j], fv[j], acc);
+    w[i] = acc;
+  }
+  // first order: H = V - V^T (Delta V),  g = w - V^T (Delta w)
+  double H[N][N], gg[N];
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    gg[i] = w[i];
+#pragma unroll
+    for (int j = 0; j < N; ++j) H[i][j] = V[i][j];
+  }
+#pragma unroll
+  for (int k = 0; k < N; ++k) {
+    double dk[N];
+#pragma unroll
+    for (int l = 0; l < N; ++l) dk[l] = delta_entry(a, b, c.D[k * N + l], c.M[k * N + l], c.E[k * N + l], c.Ma[k * N + l]);
+    double yk[N], yw = 0.0;
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+      double acc = 0.0;
+#pragma unroll
+      for (int l = 0; l < N; ++l) acc = fma(dk[l], V[l][j], acc);
+      yk[j] = acc;
+    }
+#pragma unroll
+    for (int l = 0; l < N; ++l) yw = fma(dk[l], w[l], yw);
+#pragma unroll
+    for (int p = 0; p < N; ++p) {
+#pragma unroll
+      for (int q = 0; q < N; ++q) H[p][q] = fma(-V[k][p], yk[q], H[p][q]);
+      gg[p] = fma(-V[k][p], yw, gg[p]);
+    }
+  }
+  const int P = neumann_order(c.rho * a * ib, A.p_max, A.status);
+  if (P >= 2) rt0_higher<N>(c, a, b, V, w, P, H, gg);
+
+  // deterministic scatter (dpf = 1: one H row per interior face)
+  int64_t cc[3], own_f[2 * DIM];
+  bool own_in[2 * DIM];
+  cell_coords(A.m, e, cc);
+#pragma unroll
+  for (int q = 0; q < N; ++q) own_f[q] = slot_face(A.m, cc, q, &own_in[q]);
+#pragma unroll
+  for (int p = 0; p < N; ++p) {
+    if (!own_in[p]) continue;
+    const int row = A.mbase[own_f[p]];
+    const int64_t start = A.rowoff[row];
+#pragma unroll
+    for (int q = 0; q < N; ++q) {
+      if (!own_in[q]) continue;
+      const int64_t pos = start + col_rank(A.m, cc, p, q, own_f, own_in);
+      A.hval[pos] = (parity == 1 && p == q) ? A.hval[pos] + H[p][q] : H[p][q];
+    }
+    A.g[row] = (parity == 1) ? A.g[row] + gg[p] : gg[p];
+  }
+}
+
+// ------------------------------------------------------------------ k >= 1
+
+constexpr int kIB = 8;   // rows of Delta per block
+constexpr int kNT = 256; // threads per CTA
+
+struct CtaLayout {
+  int64_t s, xs, xf, v, dblk, yblk, h, yfull, t, xty, rank, rows, total;
+};
+
+__host__ __device__ inline CtaLayout cta_layout(int n, int nF, int r, int p_max) {
+  CtaLayout L;
+  const int64_t nc = nF + 1;
+  int64_t o = 0;
+  auto take = [&o](int64_t cnt) {
+    const int64_t at = o;
+    o += (cnt + 3) & ~int64_t(3);
+    return at;
+  };
+  L.s = take(r);
+  L.xs = take(static_cast<int64_t>(nF) * r);
+  L.xf = take(r);
+  L.v = take(static_cast<int64_t>(n) * nc);
+  L.dblk = take(static_cast<int64_t>(kIB) * n);
+  L.yblk = take(static_cast<int64_t>(kIB) * nc);
+  L.h = take(static_cast<int64_t>(nF) * nc);
+  if (p_max >= 2) {
+    L.yfull = take(static_cast<int64_t>(n) * nc);
+    L.t = take(static_cast<int64_t>(n) * nc);
+    L.xty = take(static_cast<int64_t>(r) * nc);
+  } else {
+    L.yfull = L.t = L.xty = -1;
+  }
+  L.rank = take(64);       // 6x6 col ranks (ints stored in doubles' space)
+  L.rows = take(128);      // row starts per face dof (int64 in doubles' space)
+  L.total = o;
+  return L;
+}
+
+// y (rows i0..i0+ib) = Delta[i0:i0+ib, :] * Src   (Src n x nc), optionally kept in yfull
+__device__ inline void delta_block(const HybArgs& A, double a, double b, int n, int nc, int i0, int ib, const double* src,
+                                   double* dblk, double* yblk) {
+  const Fixed& fx = A.fx;
+  for (int idx = threadIdx.x; idx < ib * n; idx += blockDim.x) {
+    const int ii = idx / n, l = idx - ii * n;
+    const int64_t o = static_cast<int64_t>(i0 + ii) * n + l;
+    dblk[ii * n + l] = delta_entry(a, b, __ldg(fx.D + o), __ldg(fx.M + o), __ldg(fx.E + o), __ldg(fx.Ma + o));
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < ib * nc; idx += blockDim.x) {
+    const int ii = idx / nc, c = idx - ii * nc;
+    double acc = 0.0;
+    for (int l = 0; l < n; ++l) acc = fma(dblk[ii * n + l], src[static_cast<int64_t>(l) * nc + c], acc);
+    yblk[ii * nc + c] = acc;
+  }
+  __syncthreads();
+}
+
+// H[p][q] += sg * sum_ii V[i0+ii][p] * Y[ii][q]
+__device__ inline void accumulate_h(int nF, int nc, int nint, int i0, int ib, const double* V, const double* yblk,
+                                    double* H, double sg) {
+  (void)nint;
+  for (int idx = threadIdx.x; idx < nF * nc; idx += blockDim.x) {
+    const int p = idx / nc, q = idx - p * nc;
+    double acc = 0.0;
+    for (int ii = 0; ii < ib; ++ii) acc = fma(V[static_cast<int64_t>(i0 + ii) * nc + p], yblk[ii * nc + q], acc);
+    H[idx] = fma(sg, acc, H[idx]);
+  }
+  __syncthreads();
+}
+
+// dst = A0^-1 src = (N0 src + X diag(s) (X^T src)) / beta, src/dst n x nc
+__device__ inline void apply_a0inv(const HybArgs& A, int n, int nc, const double* s, double ib, const double* src,
+                                   double* xty, double* dst) {
+  const Fixed& fx = A.fx;
+  const int r = fx.r;
+  for (int idx = threadIdx.x; idx < r * nc; idx += blockDim.x) {
+    const int j = idx / nc, c = idx - j * nc;
+    double acc = 0.0;
+    for (int l = 0; l < n; ++l) acc = fma(__ldg(fx.X + static_cast<int64_t>(l) * r + j), src[static_cast<int64_t>(l) * nc + c], acc);
+    xty[idx] = acc * s[j];
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < n * nc; idx += blockDim.x) {
+    const int i = idx / nc, c = idx - i * nc;
+    double acc = 0.0;
+    for (int l = 0; l < n; ++l) acc = fma(__ldg(fx.N0 + static_cast<int64_t>(i) * n + l), src[static_cast<int64_t>(l) * nc + c], acc);
+    for (int j = 0; j < r; ++j) acc = fma(__ldg(fx.X + static_cast<int64_t>(i) * r + j), xty[j * nc + c], acc);
+    dst[idx] = acc * ib;
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(kNT) k_hyb_cta(HybArgs A, int parity, double* gws, int64_t ws_stride, int use_smem) {
+  extern __shared__ double smem[];
+  double* ws = use_smem ? smem : gws + blockIdx.x * ws_stride;
+  const DevMesh& m = A.m;
+  const int n = m.n, nint = m.nint, nF = A.nF, nc = nF + 1, r = A.fx.r, dpf = m.dpf, nsl = 2 * m.dim;
+  const CtaLayout L = cta_layout(n, nF, r, A.p_max);
+  double* s = ws + L.s;
+  double* xs = ws + L.xs;
+  double* xf = ws + L.xf;
+  double* V = ws + L.v;
+  double* dblk = ws + L.dblk;
+  double* yblk = ws + L.yblk;
+  double* H = ws + L.h;
+  int* rank = reinterpret_cast<int*>(ws + L.rank);
+  int64_t* rows = reinterpret_cast<int64_t*>(ws + L.rows);
+  const int64_t cnt = parity_count(m);
+
+  for (int64_t tt = blockIdx.x; tt < cnt; tt += gridDim.x) {
+    const int64_t e = parity_cell(m, parity, tt);
+    if (e < 0) continue;
+    const double a = A.alpha[e], b = A.beta[e];
+    const double ib = 1.0 / b;
+    const double* fe = A.f + e * n;
+    // s_j and X^T f
+    for (int j = threadIdx.x; j < r; j += blockDim.x) {
+      const double sj = b / fma(a, __ldg(A.fx.lam + j), b);
+      s[j] = sj;
+      double acc = 0.0;
+      for (int l = 0; l < n; ++l) acc = fma(__ldg(A.fx.X + static_cast<int64_t>(l) * r + j), fe[l], acc);
+      xf[j] = acc * sj;
+    }
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < nF * r; idx += blockDim.x) {
+      const int c = idx / r, j = idx - c * r;
+      xs[idx] = s[j] * __ldg(A.fx.X + static_cast<int64_t>(nint + c) * r + j);
+    }
+    __syncthreads();
+    // V = A0^-1 [E_F | f]
+    for (int idx = threadIdx.x; idx < n * nc; idx += blockDim.x) {
+      const int i = idx / nc, c = idx - i * nc;
+      const double* xi = A.fx.X + static_cast<int64_t>(i) * r;
+      double acc;
+      if (c < nF) {
+        acc = __ldg(A.fx.N0 + static_cast<int64_t>(i) * n + nint + c);
+        for (int j = 0; j < r; ++j) acc = fma(__ldg(xi + j), xs[c * r + j], acc);
+      } else {
+        acc = 0.0;
+        for (int l = 0; l < n; ++l) acc = fma(__ldg(A.fx.N0 + static_cast<int64_t>(i) * n + l), fe[l], acc);
+        for (int j = 0; j < r; ++j) acc = fma(__ldg(xi + j), xf[j], acc);
+      }
+      V[idx] = acc * ib;
+    }
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < nF * nc; idx += blockDim.x) {
+      const int p = idx / nc, q = idx - p * nc;
+      H[idx] = V[static_cast<int64_t>(nint + p) * nc + q];
+    }
+    const int P = neumann_order(A.fx.rho * a * ib, A.p_max, A.status);
+    double* yfull = (P >= 2) ? ws + L.yfull : nullptr;
+    __syncthreads();
+    // first order
+    for (int i0 = 0; i0 < n; i0 += kIB) {
+      const int blk = min(kIB, n - i0);
+      delta_block(A, a, b, n, nc, i0, blk, V, dblk, yblk);
+      if (yfull)
+        for (int idx = threadIdx.x; idx < blk * nc; idx += blockDim.x) yfull[static_cast<int64_t>(i0) * nc + idx] = yblk[idx];
+      accumulate_h(nF, nc, nint, i0, blk, V, yblk, H, -1.0);
+    }
+    // higher orders: T = A0^-1 Y, Y <- Delta T
+    for (int p = 2; p <= P; ++p) {
+      double* T = ws + L.t;
+      apply_a0inv(A, n, nc, s, ib, yfull, ws + L.xty, T);
+      const double sg = (p & 1) ? -1.0 : 1.0;
+      for (int i0 = 0; i0 < n; i0 += kIB) {
+        const int blk = min(kIB, n - i0);
+        delta_block(A, a, b, n, nc, i0, blk, T, dblk, yblk);
+        for (int idx = threadIdx.x; idx < blk * nc; idx += blockDim.x) yfull[static_cast<int64_t>(i0) * nc + idx] = yblk[idx];
+        accumulate_h(nF, nc, nint, i0, blk, V, yblk, H, sg);
+      }
+    }
+    // scatter: col ranks and row starts of the interior face slots
+    int64_t cc[3], own_f[6];
+    bool own_in[6];
+    cell_coords(m, e, cc);
+    for (int q = 0; q < nsl; ++q) own_f[q] = slot_face(m, cc, q, &own_in[q]);
+    for (int idx = threadIdx.x; idx < nsl * nsl; idx += blockDim.x) {
+      const int p = idx / nsl, q = idx - p * nsl;
+      rank[idx] = (own_in[p] && own_in[q]) ? col_rank(m, cc, p, q, own_f, own_in) : -1;
+    }
+    for (int idx = threadIdx.x; idx < nsl * dpf; idx += blockDim.x) {
+      const int p = idx / dpf, sub = idx - p * dpf;
+      rows[idx] = own_in[p] ? A.rowoff[A.mbase[own_f[p]] + sub] : -1;
+    }
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < nF * nc; idx += blockDim.x) {
+      const int i = idx / nc, q = idx - i * nc;
+      const int p = i / dpf;
+      if (!own_in[p]) continue;
+      const double v = H[idx];
+      if (q == nF) {
+        const int64_t row = A.mbase[own_f[p]] + (i - p * dpf);
+        A.g[row] = parity ? A.g[row] + v : v;
+        continue;
+      }
+      const int qs = q / dpf, sj = q - qs * dpf;
+      const int rk = rank[p * nsl + qs];
+      if (rk < 0) continue;
+      const int64_t pos = rows[i] + static_cast<int64_t>(rk) * dpf + sj;
+      A.hval[pos] = (parity == 1 && p == qs) ? A.hval[pos] + v : v;
+    }
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------------ recovery
+
+// x_hat_T = A_T^-1 (f_T - C_T^T lambda) by the same structured solve (one CTA per cell)
+__global__ void __launch_bounds__(kNT) k_recover_cta(RecArgs R, double* gws, int64_t ws_stride, int use_smem) {
+  extern __shared__ double smem[];
+  double* ws = use_smem ? smem : gws + blockIdx.x * ws_stride;
+  const DevMesh& m = R.m;
+  const int n = m.n, r = R.fx.r, dpf = m.dpf, nsl = 2 * m.dim, nint = m.nint;
+  double* s = ws;                 // r
+  double* y = ws + 64;            // n: current rhs
+  double* t = y + kMaxN;          // n: current term
+  double* acc = t + kMaxN;        // n: sum
+  double* xty = acc + kMaxN;      // r
+  HybArgs A;
+  A.m = R.m;
+  A.fx = R.fx;
+  for (int64_t e = blockIdx.x; e < m.ncells; e += gridDim.x) {
+    const double a = R.alpha[e], b = R.beta[e];
+    const double ib = 1.0 / b;
+    int64_t cc[3];
+    cell_coords(m, e, cc);
+    for (int j = threadIdx.x; j < r; j += blockDim.x) s[j] = b / fma(a, __ldg(R.fx.lam + j), b);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      double v = R.f[e * n + i];
+      if (i >= nint) {
+        const int p = (i - nint) / dpf, sub = (i - nint) - p * dpf;
+        bool in;
+        const int64_t f = slot_face(m, cc, p, &in);
+        if (in) v -= R.lambda[R.mbase[f] + sub];  // unit constraint rows: C_T^T lambda
+      }
+      y[i] = v;
+    }
+    __syncthreads();
+    const int P = neumann_order(R.fx.rho * a * ib, R.p_max, R.status);
+    for (int p = 0; p <= P; ++p) {
+      // t = A0^-1 y
+      for (int j = threadIdx.x; j < r; j += blockDim.x) {
+        double u = 0.0;
+        for (int l = 0; l < n; ++l) u = fma(__ldg(R.fx.X + static_cast<int64_t>(l) * r + j), y[l], u);
+        xty[j] = u * s[j];
+      }
+      __syncthreads();
+      for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        double u = 0.0;
+        for (int l = 0; l < n; ++l) u = fma(__ldg(R.fx.N0 + static_cast<int64_t>(i) * n + l), y[l], u);
+        for (int j = 0; j < r; ++j) u = fma(__ldg(R.fx.X + static_cast<int64_t>(i) * r + j), xty[j], u);
+        u *= ib;
+        t[i] = u;
+        acc[i] = (p == 0) ? u : ((p & 1) ? acc[i] - u : acc[i] + u);
+      }
+      __syncthreads();
+      if (p == P) break;
+      // y = Delta t
+      for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        double u = 0.0;
+        for (int l = 0; l < n; ++l) {
+          const int64_t o = static_cast<int64_t>(i) * n + l;
+          u = fma(delta_entry(a, b, __ldg(R.fx.D + o), __ldg(R.fx.M + o), __ldg(R.fx.E + o), __ldg(R.fx.Ma + o)), t[l], u);
+        }
+        y[i] = u;
+      }
+      __syncthreads();
+    }
+    for (int i = threadIdx.x; i < n; i += blockDim.x) R.x_hat[e * n + i] = acc[i];
+    __syncthreads();
+  }
+  (void)nsl;
+}
+
+// x = (P^T P)^-1 P^T x_hat: signed average of the face copies, bubbles copied
+// (src/reduction.cpp:396-404; the Gram matrix of the FE P is diagonal)
+__global__ void k_average(DevMesh m, const double* x_hat, double* x) {
+  const int64_t gdof = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  const int64_t nd = m.face_dof_count + m.ncells * m.nint;
+  if (gdof >= nd) return;
+  if (gdof >= m.face_dof_count) {
+    const int64_t b = gdof - m.face_dof_count;
+    const int64_t cell = b / m.nint, l = b - cell * m.nint;
+    x[gdof] = x_hat[cell * m.n + l];
+    return;
+  }
+  const int64_t f = gdof / m.dpf, sub = gdof - f * m.dpf;
+  int64_t cm, cp, co[3];
+  const int a = face_cells(m, f, &cm, &cp, co);
+  double sum = 0.0, cnt = 0.0;
+  if (cm >= 0) {  // +a face of cm: slot 2a+1, sign +1
+    sum += x_hat[cm * m.n + m.nint + (2 * a + 1) * m.dpf + sub];
+    cnt += 1.0;
+  }
+  if (cp >= 0) {  // -a face of cp: slot 2a, sign -1
+    sum += -1.0 * x_hat[cp * m.n + m.nint + (2 * a) * m.dpf + sub];
+    cnt += 1.0;
+  }
+  x[gdof] = sum * (1.0 / cnt);
+}
+
+}  // namespace
+
+void launch_hybridize_rt0(const HybArgs& a, const double* hc, int parity, cudaStream_t st) {
+  const int64_t cnt = parity_count(a.m);
+  const unsigned nb = static_cast<unsigned>((cnt + 127) / 128);
+  if (a.m.dim == 3) {
+    Rt0Const<6> c;
+    constexpr int N = 6;
+    memcpy(c.D, hc, sizeof(double) * N * N);
+    memcpy(c.M, hc + N * N, sizeof(double) * N * N);
+    memcpy(c.E, hc + 2 * N * N, sizeof(double) * N * N);
+    memcpy(c.Ma, hc + 3 * N * N, sizeof(double) * N * N);
+    memcpy(c.N0, hc + 4 * N * N, sizeof(double) * N * N);
+    memcpy(c.X, hc + 5 * N * N, sizeof(double) * N);
+    c.lam = hc[5 * N * N + N];
+    c.rho = hc[5 * N * N + N + 1];
+    k_hyb_rt0<3><<<nb, 128, 0, st>>>(a, c, parity);
+  } else {
+    Rt0Const<4> c;
+    constexpr int N = 4;
+    memcpy(c.D, hc, sizeof(double) * N * N);
+    memcpy(c.M, hc + N * N, sizeof(double) * N * N);
+    memcpy(c.E, hc + 2 * N * N, sizeof(double) * N * N);
+    memcpy(c.Ma, hc + 3 * N * N, sizeof(double) * N * N);
+    memcpy(c.N0, hc + 4 * N * N, sizeof(double) * N * N);
+    memcpy(c.X, hc + 5 * N * N, sizeof(double) * N);
+    c.lam = hc[5 * N * N + N];
+    c.rho = hc[5 * N * N + N + 1];
+    k_hyb_rt0<2><<<nb, 128, 0, st>>>(a, c, parity);
+  }
+  count_launch();
+}
+
+int64_t hybridize_cta_ws_doubles(const DevMesh& m, int nF, int r, int p_max, bool* use_smem) {
+  const CtaLayout L = cta_layout(m.n, nF, r, p_max);
+  *use_smem = L.total * 8 <= 200 * 1024;
+  return L.total;
+}
+
+static int sm_count() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+void launch_hybridize_cta(const HybArgs& a, int parity, double* gws, int64_t ws_doubles, cudaStream_t st) {
+  bool use_smem = false;
+  const int64_t need = hybridize_cta_ws_doubles(a.m, a.nF, a.fx.r, a.p_max, &use_smem);
+  const size_t smem = use_smem ? static_cast<size_t>(need) * 8 : 0;
+  if (use_smem) cudaFuncSetAttribute(k_hyb_cta, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  const int64_t cnt = parity_count(a.m);
+  int64_t grid = use_smem ? cnt : std::min<int64_t>(cnt, ws_doubles / need);
+  if (grid < 1) grid = 1;
+  if (grid > 1 << 30) grid = 1 << 30;
+  (void)sm_count;
+  k_hyb_cta<<<static_cast<unsigned>(grid), kNT, smem, st>>>(a, parity, gws, need, use_smem ? 1 : 0);
+  count_launch();
+}
+
+void launch_recover_hybrid(const RecArgs& a, double* gws, int64_t ws_doubles, cudaStream_t st) {
+  (void)gws;
+  (void)ws_doubles;
+  const size_t smem = static_cast<size_t>(64 + 3 * kMaxN + 64) * 8;
+  const int64_t grid = std::min<int64_t>(a.m.ncells, 1 << 20);
+  k_recover_cta<<<static_cast<unsigned>(grid), 128, smem, st>>>(a, nullptr, 0, 1);
+  count_launch();
+}
+
+void launch_average_faces(const DevMesh& m, const double* x_hat, double* x, cudaStream_t st) {
+  const int64_t nd = m.face_dof_count + m.ncells * m.nint;
+  k_average<<<static_cast<unsigned>((nd + 255) / 256), 256, 0, st>>>(m, x_hat, x);
+  count_launch();
+}
+
+}  // namespace hdr

@@ -1,0 +1,134 @@
+// K1: analytic CSR patterns of H (hybridize) and S (static_condense), built once
+// per space on the device.
+//
+// Reference: hybridize collects per-element triplets over the sorted multiplier
+// rows of each cell (src/reduction.cpp:304-337) and from_triplets sorts them
+// (src/csr.cpp:43-75); multiplier rows are interior faces in ascending face order
+// times dofs_per_face (multiplier_base, src/reduction.cpp:88-98).  So the H row
+// of a face F holds, ascending, the multiplier dofs of the interior faces of F's
+// two cells.  static_condense's S (src/reduction.cpp:509-555) is indexed by the
+// master global face dofs; its row of a face holds all faces of that face's cells.
+// Both are enumerated here with the same col_rank the element kernels scatter
+// with, so pattern and scatter agree by construction; tests pin the result
+// against the reference bit for bit.
+#include "hdr_device.cuh"
+#include "kernels.hpp"
+
+namespace hdr {
+
+namespace {
+
+__device__ inline int interior_faces_of(const DevMesh& m, const int64_t c[3]) {
+  int k = 0;
+  for (int s = 0; s < 2 * m.dim; ++s) {
+    bool in;
+    slot_face(m, c, s, &in);
+    k += in;
+  }
+  return k;
+}
+
+__global__ void k_face_counts(DevMesh m, int* flag, int64_t* fnnz_h, int64_t* fnnz_s) {
+  const int64_t f = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (f >= m.nfaces) return;
+  int64_t cm, cp, co[3];
+  face_cells(m, f, &cm, &cp, co);
+  const bool in = (cm >= 0 && cp >= 0);
+  flag[f] = in;
+  const int64_t d2 = static_cast<int64_t>(m.dpf) * m.dpf;
+  if (in) {
+    int64_t a[3], b[3];
+    cell_coords(m, cm, a);
+    cell_coords(m, cp, b);
+    fnnz_h[f] = d2 * (interior_faces_of(m, a) + interior_faces_of(m, b) - 1);
+    fnnz_s[f] = d2 * (4 * m.dim - 1);
+  } else {
+    fnnz_h[f] = 0;
+    fnnz_s[f] = d2 * (2 * m.dim);
+  }
+}
+
+__global__ void k_mbase(DevMesh m, const int* flag, const int* ord, int* mbase) {
+  const int64_t f = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (f >= m.nfaces) return;
+  mbase[f] = flag[f] ? ord[f] * m.dpf : -1;
+}
+
+__global__ void k_fill_patterns(DevMesh m, const int* mbase, const int64_t* fbase_h, const int64_t* fbase_s,
+                                int64_t* row_h, int32_t* col_h, int64_t* row_s, int32_t* col_s, int64_t nrows_h,
+                                int64_t nnz_h, int64_t nrows_s, int64_t nnz_s) {
+  const int64_t f = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (f == 0) {
+    row_h[nrows_h] = nnz_h;
+    row_s[nrows_s] = nnz_s;
+  }
+  if (f >= m.nfaces) return;
+  const int dpf = m.dpf, nsl = 2 * m.dim;
+  int64_t cm, cp, co[3];
+  const int a = face_cells(m, f, &cm, &cp, co);
+  const bool in = (cm >= 0 && cp >= 0);
+  const int64_t cells2[2] = {cm, cp};
+
+  // S rows: every face is a master (b = face dofs, src/reduction.cpp:474)
+  const int us = in ? 4 * m.dim - 1 : 2 * m.dim;
+  for (int sub = 0; sub < dpf; ++sub) row_s[f * dpf + sub] = fbase_s[f] + static_cast<int64_t>(sub) * dpf * us;
+  for (int w = 0; w < 2; ++w) {
+    if (cells2[w] < 0) continue;
+    int64_t c[3], own_f[6];
+    bool own_in[6];
+    cell_coords(m, cells2[w], c);
+    for (int t = 0; t < nsl; ++t) own_f[t] = slot_face(m, c, t, &own_in[t]);
+    const int s = 2 * a + (w == 0 ? 1 : 0);  // F is the +a face of cm, the -a face of cp
+    for (int t = 0; t < nsl; ++t) {
+      const int pos = col_rank(m, c, s, t, own_f, own_in, true);
+      for (int sub = 0; sub < dpf; ++sub)
+        for (int sj = 0; sj < dpf; ++sj)
+          col_s[row_s[f * dpf + sub] + static_cast<int64_t>(pos) * dpf + sj] = static_cast<int32_t>(own_f[t] * dpf + sj);
+    }
+  }
+  if (!in) return;
+  // H rows
+  const int mb = mbase[f];
+  int64_t ca[3], cb[3];
+  cell_coords(m, cm, ca);
+  cell_coords(m, cp, cb);
+  const int u = interior_faces_of(m, ca) + interior_faces_of(m, cb) - 1;
+  for (int sub = 0; sub < dpf; ++sub) row_h[mb + sub] = fbase_h[f] + static_cast<int64_t>(sub) * dpf * u;
+  for (int w = 0; w < 2; ++w) {
+    int64_t c[3], own_f[6];
+    bool own_in[6];
+    cell_coords(m, cells2[w], c);
+    for (int t = 0; t < nsl; ++t) own_f[t] = slot_face(m, c, t, &own_in[t]);
+    const int s = 2 * a + (w == 0 ? 1 : 0);
+    for (int t = 0; t < nsl; ++t) {
+      if (!own_in[t]) continue;
+      const int pos = col_rank(m, c, s, t, own_f, own_in, false);
+      const int gb = mbase[own_f[t]];
+      for (int sub = 0; sub < dpf; ++sub)
+        for (int sj = 0; sj < dpf; ++sj) col_h[row_h[mb + sub] + static_cast<int64_t>(pos) * dpf + sj] = gb + sj;
+    }
+  }
+}
+
+}  // namespace
+
+void launch_face_counts(const DevMesh& m, int* flag, int64_t* fnnz_h, int64_t* fnnz_s, cudaStream_t st) {
+  const int64_t nb = (m.nfaces + 255) / 256;
+  k_face_counts<<<static_cast<unsigned>(nb), 256, 0, st>>>(m, flag, fnnz_h, fnnz_s);
+  count_launch();
+}
+void launch_mbase(const DevMesh& m, const int* flag, const int* ord, int* mbase, cudaStream_t st) {
+  const int64_t nb = (m.nfaces + 255) / 256;
+  k_mbase<<<static_cast<unsigned>(nb), 256, 0, st>>>(m, flag, ord, mbase);
+  count_launch();
+}
+void launch_fill_patterns(const DevMesh& m, const int* mbase, const int64_t* fbase_h, const int64_t* fbase_s,
+                          int64_t* row_h, int32_t* col_h, int64_t* row_s, int32_t* col_s, int64_t nrows_h,
+                          int64_t nnz_h, int64_t nrows_s, int64_t nnz_s, cudaStream_t st) {
+  const int64_t nb = (m.nfaces + 127) / 128;
+  k_fill_patterns<<<static_cast<unsigned>(nb), 128, 0, st>>>(m, mbase, fbase_h, fbase_s, row_h, col_h, row_s, col_s,
+                                                              nrows_h, nnz_h, nrows_s, nnz_s);
+  count_launch();
+}
+
+}  // namespace hdr

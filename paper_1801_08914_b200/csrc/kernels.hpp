@@ -1,0 +1,62 @@
+// Host-side launch wrappers of the device kernels (one per .cu translation unit).
+#pragma once
+
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
+#include "hdr_device.cuh"
+
+namespace hdr {
+
+// counts every kernel this library launches (hdr_launch_count)
+void count_launch(int64_t k = 1);
+
+// ---- K1 patterns (kern_pattern.cu)
+void launch_face_counts(const DevMesh& m, int* flag, int64_t* fnnz_h, int64_t* fnnz_s, cudaStream_t st);
+void launch_mbase(const DevMesh& m, const int* flag, const int* ord, int* mbase, cudaStream_t st);
+void launch_fill_patterns(const DevMesh& m, const int* mbase, const int64_t* fbase_h, const int64_t* fbase_s,
+                          int64_t* row_h, int32_t* col_h, int64_t* row_s, int32_t* col_s, int64_t nrows_h,
+                          int64_t nnz_h, int64_t nrows_s, int64_t nnz_s, cudaStream_t st);
+
+// ---- structured element solve (kern_hybridize.cu)
+struct Fixed {  // device pointers to the per-space fixed factors (see hdr_internal.hpp)
+  const double *D, *M, *E, *Ma, *N0, *X, *lam;
+  int r;
+  double rho;
+};
+
+struct HybArgs {
+  DevMesh m;
+  Fixed fx;
+  int nF;        // face dofs per cell = 2*dim*dpf
+  int p_max;     // highest Neumann order allowed
+  const double *alpha, *beta, *f;
+  const int* mbase;
+  const int64_t* rowoff;
+  double* hval;  // H values (pattern order)
+  double* g;     // reduced rhs (m)
+  int* status;   // device flag: bit 0 = Neumann ratio out of range
+};
+
+// Small-element path (k = 0): one thread per cell, everything in registers.
+void launch_hybridize_rt0(const HybArgs& a, const double* host_consts, int parity, cudaStream_t st);
+// General path (k >= 1): one CTA per cell, shared-memory or global workspace.
+void launch_hybridize_cta(const HybArgs& a, int parity, double* gws, int64_t ws_doubles, cudaStream_t st);
+int64_t hybridize_cta_ws_doubles(const DevMesh& m, int nF, int r, int p_max, bool* use_smem);
+
+// ---- hybrid recovery: x_hat = A^-1 (f - C^T lambda) per cell (kern_hybridize.cu)
+struct RecArgs {
+  DevMesh m;
+  Fixed fx;
+  int nF, p_max;
+  const double *alpha, *beta, *f, *lambda;
+  const int* mbase;
+  double* x_hat;  // broken
+  double* x;      // global (ndofs): face dofs averaged, bubbles copied
+  int* status;
+};
+void launch_recover_hybrid(const RecArgs& a, double* gws, int64_t ws_doubles, cudaStream_t st);
+void launch_average_faces(const DevMesh& m, const double* x_hat, double* x, cudaStream_t st);
+
+}  // namespace hdr

@@ -1,0 +1,202 @@
+"""Parity of the device hybridization / recovery against the oracle (GPU).
+
+Contract:
+  * H row_offsets / col_indices bit-exact against the reference's hybridize
+    output (golden fixtures produced by the reference itself);
+  * H values, g, recovered x_hat / x within 1e-11 of max|entry| of the
+    element-wise double-double oracle evaluated on the bit-identical A_T
+    (tests/oracle_lib.py → oracle/hdr_oracle.c);
+  * bit-identical results on repeated runs (no float atomics).
+All calls go through the C ABI (libhdivred_b200.so) via the package front-end.
+"""
+import numpy as np
+import pytest
+
+from conftest import has_cuda, load_golden, GOLDEN_CASES
+from oracle_lib import Oracle, rel_err
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-11
+
+if not has_cuda():  # collected on CPU boxes too, skipped there
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_1801_08914_b200 as hd  # noqa: E402
+
+UNWEIGHTED = [c for c in GOLDEN_CASES if "weighted" not in c]
+
+
+def oracle_for(g):
+    o = Oracle(g["dim"], g["cells"], g["k"])
+    o.gen_inputs(g["coef"], g["seed"])
+    return o
+
+
+@pytest.mark.parametrize("name", UNWEIGHTED)
+def test_pattern_bit_exact_vs_reference(name):
+    g = load_golden(name)
+    sp = hd.Space(g["dim"], g["cells"], g["k"])
+    ro, ci = sp.pattern("H")
+    assert np.array_equal(ro, g["H.row_offsets"])
+    assert np.array_equal(ci, g["H.col_indices"])
+    ro, ci = sp.pattern("S")
+    assert np.array_equal(ro, g["S.row_offsets"])
+    assert np.array_equal(ci, g["S.col_indices"])
+    assert np.array_equal(sp.master_globals(), g["master_globals"])
+    gl, sg = sp.dof_map()
+    assert np.array_equal(gl, g["P.col_indices"])
+    assert np.array_equal(sg, g["P.values"])
+    dd, mm = sp.reference_matrices()
+    assert np.array_equal(dd.ravel(), g["ref_divdiv"]) and np.array_equal(mm.ravel(), g["ref_mass"])
+
+
+@pytest.mark.parametrize("name", UNWEIGHTED)
+def test_hybridize_values_vs_dd_oracle(name):
+    g = load_golden(name)
+    o = oracle_for(g)
+    o.run("port_hybridize")
+    o.run("dd_hybridize")
+    o.run("dd_recover")
+    sp = hd.Space(g["dim"], g["cells"], g["k"])
+    op = sp.hybridize(g["alpha"], g["beta"], g["f_hat"])
+    hv, gv = op.values()
+    h_dd, g_dd = o.get("H.values_dd"), o.get("g_dd")
+    assert rel_err(hv, h_dd) <= TOL, rel_err(hv, h_dd)
+    assert rel_err(gv, g_dd) <= TOL, rel_err(gv, g_dd)
+    x_hat, x = op.recover(g["lambda"], g["f_hat"])
+    assert rel_err(x_hat, o.get("x_hat_dd")) <= TOL
+    assert rel_err(x, o.get("x_dd")) <= TOL
+    # the reference's own distance to the truth, for the record
+    print(f"{name}: device-vs-DD H {rel_err(hv, h_dd):.1e} g {rel_err(gv, g_dd):.1e}; "
+          f"reference-vs-DD H {rel_err(g['H.values'], h_dd):.1e}")
+
+
+def test_explicit_reference_matrices_give_identical_bits():
+    g = load_golden("h3_rt1_2x2x2_logu")
+    n = int(np.sqrt(g["ref_divdiv"].size))
+    a = hd.Space(3, g["cells"], 1)
+    b = hd.Space(3, g["cells"], 1, ref_divdiv=g["ref_divdiv"].reshape(n, n), ref_mass=g["ref_mass"].reshape(n, n))
+    va = a.hybridize(g["alpha"], g["beta"], g["f_hat"]).values()
+    vb = b.hybridize(g["alpha"], g["beta"], g["f_hat"]).values()
+    assert np.array_equal(va[0], vb[0]) and np.array_equal(va[1], vb[1])
+
+
+@pytest.mark.parametrize("dim,cells,k,coef", [
+    (3, (8, 8, 8), 0, "logu:1e-2:1e2"), (3, (6, 5, 4), 1, "logu:1e-2:1e2"), (3, (5, 4, 4), 1, "logu:1e-3:1e3"),
+    (2, (9, 7), 1, "logu:1e-2:1e2"), (2, (6, 6), 2, "logu:1e-3:1e3"), (2, (5, 4), 3, "logu:1e-2:1e2"),
+    (3, (3, 3, 3), 2, "logu:1e-3:1e3"), (3, (3, 3, 2), 3, "checker:1e-2:1e2"), (3, (4, 4, 4), 1, "logu:1e-4:1e4"),
+])
+def test_hybridize_moderate_meshes_vs_dd(dim, cells, k, coef):
+    o = Oracle(dim, cells, k)
+    o.gen_inputs(coef, 4242)
+    o.run("port_hybridize")
+    o.run("dd_hybridize")
+    sp = hd.Space(dim, cells, k)
+    ro, ci = sp.pattern("H")
+    assert np.array_equal(ro, o.getq("H.row_offsets")) and np.array_equal(ci, o.getq("H.col_indices"))
+    op = sp.hybridize(o.get("alpha"), o.get("beta"), o.get("f_hat"))
+    hv, gv = op.values()
+    assert rel_err(hv, o.get("H.values_dd")) <= TOL
+    assert rel_err(gv, o.get("g_dd")) <= TOL
+
+
+def test_deterministic_and_device_inputs():
+    import torch
+
+    o = Oracle(3, (6, 6, 6), 1)
+    o.gen_inputs("logu:1e-2:1e2", 9)
+    a, b, f = o.get("alpha"), o.get("beta"), o.get("f_hat")
+    sp = hd.Space(3, (6, 6, 6), 1)
+    v1 = sp.hybridize(a, b, f).values()
+    v2 = sp.hybridize(a, b, f).values()
+    dev = [torch.from_numpy(x).cuda() for x in (a, b, f)]
+    v3 = sp.hybridize(*dev).values()
+    for x, y in ((v1, v2), (v1, v3)):
+        assert np.array_equal(x[0], y[0]) and np.array_equal(x[1], y[1])
+
+
+def test_zero_rhs_gives_zero_g_and_recovery():
+    """tests/unit_reduction.cpp:258-267."""
+    sp = hd.Space(3, (2, 2, 2), 0)
+    op = sp.hybridize(np.ones(8), np.ones(8), np.zeros(48))
+    _, g = op.values()
+    assert np.all(g == 0.0)
+    x_hat, x = op.recover(np.zeros(sp.m), np.zeros(48))
+    assert np.all(x_hat == 0.0) and np.all(x == 0.0)
+
+
+def test_single_cell_m0_recovery_is_direct_solve():
+    """tests/unit_reduction.cpp:268-276: m = 0, x_hat = A^-1 f."""
+    o = Oracle(3, (1, 1, 1), 1)
+    o.gen_inputs("uniform:1:1", 3)
+    sp = hd.Space(3, (1, 1, 1), 1)
+    assert sp.m == 0
+    op = sp.hybridize(o.get("alpha"), o.get("beta"), o.get("f_hat"))
+    x_hat, _ = op.recover(np.zeros(0), o.get("f_hat"))
+    ref = np.linalg.solve(o.element_matrix(0), o.get("f_hat"))
+    assert rel_err(x_hat, ref) <= 1e-11
+
+
+def test_hybridized_matrix_mirror():
+    """Mirror of the reference's python smoke test (tests/python/test_smoke.py:87-94)."""
+    (nrows, ncols, offsets, cols, vals), g = hd.hybridized_matrix({"cells": [2, 2, 2], "order": 0})
+    assert nrows == ncols == 12
+    assert len(g) == nrows and len(offsets) == nrows + 1 and len(cols) == len(vals) == offsets[-1]
+    assert all(np.isfinite(vals))
+
+
+FULL = [  # BASELINE.json configs 1, 2, 3, 5 (config 4 needs the Piola path)
+    (2, (64, 64), 0, "uniform:1:1", 1001, 55688),
+    (3, (64, 64, 64), 0, "logu:1e-2:1e2", 1002, 8394240),
+    (3, (48, 48, 48), 1, "logu:1e-2:1e2", 1003, 56088576),
+    (3, (32, 32, 32), 3, "checker:1e-2:1e2", 1005, 260505600),
+]
+
+
+@pytest.mark.parametrize("dim,cells,k,coef,seed,nnz", FULL)
+def test_full_size_sampled_rows_vs_dd(dim, cells, k, coef, seed, nnz):
+    """Full BASELINE sizes: pattern size as the analytic count, and sampled rows
+    of H / g against the element-wise DD oracle of both adjacent cells."""
+    o = Oracle(dim, cells, k)
+    o.gen_inputs(coef, seed)
+    o.run("structure")
+    sp = hd.Space(dim, cells, k)
+    assert sp.info["nnz_h"] == nnz
+    op = sp.hybridize(o.get("alpha"), o.get("beta"), o.get("f_hat"))
+    hv, gv = op.values()
+    ro, ci = sp.pattern("H")
+    assert ro[-1] == nnz and np.all(np.diff(ro) > 0)
+    assert np.all(np.isfinite(hv)) and np.all(np.isfinite(gv))
+    n = sp.n
+    rng = np.random.default_rng(seed)
+    # sampled cells and their +x neighbours, so shared-face blocks are complete
+    base = [int(e) for e in rng.choice(sp.ncells, 3 if k == 3 else 16, replace=False) if int(e) % cells[0] < cells[0] - 1]
+    have = set(base) | {e + 1 for e in base}
+    row_vals, row_g = {}, {}
+    for cell in sorted(have):
+        rows, h, gt, _ = o.dd_element(cell)
+        for a_, r in enumerate(rows):
+            row_g.setdefault(int(r), []).append(gt[a_])
+            for b_, c in enumerate(rows):
+                row_vals.setdefault((int(r), int(c)), []).append(h[a_, b_])
+    C = o.getq("C.col_indices").reshape(-1, 2)
+
+    def cells_of(row):
+        return {int(C[row, 0]) // n, int(C[row, 1]) // n}
+
+    worst_h, scale_h, worst_g, scale_g = 0.0, np.max(np.abs(hv)), 0.0, np.max(np.abs(gv))
+    checked = 0
+    for (r, c), parts in row_vals.items():
+        if not (cells_of(r) & cells_of(c)) <= have:
+            continue
+        p = ro[r] + np.searchsorted(ci[ro[r]:ro[r + 1]], c)
+        assert ci[p] == c
+        worst_h = max(worst_h, abs(hv[p] - sum(parts)))
+        checked += 1
+    for r, parts in row_g.items():
+        if cells_of(r) <= have:
+            worst_g = max(worst_g, abs(gv[r] - sum(parts)))
+    assert checked > 0
+    assert worst_h <= TOL * scale_h, worst_h / scale_h
+    assert worst_g <= TOL * scale_g, worst_g / scale_g
