@@ -35,13 +35,19 @@ __host__ __device__ inline void cell_coords(const DevMesh& m, int64_t cell, int6
   c[2] = r / m.N[1];
 }
 
-// face of slot s of the cell at c; interior iff the cell across it exists
+// face of slot s of the cell at c; interior iff the cell across it exists.
+// (Written without dynamic indexing of local arrays: an earlier form with
+// x[a] += side miscompiled under nvcc 12.9 -O3 for sm_100a.)
 __host__ __device__ inline int64_t slot_face(const DevMesh& m, const int64_t c[3], int s, bool* interior) {
   const int a = s >> 1, side = s & 1;
-  int64_t x[3] = {c[0], c[1], c[2]};
-  x[a] += side;
-  if (interior) *interior = side ? (c[a] + 1 < m.N[a]) : (c[a] > 0);
-  return face_id(m, a, x[0], x[1], x[2]);
+  const int64_t c0 = c[0], c1 = c[1], c2 = c[2];
+  const int64_t x0 = c0 + (a == 0 ? side : 0), x1 = c1 + (a == 1 ? side : 0), x2 = c2 + (a == 2 ? side : 0);
+  const int64_t ca = a == 0 ? c0 : (a == 1 ? c1 : c2);
+  const int64_t na = a == 0 ? m.N[0] : (a == 1 ? m.N[1] : m.N[2]);
+  if (interior) *interior = side ? (ca + 1 < na) : (ca > 0);
+  const int64_t d0 = m.N[0] + (a == 0), d1 = m.N[1] + (a == 1);
+  const int64_t off = a == 0 ? m.foff[0] : (a == 1 ? m.foff[1] : m.foff[2]);
+  return off + x0 + d0 * (x1 + d1 * x2);
 }
 
 // face f -> axis and the two adjacent cells (-1 if absent)   (mesh.cpp:94-120)
@@ -58,15 +64,15 @@ __host__ __device__ inline int face_cells(const DevMesh& m, int64_t f, int64_t* 
   local /= d0;
   co[1] = local % d1;
   co[2] = local / d1;
-  const int64_t plane = co[a];
+  const int64_t plane = a == 0 ? co[0] : (a == 1 ? co[1] : co[2]);
+  const int64_t na = a == 0 ? m.N[0] : (a == 1 ? m.N[1] : m.N[2]);
   *cm = -1;
   *cp = -1;
   if (plane > 0) {
-    int64_t x[3] = {co[0], co[1], co[2]};
-    x[a] -= 1;
-    *cm = x[0] + m.N[0] * (x[1] + m.N[1] * x[2]);
+    const int64_t x0 = co[0] - (a == 0), x1 = co[1] - (a == 1), x2 = co[2] - (a == 2);
+    *cm = x0 + m.N[0] * (x1 + m.N[1] * x2);
   }
-  if (plane < m.N[a]) *cp = co[0] + m.N[0] * (co[1] + m.N[1] * co[2]);
+  if (plane < na) *cp = co[0] + m.N[0] * (co[1] + m.N[1] * co[2]);
   return a;
 }
 
@@ -94,8 +100,8 @@ __host__ __device__ inline int col_rank(const DevMesh& m, const int64_t c[3], in
   for (int u = 0; u < t; ++u) r += (all_faces || own_int[u]);
   if (!own_int[s]) return r;  // boundary face: the row holds this cell's faces only
   const int a = s >> 1, side = s & 1;
-  int64_t nb[3] = {c[0], c[1], c[2]};
-  nb[a] += side ? 1 : -1;
+  const int64_t step = side ? 1 : -1;
+  const int64_t nb[3] = {c[0] + (a == 0 ? step : 0), c[1] + (a == 1 ? step : 0), c[2] + (a == 2 ? step : 0)};
   const int shared = 2 * a + (1 - side);
   const int64_t ft = own_f[t];
   for (int v = 0; v < 2 * m.dim; ++v) {
