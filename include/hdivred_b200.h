@@ -115,13 +115,24 @@ hdr_status hdr_space_dof_map(hdr_space_t space, int64_t* global, double* sign);
  * Creates a new operator in *out (device resident; nothing is copied back). */
 hdr_status hdr_hybridize_fe(hdr_space_t space, const double* alpha, const double* beta, const double* f_hat,
                             int on_device, hdr_hybrid_t* out);
-/* Same, reusing an existing operator's device buffers (steady-state loop). */
+/* Same, reusing an existing operator's device buffers (steady-state loop).
+ * Device-resident alpha/beta are borrowed (recovery re-reads them): keep them
+ * alive and unchanged until the next hybridize on this operator. */
 hdr_status hdr_hybridize_fe_into(hdr_hybrid_t op, const double* alpha, const double* beta, const double* f_hat,
                                  int on_device);
+/* Asynchronous form: enqueues the H2D staging (host inputs; pinned memory
+ * copies asynchronously) and the kernels on the space's stream and returns.
+ * Errors detected on the device are reported by the next hdr_hybrid_check. */
+hdr_status hdr_hybridize_fe_enqueue(hdr_hybrid_t op, const double* alpha, const double* beta, const double* f_hat,
+                                    int on_device);
+/* Synchronizes the stream and reports device-side status of enqueued work. */
+hdr_status hdr_hybrid_check(hdr_hybrid_t op);
 void hdr_hybrid_destroy(hdr_hybrid_t op);
 /* Copy H values (nnz_H, in the space's pattern order) and/or g (m); NULL
  * skips.  dst_on_device selects device-to-device copies. */
 hdr_status hdr_hybrid_values(hdr_hybrid_t op, double* h_values, double* g, int dst_on_device);
+/* Asynchronous copy-out (enqueued on the space's stream). */
+hdr_status hdr_hybrid_values_enqueue(hdr_hybrid_t op, double* h_values, double* g, int dst_on_device);
 /* Device pointers of H values / g / pattern (borrowed; valid while op lives).
  * row_offsets are int64, col_indices int32 on the device. */
 hdr_status hdr_hybrid_device_ptrs(hdr_hybrid_t op, const double** h_values, const double** g,
@@ -180,6 +191,9 @@ const char* hdr_version(void);
 /* Number of kernels this library launched since load (launch accounting for
  * bench.py's gpu_launches). */
 int64_t hdr_launch_count(void);
+/* FP64 FMA throughput of device 0 in TFLOP/s (2 flops per DFMA), measured with
+ * a register-resident DFMA chain kernel; the fp64 roofline denominator. */
+hdr_status hdr_measure_fp64_peak(double* tflops, double* ms);
 /* Synchronize the space's stream. */
 hdr_status hdr_space_synchronize(hdr_space_t space);
 

@@ -217,8 +217,12 @@ class Space:
         return gl, sg
 
     def set_stream(self, stream_ptr: Optional[int]) -> None:
-        """Run on a caller's CUDA stream (e.g. torch.cuda.current_stream().cuda_stream)."""
-        _check(_lib().hdr_space_set_stream(self._h, ctypes.c_void_p(stream_ptr) if stream_ptr else None))
+        """Run on a caller's CUDA stream handle (e.g. torch.cuda.Stream().cuda_stream).
+        0 binds the legacy default stream; None restores the library's own stream."""
+        if stream_ptr is None:
+            _check(_lib().hdr_space_set_stream(self._h, None))
+        else:
+            _check(_lib().hdr_space_set_stream(self._h, ctypes.c_void_p(stream_ptr if stream_ptr else 1)))
 
     def synchronize(self) -> None:
         _check(_lib().hdr_space_synchronize(self._h))
@@ -265,6 +269,21 @@ class HybridizedOperator:
         f = _as_f64(f_hat, sp.broken_ndofs, "f_hat")
         dev = _same_device([a, b, f])
         _check(_lib().hdr_hybridize_fe_into(self._h, _ptr(a)[0], _ptr(b)[0], _ptr(f)[0], dev))
+
+    def enqueue(self, alpha, beta, f_hat) -> None:
+        """Asynchronous hybridize on the space's stream (no host sync); host
+        inputs should be pinned.  Device errors surface in check()."""
+        sp = self.space
+        dev = _same_device([alpha, beta, f_hat])
+        _check(_lib().hdr_hybridize_fe_enqueue(self._h, _ptr(alpha)[0], _ptr(beta)[0], _ptr(f_hat)[0], dev))
+
+    def values_enqueue(self, h_out, g_out) -> None:
+        """Asynchronous copy of H values / g into caller buffers (host pinned or device)."""
+        dev = _same_device([h_out, g_out])
+        _check(_lib().hdr_hybrid_values_enqueue(self._h, _ptr(h_out)[0], _ptr(g_out)[0], dev))
+
+    def check(self) -> None:
+        _check(_lib().hdr_hybrid_check(self._h))
 
     def values(self):
         """(H values in pattern order, g) as host arrays."""
@@ -479,6 +498,14 @@ def space_info(dim: int, cells: Sequence[int], order: int) -> dict:
     ndofs = nfaces * dpf + ncells * nint
     return {"ncells": ncells, "nfaces": nfaces, "ndofs": ndofs, "broken_ndofs": ncells * (2 * dim * dpf + nint),
             "dofs_per_face": dpf, "interior_dofs_per_cell": nint}
+
+
+def measure_fp64_peak() -> tuple[float, float]:
+    """(TFLOP/s, ms) of the device's DFMA throughput (fp64 roofline denominator)."""
+    t = ctypes.c_double()
+    ms = ctypes.c_double()
+    _check(_lib().hdr_measure_fp64_peak(ctypes.byref(t), ctypes.byref(ms)))
+    return t.value, ms.value
 
 
 def launch_count() -> int:

@@ -102,6 +102,8 @@ struct hdr_hybrid_s {
   DBuf<double> hval, g, alpha, beta, f, ws;
   DBuf<int> status;
   int64_t ws_doubles = 0;
+  const double* a_ptr = nullptr;  // coefficients used by the last hybridize (owned copy or borrowed device input)
+  const double* b_ptr = nullptr;
 };
 
 struct hdr_condensed_s {
@@ -145,6 +147,17 @@ void stage(DBuf<double>& dst, const double* src, int64_t count, int on_device, c
   if (count == 0) return;
   CK(cudaMemcpyAsync(dst.p, src, static_cast<size_t>(count) * 8,
                      on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+}
+
+// Synchronizes the stream and reports (then clears) the sticky device status.
+hdr_status check_status(int* d_status, cudaStream_t st) {
+  int status = 0;
+  CK(cudaMemcpyAsync(&status, d_status, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (status) CK(cudaMemsetAsync(d_status, 0, sizeof(int), st));
+  if (status & 1)
+    return fail(HDR_UNSUPPORTED, "coefficient ratio alpha/beta outside the structured solve's range on some cell");
+  return HDR_OK;
 }
 
 }  // namespace
@@ -437,28 +450,28 @@ hdr_status hdr_space_dof_map(hdr_space_t sp, int64_t* global, double* sign) {
 }
 
 static hdr_status run_hybridize(hdr_hybrid_t op, const double* alpha, const double* beta, const double* f_hat,
-                                int on_device) {
+                                int on_device, bool sync) {
   hdr_space_t sp = op->sp;
   return catch_all([&]() -> hdr_status {
     cudaStream_t st = sp->stream;
     const double *da = alpha, *db = beta, *df = f_hat;
-    if (!on_device) {
+    if (!on_device) {  // host inputs: staged into owned device buffers (pinned sources copy asynchronously)
       stage(op->alpha, alpha, sp->ncells, 0, st);
       stage(op->beta, beta, sp->ncells, 0, st);
       stage(op->f, f_hat, sp->broken, 0, st);
       da = op->alpha.p;
       db = op->beta.p;
       df = op->f.p;
-    } else {  // recovery needs the coefficients later: keep device copies (16 B/cell)
-      stage(op->alpha, alpha, sp->ncells, 1, st);
-      stage(op->beta, beta, sp->ncells, 1, st);
-      da = op->alpha.p;
-      db = op->beta.p;
     }
+    // device inputs are borrowed: recovery re-reads alpha/beta from them
+    op->a_ptr = da;
+    op->b_ptr = db;
     if (!op->hval.p) op->hval.alloc(sp->nnz_h);
     if (!op->g.p) op->g.alloc(sp->m);
-    if (!op->status.p) op->status.alloc(1);
-    CK(cudaMemsetAsync(op->status.p, 0, sizeof(int), st));
+    if (!op->status.p) {
+      op->status.alloc(1);
+      CK(cudaMemsetAsync(op->status.p, 0, sizeof(int), st));
+    }
     HybArgs A{};
     A.m = sp->dm;
     A.fx = sp->fx;
@@ -484,12 +497,8 @@ static hdr_status run_hybridize(hdr_hybrid_t op, const double* alpha, const doub
       for (int parity = 0; parity < 2; ++parity) launch_hybridize_cta(A, parity, op->ws.p, op->ws_doubles, st);
     }
     CK(cudaGetLastError());
-    int status = 0;
-    CK(cudaMemcpyAsync(&status, op->status.p, sizeof(int), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    if (status & 1)
-      return fail(HDR_UNSUPPORTED, "coefficient ratio alpha/beta outside the structured solve's range on some cell");
-    return HDR_OK;
+    if (!sync) return HDR_OK;
+    return check_status(op->status.p, st);
   });
 }
 
@@ -499,7 +508,7 @@ hdr_status hdr_hybridize_fe(hdr_space_t sp, const double* alpha, const double* b
   *out = nullptr;
   auto op = std::make_unique<hdr_hybrid_s>();
   op->sp = sp;
-  const hdr_status s = run_hybridize(op.get(), alpha, beta, f_hat, on_device);
+  const hdr_status s = run_hybridize(op.get(), alpha, beta, f_hat, on_device, true);
   if (s != HDR_OK) return s;
   *out = op.release();
   return HDR_OK;
@@ -508,7 +517,30 @@ hdr_status hdr_hybridize_fe(hdr_space_t sp, const double* alpha, const double* b
 hdr_status hdr_hybridize_fe_into(hdr_hybrid_t op, const double* alpha, const double* beta, const double* f_hat,
                                  int on_device) {
   if (!op || !alpha || !beta || !f_hat) return fail(HDR_INVALID_ARGUMENT, "null argument");
-  return run_hybridize(op, alpha, beta, f_hat, on_device);
+  return run_hybridize(op, alpha, beta, f_hat, on_device, true);
+}
+
+hdr_status hdr_hybridize_fe_enqueue(hdr_hybrid_t op, const double* alpha, const double* beta, const double* f_hat,
+                                   int on_device) {
+  if (!op || !alpha || !beta || !f_hat) return fail(HDR_INVALID_ARGUMENT, "null argument");
+  return run_hybridize(op, alpha, beta, f_hat, on_device, false);
+}
+
+hdr_status hdr_hybrid_check(hdr_hybrid_t op) {
+  if (!op) return fail(HDR_INVALID_ARGUMENT, "null operator");
+  return catch_all([&]() -> hdr_status { return check_status(op->status.p, op->sp->stream); });
+}
+
+hdr_status hdr_hybrid_values_enqueue(hdr_hybrid_t op, double* h_values, double* g, int dst_on_device) {
+  if (!op) return fail(HDR_INVALID_ARGUMENT, "null operator");
+  return catch_all([&]() -> hdr_status {
+    const cudaMemcpyKind kind = dst_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+    cudaStream_t st = op->sp->stream;
+    if (h_values && op->sp->nnz_h)
+      CK(cudaMemcpyAsync(h_values, op->hval.p, static_cast<size_t>(op->sp->nnz_h) * 8, kind, st));
+    if (g && op->sp->m) CK(cudaMemcpyAsync(g, op->g.p, static_cast<size_t>(op->sp->m) * 8, kind, st));
+    return HDR_OK;
+  });
 }
 
 void hdr_hybrid_destroy(hdr_hybrid_t op) { delete op; }
@@ -560,15 +592,17 @@ hdr_status hdr_recover_hybrid(hdr_hybrid_t op, const double* lambda, const doubl
       dx.alloc(sp->ndofs);
       px = dx.p;
     }
-    if (!op->status.p) op->status.alloc(1);
-    CK(cudaMemsetAsync(op->status.p, 0, sizeof(int), st));
+    if (!op->status.p) {
+      op->status.alloc(1);
+      CK(cudaMemsetAsync(op->status.p, 0, sizeof(int), st));
+    }
     RecArgs R{};
     R.m = sp->dm;
     R.fx = sp->fx;
     R.nF = sp->nF;
     R.p_max = 4;
-    R.alpha = op->alpha.p;
-    R.beta = op->beta.p;
+    R.alpha = op->a_ptr;
+    R.beta = op->b_ptr;
     R.f = pf;
     R.lambda = pl;
     R.mbase = sp->mbase.p;
@@ -582,11 +616,7 @@ hdr_status hdr_recover_hybrid(hdr_hybrid_t op, const double* lambda, const doubl
       if (x_hat) CK(cudaMemcpyAsync(x_hat, pxh, static_cast<size_t>(sp->broken) * 8, cudaMemcpyDeviceToHost, st));
       if (x) CK(cudaMemcpyAsync(x, px, static_cast<size_t>(sp->ndofs) * 8, cudaMemcpyDeviceToHost, st));
     }
-    int status = 0;
-    CK(cudaMemcpyAsync(&status, op->status.p, sizeof(int), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    if (status & 1) return fail(HDR_UNSUPPORTED, "coefficient ratio outside the structured solve's range");
-    return HDR_OK;
+    return check_status(op->status.p, st);
   });
 }
 
