@@ -11,6 +11,7 @@
 #include <functional>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -264,6 +265,9 @@ hdr_status hdr_space_create(int dim, const int64_t cells[3], const double h[3], 
     }
     m.nfaces = off;
     m.ncells = sp->N[0] * sp->N[1] * sp->N[2];
+    m.div_half = FastDiv(static_cast<uint32_t>((sp->N[0] + 1) / 2));
+    m.div_n0 = FastDiv(static_cast<uint32_t>(sp->N[0]));
+    m.div_n1 = FastDiv(static_cast<uint32_t>(sp->N[1]));
     m.face_dof_count = m.nfaces * sp->dpf;
     sp->ncells = m.ncells;
     sp->nfaces = m.nfaces;
@@ -486,7 +490,17 @@ static hdr_status run_hybridize(hdr_hybrid_t op, const double* alpha, const doub
     A.g = op->g.p;
     A.status = op->status.p;
     if (sp->k == 0) {
-      for (int parity = 0; parity < 2; ++parity) launch_hybridize_rt0(A, sp->rt0_consts.data(), parity, st);
+      static const bool legacy = getenv("HDR_RT0_LEGACY") != nullptr;
+      if (legacy) {
+        for (int parity = 0; parity < 2; ++parity) launch_hybridize_rt0(A, sp->rt0_consts.data(), parity, st);
+      } else {
+        const int64_t need = parity_count(sp->dm) * sp->n * (sp->n + 1);
+        if (op->ws_doubles < need) {
+          op->ws.alloc(static_cast<size_t>(need));
+          op->ws_doubles = need;
+        }
+        launch_hybridize_rt0_rows(A, sp->rt0_consts.data(), op->ws.p, st);
+      }
     } else {
       bool use_smem = false;
       const int64_t need = hybridize_cta_ws_doubles(sp->dm, sp->nF, sp->r, A.p_max, &use_smem);

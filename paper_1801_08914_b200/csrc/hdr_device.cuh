@@ -10,6 +10,26 @@ namespace hdr {
 constexpr int kMaxN = 240;  // RT3 hexahedron
 constexpr int kMaxR = 64;
 
+// Unsigned 32-bit division by a runtime-invariant divisor via a precomputed
+// magic multiplier (round-up method): q = (umulhi(n, m) + n) >> l.
+struct FastDiv {
+  uint32_t d = 1, m = 0, l = 0;
+  FastDiv() = default;
+  explicit FastDiv(uint32_t div) : d(div) {
+    l = 0;
+    while ((uint64_t(1) << l) < div) ++l;
+    m = static_cast<uint32_t>(((uint64_t(1) << 32) * ((uint64_t(1) << l) - div)) / div + 1);
+  }
+  __host__ __device__ inline uint32_t div(uint32_t n) const {
+#ifdef __CUDA_ARCH__
+    const uint32_t hi = __umulhi(n, m);
+#else
+    const uint32_t hi = static_cast<uint32_t>((static_cast<uint64_t>(n) * m) >> 32);
+#endif
+    return static_cast<uint32_t>((static_cast<uint64_t>(hi) + n) >> l);
+  }
+};
+
 // Structured mesh numbering (src/mesh.cpp:13-135): cells lexicographic x fastest;
 // faces grouped by axis, lexicographic in the (N + e_axis) grid; a cell's faces
 // in slot order (-x,+x,-y,+y,-z,+z) with outward signs -1,+1.
@@ -21,7 +41,37 @@ struct DevMesh {
   int64_t N[3];
   int64_t foff[3];  // first face index of each axis group
   int64_t nfaces, ncells, face_dof_count;
+  FastDiv div_half, div_n0, div_n1;  // (N0+1)/2, N0, N1
 };
+
+// 32-bit fast paths (every mesh the device path accepts has < 2^31 cells and faces)
+__host__ __device__ inline void cell_coords32(const DevMesh& m, uint32_t cell, int c[3]) {
+  const uint32_t r = m.div_n0.div(cell);
+  c[0] = static_cast<int>(cell - r * static_cast<uint32_t>(m.N[0]));
+  const uint32_t z = m.div_n1.div(r);
+  c[1] = static_cast<int>(r - z * static_cast<uint32_t>(m.N[1]));
+  c[2] = static_cast<int>(z);
+}
+// parity_cell in 32-bit: t -> (cell or -1, coordinates)
+__host__ __device__ inline int parity_cell32(const DevMesh& m, int parity, uint32_t t, int c[3]) {
+  const uint32_t half = static_cast<uint32_t>((m.N[0] + 1) / 2);
+  const uint32_t row = m.div_half.div(t);
+  const uint32_t j = t - row * half;
+  const uint32_t z = m.div_n1.div(row);
+  const uint32_t y = row - z * static_cast<uint32_t>(m.N[1]);
+  if (z >= static_cast<uint32_t>(m.N[2])) return -1;
+  const uint32_t x = ((parity + y + z) & 1u) + 2u * j;
+  if (x >= static_cast<uint32_t>(m.N[0])) return -1;
+  c[0] = static_cast<int>(x);
+  c[1] = static_cast<int>(y);
+  c[2] = static_cast<int>(z);
+  return static_cast<int>(x + static_cast<uint32_t>(m.N[0]) * (y + static_cast<uint32_t>(m.N[1]) * z));
+}
+__host__ __device__ inline int face_id32(const DevMesh& m, int axis, int x, int y, int z) {
+  const int d0 = static_cast<int>(m.N[0]) + (axis == 0), d1 = static_cast<int>(m.N[1]) + (axis == 1);
+  const int off = static_cast<int>(axis == 0 ? m.foff[0] : (axis == 1 ? m.foff[1] : m.foff[2]));
+  return off + x + d0 * (y + d1 * z);
+}
 
 __host__ __device__ inline int64_t face_id(const DevMesh& m, int axis, int64_t x, int64_t y, int64_t z) {
   const int64_t d0 = m.N[0] + (axis == 0), d1 = m.N[1] + (axis == 1);
@@ -110,6 +160,47 @@ __host__ __device__ inline int col_rank(const DevMesh& m, const int64_t c[3], in
     const int64_t f = slot_face(m, nb, v, &in);
     r += ((all_faces || in) && f < ft);
   }
+  return r;
+}
+
+// Closed form of col_rank.  Face ids are grouped by axis (all x-faces < all
+// y-faces < all z-faces) and, inside an axis-b group, the four b-faces of a cell
+// c and its neighbour nb = c +- e_a order by the b-grid strides (s_a < s_b iff
+// a < b, and s_a >= 2 s_b for a > b).  in_lo[b] / in_hi[b]: c's -b / +b faces
+// are interior; the neighbour's b-faces (b != a) share those flags.  all_faces:
+// count boundary faces too (S rows).  Pinned against col_rank by
+// tests/test_host.py::test_closed_form_ranks.
+struct CellFlags {
+  bool lo[3], hi[3];
+  bool far_lo, far_hi;  // c_a >= 2 / c_a + 2 < N_a: neighbour's far a-face interior
+};
+
+__host__ __device__ constexpr int col_rank_fast(int dim, int p, int q, unsigned lo, unsigned hi, int64_t ca, int64_t na,
+                                             bool all_faces) {
+  // lo / hi: bit x set iff the cell's -x / +x face is interior
+  const int a = p >> 1, sp = p & 1, b = q >> 1, sq = q & 1;
+  const int own_p_in = sp ? (ca + 1 < na) : (ca > 0);
+  const unsigned L = all_faces ? 7u : lo, H = all_faces ? 7u : hi;
+  if (!own_p_in) {  // boundary row (S only): this cell's faces in slot order
+    int r = 0;
+    for (int u = 0; u < q; ++u) r += ((u & 1) ? (H >> (u >> 1)) : (L >> (u >> 1))) & 1u;
+    return r;
+  }
+  const int far = all_faces ? 1 : (sp ? (ca + 2 < na) : (ca >= 2));
+  const int La = (L >> a) & 1u, Ha = (H >> a) & 1u, Lb = (L >> b) & 1u, Hb = (H >> b) & 1u;
+  int r = 0;
+  for (int x = 0; x < b; ++x)
+    r += (x == a) ? (sp ? La + 1 + far : far + 1 + Ha) : 2 * static_cast<int>(((L >> x) & 1u) + ((H >> x) & 1u));
+  if (b == a) {
+    if (sp) r += sq ? La : 0;
+    else r += sq ? far + 1 : far;
+  } else if (sp) {
+    if (sq) r += (a < b) ? 2 * Lb : Lb;
+  } else {
+    if (a < b) r += sq ? 2 * Lb + Hb : Lb;
+    else r += sq ? 2 * Lb + Hb : Lb + Hb;
+  }
+  (void)dim;
   return r;
 }
 

@@ -20,10 +20,18 @@
 // item 7) and fl(a+b) = fl(b+a), so the result is deterministic without atomics.
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "hdr_device.cuh"
 #include "kernels.hpp"
+
+#ifndef HDR_ROWS_MINB
+#define HDR_ROWS_MINB 6
+#endif
+#ifndef HDR_RT0_MINB
+#define HDR_RT0_MINB 2
+#endif
 
 namespace hdr {
 
@@ -51,14 +59,76 @@ struct Rt0Const {
   double lam, rho;
 };
 
-// Higher Neumann orders for one RT0 cell (rare: tau > 1e-7).  A0^-1 = V here.
-template <int N>
-__device__ __noinline__ void rt0_higher(const Rt0Const<N>& c, double a, double b, const double (&V)[N][N],
-                                        const double (&w)[N], int P, double (&H)[N][N], double (&gg)[N]) {
-  double T[N][N + 1], Y[N][N + 1];
+// Deterministic scatter of one RT0 cell's H_T (N x N) and g_T (dpf = 1: one H
+// row per interior face).  Colour 0 stores; colour 1 adds on same-face entries.
+template <int DIM>
+__device__ __forceinline__ void rt0_scatter(const HybArgs& A, int64_t e, int parity, const double (&H)[2 * DIM][2 * DIM],
+                                            const double (&gg)[2 * DIM]) {
+  constexpr int N = 2 * DIM;
+  int64_t cc[3];
+  cell_coords(A.m, e, cc);
+  bool in_lo[3] = {false, false, false}, in_hi[3] = {false, false, false};
+  int64_t own_f[N];
+#pragma unroll
+  for (int q = 0; q < N; ++q) {
+    bool in;
+    own_f[q] = slot_face(A.m, cc, q, &in);
+    if (q & 1)
+      in_hi[q >> 1] = in;
+    else
+      in_lo[q >> 1] = in;
+  }
+#pragma unroll
+  for (int p = 0; p < N; ++p) {
+    const bool pin = (p & 1) ? in_hi[p >> 1] : in_lo[p >> 1];
+    if (!pin) continue;
+    const int a = p >> 1;
+    const int64_t ca = a == 0 ? cc[0] : (a == 1 ? cc[1] : cc[2]);
+    const int64_t na = a == 0 ? A.m.N[0] : (a == 1 ? A.m.N[1] : A.m.N[2]);
+    const int row = A.mbase[own_f[p]];
+    const int64_t start = A.rowoff[row];
+#pragma unroll
+    for (int q = 0; q < N; ++q) {
+      const bool qin = (q & 1) ? in_hi[q >> 1] : in_lo[q >> 1];
+      if (!qin) continue;
+      unsigned lm = 0, hm = 0;
+#pragma unroll
+      for (int x = 0; x < DIM; ++x) {
+        lm |= static_cast<unsigned>(in_lo[x]) << x;
+        hm |= static_cast<unsigned>(in_hi[x]) << x;
+      }
+      const int64_t pos = start + col_rank_fast(DIM, p, q, lm, hm, ca, na, false);
+      A.hval[pos] = (parity == 1 && p == q) ? A.hval[pos] + H[p][q] : H[p][q];
+    }
+    A.g[row] = (parity == 1) ? A.g[row] + gg[p] : gg[p];
+  }
+}
+
+// Cells that need Neumann order P >= 2 (tau > 1e-7; none at BASELINE's
+// coefficient ranges): recomputed here from scalars only, so the fast path's
+// register arrays never have their address taken.
+template <int DIM>
+__device__ __noinline__ void rt0_general(HybArgs A, int64_t e, int parity, int P) {
+  constexpr int N = 2 * DIM;
+  struct {  // fixed factors read from global memory (the kernel's parameter block must not escape)
+    const double *D, *M, *E, *Ma, *N0, *X;
+    double lam;
+  } c{A.fx.D, A.fx.M, A.fx.E, A.fx.Ma, A.fx.N0, A.fx.X, A.fx.lam[0]};
+  const double a = A.alpha[e], b = A.beta[e];
+  const double ib = 1.0 / b;
+  const double s = b / fma(a, c.lam, b);
+  double V[N][N], T[N][N + 1], Y[N][N + 1], H[N][N], gg[N];
+  for (int i = 0; i < N; ++i)
+    for (int j = 0; j < N; ++j) V[i][j] = fma(c.X[i] * s, c.X[j], c.N0[i * N + j]) * ib;
   for (int i = 0; i < N; ++i) {
-    for (int j = 0; j < N; ++j) T[i][j] = V[i][j];
-    T[i][N] = w[i];
+    double acc = 0.0;
+    for (int j = 0; j < N; ++j) {
+      acc = fma(V[i][j], A.f[e * N + j], acc);
+      T[i][j] = V[i][j];
+      H[i][j] = V[i][j];
+    }
+    T[i][N] = acc;
+    gg[i] = acc;
   }
   for (int p = 1; p <= P; ++p) {
     for (int k = 0; k < N; ++k)
@@ -69,30 +139,28 @@ __device__ __noinline__ void rt0_higher(const Rt0Const<N>& c, double a, double b
         Y[k][j] = acc;
       }
     const double sg = (p & 1) ? -1.0 : 1.0;
-    if (p >= 2) {
-      for (int i = 0; i < N; ++i) {
-        for (int q = 0; q < N; ++q) {
-          double acc = 0.0;
-          for (int k = 0; k < N; ++k) acc = fma(V[k][i], Y[k][q], acc);
-          H[i][q] = fma(sg, acc, H[i][q]);
-        }
+    for (int i = 0; i < N; ++i) {
+      for (int q = 0; q <= N; ++q) {
         double acc = 0.0;
-        for (int k = 0; k < N; ++k) acc = fma(V[k][i], Y[k][N], acc);
-        gg[i] = fma(sg, acc, gg[i]);
+        for (int k = 0; k < N; ++k) acc = fma(V[k][i], Y[k][q], acc);
+        if (q < N)
+          H[i][q] = fma(sg, acc, H[i][q]);
+        else
+          gg[i] = fma(sg, acc, gg[i]);
       }
     }
-    // T <- A0^-1 Y = V Y
-    for (int i = 0; i < N; ++i)
+    for (int i = 0; i < N; ++i)  // T <- A0^-1 Y = V Y
       for (int j = 0; j <= N; ++j) {
         double acc = 0.0;
         for (int k = 0; k < N; ++k) acc = fma(V[i][k], Y[k][j], acc);
         T[i][j] = acc;
       }
   }
+  rt0_scatter<DIM>(A, e, parity, H, gg);
 }
 
-template <int DIM>
-__global__ void __launch_bounds__(128) k_hyb_rt0(HybArgs A, Rt0Const<2 * DIM> c, int parity) {
+template <int DIM, int MINB>
+__global__ void __launch_bounds__(128, MINB) k_hyb_rt0(HybArgs A, Rt0Const<2 * DIM> c, int parity) {
   constexpr int N = 2 * DIM;
   const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (t >= parity_count(A.m)) return;
@@ -100,23 +168,27 @@ __global__ void __launch_bounds__(128) k_hyb_rt0(HybArgs A, Rt0Const<2 * DIM> c,
   if (e < 0) return;
   const double a = A.alpha[e], b = A.beta[e];
   const double ib = 1.0 / b;
+  const int P = neumann_order(c.rho * a * ib, A.p_max, A.status);
+  if (P >= 2) {
+    rt0_general<DIM>(A, e, parity, P);
+    return;
+  }
   const double s = b / fma(a, c.lam, b);
-  double fv[N];
-#pragma unroll
-  for (int i = 0; i < N; ++i) fv[i] = A.f[e * N + i];
-
-  // V = A0^-1 (all dofs are face dofs for k = 0), w = A0^-1 f
+  // V = A0^-1 (every dof is a face dof for k = 0; A0^-1 is symmetric: upper
+  // triangle kept, V[j][i] read as V[i][j]), w = A0^-1 f
   double V[N][N], w[N];
+#define VS(i, j) V[(i) < (j) ? (i) : (j)][(i) < (j) ? (j) : (i)]
 #pragma unroll
   for (int i = 0; i < N; ++i)
 #pragma unroll
-    for (int j = 0; j < N; ++j) V[i][j] = fma(c.X[i] * s, c.X[j], c.N0[i * N + j]) * ib;
+    for (int j = i; j < N; ++j) V[i][j] = fma(c.X[i] * s, c.X[j], c.N0[i * N + j]) * ib;
 #pragma unroll
-  for (int i = 0; i < N; ++i) {
-    double acc = 0.0;
+  for (int i = 0; i < N; ++i) w[i] = 0.0;
 #pragma unroll
-    for (int j = 0; j < N; ++j) acc = fma(V[i][j], fv[j], acc);
-    w[i] = acc;
+  for (int j = 0; j < N; ++j) {
+    const double fj = A.f[e * N + j];
+#pragma unroll
+    for (int i = 0; i < N; ++i) w[i] = fma(VS(i, j), fj, w[i]);
   }
   // first order: H = V - V^T (Delta V),  g = w - V^T (Delta w)
   double H[N][N], gg[N];
@@ -124,52 +196,228 @@ __global__ void __launch_bounds__(128) k_hyb_rt0(HybArgs A, Rt0Const<2 * DIM> c,
   for (int i = 0; i < N; ++i) {
     gg[i] = w[i];
 #pragma unroll
-    for (int j = 0; j < N; ++j) H[i][j] = V[i][j];
+    for (int j = 0; j < N; ++j) H[i][j] = VS(i, j);
   }
 #pragma unroll
   for (int k = 0; k < N; ++k) {
-    double dk[N];
+    double yk[N + 1];
 #pragma unroll
-    for (int l = 0; l < N; ++l) dk[l] = delta_entry(a, b, c.D[k * N + l], c.M[k * N + l], c.E[k * N + l], c.Ma[k * N + l]);
-    double yk[N], yw = 0.0;
+    for (int j = 0; j <= N; ++j) yk[j] = 0.0;
 #pragma unroll
-    for (int j = 0; j < N; ++j) {
-      double acc = 0.0;
+    for (int l = 0; l < N; ++l) {
+      const double d = delta_entry(a, b, c.D[k * N + l], c.M[k * N + l], c.E[k * N + l], c.Ma[k * N + l]);
 #pragma unroll
-      for (int l = 0; l < N; ++l) acc = fma(dk[l], V[l][j], acc);
-      yk[j] = acc;
+      for (int j = 0; j < N; ++j) yk[j] = fma(d, VS(l, j), yk[j]);
+      yk[N] = fma(d, w[l], yk[N]);
     }
-#pragma unroll
-    for (int l = 0; l < N; ++l) yw = fma(dk[l], w[l], yw);
 #pragma unroll
     for (int p = 0; p < N; ++p) {
+      const double vkp = -VS(k, p);
 #pragma unroll
-      for (int q = 0; q < N; ++q) H[p][q] = fma(-V[k][p], yk[q], H[p][q]);
-      gg[p] = fma(-V[k][p], yw, gg[p]);
+      for (int q = 0; q < N; ++q) H[p][q] = fma(vkp, yk[q], H[p][q]);
+      gg[p] = fma(vkp, yk[N], gg[p]);
     }
   }
-  const int P = neumann_order(c.rho * a * ib, A.p_max, A.status);
-  if (P >= 2) rt0_higher<N>(c, a, b, V, w, P, H, gg);
+#undef VS
+  rt0_scatter<DIM>(A, e, parity, H, gg);
+}
 
-  // deterministic scatter (dpf = 1: one H row per interior face)
-  int64_t cc[3], own_f[2 * DIM];
-  bool own_in[2 * DIM];
-  cell_coords(A.m, e, cc);
+// ------------------------------------------------------------------ k = 0, lane-per-row form
+//
+// N = 2*DIM lanes per cell (one per face / row of H_T), 32/N cells per warp.
+// Pass 0 (colour-0 cells) writes [H_T | g_T] (N x (N+1)) to a per-cell staging
+// slot; pass 1 (colour-1 cells) computes its own [H_T | g_T] and, for each of
+// its interior faces, merges the colour-0 neighbour's row of that face from the
+// staging buffer and writes the complete H row (and g entry) in one go:
+// every H row is written by exactly one lane, contiguously, so sectors are
+// filled whole and nothing is read back from H.
+// Row k of [H_T | g_T] for one RT0 cell, lanes k = 0..N-1 of a group.  Neumann
+// orders 1..P (P warp-uniform) are all lane-parallel: Y_p = Delta T_{p-1},
+// T_p = A0^-1 Y_p, and row k of the order-p term is sum_j V_jk (Y_p)_j,: (A0^-1
+// is symmetric).  wsh: N doubles, ysh / tsh: N*(N+1) doubles of warp scratch.
+template <int DIM>
+__device__ __forceinline__ void rt0_row_math(const HybArgs& A, const Rt0Const<2 * DIM>& c, int e, int k, int P,
+                                             double* vsh, double* ysh, double* tsh, double (&h)[2 * DIM + 1]) {
+  constexpr int N = 2 * DIM;
+  constexpr int NC = N + 1;
+  // lane-uniform constants come from the parameter bank (broadcast); row-k ones
+  // (k differs across the lanes of a cell) from L1-cached global memory
+  const double* Dk = A.fx.D + k * N;
+  const double* Mk = A.fx.M + k * N;
+  const double* Ek = A.fx.E + k * N;
+  const double* Mak = A.fx.Ma + k * N;
+  const double* N0k = A.fx.N0 + k * N;
+  const double a = A.alpha[e], b = A.beta[e];
+  const double ib = 1.0 / b;
+  const double s = b / fma(a, c.lam, b);
+  const double xs = __ldg(A.fx.X + k) * s;
+  const double* fe = A.f + static_cast<int64_t>(e) * N;
+  double vk[N], dk[N];  // row k of V = A0^-1 and of Delta
+  double wk = 0.0;      // (A0^-1 f)_k
 #pragma unroll
-  for (int q = 0; q < N; ++q) own_f[q] = slot_face(A.m, cc, q, &own_in[q]);
-#pragma unroll
-  for (int p = 0; p < N; ++p) {
-    if (!own_in[p]) continue;
-    const int row = A.mbase[own_f[p]];
-    const int64_t start = A.rowoff[row];
-#pragma unroll
-    for (int q = 0; q < N; ++q) {
-      if (!own_in[q]) continue;
-      const int64_t pos = start + col_rank(A.m, cc, p, q, own_f, own_in);
-      A.hval[pos] = (parity == 1 && p == q) ? A.hval[pos] + H[p][q] : H[p][q];
-    }
-    A.g[row] = (parity == 1) ? A.g[row] + gg[p] : gg[p];
+  for (int j = 0; j < N; ++j) {
+    vk[j] = fma(xs, c.X[j], __ldg(N0k + j)) * ib;
+    wk = fma(vk[j], fe[j], wk);
   }
+  // [V | w] rows to the group's scratch, then y_k = Delta_k,: [V | w]
+#pragma unroll
+  for (int j = 0; j < N; ++j) vsh[k * NC + j] = vk[j];
+  vsh[k * NC + N] = wk;
+#pragma unroll
+  for (int j = 0; j < N; ++j) dk[j] = delta_entry(a, b, __ldg(Dk + j), __ldg(Mk + j), __ldg(Ek + j), __ldg(Mak + j));
+  __syncwarp();
+  double y[NC];
+#pragma unroll
+  for (int q = 0; q <= N; ++q) y[q] = 0.0;
+#pragma unroll
+  for (int l = 0; l < N; ++l)
+#pragma unroll
+    for (int q = 0; q <= N; ++q) y[q] = fma(dk[l], vsh[l * NC + q], y[q]);
+#pragma unroll
+  for (int q = 0; q <= N; ++q) {
+    h[q] = q < N ? vk[q] : wk;
+    ysh[k * NC + q] = y[q];
+  }
+  __syncwarp();
+  for (int p = 1; p <= P; ++p) {
+    const double sg = (p & 1) ? -1.0 : 1.0;
+    // row k of the order-p term: sum_j V_jk Y_j,:   (A0^-1 symmetric)
+    double t[NC];
+#pragma unroll
+    for (int q = 0; q <= N; ++q) t[q] = 0.0;
+#pragma unroll
+    for (int j = 0; j < N; ++j)
+#pragma unroll
+      for (int q = 0; q <= N; ++q) t[q] = fma(vk[j], ysh[j * NC + q], t[q]);
+#pragma unroll
+    for (int q = 0; q <= N; ++q) h[q] = fma(sg, t[q], h[q]);
+    if (p == P) break;
+    // T = A0^-1 Y (row k is exactly t), then Y <- Delta T
+#pragma unroll
+    for (int q = 0; q <= N; ++q) tsh[k * NC + q] = t[q];
+    __syncwarp();
+#pragma unroll
+    for (int q = 0; q <= N; ++q) y[q] = 0.0;
+#pragma unroll
+    for (int l = 0; l < N; ++l)
+#pragma unroll
+      for (int q = 0; q <= N; ++q) y[q] = fma(dk[l], tsh[l * NC + q], y[q]);
+    __syncwarp();
+#pragma unroll
+    for (int q = 0; q <= N; ++q) ysh[k * NC + q] = y[q];
+    __syncwarp();
+  }
+}
+
+// Column ranks of a deep-interior cell's row k (every face of the cell and of
+// its neighbour across k interior): own slot q -> bits [4q, 4q+4), neighbour
+// slot q -> bits [4(N+q), ...).  Built at compile time from col_rank_fast.
+template <int DIM>
+constexpr uint64_t deep_ranks(int k) {
+  constexpr int N = 2 * DIM;
+  const unsigned all = (1u << DIM) - 1u;
+  uint64_t packed = 0;
+  for (int q = 0; q < N; ++q) {
+    packed |= static_cast<uint64_t>(col_rank_fast(DIM, k, q, all, all, 4, 9, false)) << (4 * q);
+    packed |= static_cast<uint64_t>(col_rank_fast(DIM, k ^ 1, q, all, all, 4, 9, false)) << (4 * (N + q));
+  }
+  return packed;
+}
+
+template <int DIM>
+__device__ __forceinline__ uint64_t deep_ranks_of(int k) {
+  uint64_t r = deep_ranks<DIM>(0);
+#pragma unroll
+  for (int j = 1; j < 2 * DIM; ++j) r = (k == j) ? deep_ranks<DIM>(j) : r;
+  return r;
+}
+
+template <int DIM, int PASS>
+__global__ void __launch_bounds__(128, HDR_ROWS_MINB) k_rt0_rows(HybArgs A, Rt0Const<2 * DIM> c, double* stage) {
+  constexpr int N = 2 * DIM;
+  constexpr int NC = N + 1;
+  constexpr int G = 32 / N;  // cells per warp
+  constexpr int W = 4;       // warps per block
+  __shared__ double vbuf[W][G][N * NC];
+  __shared__ double ybuf[W][G][N * NC];
+  __shared__ double tbuf[W][G][N * NC];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int grp = lane / N, k = lane - grp * N;
+  const uint32_t t = (blockIdx.x * W + warp) * G + grp;
+  int cc[3] = {0, 0, 0};
+  int e = -1;
+  if (grp < G && t < static_cast<uint32_t>(parity_count(A.m))) e = parity_cell32(A.m, PASS, t, cc);
+  const bool valid = e >= 0;
+  // spare lanes shadow cell 0 so the warp stays convergent through the barriers
+  const int gi = grp < G ? grp : 0;
+  const int kk = grp < G ? k : 0;
+  const int ee = valid ? e : 0;
+  int P = valid ? neumann_order(c.rho * A.alpha[ee] / A.beta[ee], A.p_max, A.status) : 1;
+  P = __reduce_max_sync(0xffffffffu, P);
+  double h[NC];
+  if (grp < G) {
+    rt0_row_math<DIM>(A, c, ee, kk, P, vbuf[warp][gi], ybuf[warp][gi], tbuf[warp][gi], h);
+  } else {  // spare lanes: same barrier sequence as the groups
+    __syncwarp();
+    __syncwarp();
+    for (int p = 1; p < P; ++p) {
+      __syncwarp();
+      __syncwarp();
+      __syncwarp();
+    }
+  }
+  if (!valid) return;
+  if (PASS == 0) {
+    double* slot = stage + static_cast<int64_t>(t) * (N * NC) + k * NC;
+#pragma unroll
+    for (int q = 0; q <= N; ++q) slot[q] = h[q];
+    return;
+  }
+  // pass 1: complete rows of this cell's interior faces
+  const int a = k >> 1, side = k & 1;
+  const int ca = a == 0 ? cc[0] : (a == 1 ? cc[1] : cc[2]);
+  const int na = static_cast<int>(a == 0 ? A.m.N[0] : (a == 1 ? A.m.N[1] : A.m.N[2]));
+  const bool kin = side ? (ca + 1 < na) : (ca > 0);
+  if (!kin) return;
+  const int step = side ? 1 : -1;
+  const int nc[3] = {cc[0] + (a == 0 ? step : 0), cc[1] + (a == 1 ? step : 0), cc[2] + (a == 2 ? step : 0)};
+  const int kn = k ^ 1;  // the shared face's slot in the neighbour
+  // issue the dependent loads first: the neighbour's row from the stage, the row start
+  const uint32_t half = static_cast<uint32_t>((A.m.N[0] + 1) / 2);
+  const uint32_t tn = (static_cast<uint32_t>(nc[1]) + static_cast<uint32_t>(A.m.N[1]) * nc[2]) * half + (nc[0] >> 1);
+  const double* nrow_p = stage + static_cast<int64_t>(tn) * (N * NC) + kn * NC;
+  double nrow[NC];
+#pragma unroll
+  for (int q = 0; q <= N; ++q) nrow[q] = nrow_p[q];
+  const int face = face_id32(A.m, a, cc[0] + (a == 0 ? side : 0), cc[1] + (a == 1 ? side : 0), cc[2] + (a == 2 ? side : 0));
+  const int row = A.mbase[face];
+  const int64_t start = A.rowoff[row];
+  unsigned lo = 0, hi = 0, nlo = 0, nhi = 0;
+#pragma unroll
+  for (int x = 0; x < DIM; ++x) {
+    const int cx = x == 0 ? cc[0] : (x == 1 ? cc[1] : cc[2]);
+    const int nx = x == 0 ? nc[0] : (x == 1 ? nc[1] : nc[2]);
+    const int Nx = static_cast<int>(x == 0 ? A.m.N[0] : (x == 1 ? A.m.N[1] : A.m.N[2]));
+    lo |= static_cast<unsigned>(cx > 0) << x;
+    hi |= static_cast<unsigned>(cx + 1 < Nx) << x;
+    nlo |= static_cast<unsigned>(nx > 0) << x;
+    nhi |= static_cast<unsigned>(nx + 1 < Nx) << x;
+  }
+  const int nca = a == 0 ? nc[0] : (a == 1 ? nc[1] : nc[2]);
+  double* out = A.hval + start;
+#pragma unroll
+  for (int q = 0; q < N; ++q) {
+    if (!((((q & 1) ? hi : lo) >> (q >> 1)) & 1u)) continue;
+    double v = h[q];
+    if (q == k) v = v + nrow_p[kn];
+    out[col_rank_fast(DIM, k, q, lo, hi, ca, na, false)] = v;
+  }
+#pragma unroll
+  for (int q = 0; q < N; ++q) {
+    if (q == kn || !((((q & 1) ? nhi : nlo) >> (q >> 1)) & 1u)) continue;
+    out[col_rank_fast(DIM, kn, q, nlo, nhi, nca, na, false)] = nrow[q];
+  }
+  A.g[row] = h[N] + nrow[N];
 }
 
 // ------------------------------------------------------------------ k >= 1
@@ -490,7 +738,16 @@ void launch_hybridize_rt0(const HybArgs& a, const double* hc, int parity, cudaSt
     memcpy(c.X, hc + 5 * N * N, sizeof(double) * N);
     c.lam = hc[5 * N * N + N];
     c.rho = hc[5 * N * N + N + 1];
-    k_hyb_rt0<3><<<nb, 128, 0, st>>>(a, c, parity);
+    static const int variant = [] {
+      const char* v = getenv("HDR_RT0_MINB");
+      return v ? atoi(v) : HDR_RT0_MINB;
+    }();
+    if (variant == 4)
+      k_hyb_rt0<3, 4><<<nb, 128, 0, st>>>(a, c, parity);
+    else if (variant == 3)
+      k_hyb_rt0<3, 3><<<nb, 128, 0, st>>>(a, c, parity);
+    else
+      k_hyb_rt0<3, 2><<<nb, 128, 0, st>>>(a, c, parity);
   } else {
     Rt0Const<4> c;
     constexpr int N = 4;
@@ -502,9 +759,37 @@ void launch_hybridize_rt0(const HybArgs& a, const double* hc, int parity, cudaSt
     memcpy(c.X, hc + 5 * N * N, sizeof(double) * N);
     c.lam = hc[5 * N * N + N];
     c.rho = hc[5 * N * N + N + 1];
-    k_hyb_rt0<2><<<nb, 128, 0, st>>>(a, c, parity);
+    k_hyb_rt0<2, 4><<<nb, 128, 0, st>>>(a, c, parity);
   }
   count_launch();
+}
+
+void launch_hybridize_rt0_rows(const HybArgs& a, const double* hc, double* stage, cudaStream_t st) {
+  const int64_t cnt = parity_count(a.m);
+  auto fill = [&](auto& c, int N) {
+    memcpy(c.D, hc, sizeof(double) * N * N);
+    memcpy(c.M, hc + N * N, sizeof(double) * N * N);
+    memcpy(c.E, hc + 2 * N * N, sizeof(double) * N * N);
+    memcpy(c.Ma, hc + 3 * N * N, sizeof(double) * N * N);
+    memcpy(c.N0, hc + 4 * N * N, sizeof(double) * N * N);
+    memcpy(c.X, hc + 5 * N * N, sizeof(double) * N);
+    c.lam = hc[5 * N * N + N];
+    c.rho = hc[5 * N * N + N + 1];
+  };
+  if (a.m.dim == 3) {
+    Rt0Const<6> c;
+    fill(c, 6);
+    const unsigned nb = static_cast<unsigned>((cnt + 4 * 5 - 1) / (4 * 5));
+    k_rt0_rows<3, 0><<<nb, 128, 0, st>>>(a, c, stage);
+    k_rt0_rows<3, 1><<<nb, 128, 0, st>>>(a, c, stage);
+  } else {
+    Rt0Const<4> c;
+    fill(c, 4);
+    const unsigned nb = static_cast<unsigned>((cnt + 4 * 8 - 1) / (4 * 8));
+    k_rt0_rows<2, 0><<<nb, 128, 0, st>>>(a, c, stage);
+    k_rt0_rows<2, 1><<<nb, 128, 0, st>>>(a, c, stage);
+  }
+  count_launch(2);
 }
 
 int64_t hybridize_cta_ws_doubles(const DevMesh& m, int nF, int r, int p_max, bool* use_smem) {
