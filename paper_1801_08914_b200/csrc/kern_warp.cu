@@ -38,109 +38,168 @@ struct Shape {
 constexpr int kWarps = 4;  // cells per CTA
 
 template <int DIM, int K>
+struct Tiles;  // register tiles (TM x TN per lane) of the three warp GEMMs
+template <> struct Tiles<3, 1> { static constexpr int V_M = 6, V_N = 5, Y_M = 6, Y_N = 5, C_M = 4, C_N = 5; };
+template <> struct Tiles<2, 1> { static constexpr int V_M = 3, V_N = 3, Y_M = 3, Y_N = 3, C_M = 2, C_N = 3; };
+template <> struct Tiles<2, 2> { static constexpr int V_M = 4, V_N = 4, Y_M = 4, Y_N = 4, C_M = 3, C_N = 4; };
+template <> struct Tiles<2, 3> { static constexpr int V_M = 5, V_N = 6, Y_M = 5, Y_N = 6, C_M = 4, C_N = 5; };
+
+template <int DIM, int K>
 struct WarpSmem {
   using S = Shape<DIM, K>;
   static constexpr int NCP = (S::NC + 3) & ~3;  // padded row length of [V | w] and Y
   float d32t[S::N * S::N];     // Delta32 transposed: d32t[l * N + i] = Delta_il
-  float v32[S::N * NCP];       // [V | w] row-major
-  float y32[S::N * NCP];       // Y = Delta V, later reused for the correction C (NF x NCP)
+  float v32[S::N * NCP];       // [V | w] row-major (fp32 operand)
+  float y32[S::N * NCP];       // Y = Delta V
+  float corr[S::NF * NCP];     // C = V_F^T Y (+ higher orders)
+  double vf[S::NF * S::NC];    // fp64 face rows of [V | w]: H0 and g0
   double z[S::R * S::NC];      // z[j][c] = s_j X_F_c,j (c < NF), s_j (X^T f)_j (c = NF)
-  double zh[S::R * S::NC];     // copy of the first z (higher orders overwrite z)
-  __device__ double z0(int j, int c) const { return zh[j * S::NC + c]; }
+  double f[S::N];              // f_T
   double nf[S::N];             // N0 f
   double s[S::R];
+  long long rstart[2 * DIM];  // H row offset of the first row of each interior face slot (-1: boundary)
+  int rlen[2 * DIM];          // H row length of that face's rows
+  int grow[2 * DIM];          // multiplier index of the face's first row
+  int rank[4 * DIM * DIM];    // column-block rank of own slot t in the rows of slot s (-1: boundary)
+};
+
+template <int DIM, int K>
+struct CtaShared {  // fixed per space, staged once per CTA
+  using S = Shape<DIM, K>;
+  double xt[S::R * S::N];  // X^T
+  double n0[S::N * S::N];  // N0
 };
 
 // C[M x NN] = A[M x KK] * B[KK x NN] on one warp, operands in shared memory:
 // A given transposed (at[k * lda + m]), B row-major (b[k * ldb + n]).  Each
 // lane owns a TM x TN register tile; tiles beyond 32 lanes loop.
-template <int M, int NN, int KK, int TM, int TN>
-__device__ __forceinline__ void warp_gemm(const float* at, int lda, const float* bm, int ldb, float* cm, int ldc,
-                                          int lane, float scale_in = 0.f, bool accumulate = false) {
+template <int M, int NN, int KK, int TM, int TN, class T = float>
+__device__ __forceinline__ void warp_gemm(const T* at, int lda, const T* bm, int ldb, T* cm, int ldc, int lane,
+                                          T scale_in = T(0), bool accumulate = false) {
   constexpr int TMS = (M + TM - 1) / TM, TNS = (NN + TN - 1) / TN;
   for (int tile = lane; tile < TMS * TNS; tile += 32) {
     const int m0 = (tile / TNS) * TM, n0 = (tile % TNS) * TN;
-    float acc[TM][TN];
+    T acc[TM][TN];
 #pragma unroll
     for (int i = 0; i < TM; ++i)
 #pragma unroll
-      for (int j = 0; j < TN; ++j) acc[i][j] = 0.f;
+      for (int j = 0; j < TN; ++j) acc[i][j] = T(0);
 #pragma unroll 4
     for (int k = 0; k < KK; ++k) {
-      float av[TM], bv[TN];
+      T av[TM], bv[TN];
 #pragma unroll
-      for (int i = 0; i < TM; ++i) av[i] = (m0 + i < M) ? at[k * lda + m0 + i] : 0.f;
+      for (int i = 0; i < TM; ++i) av[i] = (m0 + i < M) ? at[k * lda + m0 + i] : T(0);
 #pragma unroll
-      for (int j = 0; j < TN; ++j) bv[j] = (n0 + j < NN) ? bm[k * ldb + n0 + j] : 0.f;
+      for (int j = 0; j < TN; ++j) bv[j] = (n0 + j < NN) ? bm[k * ldb + n0 + j] : T(0);
 #pragma unroll
       for (int i = 0; i < TM; ++i)
 #pragma unroll
-        for (int j = 0; j < TN; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+        for (int j = 0; j < TN; ++j) acc[i][j] = fma(av[i], bv[j], acc[i][j]);
     }
 #pragma unroll
     for (int i = 0; i < TM; ++i)
 #pragma unroll
       for (int j = 0; j < TN; ++j)
         if (m0 + i < M && n0 + j < NN) {
-          float* dst = cm + (m0 + i) * ldc + n0 + j;
-          *dst = accumulate ? fmaf(scale_in, acc[i][j], *dst) : acc[i][j];
+          T* dst = cm + (m0 + i) * ldc + n0 + j;
+          *dst = accumulate ? fma(scale_in, acc[i][j], *dst) : acc[i][j];
         }
   }
 }
 
+// per-warp global scratch: the higher-order buffer T (N x NCP fp32), rarely used
+template <int DIM, int K>
+constexpr int64_t scratch_doubles_per_warp() {
+  using S = Shape<DIM, K>;
+  constexpr int NCP = WarpSmem<DIM, K>::NCP;
+  return (S::N * NCP + 1) / 2 + 8;
+}
+
 template <int DIM, int K>
 __device__ __forceinline__ void warp_cell(const HybArgs& A, int e, int parity, int lane, WarpSmem<DIM, K>& sm,
-                                          float* gscratch) {
+                                          const CtaShared<DIM, K>& cs, double* scratch) {
   using S = Shape<DIM, K>;
   using SM = WarpSmem<DIM, K>;
+  using TL = Tiles<DIM, K>;
   constexpr int N = S::N, NF = S::NF, NC = S::NC, R = S::R, NINT = S::NINT, DPF = S::DPF, NCP = SM::NCP;
-  constexpr int TM1 = 4, TN1 = (NCP + 7) / 8;  // GEMM tiles sized so ~32 lanes cover the outputs
   const Fixed& fx = A.fx;
+  float* tbuf = reinterpret_cast<float*>(scratch);  // N x NCP
   const double a = A.alpha[e], b = A.beta[e];
   const double ib = 1.0 / b;
   const double* fe = A.f + static_cast<int64_t>(e) * N;
-  // s, N0 f
+  for (int i = lane; i < N; i += 32) sm.f[i] = fe[i];
   for (int j = lane; j < R; j += 32) sm.s[j] = b / fma(a, __ldg(fx.lam + j), b);
+  __syncwarp();
   for (int i = lane; i < N; i += 32) {
     double acc = 0.0;
-    for (int l = 0; l < N; ++l) acc = fma(__ldg(fx.N0 + i * N + l), fe[l], acc);
+#pragma unroll 6
+    for (int l = 0; l < N; ++l) acc = fma(cs.n0[i * N + l], sm.f[l], acc);
     sm.nf[i] = acc;
   }
+  // z = [s X_F^T | s X^T f]; the X^T f dots are split over 4 lanes each
+  for (int idx = lane; idx < R * NF; idx += 32) {
+    const int j = idx / NF, c = idx - j * NF;
+    sm.z[j * NC + c] = sm.s[j] * cs.xt[j * N + NINT + c];
+  }
+  for (int j0 = 0; j0 < R; j0 += 8) {
+    const int j = j0 + (lane >> 2), part = lane & 3;
+    double acc = 0.0;
+    if (j < R)
+      for (int l = part; l < N; l += 4) acc = fma(cs.xt[j * N + l], sm.f[l], acc);
+    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+    acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+    if (j < R && part == 0) sm.z[j * NC + NF] = sm.s[j] * acc;
+  }
   __syncwarp();
-  // z = [s X_F^T | s X^T f]
-  for (int idx = lane; idx < R * NC; idx += 32) {
-    const int j = idx / NC, c = idx - j * NC;
-    double v;
-    if (c < NF) {
-      v = sm.s[j] * __ldg(fx.X + (NINT + c) * R + j);
-    } else {
-      double acc = 0.0;
-      for (int l = 0; l < N; ++l) acc = fma(__ldg(fx.X + l * R + j), fe[l], acc);
-      v = sm.s[j] * acc;
+  // [V | w] = (base + X z) / beta, base = N0_:,F | N0 f: register tiles over (rows, cols),
+  // fp32 copy for the correction GEMMs, fp64 face rows kept for H0 / g0
+  {
+    constexpr int TM = TL::V_M, TN = TL::V_N;
+    constexpr int TMS = (N + TM - 1) / TM, TNS = (NC + TN - 1) / TN;
+    for (int tile = lane; tile < TMS * TNS; tile += 32) {
+      const int m0 = (tile / TNS) * TM, n0 = (tile % TNS) * TN;
+      double acc[TM][TN];
+#pragma unroll
+      for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int jj = 0; jj < TN; ++jj) acc[i][jj] = 0.0;
+#pragma unroll 4
+      for (int j = 0; j < R; ++j) {
+        double xv[TM], zv[TN];
+#pragma unroll
+        for (int i = 0; i < TM; ++i) xv[i] = (m0 + i < N) ? cs.xt[j * N + m0 + i] : 0.0;
+#pragma unroll
+        for (int jj = 0; jj < TN; ++jj) zv[jj] = (n0 + jj < NC) ? sm.z[j * NC + n0 + jj] : 0.0;
+#pragma unroll
+        for (int i = 0; i < TM; ++i)
+#pragma unroll
+          for (int jj = 0; jj < TN; ++jj) acc[i][jj] = fma(xv[i], zv[jj], acc[i][jj]);
+      }
+#pragma unroll
+      for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int jj = 0; jj < TN; ++jj) {
+          const int row = m0 + i, col = n0 + jj;
+          if (row >= N || col >= NC) continue;
+          const double base = (col < NF) ? cs.n0[row * N + NINT + col] : sm.nf[row];
+          const double v = (base + acc[i][jj]) * ib;
+          sm.v32[row * NCP + col] = static_cast<float>(v);
+          if (row >= NINT) sm.vf[(row - NINT) * NC + col] = v;
+        }
     }
-    sm.z[idx] = v;
-    sm.zh[idx] = v;
   }
-  __syncwarp();
-  // [V | w] (fp64 -> fp32 operand) and Delta32^T (fp64 rounding errors -> fp32)
-  for (int idx = lane; idx < N * NC; idx += 32) {
-    const int i = idx / NC, c = idx - i * NC;
-    double acc = (c < NF) ? __ldg(fx.N0 + i * N + NINT + c) : sm.nf[i];
-#pragma unroll 8
-    for (int j = 0; j < R; ++j) acc = fma(__ldg(fx.X + i * R + j), sm.z[j * NC + c], acc);
-    sm.v32[i * NCP + c] = static_cast<float>(acc * ib);
-  }
+  // Delta32^T (fp64 exact rounding errors -> fp32)
   for (int idx = lane; idx < N * N; idx += 32) {
     const int i = idx / N, l = idx - i * N;
     sm.d32t[l * N + i] = static_cast<float>(
         delta_entry(a, b, __ldg(fx.D + idx), __ldg(fx.M + idx), __ldg(fx.E + idx), __ldg(fx.Ma + idx)));
   }
   __syncwarp();
-  // first order: Y = Delta32 [V | w];  C = V_F^T Y  (stored over Y once consumed)
-  warp_gemm<N, NC, N, TM1, TN1>(sm.d32t, N, sm.v32, NCP, sm.y32, NCP, lane);
+  // first order: Y = Delta32 [V | w];  C = V_F^T Y
+  warp_gemm<N, NC, N, TL::Y_M, TL::Y_N>(sm.d32t, N, sm.v32, NCP, sm.y32, NCP, lane);
   __syncwarp();
-  float* corr = gscratch;  // NF x NCP in global scratch (L1/L2 resident)
-  warp_gemm<NF, NC, N, 4, TN1>(sm.v32, NCP, sm.y32, NCP, corr, NCP, lane);
+  float* corr = sm.corr;
+  warp_gemm<NF, NC, N, TL::C_M, TL::C_N>(sm.v32, NCP, sm.y32, NCP, corr, NCP, lane);
   __syncwarp();
   // a-posteriori size of the first-order term: 10 (|C|/|H0|)^2 <= 1e-12 -> order 1 suffices
   float cmax = 0.f, hmax = 0.f;
@@ -163,100 +222,129 @@ __device__ __forceinline__ void warp_cell(const HybArgs& A, int e, int parity, i
     }
     if (!(ratio < 0.25) && lane == 0) atomicOr(A.status, 1);
   }
-  // higher orders (rare): T = A0^-1 Y (fp64 accumulation, fp32 storage), Y <- Delta32 T,
-  // C += (-1)^(p+1) V_F^T Y   (C is subtracted from H0)
-  float* tbuf = gscratch + NF * NCP;
+  // higher orders (rare): T = A0^-1 Y, Y <- Delta32 T, C += (-1)^(p+1) V_F^T Y (C is subtracted)
   for (int p = 2; p <= P; ++p) {
-    for (int idx = lane; idx < R * NC; idx += 32) {  // z <- s (X^T Y) (reuse z)
+    for (int idx = lane; idx < R * NC; idx += 32) {
       const int j = idx / NC, c = idx - j * NC;
       double acc = 0.0;
-      for (int l = 0; l < N; ++l) acc = fma(__ldg(fx.X + l * R + j), static_cast<double>(sm.y32[l * NCP + c]), acc);
+      for (int l = 0; l < N; ++l) acc = fma(cs.xt[j * N + l], static_cast<double>(sm.y32[l * NCP + c]), acc);
       sm.z[idx] = sm.s[j] * acc;
     }
     __syncwarp();
     for (int idx = lane; idx < N * NC; idx += 32) {
       const int i = idx / NC, c = idx - i * NC;
       double acc = 0.0;
-      for (int l = 0; l < N; ++l) acc = fma(__ldg(fx.N0 + i * N + l), static_cast<double>(sm.y32[l * NCP + c]), acc);
-      for (int j = 0; j < R; ++j) acc = fma(__ldg(fx.X + i * R + j), sm.z[j * NC + c], acc);
+      for (int l = 0; l < N; ++l) acc = fma(cs.n0[i * N + l], static_cast<double>(sm.y32[l * NCP + c]), acc);
+      for (int j = 0; j < R; ++j) acc = fma(cs.xt[j * N + i], sm.z[j * NC + c], acc);
       tbuf[i * NCP + c] = static_cast<float>(acc * ib);
     }
     __syncwarp();
-    warp_gemm<N, NC, N, TM1, TN1>(sm.d32t, N, tbuf, NCP, sm.y32, NCP, lane);
+    warp_gemm<N, NC, N, TL::Y_M, TL::Y_N>(sm.d32t, N, tbuf, NCP, sm.y32, NCP, lane);
     __syncwarp();
-    warp_gemm<NF, NC, N, 4, TN1>(sm.v32, NCP, sm.y32, NCP, corr, NCP, lane, (p & 1) ? 1.f : -1.f, true);
+    warp_gemm<NF, NC, N, TL::C_M, TL::C_N>(sm.v32, NCP, sm.y32, NCP, corr, NCP, lane, (p & 1) ? 1.f : -1.f, true);
     __syncwarp();
   }
-  // scatter: H_pc = V_F(p, c) (fp64) - C_pc ; g_p = w_F(p) - C_p,NF
-  int cc[3];
+  // scatter: H_pc = V_F(p, c) (fp64) - C_pc ; g_p = w_F(p) - C_p,NF.  Per-cell tables
+  // (row starts / lengths of each face slot, column-block ranks) first, then one
+  // cheap position per entry; consecutive lanes write consecutive columns.
+  constexpr int NS = 2 * DIM;
   {
+    int cc[3];
     const uint32_t r0 = A.m.div_n0.div(static_cast<uint32_t>(e));
     cc[0] = static_cast<int>(static_cast<uint32_t>(e) - r0 * static_cast<uint32_t>(A.m.N[0]));
     const uint32_t z2 = A.m.div_n1.div(r0);
     cc[1] = static_cast<int>(r0 - z2 * static_cast<uint32_t>(A.m.N[1]));
     cc[2] = static_cast<int>(z2);
-  }
-  unsigned lo = 0, hi = 0;
+    unsigned lo = 0, hi = 0;
 #pragma unroll
-  for (int x = 0; x < DIM; ++x) {
-    const int cx = x == 0 ? cc[0] : (x == 1 ? cc[1] : cc[2]);
-    const int Nx = static_cast<int>(x == 0 ? A.m.N[0] : (x == 1 ? A.m.N[1] : A.m.N[2]));
-    lo |= static_cast<unsigned>(cx > 0) << x;
-    hi |= static_cast<unsigned>(cx + 1 < Nx) << x;
+    for (int x = 0; x < DIM; ++x) {
+      const int cx = x == 0 ? cc[0] : (x == 1 ? cc[1] : cc[2]);
+      const int Nx = static_cast<int>(x == 0 ? A.m.N[0] : (x == 1 ? A.m.N[1] : A.m.N[2]));
+      lo |= static_cast<unsigned>(cx > 0) << x;
+      hi |= static_cast<unsigned>(cx + 1 < Nx) << x;
+    }
+    for (int idx = lane; idx < NS * NS; idx += 32) {
+      const int ps = idx / NS, qs = idx - ps * NS;
+      const int a_ = ps >> 1;
+      const bool pin = (((ps & 1) ? hi : lo) >> a_) & 1u;
+      const bool qin = (((qs & 1) ? hi : lo) >> (qs >> 1)) & 1u;
+      const int ca = a_ == 0 ? cc[0] : (a_ == 1 ? cc[1] : cc[2]);
+      const int na = static_cast<int>(a_ == 0 ? A.m.N[0] : (a_ == 1 ? A.m.N[1] : A.m.N[2]));
+      sm.rank[idx] = (pin && qin) ? col_rank_fast(DIM, ps, qs, lo, hi, ca, na, false) : -1;
+      if (qs == 0) {
+        const int side = ps & 1;
+        if (pin) {
+          const int face = face_id32(A.m, a_, cc[0] + (a_ == 0 ? side : 0), cc[1] + (a_ == 1 ? side : 0),
+                                     cc[2] + (a_ == 2 ? side : 0));
+          const int row = A.mbase[face];
+          const int64_t r0s = A.rowoff[row];
+          sm.rstart[ps] = r0s;
+          sm.rlen[ps] = static_cast<int>(A.rowoff[row + 1] - r0s);
+          sm.grow[ps] = row;
+        } else {
+          sm.rstart[ps] = -1;
+        }
+      }
+    }
   }
+  __syncwarp();
   for (int idx = lane; idx < NF * NC; idx += 32) {
     const int p = idx / NC, c = idx - p * NC;
     const int ps = p / DPF, sub = p - ps * DPF;
-    const int a_ = ps >> 1, side = ps & 1;
-    if (!((((side) ? hi : lo) >> a_) & 1u)) continue;
-    const int qs = c / DPF, sj = c - qs * DPF;
-    if (c < NF && !((((qs & 1) ? hi : lo) >> (qs >> 1)) & 1u)) continue;
-    // H0 entry in fp64: row NINT+p of [V | w]
-    double h0 = (c < NF) ? __ldg(fx.N0 + (NINT + p) * N + NINT + c) : sm.nf[NINT + p];
-#pragma unroll 8
-    for (int j = 0; j < R; ++j) h0 = fma(__ldg(fx.X + (NINT + p) * R + j), sm.z0(j, c), h0);
-    const double v = h0 * ib - static_cast<double>(corr[p * NCP + c]);
-    const int face = face_id32(A.m, a_, cc[0] + (a_ == 0 ? side : 0), cc[1] + (a_ == 1 ? side : 0),
-                               cc[2] + (a_ == 2 ? side : 0));
-    const int row = A.mbase[face] + sub;
+    const int64_t rs = sm.rstart[ps];
+    if (rs < 0) continue;
+    const double v = sm.vf[p * NC + c] - static_cast<double>(corr[p * NCP + c]);
     if (c == NF) {
-      A.g[row] = parity ? A.g[row] + v : v;
+      double* gp = A.g + sm.grow[ps] + sub;
+      *gp = parity ? *gp + v : v;
       continue;
     }
-    const int ca = a_ == 0 ? cc[0] : (a_ == 1 ? cc[1] : cc[2]);
-    const int na = static_cast<int>(a_ == 0 ? A.m.N[0] : (a_ == 1 ? A.m.N[1] : A.m.N[2]));
-    const int64_t pos =
-        A.rowoff[row] + static_cast<int64_t>(col_rank_fast(DIM, ps, qs, lo, hi, ca, na, false)) * DPF + sj;
-    A.hval[pos] = (parity == 1 && ps == qs) ? A.hval[pos] + v : v;
+    const int qs = c / DPF, sj = c - qs * DPF;
+    const int rk = sm.rank[ps * NS + qs];
+    if (rk < 0) continue;
+    double* hp = A.hval + rs + static_cast<int64_t>(sub) * sm.rlen[ps] + rk * DPF + sj;
+    *hp = (parity == 1 && ps == qs) ? *hp + v : v;
   }
   __syncwarp();
 }
 
 template <int DIM, int K>
-__global__ void __launch_bounds__(32 * kWarps) k_hyb_warp(HybArgs A, int parity, float* gws) {
+__global__ void __launch_bounds__(32 * kWarps) k_hyb_warp(HybArgs A, int parity, double* gws) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  auto* sm = reinterpret_cast<WarpSmem<DIM, K>*>(smem_raw) + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
+  auto* cs = reinterpret_cast<CtaShared<DIM, K>*>(smem_raw);
+  auto* sm = reinterpret_cast<WarpSmem<DIM, K>*>(smem_raw + ((sizeof(CtaShared<DIM, K>) + 15) & ~size_t(15))) +
+             (threadIdx.x >> 5);
   using S = Shape<DIM, K>;
-  float* scratch = gws + (static_cast<int64_t>(blockIdx.x) * kWarps + (threadIdx.x >> 5)) *
-                             (2 * S::N * WarpSmem<DIM, K>::NCP);
+  for (int idx = threadIdx.x; idx < S::R * S::N; idx += blockDim.x) {
+    const int j = idx / S::N, i = idx - j * S::N;
+    cs->xt[idx] = __ldg(A.fx.X + i * S::R + j);
+  }
+  for (int idx = threadIdx.x; idx < S::N * S::N; idx += blockDim.x) cs->n0[idx] = __ldg(A.fx.N0 + idx);
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  double* scratch = gws + (static_cast<int64_t>(blockIdx.x) * kWarps + (threadIdx.x >> 5)) * scratch_doubles_per_warp<DIM, K>();
   const uint32_t cnt = static_cast<uint32_t>(parity_count(A.m));
   for (uint32_t t = blockIdx.x * kWarps + (threadIdx.x >> 5); t < cnt; t += gridDim.x * kWarps) {
     int cc[3];
     const int e = parity_cell32(A.m, parity, t, cc);
     if (e < 0) continue;
-    warp_cell<DIM, K>(A, e, parity, lane, *sm, scratch);
+    warp_cell<DIM, K>(A, e, parity, lane, *sm, *cs, scratch);
   }
 }
 
 template <int DIM, int K>
-int64_t scratch_floats_t(int64_t grid) {
-  return grid * kWarps * 2 * Shape<DIM, K>::N * WarpSmem<DIM, K>::NCP;
+size_t smem_t() {
+  return ((sizeof(CtaShared<DIM, K>) + 15) & ~size_t(15)) + sizeof(WarpSmem<DIM, K>) * kWarps;
+}
+
+template <int DIM, int K>
+int64_t scratch_doubles_t(int64_t grid) {
+  return grid * kWarps * scratch_doubles_per_warp<DIM, K>();
 }
 
 template <int DIM, int K>
 int64_t grid_t(const HybArgs& a) {
-  const size_t smem = sizeof(WarpSmem<DIM, K>) * kWarps;
+  const size_t smem = smem_t<DIM, K>();
   cudaFuncSetAttribute(k_hyb_warp<DIM, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   const int64_t cnt = parity_count(a.m);
   int dev = 0, sms = 148, per_sm = 1;
@@ -268,8 +356,8 @@ int64_t grid_t(const HybArgs& a) {
 }
 
 template <int DIM, int K>
-void launch_t(const HybArgs& a, int parity, float* gws, cudaStream_t st) {
-  const size_t smem = sizeof(WarpSmem<DIM, K>) * kWarps;
+void launch_t(const HybArgs& a, int parity, double* gws, cudaStream_t st) {
+  const size_t smem = smem_t<DIM, K>();
   const int64_t grid = grid_t<DIM, K>(a);
   k_hyb_warp<DIM, K><<<static_cast<unsigned>(grid), 32 * kWarps, smem, st>>>(a, parity, gws);
 }
@@ -284,15 +372,15 @@ static int order_of(const DevMesh& m) {
   return (m.dpf == 1) ? 0 : (m.dim == 3 ? static_cast<int>(lround(sqrt(static_cast<double>(m.dpf)))) - 1 : m.dpf - 1);
 }
 
-int64_t hybridize_warp_scratch_floats(const HybArgs& a) {
+int64_t hybridize_warp_scratch_doubles(const HybArgs& a) {
   const int dim = a.m.dim, k = order_of(a.m);
-  if (dim == 3 && k == 1) return scratch_floats_t<3, 1>(grid_t<3, 1>(a));
-  if (dim == 2 && k == 1) return scratch_floats_t<2, 1>(grid_t<2, 1>(a));
-  if (dim == 2 && k == 2) return scratch_floats_t<2, 2>(grid_t<2, 2>(a));
-  return scratch_floats_t<2, 3>(grid_t<2, 3>(a));
+  if (dim == 3 && k == 1) return scratch_doubles_t<3, 1>(grid_t<3, 1>(a));
+  if (dim == 2 && k == 1) return scratch_doubles_t<2, 1>(grid_t<2, 1>(a));
+  if (dim == 2 && k == 2) return scratch_doubles_t<2, 2>(grid_t<2, 2>(a));
+  return scratch_doubles_t<2, 3>(grid_t<2, 3>(a));
 }
 
-void launch_hybridize_warp(const HybArgs& a, int parity, float* gws, cudaStream_t st) {
+void launch_hybridize_warp(const HybArgs& a, int parity, double* gws, cudaStream_t st) {
   const int dim = a.m.dim, k = order_of(a.m);
   if (dim == 3 && k == 1) launch_t<3, 1>(a, parity, gws, st);
   else if (dim == 2 && k == 1) launch_t<2, 1>(a, parity, gws, st);

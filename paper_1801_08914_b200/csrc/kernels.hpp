@@ -45,8 +45,8 @@ void launch_hybridize_rt0(const HybArgs& a, const double* host_consts, int parit
 void launch_hybridize_rt0_rows(const HybArgs& a, const double* host_consts, double* stage, cudaStream_t st);
 // k >= 1 with nF + 1 <= 32 (RT1 hexes, RT1..RT3 quads): one warp per cell (kern_warp.cu)
 bool hybridize_warp_supported(int dim, int k);
-int64_t hybridize_warp_scratch_floats(const HybArgs& a);
-void launch_hybridize_warp(const HybArgs& a, int parity, float* gws, cudaStream_t st);
+int64_t hybridize_warp_scratch_doubles(const HybArgs& a);
+void launch_hybridize_warp(const HybArgs& a, int parity, double* gws, cudaStream_t st);
 // General path (k >= 1): one CTA per cell, shared-memory or global workspace.
 void launch_hybridize_cta(const HybArgs& a, int parity, double* gws, int64_t ws_doubles, cudaStream_t st);
 int64_t hybridize_cta_ws_doubles(const DevMesh& m, int nF, int r, int p_max, bool* use_smem);
