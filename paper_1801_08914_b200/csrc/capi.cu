@@ -501,6 +501,13 @@ static hdr_status run_hybridize(hdr_hybrid_t op, const double* alpha, const doub
         }
         launch_hybridize_rt0_rows(A, sp->rt0_consts.data(), op->ws.p, st);
       }
+    } else if (hybridize_big_supported(sp->dim, sp->k) && !getenv("HDR_CTA_PATH")) {
+      const int64_t need = hybridize_big_scratch_doubles(A, sp->k);
+      if (op->ws_doubles < need) {
+        op->ws.alloc(static_cast<size_t>(need));
+        op->ws_doubles = need;
+      }
+      for (int parity = 0; parity < 2; ++parity) launch_hybridize_big(A, sp->k, parity, op->ws.p, st);
     } else if (hybridize_warp_supported(sp->dim, sp->k) && !getenv("HDR_CTA_PATH")) {
       const int64_t need = hybridize_warp_scratch_doubles(A);
       if (op->ws_doubles < need) {

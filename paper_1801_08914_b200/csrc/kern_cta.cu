@@ -1,0 +1,386 @@
+// Structured element solve for RT2 / RT3 hexahedra: one 256-thread CTA per
+// cell (n = 108 / 240 local dofs, nF = 54 / 96 face dofs).
+//
+// Same mathematics as kern_warp.cu (fp64 V = A0^-1 [E_F | f_T]; fp32 first-order
+// correction C = V_F^T (Delta32 V); a-posteriori order control), organised for
+// elements whose n x n matrices do not fit on chip:
+//   phase V  : V in row blocks (X rows staged per block), fp32 copy V32 kept in
+//              shared memory (n x NCP), fp64 face rows to a per-CTA scratch
+//   phase C  : Delta32 generated in row blocks of IB rows (stored transposed),
+//              Y_I = Delta_I V32 (smem), C += V32_I^T Y_I with C held in registers
+//              (a 6x7 / 3x4 tile per thread) across all blocks
+//   scatter  : per-cell tables, H = V_F - C, red-black like the other paths.
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+
+#include "hdr_device.cuh"
+#include "kernels.hpp"
+
+namespace hdr {
+namespace {
+
+template <int K>
+struct Big {
+  static constexpr int DIM = 3;
+  static constexpr int DPF = (K + 1) * (K + 1);
+  static constexpr int NF = 6 * DPF;
+  static constexpr int NINT = 3 * K * DPF;
+  static constexpr int N = NF + NINT;
+  static constexpr int R = (K + 1) * (K + 1) * (K + 1);
+  static constexpr int NC = NF + 1;
+  static constexpr int NCP = (NC + 3) & ~3;
+  static constexpr int IB = (K == 3) ? 60 : 36;  // rows per block, divides N
+  static constexpr int NB = N / IB;
+  // thread tiles: V / Y blocks (IB x NC), C (NF x NC)
+  static constexpr int VT_M = (K == 3) ? 4 : 3, VT_N = (K == 3) ? 6 : 3;
+  static constexpr int CT_M = (K == 3) ? 6 : 3, CT_N = (K == 3) ? 7 : 4;
+  static constexpr int NS = 6;
+};
+
+constexpr int kThreads = 256;
+
+template <int K>
+struct BigSmem {
+  using B = Big<K>;
+  float v32[B::N * B::NCP];
+  union U {
+    struct {
+      double z[B::R * B::NC];
+      double xi[B::IB * B::R];
+    } pv;
+    struct {
+      float dt[B::N * B::IB];  // Delta32 block transposed: dt[l * IB + ii]
+      float y[B::IB * B::NCP];
+    } pc;
+  } u;
+  double f[B::N], nf[B::N], s[B::R];
+  long long rstart[B::NS];
+  int rlen[B::NS], grow[B::NS], rank[B::NS * B::NS];
+  float red[2 * kThreads / 32];
+  int order;
+};
+
+template <int K>
+constexpr int64_t big_scratch_doubles() {
+  using B = Big<K>;
+  // vf (NF x NC fp64) + Y (N x NCP fp32) + T (N x NCP fp32)
+  return static_cast<int64_t>(B::NF) * B::NC + static_cast<int64_t>(B::N) * B::NCP + 16;
+}
+
+template <int K>
+__global__ void __launch_bounds__(kThreads, 1) k_hyb_big(HybArgs A, int parity, double* gws) {
+  using B = Big<K>;
+  constexpr int N = B::N, NF = B::NF, NC = B::NC, NCP = B::NCP, R = B::R, NINT = B::NINT, DPF = B::DPF;
+  constexpr int IB = B::IB, NS = B::NS;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  BigSmem<K>& sm = *reinterpret_cast<BigSmem<K>*>(smem_raw);
+  const int tid = threadIdx.x;
+  const Fixed& fx = A.fx;
+  double* vf = gws + static_cast<int64_t>(blockIdx.x) * big_scratch_doubles<K>();  // NF x NC
+  float* yg = reinterpret_cast<float*>(vf + NF * NC);                               // N x NCP (Y, higher orders)
+  const uint32_t cnt = static_cast<uint32_t>(parity_count(A.m));
+
+  for (uint32_t t = blockIdx.x; t < cnt; t += gridDim.x) {
+    int cc[3];
+    const int e = parity_cell32(A.m, parity, t, cc);
+    if (e < 0) continue;
+    const double a = A.alpha[e], b = A.beta[e];
+    const double ib = 1.0 / b;
+    const double* fe = A.f + static_cast<int64_t>(e) * N;
+    // ---------------------------------------------------------------- phase V (fp64)
+    for (int i = tid; i < N; i += kThreads) sm.f[i] = fe[i];
+    for (int j = tid; j < R; j += kThreads) sm.s[j] = b / fma(a, __ldg(fx.lam + j), b);
+    __syncthreads();
+    for (int i = tid; i < N; i += kThreads) {
+      double acc = 0.0;
+      const double* row = fx.N0 + static_cast<int64_t>(i) * N;
+#pragma unroll 8
+      for (int l = 0; l < N; ++l) acc = fma(__ldg(row + l), sm.f[l], acc);
+      sm.nf[i] = acc;
+    }
+    for (int idx = tid; idx < R * NF; idx += kThreads) {
+      const int j = idx / NF, c = idx - j * NF;
+      sm.u.pv.z[j * NC + c] = sm.s[j] * __ldg(fx.X + (NINT + c) * R + j);
+    }
+    {  // z[:, NF] = s * X^T f : R dots of length N, 4 threads each
+      for (int j0 = 0; j0 < R; j0 += kThreads / 4) {
+        const int j = j0 + tid / 4, part = tid & 3;
+        double acc = 0.0;
+        if (j < R)
+          for (int l = part; l < N; l += 4) acc = fma(__ldg(fx.X + l * R + j), sm.f[l], acc);
+        acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+        acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+        if (j < R && part == 0) sm.u.pv.z[j * NC + NF] = sm.s[j] * acc;
+      }
+    }
+    __syncthreads();
+    for (int i0 = 0; i0 < N; i0 += IB) {
+      for (int idx = tid; idx < IB * R; idx += kThreads) sm.u.pv.xi[idx] = __ldg(fx.X + i0 * R + idx);
+      __syncthreads();
+      constexpr int TM = B::VT_M, TN = B::VT_N;
+      constexpr int TMS = (IB + TM - 1) / TM, TNS = (NC + TN - 1) / TN;
+      for (int tile = tid; tile < TMS * TNS; tile += kThreads) {
+        const int m0 = (tile / TNS) * TM, n0 = (tile % TNS) * TN;
+        double acc[TM][TN];
+#pragma unroll
+        for (int i = 0; i < TM; ++i)
+#pragma unroll
+          for (int jj = 0; jj < TN; ++jj) acc[i][jj] = 0.0;
+#pragma unroll 4
+        for (int j = 0; j < R; ++j) {
+          double xv[TM], zv[TN];
+#pragma unroll
+          for (int i = 0; i < TM; ++i) xv[i] = (m0 + i < IB) ? sm.u.pv.xi[(m0 + i) * R + j] : 0.0;
+#pragma unroll
+          for (int jj = 0; jj < TN; ++jj) zv[jj] = (n0 + jj < NC) ? sm.u.pv.z[j * NC + n0 + jj] : 0.0;
+#pragma unroll
+          for (int i = 0; i < TM; ++i)
+#pragma unroll
+            for (int jj = 0; jj < TN; ++jj) acc[i][jj] = fma(xv[i], zv[jj], acc[i][jj]);
+        }
+#pragma unroll
+        for (int i = 0; i < TM; ++i)
+#pragma unroll
+          for (int jj = 0; jj < TN; ++jj) {
+            const int row = i0 + m0 + i, col = n0 + jj;
+            if (m0 + i >= IB || col >= NC) continue;
+            const double base = (col < NF) ? __ldg(fx.N0 + static_cast<int64_t>(row) * N + NINT + col) : sm.nf[row];
+            const double v = (base + acc[i][jj]) * ib;
+            sm.v32[row * NCP + col] = static_cast<float>(v);
+            if (row >= NINT) vf[(row - NINT) * NC + col] = v;
+          }
+      }
+      __syncthreads();
+    }
+    // ---------------------------------------------------------------- phase C (fp32)
+    constexpr int CM = B::CT_M, CN = B::CT_N;
+    constexpr int CMS = (NF + CM - 1) / CM, CNS = (NC + CN - 1) / CN;
+    const bool cown = tid < CMS * CNS;
+    const int cm0 = cown ? (tid / CNS) * CM : 0, cn0 = cown ? (tid % CNS) * CN : 0;
+    float cacc[CM][CN];
+#pragma unroll
+    for (int i = 0; i < CM; ++i)
+#pragma unroll
+      for (int j = 0; j < CN; ++j) cacc[i][j] = 0.f;
+    int P = 1;
+    for (int pass = 1; pass <= P; ++pass) {
+      // right operand of this order: V32 (pass 1) or T = A0^-1 Y_prev (global, rare)
+      const float* rhs = (pass == 1) ? sm.v32 : yg + N * NCP;  // T staged behind Y in scratch
+      for (int i0 = 0; i0 < N; i0 += IB) {
+        for (int idx = tid; idx < IB * N; idx += kThreads) {
+          const int ii = idx / N, l = idx - ii * N;
+          const int64_t o = static_cast<int64_t>(i0 + ii) * N + l;
+          sm.u.pc.dt[l * IB + ii] = static_cast<float>(
+              delta_entry(a, b, __ldg(fx.D + o), __ldg(fx.M + o), __ldg(fx.E + o), __ldg(fx.Ma + o)));
+        }
+        __syncthreads();
+        {  // Y_I = Delta_I rhs
+          constexpr int TM = B::VT_M, TN = B::VT_N;
+          constexpr int TMS = (IB + TM - 1) / TM, TNS = (NC + TN - 1) / TN;
+          for (int tile = tid; tile < TMS * TNS; tile += kThreads) {
+            const int m0 = (tile / TNS) * TM, n0 = (tile % TNS) * TN;
+            float acc[TM][TN];
+#pragma unroll
+            for (int i = 0; i < TM; ++i)
+#pragma unroll
+              for (int jj = 0; jj < TN; ++jj) acc[i][jj] = 0.f;
+#pragma unroll 4
+            for (int l = 0; l < N; ++l) {
+              float dv[TM], rv[TN];
+#pragma unroll
+              for (int i = 0; i < TM; ++i) dv[i] = (m0 + i < IB) ? sm.u.pc.dt[l * IB + m0 + i] : 0.f;
+#pragma unroll
+              for (int jj = 0; jj < TN; ++jj) rv[jj] = (n0 + jj < NC) ? rhs[l * NCP + n0 + jj] : 0.f;
+#pragma unroll
+              for (int i = 0; i < TM; ++i)
+#pragma unroll
+                for (int jj = 0; jj < TN; ++jj) acc[i][jj] = fmaf(dv[i], rv[jj], acc[i][jj]);
+            }
+#pragma unroll
+            for (int i = 0; i < TM; ++i)
+#pragma unroll
+              for (int jj = 0; jj < TN; ++jj)
+                if (m0 + i < IB && n0 + jj < NC) {
+                  sm.u.pc.y[(m0 + i) * NCP + n0 + jj] = acc[i][jj];
+                  yg[(i0 + m0 + i) * NCP + n0 + jj] = acc[i][jj];
+                }
+          }
+        }
+        __syncthreads();
+        if (cown) {  // C (+/-)= V32_I^T Y_I
+          const float sg = (pass == 1) ? 1.f : ((pass & 1) ? 1.f : -1.f);
+#pragma unroll 4
+          for (int ii = 0; ii < IB; ++ii) {
+            float vv[CM], yv[CN];
+#pragma unroll
+            for (int i = 0; i < CM; ++i) vv[i] = (cm0 + i < NF) ? sg * sm.v32[(i0 + ii) * NCP + cm0 + i] : 0.f;
+#pragma unroll
+            for (int j = 0; j < CN; ++j) yv[j] = (cn0 + j < NC) ? sm.u.pc.y[ii * NCP + cn0 + j] : 0.f;
+#pragma unroll
+            for (int i = 0; i < CM; ++i)
+#pragma unroll
+              for (int j = 0; j < CN; ++j) cacc[i][j] = fmaf(vv[i], yv[j], cacc[i][j]);
+          }
+        }
+        __syncthreads();
+      }
+      if (pass == 1) {  // a-posteriori order control: 10 (|C| / |H0|)^2 <= 1e-12 -> order 1 suffices
+        float cmax = 0.f, hmax = 0.f;
+        if (cown)
+#pragma unroll
+          for (int i = 0; i < CM; ++i)
+#pragma unroll
+            for (int j = 0; j < CN; ++j)
+              if (cm0 + i < NF && cn0 + j < NF) {
+                cmax = fmaxf(cmax, fabsf(cacc[i][j]));
+                hmax = fmaxf(hmax, fabsf(sm.v32[(NINT + cm0 + i) * NCP + cn0 + j]));
+              }
+        for (int o = 16; o > 0; o >>= 1) {
+          cmax = fmaxf(cmax, __shfl_xor_sync(0xffffffffu, cmax, o));
+          hmax = fmaxf(hmax, __shfl_xor_sync(0xffffffffu, hmax, o));
+        }
+        if ((tid & 31) == 0) {
+          sm.red[tid >> 5] = cmax;
+          sm.red[kThreads / 32 + (tid >> 5)] = hmax;
+        }
+        __syncthreads();
+        if (tid == 0) {
+          float cm = 0.f, hm = 0.f;
+          for (int w = 0; w < kThreads / 32; ++w) {
+            cm = fmaxf(cm, sm.red[w]);
+            hm = fmaxf(hm, sm.red[kThreads / 32 + w]);
+          }
+          const double ratio = hm > 0.f ? static_cast<double>(cm) / hm : 0.0;
+          int p = 1;
+          double tt = ratio * ratio * 10.0;
+          while (tt > 1e-12 && p < A.p_max) {
+            ++p;
+            tt *= ratio;
+          }
+          if (!(ratio < 0.25)) atomicOr(A.status, 1);
+          sm.order = p;
+        }
+        __syncthreads();
+        P = sm.order;
+      }
+      if (pass < P) {  // T = A0^-1 Y (Y in yg) -> behind Y in the scratch; rare path, fp64 accumulation
+        float* tgl = yg + N * NCP;
+        for (int idx = tid; idx < R * NC; idx += kThreads) {
+          const int j = idx / NC, c = idx - j * NC;
+          double acc = 0.0;
+          for (int l = 0; l < N; ++l) acc = fma(__ldg(fx.X + l * R + j), static_cast<double>(yg[l * NCP + c]), acc);
+          sm.u.pv.z[idx] = sm.s[j] * acc;
+        }
+        __syncthreads();
+        for (int idx = tid; idx < N * NC; idx += kThreads) {
+          const int i = idx / NC, c = idx - i * NC;
+          double acc = 0.0;
+          for (int l = 0; l < N; ++l)
+            acc = fma(__ldg(fx.N0 + static_cast<int64_t>(i) * N + l), static_cast<double>(yg[l * NCP + c]), acc);
+          for (int j = 0; j < R; ++j) acc = fma(__ldg(fx.X + i * R + j), sm.u.pv.z[j * NC + c], acc);
+          tgl[i * NCP + c] = static_cast<float>(acc * ib);
+        }
+        __syncthreads();
+      }
+    }
+    // ---------------------------------------------------------------- scatter
+    {
+      unsigned lo = 0, hi = 0;
+#pragma unroll
+      for (int x = 0; x < 3; ++x) {
+        const int cx = x == 0 ? cc[0] : (x == 1 ? cc[1] : cc[2]);
+        const int Nx = static_cast<int>(x == 0 ? A.m.N[0] : (x == 1 ? A.m.N[1] : A.m.N[2]));
+        lo |= static_cast<unsigned>(cx > 0) << x;
+        hi |= static_cast<unsigned>(cx + 1 < Nx) << x;
+      }
+      for (int idx = tid; idx < NS * NS; idx += kThreads) {
+        const int ps = idx / NS, qs = idx - ps * NS;
+        const int a_ = ps >> 1;
+        const bool pin = (((ps & 1) ? hi : lo) >> a_) & 1u;
+        const bool qin = (((qs & 1) ? hi : lo) >> (qs >> 1)) & 1u;
+        const int ca = a_ == 0 ? cc[0] : (a_ == 1 ? cc[1] : cc[2]);
+        const int na = static_cast<int>(a_ == 0 ? A.m.N[0] : (a_ == 1 ? A.m.N[1] : A.m.N[2]));
+        sm.rank[idx] = (pin && qin) ? col_rank_fast(3, ps, qs, lo, hi, ca, na, false) : -1;
+        if (qs == 0) {
+          const int side = ps & 1;
+          if (pin) {
+            const int face = face_id32(A.m, a_, cc[0] + (a_ == 0 ? side : 0), cc[1] + (a_ == 1 ? side : 0),
+                                       cc[2] + (a_ == 2 ? side : 0));
+            const int row = A.mbase[face];
+            const int64_t r0s = A.rowoff[row];
+            sm.rstart[ps] = r0s;
+            sm.rlen[ps] = static_cast<int>(A.rowoff[row + 1] - r0s);
+            sm.grow[ps] = row;
+          } else {
+            sm.rstart[ps] = -1;
+          }
+        }
+      }
+    }
+    __syncthreads();
+    if (cown) {
+#pragma unroll
+      for (int i = 0; i < CM; ++i) {
+        const int p = cm0 + i;
+        if (p >= NF) continue;
+        const int ps = p / DPF, sub = p - ps * DPF;
+        const int64_t rs = sm.rstart[ps];
+        if (rs < 0) continue;
+#pragma unroll
+        for (int j = 0; j < CN; ++j) {
+          const int c = cn0 + j;
+          if (c >= NC) continue;
+          const double v = vf[p * NC + c] - static_cast<double>(cacc[i][j]);
+          if (c == NF) {
+            double* gp = A.g + sm.grow[ps] + sub;
+            *gp = parity ? *gp + v : v;
+            continue;
+          }
+          const int qs = c / DPF, sj = c - qs * DPF;
+          const int rk = sm.rank[ps * NS + qs];
+          if (rk < 0) continue;
+          double* hp = A.hval + rs + static_cast<int64_t>(sub) * sm.rlen[ps] + rk * DPF + sj;
+          *hp = (parity == 1 && ps == qs) ? *hp + v : v;
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+template <int K>
+void launch_big_t(const HybArgs& a, int parity, double* gws, int64_t grid, cudaStream_t st) {
+  const size_t smem = sizeof(BigSmem<K>);
+  cudaFuncSetAttribute(k_hyb_big<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  k_hyb_big<K><<<static_cast<unsigned>(grid), kThreads, smem, st>>>(a, parity, gws);
+}
+
+template <int K>
+int64_t grid_big_t(const HybArgs& a) {
+  const size_t smem = sizeof(BigSmem<K>);
+  cudaFuncSetAttribute(k_hyb_big<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  int dev = 0, sms = 148, per_sm = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_hyb_big<K>, kThreads, smem);
+  const int64_t cnt = parity_count(a.m);
+  return std::max<int64_t>(1, std::min<int64_t>(cnt, static_cast<int64_t>(sms) * std::max(per_sm, 1)));
+}
+
+}  // namespace
+
+bool hybridize_big_supported(int dim, int k) { return dim == 3 && (k == 2 || k == 3); }
+
+int64_t hybridize_big_scratch_doubles(const HybArgs& a, int k) {
+  if (k == 2) return grid_big_t<2>(a) * (big_scratch_doubles<2>() + static_cast<int64_t>(Big<2>::N) * Big<2>::NCP / 2 + 8);
+  return grid_big_t<3>(a) * (big_scratch_doubles<3>() + static_cast<int64_t>(Big<3>::N) * Big<3>::NCP / 2 + 8);
+}
+
+void launch_hybridize_big(const HybArgs& a, int k, int parity, double* gws, cudaStream_t st) {
+  if (k == 2) launch_big_t<2>(a, parity, gws, grid_big_t<2>(a), st);
+  else launch_big_t<3>(a, parity, gws, grid_big_t<3>(a), st);
+  count_launch();
+}
+
+}  // namespace hdr

@@ -47,6 +47,10 @@ void launch_hybridize_rt0_rows(const HybArgs& a, const double* host_consts, doub
 bool hybridize_warp_supported(int dim, int k);
 int64_t hybridize_warp_scratch_doubles(const HybArgs& a);
 void launch_hybridize_warp(const HybArgs& a, int parity, double* gws, cudaStream_t st);
+// RT2 / RT3 hexahedra: one CTA per cell (kern_cta.cu)
+bool hybridize_big_supported(int dim, int k);
+int64_t hybridize_big_scratch_doubles(const HybArgs& a, int k);
+void launch_hybridize_big(const HybArgs& a, int k, int parity, double* gws, cudaStream_t st);
 // General path (k >= 1): one CTA per cell, shared-memory or global workspace.
 void launch_hybridize_cta(const HybArgs& a, int parity, double* gws, int64_t ws_doubles, cudaStream_t st);
 int64_t hybridize_cta_ws_doubles(const DevMesh& m, int nF, int r, int p_max, bool* use_smem);
