@@ -109,7 +109,11 @@ struct hdr_hybrid_s {
 
 struct hdr_condensed_s {
   hdr_space_t sp = nullptr;
-  DBuf<double> sval, fs, alpha, beta, f;
+  DBuf<double> sval, fs, alpha, beta, f, ws;
+  DBuf<int> status;
+  int64_t ws_doubles = 0;
+  const double* a_ptr = nullptr;
+  const double* b_ptr = nullptr;
 };
 
 namespace {
@@ -648,29 +652,175 @@ hdr_status hdr_recover_hybrid(hdr_hybrid_t op, const double* lambda, const doubl
   });
 }
 
-// ---- placeholders until the condensation / spmv kernels land
-hdr_status hdr_static_condense_fe(hdr_space_t, const double*, const double*, const double*, int, hdr_condensed_t* out) {
-  if (out) *out = nullptr;
-  return fail(HDR_UNSUPPORTED, "static condensation not built yet");
+static hdr_status check_cond_status(int* d_status, cudaStream_t st) {
+  int status = 0;
+  CK(cudaMemcpyAsync(&status, d_status, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (status) CK(cudaMemsetAsync(d_status, 0, sizeof(int), st));
+  if (status & 2) return fail(HDR_SINGULAR_BLOCK, "static_condense: an interior block A_ii is not positive definite");
+  return HDR_OK;
 }
-hdr_status hdr_static_condense_fe_into(hdr_condensed_t, const double*, const double*, const double*, int) {
-  return fail(HDR_UNSUPPORTED, "static condensation not built yet");
+
+static hdr_status run_condense(hdr_condensed_t op, const double* alpha, const double* beta, const double* f_hat,
+                               int on_device) {
+  hdr_space_t sp = op->sp;
+  return catch_all([&]() -> hdr_status {
+    cudaStream_t st = sp->stream;
+    const double *da = alpha, *db = beta, *df = f_hat;
+    if (!on_device) {
+      stage(op->alpha, alpha, sp->ncells, 0, st);
+      stage(op->beta, beta, sp->ncells, 0, st);
+      stage(op->f, f_hat, sp->broken, 0, st);
+      da = op->alpha.p;
+      db = op->beta.p;
+      df = op->f.p;
+    }
+    op->a_ptr = da;
+    op->b_ptr = db;
+    if (!op->sval.p) op->sval.alloc(sp->nnz_s);
+    if (!op->fs.p) op->fs.alloc(sp->ns);
+    if (!op->status.p) {
+      op->status.alloc(1);
+      CK(cudaMemsetAsync(op->status.p, 0, sizeof(int), st));
+    }
+    const int64_t need = condense_ws_doubles(sp->dm, sp->nF);
+    if (need > op->ws_doubles) {
+      op->ws.alloc(static_cast<size_t>(need));
+      op->ws_doubles = need;
+    }
+    CondArgs C{};
+    C.m = sp->dm;
+    C.fx = sp->fx;
+    C.nF = sp->nF;
+    C.alpha = da;
+    C.beta = db;
+    C.f = df;
+    C.rowoff = sp->row_s.p;
+    C.sval = op->sval.p;
+    C.fs = op->fs.p;
+    C.status = op->status.p;
+    for (int parity = 0; parity < 2; ++parity) launch_condense(C, parity, op->ws.p, op->ws_doubles, st);
+    CK(cudaGetLastError());
+    return check_cond_status(op->status.p, st);
+  });
 }
+
+hdr_status hdr_static_condense_fe(hdr_space_t sp, const double* alpha, const double* beta, const double* f_hat,
+                                  int on_device, hdr_condensed_t* out) {
+  if (!sp || !out || !alpha || !beta || !f_hat) return fail(HDR_INVALID_ARGUMENT, "null argument");
+  *out = nullptr;
+  auto op = std::make_unique<hdr_condensed_s>();
+  op->sp = sp;
+  const hdr_status s = run_condense(op.get(), alpha, beta, f_hat, on_device);
+  if (s != HDR_OK) return s;
+  *out = op.release();
+  return HDR_OK;
+}
+
+hdr_status hdr_static_condense_fe_into(hdr_condensed_t op, const double* alpha, const double* beta,
+                                       const double* f_hat, int on_device) {
+  if (!op || !alpha || !beta || !f_hat) return fail(HDR_INVALID_ARGUMENT, "null argument");
+  return run_condense(op, alpha, beta, f_hat, on_device);
+}
+
 void hdr_condensed_destroy(hdr_condensed_t op) { delete op; }
-hdr_status hdr_condensed_values(hdr_condensed_t, double*, double*, int) {
-  return fail(HDR_UNSUPPORTED, "static condensation not built yet");
+
+hdr_status hdr_condensed_values(hdr_condensed_t op, double* s_values, double* f_s, int dst_on_device) {
+  if (!op) return fail(HDR_INVALID_ARGUMENT, "null operator");
+  return catch_all([&]() -> hdr_status {
+    const cudaMemcpyKind kind = dst_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+    cudaStream_t st = op->sp->stream;
+    if (s_values && op->sp->nnz_s)
+      CK(cudaMemcpyAsync(s_values, op->sval.p, static_cast<size_t>(op->sp->nnz_s) * 8, kind, st));
+    if (f_s && op->sp->ns) CK(cudaMemcpyAsync(f_s, op->fs.p, static_cast<size_t>(op->sp->ns) * 8, kind, st));
+    CK(cudaStreamSynchronize(st));
+    return HDR_OK;
+  });
 }
-hdr_status hdr_recover_condensed(hdr_condensed_t, const double*, const double*, int, double*) {
-  return fail(HDR_UNSUPPORTED, "static condensation not built yet");
+
+hdr_status hdr_recover_condensed(hdr_condensed_t op, const double* x_b, const double* f_hat, int on_device,
+                                 double* x) {
+  if (!op || !x_b || !f_hat || !x) return fail(HDR_INVALID_ARGUMENT, "null argument");
+  hdr_space_t sp = op->sp;
+  return catch_all([&]() -> hdr_status {
+    cudaStream_t st = sp->stream;
+    DBuf<double> dxb, df, dx;
+    const double *pxb = x_b, *pf = f_hat;
+    double* px = x;
+    if (!on_device) {
+      stage(dxb, x_b, sp->ns, 0, st);
+      stage(df, f_hat, sp->broken, 0, st);
+      dx.alloc(sp->ndofs);
+      pxb = dxb.p;
+      pf = df.p;
+      px = dx.p;
+    }
+    const int64_t need = condense_ws_doubles(sp->dm, sp->nF);
+    if (need > op->ws_doubles) {
+      op->ws.alloc(static_cast<size_t>(need));
+      op->ws_doubles = need;
+    }
+    CondArgs C{};
+    C.m = sp->dm;
+    C.fx = sp->fx;
+    C.nF = sp->nF;
+    C.alpha = op->a_ptr;
+    C.beta = op->b_ptr;
+    C.f = pf;
+    C.xb = pxb;
+    C.x = px;
+    C.status = op->status.p;
+    launch_recover_condensed(C, op->ws.p, op->ws_doubles, st);
+    CK(cudaGetLastError());
+    if (!on_device) CK(cudaMemcpyAsync(x, px, static_cast<size_t>(sp->ndofs) * 8, cudaMemcpyDeviceToHost, st));
+    return check_cond_status(op->status.p, st);
+  });
 }
-hdr_status hdr_hybrid_spmv(hdr_hybrid_t, const double*, double*, int) {
-  return fail(HDR_UNSUPPORTED, "spmv not built yet");
+
+static hdr_status spmv_common(hdr_space_t sp, int which, const double* vals, const double* x, double* y,
+                              int on_device) {
+  return catch_all([&]() -> hdr_status {
+    cudaStream_t st = sp->stream;
+    const int64_t nr = which == 0 ? sp->m : sp->ns;
+    DBuf<double> dx, dy;
+    const double* px = x;
+    double* py = y;
+    if (!on_device) {
+      stage(dx, x, nr, 0, st);
+      dy.alloc(nr);
+      px = dx.p;
+      py = dy.p;
+    }
+    if (which == 0)
+      launch_spmv32(nr, sp->row_h.p, sp->col_h.p, vals, px, py, st);
+    else
+      launch_spmv32(nr, sp->row_s.p, sp->col_s.p, vals, px, py, st);
+    CK(cudaGetLastError());
+    if (!on_device) CK(cudaMemcpyAsync(y, py, static_cast<size_t>(nr) * 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    return HDR_OK;
+  });
 }
-hdr_status hdr_condensed_spmv(hdr_condensed_t, const double*, double*, int) {
-  return fail(HDR_UNSUPPORTED, "spmv not built yet");
+
+hdr_status hdr_hybrid_spmv(hdr_hybrid_t op, const double* x, double* y, int on_device) {
+  if (!op || !x || !y) return fail(HDR_INVALID_ARGUMENT, "null argument");
+  return spmv_common(op->sp, 0, op->hval.p, x, y, on_device);
 }
-hdr_status hdr_csr_spmv_device(int64_t, const int64_t*, const int64_t*, const double*, const double*, double*, void*) {
-  return fail(HDR_UNSUPPORTED, "spmv not built yet");
+
+hdr_status hdr_condensed_spmv(hdr_condensed_t op, const double* x, double* y, int on_device) {
+  if (!op || !x || !y) return fail(HDR_INVALID_ARGUMENT, "null argument");
+  return spmv_common(op->sp, 1, op->sval.p, x, y, on_device);
+}
+
+hdr_status hdr_csr_spmv_device(int64_t nrows, const int64_t* row_offsets, const int64_t* col_indices,
+                               const double* values, const double* x, double* y, void* stream) {
+  if (nrows < 0 || (nrows > 0 && (!row_offsets || !col_indices || !values || !x || !y)))
+    return fail(HDR_INVALID_ARGUMENT, "null argument");
+  return catch_all([&]() -> hdr_status {
+    launch_spmv64(nrows, row_offsets, col_indices, values, x, y, static_cast<cudaStream_t>(stream));
+    CK(cudaGetLastError());
+    return HDR_OK;
+  });
 }
 
 }  // extern "C"

@@ -69,4 +69,27 @@ struct RecArgs {
 void launch_recover_hybrid(const RecArgs& a, double* gws, int64_t ws_doubles, cudaStream_t st);
 void launch_average_faces(const DevMesh& m, const double* x_hat, double* x, cudaStream_t st);
 
+// ---- static condensation / recover_condensed (kern_condense.cu)
+struct CondArgs {
+  DevMesh m;
+  Fixed fx;
+  int nF;
+  const double *alpha, *beta, *f;
+  const int64_t* rowoff;  // S pattern
+  double* sval;
+  double* fs;
+  const double* xb;  // recover_condensed input (nS)
+  double* x;         // recover_condensed output (ndofs)
+  int* status;       // bit 1: A_ii not SPD
+};
+void launch_condense(const CondArgs& c, int parity, double* gws, int64_t ws_doubles, cudaStream_t st);
+int64_t condense_ws_doubles(const DevMesh& m, int nF);
+void launch_recover_condensed(const CondArgs& c, double* gws, int64_t ws_doubles, cudaStream_t st);
+
+// ---- spmv (kern_spmv.cu)
+void launch_spmv32(int64_t nrows, const int64_t* ro, const int32_t* ci, const double* v, const double* x, double* y,
+                   cudaStream_t st);
+void launch_spmv64(int64_t nrows, const int64_t* ro, const int64_t* ci, const double* v, const double* x, double* y,
+                   cudaStream_t st);
+
 }  // namespace hdr
