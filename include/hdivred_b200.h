@@ -166,6 +166,9 @@ hdr_status hdr_recover_condensed(hdr_condensed_t op, const double* x_b, const do
  * (hybrid) / y = S x (condensed).  Row sums accumulate in storage order. */
 hdr_status hdr_hybrid_spmv(hdr_hybrid_t op, const double* x, double* y, int on_device);
 hdr_status hdr_condensed_spmv(hdr_condensed_t op, const double* x, double* y, int on_device);
+/* Host-array form of spmv for a caller-owned CsrMatrix (copies in and out). */
+hdr_status hdr_csr_spmv_host(int64_t nrows, int64_t ncols, const int64_t* row_offsets, const int64_t* col_indices,
+                             const double* values, const double* x, double* y);
 /* General CSR SpMV on device arrays (int64 offsets, int64 columns). */
 hdr_status hdr_csr_spmv_device(int64_t nrows, const int64_t* row_offsets, const int64_t* col_indices,
                                const double* values, const double* x, double* y, void* stream);

@@ -50,6 +50,7 @@ _SIGS = {
     "hdr_hybrid_spmv": (_i32, [_vp, _vp, _vp, _i32]),
     "hdr_condensed_spmv": (_i32, [_vp, _vp, _vp, _i32]),
     "hdr_csr_spmv_device": (_i32, [_i64, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "hdr_csr_spmv_host": (_i32, [_i64, _i64, _vp, _vp, _vp, _vp, _vp]),
     "hdr_reference_element": (_i32, [_i32, _i32, _vp, _vp, _vp, _vp, _vp]),
     "hdr_structured_factors": (_i32, [_i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "hdr_last_error": (ctypes.c_char_p, []),

@@ -812,6 +812,34 @@ hdr_status hdr_condensed_spmv(hdr_condensed_t op, const double* x, double* y, in
   return spmv_common(op->sp, 1, op->sval.p, x, y, on_device);
 }
 
+hdr_status hdr_csr_spmv_host(int64_t nrows, int64_t ncols, const int64_t* row_offsets, const int64_t* col_indices,
+                             const double* values, const double* x, double* y) {
+  if (nrows < 0 || ncols < 0 || !row_offsets || (nrows > 0 && (!col_indices || !values || !x || !y)))
+    return fail(HDR_INVALID_ARGUMENT, "null argument");
+  return catch_all([&]() -> hdr_status {
+    int devs = 0;
+    if (cudaGetDeviceCount(&devs) != cudaSuccess || devs == 0) return fail(HDR_CUDA_ERROR, "no CUDA device available");
+    const int64_t nnz = row_offsets[nrows];
+    DBuf<int64_t> ro, ci;
+    DBuf<double> v, dx, dy;
+    ro.alloc(nrows + 1);
+    ci.alloc(nnz);
+    v.alloc(nnz);
+    dx.alloc(ncols);
+    dy.alloc(nrows);
+    CK(cudaMemcpy(ro.p, row_offsets, static_cast<size_t>(nrows + 1) * 8, cudaMemcpyHostToDevice));
+    if (nnz) {
+      CK(cudaMemcpy(ci.p, col_indices, static_cast<size_t>(nnz) * 8, cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(v.p, values, static_cast<size_t>(nnz) * 8, cudaMemcpyHostToDevice));
+    }
+    if (ncols) CK(cudaMemcpy(dx.p, x, static_cast<size_t>(ncols) * 8, cudaMemcpyHostToDevice));
+    launch_spmv64(nrows, ro.p, ci.p, v.p, dx.p, dy.p, nullptr);
+    CK(cudaGetLastError());
+    if (nrows) CK(cudaMemcpy(y, dy.p, static_cast<size_t>(nrows) * 8, cudaMemcpyDeviceToHost));
+    return HDR_OK;
+  });
+}
+
 hdr_status hdr_csr_spmv_device(int64_t nrows, const int64_t* row_offsets, const int64_t* col_indices,
                                const double* values, const double* x, double* y, void* stream) {
   if (nrows < 0 || (nrows > 0 && (!row_offsets || !col_indices || !values || !x || !y)))

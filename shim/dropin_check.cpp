@@ -1,0 +1,56 @@
+// Drop-in check: runs the REFERENCE (linked from oracle/_ref/libhdivred_ref.a)
+// and the B200 path through the shim on the same seeded FE inputs, in one
+// process, through the reference's own C++ types.  Prints one JSON line.
+// TEST INFRASTRUCTURE (built by shim/Makefile; run by tests/test_dropin_gpu.py).
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <string>
+
+#include "hdivred/reduction.hpp"
+#include "hdivred_b200_shim.hpp"
+
+using namespace hdivred;
+
+int main(int argc, char** argv) {
+  const int n = argc > 1 ? std::atoi(argv[1]) : 4;
+  const int k = argc > 2 ? std::atoi(argv[2]) : 1;
+  const double h = 1.0 / n;
+  const CartesianMesh mesh = build_mesh(3, {n, n, n}, {h, h, h});
+  const RtSpace sp = build_space(mesh, k);
+  CellCoefficients co = soft_hard_coefficients(mesh, 4);
+  ReductionInputs in = build_reduction_inputs(sp, co);
+  std::uint64_t s = 12345;
+  for (auto& v : in.f_hat) {
+    s ^= s << 13; s ^= s >> 7; s ^= s << 17;
+    v = -1.0 + 2.0 * (static_cast<double>(s >> 11) * 0x1.0p-53);
+  }
+  auto [ref, g_ref] = hybridize(in);
+  auto [gpu, g_gpu] = hdivred_b200::hybridize(sp, co, in.f_hat);
+  const bool pattern = ref.h_mat.row_offsets == gpu.h_mat.row_offsets && ref.h_mat.col_indices == gpu.h_mat.col_indices;
+  double dh = 0, mh = 0, dg = 0, mg = 0;
+  for (size_t i = 0; i < ref.h_mat.values.size(); ++i) {
+    dh = std::max(dh, std::fabs(ref.h_mat.values[i] - gpu.h_mat.values[i]));
+    mh = std::max(mh, std::fabs(ref.h_mat.values[i]));
+  }
+  for (size_t i = 0; i < g_ref.size(); ++i) {
+    dg = std::max(dg, std::fabs(g_ref[i] - g_gpu[i]));
+    mg = std::max(mg, std::fabs(g_ref[i]));
+  }
+  auto [cref, fs_ref] = static_condense(in);
+  auto [cgpu, fs_gpu] = hdivred_b200::static_condense(sp, co, in.f_hat);
+  const bool spat = cref.s_mat.row_offsets == cgpu.s_mat.row_offsets &&
+                    cref.s_mat.col_indices == cgpu.s_mat.col_indices && cref.master_globals == cgpu.master_globals;
+  double ds = 0, ms = 0;
+  for (size_t i = 0; i < cref.s_mat.values.size(); ++i) {
+    ds = std::max(ds, std::fabs(cref.s_mat.values[i] - cgpu.s_mat.values[i]));
+    ms = std::max(ms, std::fabs(cref.s_mat.values[i]));
+  }
+  const std::vector<double> y_ref = spmv(ref.h_mat, g_ref);
+  const std::vector<double> y_gpu = hdivred_b200::spmv(ref.h_mat, g_ref);
+  std::printf("{\"n\": %d, \"k\": %d, \"h_pattern_identical\": %s, \"h_rel\": %.3e, \"g_rel\": %.3e, "
+              "\"s_pattern_identical\": %s, \"s_rel\": %.3e, \"spmv_identical\": %s}\n",
+              n, k, pattern ? "true" : "false", dh / mh, dg / (mg > 0 ? mg : 1), spat ? "true" : "false", ds / ms,
+              y_ref == y_gpu ? "true" : "false");
+  return (pattern && spat && y_ref == y_gpu) ? 0 : 1;
+}

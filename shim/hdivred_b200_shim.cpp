@@ -1,0 +1,138 @@
+// See hdivred_b200_shim.hpp.  Maps hdr_status to the reference's exceptions.
+#include "hdivred_b200_shim.hpp"
+
+#include <array>
+#include <memory>
+#include <stdexcept>
+#include <string>
+
+#include "hdivred/errors.hpp"
+#include "hdivred_b200.h"
+
+namespace hdivred_b200 {
+namespace {
+
+void check(hdr_status s) {
+  if (s == HDR_OK) return;
+  const std::string msg = hdr_last_error();
+  switch (s) {
+    case HDR_SINGULAR_BLOCK: throw hdivred::SingularBlock(msg);
+    case HDR_DIMENSION_MISMATCH: throw hdivred::DimensionMismatch(msg);
+    case HDR_VALIDATION: throw hdivred::ValidationError(msg);
+    case HDR_INVALID_ARGUMENT: throw std::invalid_argument(msg);
+    default: throw std::runtime_error("hdivred_b200: " + msg);
+  }
+}
+
+struct SpaceDeleter {
+  void operator()(hdr_space_s* s) const { hdr_space_destroy(s); }
+};
+using SpacePtr = std::unique_ptr<hdr_space_s, SpaceDeleter>;
+
+SpacePtr make_space(const hdivred::RtSpace& sp) {
+  const int64_t cells[3] = {sp.mesh.ncells_per_axis[0], sp.mesh.ncells_per_axis[1], sp.mesh.ncells_per_axis[2]};
+  const double h[3] = {sp.mesh.cell_sizes[0], sp.mesh.cell_sizes[1], sp.mesh.cell_sizes[2]};
+  hdr_space_t s = nullptr;
+  // bind the caller's reference element matrices (their exact bits)
+  check(hdr_space_create(sp.mesh.dim, cells, h, sp.order, sp.ref_divdiv.entries.data(), sp.ref_mass.entries.data(), 0,
+                         nullptr, &s));
+  return SpacePtr(s);
+}
+
+std::array<int64_t, HDR_INFO_COUNT> info(hdr_space_t s) {
+  std::array<int64_t, HDR_INFO_COUNT> o{};
+  check(hdr_space_info(s, o.data()));
+  return o;
+}
+
+std::vector<hdivred::index_t> block_offsets(const hdivred::RtSpace& sp) {
+  std::vector<hdivred::index_t> off(static_cast<size_t>(sp.mesh.ncells()) + 1, 0);
+  for (size_t c = 0; c + 1 < off.size(); ++c) off[c + 1] = off[c] + sp.element_ndofs;
+  return off;
+}
+
+}  // namespace
+
+std::pair<hdivred::HybridizedOperator, std::vector<double>> hybridize(const hdivred::RtSpace& space,
+                                                                      const hdivred::CellCoefficients& coeffs,
+                                                                      const std::vector<double>& f_hat) {
+  if (static_cast<hdivred::index_t>(f_hat.size()) != space.broken_ndofs ||
+      static_cast<hdivred::index_t>(coeffs.alpha.size()) != space.mesh.ncells() ||
+      static_cast<hdivred::index_t>(coeffs.beta.size()) != space.mesh.ncells())
+    throw hdivred::DimensionMismatch("hybridize: inconsistent input dimensions");
+  SpacePtr s = make_space(space);
+  const auto in = info(s.get());
+  hdr_hybrid_t op = nullptr;
+  check(hdr_hybridize_fe(s.get(), coeffs.alpha.data(), coeffs.beta.data(), f_hat.data(), 0, &op));
+  std::unique_ptr<hdr_hybrid_s, void (*)(hdr_hybrid_s*)> guard(op, hdr_hybrid_destroy);
+  hdivred::HybridizedOperator out;
+  const int64_t m = in[HDR_INFO_M], nnz = in[HDR_INFO_NNZ_H];
+  out.h_mat = hdivred::CsrMatrix(m, m);
+  out.h_mat.col_indices.resize(static_cast<size_t>(nnz));
+  out.h_mat.values.resize(static_cast<size_t>(nnz));
+  std::vector<double> g(static_cast<size_t>(m));
+  check(hdr_space_pattern(s.get(), 0, out.h_mat.row_offsets.data(), out.h_mat.col_indices.data()));
+  check(hdr_hybrid_values(op, out.h_mat.values.data(), g.data(), 0));
+  out.block_offsets = block_offsets(space);
+  // diag(P^T P): 1 for bubbles and boundary faces, 2 for interior faces
+  const int64_t nd = space.ndofs;
+  out.recovery_scale.assign(static_cast<size_t>(nd), 1.0);
+  std::vector<int64_t> gl(static_cast<size_t>(space.broken_ndofs));
+  std::vector<double> sg(static_cast<size_t>(space.broken_ndofs));
+  check(hdr_space_dof_map(s.get(), gl.data(), sg.data()));
+  std::vector<double> cnt(static_cast<size_t>(nd), 0.0);
+  for (size_t r = 0; r < gl.size(); ++r) cnt[static_cast<size_t>(gl[r])] += sg[r] * sg[r];
+  for (int64_t i = 0; i < nd; ++i) out.recovery_scale[static_cast<size_t>(i)] = 1.0 / cnt[static_cast<size_t>(i)];
+  out.diagonal_gram = true;
+  return {std::move(out), std::move(g)};
+}
+
+std::pair<hdivred::CondensedOperator, std::vector<double>> static_condense(const hdivred::RtSpace& space,
+                                                                          const hdivred::CellCoefficients& coeffs,
+                                                                          const std::vector<double>& f_hat) {
+  if (static_cast<hdivred::index_t>(f_hat.size()) != space.broken_ndofs)
+    throw hdivred::DimensionMismatch("static_condense: inconsistent input dimensions");
+  SpacePtr s = make_space(space);
+  const auto in = info(s.get());
+  hdr_condensed_t op = nullptr;
+  check(hdr_static_condense_fe(s.get(), coeffs.alpha.data(), coeffs.beta.data(), f_hat.data(), 0, &op));
+  std::unique_ptr<hdr_condensed_s, void (*)(hdr_condensed_s*)> guard(op, hdr_condensed_destroy);
+  hdivred::CondensedOperator out;
+  const int64_t ns = in[HDR_INFO_NS], nnz = in[HDR_INFO_NNZ_S];
+  out.s_mat = hdivred::CsrMatrix(ns, ns);
+  out.s_mat.col_indices.resize(static_cast<size_t>(nnz));
+  out.s_mat.values.resize(static_cast<size_t>(nnz));
+  std::vector<double> f_s(static_cast<size_t>(ns));
+  check(hdr_space_pattern(s.get(), 1, out.s_mat.row_offsets.data(), out.s_mat.col_indices.data()));
+  check(hdr_condensed_values(op, out.s_mat.values.data(), f_s.data(), 0));
+  out.master_globals.resize(static_cast<size_t>(ns));
+  check(hdr_space_master_globals(s.get(), out.master_globals.data()));
+  out.block_offsets = block_offsets(space);
+  out.n_global = space.ndofs;
+  return {std::move(out), std::move(f_s)};
+}
+
+std::pair<std::vector<double>, std::vector<double>> recover_hybrid(const hdivred::RtSpace& space,
+                                                                   const hdivred::CellCoefficients& coeffs,
+                                                                   const std::vector<double>& lambda,
+                                                                   const std::vector<double>& f_hat) {
+  SpacePtr s = make_space(space);
+  hdr_hybrid_t op = nullptr;
+  check(hdr_hybridize_fe(s.get(), coeffs.alpha.data(), coeffs.beta.data(), f_hat.data(), 0, &op));
+  std::unique_ptr<hdr_hybrid_s, void (*)(hdr_hybrid_s*)> guard(op, hdr_hybrid_destroy);
+  std::vector<double> x_hat(static_cast<size_t>(space.broken_ndofs)), x(static_cast<size_t>(space.ndofs));
+  if (static_cast<hdivred::index_t>(lambda.size()) != info(s.get())[HDR_INFO_M])
+    throw hdivred::DimensionMismatch("recover_hybrid: lambda length");
+  check(hdr_recover_hybrid(op, lambda.data(), f_hat.data(), 0, x_hat.data(), x.data()));
+  return {std::move(x_hat), std::move(x)};
+}
+
+std::vector<double> spmv(const hdivred::CsrMatrix& a, const std::vector<double>& x) {
+  if (static_cast<hdivred::index_t>(x.size()) != a.ncols) throw hdivred::DimensionMismatch("spmv: vector length != ncols");
+  std::vector<double> y(static_cast<size_t>(a.nrows));
+  check(hdr_csr_spmv_host(a.nrows, a.ncols, a.row_offsets.data(), a.col_indices.data(), a.values.data(), x.data(),
+                          y.data()));
+  return y;
+}
+
+}  // namespace hdivred_b200

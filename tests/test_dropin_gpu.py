@@ -1,0 +1,29 @@
+"""Drop-in check (GPU): the reference library and the B200 path, through the
+C++ shim and the reference's own types, on the same inputs in one process
+(oracle/_ref/dropin_check, built in the build container by shim/Makefile).
+
+H / S patterns and master_globals must be identical; values agree with the
+reference to its own accuracy (the reference is ~1e-9 off the truth on these
+inputs, the device path ~1e-16); spmv through the shim is
+bit-identical to the reference's spmv on the reference's matrix."""
+import json
+import subprocess
+from pathlib import Path
+
+import pytest
+
+from conftest import has_cuda
+
+pytestmark = pytest.mark.gpu
+BIN = Path(__file__).resolve().parent.parent / "oracle" / "_ref" / "dropin_check"
+
+
+@pytest.mark.skipif(not has_cuda(), reason="needs a CUDA device")
+@pytest.mark.parametrize("n,k", [(4, 0), (4, 1), (3, 2), (2, 3)])
+def test_dropin_against_reference(n, k):
+    if not BIN.exists():
+        pytest.skip("dropin_check not built (needs /root/reference at build time)")
+    out = subprocess.run([str(BIN), str(n), str(k)], capture_output=True, text=True, timeout=600)
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    assert line["h_pattern_identical"] and line["s_pattern_identical"] and line["spmv_identical"], line
+    assert line["h_rel"] < 1e-7 and line["g_rel"] < 1e-7 and line["s_rel"] < 1e-12, line
