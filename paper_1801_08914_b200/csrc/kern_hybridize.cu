@@ -231,17 +231,20 @@ __global__ void __launch_bounds__(128, MINB) k_hyb_rt0(HybArgs A, Rt0Const<2 * D
 // staging buffer and writes the complete H row (and g entry) in one go:
 // every H row is written by exactly one lane, contiguously, so sectors are
 // filled whole and nothing is read back from H.
-// Row k of [H_T | g_T] for one RT0 cell, lanes k = 0..N-1 of a group.  Neumann
-// orders 1..P (P warp-uniform) are all lane-parallel: Y_p = Delta T_{p-1},
-// T_p = A0^-1 Y_p, and row k of the order-p term is sum_j V_jk (Y_p)_j,: (A0^-1
-// is symmetric).  wsh: N doubles, ysh / tsh: N*(N+1) doubles of warp scratch.
+// Row k of [H_T | g_T] for one RT0 cell, lanes k = 0..N-1 of a group.
+// fp64: row k of V = A0^-1 (and of [V | w]), the exact rounding errors delta_k,:
+// (full error-free transform only where M_kl != 0, i.e. the two slots of k's
+// axis; elsewhere A_kl = fl(alpha D_kl) and delta = -err(alpha D_kl)).
+// fp32: the Neumann correction (<= 1.5e-8 |H| on BASELINE inputs):
+// Y_p = Delta T_{p-1}, row k of the order-p term = sum_j V_kj (Y_p)_j,:  (A0^-1
+// symmetric), T_p rows = those terms.  P is warp-uniform.
+// vsh / ysh / tsh: N x (N+1) fp32, dsh: N x N fp32 warp scratch of this cell.
 template <int DIM>
-__device__ __forceinline__ void rt0_row_math(const HybArgs& A, const Rt0Const<2 * DIM>& c, int e, int k, int P,
-                                             double* vsh, double* ysh, double* tsh, double (&h)[2 * DIM + 1]) {
+__device__ __forceinline__ void rt0_row_math(const HybArgs& A, const Rt0Const<2 * DIM>& c, int e, int k, int& P,
+                                             bool real, float* vsh, float* ysh, float* tsh, float* dsh,
+                                             double (&h)[2 * DIM + 1]) {
   constexpr int N = 2 * DIM;
   constexpr int NC = N + 1;
-  // lane-uniform constants come from the parameter bank (broadcast); row-k ones
-  // (k differs across the lanes of a cell) from L1-cached global memory
   const double* Dk = A.fx.D + k * N;
   const double* Mk = A.fx.M + k * N;
   const double* Ek = A.fx.E + k * N;
@@ -252,61 +255,107 @@ __device__ __forceinline__ void rt0_row_math(const HybArgs& A, const Rt0Const<2 
   const double s = b / fma(a, c.lam, b);
   const double xs = __ldg(A.fx.X + k) * s;
   const double* fe = A.f + static_cast<int64_t>(e) * N;
-  double vk[N], dk[N];  // row k of V = A0^-1 and of Delta
-  double wk = 0.0;      // (A0^-1 f)_k
+  double vk[N];
+  double wk = 0.0;  // (A0^-1 f)_k
 #pragma unroll
   for (int j = 0; j < N; ++j) {
     vk[j] = fma(xs, c.X[j], __ldg(N0k + j)) * ib;
     wk = fma(vk[j], fe[j], wk);
   }
-  // [V | w] rows to the group's scratch, then y_k = Delta_k,: [V | w]
 #pragma unroll
-  for (int j = 0; j < N; ++j) vsh[k * NC + j] = vk[j];
-  vsh[k * NC + N] = wk;
+  for (int j = 0; j < N; ++j) vsh[k * NC + j] = static_cast<float>(vk[j]);
+  vsh[k * NC + N] = static_cast<float>(wk);
+  // Delta row k
+  const int k0 = k & ~1;
 #pragma unroll
-  for (int j = 0; j < N; ++j) dk[j] = delta_entry(a, b, __ldg(Dk + j), __ldg(Mk + j), __ldg(Ek + j), __ldg(Mak + j));
-  __syncwarp();
-  double y[NC];
+  for (int j = 0; j < 2; ++j) {  // same axis: M_kl != 0
+    const int l = k0 + j;
+    dsh[k * N + l] = static_cast<float>(delta_entry(a, b, __ldg(Dk + l), __ldg(Mk + l), __ldg(Ek + l), __ldg(Mak + l)));
+  }
 #pragma unroll
-  for (int q = 0; q <= N; ++q) y[q] = 0.0;
-#pragma unroll
-  for (int l = 0; l < N; ++l)
-#pragma unroll
-    for (int q = 0; q <= N; ++q) y[q] = fma(dk[l], vsh[l * NC + q], y[q]);
-#pragma unroll
-  for (int q = 0; q <= N; ++q) {
-    h[q] = q < N ? vk[q] : wk;
-    ysh[k * NC + q] = y[q];
+  for (int j = 0; j < N - 2; ++j) {  // other axes: M_kl = Ma_kl = 0 exactly
+    int l = k0 + 2 + j;
+    l = l >= N ? l - N : l;
+    const double d = __ldg(Dk + l);
+    const double p1 = __dmul_rn(a, d);
+    const double e1 = __fma_rn(a, d, -p1);
+    dsh[k * N + l] = static_cast<float>(__fma_rn(a, __ldg(Ek + l), -e1));
   }
   __syncwarp();
-  for (int p = 1; p <= P; ++p) {
-    const double sg = (p & 1) ? -1.0 : 1.0;
-    // row k of the order-p term: sum_j V_jk Y_j,:   (A0^-1 symmetric)
-    double t[NC];
+  // order 1: y_k = Delta_k,: [V | w]
+  float y[NC];
 #pragma unroll
-    for (int q = 0; q <= N; ++q) t[q] = 0.0;
+  for (int q = 0; q <= N; ++q) y[q] = 0.f;
+#pragma unroll
+  for (int l = 0; l < N; ++l) {
+    const float dl = dsh[k * N + l];
+#pragma unroll
+    for (int q = 0; q <= N; ++q) y[q] = fmaf(dl, vsh[l * NC + q], y[q]);
+  }
+#pragma unroll
+  for (int q = 0; q <= N; ++q) ysh[k * NC + q] = y[q];
+  float vk32[N];
+#pragma unroll
+  for (int j = 0; j < N; ++j) vk32[j] = static_cast<float>(vk[j]);
+  __syncwarp();
+  float corr[NC];
+#pragma unroll
+  for (int q = 0; q <= N; ++q) corr[q] = 0.f;
+  for (int p = 1; p <= P; ++p) {
+    const float sg = (p & 1) ? 1.f : -1.f;  // corr is subtracted: order p enters as (-1)^p
+    float t[NC];
+#pragma unroll
+    for (int q = 0; q <= N; ++q) t[q] = 0.f;
 #pragma unroll
     for (int j = 0; j < N; ++j)
 #pragma unroll
-      for (int q = 0; q <= N; ++q) t[q] = fma(vk[j], ysh[j * NC + q], t[q]);
+      for (int q = 0; q <= N; ++q) t[q] = fmaf(vk32[j], ysh[j * NC + q], t[q]);
 #pragma unroll
-    for (int q = 0; q <= N; ++q) h[q] = fma(sg, t[q], h[q]);
+    for (int q = 0; q <= N; ++q) corr[q] = fmaf(sg, t[q], corr[q]);
+    if (p == 1) {
+      // a-posteriori order control (as kern_warp.cu): 10 (|C| / |H0|)^2 <= 1e-12 -> order 1 suffices
+      float cm = 0.f, hm = 0.f;
+#pragma unroll
+      for (int q = 0; q < N; ++q) {
+        cm = fmaxf(cm, fabsf(corr[q]));
+        hm = fmaxf(hm, fabsf(vk32[q]));
+      }
+      const int lane = threadIdx.x & 31, base = lane - k;
+#pragma unroll
+      for (int j = 0; j < N; ++j) {
+        cm = fmaxf(cm, __shfl_sync(0xffffffffu, cm, base + j));
+        hm = fmaxf(hm, __shfl_sync(0xffffffffu, hm, base + j));
+      }
+      const double ratio = hm > 0.f ? static_cast<double>(cm) / hm : 0.0;
+      int pc = 1;
+      double tt = ratio * ratio * 10.0;
+      while (tt > 1e-12 && pc < A.p_max) {
+        ++pc;
+        tt *= ratio;
+      }
+      if (!real) pc = 1;
+      else if (!(ratio < 0.25) && k == 0) atomicOr(A.status, 1);
+      P = __reduce_max_sync(0xffffffffu, pc);
+    }
     if (p == P) break;
-    // T = A0^-1 Y (row k is exactly t), then Y <- Delta T
 #pragma unroll
     for (int q = 0; q <= N; ++q) tsh[k * NC + q] = t[q];
     __syncwarp();
 #pragma unroll
-    for (int q = 0; q <= N; ++q) y[q] = 0.0;
+    for (int q = 0; q <= N; ++q) y[q] = 0.f;
 #pragma unroll
-    for (int l = 0; l < N; ++l)
+    for (int l = 0; l < N; ++l) {
+      const float dl = dsh[k * N + l];
 #pragma unroll
-      for (int q = 0; q <= N; ++q) y[q] = fma(dk[l], tsh[l * NC + q], y[q]);
+      for (int q = 0; q <= N; ++q) y[q] = fmaf(dl, tsh[l * NC + q], y[q]);
+    }
     __syncwarp();
 #pragma unroll
     for (int q = 0; q <= N; ++q) ysh[k * NC + q] = y[q];
     __syncwarp();
   }
+#pragma unroll
+  for (int q = 0; q <= N; ++q) h[q] = (q < N ? vk[q] : wk) - static_cast<double>(corr[q]);
 }
 
 // Column ranks of a deep-interior cell's row k (every face of the cell and of
@@ -338,9 +387,10 @@ __global__ void __launch_bounds__(128, HDR_ROWS_MINB) k_rt0_rows(HybArgs A, Rt0C
   constexpr int NC = N + 1;
   constexpr int G = 32 / N;  // cells per warp
   constexpr int W = 4;       // warps per block
-  __shared__ double vbuf[W][G][N * NC];
-  __shared__ double ybuf[W][G][N * NC];
-  __shared__ double tbuf[W][G][N * NC];
+  __shared__ float vbuf[W][G + 1][N * NC];  // group G: scratch of the spare lanes
+  __shared__ float ybuf[W][G + 1][N * NC];
+  __shared__ float tbuf[W][G + 1][N * NC];
+  __shared__ float dbuf[W][G + 1][N * N];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int grp = lane / N, k = lane - grp * N;
   const uint32_t t = (blockIdx.x * W + warp) * G + grp;
@@ -348,24 +398,14 @@ __global__ void __launch_bounds__(128, HDR_ROWS_MINB) k_rt0_rows(HybArgs A, Rt0C
   int e = -1;
   if (grp < G && t < static_cast<uint32_t>(parity_count(A.m))) e = parity_cell32(A.m, PASS, t, cc);
   const bool valid = e >= 0;
-  // spare lanes shadow cell 0 so the warp stays convergent through the barriers
-  const int gi = grp < G ? grp : 0;
-  const int kk = grp < G ? k : 0;
+  // spare lanes compute on cell 0 in their own scratch group (results discarded)
+  // so every lane takes part in the warp barriers, shuffles and reductions
+  const int gi = grp < G ? grp : G;
+  const int kk = k;
   const int ee = valid ? e : 0;
-  int P = valid ? neumann_order(c.rho * A.alpha[ee] / A.beta[ee], A.p_max, A.status) : 1;
-  P = __reduce_max_sync(0xffffffffu, P);
-  double h[NC];
-  if (grp < G) {
-    rt0_row_math<DIM>(A, c, ee, kk, P, vbuf[warp][gi], ybuf[warp][gi], tbuf[warp][gi], h);
-  } else {  // spare lanes: same barrier sequence as the groups
-    __syncwarp();
-    __syncwarp();
-    for (int p = 1; p < P; ++p) {
-      __syncwarp();
-      __syncwarp();
-      __syncwarp();
-    }
-  }
+  int P = 1;
+  double h[N + 1];
+  rt0_row_math<DIM>(A, c, ee, kk, P, valid, vbuf[warp][gi], ybuf[warp][gi], tbuf[warp][gi], dbuf[warp][gi], h);
   if (!valid) return;
   if (PASS == 0) {
     double* slot = stage + static_cast<int64_t>(t) * (N * NC) + k * NC;
