@@ -92,6 +92,7 @@ struct hdr_space_s {
   DBuf<int32_t> col_h, col_s;
   DBuf<double> fixed;  // D, M, E, Ma, N0 (n*n each), X (n*r), lam (r)
   std::vector<double> rt0_consts;  // packed constant block of the k = 0 kernel
+  DBuf<uint64_t> rank_tab;         // k = 0 row-rank table
   Fixed fx{};
   ~hdr_space_s() {
     if (own_stream && stream) cudaStreamDestroy(stream);
@@ -345,6 +346,9 @@ hdr_status hdr_space_create(int dim, const int64_t cells[3], const double h[3], 
     if (order == 0) {  // constant block for the register kernel: D, M, E, Ma, N0, X, lam, rho
       sp->rt0_consts.assign(pack.begin(), pack.begin() + 5 * nn + n + 1);
       sp->rt0_consts.push_back(sp->st.rho);
+      const std::vector<uint64_t> tab = rank_table_rt0(dim);
+      sp->rank_tab.alloc(tab.size());
+      CK(cudaMemcpyAsync(sp->rank_tab.p, tab.data(), tab.size() * 8, cudaMemcpyHostToDevice, st));
     }
     CK(cudaStreamSynchronize(st));
     CK(cudaGetLastError());
@@ -493,6 +497,7 @@ static hdr_status run_hybridize(hdr_hybrid_t op, const double* alpha, const doub
     A.hval = op->hval.p;
     A.g = op->g.p;
     A.status = op->status.p;
+    A.rank_tab = sp->rank_tab.p;
     if (sp->k == 0) {
       static const bool legacy = getenv("HDR_RT0_LEGACY") != nullptr;
       if (legacy) {

@@ -175,18 +175,16 @@ struct CellFlags {
   bool far_lo, far_hi;  // c_a >= 2 / c_a + 2 < N_a: neighbour's far a-face interior
 };
 
-__host__ __device__ constexpr int col_rank_fast(int dim, int p, int q, unsigned lo, unsigned hi, int64_t ca, int64_t na,
-                                             bool all_faces) {
-  // lo / hi: bit x set iff the cell's -x / +x face is interior
+// Column rank from boundary flags only: lo / hi (bit x set iff the cell's -x / +x
+// face is interior), own_p_in (slot p's face interior), far (the face beyond the
+// neighbour across p interior).
+__host__ __device__ constexpr int col_rank_flags(int p, int q, unsigned L, unsigned H, int own_p_in, int far) {
   const int a = p >> 1, sp = p & 1, b = q >> 1, sq = q & 1;
-  const int own_p_in = sp ? (ca + 1 < na) : (ca > 0);
-  const unsigned L = all_faces ? 7u : lo, H = all_faces ? 7u : hi;
   if (!own_p_in) {  // boundary row (S only): this cell's faces in slot order
     int r = 0;
     for (int u = 0; u < q; ++u) r += ((u & 1) ? (H >> (u >> 1)) : (L >> (u >> 1))) & 1u;
     return r;
   }
-  const int far = all_faces ? 1 : (sp ? (ca + 2 < na) : (ca >= 2));
   const int La = (L >> a) & 1u, Ha = (H >> a) & 1u, Lb = (L >> b) & 1u, Hb = (H >> b) & 1u;
   int r = 0;
   for (int x = 0; x < b; ++x)
@@ -200,8 +198,17 @@ __host__ __device__ constexpr int col_rank_fast(int dim, int p, int q, unsigned 
     if (a < b) r += sq ? 2 * Lb + Hb : Lb;
     else r += sq ? 2 * Lb + Hb : Lb + Hb;
   }
-  (void)dim;
   return r;
+}
+
+__host__ __device__ constexpr int col_rank_fast(int dim, int p, int q, unsigned lo, unsigned hi, int64_t ca, int64_t na,
+                                             bool all_faces) {
+  const int sp = p & 1;
+  const int own_p_in = sp ? (ca + 1 < na) : (ca > 0);
+  const unsigned L = all_faces ? 7u : lo, H = all_faces ? 7u : hi;
+  const int far = all_faces ? 1 : (sp ? (ca + 2 < na) : (ca >= 2));
+  (void)dim;
+  return col_rank_flags(p, q, L, H, own_p_in, far);
 }
 
 // ------------------------------------------------------------ error-free transforms

@@ -358,29 +358,6 @@ __device__ __forceinline__ void rt0_row_math(const HybArgs& A, const Rt0Const<2 
   for (int q = 0; q <= N; ++q) h[q] = (q < N ? vk[q] : wk) - static_cast<double>(corr[q]);
 }
 
-// Column ranks of a deep-interior cell's row k (every face of the cell and of
-// its neighbour across k interior): own slot q -> bits [4q, 4q+4), neighbour
-// slot q -> bits [4(N+q), ...).  Built at compile time from col_rank_fast.
-template <int DIM>
-constexpr uint64_t deep_ranks(int k) {
-  constexpr int N = 2 * DIM;
-  const unsigned all = (1u << DIM) - 1u;
-  uint64_t packed = 0;
-  for (int q = 0; q < N; ++q) {
-    packed |= static_cast<uint64_t>(col_rank_fast(DIM, k, q, all, all, 4, 9, false)) << (4 * q);
-    packed |= static_cast<uint64_t>(col_rank_fast(DIM, k ^ 1, q, all, all, 4, 9, false)) << (4 * (N + q));
-  }
-  return packed;
-}
-
-template <int DIM>
-__device__ __forceinline__ uint64_t deep_ranks_of(int k) {
-  uint64_t r = deep_ranks<DIM>(0);
-#pragma unroll
-  for (int j = 1; j < 2 * DIM; ++j) r = (k == j) ? deep_ranks<DIM>(j) : r;
-  return r;
-}
-
 template <int DIM, int PASS>
 __global__ void __launch_bounds__(128, HDR_ROWS_MINB) k_rt0_rows(HybArgs A, Rt0Const<2 * DIM> c, double* stage) {
   constexpr int N = 2 * DIM;
@@ -432,30 +409,35 @@ __global__ void __launch_bounds__(128, HDR_ROWS_MINB) k_rt0_rows(HybArgs A, Rt0C
   const int face = face_id32(A.m, a, cc[0] + (a == 0 ? side : 0), cc[1] + (a == 1 ? side : 0), cc[2] + (a == 2 ? side : 0));
   const int row = A.mbase[face];
   const int64_t start = A.rowoff[row];
-  unsigned lo = 0, hi = 0, nlo = 0, nhi = 0;
+  // boundary flags of the cell (own faces) and the neighbour's far face along k's axis
+  unsigned lo = 0, hi = 0;
 #pragma unroll
   for (int x = 0; x < DIM; ++x) {
     const int cx = x == 0 ? cc[0] : (x == 1 ? cc[1] : cc[2]);
-    const int nx = x == 0 ? nc[0] : (x == 1 ? nc[1] : nc[2]);
     const int Nx = static_cast<int>(x == 0 ? A.m.N[0] : (x == 1 ? A.m.N[1] : A.m.N[2]));
     lo |= static_cast<unsigned>(cx > 0) << x;
     hi |= static_cast<unsigned>(cx + 1 < Nx) << x;
-    nlo |= static_cast<unsigned>(nx > 0) << x;
-    nhi |= static_cast<unsigned>(nx + 1 < Nx) << x;
   }
-  const int nca = a == 0 ? nc[0] : (a == 1 ? nc[1] : nc[2]);
+  const unsigned far = side ? static_cast<unsigned>(ca + 2 < na) : static_cast<unsigned>(ca >= 2);
+  const unsigned flags = lo | (hi << DIM) | (far << (2 * DIM));
+  // packed column ranks of this row (host-built table, rank_table_rt0): own slot q
+  // -> bits 4q, neighbour slot q -> bits 4(N+q); 15 = absent
+  const uint64_t* tab = A.rank_tab + (static_cast<size_t>(k) << (2 * DIM + 1)) * 2 + flags * 2;
+  const uint64_t own = __ldg(tab), nbr = __ldg(tab + 1);
   double* out = A.hval + start;
 #pragma unroll
   for (int q = 0; q < N; ++q) {
-    if (!((((q & 1) ? hi : lo) >> (q >> 1)) & 1u)) continue;
+    const unsigned r = static_cast<unsigned>(own >> (4 * q)) & 15u;
+    if (r == 15u) continue;
     double v = h[q];
     if (q == k) v = v + nrow_p[kn];
-    out[col_rank_fast(DIM, k, q, lo, hi, ca, na, false)] = v;
+    out[r] = v;
   }
 #pragma unroll
   for (int q = 0; q < N; ++q) {
-    if (q == kn || !((((q & 1) ? nhi : nlo) >> (q >> 1)) & 1u)) continue;
-    out[col_rank_fast(DIM, kn, q, nlo, nhi, nca, na, false)] = nrow[q];
+    const unsigned r = static_cast<unsigned>(nbr >> (4 * q)) & 15u;
+    if (r == 15u) continue;
+    out[r] = nrow[q];
   }
   A.g[row] = h[N] + nrow[N];
 }

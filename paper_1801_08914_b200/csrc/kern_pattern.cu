@@ -132,3 +132,49 @@ void launch_fill_patterns(const DevMesh& m, const int* mbase, const int64_t* fba
 }
 
 }  // namespace hdr
+
+namespace hdr {
+
+std::vector<uint64_t> rank_table_rt0(int dim) {
+  const int N = 2 * dim, nflags = 1 << (2 * dim + 1);
+  std::vector<uint64_t> tab(static_cast<size_t>(N) * nflags * 2, 0);
+  for (int k = 0; k < N; ++k)
+    for (int flags = 0; flags < nflags; ++flags) {
+      const unsigned all = (1u << dim) - 1u;
+      const unsigned lo = flags & all, hi = (flags >> dim) & all, far = (flags >> (2 * dim)) & 1u;
+      const int a = k >> 1, side = k & 1;
+      uint64_t own = ~uint64_t(0), nbr = ~uint64_t(0);
+      const bool kin = side ? ((hi >> a) & 1u) : ((lo >> a) & 1u);
+      if (kin) {
+        // neighbour across k: same flags off axis a; along a its face k^1 is the
+        // shared (interior) face and its face k is the far face
+        unsigned nlo = lo, nhi = hi;
+        if (side) {
+          nlo |= (1u << a);
+          nhi = (nhi & ~(1u << a)) | (far << a);
+        } else {
+          nhi |= (1u << a);
+          nlo = (nlo & ~(1u << a)) | (far << a);
+        }
+        // the face beyond our cell, seen from the neighbour, is our face k^1
+        const int nfar = side ? static_cast<int>((lo >> a) & 1u) : static_cast<int>((hi >> a) & 1u);
+        for (int q = 0; q < N; ++q) {
+          const bool qin = (q & 1) ? ((hi >> (q >> 1)) & 1u) : ((lo >> (q >> 1)) & 1u);
+          if (qin) {
+            const uint64_t r = static_cast<uint64_t>(col_rank_flags(k, q, lo, hi, 1, static_cast<int>(far)));
+            own = (own & ~(uint64_t(15) << (4 * q))) | (r << (4 * q));
+          }
+          const bool nin = (q & 1) ? ((nhi >> (q >> 1)) & 1u) : ((nlo >> (q >> 1)) & 1u);
+          if (nin && q != (k ^ 1)) {
+            const uint64_t r = static_cast<uint64_t>(col_rank_flags(k ^ 1, q, nlo, nhi, 1, nfar));
+            nbr = (nbr & ~(uint64_t(15) << (4 * q))) | (r << (4 * q));
+          }
+        }
+      }
+      tab[(static_cast<size_t>(k) * nflags + flags) * 2] = own;
+      tab[(static_cast<size_t>(k) * nflags + flags) * 2 + 1] = nbr;
+    }
+  return tab;
+}
+
+}  // namespace hdr

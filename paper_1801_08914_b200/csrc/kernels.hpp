@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cstdint>
+#include <vector>
 
 #include <cuda_runtime.h>
 
@@ -37,7 +38,13 @@ struct HybArgs {
   double* hval;  // H values (pattern order)
   double* g;     // reduced rhs (m)
   int* status;   // device flag: bit 0 = Neumann ratio out of range
+  const uint64_t* rank_tab;  // k = 0 row-rank table (rank_table_rt0)
 };
+
+// Row-rank table of the k = 0 kernel: for row slot k and boundary flags
+// (own lo bits | own hi bits << dim | neighbour far face << 2 dim), two words of
+// 4-bit column ranks (own slots, then the neighbour's slots; 15 = absent).
+std::vector<uint64_t> rank_table_rt0(int dim);
 
 // Small-element path (k = 0): one thread per cell, everything in registers.
 void launch_hybridize_rt0(const HybArgs& a, const double* host_consts, int parity, cudaStream_t st);
