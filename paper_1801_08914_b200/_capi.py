@@ -10,7 +10,8 @@ import ctypes
 import os
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "libhdivred_b200.so"
+# HDR_LIB: an alternative build of the same library (kernel-variant experiments)
+LIB_PATH = Path(os.environ.get("HDR_LIB") or Path(__file__).resolve().parent / "libhdivred_b200.so")
 
 # status codes (hdr_status)
 OK, SINGULAR_BLOCK, DIMENSION_MISMATCH, VALIDATION, UNSUPPORTED, CUDA_ERROR, INVALID_ARGUMENT = range(7)

@@ -211,6 +211,29 @@ __host__ __device__ constexpr int col_rank_fast(int dim, int p, int q, unsigned 
   return col_rank_flags(p, q, L, H, own_p_in, far);
 }
 
+// ------------------------------------------------------------ L2 eviction-priority hints
+// A staged intermediate that is read back by the next launch is stored evict_last
+// so the streaming output written in between does not push it out of L2; the
+// streaming output itself is stored evict_first.
+__device__ __forceinline__ uint64_t l2_policy_evict_last() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void st_l2hint(double* a, double v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(a), "d"(v), "l"(pol) : "memory");
+}
+__device__ __forceinline__ double ld_l2hint(const double* a, uint64_t pol) {
+  double v;
+  asm volatile("ld.global.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(a), "l"(pol));
+  return v;
+}
+
 // ------------------------------------------------------------ error-free transforms
 
 __device__ __forceinline__ void two_prod(double a, double b, double& p, double& e) {

@@ -26,6 +26,9 @@
 #include "hdr_device.cuh"
 #include "kernels.hpp"
 
+#ifndef HDR_L2HINT
+#define HDR_L2HINT 1
+#endif
 #ifndef HDR_ROWS_MINB
 #define HDR_ROWS_MINB 6
 #endif
@@ -386,8 +389,14 @@ __global__ void __launch_bounds__(128, HDR_ROWS_MINB) k_rt0_rows(HybArgs A, Rt0C
   if (!valid) return;
   if (PASS == 0) {
     double* slot = stage + static_cast<int64_t>(t) * (N * NC) + k * NC;
+    if (HDR_L2HINT >= 1) {
+      const uint64_t pol = l2_policy_evict_last();
 #pragma unroll
-    for (int q = 0; q <= N; ++q) slot[q] = h[q];
+      for (int q = 0; q <= N; ++q) st_l2hint(slot + q, h[q], pol);
+    } else {
+#pragma unroll
+      for (int q = 0; q <= N; ++q) slot[q] = h[q];
+    }
     return;
   }
   // pass 1: complete rows of this cell's interior faces
@@ -404,8 +413,9 @@ __global__ void __launch_bounds__(128, HDR_ROWS_MINB) k_rt0_rows(HybArgs A, Rt0C
   const uint32_t tn = (static_cast<uint32_t>(nc[1]) + static_cast<uint32_t>(A.m.N[1]) * nc[2]) * half + (nc[0] >> 1);
   const double* nrow_p = stage + static_cast<int64_t>(tn) * (N * NC) + kn * NC;
   double nrow[NC];
+  const uint64_t pol_first = l2_policy_evict_first();
 #pragma unroll
-  for (int q = 0; q <= N; ++q) nrow[q] = nrow_p[q];
+  for (int q = 0; q <= N; ++q) nrow[q] = HDR_L2HINT >= 2 ? ld_l2hint(nrow_p + q, pol_first) : nrow_p[q];
   const int face = face_id32(A.m, a, cc[0] + (a == 0 ? side : 0), cc[1] + (a == 1 ? side : 0), cc[2] + (a == 2 ? side : 0));
   const int row = A.mbase[face];
   const int64_t start = A.rowoff[row];
@@ -431,13 +441,15 @@ __global__ void __launch_bounds__(128, HDR_ROWS_MINB) k_rt0_rows(HybArgs A, Rt0C
     if (r == 15u) continue;
     double v = h[q];
     if (q == k) v = v + nrow_p[kn];
-    out[r] = v;
+    if (HDR_L2HINT >= 1) st_l2hint(out + r, v, pol_first);
+    else out[r] = v;
   }
 #pragma unroll
   for (int q = 0; q < N; ++q) {
     const unsigned r = static_cast<unsigned>(nbr >> (4 * q)) & 15u;
     if (r == 15u) continue;
-    out[r] = nrow[q];
+    if (HDR_L2HINT >= 1) st_l2hint(out + r, nrow[q], pol_first);
+    else out[r] = nrow[q];
   }
   A.g[row] = h[N] + nrow[N];
 }
