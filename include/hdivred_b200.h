@@ -127,6 +127,8 @@ hdr_status hdr_hybridize_fe_enqueue(hdr_hybrid_t op, const double* alpha, const 
                                     int on_device);
 /* Synchronizes the stream and reports device-side status of enqueued work. */
 hdr_status hdr_hybrid_check(hdr_hybrid_t op);
+/* In-place symmetrization of the operator's H values (see hdr_alg_symmetrize). */
+hdr_status hdr_hybrid_symmetrize(hdr_hybrid_t op);
 void hdr_hybrid_destroy(hdr_hybrid_t op);
 /* Copy H values (nnz_H, in the space's pattern order) and/or g (m); NULL
  * skips.  dst_on_device selects device-to-device copies. */
@@ -172,6 +174,77 @@ hdr_status hdr_csr_spmv_host(int64_t nrows, int64_t ncols, const int64_t* row_of
 /* General CSR SpMV on device arrays (int64 offsets, int64 columns). */
 hdr_status hdr_csr_spmv_device(int64_t nrows, const int64_t* row_offsets, const int64_t* col_indices,
                                const double* values, const double* x, double* y, void* stream);
+
+/* ------------------------------------------- algebraic batch (ReductionInputs)
+ *
+ * Drop-in for the reference's algebraic entry points on a general
+ * ReductionInputs (include/hdivred/reduction.hpp:16-33): arbitrary square dense
+ * element blocks (ElementBlockOperator, block_operator.hpp:22-38), P (n_hat x n)
+ * and C (m x n_hat) as CSR, f_hat, interior_global_begin.  Arrays are host
+ * memory, caller-owned, read during the call only.  The handle keeps what the
+ * recoveries need on the device.
+ *   hdr_alg_hybridize        <- hybridize(const ReductionInputs&)        reduction.hpp:70, reduction.cpp:262-354
+ *   hdr_alg_recover_hybrid   <- recover_hybrid(op, lambda, f_hat)        reduction.hpp:73-75, reduction.cpp:356-446
+ *   hdr_alg_static_condense  <- static_condense(const ReductionInputs&)  reduction.hpp:97, reduction.cpp:448-557
+ *   hdr_alg_recover_condensed<- recover_condensed(op, x_b, f_hat)        reduction.hpp:101-102, reduction.cpp:559-587
+ * Errors: HDR_DIMENSION_MISMATCH (inconsistent sizes, as the reference's
+ * DimensionMismatch), HDR_VALIDATION (P column empty; interior dof not mapped
+ * to a single global), HDR_SINGULAR_BLOCK (A_ii or S_b pivot <= 1e-14 max|block|;
+ * hdr_last_error names the element). */
+typedef struct hdr_alg_inputs {
+  int64_t nblocks;
+  const int64_t* block_sizes;   /* n_e of each block (dof_map.size()) */
+  const double* blocks;         /* row-major blocks, concatenated in block order */
+  const int64_t* dof_global;    /* n_hat: dof_map[l].global, block order; needed when interior_global_begin >= 0 */
+  int64_t p_nrows, p_ncols;
+  const int64_t* p_row_offsets; /* CsrMatrix p_mat */
+  const int64_t* p_col_indices;
+  const double* p_values;
+  int64_t c_nrows, c_ncols;
+  const int64_t* c_row_offsets; /* CsrMatrix c_mat */
+  const int64_t* c_col_indices;
+  const double* c_values;
+  int64_t f_len;
+  const double* f_hat;
+  int64_t interior_global_begin; /* -1: algebraic partition (zero columns of C) */
+} hdr_alg_inputs;
+
+typedef struct hdr_alg_s* hdr_alg_t;
+
+enum {
+  HDR_ALG_NROWS = 0,      /* m (hybrid) or n_master (condensed) */
+  HDR_ALG_NNZ,            /* nnz of h_mat / s_mat */
+  HDR_ALG_N_HAT,
+  HDR_ALG_N_GLOBAL,
+  HDR_ALG_DIAGONAL_GRAM,  /* HybridizedOperator::diagonal_gram */
+  HDR_ALG_KIND,           /* 0 hybrid, 1 condensed */
+  HDR_ALG_INFO_COUNT
+};
+
+hdr_status hdr_alg_hybridize(const hdr_alg_inputs* inputs, hdr_alg_t* out);
+hdr_status hdr_alg_static_condense(const hdr_alg_inputs* inputs, hdr_alg_t* out);
+/* out[HDR_ALG_INFO_COUNT] */
+hdr_status hdr_alg_info(hdr_alg_t op, int64_t* out);
+/* The reduced CSR matrix (h_mat / s_mat: row_offsets nrows+1, col_indices nnz,
+ * values nnz) and right-hand side (g / f_s); NULL skips. */
+hdr_status hdr_alg_matrix(hdr_alg_t op, int64_t* row_offsets, int64_t* col_indices, double* values, double* rhs);
+/* Condensed: CondensedOperator::master_globals (nrows). */
+hdr_status hdr_alg_master_globals(hdr_alg_t op, int64_t* out);
+/* Hybrid: HybridizedOperator::recovery_scale = 1 / diag(P^T P) (n_global). */
+hdr_status hdr_alg_recovery_scale(hdr_alg_t op, double* out);
+/* x_hat (n_hat) and x (n_global); either may be NULL. */
+hdr_status hdr_alg_recover_hybrid(hdr_alg_t op, const double* lambda, int64_t lambda_len, const double* f_hat,
+                                  int64_t f_len, double* x_hat, double* x);
+/* x (n_global) */
+hdr_status hdr_alg_recover_condensed(hdr_alg_t op, const double* x_b, int64_t xb_len, const double* f_hat,
+                                     int64_t f_len, double* x);
+void hdr_alg_destroy(hdr_alg_t op);
+/* In-place a_ij = a_ji = 0.5 (a_ij + a_ji) of h_mat / s_mat: the reference's
+ * symmetrize of H_e / S_hat (reduction.cpp:65-72, 295, 316, 489) applied to the
+ * assembled matrix, for consumers that require exact symmetry (its pcg checks
+ * |A - A^T| <= 1e-10 max|A|, solvers.cpp:25-30).  The default output is the
+ * unsymmetrized element-exact value the parity contract is stated on. */
+hdr_status hdr_alg_symmetrize(hdr_alg_t op);
 
 /* ------------------------------------------------- host-only introspection */
 

@@ -513,8 +513,10 @@ def launch_count() -> int:
     return int(_lib().hdr_launch_count())
 
 
+from . import algebraic  # noqa: E402  (ReductionInputs-level API; needs _check/_lib above)
+
 __all__ = [
-    "CapExceededError", "FormatError", "SingularBlockError", "ValidationError", "DimensionMismatch",
+    "algebraic", "CapExceededError", "FormatError", "SingularBlockError", "ValidationError", "DimensionMismatch",
     "UnsupportedError", "DeviceError", "Space", "HybridizedOperator", "CondensedOperator", "hybridized_matrix",
     "space_info", "coefficients_from_config", "space_from_config", "launch_count", "__version__",
 ]

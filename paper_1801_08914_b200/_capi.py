@@ -22,6 +22,19 @@ INFO_NAMES = ["dim", "order", "ncells", "nfaces", "ndofs", "broken_ndofs", "elem
 
 _vp, _i32, _i64, _d = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_double
 
+class AlgInputs(ctypes.Structure):
+    """hdr_alg_inputs (include/hdivred_b200.h): a ReductionInputs as plain arrays."""
+    _fields_ = [
+        ("nblocks", _i64), ("block_sizes", _vp), ("blocks", _vp), ("dof_global", _vp),
+        ("p_nrows", _i64), ("p_ncols", _i64), ("p_row_offsets", _vp), ("p_col_indices", _vp), ("p_values", _vp),
+        ("c_nrows", _i64), ("c_ncols", _i64), ("c_row_offsets", _vp), ("c_col_indices", _vp), ("c_values", _vp),
+        ("f_len", _i64), ("f_hat", _vp), ("interior_global_begin", _i64),
+    ]
+
+
+# hdr_alg_info indices
+ALG_INFO_NAMES = ["nrows", "nnz", "n_hat", "n_global", "diagonal_gram", "kind"]
+
 _SIGS = {
     "hdr_space_create": (_i32, [_i32, _vp, _vp, _i32, _vp, _vp, _i32, _vp, _vp]),
     "hdr_space_destroy": (None, [_vp]),
@@ -54,6 +67,17 @@ _SIGS = {
     "hdr_csr_spmv_host": (_i32, [_i64, _i64, _vp, _vp, _vp, _vp, _vp]),
     "hdr_reference_element": (_i32, [_i32, _i32, _vp, _vp, _vp, _vp, _vp]),
     "hdr_structured_factors": (_i32, [_i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "hdr_alg_hybridize": (_i32, [_vp, _vp]),
+    "hdr_alg_static_condense": (_i32, [_vp, _vp]),
+    "hdr_alg_info": (_i32, [_vp, _vp]),
+    "hdr_alg_matrix": (_i32, [_vp, _vp, _vp, _vp, _vp]),
+    "hdr_alg_master_globals": (_i32, [_vp, _vp]),
+    "hdr_alg_recovery_scale": (_i32, [_vp, _vp]),
+    "hdr_alg_recover_hybrid": (_i32, [_vp, _vp, _i64, _vp, _i64, _vp, _vp]),
+    "hdr_alg_recover_condensed": (_i32, [_vp, _vp, _i64, _vp, _i64, _vp]),
+    "hdr_alg_destroy": (None, [_vp]),
+    "hdr_alg_symmetrize": (_i32, [_vp]),
+    "hdr_hybrid_symmetrize": (_i32, [_vp]),
     "hdr_last_error": (ctypes.c_char_p, []),
     "hdr_version": (ctypes.c_char_p, []),
     "hdr_launch_count": (_i64, []),

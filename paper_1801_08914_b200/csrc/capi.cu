@@ -20,6 +20,7 @@
 #include <cub/cub.cuh>
 
 #include "../../include/hdivred_b200.h"
+#include "capi_util.hpp"
 #include "hdr_internal.hpp"
 #include "kernels.hpp"
 
@@ -28,49 +29,11 @@ namespace hdr {
 static std::atomic<int64_t> g_launches{0};
 void count_launch(int64_t k) { g_launches += k; }
 
-namespace {
-
-thread_local std::string g_err;
-
-hdr_status fail(hdr_status s, const std::string& msg) {
-  g_err = msg;
+std::string& last_error_ref() {
+  thread_local std::string s;
   return s;
 }
 
-struct CudaError : std::exception {
-  cudaError_t e;
-  std::string where;
-  CudaError(cudaError_t err, const char* w) : e(err), where(w) {}
-};
-
-#define CK(call)                                    \
-  do {                                              \
-    cudaError_t _e = (call);                        \
-    if (_e != cudaSuccess) throw CudaError(_e, #call); \
-  } while (0)
-
-template <class T>
-struct DBuf {  // owning device buffer
-  T* p = nullptr;
-  size_t n = 0;
-  DBuf() = default;
-  DBuf(const DBuf&) = delete;
-  DBuf& operator=(const DBuf&) = delete;
-  ~DBuf() { reset(); }
-  void reset() {
-    if (p) cudaFree(p);
-    p = nullptr;
-    n = 0;
-  }
-  void alloc(size_t count) {
-    reset();
-    if (count == 0) count = 1;
-    CK(cudaMalloc(&p, count * sizeof(T)));
-    n = count;
-  }
-};
-
-}  // namespace
 }  // namespace hdr
 
 using namespace hdr;
@@ -125,18 +88,6 @@ int64_t ipow(int64_t b, int e) {
   return r;
 }
 
-hdr_status catch_all(const std::function<hdr_status()>& fn) {
-  try {
-    return fn();
-  } catch (const CudaError& e) {
-    return fail(HDR_CUDA_ERROR, std::string("CUDA error in ") + e.where + ": " + cudaGetErrorString(e.e));
-  } catch (const std::bad_alloc&) {
-    return fail(HDR_CUDA_ERROR, "host allocation failed");
-  } catch (const std::exception& e) {
-    return fail(HDR_UNSUPPORTED, e.what());
-  }
-}
-
 template <class T>
 void exclusive_scan(const T* in, T* out, int64_t count, cudaStream_t st) {
   size_t bytes = 0;
@@ -170,7 +121,7 @@ hdr_status check_status(int* d_status, cudaStream_t st) {
 
 extern "C" {
 
-const char* hdr_last_error(void) { return g_err.c_str(); }
+const char* hdr_last_error(void) { return last_error_ref().c_str(); }
 const char* hdr_version(void) { return "hdivred_b200 0.1.0 sm_100a"; }
 int64_t hdr_launch_count(void) { return g_launches.load(); }
 
@@ -566,6 +517,16 @@ hdr_status hdr_hybridize_fe_enqueue(hdr_hybrid_t op, const double* alpha, const 
 hdr_status hdr_hybrid_check(hdr_hybrid_t op) {
   if (!op) return fail(HDR_INVALID_ARGUMENT, "null operator");
   return catch_all([&]() -> hdr_status { return check_status(op->status.p, op->sp->stream); });
+}
+
+hdr_status hdr_hybrid_symmetrize(hdr_hybrid_t op) {
+  if (!op) return fail(HDR_INVALID_ARGUMENT, "null operator");
+  return catch_all([&]() -> hdr_status {
+    launch_csr_symmetrize32(op->sp->m, op->sp->row_h.p, op->sp->col_h.p, op->hval.p, op->sp->stream);
+    CK(cudaStreamSynchronize(op->sp->stream));
+    CK(cudaGetLastError());
+    return HDR_OK;
+  });
 }
 
 hdr_status hdr_hybrid_values_enqueue(hdr_hybrid_t op, double* h_values, double* g, int dst_on_device) {

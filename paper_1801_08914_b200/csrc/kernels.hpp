@@ -99,4 +99,69 @@ void launch_spmv32(int64_t nrows, const int64_t* ro, const int32_t* ci, const do
 void launch_spmv64(int64_t nrows, const int64_t* ro, const int64_t* ci, const double* v, const double* x, double* y,
                    cudaStream_t st);
 
+
+// ---- algebraic batch path (kern_alg.cu): general ReductionInputs
+enum { ALG_HYB = 0, ALG_REC = 1, ALG_COND = 2, ALG_RECC = 3 };
+struct AlgArgs {
+  int64_t ne;                  // elements (blocks)
+  const int64_t* boff;         // ne + 1 broken offsets
+  const int64_t* aoff;         // ne block offsets into blocks (sum of n_e^2)
+  const double* blocks;        // row-major element blocks
+  const int* idx;              // per element: its n local dofs ordered [i | b] (at boff[e])
+  const int* ni;               // interior (unconstrained / marker) dof count per element
+  const double* f;             // f_hat (broken)
+  int* status;                 // bit 1: singular block
+  unsigned long long* bad_elem;  // smallest singular element id
+  // hybrid modes
+  int64_t m;                   // multiplier count
+  const int64_t* goff;         // ne + 1 offsets of each element's multiplier rows
+  const int64_t* mrows;        // sorted global multiplier rows per element
+  const int64_t* hoff;         // ne offsets of H_e (nr x nr) in hbuf
+  const int64_t* cptr;         // sum(nr) + 1: entry range of each (element, local row)
+  const int* cent_r;           // entry local row
+  const int* cent_a;           // entry local dof position in the [i | b] order
+  const double* cent_v;        // entry value (C)
+  double* hbuf;                // H_e blocks
+  double* gbuf;                // g_e blocks
+  const double* lambda;        // recover: multipliers
+  double* x_hat;               // recover: broken solution
+  // condense modes
+  int64_t n_master;
+  const int64_t* bdof_off;     // ne + 1 offsets of each element's b dofs (sum nb)
+  const int64_t* bm_ptr;       // sum(nb) + 1: P-row entries of each b dof
+  const int64_t* bm_ord;       // entry master ordinal
+  const double* bm_w;          // entry weight (P value)
+  const int* bm_loc;           // entry's local b dof j
+  const int64_t* soff;         // ne offsets of S_hat (nb x nb) in sbuf
+  double* sbuf;                // S_hat blocks
+  double* fsbuf;               // f_S blocks (sum nb)
+  const int64_t* ibase;        // ne offsets of the element's i dofs (sum ni)
+  const int64_t* i_global;     // global dof of each i dof
+  const double* i_sign;        // its P value
+  const double* xb;            // recover_condensed: master values
+  double* x;                   // recover_condensed: global solution
+};
+int64_t alg_ws_doubles(int d, int nc);
+bool alg_ws_in_smem(int64_t ws_doubles);
+void launch_alg(const AlgArgs& a, int mode, int64_t ws_doubles, double* gws, int grid, cudaStream_t st);
+void launch_alg_hkeys(const AlgArgs& a, uint64_t* hkeys, int64_t* hsrc, uint64_t* gkeys, int64_t* gsrc, cudaStream_t st);
+void launch_alg_skeys(const AlgArgs& a, const int64_t* trip_off, const int64_t* ftrip_off, uint64_t* skeys,
+                      int64_t* ssrc, double* sw, uint64_t* fkeys, int64_t* fsrc, double* fw, cudaStream_t st);
+void launch_run_heads(int64_t n, const uint64_t* keys, int* head, cudaStream_t st);
+void launch_run_csr(int64_t n, const uint64_t* keys, const int* head, const int* pos, int64_t ncols, int64_t* run_start,
+                    int64_t* cols, int64_t* row_cnt, cudaStream_t st);
+void launch_run_sum(int64_t nruns, const int64_t* run_start, const int64_t* src, const double* w, const double* buf,
+                    double* out, const int64_t* out_index, int from_zero, cudaStream_t st);
+void launch_row_sumsq(int64_t nrows, const int64_t* ro, const double* v, double* out, cudaStream_t st);
+// op 0: out = x * y; 1: out += a x; 2: out = x + a out; 3: out = 1 / x (0 stays 0)
+void launch_vec_op(int64_t n, int op, double a, const double* x, const double* y, double* out, cudaStream_t st);
+// deterministic dot product (part: 1024 doubles of scratch), result on the device
+void launch_gather_i64(int64_t n, const int64_t* pos, const int64_t* in, int64_t* out, cudaStream_t st);
+void launch_gather_f64(int64_t n, const int64_t* pos, const double* in, double* out, cudaStream_t st);
+void launch_scatter(int64_t n, const int64_t* index, const double* v, double* out, cudaStream_t st);
+void launch_iota(int64_t n, int64_t* out, cudaStream_t st);
+void launch_csr_symmetrize64(int64_t nrows, const int64_t* ro, const int64_t* ci, double* v, cudaStream_t st);
+void launch_csr_symmetrize32(int64_t nrows, const int64_t* ro, const int32_t* ci, double* v, cudaStream_t st);
+void launch_dot(int64_t n, const double* x, const double* y, double* part, double* out, cudaStream_t st);
+
 }  // namespace hdr
