@@ -282,6 +282,11 @@ class HybridizedOperator:
         dev = _same_device([h_out, g_out])
         _check(_lib().hdr_hybrid_values_enqueue(self._h, _ptr(h_out)[0], _ptr(g_out)[0], dev))
 
+    def symmetrize(self) -> None:
+        """In place H <- (H + H^T) / 2, the reference's symmetrize (reduction.cpp:316):
+        exactly symmetric H for consumers such as its pcg (solvers.cpp:25-30)."""
+        _check(_lib().hdr_hybrid_symmetrize(self._h))
+
     def check(self) -> None:
         _check(_lib().hdr_hybrid_check(self._h))
 

@@ -46,11 +46,52 @@ int main(int argc, char** argv) {
     ds = std::max(ds, std::fabs(cref.s_mat.values[i] - cgpu.s_mat.values[i]));
     ms = std::max(ms, std::fabs(cref.s_mat.values[i]));
   }
+  // algebraic drop-ins on the reference's own ReductionInputs
+  auto rel = [](const std::vector<double>& a, const std::vector<double>& b) {
+    double d = 0, m = 0;
+    for (size_t i = 0; i < a.size(); ++i) {
+      d = std::max(d, std::fabs(a[i] - b[i]));
+      m = std::max(m, std::fabs(a[i]));
+    }
+    return d / (m > 0 ? m : 1.0);
+  };
+  auto [ahyb, g_alg] = hdivred_b200::hybridize(in);
+  const bool apat = ref.h_mat.row_offsets == ahyb.op.h_mat.row_offsets &&
+                    ref.h_mat.col_indices == ahyb.op.h_mat.col_indices;
+  bool asym = true;
+  {
+    const CsrMatrix t = transpose(ahyb.op.h_mat);
+    asym = t.values == ahyb.op.h_mat.values && t.col_indices == ahyb.op.h_mat.col_indices;
+  }
+  std::vector<double> lam(g_ref.size());
+  for (auto& v : lam) {
+    s ^= s << 13; s ^= s >> 7; s ^= s << 17;
+    v = -1.0 + 2.0 * (static_cast<double>(s >> 11) * 0x1.0p-53);
+  }
+  auto [xh_ref, x_ref] = recover_hybrid(ref, lam, in.f_hat);
+  auto [xh_alg, x_alg] = hdivred_b200::recover_hybrid(ahyb, lam, in.f_hat);
+  auto [acond, fs_alg] = hdivred_b200::static_condense(in);
+  const bool acpat = cref.s_mat.row_offsets == acond.op.s_mat.row_offsets &&
+                     cref.s_mat.col_indices == acond.op.s_mat.col_indices &&
+                     cref.master_globals == acond.op.master_globals;
+  std::vector<double> xb(fs_ref.size());
+  for (auto& v : xb) {
+    s ^= s << 13; s ^= s >> 7; s ^= s << 17;
+    v = -1.0 + 2.0 * (static_cast<double>(s >> 11) * 0x1.0p-53);
+  }
+  const std::vector<double> xc_ref = recover_condensed(cref, xb, in.f_hat);
+  const std::vector<double> xc_alg = hdivred_b200::recover_condensed(acond, xb, in.f_hat);
   const std::vector<double> y_ref = spmv(ref.h_mat, g_ref);
   const std::vector<double> y_gpu = hdivred_b200::spmv(ref.h_mat, g_ref);
   std::printf("{\"n\": %d, \"k\": %d, \"h_pattern_identical\": %s, \"h_rel\": %.3e, \"g_rel\": %.3e, "
-              "\"s_pattern_identical\": %s, \"s_rel\": %.3e, \"spmv_identical\": %s}\n",
+              "\"s_pattern_identical\": %s, \"s_rel\": %.3e, \"spmv_identical\": %s, "
+              "\"alg_h_pattern_identical\": %s, \"alg_h_symmetric\": %s, \"alg_h_rel\": %.3e, \"alg_g_rel\": %.3e, "
+              "\"alg_x_hat_rel\": %.3e, \"alg_x_rel\": %.3e, \"alg_s_pattern_identical\": %s, \"alg_s_rel\": %.3e, "
+              "\"alg_f_s_rel\": %.3e, \"alg_x_cond_rel\": %.3e}\n",
               n, k, pattern ? "true" : "false", dh / mh, dg / (mg > 0 ? mg : 1), spat ? "true" : "false", ds / ms,
-              y_ref == y_gpu ? "true" : "false");
-  return (pattern && spat && y_ref == y_gpu) ? 0 : 1;
+              y_ref == y_gpu ? "true" : "false", apat ? "true" : "false", asym ? "true" : "false",
+              rel(ref.h_mat.values, ahyb.op.h_mat.values), rel(g_ref, g_alg), rel(xh_ref, xh_alg), rel(x_ref, x_alg),
+              acpat ? "true" : "false", rel(cref.s_mat.values, acond.op.s_mat.values), rel(fs_ref, fs_alg),
+              rel(xc_ref, xc_alg));
+  return (pattern && spat && y_ref == y_gpu && apat && asym && acpat) ? 0 : 1;
 }

@@ -55,7 +55,8 @@ std::vector<hdivred::index_t> block_offsets(const hdivred::RtSpace& sp) {
 
 std::pair<hdivred::HybridizedOperator, std::vector<double>> hybridize(const hdivred::RtSpace& space,
                                                                       const hdivred::CellCoefficients& coeffs,
-                                                                      const std::vector<double>& f_hat) {
+                                                                      const std::vector<double>& f_hat,
+                                                                      bool symmetric) {
   if (static_cast<hdivred::index_t>(f_hat.size()) != space.broken_ndofs ||
       static_cast<hdivred::index_t>(coeffs.alpha.size()) != space.mesh.ncells() ||
       static_cast<hdivred::index_t>(coeffs.beta.size()) != space.mesh.ncells())
@@ -65,6 +66,7 @@ std::pair<hdivred::HybridizedOperator, std::vector<double>> hybridize(const hdiv
   hdr_hybrid_t op = nullptr;
   check(hdr_hybridize_fe(s.get(), coeffs.alpha.data(), coeffs.beta.data(), f_hat.data(), 0, &op));
   std::unique_ptr<hdr_hybrid_s, void (*)(hdr_hybrid_s*)> guard(op, hdr_hybrid_destroy);
+  if (symmetric) check(hdr_hybrid_symmetrize(op));
   hdivred::HybridizedOperator out;
   const int64_t m = in[HDR_INFO_M], nnz = in[HDR_INFO_NNZ_H];
   out.h_mat = hdivred::CsrMatrix(m, m);
@@ -125,6 +127,136 @@ std::pair<std::vector<double>, std::vector<double>> recover_hybrid(const hdivred
     throw hdivred::DimensionMismatch("recover_hybrid: lambda length");
   check(hdr_recover_hybrid(op, lambda.data(), f_hat.data(), 0, x_hat.data(), x.data()));
   return {std::move(x_hat), std::move(x)};
+}
+
+namespace {
+
+// ReductionInputs -> hdr_alg_inputs (views into the caller's structure plus
+// the concatenated blocks / dof globals kept alive in `keep`)
+struct AlgView {
+  std::vector<int64_t> sizes, dof_global;
+  std::vector<double> blocks;
+  hdr_alg_inputs in{};
+};
+
+void view_inputs(const hdivred::ReductionInputs& r, AlgView& v) {
+  const auto& bl = r.a_hat.blocks;
+  v.sizes.resize(bl.size());
+  size_t total = 0;
+  for (size_t e = 0; e < bl.size(); ++e) {
+    v.sizes[e] = static_cast<int64_t>(bl[e].dof_map.size());
+    total += bl[e].matrix.entries.size();
+  }
+  v.blocks.reserve(total);
+  for (const auto& b : bl) {
+    if (b.matrix.nrows != static_cast<hdivred::index_t>(b.dof_map.size()) || b.matrix.ncols != b.matrix.nrows)
+      throw hdivred::DimensionMismatch("ElementBlockOperator: block matrix size != dof_map size");
+    v.blocks.insert(v.blocks.end(), b.matrix.entries.begin(), b.matrix.entries.end());
+    for (const auto& d : b.dof_map) v.dof_global.push_back(d.global);
+  }
+  hdr_alg_inputs& in = v.in;
+  in.nblocks = static_cast<int64_t>(bl.size());
+  in.block_sizes = v.sizes.data();
+  in.blocks = v.blocks.data();
+  in.dof_global = v.dof_global.data();
+  in.p_nrows = r.p_mat.nrows;
+  in.p_ncols = r.p_mat.ncols;
+  in.p_row_offsets = r.p_mat.row_offsets.data();
+  in.p_col_indices = r.p_mat.col_indices.data();
+  in.p_values = r.p_mat.values.data();
+  in.c_nrows = r.c_mat.nrows;
+  in.c_ncols = r.c_mat.ncols;
+  in.c_row_offsets = r.c_mat.row_offsets.data();
+  in.c_col_indices = r.c_mat.col_indices.data();
+  in.c_values = r.c_mat.values.data();
+  in.f_len = static_cast<int64_t>(r.f_hat.size());
+  in.f_hat = r.f_hat.data();
+  in.interior_global_begin = r.interior_global_begin;
+}
+
+std::shared_ptr<void> own(hdr_alg_t h) {
+  return std::shared_ptr<void>(h, [](void* p) { hdr_alg_destroy(static_cast<hdr_alg_t>(p)); });
+}
+
+std::array<int64_t, HDR_ALG_INFO_COUNT> alg_info(hdr_alg_t h) {
+  std::array<int64_t, HDR_ALG_INFO_COUNT> o{};
+  check(hdr_alg_info(h, o.data()));
+  return o;
+}
+
+hdivred::CsrMatrix alg_matrix(hdr_alg_t h, std::vector<double>& rhs) {
+  const auto o = alg_info(h);
+  hdivred::CsrMatrix a(o[HDR_ALG_NROWS], o[HDR_ALG_NROWS]);
+  a.col_indices.resize(static_cast<size_t>(o[HDR_ALG_NNZ]));
+  a.values.resize(static_cast<size_t>(o[HDR_ALG_NNZ]));
+  rhs.resize(static_cast<size_t>(o[HDR_ALG_NROWS]));
+  check(hdr_alg_matrix(h, a.row_offsets.data(), a.col_indices.data(), a.values.data(), rhs.data()));
+  return a;
+}
+
+std::vector<hdivred::index_t> offsets_of(const hdivred::ReductionInputs& r) {
+  std::vector<hdivred::index_t> off(r.a_hat.blocks.size() + 1, 0);
+  for (size_t e = 0; e < r.a_hat.blocks.size(); ++e)
+    off[e + 1] = off[e] + static_cast<hdivred::index_t>(r.a_hat.blocks[e].dof_map.size());
+  return off;
+}
+
+}  // namespace
+
+std::pair<AlgHybridized, std::vector<double>> hybridize(const hdivred::ReductionInputs& inputs, bool symmetric) {
+  AlgView v;
+  view_inputs(inputs, v);
+  hdr_alg_t h = nullptr;
+  check(hdr_alg_hybridize(&v.in, &h));
+  AlgHybridized out;
+  out.device = own(h);
+  if (symmetric) check(hdr_alg_symmetrize(h));
+  std::vector<double> g;
+  out.op.h_mat = alg_matrix(h, g);
+  out.op.p_mat = inputs.p_mat;
+  out.op.block_offsets = offsets_of(inputs);
+  const auto o = alg_info(h);
+  out.op.diagonal_gram = o[HDR_ALG_DIAGONAL_GRAM] != 0;
+  out.op.recovery_scale.resize(static_cast<size_t>(o[HDR_ALG_N_GLOBAL]));
+  check(hdr_alg_recovery_scale(h, out.op.recovery_scale.data()));
+  return {std::move(out), std::move(g)};
+}
+
+std::pair<std::vector<double>, std::vector<double>> recover_hybrid(const AlgHybridized& op,
+                                                                   const std::vector<double>& lambda,
+                                                                   const std::vector<double>& f_hat) {
+  hdr_alg_t h = static_cast<hdr_alg_t>(op.device.get());
+  const auto o = alg_info(h);
+  std::vector<double> x_hat(static_cast<size_t>(o[HDR_ALG_N_HAT])), x(static_cast<size_t>(o[HDR_ALG_N_GLOBAL]));
+  check(hdr_alg_recover_hybrid(h, lambda.data(), static_cast<int64_t>(lambda.size()), f_hat.data(),
+                               static_cast<int64_t>(f_hat.size()), x_hat.data(), x.data()));
+  return {std::move(x_hat), std::move(x)};
+}
+
+std::pair<AlgCondensed, std::vector<double>> static_condense(const hdivred::ReductionInputs& inputs, bool symmetric) {
+  AlgView v;
+  view_inputs(inputs, v);
+  hdr_alg_t h = nullptr;
+  check(hdr_alg_static_condense(&v.in, &h));
+  AlgCondensed out;
+  out.device = own(h);
+  if (symmetric) check(hdr_alg_symmetrize(h));
+  std::vector<double> f_s;
+  out.op.s_mat = alg_matrix(h, f_s);
+  out.op.master_globals.resize(static_cast<size_t>(out.op.s_mat.nrows));
+  check(hdr_alg_master_globals(h, out.op.master_globals.data()));
+  out.op.block_offsets = offsets_of(inputs);
+  out.op.n_global = inputs.p_mat.ncols;
+  return {std::move(out), std::move(f_s)};
+}
+
+std::vector<double> recover_condensed(const AlgCondensed& op, const std::vector<double>& x_b,
+                                      const std::vector<double>& f_hat) {
+  hdr_alg_t h = static_cast<hdr_alg_t>(op.device.get());
+  std::vector<double> x(static_cast<size_t>(op.op.n_global));
+  check(hdr_alg_recover_condensed(h, x_b.data(), static_cast<int64_t>(x_b.size()), f_hat.data(),
+                                  static_cast<int64_t>(f_hat.size()), x.data()));
+  return x;
 }
 
 std::vector<double> spmv(const hdivred::CsrMatrix& a, const std::vector<double>& x) {

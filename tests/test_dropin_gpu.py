@@ -27,3 +27,9 @@ def test_dropin_against_reference(n, k):
     line = json.loads(out.stdout.strip().splitlines()[-1])
     assert line["h_pattern_identical"] and line["s_pattern_identical"] and line["spmv_identical"], line
     assert line["h_rel"] < 1e-7 and line["g_rel"] < 1e-7 and line["s_rel"] < 1e-12, line
+    # algebraic drop-ins (hybridize / static_condense on the reference's own ReductionInputs)
+    assert line["alg_h_pattern_identical"] and line["alg_s_pattern_identical"] and line["alg_h_symmetric"], line
+    assert line["alg_h_rel"] < 1e-7 and line["alg_g_rel"] < 1e-7 and line["alg_s_rel"] < 1e-12, line
+    assert line["alg_x_hat_rel"] < 1e-7 and line["alg_x_rel"] < 1e-7, line
+    assert line["alg_f_s_rel"] < 1e-7 and line["alg_x_cond_rel"] < 1e-7, line
+    print(line)
