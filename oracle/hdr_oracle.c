@@ -366,12 +366,14 @@ static void tangent_axes(int dim, int axis, int t[2]) {
     if (a != axis) t[c++] = a;
 }
 
-int hdo_build_reference(int dim, int k, const double h[3], int nq, double* divdiv, double* mass, double* face_moments,
-                        double* unit_load) {
-  spoly polys[256], inter[256];
+/* basis coefficients phi (n x n, row = Legendre-product monomial q, column =
+ * basis function j) = lu_inverse(lu_factor(dof_vandermonde)) (rt_space.cpp:136-189) */
+static double* ref_basis(int dim, int k, spoly* polys, int* n_out) {
+  spoly inter[256];
   const int n = space_polys(dim, k, polys);
   const int nint = interior_moments(dim, k, inter);
   const long long dpf = llround(pow(k + 1, dim - 1));
+  *n_out = n;
 
   /* dof_vandermonde (rt_space.cpp:136-172) */
   double* V = calloc((size_t)(n * n), 8);
@@ -405,7 +407,7 @@ int hdo_build_reference(int dim, int k, const double h[3], int nq, double* divdi
   if (lu_factor(V, n, piv) >= 0) {
     free(V);
     free(piv);
-    return 2;
+    return NULL;
   }
   double* phi = calloc((size_t)(n * n), 8);
   double* col = malloc((size_t)n * 8);
@@ -417,6 +419,16 @@ int hdo_build_reference(int dim, int k, const double h[3], int nq, double* divdi
   free(col);
   free(piv);
   free(V);
+  return phi;
+}
+
+int hdo_build_reference(int dim, int k, const double h[3], int nq, double* divdiv, double* mass, double* face_moments,
+                        double* unit_load) {
+  spoly polys[256];
+  int n = 0;
+  double* phi = ref_basis(dim, k, polys, &n);
+  if (!phi) return 2;
+  const long long dpf = llround(pow(k + 1, dim - 1));
 
   double qs[16], qw[16];
   gauss_legendre_01(nq, qs, qw);
@@ -519,6 +531,126 @@ int hdo_build_reference(int dim, int k, const double h[3], int nq, double* divdi
   free(bdiv);
   free(phi);
   return 0;
+}
+
+/* ------------------------------------------- perturbed trilinear cells (config 4)
+ *
+ * RESTATEMENT, NOT THE REFERENCE: the reference supports affine boxes only
+ * (SURVEY.md §8(c) "Coverage gaps").  The reference's box element (basis, dofs
+ * and numbering of rt_space.cpp) is mapped to the trilinear cell by the
+ * contravariant Piola transform of F = X o B^-1 (B: s -> x0 + h s the box map,
+ * X: s -> sum_v N_v(s) x_v the trilinear map):
+ *   phi = DF phi_box / det DF,  div phi = div phi_box / det DF,
+ *   DF = J J0^-1 (J = dX/ds, J0 = diag(h)),  dx = det J ds,
+ * so   M_ij = sum_p w_p (det J0^2 / det J) (K phi^_i) . (K phi^_j),   K = J J0^-1
+ *      D_ij = sum_p w_p (det J0^2 / det J) divh_i divh_j,   divh = sum_a d_a phi^_a / h_a
+ * with the reference's (k+2)^3 Gauss points.  J = J0 (no perturbation) gives
+ * the reference's divdiv / mass up to rounding (tests/test_oracle_piola.py).
+ * verts: 8 x 3 physical coordinates, local vertex v = vx + 2 (vy + 2 vz). */
+static void piola_accumulate(int k, const double* phi, const spoly* polys, int n, const double h[3],
+                             const double* verts, int nq, double* divdiv, double* mass, double* pdiv_form,
+                             double* pmass) {
+  double qs[16], qw[16];
+  gauss_legendre_01(nq, qs, qw);
+  memset(divdiv, 0, (size_t)(n * n) * 8);
+  memset(mass, 0, (size_t)(n * n) * 8);
+  const int npr = (k + 1) * (k + 1) * (k + 1);
+  if (pdiv_form) memset(pdiv_form, 0, (size_t)(npr * n) * 8);
+  if (pmass) memset(pmass, 0, (size_t)(npr * npr) * 8);
+  double* pval = malloc((size_t)n * 8);
+  double* pdiv = malloc((size_t)n * 8);
+  double* psi = malloc((size_t)(3 * n) * 8);
+  double* bdiv = malloc((size_t)n * 8);
+  double* qv = malloc((size_t)(npr + 1) * 8);
+  const double det0 = h[0] * h[1] * h[2];
+  for (int iz = 0; iz < nq; ++iz)
+    for (int iy = 0; iy < nq; ++iy)
+      for (int ix = 0; ix < nq; ++ix) {
+        const double s[3] = {qs[ix], qs[iy], qs[iz]};
+        /* J[c][a] = sum_v x_v[c] dN_v/ds_a */
+        double J[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+        for (int v = 0; v < 8; ++v) {
+          const int b[3] = {v & 1, (v >> 1) & 1, (v >> 2) & 1};
+          double f[3], d[3];
+          for (int a = 0; a < 3; ++a) {
+            f[a] = b[a] ? s[a] : 1.0 - s[a];
+            d[a] = b[a] ? 1.0 : -1.0;
+          }
+          const double dN[3] = {d[0] * f[1] * f[2], f[0] * d[1] * f[2], f[0] * f[1] * d[2]};
+          for (int c = 0; c < 3; ++c)
+            for (int a = 0; a < 3; ++a) J[c][a] += verts[3 * v + c] * dN[a];
+        }
+        const double detJ = J[0][0] * (J[1][1] * J[2][2] - J[1][2] * J[2][1]) -
+                            J[0][1] * (J[1][0] * J[2][2] - J[1][2] * J[2][0]) +
+                            J[0][2] * (J[1][0] * J[2][1] - J[1][1] * J[2][0]);
+        const double w = qw[ix] * qw[iy] * qw[iz] * (det0 * det0 / detJ);
+        for (int q = 0; q < n; ++q) {
+          const spoly* t = &polys[q];
+          double val = 1.0;
+          for (int a = 0; a < 3; ++a) val *= legendre01(t->deg[a], s[a]);
+          pval[q] = val;
+          double dv = legendre01_deriv(t->deg[t->comp], s[t->comp]) / h[t->comp];
+          for (int a = 0; a < 3; ++a)
+            if (a != t->comp) dv *= legendre01(t->deg[a], s[a]);
+          pdiv[q] = dv;
+        }
+        for (int j = 0; j < n; ++j) {
+          double bv[3] = {0.0, 0.0, 0.0}, dsum = 0.0;
+          for (int q = 0; q < n; ++q) {
+            const double c = phi[q * n + j];
+            if (c == 0.0) continue;
+            bv[polys[q].comp] += c * pval[q];
+            dsum += c * pdiv[q];
+          }
+          for (int c = 0; c < 3; ++c) psi[3 * j + c] = J[c][0] / h[0] * bv[0] + J[c][1] / h[1] * bv[1] + J[c][2] / h[2] * bv[2];
+          bdiv[j] = dsum;
+        }
+        for (int i = 0; i < n; ++i)
+          for (int j = 0; j < n; ++j) {
+            divdiv[i * n + j] += w * bdiv[i] * bdiv[j];
+            mass[i * n + j] += w * (psi[3 * i] * psi[3 * j] + psi[3 * i + 1] * psi[3 * j + 1] + psi[3 * i + 2] * psi[3 * j + 2]);
+          }
+        if (pdiv_form || pmass) {
+          /* mapped pressures q = q^ det J0 / det J, q^ Legendre products of degree <= k */
+          int cnt = 0;
+          for (int dz = 0; dz <= k; ++dz)
+            for (int dy = 0; dy <= k; ++dy)
+              for (int dx = 0; dx <= k; ++dx)
+                qv[cnt++] = legendre01(dx, s[0]) * legendre01(dy, s[1]) * legendre01(dz, s[2]);
+          for (int p = 0; p < npr; ++p) {
+            if (pdiv_form)
+              for (int j = 0; j < n; ++j) pdiv_form[p * n + j] += w * qv[p] * bdiv[j];
+            if (pmass)
+              for (int r = 0; r < npr; ++r) pmass[p * npr + r] += w * qv[p] * qv[r];
+          }
+        }
+      }
+  free(pval);
+  free(pdiv);
+  free(psi);
+  free(bdiv);
+  free(qv);
+}
+
+int hdo_piola_element(int k, const double h[3], const double* verts, int nq, double* divdiv, double* mass,
+                      double* div_form, double* pressure_mass) {
+  spoly polys[256];
+  int n = 0;
+  double* phi = ref_basis(3, k, polys, &n);
+  if (!phi) return 2;
+  piola_accumulate(k, phi, polys, n, h, verts, nq, divdiv, mass, div_form, pressure_mass);
+  free(phi);
+  return 0;
+}
+
+/* the 8 vertices of a cell from the mesh vertex array ((N0+1)(N1+1)(N2+1) x 3) */
+static void cell_vertices(const hdo_ctx* c, const double* vtx, long long cell, double* out) {
+  const long long cx = cell % c->N[0], cy = (cell / c->N[0]) % c->N[1], cz = cell / (c->N[0] * c->N[1]);
+  for (int v = 0; v < 8; ++v) {
+    const long long ix = cx + (v & 1), iy = cy + ((v >> 1) & 1), iz = cz + ((v >> 2) & 1);
+    const long long g = ix + (c->N[0] + 1) * (iy + (c->N[1] + 1) * iz);
+    for (int a = 0; a < 3; ++a) out[3 * v + a] = vtx[3 * g + a];
+  }
 }
 
 /* --------------------------------------------------- mesh, mesh.cpp:13-135 */
@@ -775,6 +907,28 @@ int hdo_gen_inputs(hdo_ctx* c, const char* coef, unsigned long long seed) {
   for (long long i = 0; i < c->m; ++i) lam[i] = rng_uniform2(&r, -1.0, 1.0);
   double* xb = put_arr(c, "x_b", 'd', c->nS);
   for (long long i = 0; i < c->nS; ++i) xb[i] = rng_uniform2(&r, -1.0, 1.0);
+  /* config 4: ";perturb=f" displaces every interior vertex
+   * coordinate by U[-f h, f h], vertices lexicographic (x fastest), x then y then
+   * z, drawn after all other inputs; boundary vertices stay fixed */
+  const char* pt = strstr(coef, ";perturb=");
+  if (pt && c->dim == 3) {
+    const double frac = atof(pt + 9);
+    const long long nv0 = c->N[0] + 1, nv1 = c->N[1] + 1, nv2 = c->N[2] + 1;
+    double* vtx = put_arr(c, "vertices", 'd', nv0 * nv1 * nv2 * 3);
+    for (long long iz = 0; iz < nv2; ++iz)
+      for (long long iy = 0; iy < nv1; ++iy)
+        for (long long ix = 0; ix < nv0; ++ix) {
+          const long long g = ix + nv0 * (iy + nv1 * iz);
+          const long long idx[3] = {ix, iy, iz};
+          int interior = 1;
+          for (int a = 0; a < 3; ++a)
+            if (idx[a] == 0 || idx[a] == c->N[a]) interior = 0;
+          for (int a = 0; a < 3; ++a) {
+            vtx[3 * g + a] = (double)idx[a] * c->h[a];
+            if (interior) vtx[3 * g + a] += rng_uniform2(&r, -frac * c->h[a], frac * c->h[a]);
+          }
+        }
+  }
   return 0;
 }
 
@@ -794,12 +948,29 @@ int hdo_element_matrix(hdo_ctx* c, long long cell, double* a_t) {
     return 1;
   }
   const double alpha = al[cell], beta = be[cell];
+  const double* vtx = get_d(c, "vertices");
+  const double* D = c->divdiv;
+  const double* M = c->mass;
+  double* dm = NULL;
+  if (vtx && c->dim == 3) { /* perturbed trilinear cell (config 4): Piola element matrices */
+    dm = malloc((size_t)(2 * n * n) * 8);
+    double verts[24];
+    cell_vertices(c, vtx, cell, verts);
+    if (hdo_piola_element(c->k, c->h, verts, c->k + 2, dm, dm + n * n, NULL, NULL) != 0) {
+      free(dm);
+      set_err(c, "piola element failed");
+      return 1;
+    }
+    D = dm;
+    M = dm + n * n;
+  }
   for (long long i = 0; i < n * n; ++i) {
     double v = 0.0;
-    v += alpha * c->divdiv[i];
-    v += beta * c->mass[i];
+    v += alpha * D[i];
+    v += beta * M[i];
     a_t[i] = v;
   }
+  free(dm);
   return 0;
 }
 

@@ -85,6 +85,17 @@ int hdo_element_matrix(hdo_ctx* ctx, long long cell, double* a_t);
 
 const char* hdo_last_error(const hdo_ctx* ctx);
 
+/* Config 4 (RESTATEMENT — the reference has no curved / trilinear cells): the
+ * reference box element mapped to a trilinear hexahedron by the contravariant
+ * Piola transform, with the reference's nq^3 Gauss points.  h: the unperturbed
+ * cell size (the box the reference element lives on), verts: 8 x 3 vertex
+ * coordinates (v = vx + 2 vy + 4 vz).  divdiv, mass: n x n; div_form ((k+1)^3 x n)
+ * and pressure_mass ((k+1)^3 squared) of the Piola-mapped pressures, or NULL.
+ * With the context array "vertices" ((N+1)^3 x 3, set by hdo_gen_inputs'
+ * ";perturb=f" or hdo_set_d) element matrices use this map. */
+int hdo_piola_element(int k, const double h[3], const double* verts, int nq, double* divdiv, double* mass,
+                      double* div_form, double* pressure_mass);
+
 /* Reference element (restates build_reference): divdiv (n*n), mass (n*n),
  * face_moments (2*dim*dpf*n), unit_load (3*n). nq = quadrature points/axis. */
 int hdo_build_reference(int dim, int k, const double h[3], int nq, double* divdiv, double* mass,

@@ -47,6 +47,8 @@ def lib():
         L.hdo_element_matrix.argtypes = [ctypes.c_void_p, ctypes.c_longlong, ctypes.c_void_p]
         L.hdo_build_reference.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_double), ctypes.c_int,
                                           ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+        L.hdo_piola_element.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_double), ctypes.c_void_p, ctypes.c_int,
+                                        ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
         _lib = L
     return _lib
 
@@ -140,6 +142,30 @@ def build_reference(dim: int, k: int, h, nq: int):
     if rc != 0:
         raise OracleError("build_reference failed")
     return dd_.reshape(n, n), mm.reshape(n, n), fm, ul
+
+
+def piola_element(k: int, h, verts, nq: int, pressure: bool = False):
+    """Config-4 restatement: (divdiv, mass[, div_form, pressure_mass]) of the trilinear cell
+    with the 8 vertices verts (8 x 3, v = vx + 2 vy + 4 vz) mapped from the h box."""
+    n = 3 * (k + 1) ** 2 * 2 + 3 * k * (k + 1) ** 2
+    npr = (k + 1) ** 3
+    hh = (ctypes.c_double * 3)(*h)
+    v = np.ascontiguousarray(verts, dtype=np.float64).reshape(24)
+    D = np.zeros(n * n)
+    M = np.zeros(n * n)
+    B = np.zeros(npr * n)
+    W = np.zeros(npr * npr)
+    rc = lib().hdo_piola_element(k, hh, v.ctypes.data, nq, D.ctypes.data, M.ctypes.data,
+                                 B.ctypes.data if pressure else None, W.ctypes.data if pressure else None)
+    if rc != 0:
+        raise OracleError("piola_element failed")
+    if pressure:
+        return D.reshape(n, n), M.reshape(n, n), B.reshape(npr, n), W.reshape(npr, npr)
+    return D.reshape(n, n), M.reshape(n, n)
+
+
+def box_vertices(h, origin=(0.0, 0.0, 0.0)) -> np.ndarray:
+    return np.array([[origin[a] + h[a] * ((v >> a) & 1) for a in range(3)] for v in range(8)], dtype=np.float64)
 
 
 def read_dump(path) -> dict:
