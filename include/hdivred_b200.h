@@ -68,6 +68,16 @@ enum {
 
 /* ------------------------------------------------------------------ space */
 
+/* Config 4: attach vertex coordinates ((N0+1)(N1+1)(N2+1) x 3, lexicographic x
+ * fastest, host memory) to a 3D space; the cells become trilinear hexahedra and
+ * the element matrices the contravariant Piola map of the reference element
+ * (kern_piola.cu; oracle restatement hdo_piola_element — the reference has
+ * affine boxes only).  Hybridize / condense / recoveries then
+ * run the per-cell elimination of the algebraic path.  NULL detaches. */
+hdr_status hdr_space_set_vertices(hdr_space_t space, const double* vertices);
+/* The A_T blocks (ncells x n x n) of the last mapped-geometry call (host copy). */
+hdr_status hdr_space_element_matrices(hdr_space_t space, double* out);
+
 /* Builds the FE space on the device.  Replaces build_mesh (src/mesh.cpp:137)
  * + build_space (src/rt_space.cpp:318) as far as the hot path needs them.
  *  dim 2|3; cells[3]; cell sizes h[3] (cells congruent, axis aligned); order k

@@ -216,6 +216,26 @@ class Space:
         _check(_lib().hdr_space_dof_map(self._h, gl.ctypes.data, sg.ctypes.data))
         return gl, sg
 
+    def set_vertices(self, vertices) -> None:
+        """Config 4: trilinear cells with these vertex coordinates ((N0+1)(N1+1)(N2+1) x 3,
+        x fastest); None returns to the affine boxes."""
+        if vertices is None:
+            _check(_lib().hdr_space_set_vertices(self._h, None))
+            self.vertices = None
+            return
+        nv = int(np.prod([c + 1 for c in self.cells[:3]]))
+        v = np.ascontiguousarray(vertices, dtype=np.float64).reshape(-1)
+        if v.size != 3 * nv:
+            raise DimensionMismatch(f"vertices: expected {3 * nv} values, got {v.size}")
+        _check(_lib().hdr_space_set_vertices(self._h, v.ctypes.data))
+        self.vertices = v
+
+    def element_matrices(self) -> np.ndarray:
+        """A_T of every cell from the last mapped-geometry call (ncells x n x n)."""
+        out = np.empty(self.ncells * self.n * self.n)
+        _check(_lib().hdr_space_element_matrices(self._h, out.ctypes.data))
+        return out.reshape(self.ncells, self.n, self.n)
+
     def set_stream(self, stream_ptr: Optional[int]) -> None:
         """Run on a caller's CUDA stream handle (e.g. torch.cuda.Stream().cuda_stream).
         0 binds the legacy default stream; None restores the library's own stream."""

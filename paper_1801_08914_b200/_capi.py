@@ -77,6 +77,8 @@ _SIGS = {
     "hdr_alg_recover_condensed": (_i32, [_vp, _vp, _i64, _vp, _i64, _vp]),
     "hdr_alg_destroy": (None, [_vp]),
     "hdr_alg_symmetrize": (_i32, [_vp]),
+    "hdr_space_set_vertices": (_i32, [_vp, _vp]),
+    "hdr_space_element_matrices": (_i32, [_vp, _vp]),
     "hdr_hybrid_symmetrize": (_i32, [_vp]),
     "hdr_last_error": (ctypes.c_char_p, []),
     "hdr_version": (ctypes.c_char_p, []),

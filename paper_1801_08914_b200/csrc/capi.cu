@@ -21,6 +21,7 @@
 
 #include "../../include/hdivred_b200.h"
 #include "capi_util.hpp"
+#include "geom.hpp"
 #include "hdr_internal.hpp"
 #include "kernels.hpp"
 
@@ -57,7 +58,9 @@ struct hdr_space_s {
   std::vector<double> rt0_consts;  // packed constant block of the k = 0 kernel
   DBuf<uint64_t> rank_tab;         // k = 0 row-rank table
   Fixed fx{};
+  GeomState* geom = nullptr;  // mapped (trilinear) cells: hdr_space_set_vertices
   ~hdr_space_s() {
+    if (geom) geom_destroy(geom);
     if (own_stream && stream) cudaStreamDestroy(stream);
   }
 };
@@ -310,6 +313,40 @@ hdr_status hdr_space_create(int dim, const int64_t cells[3], const double h[3], 
 
 void hdr_space_destroy(hdr_space_t sp) { delete sp; }
 
+hdr_status hdr_space_set_vertices(hdr_space_t sp, const double* vertices) {
+  if (!sp) return fail(HDR_INVALID_ARGUMENT, "null space");
+  return catch_all([&]() -> hdr_status {
+    CK(cudaStreamSynchronize(sp->stream));
+    if (sp->geom) {
+      geom_destroy(sp->geom);
+      sp->geom = nullptr;
+    }
+    if (!vertices) return HDR_OK;
+    if (sp->dim != 3) return fail(HDR_UNSUPPORTED, "mapped geometry: 3D spaces only");
+    std::vector<int> mb(static_cast<size_t>(sp->nfaces));
+    CK(cudaMemcpy(mb.data(), sp->mbase.p, mb.size() * sizeof(int), cudaMemcpyDeviceToHost));
+    sp->geom = geom_create(sp->re, sp->dm, mb, sp->h, sp->m, sp->ndofs, vertices, sp->stream);
+    if (geom_nnz_h(sp->geom) != sp->nnz_h) {
+      geom_destroy(sp->geom);
+      sp->geom = nullptr;
+      return fail(HDR_VALIDATION, "mapped geometry: H pattern mismatch");
+    }
+    return HDR_OK;
+  });
+}
+
+hdr_status hdr_space_element_matrices(hdr_space_t sp, double* out) {
+  if (!sp || !out) return fail(HDR_INVALID_ARGUMENT, "null argument");
+  if (!sp->geom || !geom_element_blocks(sp->geom))
+    return fail(HDR_INVALID_ARGUMENT, "element matrices: no mapped geometry hybridized / condensed yet");
+  return catch_all([&]() -> hdr_status {
+    CK(cudaStreamSynchronize(sp->stream));
+    CK(cudaMemcpy(out, geom_element_blocks(sp->geom), static_cast<size_t>(sp->ncells) * sp->n * sp->n * 8,
+                  cudaMemcpyDeviceToHost));
+    return HDR_OK;
+  });
+}
+
 hdr_status hdr_space_info(hdr_space_t sp, int64_t* o) {
   if (!sp || !o) return fail(HDR_INVALID_ARGUMENT, "null argument");
   o[HDR_INFO_DIM] = sp->dim;
@@ -435,6 +472,7 @@ static hdr_status run_hybridize(hdr_hybrid_t op, const double* alpha, const doub
       op->status.alloc(1);
       CK(cudaMemsetAsync(op->status.p, 0, sizeof(int), st));
     }
+    if (sp->geom) return geom_hybridize(sp->geom, da, db, df, op->hval.p, op->g.p, st);
     HybArgs A{};
     A.m = sp->dm;
     A.fx = sp->fx;
@@ -594,6 +632,16 @@ hdr_status hdr_recover_hybrid(hdr_hybrid_t op, const double* lambda, const doubl
       op->status.alloc(1);
       CK(cudaMemsetAsync(op->status.p, 0, sizeof(int), st));
     }
+    if (sp->geom) {
+      const hdr_status s = geom_recover_hybrid(sp->geom, op->a_ptr, op->b_ptr, pl, pf, pxh, px, st);
+      if (s != HDR_OK) return s;
+      if (!on_device) {
+        if (x_hat) CK(cudaMemcpyAsync(x_hat, pxh, static_cast<size_t>(sp->broken) * 8, cudaMemcpyDeviceToHost, st));
+        if (x) CK(cudaMemcpyAsync(x, px, static_cast<size_t>(sp->ndofs) * 8, cudaMemcpyDeviceToHost, st));
+      }
+      CK(cudaStreamSynchronize(st));
+      return HDR_OK;
+    }
     RecArgs R{};
     R.m = sp->dm;
     R.fx = sp->fx;
@@ -649,6 +697,7 @@ static hdr_status run_condense(hdr_condensed_t op, const double* alpha, const do
       op->status.alloc(1);
       CK(cudaMemsetAsync(op->status.p, 0, sizeof(int), st));
     }
+    if (sp->geom) return geom_condense(sp->geom, da, db, df, op->sval.p, op->fs.p, st);
     const int64_t need = condense_ws_doubles(sp->dm, sp->nF);
     if (need > op->ws_doubles) {
       op->ws.alloc(static_cast<size_t>(need));
@@ -720,6 +769,13 @@ hdr_status hdr_recover_condensed(hdr_condensed_t op, const double* x_b, const do
       pxb = dxb.p;
       pf = df.p;
       px = dx.p;
+    }
+    if (sp->geom) {
+      const hdr_status s = geom_recover_condensed(sp->geom, op->a_ptr, op->b_ptr, pxb, pf, px, st);
+      if (s != HDR_OK) return s;
+      if (!on_device) CK(cudaMemcpyAsync(x, px, static_cast<size_t>(sp->ndofs) * 8, cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      return HDR_OK;
     }
     const int64_t need = condense_ws_doubles(sp->dm, sp->nF);
     if (need > op->ws_doubles) {

@@ -162,6 +162,24 @@ void launch_scatter(int64_t n, const int64_t* index, const double* v, double* ou
 void launch_iota(int64_t n, int64_t* out, cudaStream_t st);
 void launch_csr_symmetrize64(int64_t nrows, const int64_t* ro, const int64_t* ci, double* v, cudaStream_t st);
 void launch_csr_symmetrize32(int64_t nrows, const int64_t* ro, const int32_t* ci, double* v, cudaStream_t st);
+// ---- config 4: Piola element matrices of trilinear cells (kern_piola.cu)
+struct PiolaArgs {
+  int n, nq;
+  int64_t ncells;
+  int64_t N[3];
+  const double* verts;   // (N0+1)(N1+1)(N2+1) x 3
+  const double* qs;      // nq 1D Gauss points
+  const double* bq_val;  // nq^3 x n x 3 reference basis values
+  const double* bq_div;  // nq^3 x n
+  const double* bq_w;    // nq^3 weights
+  double h[3];
+  double det0;
+  const double *alpha, *beta;
+  double* ablk;          // ncells x n x n: A_T
+  double* dm;            // optional ncells x 2 x n x n: D_T, M_T
+};
+size_t piola_smem_bytes(int n);
+void launch_piola_assemble(const PiolaArgs& a, int grid, cudaStream_t st);
 void launch_dot(int64_t n, const double* x, const double* y, double* part, double* out, cudaStream_t st);
 
 }  // namespace hdr

@@ -192,6 +192,8 @@ RefElement build_reference_element(int dim, int k, const double h[3]) {
 
   std::vector<double> pv(n), pd(n), bv(3 * static_cast<size_t>(n)), bd(n);
   const int nqz = (dim == 3) ? nq : 1;
+  re.nq = nq;
+  re.qs.assign(qs, qs + nq);
   for (int iz = 0; iz < nqz; ++iz)
     for (int iy = 0; iy < nq; ++iy)
       for (int ix = 0; ix < nq; ++ix) {
@@ -219,6 +221,11 @@ RefElement build_reference_element(int dim, int k, const double h[3]) {
             ds += c * pd[q];
           }
           bd[j] = ds;
+        }
+        if (dim == 3) {
+          re.bq_val.insert(re.bq_val.end(), bv.begin(), bv.end());
+          re.bq_div.insert(re.bq_div.end(), bd.begin(), bd.end());
+          re.bq_w.push_back(qw[ix] * qw[iy] * qw[iz]);
         }
         for (int i = 0; i < n; ++i) {
           const double dvi = bd[i];

@@ -1,0 +1,90 @@
+"""Config 4 on the device: perturbed trilinear hexahedra (GPU).
+
+Contract: the device A_T against the CPU
+restatement (oracle hdo_piola_element — there is no reference for curved
+cells) — here bit-identical, the kernel follows it operation for operation;
+H / g / x_hat / x / S / f_S / x_cond within 1e-11 of max|entry| of the
+double-double oracle on the same A_T; patterns identical to the affine ones
+(same topology); the unperturbed vertex set reproduces the affine path.
+"""
+import numpy as np
+import pytest
+
+from conftest import has_cuda
+from oracle_lib import Oracle, rel_err
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-11
+
+if not has_cuda():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_1801_08914_b200 as hd  # noqa: E402
+
+CASES = [((3, 2, 2), 1, 1004), ((2, 2, 2), 2, 1004), ((2, 2, 1), 2, 7), ((3, 3, 3), 0, 11)]
+
+
+def _setup(cells, k, seed):
+    o = Oracle(3, cells, k)
+    o.gen_inputs("logu:1e-3:1e3;perturb=0.2", seed)
+    sp = hd.Space(3, cells, k)
+    sp.set_vertices(o.get("vertices"))
+    return o, sp
+
+
+@pytest.mark.parametrize("cells,k,seed", CASES)
+def test_piola_hybridize_vs_dd(cells, k, seed):
+    o, sp = _setup(cells, k, seed)
+    o.run("port_hybridize")
+    o.run("dd_hybridize")
+    o.run("dd_recover")
+    op = sp.hybridize(o.get("alpha"), o.get("beta"), o.get("f_hat"))
+    A = sp.element_matrices()
+    for e in range(sp.ncells):
+        assert np.array_equal(A[e], o.element_matrix(e)), e
+    ro, ci = sp.pattern("H")
+    assert np.array_equal(ro, o.getq("H.row_offsets")) and np.array_equal(ci, o.getq("H.col_indices"))
+    hv, g = op.values()
+    e_h, e_g = rel_err(hv, o.get("H.values_dd")), rel_err(g, o.get("g_dd"))
+    assert e_h <= TOL and e_g <= TOL, (e_h, e_g)
+    x_hat, x = op.recover(o.get("lambda"), o.get("f_hat"))
+    assert rel_err(x_hat, o.get("x_hat_dd")) <= TOL
+    assert rel_err(x, o.get("x_dd")) <= TOL
+    print(f"{cells} k={k}: H {e_h:.1e} g {e_g:.1e} (port vs DD {rel_err(o.get('H.values'), o.get('H.values_dd')):.1e})")
+
+
+@pytest.mark.parametrize("cells,k,seed", CASES)
+def test_piola_condense_vs_dd(cells, k, seed):
+    o, sp = _setup(cells, k, seed)
+    o.run("port_condense")
+    o.run("dd_condense")
+    o.run("dd_recover_condensed")
+    op = sp.static_condense(o.get("alpha"), o.get("beta"), o.get("f_hat"))
+    sv, fs = op.values()
+    assert rel_err(sv, o.get("S.values_dd")) <= TOL
+    assert rel_err(fs, o.get("f_s_dd")) <= TOL
+    x = op.recover(o.get("x_b"), o.get("f_hat"))
+    assert rel_err(x, o.get("x_cond_dd")) <= TOL
+
+
+def test_unperturbed_vertices_reproduce_affine():
+    cells, k = (3, 2, 2), 1
+    o = Oracle(3, cells, k)
+    o.gen_inputs("logu:1e-2:1e2", 5)
+    h = [1 / c for c in cells]
+    g = np.stack(np.meshgrid(*[np.arange(c + 1) * hh for c, hh in zip(cells, h)], indexing="ij"), -1)
+    verts = g.transpose(2, 1, 0, 3).reshape(-1, 3)
+    sp = hd.Space(3, cells, k)
+    ref = sp.hybridize(o.get("alpha"), o.get("beta"), o.get("f_hat")).values()
+    sp.set_vertices(verts)
+    mapped = sp.hybridize(o.get("alpha"), o.get("beta"), o.get("f_hat")).values()
+    # the mapped A_T equals the reference's affine A_T up to rounding ...
+    A = sp.element_matrices()
+    for e in range(sp.ncells):
+        assert rel_err(A[e], o.element_matrix(e)) <= 2e-15
+    # ... and H moves by the reference's own sensitivity to 1-ulp changes of A_T
+    # (about 1e-9 here), not more
+    assert rel_err(mapped[0], ref[0]) <= 1e-8 and rel_err(mapped[1], ref[1]) <= 1e-8
+    sp.set_vertices(None)
+    back = sp.hybridize(o.get("alpha"), o.get("beta"), o.get("f_hat")).values()
+    assert np.array_equal(back[0], ref[0])
