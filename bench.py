@@ -34,7 +34,7 @@ sys.path.insert(0, str(ROOT))
 METRIC = "elements/s of hybridization (assemble+eliminate+scatter), % of fp64/HBM roofline"
 UNIT = "elements/s"
 
-# BASELINE.json configs (config 4 = perturbed trilinear hexes, not in this bench yet)
+# BASELINE.json configs
 CONFIGS = {
     1: dict(dim=2, cells=(64, 64), k=0, coef=("uniform", 1.0, 1.0), seed=1001,
             desc="cfg1: 2D unit-square 64x64 quads, RT_0, alpha=beta=1"),
@@ -42,11 +42,14 @@ CONFIGS = {
             desc="cfg2: 3D unit-cube 64^3 hexes (262,144 elems), RT_0, alpha,beta log-uniform [1e-2,1e2]"),
     3: dict(dim=3, cells=(48, 48, 48), k=1, coef=("logu", 1e-2, 1e2), seed=1003,
             desc="cfg3: 3D unit-cube 48^3 hexes (110,592 elems), RT_1, alpha,beta log-uniform [1e-2,1e2]"),
+    4: dict(dim=3, cells=(24, 24, 24), k=2, coef=("logu", 1e-3, 1e3), seed=1004, perturb=0.2,
+            desc="cfg4: 3D 24^3 perturbed trilinear hexes (13,824 elems, interior vertices moved U[-0.2h,0.2h]), "
+                 "RT_2 (Piola), alpha,beta log-uniform [1e-3,1e3]"),
     5: dict(dim=3, cells=(32, 32, 32), k=3, coef=("checker", 1e-2, 1e2), seed=1005,
             desc="cfg5: 3D unit-cube 32^3 hexes (32,768 elems), RT_3, 4^3 checkerboard sigma_t in {1e-2,1e2}"),
 }
 # bounded CPU samples of each workload for the reference / cpu_baseline legs
-CPU_SAMPLE = {1: (2, (64, 64)), 2: (3, (32, 32, 32)), 3: (3, (16, 16, 16)), 5: (3, (4, 4, 4))}
+CPU_SAMPLE = {1: (2, (64, 64)), 2: (3, (32, 32, 32)), 3: (3, (16, 16, 16)), 4: (3, (3, 3, 3)), 5: (3, (4, 4, 4))}
 
 
 def make_inputs(cfg: dict, seed: int):
@@ -70,6 +73,20 @@ def make_inputs(cfg: dict, seed: int):
     n = 2 * cfg["dim"] * dpf + cfg["dim"] * cfg["k"] * dpf
     f_hat = rng.uniform(-1.0, 1.0, nc * n)
     return alpha, beta, f_hat
+
+
+def make_vertices(cfg: dict, seed: int):
+    """Config 4 geometry: unit-cube grid, every interior vertex coordinate moved by
+    U[-f h, f h] (boundary vertices fixed), vertices lexicographic x fastest."""
+    cells = cfg["cells"]
+    h = [1.0 / c for c in cells]
+    g = np.stack(np.meshgrid(*[np.arange(c + 1) * hh for c, hh in zip(cells, h)], indexing="ij"), -1)
+    g = g.transpose(2, 1, 0, 3).copy()  # (z, y, x, coord)
+    rng = np.random.default_rng(seed + 17)
+    inner = (slice(1, -1),) * 3
+    f = cfg["perturb"]
+    g[inner] += rng.uniform(-f, f, g[inner].shape) * np.array(h)
+    return g.reshape(-1, 3)
 
 
 def load_peaks():
@@ -150,8 +167,34 @@ def run_reference_sample(cfg_id: int, reps: int, threads: int):
     return recs, ncells, sample
 
 
+def port_sample(cfg_id: int, reps: int = 1):
+    """The oracle's port of hybridize (single thread) on the bounded sample; for
+    config 4 the only CPU implementation of the path (the reference has affine
+    boxes only)."""
+    sys.path.insert(0, str(ROOT / "tests"))
+    from oracle_lib import Oracle
+
+    cfg = CONFIGS[cfg_id]
+    dim, cells = CPU_SAMPLE[cfg_id]
+    kind, lo, hi = cfg["coef"]
+    spec = f"{kind}:{lo}:{hi}" + (f";perturb={cfg['perturb']}" if cfg.get("perturb") else "")
+    times = []
+    for _ in range(reps):
+        o = Oracle(dim, cells, cfg["k"])
+        o.gen_inputs(spec, cfg["seed"])
+        t0 = time.perf_counter()
+        o.run("port_hybridize")
+        times.append(time.perf_counter() - t0)
+    sample = (f"{'x'.join(map(str, cells))} mesh ({int(np.prod(cells))} cells) of the {cfg['desc'].split(':')[0]} "
+              f"workload, oracle port of the reference hybridize (element assembly included)")
+    return times, int(np.prod(cells)), sample
+
+
 def cpu_baseline(cfg_id: int):
     threads = os.cpu_count() or 1
+    if CONFIGS[cfg_id].get("perturb"):
+        times, ncells, sample = port_sample(cfg_id, 1)
+        return {"value": ncells / times[0], "unit": UNIT, "cores": 1, "kind": "port", "sample": sample}
     if ref_harness_path().exists():
         recs, ncells, sample = run_reference_sample(cfg_id, 3, threads)
         t = float(np.median([r["metric_s"] for r in recs]))
@@ -172,6 +215,16 @@ def cpu_baseline(cfg_id: int):
             "sample": f"{'x'.join(map(str, cells))} mesh, oracle port of hybridize (reference build unavailable)"}
 
 
+def kernel_name(cfg: dict) -> str:
+    if cfg.get("perturb"):
+        return "k_piola_assemble + k_alg<HYB> + k_run_sum"
+    if cfg["k"] == 0:
+        return "k_rt0_rows<dim,0> + k_rt0_rows<dim,1> (colour passes)"
+    if cfg["dim"] == 3 and cfg["k"] >= 2:
+        return "k_hyb_big<k> x2 colours"
+    return "k_hyb_warp x2 colours"
+
+
 def dist_setup():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -186,6 +239,18 @@ def reference_arm(args):
     cfg_id = args.config
     threads = os.cpu_count() or 1
     cfg = CONFIGS[cfg_id]
+    if cfg.get("perturb"):  # no reference implementation of mapped cells: the oracle port stands in
+        times, ncells, sample = port_sample(cfg_id, args.warmup + args.steps)
+        timed = times[args.warmup:]
+        value = ncells * len(timed) / float(np.sum(timed))
+        print(json.dumps({
+            "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * float(np.mean(timed)),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": cfg["desc"], "sample": sample, "threads": 1},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "port", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
+        return 0
     if not ref_harness_path().exists():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/ref_harness not built (needs /root/reference at build time)"}))
         return 0
@@ -220,6 +285,8 @@ def ours(args):
     cfg = CONFIGS[args.config]
     alpha, beta, f_hat = make_inputs(cfg, cfg["seed"] + 7919 * rank)
     sp = hd.Space(cfg["dim"], cfg["cells"], cfg["k"])
+    if cfg.get("perturb"):
+        sp.set_vertices(make_vertices(cfg, cfg["seed"] + 7919 * rank))
     stream = torch.cuda.Stream()  # one non-default stream for the library, the events and the flush
     torch.cuda.set_stream(stream)
     sp.set_stream(stream.cuda_stream)
@@ -302,6 +369,8 @@ def ours(args):
     # ---- roofline of the dominant kernel (the fused hybridize kernel; one launch per colour)
     peak, peak_kind = load_peaks()
     alg_bytes = 8 * (2 * ncells + sp.broken_ndofs + sp.info["nnz_h"] + sp.m)
+    if cfg.get("perturb"):
+        alg_bytes += 8 * 3 * 8 * ncells  # the cell's vertex coordinates
     achieved = alg_bytes / (ms_per_step * 1e-3) / 1e9
     traffic = None
     tf = ROOT / "profiles" / "ncu_traffic.json"
@@ -310,12 +379,14 @@ def ours(args):
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
             "traffic": traffic, "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
             "algorithmic_bytes_per_step": alg_bytes,
-            "kernel": "k_hyb_rt0<3> x2 colours" if cfg["k"] == 0 else "k_hyb_cta x2 colours"}
+            "kernel": kernel_name(cfg)}
     if cfg["k"] > 0 or args.fp64:
         tfl, _ = hd.measure_fp64_peak()
         n = sp.n
         b = sp.info["dofs_per_face"] * 2 * cfg["dim"]
         flop_cell = 2 * n ** 3 / 3 + 4 * b ** 3 / 3 + 2 * n ** 2 + 3 * n ** 2
+        if cfg.get("perturb"):  # + mapped-element assembly (mass and divdiv, symmetric halves)
+            flop_cell += 2 * (n * (n + 1) / 2) * (cfg["k"] + 2) ** 3 * 2
         fl = flop_cell * ncells / (ms_per_step * 1e-3) / 1e12
         roof_fp64 = {"bound": "fp64", "achieved": fl, "peak": tfl, "unit": "TFLOP/s", "frac": fl / tfl,
                      "peak_source": "measured DFMA (hdr_measure_fp64_peak)", "flops_per_cell": flop_cell}
