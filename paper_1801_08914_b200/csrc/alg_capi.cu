@@ -27,8 +27,7 @@ struct hdr_alg_s {
   cudaStream_t st = nullptr;
   int64_t ne = 0, n_hat = 0, n_global = 0, m = 0, nrows = 0, nnz = 0, n_master = 0;
   bool diagonal_gram = true;
-  int64_t ws_doubles = 0;
-  int grid = 1;
+  AlgPlan plan;
   // element data kept for the recoveries
   DBuf<int64_t> boff, aoff, goff, mrows, hoff, cptr, bdof_off, bm_ptr, bm_ord, soff, ibase, i_global, masters;
   DBuf<int> idx, ni, cent_r, cent_a, bm_loc;
@@ -107,13 +106,9 @@ void transpose_csr(int64_t nrows, int64_t ncols, const int64_t* ro, const int64_
     }
 }
 
-void finish_launch_config(hdr_alg_s* op, int64_t ws) {
-  op->ws_doubles = ws;
-  const int sms = sm_count_alg();
-  int per_sm = 2;
-  if (alg_ws_in_smem(ws)) per_sm = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(4, (220 * 1024) / (ws * 8 + 1024))));
-  op->grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(op->ne, static_cast<int64_t>(sms) * per_sm)));
-  if (!alg_ws_in_smem(ws)) op->gws.alloc(static_cast<size_t>(op->grid) * ws);
+void finish_launch_config(hdr_alg_s* op, int dmax, int ncmax) {
+  op->plan = alg_plan(op->ne, dmax, ncmax);
+  op->gws.alloc(static_cast<size_t>(alg_gws_doubles(op->plan)));
 }
 
 hdr_status read_status(hdr_alg_s* op, const char* who) {
@@ -207,7 +202,7 @@ hdr_status hdr_alg_hybridize(const hdr_alg_inputs* in, hdr_alg_t* out) {
     std::vector<int64_t> goff(static_cast<size_t>(ne) + 1, 0), hoff(static_cast<size_t>(ne) + 1, 0), mrows, cptr;
     std::vector<int> cent_r, cent_a;
     std::vector<double> cent_v;
-    int64_t ws = 1;
+    int dmax = 1, ncmax = 1;
     std::vector<int64_t> rows;
     std::vector<int> pos_of(1, -1);
     for (int64_t e = 0; e < ne; ++e) {
@@ -247,7 +242,8 @@ hdr_status hdr_alg_hybridize(const hdr_alg_inputs* in, hdr_alg_t* out) {
       }
       goff[e + 1] = goff[e] + nr;
       hoff[e + 1] = hoff[e] + static_cast<int64_t>(nr) * nr;
-      ws = std::max(ws, alg_ws_doubles(n, nr + 1));
+      dmax = std::max(dmax, n);
+      ncmax = std::max(ncmax, nr + 1);
     }
     cptr.push_back(static_cast<int64_t>(cent_v.size()));
     op->idx.upload(idx);
@@ -259,7 +255,7 @@ hdr_status hdr_alg_hybridize(const hdr_alg_inputs* in, hdr_alg_t* out) {
     op->cent_r.upload(cent_r);
     op->cent_a.upload(cent_a);
     op->cent_v.upload(cent_v);
-    finish_launch_config(op.get(), ws);
+    finish_launch_config(op.get(), dmax, ncmax);
     DBuf<double> f, hbuf, gbuf;
     f.upload(in->f_hat, static_cast<size_t>(n_hat));
     hbuf.alloc(static_cast<size_t>(hoff.back()));
@@ -268,7 +264,7 @@ hdr_status hdr_alg_hybridize(const hdr_alg_inputs* in, hdr_alg_t* out) {
     a.f = f.p;
     a.hbuf = hbuf.p;
     a.gbuf = gbuf.p;
-    launch_alg(a, ALG_HYB, op->ws_doubles, op->gws.p, op->grid, st);
+    launch_alg(a, ALG_HYB, op->plan, op->gws.p, st);
     const hdr_status s = read_status(op.get(), "hybridize");
     if (s != HDR_OK) return s;
 
@@ -350,7 +346,7 @@ hdr_status hdr_alg_static_condense(const hdr_alg_inputs* in, hdr_alg_t* out) {
         ibase(static_cast<size_t>(ne) + 1, 0), i_global;
     std::vector<double> i_sign;
     std::vector<char> is_master(static_cast<size_t>(ng), 0);
-    int64_t ws = 1;
+    int dmax = 1, ncmax = 1;
     for (int64_t e = 0; e < ne; ++e) {
       const int64_t o = off[e];
       const int n = static_cast<int>(off[e + 1] - o);
@@ -379,7 +375,8 @@ hdr_status hdr_alg_static_condense(const hdr_alg_inputs* in, hdr_alg_t* out) {
       bdof_off[e + 1] = bdof_off[e] + nb;
       soff[e + 1] = soff[e] + static_cast<int64_t>(nb) * nb;
       ibase[e + 1] = ibase[e] + ni[e];
-      ws = std::max(ws, alg_ws_doubles(ni[e], nb + 1));
+      dmax = std::max(dmax, ni[e]);
+      ncmax = std::max(ncmax, nb + 1);
     }
     std::vector<int64_t> ordinal(static_cast<size_t>(ng), -1);
     for (int64_t g = 0; g < ng; ++g)
@@ -421,7 +418,7 @@ hdr_status hdr_alg_static_condense(const hdr_alg_inputs* in, hdr_alg_t* out) {
     op->bm_w.upload(bm_w);
     op->bm_loc.upload(bm_loc);
     op->masters.upload(op->master_globals);
-    finish_launch_config(op.get(), ws);
+    finish_launch_config(op.get(), dmax, ncmax);
     DBuf<double> f, sbuf, fsbuf;
     f.upload(in->f_hat, static_cast<size_t>(n_hat));
     sbuf.alloc(static_cast<size_t>(soff.back()));
@@ -430,7 +427,7 @@ hdr_status hdr_alg_static_condense(const hdr_alg_inputs* in, hdr_alg_t* out) {
     a.f = f.p;
     a.sbuf = sbuf.p;
     a.fsbuf = fsbuf.p;
-    launch_alg(a, ALG_COND, op->ws_doubles, op->gws.p, op->grid, st);
+    launch_alg(a, ALG_COND, op->plan, op->gws.p, st);
     const hdr_status s = read_status(op.get(), "static_condense");
     if (s != HDR_OK) return s;
 
@@ -537,7 +534,7 @@ hdr_status hdr_alg_recover_hybrid(hdr_alg_t op, const double* lambda, int64_t la
     a.f = df.p;
     a.lambda = dl.p;
     a.x_hat = dxh.p;
-    launch_alg(a, ALG_REC, op->ws_doubles, op->gws.p, op->grid, st);
+    launch_alg(a, ALG_REC, op->plan, op->gws.p, st);
     const hdr_status s = read_status(op, "recover_hybrid");
     if (s != HDR_OK) return s;
     // x = (P^T P)^-1 P^T x_hat
@@ -615,7 +612,7 @@ hdr_status hdr_alg_recover_condensed(hdr_alg_t op, const double* x_b, int64_t xb
     a.f = df.p;
     a.xb = dxb.p;
     a.x = dx.p;
-    launch_alg(a, ALG_RECC, op->ws_doubles, op->gws.p, op->grid, st);
+    launch_alg(a, ALG_RECC, op->plan, op->gws.p, st);
     const hdr_status s = read_status(op, "recover_condensed");
     if (s != HDR_OK) return s;
     if (ng) CK(cudaMemcpyAsync(x, dx.p, static_cast<size_t>(ng) * 8, cudaMemcpyDeviceToHost, st));

@@ -34,18 +34,17 @@ struct GeomState {
   DBuf<int> idx_h, ni_h, cent_r, cent_a;
   DBuf<double> cent_v;
   Runs HR, GR;
-  int64_t ws_h = 0;
+  AlgPlan plan_h;
   // condense descriptors (built on first use)
   bool cond_ready = false;
   DBuf<int64_t> bdof_off, bm_ptr, bm_ord, soff, ibase, i_global;
   DBuf<int> idx_c, ni_c, bm_loc;
   DBuf<double> bm_w, i_sign;
   Runs SR, FR;
-  int64_t ws_c = 0;
+  AlgPlan plan_c;
   // scratch
   DBuf<double> ablk, hbuf, gbuf, sbuf, fsbuf, gws;
   int64_t gws_doubles = 0;
-  int grid = 1;
   DBuf<int> status;
   DBuf<unsigned long long> bad;
 };
@@ -59,9 +58,8 @@ int sms() {
   return n > 0 ? n : 148;
 }
 
-void ensure_ws(GeomState* G, int64_t ws) {
-  if (alg_ws_in_smem(ws)) return;
-  const int64_t need = ws * G->grid;
+void ensure_ws(GeomState* G, const AlgPlan& p) {
+  const int64_t need = alg_gws_doubles(p);
   if (need > G->gws_doubles) {
     G->gws.alloc(static_cast<size_t>(need));
     G->gws_doubles = need;
@@ -177,8 +175,8 @@ void build_condense(GeomState* G, cudaStream_t st) {
   G->ibase.upload(ibase);
   G->i_global.upload(i_global);
   G->i_sign.upload(i_sign);
-  G->ws_c = alg_ws_doubles(nint, nF + 1);
-  ensure_ws(G, G->ws_c);
+  G->plan_c = alg_plan(ne, nint, nF + 1);
+  ensure_ws(G, G->plan_c);
   AlgArgs a{};
   a.ne = ne;
   a.boff = G->boff.p;
@@ -267,7 +265,6 @@ GeomState* geom_create(const RefElement& re, const DevMesh& dm, const std::vecto
   CK(cudaMemset(G->status.p, 0, sizeof(int)));
   G->bad.alloc(1);
   CK(cudaMemset(G->bad.p, 0xff, sizeof(unsigned long long)));
-  G->grid = 2 * sms();
 
   // hybrid descriptors: i = bubbles + boundary-face dofs, b = interior-face
   // dofs (zero columns of C, reduction.cpp:236-258); multiplier rows = the
@@ -322,8 +319,8 @@ GeomState* geom_create(const RefElement& re, const DevMesh& dm, const std::vecto
   G->cent_r.upload(cent_r);
   G->cent_a.upload(cent_a);
   G->cent_v.upload(cent_v);
-  G->ws_h = alg_ws_doubles(n, max_nr + 1);
-  ensure_ws(G.get(), G->ws_h);
+  G->plan_h = alg_plan(ne, n, max_nr + 1);
+  ensure_ws(G.get(), G->plan_h);
   G->hbuf.alloc(static_cast<size_t>(hoff.back()));
   G->gbuf.alloc(static_cast<size_t>(goff.back()));
   // from_triplets order of H and g, once
@@ -355,7 +352,7 @@ hdr_status geom_hybridize(GeomState* G, const double* alpha, const double* beta,
   AlgArgs a = hyb_args(G, f);
   a.hbuf = G->hbuf.p;
   a.gbuf = G->gbuf.p;
-  launch_alg(a, ALG_HYB, G->ws_h, G->gws.p, G->grid, st);
+  launch_alg(a, ALG_HYB, G->plan_h, G->gws.p, st);
   launch_run_sum(G->HR.nruns, G->HR.start.p, G->HR.src.p, nullptr, G->hbuf.p, hval, nullptr, 0, st);
   CK(cudaMemsetAsync(g, 0, static_cast<size_t>(G->m) * 8, st));
   launch_run_sum(G->GR.nruns, G->GR.start.p, G->GR.src.p, nullptr, G->gbuf.p, g, G->GR.index.p, 1, st);
@@ -368,7 +365,7 @@ hdr_status geom_recover_hybrid(GeomState* G, const double* alpha, const double* 
   AlgArgs a = hyb_args(G, f);
   a.lambda = lambda;
   a.x_hat = x_hat;
-  launch_alg(a, ALG_REC, G->ws_h, G->gws.p, G->grid, st);
+  launch_alg(a, ALG_REC, G->plan_h, G->gws.p, st);
   launch_average_faces(G->dm, x_hat, x, st);
   return read_geom_status(G, st, "recover_hybrid");
 }
@@ -378,7 +375,7 @@ hdr_status geom_condense(GeomState* G, const double* alpha, const double* beta, 
   if (!G->cond_ready) build_condense(G, st);
   assemble(G, alpha, beta, st);
   AlgArgs a = cond_args(G, f);
-  launch_alg(a, ALG_COND, G->ws_c, G->gws.p, G->grid, st);
+  launch_alg(a, ALG_COND, G->plan_c, G->gws.p, st);
   launch_run_sum(G->SR.nruns, G->SR.start.p, G->SR.src.p, G->SR.w.p, G->sbuf.p, sval, nullptr, 0, st);
   CK(cudaMemsetAsync(fs, 0, static_cast<size_t>(G->fdc) * 8, st));
   launch_run_sum(G->FR.nruns, G->FR.start.p, G->FR.src.p, G->FR.w.p, G->fsbuf.p, fs, G->FR.index.p, 1, st);
@@ -394,7 +391,7 @@ hdr_status geom_recover_condensed(GeomState* G, const double* alpha, const doubl
   AlgArgs a = cond_args(G, f);
   a.xb = x_b;
   a.x = x;
-  launch_alg(a, ALG_RECC, G->ws_c, G->gws.p, G->grid, st);
+  launch_alg(a, ALG_RECC, G->plan_c, G->gws.p, st);
   return read_geom_status(G, st, "recover_condensed");
 }
 

@@ -18,8 +18,11 @@
 // steps on a rounded Schur complement are not).  Products
 // with C, A_bi in the epilogues are compensated as well.
 //
-// Layout of the per-CTA workspace (shared memory when it fits, else a global
-// slot): LU column-major d x d, X / R / B0 column-major d x nc.
+// Per-CTA workspace: LU (column-major d x d), X and R (row-major d x nc) in
+// shared memory when they fit, else in a global slot; B0 and the low parts Xl
+// (row-major d x nc) in the global slot.
+#include <algorithm>
+
 #include "hdr_device.cuh"
 #include "kernels.hpp"
 
@@ -27,7 +30,7 @@ namespace hdr {
 
 namespace {
 
-constexpr int kAT = 256;  // threads per CTA
+constexpr int kAT = 1024;  // threads per CTA
 constexpr int kAW = kAT / 32;
 
 struct DD {
@@ -123,9 +126,10 @@ __device__ __forceinline__ double Mget(const Elem& E, int i, int k) {
 // singular pivot.
 __device__ bool block_lu(const Elem& E, int ni_piv, double* lu, int* piv, double* sv, int* si) {
   const int d = E.d;
-  for (int t = threadIdx.x; t < d * d; t += kAT) {
-    const int i = t % d, k = t / d;
-    lu[t] = Mget(E, i, k);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int k = warp; k < d; k += kAW) {
+    const double* arow_k = E.A + E.idx[k];  // column idx[k] of A, stride n
+    for (int i = lane; i < d; i += 32) lu[k * d + i] = __ldg(arow_k + static_cast<int64_t>(E.idx[i]) * E.n);
   }
   __syncthreads();
   double thr = 0.0;
@@ -167,105 +171,154 @@ __device__ bool block_lu(const Elem& E, int ni_piv, double* lu, int* piv, double
     const double inv = lu[j * d + j];
     for (int i = j + 1 + threadIdx.x; i < d; i += kAT) lu[j * d + i] = lu[j * d + i] / inv;
     __syncthreads();
-    const int w = d - j - 1;
-    for (int t = threadIdx.x; t < w * w; t += kAT) {
-      const int i = j + 1 + t % w, k = j + 1 + t / w;
-      lu[k * d + i] = fma(-lu[j * d + i], lu[k * d + j], lu[k * d + i]);
+    for (int k = j + 1 + warp; k < d; k += kAW) {
+      const double ukj = lu[k * d + j];
+      for (int i = j + 1 + lane; i < d; i += 32) lu[k * d + i] = fma(-lu[j * d + i], ukj, lu[k * d + i]);
     }
     __syncthreads();
   }
   return true;
 }
 
-// Y <- LU^-1 P Y for the nc columns of Y (column-major d x nc); one warp per column
+// Y <- LU^-1 P Y for the nc columns of Y (row-major d x nc: Y[i*nc + c]),
+// blocked by kSB rows: the diagonal triangle of a block is solved column by
+// column (one thread per column), the rows below / above are updated by a
+// kSB-deep product (warps over rows, lanes over columns) — two barriers per
+// block instead of one or two per row.
+constexpr int kSB = 8;
 __device__ void block_solve(int d, int nc, const double* lu, const int* piv, double* Y) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int c = warp; c < nc; c += kAW) {
-    double* y = Y + static_cast<int64_t>(c) * d;
-    if (lane == 0)
-      for (int j = 0; j < d; ++j) {
-        const int p = piv[j];
-        if (p != j) {
-          const double a = y[j];
-          y[j] = y[p];
-          y[p] = a;
-        }
-      }
-    __syncwarp();
+  for (int c = threadIdx.x; c < nc; c += kAT)
     for (int j = 0; j < d; ++j) {
-      const double yj = y[j];
-      for (int i = j + 1 + lane; i < d; i += 32) y[i] = fma(-lu[j * d + i], yj, y[i]);
-      __syncwarp();
-    }
-    for (int j = d - 1; j >= 0; --j) {
-      if (lane == 0) y[j] = y[j] / lu[j * d + j];
-      __syncwarp();
-      const double yj = y[j];
-      for (int i = lane; i < j; i += 32) y[i] = fma(-lu[j * d + i], yj, y[i]);
-      __syncwarp();
-    }
-  }
-  __syncthreads();
-}
-
-// X + Xl <- M^-1 B0 (B0 = b0h + b0l, column-major d x nc) as a double-double
-// (X the rounded value, Xl the remainder): residuals B0 - M (X + Xl) are
-// accumulated exactly, corrections solved with the LU and folded in with
-// two_sum, until a correction is below 2^-100 of the solution.  The
-// remainder matters where the epilogue cancels (f_S = f_b - A_bi A_ii^-1 f_i).
-// R is scratch.  Returns the number of refinement steps taken.
-__device__ int refined_solve(const Elem& E, int nc, const double* lu, const int* piv, const double* b0h,
-                             const double* b0l, double* X, double* Xl, double* R, double* sv) {
-  const int d = E.d;
-  for (int t = threadIdx.x; t < d * nc; t += kAT) {
-    X[t] = b0h[t];
-    Xl[t] = 0.0;
-  }
-  __syncthreads();
-  block_solve(d, nc, lu, piv, X);
-  int steps = 0;
-  for (; steps < 8; ++steps) {
-    for (int t = threadIdx.x; t < d * nc; t += kAT) {
-      const int i = t % d, c = t / d;
-      double hi = b0h[t], lo = b0l ? b0l[t] : 0.0;
-      const double* x = X + static_cast<int64_t>(c) * d;
-      const double* xl = Xl + static_cast<int64_t>(c) * d;
-      const double* arow = E.A + static_cast<int64_t>(E.idx[i]) * E.n;
-      for (int k = 0; k < d; ++k) {
-        const double m = -__ldg(arow + E.idx[k]);
-        dd_fma(hi, lo, m, x[k]);
-        lo = fma(m, xl[k], lo);
+      const int p = piv[j];
+      if (p != j) {
+        const double t = Y[j * nc + c];
+        Y[j * nc + c] = Y[p * nc + c];
+        Y[p * nc + c] = t;
       }
-      R[t] = hi + lo;
+    }
+  __syncthreads();
+  for (int jb = 0; jb < d; jb += kSB) {  // forward, unit lower L
+    const int je = min(jb + kSB, d);
+    for (int c = threadIdx.x; c < nc; c += kAT)
+      for (int j = jb; j < je; ++j) {
+        const double yj = Y[j * nc + c];
+        for (int i = j + 1; i < je; ++i) Y[i * nc + c] = fma(-lu[j * d + i], yj, Y[i * nc + c]);
+      }
+    __syncthreads();
+    for (int i = je + warp; i < d; i += kAW) {
+      double l[kSB];
+#pragma unroll
+      for (int t = 0; t < kSB; ++t) l[t] = jb + t < je ? lu[(jb + t) * d + i] : 0.0;
+      for (int c = lane; c < nc; c += 32) {
+        double acc = Y[i * nc + c];
+#pragma unroll
+        for (int t = 0; t < kSB; ++t)
+          if (jb + t < je) acc = fma(-l[t], Y[(jb + t) * nc + c], acc);
+        Y[i * nc + c] = acc;
+      }
     }
     __syncthreads();
-    block_solve(d, nc, lu, piv, R);
-    double cm = 0.0, xm = 0.0;
-    for (int t = threadIdx.x; t < d * nc; t += kAT) {
-      const double c = R[t];
-      double hi, e;
-      two_sum(X[t], c + Xl[t], hi, e);
-      X[t] = hi;
-      Xl[t] = e;
-      cm = fmax(cm, fabs(c));
-      xm = fmax(xm, fabs(hi));
-    }
-    cm = block_max(cm, sv);
-    xm = block_max(xm, sv);
-    if (!(cm > 0x1p-100 * xm)) {
-      ++steps;
-      break;
-    }
   }
-  return steps;
+  for (int je = d; je > 0; je -= kSB) {  // backward, upper U
+    const int jb = max(0, je - kSB);
+    for (int c = threadIdx.x; c < nc; c += kAT)
+      for (int j = je - 1; j >= jb; --j) {
+        const double yj = Y[j * nc + c] / lu[j * d + j];
+        Y[j * nc + c] = yj;
+        for (int i = jb; i < j; ++i) Y[i * nc + c] = fma(-lu[j * d + i], yj, Y[i * nc + c]);
+      }
+    __syncthreads();
+    for (int i = warp; i < jb; i += kAW) {
+      double u[kSB];
+#pragma unroll
+      for (int t = 0; t < kSB; ++t) u[t] = jb + t < je ? lu[(jb + t) * d + i] : 0.0;
+      for (int c = lane; c < nc; c += 32) {
+        double acc = Y[i * nc + c];
+#pragma unroll
+        for (int t = 0; t < kSB; ++t)
+          if (jb + t < je) acc = fma(-u[t], Y[(jb + t) * nc + c], acc);
+        Y[i * nc + c] = acc;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// Xg + Xlg <- M^-1 B0 (B0 = b0h + b0l; all row-major d x nc, global) as a
+// double-double (Xg the rounded value, Xlg the remainder), in column chunks of
+// at most ncc held in shared memory (Xs, Xls, Rs: d x cw each): residuals
+// B0 - M (X + Xl) are accumulated exactly (one warp per row, lanes over the
+// chunk's columns), corrections solved with the LU and folded in with two_sum.
+// Stops when the correction, scaled by its observed contraction rate, is below
+// tgt of the solution (tgt = 2^-100 where the epilogue cancels: f_S = f_b -
+// A_bi A_ii^-1 f_i; 2^-60 elsewhere).
+__device__ void refined_solve(const Elem& E, int nc, int ncc, const double* lu, const int* piv, const double* b0h,
+                              const double* b0l, double* Xg, double* Xlg, double* Xs, double* Xls, double* Rs,
+                              double* sv, double tgt) {
+  const int d = E.d;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int c0 = 0; c0 < nc; c0 += ncc) {
+    const int cw = min(ncc, nc - c0);
+    for (int i = warp; i < d; i += kAW)
+      for (int c = lane; c < cw; c += 32) {
+        Xs[i * cw + c] = b0h[i * nc + c0 + c];
+        Xls[i * cw + c] = 0.0;
+      }
+    __syncthreads();
+    block_solve(d, cw, lu, piv, Xs);
+    double prev = 0.0;
+    for (int step = 0; step < 8; ++step) {
+      for (int i = warp; i < d; i += kAW) {
+        const double* arow = E.A + static_cast<int64_t>(E.idx[i]) * E.n;
+        for (int c = lane; c < cw; c += 32) {
+          double hi = b0h[i * nc + c0 + c], lo = b0l ? b0l[i * nc + c0 + c] : 0.0;
+          for (int k = 0; k < d; ++k) {
+            const double m = -__ldg(arow + E.idx[k]);
+            dd_fma(hi, lo, m, Xs[k * cw + c]);
+            lo = fma(m, Xls[k * cw + c], lo);
+          }
+          Rs[i * cw + c] = hi + lo;
+        }
+      }
+      __syncthreads();
+      block_solve(d, cw, lu, piv, Rs);
+      double cm = 0.0, xm = 0.0;
+      for (int t = threadIdx.x; t < d * cw; t += kAT) {
+        const double c = Rs[t];
+        double hi, e;
+        two_sum(Xs[t], c + Xls[t], hi, e);
+        Xs[t] = hi;
+        Xls[t] = e;
+        cm = fmax(cm, fabs(c));
+        xm = fmax(xm, fabs(hi));
+      }
+      cm = block_max(cm, sv);
+      xm = block_max(xm, sv);
+      // the next correction is about rho * cm (rho: observed contraction)
+      const double rho = step > 0 && prev > 0.0 ? fmin(1.0, cm / prev) : 1.0;
+      prev = cm;
+      if (!(cm * fmax(rho, 0x1p-52) > tgt * xm)) break;
+    }
+    for (int i = warp; i < d; i += kAW)
+      for (int c = lane; c < cw; c += 32) {
+        Xg[i * nc + c0 + c] = Xs[i * cw + c];
+        Xlg[i * nc + c0 + c] = Xls[i * cw + c];
+      }
+    __syncthreads();
+  }
 }
 
 template <int MODE>
-__global__ void __launch_bounds__(kAT) k_alg(AlgArgs a, double* gws, int64_t ws_stride, int use_smem) {
+__global__ void __launch_bounds__(kAT) k_alg(AlgArgs a, double* gws, AlgPlan p) {
   extern __shared__ __align__(16) double smem[];
   __shared__ double sv[kAW + 1];
   __shared__ int si[kAW + 1];
-  double* W = use_smem ? smem : gws + static_cast<int64_t>(blockIdx.x) * ws_stride;
+  // fast region (LU, column-chunk buffers, piv): shared memory when it fits;
+  // slow region (B0h, B0l, X, Xl: element-wise traffic only) in the CTA's global slot
+  const int64_t stride = p.slow + (p.smem ? 0 : p.fast);
+  double* Ws = gws + static_cast<int64_t>(blockIdx.x) * stride;
+  double* Wf = p.smem ? smem : Ws + p.slow;
   for (int64_t e = blockIdx.x; e < a.ne; e += gridDim.x) {
     Elem E;
     E.boff = a.boff[e];
@@ -280,14 +333,17 @@ __global__ void __launch_bounds__(kAT) k_alg(AlgArgs a, double* gws, int64_t ws_
     int nc = 1;
     if (MODE == ALG_HYB) nc = nr + 1;
     if (MODE == ALG_COND) nc = nb + 1;
-    // workspace carve: LU d*d | X d*nc | R d*nc | B0h d*nc | B0l d*nc (rec modes) | piv d ints
-    double* lu = W;
-    double* X = lu + static_cast<int64_t>(d) * d;
-    double* R = X + static_cast<int64_t>(d) * nc;
-    double* b0h = R + static_cast<int64_t>(d) * nc;
+    const int ncc = min(nc, p.ncc);
+    // workspace carve
+    double* lu = Wf;
+    double* Xs = lu + static_cast<int64_t>(d) * d;
+    double* Xls = Xs + static_cast<int64_t>(d) * ncc;
+    double* Rs = Xls + static_cast<int64_t>(d) * ncc;
+    int* piv = reinterpret_cast<int*>(Rs + static_cast<int64_t>(d) * ncc);
+    double* b0h = Ws;
     double* b0l = b0h + static_cast<int64_t>(d) * nc;
-    double* Xl = b0l + static_cast<int64_t>(d) * nc;
-    int* piv = reinterpret_cast<int*>(Xl + static_cast<int64_t>(d) * nc);
+    double* X = b0l + static_cast<int64_t>(d) * nc;
+    double* Xl = X + static_cast<int64_t>(d) * nc;
     const bool rec = MODE == ALG_REC || MODE == ALG_RECC;
     bool ok = true;
     if (d > 0) {
@@ -306,11 +362,11 @@ __global__ void __launch_bounds__(kAT) k_alg(AlgArgs a, double* gws, int64_t ws_
         __syncthreads();
         // C_T^T: column r holds row r of the element's constraint slice
         for (int64_t q = a.cptr[a.goff[e]] + threadIdx.x; q < a.cptr[a.goff[e + 1]]; q += kAT)
-          b0h[static_cast<int64_t>(a.cent_r[q]) * d + a.cent_a[q]] = a.cent_v[q];
-        for (int i = threadIdx.x; i < d; i += kAT) b0h[static_cast<int64_t>(nr) * d + i] = a.f[E.boff + E.idx[i]];
+          b0h[static_cast<int64_t>(a.cent_a[q]) * nc + a.cent_r[q]] = a.cent_v[q];
+        for (int i = threadIdx.x; i < d; i += kAT) b0h[static_cast<int64_t>(i) * nc + nr] = a.f[E.boff + E.idx[i]];
       } else if (MODE == ALG_COND) {
         for (int t = threadIdx.x; t < d * nc; t += kAT) {
-          const int i = t % d, c = t / d;
+          const int i = t / nc, c = t % nc;
           b0h[t] = c < nb ? Mget(E, i, E.ni + c) : a.f[E.boff + E.idx[i]];
         }
       } else if (MODE == ALG_REC) {
@@ -336,7 +392,8 @@ __global__ void __launch_bounds__(kAT) k_alg(AlgArgs a, double* gws, int64_t ws_
         }
       }
       __syncthreads();
-      refined_solve(E, nc, lu, piv, b0h, rec ? b0l : nullptr, X, Xl, R, sv);
+      refined_solve(E, nc, ncc, lu, piv, b0h, rec ? b0l : nullptr, X, Xl, Xs, Xls, Rs, sv,
+                    MODE == ALG_COND ? 0x1p-100 : 0x1p-60);
     }
     // epilogues
     if (MODE == ALG_HYB) {
@@ -348,7 +405,7 @@ __global__ void __launch_bounds__(kAT) k_alg(AlgArgs a, double* gws, int64_t ws_
         double hi = 0.0, lo = 0.0;
         for (int64_t z = a.cptr[a.goff[e] + r]; z < a.cptr[a.goff[e] + r + 1]; ++z)
         {
-          const int64_t xi = static_cast<int64_t>(q) * d + a.cent_a[z];
+          const int64_t xi = static_cast<int64_t>(a.cent_a[z]) * nc + q;
           dd_fma(hi, lo, a.cent_v[z], X[xi]);
           lo = fma(a.cent_v[z], Xl[xi], lo);
         }
@@ -367,8 +424,8 @@ __global__ void __launch_bounds__(kAT) k_alg(AlgArgs a, double* gws, int64_t ws_
         double hi = k < nb ? Mget(E, E.ni + j, E.ni + k) : a.f[E.boff + E.idx[E.ni + j]], lo = 0.0;
         for (int l = 0; l < d; ++l) {
           const double m = -Mget(E, E.ni + j, l);
-          dd_fma(hi, lo, m, X[static_cast<int64_t>(k) * d + l]);
-          lo = fma(m, Xl[static_cast<int64_t>(k) * d + l], lo);
+          dd_fma(hi, lo, m, X[static_cast<int64_t>(l) * nc + k]);
+          lo = fma(m, Xl[static_cast<int64_t>(l) * nc + k], lo);
         }
         if (k < nb) s[static_cast<int64_t>(j) * nb + k] = hi + lo;
         else fs[j] = hi + lo;
@@ -470,18 +527,34 @@ __global__ void k_run_sum(int64_t nruns, const int64_t* run_start, const int64_t
 
 }  // namespace
 
-int64_t alg_ws_doubles(int d, int nc) {
-  // LU + X + R + B0h + B0l + Xl + piv (as doubles, rounded up)
-  return static_cast<int64_t>(d) * d + 5 * static_cast<int64_t>(d) * nc + (d + 1) / 2 + 1;
+AlgPlan alg_plan(int64_t ne, int dmax, int ncmax) {
+  AlgPlan p;
+  const int64_t budget = 200 * 1024 / 8;  // doubles of dynamic shared memory
+  const int64_t fixed = static_cast<int64_t>(dmax) * dmax + (dmax + 1) / 2 + 1;
+  const int64_t per_col = 3 * static_cast<int64_t>(dmax);
+  int64_t ncc = per_col > 0 ? (budget - fixed) / per_col : ncmax;
+  p.smem = ncc >= 1;
+  p.ncc = p.smem ? static_cast<int>(std::min<int64_t>(ncc, ncmax)) : ncmax;
+  if (p.ncc < 1) p.ncc = 1;
+  p.fast = fixed + per_col * p.ncc;
+  p.slow = 4 * static_cast<int64_t>(dmax) * ncmax + 1;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (sms <= 0) sms = 148;
+  int per_sm = 2;
+  if (p.smem) per_sm = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(4, (226 * 1024) / (p.fast * 8 + 2048))));
+  p.grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ne, static_cast<int64_t>(sms) * per_sm)));
+  return p;
 }
 
-void launch_alg(const AlgArgs& a, int mode, int64_t ws_doubles, double* gws, int grid, cudaStream_t st) {
-  const size_t smem = static_cast<size_t>(ws_doubles) * 8;
-  const bool use_smem = smem <= 200 * 1024;
-  const size_t dyn = use_smem ? smem : 0;
+int64_t alg_gws_doubles(const AlgPlan& p) { return static_cast<int64_t>(p.grid) * (p.slow + (p.smem ? 0 : p.fast)); }
+
+void launch_alg(const AlgArgs& a, int mode, const AlgPlan& p, double* gws, cudaStream_t st) {
+  const size_t dyn = p.smem ? static_cast<size_t>(p.fast) * 8 : 0;
   auto go = [&](auto kern) {
-    if (use_smem) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dyn));
-    kern<<<grid, kAT, dyn, st>>>(a, gws, ws_doubles, use_smem ? 1 : 0);
+    if (p.smem) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dyn));
+    kern<<<p.grid, kAT, dyn, st>>>(a, gws, p);
   };
   switch (mode) {
     case ALG_HYB: go(k_alg<ALG_HYB>); break;
@@ -491,8 +564,6 @@ void launch_alg(const AlgArgs& a, int mode, int64_t ws_doubles, double* gws, int
   }
   count_launch();
 }
-
-bool alg_ws_in_smem(int64_t ws_doubles) { return ws_doubles * 8 <= 200 * 1024; }
 
 void launch_alg_hkeys(const AlgArgs& a, uint64_t* hkeys, int64_t* hsrc, uint64_t* gkeys, int64_t* gsrc, cudaStream_t st) {
   const int grid = static_cast<int>(a.ne < 4096 ? (a.ne > 0 ? a.ne : 1) : 4096);

@@ -141,9 +141,16 @@ struct AlgArgs {
   const double* xb;            // recover_condensed: master values
   double* x;                   // recover_condensed: global solution
 };
-int64_t alg_ws_doubles(int d, int nc);
-bool alg_ws_in_smem(int64_t ws_doubles);
-void launch_alg(const AlgArgs& a, int mode, int64_t ws_doubles, double* gws, int grid, cudaStream_t st);
+// launch plan for elements of order <= dmax with <= ncmax right-hand sides
+struct AlgPlan {
+  int64_t fast = 0, slow = 0;  // doubles per CTA: LU + column-chunk buffers (+piv), and B0h/B0l/X/Xl
+  int ncc = 1;                 // right-hand-side columns per chunk
+  bool smem = false;           // fast region in shared memory
+  int grid = 1;
+};
+AlgPlan alg_plan(int64_t ne, int dmax, int ncmax);
+int64_t alg_gws_doubles(const AlgPlan& p);  // global scratch the plan needs
+void launch_alg(const AlgArgs& a, int mode, const AlgPlan& p, double* gws, cudaStream_t st);
 void launch_alg_hkeys(const AlgArgs& a, uint64_t* hkeys, int64_t* hsrc, uint64_t* gkeys, int64_t* gsrc, cudaStream_t st);
 void launch_alg_skeys(const AlgArgs& a, const int64_t* trip_off, const int64_t* ftrip_off, uint64_t* skeys,
                       int64_t* ssrc, double* sw, uint64_t* fkeys, int64_t* fsrc, double* fw, cudaStream_t st);
