@@ -127,7 +127,7 @@ class Space:
     """
 
     def __init__(self, dim: int, cells: Sequence[int], order: int, sizes: Optional[Sequence[float]] = None,
-                 ref_divdiv=None, ref_mass=None):
+                 ref_divdiv=None, ref_mass=None, weighted: bool = False):
         cells = list(cells) + [1] * (3 - len(cells))
         if sizes is None:
             sizes = [1.0 / c if a < dim else 1.0 for a, c in enumerate(cells)]
@@ -141,12 +141,13 @@ class Space:
         h = ctypes.c_void_p()
         _check(_lib().hdr_space_create(dim, ctypes.addressof(carr), ctypes.addressof(harr), order,
                                        None if dd is None else dd.ctypes.data,
-                                       None if mm is None else mm.ctypes.data, 0, None, ctypes.byref(h)))
+                                       None if mm is None else mm.ctypes.data, 1 if weighted else 0, None,
+                                       ctypes.byref(h)))
         self._h = h
         info = np.zeros(len(_capi.INFO_NAMES), np.int64)
         _check(_lib().hdr_space_info(self._h, info.ctypes.data))
         self.info = {k: int(v) for k, v in zip(_capi.INFO_NAMES, info)}
-        self.dim, self.order = dim, order
+        self.dim, self.order, self.weighted = dim, order, bool(weighted)
         self.cells = tuple(cells[:dim])
         self.sizes = tuple(sizes[:3])
 
@@ -484,11 +485,9 @@ def space_from_config(config: dict) -> Space:
             sizes[a] = 1.0 / cells[a]
     if dim == 2:
         cells[2], sizes[2] = 1, 1.0
-    if config.get("weighted", False):
-        raise UnsupportedError("weighted constraint rows are not implemented on the device path yet")
     if config.get("essential_boundary", False):
         raise UnsupportedError("essential-boundary elimination is outside the FE fast path")
-    return Space(dim, cells[:dim], int(config.get("order", 0)), sizes)
+    return Space(dim, cells[:dim], int(config.get("order", 0)), sizes, weighted=bool(config.get("weighted", False)))
 
 
 def hybridized_matrix(config: dict):

@@ -179,7 +179,6 @@ hdr_status hdr_space_create(int dim, const int64_t cells[3], const double h[3], 
     if (cells[a] < 1) return fail(HDR_INVALID_ARGUMENT, "build_mesh: cell counts must be >= 1");
     if (h && !(h[a] > 0.0)) return fail(HDR_INVALID_ARGUMENT, "build_mesh: cell sizes must be > 0");
   }
-  if (weighted) return fail(HDR_UNSUPPORTED, "weighted constraint rows are not implemented on the device path yet");
   (void)ref_face_moments;
   return catch_all([&]() -> hdr_status {
     int dev_count = 0;
@@ -188,6 +187,7 @@ hdr_status hdr_space_create(int dim, const int64_t cells[3], const double h[3], 
     auto sp = std::make_unique<hdr_space_s>();
     sp->dim = dim;
     sp->k = order;
+    sp->weighted = weighted ? 1 : 0;
     for (int a = 0; a < 3; ++a) {
       sp->N[a] = a < dim ? cells[a] : 1;
       sp->h[a] = a < dim ? (h ? h[a] : 1.0 / static_cast<double>(cells[a])) : 1.0;
@@ -304,6 +304,11 @@ hdr_status hdr_space_create(int dim, const int64_t cells[3], const double h[3], 
       sp->rank_tab.alloc(tab.size());
       CK(cudaMemcpyAsync(sp->rank_tab.p, tab.data(), tab.size() * 8, cudaMemcpyHostToDevice, st));
     }
+    if (sp->weighted) {  // weighted constraint rows: the per-cell elimination path (geom.cu, affine cells)
+      std::vector<int> mb(static_cast<size_t>(sp->nfaces));
+      CK(cudaMemcpy(mb.data(), sp->mbase.p, mb.size() * sizeof(int), cudaMemcpyDeviceToHost));
+      sp->geom = geom_create(sp->re, sp->dm, mb, sp->h, sp->m, sp->ndofs, nullptr, true, st);
+    }
     CK(cudaStreamSynchronize(st));
     CK(cudaGetLastError());
     *out = sp.release();
@@ -321,11 +326,11 @@ hdr_status hdr_space_set_vertices(hdr_space_t sp, const double* vertices) {
       geom_destroy(sp->geom);
       sp->geom = nullptr;
     }
-    if (!vertices) return HDR_OK;
-    if (sp->dim != 3) return fail(HDR_UNSUPPORTED, "mapped geometry: 3D spaces only");
+    if (!vertices && !sp->weighted) return HDR_OK;
+    if (vertices && sp->dim != 3) return fail(HDR_UNSUPPORTED, "mapped geometry: 3D spaces only");
     std::vector<int> mb(static_cast<size_t>(sp->nfaces));
     CK(cudaMemcpy(mb.data(), sp->mbase.p, mb.size() * sizeof(int), cudaMemcpyDeviceToHost));
-    sp->geom = geom_create(sp->re, sp->dm, mb, sp->h, sp->m, sp->ndofs, vertices, sp->stream);
+    sp->geom = geom_create(sp->re, sp->dm, mb, sp->h, sp->m, sp->ndofs, vertices, sp->weighted != 0, sp->stream);
     if (geom_nnz_h(sp->geom) != sp->nnz_h) {
       geom_destroy(sp->geom);
       sp->geom = nullptr;

@@ -29,6 +29,8 @@ struct GeomState {
   DevMesh dm{};
   double h[3] = {1, 1, 1}, det0 = 1;
   DBuf<double> verts, qs, bq_val, bq_div, bq_w;
+  bool mapped = false;   // trilinear cells (vertices attached); else the affine reference element
+  DBuf<double> ref_dm;   // affine: D_ref, M_ref (n x n each)
   // hybrid descriptors
   DBuf<int64_t> boff, aoff, goff, mrows, hoff, cptr;
   DBuf<int> idx_h, ni_h, cent_r, cent_a;
@@ -68,6 +70,10 @@ void ensure_ws(GeomState* G, const AlgPlan& p) {
 
 void assemble(GeomState* G, const double* alpha, const double* beta, cudaStream_t st) {
   if (!G->ablk.p) G->ablk.alloc(static_cast<size_t>(G->ncells) * G->n * G->n);
+  if (!G->mapped) {  // affine cells (weighted constraint rows): A_T = fl(fl(alpha D) + fl(beta M))
+    launch_affine_assemble(G->ncells, G->n, G->ref_dm.p, alpha, beta, G->ablk.p, st);
+    return;
+  }
   PiolaArgs P{};
   P.n = G->n;
   P.nq = G->nq;
@@ -239,9 +245,10 @@ AlgArgs cond_args(GeomState* G, const double* f) {
 }  // namespace
 
 GeomState* geom_create(const RefElement& re, const DevMesh& dm, const std::vector<int>& mbase, const double h[3],
-                       int64_t m, int64_t ndofs, const double* verts_host, cudaStream_t st) {
-  if (dm.dim != 3 || re.bq_w.empty()) throw StatusError(HDR_UNSUPPORTED, "mapped geometry needs a 3D space");
+                       int64_t m, int64_t ndofs, const double* verts_host, bool weighted, cudaStream_t st) {
+  if (verts_host && (dm.dim != 3 || re.bq_w.empty())) throw StatusError(HDR_UNSUPPORTED, "mapped geometry needs a 3D space");
   auto G = std::make_unique<GeomState>();
+  G->mapped = verts_host != nullptr;
   G->n = re.n;
   G->nint = re.nint;
   G->dpf = re.dpf;
@@ -255,12 +262,18 @@ GeomState* geom_create(const RefElement& re, const DevMesh& dm, const std::vecto
   G->dm = dm;
   for (int a = 0; a < 3; ++a) G->h[a] = h[a];
   G->det0 = h[0] * h[1] * h[2];
-  const int64_t nv = (dm.N[0] + 1) * (dm.N[1] + 1) * (dm.N[2] + 1);
-  G->verts.upload(verts_host, static_cast<size_t>(nv) * 3);
-  G->qs.upload(re.qs);
-  G->bq_val.upload(re.bq_val);
-  G->bq_div.upload(re.bq_div);
-  G->bq_w.upload(re.bq_w);
+  if (G->mapped) {
+    const int64_t nv = (dm.N[0] + 1) * (dm.N[1] + 1) * (dm.N[2] + 1);
+    G->verts.upload(verts_host, static_cast<size_t>(nv) * 3);
+    G->qs.upload(re.qs);
+    G->bq_val.upload(re.bq_val);
+    G->bq_div.upload(re.bq_div);
+    G->bq_w.upload(re.bq_w);
+  } else {
+    std::vector<double> dmv(re.divdiv);
+    dmv.insert(dmv.end(), re.mass.begin(), re.mass.end());
+    G->ref_dm.upload(dmv);
+  }
   G->status.alloc(1);
   CK(cudaMemset(G->status.p, 0, sizeof(int)));
   G->bad.alloc(1);
@@ -292,17 +305,27 @@ GeomState* geom_create(const RefElement& re, const DevMesh& dm, const std::vecto
     ni[e] = k;
     int nr = 0;
     for (int s = 0; s < 2 * dm.dim; ++s)
-      if (in[s])
-        for (int sub = 0; sub < dpf; ++sub) {
-          idx[e * n + k] = nint + s * dpf + sub;
+      if (in[s]) {
+        const int k0 = k;  // position of the slot's first dof in the [i | b] order
+        for (int sub = 0; sub < dpf; ++sub) idx[e * n + k++] = nint + s * dpf + sub;
+        for (int r = 0; r < dpf; ++r) {
           cptr.push_back(static_cast<int64_t>(cent_v.size()));
-          cent_r.push_back(nr);
-          cent_a.push_back(k);  // unweighted C: one +1 entry per interior-face dof (build_C, reduction.cpp:152-198)
-          cent_v.push_back(1.0);
-          mrows.push_back(static_cast<int64_t>(mbase[face[s]]) + sub);
-          ++k;
+          if (!weighted) {  // unit rows: one +1 per interior-face dof (build_C, reduction.cpp:172-181)
+            cent_r.push_back(nr);
+            cent_a.push_back(k0 + r);
+            cent_v.push_back(1.0);
+          } else {  // weighted rows: face moments over the slot's dofs (reduction.cpp:182-195)
+            const double* fm = re.face_moments.data() + (static_cast<size_t>(s) * dpf + r) * n;
+            for (int sub = 0; sub < dpf; ++sub) {
+              cent_r.push_back(nr);
+              cent_a.push_back(k0 + sub);
+              cent_v.push_back(fm[nint + s * dpf + sub]);
+            }
+          }
+          mrows.push_back(static_cast<int64_t>(mbase[face[s]]) + r);
           ++nr;
         }
+      }
     goff[e + 1] = goff[e] + nr;
     hoff[e + 1] = hoff[e] + static_cast<int64_t>(nr) * nr;
     max_nr = std::max(max_nr, nr);
@@ -396,5 +419,6 @@ hdr_status geom_recover_condensed(GeomState* G, const double* alpha, const doubl
 }
 
 const double* geom_element_blocks(const GeomState* G) { return G->ablk.p; }
+bool geom_mapped(const GeomState* G) { return G->mapped; }
 
 }  // namespace hdr

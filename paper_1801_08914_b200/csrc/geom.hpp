@@ -14,7 +14,8 @@ namespace hdr {
 
 struct GeomState;
 GeomState* geom_create(const RefElement& re, const DevMesh& dm, const std::vector<int>& mbase, const double h[3],
-                       int64_t m, int64_t ndofs, const double* verts_host, cudaStream_t st);
+                       int64_t m, int64_t ndofs, const double* verts_host, bool weighted, cudaStream_t st);
+bool geom_mapped(const GeomState* G);
 void geom_destroy(GeomState* G);
 int64_t geom_nnz_h(const GeomState* G);
 hdr_status geom_hybridize(GeomState* G, const double* alpha, const double* beta, const double* f, double* hval,

@@ -113,7 +113,23 @@ __global__ void __launch_bounds__(kPT, 1) k_piola_assemble(PiolaArgs P) {
   }
 }
 
+__global__ void k_affine_assemble(int64_t ncells, int n, const double* dm, const double* alpha, const double* beta,
+                                  double* out) {
+  const int64_t nn = static_cast<int64_t>(n) * n;
+  for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < ncells * nn;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t e = t / nn, ij = t - e * nn;
+    out[t] = add(mul(alpha[e], dm[ij]), mul(beta[e], dm[nn + ij]));
+  }
+}
+
 }  // namespace
+
+void launch_affine_assemble(int64_t ncells, int n, const double* dm, const double* alpha, const double* beta,
+                            double* out, cudaStream_t st) {
+  k_affine_assemble<<<148 * 8, 256, 0, st>>>(ncells, n, dm, alpha, beta, out);
+  count_launch();
+}
 
 size_t piola_smem_bytes(int n) { return static_cast<size_t>(kCP * n * 4 + kCP * 10) * 8; }
 

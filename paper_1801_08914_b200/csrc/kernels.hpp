@@ -186,6 +186,9 @@ struct PiolaArgs {
   double* dm;            // optional ncells x 2 x n x n: D_T, M_T
 };
 size_t piola_smem_bytes(int n);
+// affine cells: A_T = fl(fl(alpha D) + fl(beta M)) for every cell (dm = [D | M], n x n each)
+void launch_affine_assemble(int64_t ncells, int n, const double* dm, const double* alpha, const double* beta,
+                            double* out, cudaStream_t st);
 void launch_piola_assemble(const PiolaArgs& a, int grid, cudaStream_t st);
 void launch_dot(int64_t n, const double* x, const double* y, double* part, double* out, cudaStream_t st);
 
