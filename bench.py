@@ -281,12 +281,13 @@ def ours(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     import paper_1801_08914_b200 as hd
+    from paper_1801_08914_b200 import dist as hdist
 
     cfg = CONFIGS[args.config]
-    alpha, beta, f_hat = make_inputs(cfg, cfg["seed"] + 7919 * rank)
+    alpha, beta, f_hat = make_inputs(cfg, hdist.replica_seed(cfg["seed"], rank))
     sp = hd.Space(cfg["dim"], cfg["cells"], cfg["k"])
     if cfg.get("perturb"):
-        sp.set_vertices(make_vertices(cfg, cfg["seed"] + 7919 * rank))
+        sp.set_vertices(make_vertices(cfg, hdist.replica_seed(cfg["seed"], rank)))
     stream = torch.cuda.Stream()  # one non-default stream for the library, the events and the flush
     torch.cuda.set_stream(stream)
     sp.set_stream(stream.cuda_stream)
@@ -294,9 +295,7 @@ def ours(args):
     op = sp.hybridize(a_d, b_d, f_d)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float64, device="cuda")  # 512 MiB > 126 MB L2
 
-    def barrier():
-        if world > 1:
-            torch.distributed.barrier()
+    barrier = hdist.barrier
 
     # warmup (device-resident inputs)
     for i in range(args.warmup):
@@ -321,11 +320,7 @@ def ours(args):
     op.check()
     launches = hd.launch_count() - launches0
     step_ms = [a.elapsed_time(b) for a, b in zip(ev0, ev1)]
-    total_ms = float(np.sum(step_ms))
-    if world > 1:
-        t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        total_ms = float(t.item())
+    total_ms = hdist.reduce_max(float(np.sum(step_ms)))  # device time, max over ranks
     ncells = sp.ncells
     value = ncells * world * args.steps / (total_ms * 1e-3)
     ms_per_step = total_ms / args.steps
@@ -351,11 +346,7 @@ def ours(args):
             e1[i].record(stream)
         torch.cuda.synchronize()
         op.check()
-        e2e_ms = float(np.sum([a.elapsed_time(b) for a, b in zip(e0, e1)]))
-        if world > 1:
-            t = torch.tensor([e2e_ms], dtype=torch.float64, device="cuda")
-            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-            e2e_ms = float(t.item())
+        e2e_ms = hdist.reduce_max(float(np.sum([a.elapsed_time(b) for a, b in zip(e0, e1)])))
         e2e = {"value": ncells * world * args.steps / (e2e_ms * 1e-3), "unit": UNIT,
                "h2d_bytes_per_step": 8 * (2 * ncells + sp.broken_ndofs),
                "d2h_bytes_per_step": 8 * (sp.info["nnz_h"] + sp.m),
