@@ -493,17 +493,12 @@ static hdr_status run_hybridize(hdr_hybrid_t op, const double* alpha, const doub
     A.status = op->status.p;
     A.rank_tab = sp->rank_tab.p;
     if (sp->k == 0) {
-      static const bool legacy = getenv("HDR_RT0_LEGACY") != nullptr;
-      if (legacy) {
-        for (int parity = 0; parity < 2; ++parity) launch_hybridize_rt0(A, sp->rt0_consts.data(), parity, st);
-      } else {
-        const int64_t need = parity_count(sp->dm) * sp->n * (sp->n + 1);
-        if (op->ws_doubles < need) {
-          op->ws.alloc(static_cast<size_t>(need));
-          op->ws_doubles = need;
-        }
-        launch_hybridize_rt0_rows(A, sp->rt0_consts.data(), op->ws.p, st);
+      const int64_t need = parity_count(sp->dm) * sp->n * (sp->n + 1);  // colour-0 staging
+      if (op->ws_doubles < need) {
+        op->ws.alloc(static_cast<size_t>(need));
+        op->ws_doubles = need;
       }
+      launch_hybridize_rt0_rows(A, sp->rt0_consts.data(), op->ws.p, st);
     } else if (hybridize_big_supported(sp->dim, sp->k) && !getenv("HDR_CTA_PATH")) {
       const int64_t need = hybridize_big_scratch_doubles(A, sp->k);
       if (op->ws_doubles < need) {

@@ -32,9 +32,6 @@
 #ifndef HDR_ROWS_MINB
 #define HDR_ROWS_MINB 6
 #endif
-#ifndef HDR_RT0_MINB
-#define HDR_RT0_MINB 2
-#endif
 
 namespace hdr {
 
@@ -61,169 +58,6 @@ struct Rt0Const {
   double D[N * N], M[N * N], E[N * N], Ma[N * N], N0[N * N], X[N];
   double lam, rho;
 };
-
-// Deterministic scatter of one RT0 cell's H_T (N x N) and g_T (dpf = 1: one H
-// row per interior face).  Colour 0 stores; colour 1 adds on same-face entries.
-template <int DIM>
-__device__ __forceinline__ void rt0_scatter(const HybArgs& A, int64_t e, int parity, const double (&H)[2 * DIM][2 * DIM],
-                                            const double (&gg)[2 * DIM]) {
-  constexpr int N = 2 * DIM;
-  int64_t cc[3];
-  cell_coords(A.m, e, cc);
-  bool in_lo[3] = {false, false, false}, in_hi[3] = {false, false, false};
-  int64_t own_f[N];
-#pragma unroll
-  for (int q = 0; q < N; ++q) {
-    bool in;
-    own_f[q] = slot_face(A.m, cc, q, &in);
-    if (q & 1)
-      in_hi[q >> 1] = in;
-    else
-      in_lo[q >> 1] = in;
-  }
-#pragma unroll
-  for (int p = 0; p < N; ++p) {
-    const bool pin = (p & 1) ? in_hi[p >> 1] : in_lo[p >> 1];
-    if (!pin) continue;
-    const int a = p >> 1;
-    const int64_t ca = a == 0 ? cc[0] : (a == 1 ? cc[1] : cc[2]);
-    const int64_t na = a == 0 ? A.m.N[0] : (a == 1 ? A.m.N[1] : A.m.N[2]);
-    const int row = A.mbase[own_f[p]];
-    const int64_t start = A.rowoff[row];
-#pragma unroll
-    for (int q = 0; q < N; ++q) {
-      const bool qin = (q & 1) ? in_hi[q >> 1] : in_lo[q >> 1];
-      if (!qin) continue;
-      unsigned lm = 0, hm = 0;
-#pragma unroll
-      for (int x = 0; x < DIM; ++x) {
-        lm |= static_cast<unsigned>(in_lo[x]) << x;
-        hm |= static_cast<unsigned>(in_hi[x]) << x;
-      }
-      const int64_t pos = start + col_rank_fast(DIM, p, q, lm, hm, ca, na, false);
-      A.hval[pos] = (parity == 1 && p == q) ? A.hval[pos] + H[p][q] : H[p][q];
-    }
-    A.g[row] = (parity == 1) ? A.g[row] + gg[p] : gg[p];
-  }
-}
-
-// Cells that need Neumann order P >= 2 (tau > 1e-7; none at BASELINE's
-// coefficient ranges): recomputed here from scalars only, so the fast path's
-// register arrays never have their address taken.
-template <int DIM>
-__device__ __noinline__ void rt0_general(HybArgs A, int64_t e, int parity, int P) {
-  constexpr int N = 2 * DIM;
-  struct {  // fixed factors read from global memory (the kernel's parameter block must not escape)
-    const double *D, *M, *E, *Ma, *N0, *X;
-    double lam;
-  } c{A.fx.D, A.fx.M, A.fx.E, A.fx.Ma, A.fx.N0, A.fx.X, A.fx.lam[0]};
-  const double a = A.alpha[e], b = A.beta[e];
-  const double ib = 1.0 / b;
-  const double s = b / fma(a, c.lam, b);
-  double V[N][N], T[N][N + 1], Y[N][N + 1], H[N][N], gg[N];
-  for (int i = 0; i < N; ++i)
-    for (int j = 0; j < N; ++j) V[i][j] = fma(c.X[i] * s, c.X[j], c.N0[i * N + j]) * ib;
-  for (int i = 0; i < N; ++i) {
-    double acc = 0.0;
-    for (int j = 0; j < N; ++j) {
-      acc = fma(V[i][j], A.f[e * N + j], acc);
-      T[i][j] = V[i][j];
-      H[i][j] = V[i][j];
-    }
-    T[i][N] = acc;
-    gg[i] = acc;
-  }
-  for (int p = 1; p <= P; ++p) {
-    for (int k = 0; k < N; ++k)
-      for (int j = 0; j <= N; ++j) {
-        double acc = 0.0;
-        for (int l = 0; l < N; ++l)
-          acc = fma(delta_entry(a, b, c.D[k * N + l], c.M[k * N + l], c.E[k * N + l], c.Ma[k * N + l]), T[l][j], acc);
-        Y[k][j] = acc;
-      }
-    const double sg = (p & 1) ? -1.0 : 1.0;
-    for (int i = 0; i < N; ++i) {
-      for (int q = 0; q <= N; ++q) {
-        double acc = 0.0;
-        for (int k = 0; k < N; ++k) acc = fma(V[k][i], Y[k][q], acc);
-        if (q < N)
-          H[i][q] = fma(sg, acc, H[i][q]);
-        else
-          gg[i] = fma(sg, acc, gg[i]);
-      }
-    }
-    for (int i = 0; i < N; ++i)  // T <- A0^-1 Y = V Y
-      for (int j = 0; j <= N; ++j) {
-        double acc = 0.0;
-        for (int k = 0; k < N; ++k) acc = fma(V[i][k], Y[k][j], acc);
-        T[i][j] = acc;
-      }
-  }
-  rt0_scatter<DIM>(A, e, parity, H, gg);
-}
-
-template <int DIM, int MINB>
-__global__ void __launch_bounds__(128, MINB) k_hyb_rt0(HybArgs A, Rt0Const<2 * DIM> c, int parity) {
-  constexpr int N = 2 * DIM;
-  const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (t >= parity_count(A.m)) return;
-  const int64_t e = parity_cell(A.m, parity, t);
-  if (e < 0) return;
-  const double a = A.alpha[e], b = A.beta[e];
-  const double ib = 1.0 / b;
-  const int P = neumann_order(c.rho * a * ib, A.p_max, A.status);
-  if (P >= 2) {
-    rt0_general<DIM>(A, e, parity, P);
-    return;
-  }
-  const double s = b / fma(a, c.lam, b);
-  // V = A0^-1 (every dof is a face dof for k = 0; A0^-1 is symmetric: upper
-  // triangle kept, V[j][i] read as V[i][j]), w = A0^-1 f
-  double V[N][N], w[N];
-#define VS(i, j) V[(i) < (j) ? (i) : (j)][(i) < (j) ? (j) : (i)]
-#pragma unroll
-  for (int i = 0; i < N; ++i)
-#pragma unroll
-    for (int j = i; j < N; ++j) V[i][j] = fma(c.X[i] * s, c.X[j], c.N0[i * N + j]) * ib;
-#pragma unroll
-  for (int i = 0; i < N; ++i) w[i] = 0.0;
-#pragma unroll
-  for (int j = 0; j < N; ++j) {
-    const double fj = A.f[e * N + j];
-#pragma unroll
-    for (int i = 0; i < N; ++i) w[i] = fma(VS(i, j), fj, w[i]);
-  }
-  // first order: H = V - V^T (Delta V),  g = w - V^T (Delta w)
-  double H[N][N], gg[N];
-#pragma unroll
-  for (int i = 0; i < N; ++i) {
-    gg[i] = w[i];
-#pragma unroll
-    for (int j = 0; j < N; ++j) H[i][j] = VS(i, j);
-  }
-#pragma unroll
-  for (int k = 0; k < N; ++k) {
-    double yk[N + 1];
-#pragma unroll
-    for (int j = 0; j <= N; ++j) yk[j] = 0.0;
-#pragma unroll
-    for (int l = 0; l < N; ++l) {
-      const double d = delta_entry(a, b, c.D[k * N + l], c.M[k * N + l], c.E[k * N + l], c.Ma[k * N + l]);
-#pragma unroll
-      for (int j = 0; j < N; ++j) yk[j] = fma(d, VS(l, j), yk[j]);
-      yk[N] = fma(d, w[l], yk[N]);
-    }
-#pragma unroll
-    for (int p = 0; p < N; ++p) {
-      const double vkp = -VS(k, p);
-#pragma unroll
-      for (int q = 0; q < N; ++q) H[p][q] = fma(vkp, yk[q], H[p][q]);
-      gg[p] = fma(vkp, yk[N], gg[p]);
-    }
-  }
-#undef VS
-  rt0_scatter<DIM>(A, e, parity, H, gg);
-}
 
 // ------------------------------------------------------------------ k = 0, lane-per-row form
 //
@@ -757,46 +591,6 @@ __global__ void k_average(DevMesh m, const double* x_hat, double* x) {
 }
 
 }  // namespace
-
-void launch_hybridize_rt0(const HybArgs& a, const double* hc, int parity, cudaStream_t st) {
-  const int64_t cnt = parity_count(a.m);
-  const unsigned nb = static_cast<unsigned>((cnt + 127) / 128);
-  if (a.m.dim == 3) {
-    Rt0Const<6> c;
-    constexpr int N = 6;
-    memcpy(c.D, hc, sizeof(double) * N * N);
-    memcpy(c.M, hc + N * N, sizeof(double) * N * N);
-    memcpy(c.E, hc + 2 * N * N, sizeof(double) * N * N);
-    memcpy(c.Ma, hc + 3 * N * N, sizeof(double) * N * N);
-    memcpy(c.N0, hc + 4 * N * N, sizeof(double) * N * N);
-    memcpy(c.X, hc + 5 * N * N, sizeof(double) * N);
-    c.lam = hc[5 * N * N + N];
-    c.rho = hc[5 * N * N + N + 1];
-    static const int variant = [] {
-      const char* v = getenv("HDR_RT0_MINB");
-      return v ? atoi(v) : HDR_RT0_MINB;
-    }();
-    if (variant == 4)
-      k_hyb_rt0<3, 4><<<nb, 128, 0, st>>>(a, c, parity);
-    else if (variant == 3)
-      k_hyb_rt0<3, 3><<<nb, 128, 0, st>>>(a, c, parity);
-    else
-      k_hyb_rt0<3, 2><<<nb, 128, 0, st>>>(a, c, parity);
-  } else {
-    Rt0Const<4> c;
-    constexpr int N = 4;
-    memcpy(c.D, hc, sizeof(double) * N * N);
-    memcpy(c.M, hc + N * N, sizeof(double) * N * N);
-    memcpy(c.E, hc + 2 * N * N, sizeof(double) * N * N);
-    memcpy(c.Ma, hc + 3 * N * N, sizeof(double) * N * N);
-    memcpy(c.N0, hc + 4 * N * N, sizeof(double) * N * N);
-    memcpy(c.X, hc + 5 * N * N, sizeof(double) * N);
-    c.lam = hc[5 * N * N + N];
-    c.rho = hc[5 * N * N + N + 1];
-    k_hyb_rt0<2, 4><<<nb, 128, 0, st>>>(a, c, parity);
-  }
-  count_launch();
-}
 
 void launch_hybridize_rt0_rows(const HybArgs& a, const double* hc, double* stage, cudaStream_t st) {
   const int64_t cnt = parity_count(a.m);

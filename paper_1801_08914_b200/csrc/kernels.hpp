@@ -46,8 +46,6 @@ struct HybArgs {
 // 4-bit column ranks (own slots, then the neighbour's slots; 15 = absent).
 std::vector<uint64_t> rank_table_rt0(int dim);
 
-// Small-element path (k = 0): one thread per cell, everything in registers.
-void launch_hybridize_rt0(const HybArgs& a, const double* host_consts, int parity, cudaStream_t st);
 // k = 0, lane-per-row form with row-complete writes (stage: parity_count * N*(N+1) doubles)
 void launch_hybridize_rt0_rows(const HybArgs& a, const double* host_consts, double* stage, cudaStream_t st);
 // k >= 1 with nF + 1 <= 32 (RT1 hexes, RT1..RT3 quads): one warp per cell (kern_warp.cu)
