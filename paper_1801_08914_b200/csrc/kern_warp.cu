@@ -37,12 +37,26 @@ struct Shape {
 
 constexpr int kWarps = 4;  // cells per CTA
 
+// threads cooperating on one cell: one warp (2D), four warps (3D RT1: 36 x 25
+// outputs per GEMM, so 128 threads with 3 x 3 tiles keep every thread busy and
+// the per-SM cell count is set by shared memory, not by registers)
 template <int DIM, int K>
-struct Tiles;  // register tiles (TM x TN per lane) of the three warp GEMMs
-template <> struct Tiles<3, 1> { static constexpr int V_M = 6, V_N = 5, Y_M = 6, Y_N = 5, C_M = 4, C_N = 5; };
+struct Group {
+  static constexpr int GT = (DIM == 3 && K == 1) ? 128 : 32;
+};
+
+template <int DIM, int K>
+struct Tiles;  // register tiles (TM x TN per thread) of the three GEMMs
+template <> struct Tiles<3, 1> { static constexpr int V_M = 3, V_N = 3, Y_M = 3, Y_N = 3, C_M = 2, C_N = 3; };
 template <> struct Tiles<2, 1> { static constexpr int V_M = 3, V_N = 3, Y_M = 3, Y_N = 3, C_M = 2, C_N = 3; };
 template <> struct Tiles<2, 2> { static constexpr int V_M = 4, V_N = 4, Y_M = 4, Y_N = 4, C_M = 3, C_N = 4; };
 template <> struct Tiles<2, 3> { static constexpr int V_M = 5, V_N = 6, Y_M = 5, Y_N = 6, C_M = 4, C_N = 5; };
+
+template <int GT>
+__device__ __forceinline__ void gsync() {
+  if (GT == 32) __syncwarp();
+  else __syncthreads();
+}
 
 template <int DIM, int K>
 struct WarpSmem {
@@ -61,6 +75,7 @@ struct WarpSmem {
   int rlen[2 * DIM];          // H row length of that face's rows
   int grow[2 * DIM];          // multiplier index of the face's first row
   int rank[4 * DIM * DIM];    // column-block rank of own slot t in the rows of slot s (-1: boundary)
+  float red[8];               // cross-warp reduction scratch
 };
 
 template <int DIM, int K>
@@ -73,11 +88,11 @@ struct CtaShared {  // fixed per space, staged once per CTA
 // C[M x NN] = A[M x KK] * B[KK x NN] on one warp, operands in shared memory:
 // A given transposed (at[k * lda + m]), B row-major (b[k * ldb + n]).  Each
 // lane owns a TM x TN register tile; tiles beyond 32 lanes loop.
-template <int M, int NN, int KK, int TM, int TN, class T = float>
+template <int M, int NN, int KK, int TM, int TN, int GT, class T = float>
 __device__ __forceinline__ void warp_gemm(const T* at, int lda, const T* bm, int ldb, T* cm, int ldc, int lane,
                                           T scale_in = T(0), bool accumulate = false) {
   constexpr int TMS = (M + TM - 1) / TM, TNS = (NN + TN - 1) / TN;
-  for (int tile = lane; tile < TMS * TNS; tile += 32) {
+  for (int tile = lane; tile < TMS * TNS; tile += GT) {
     const int m0 = (tile / TNS) * TM, n0 = (tile % TNS) * TN;
     T acc[TM][TN];
 #pragma unroll
@@ -118,6 +133,7 @@ constexpr int64_t scratch_doubles_per_warp() {
 template <int DIM, int K>
 __device__ __forceinline__ void warp_cell(const HybArgs& A, int e, int parity, int lane, WarpSmem<DIM, K>& sm,
                                           const CtaShared<DIM, K>& cs, double* scratch) {
+  constexpr int GT = Group<DIM, K>::GT;  // "lane" is the thread index within the cell's group
   using S = Shape<DIM, K>;
   using SM = WarpSmem<DIM, K>;
   using TL = Tiles<DIM, K>;
@@ -127,21 +143,21 @@ __device__ __forceinline__ void warp_cell(const HybArgs& A, int e, int parity, i
   const double a = A.alpha[e], b = A.beta[e];
   const double ib = 1.0 / b;
   const double* fe = A.f + static_cast<int64_t>(e) * N;
-  for (int i = lane; i < N; i += 32) sm.f[i] = fe[i];
-  for (int j = lane; j < R; j += 32) sm.s[j] = b / fma(a, __ldg(fx.lam + j), b);
-  __syncwarp();
-  for (int i = lane; i < N; i += 32) {
+  for (int i = lane; i < N; i += GT) sm.f[i] = fe[i];
+  for (int j = lane; j < R; j += GT) sm.s[j] = b / fma(a, __ldg(fx.lam + j), b);
+  gsync<GT>();
+  for (int i = lane; i < N; i += GT) {
     double acc = 0.0;
 #pragma unroll 6
     for (int l = 0; l < N; ++l) acc = fma(cs.n0[i * N + l], sm.f[l], acc);
     sm.nf[i] = acc;
   }
   // z = [s X_F^T | s X^T f]; the X^T f dots are split over 4 lanes each
-  for (int idx = lane; idx < R * NF; idx += 32) {
+  for (int idx = lane; idx < R * NF; idx += GT) {
     const int j = idx / NF, c = idx - j * NF;
     sm.z[j * NC + c] = sm.s[j] * cs.xt[j * N + NINT + c];
   }
-  for (int j0 = 0; j0 < R; j0 += 8) {
+  for (int j0 = 0; j0 < R; j0 += GT / 4) {
     const int j = j0 + (lane >> 2), part = lane & 3;
     double acc = 0.0;
     if (j < R)
@@ -150,13 +166,13 @@ __device__ __forceinline__ void warp_cell(const HybArgs& A, int e, int parity, i
     acc += __shfl_xor_sync(0xffffffffu, acc, 2);
     if (j < R && part == 0) sm.z[j * NC + NF] = sm.s[j] * acc;
   }
-  __syncwarp();
+  gsync<GT>();
   // [V | w] = (base + X z) / beta, base = N0_:,F | N0 f: register tiles over (rows, cols),
   // fp32 copy for the correction GEMMs, fp64 face rows kept for H0 / g0
   {
     constexpr int TM = TL::V_M, TN = TL::V_N;
     constexpr int TMS = (N + TM - 1) / TM, TNS = (NC + TN - 1) / TN;
-    for (int tile = lane; tile < TMS * TNS; tile += 32) {
+    for (int tile = lane; tile < TMS * TNS; tile += GT) {
       const int m0 = (tile / TNS) * TM, n0 = (tile % TNS) * TN;
       double acc[TM][TN];
 #pragma unroll
@@ -189,21 +205,21 @@ __device__ __forceinline__ void warp_cell(const HybArgs& A, int e, int parity, i
     }
   }
   // Delta32^T (fp64 exact rounding errors -> fp32)
-  for (int idx = lane; idx < N * N; idx += 32) {
+  for (int idx = lane; idx < N * N; idx += GT) {
     const int i = idx / N, l = idx - i * N;
     sm.d32t[l * N + i] = static_cast<float>(
         delta_entry(a, b, __ldg(fx.D + idx), __ldg(fx.M + idx), __ldg(fx.E + idx), __ldg(fx.Ma + idx)));
   }
-  __syncwarp();
+  gsync<GT>();
   // first order: Y = Delta32 [V | w];  C = V_F^T Y
-  warp_gemm<N, NC, N, TL::Y_M, TL::Y_N>(sm.d32t, N, sm.v32, NCP, sm.y32, NCP, lane);
-  __syncwarp();
+  warp_gemm<N, NC, N, TL::Y_M, TL::Y_N, GT>(sm.d32t, N, sm.v32, NCP, sm.y32, NCP, lane);
+  gsync<GT>();
   float* corr = sm.corr;
-  warp_gemm<NF, NC, N, TL::C_M, TL::C_N>(sm.v32, NCP, sm.y32, NCP, corr, NCP, lane);
-  __syncwarp();
+  warp_gemm<NF, NC, N, TL::C_M, TL::C_N, GT>(sm.v32, NCP, sm.y32, NCP, corr, NCP, lane);
+  gsync<GT>();
   // a-posteriori size of the first-order term: 10 (|C|/|H0|)^2 <= 1e-12 -> order 1 suffices
   float cmax = 0.f, hmax = 0.f;
-  for (int idx = lane; idx < NF * NF; idx += 32) {
+  for (int idx = lane; idx < NF * NF; idx += GT) {
     const int p = idx / NF, q = idx - p * NF;
     cmax = fmaxf(cmax, fabsf(corr[p * NCP + q]));
     hmax = fmaxf(hmax, fabsf(sm.v32[(NINT + p) * NCP + q]));
@@ -211,6 +227,18 @@ __device__ __forceinline__ void warp_cell(const HybArgs& A, int e, int parity, i
   for (int o = 16; o > 0; o >>= 1) {
     cmax = fmaxf(cmax, __shfl_xor_sync(0xffffffffu, cmax, o));
     hmax = fmaxf(hmax, __shfl_xor_sync(0xffffffffu, hmax, o));
+  }
+  if (GT > 32) {  // across the group's warps
+    if ((lane & 31) == 0) {
+      sm.red[2 * (lane >> 5)] = cmax;
+      sm.red[2 * (lane >> 5) + 1] = hmax;
+    }
+    gsync<GT>();
+    for (int w = 0; w < GT / 32; ++w) {
+      cmax = fmaxf(cmax, sm.red[2 * w]);
+      hmax = fmaxf(hmax, sm.red[2 * w + 1]);
+    }
+    gsync<GT>();
   }
   const double ratio = hmax > 0.f ? static_cast<double>(cmax) / hmax : 0.0;
   int P = 1;
@@ -224,25 +252,25 @@ __device__ __forceinline__ void warp_cell(const HybArgs& A, int e, int parity, i
   }
   // higher orders (rare): T = A0^-1 Y, Y <- Delta32 T, C += (-1)^(p+1) V_F^T Y (C is subtracted)
   for (int p = 2; p <= P; ++p) {
-    for (int idx = lane; idx < R * NC; idx += 32) {
+    for (int idx = lane; idx < R * NC; idx += GT) {
       const int j = idx / NC, c = idx - j * NC;
       double acc = 0.0;
       for (int l = 0; l < N; ++l) acc = fma(cs.xt[j * N + l], static_cast<double>(sm.y32[l * NCP + c]), acc);
       sm.z[idx] = sm.s[j] * acc;
     }
-    __syncwarp();
-    for (int idx = lane; idx < N * NC; idx += 32) {
+    gsync<GT>();
+    for (int idx = lane; idx < N * NC; idx += GT) {
       const int i = idx / NC, c = idx - i * NC;
       double acc = 0.0;
       for (int l = 0; l < N; ++l) acc = fma(cs.n0[i * N + l], static_cast<double>(sm.y32[l * NCP + c]), acc);
       for (int j = 0; j < R; ++j) acc = fma(cs.xt[j * N + i], sm.z[j * NC + c], acc);
       tbuf[i * NCP + c] = static_cast<float>(acc * ib);
     }
-    __syncwarp();
-    warp_gemm<N, NC, N, TL::Y_M, TL::Y_N>(sm.d32t, N, tbuf, NCP, sm.y32, NCP, lane);
-    __syncwarp();
-    warp_gemm<NF, NC, N, TL::C_M, TL::C_N>(sm.v32, NCP, sm.y32, NCP, corr, NCP, lane, (p & 1) ? 1.f : -1.f, true);
-    __syncwarp();
+    gsync<GT>();
+    warp_gemm<N, NC, N, TL::Y_M, TL::Y_N, GT>(sm.d32t, N, tbuf, NCP, sm.y32, NCP, lane);
+    gsync<GT>();
+    warp_gemm<NF, NC, N, TL::C_M, TL::C_N, GT>(sm.v32, NCP, sm.y32, NCP, corr, NCP, lane, (p & 1) ? 1.f : -1.f, true);
+    gsync<GT>();
   }
   // scatter: H_pc = V_F(p, c) (fp64) - C_pc ; g_p = w_F(p) - C_p,NF.  Per-cell tables
   // (row starts / lengths of each face slot, column-block ranks) first, then one
@@ -263,7 +291,7 @@ __device__ __forceinline__ void warp_cell(const HybArgs& A, int e, int parity, i
       lo |= static_cast<unsigned>(cx > 0) << x;
       hi |= static_cast<unsigned>(cx + 1 < Nx) << x;
     }
-    for (int idx = lane; idx < NS * NS; idx += 32) {
+    for (int idx = lane; idx < NS * NS; idx += GT) {
       const int ps = idx / NS, qs = idx - ps * NS;
       const int a_ = ps >> 1;
       const bool pin = (((ps & 1) ? hi : lo) >> a_) & 1u;
@@ -287,8 +315,8 @@ __device__ __forceinline__ void warp_cell(const HybArgs& A, int e, int parity, i
       }
     }
   }
-  __syncwarp();
-  for (int idx = lane; idx < NF * NC; idx += 32) {
+  gsync<GT>();
+  for (int idx = lane; idx < NF * NC; idx += GT) {
     const int p = idx / NC, c = idx - p * NC;
     const int ps = p / DPF, sub = p - ps * DPF;
     const int64_t rs = sm.rstart[ps];
@@ -305,15 +333,17 @@ __device__ __forceinline__ void warp_cell(const HybArgs& A, int e, int parity, i
     double* hp = A.hval + rs + static_cast<int64_t>(sub) * sm.rlen[ps] + rk * DPF + sj;
     *hp = (parity == 1 && ps == qs) ? *hp + v : v;
   }
-  __syncwarp();
+  gsync<GT>();
 }
 
 template <int DIM, int K>
 __global__ void __launch_bounds__(32 * kWarps) k_hyb_warp(HybArgs A, int parity, double* gws) {
+  constexpr int GT = Group<DIM, K>::GT;
+  constexpr int CPB = 32 * kWarps / GT;  // cells per CTA iteration
   extern __shared__ __align__(16) unsigned char smem_raw[];
   auto* cs = reinterpret_cast<CtaShared<DIM, K>*>(smem_raw);
-  auto* sm = reinterpret_cast<WarpSmem<DIM, K>*>(smem_raw + ((sizeof(CtaShared<DIM, K>) + 15) & ~size_t(15))) +
-             (threadIdx.x >> 5);
+  const int grp = threadIdx.x / GT, tid = threadIdx.x - grp * GT;
+  auto* sm = reinterpret_cast<WarpSmem<DIM, K>*>(smem_raw + ((sizeof(CtaShared<DIM, K>) + 15) & ~size_t(15))) + grp;
   using S = Shape<DIM, K>;
   for (int idx = threadIdx.x; idx < S::R * S::N; idx += blockDim.x) {
     const int j = idx / S::N, i = idx - j * S::N;
@@ -321,25 +351,30 @@ __global__ void __launch_bounds__(32 * kWarps) k_hyb_warp(HybArgs A, int parity,
   }
   for (int idx = threadIdx.x; idx < S::N * S::N; idx += blockDim.x) cs->n0[idx] = __ldg(A.fx.N0 + idx);
   __syncthreads();
-  const int lane = threadIdx.x & 31;
-  double* scratch = gws + (static_cast<int64_t>(blockIdx.x) * kWarps + (threadIdx.x >> 5)) * scratch_doubles_per_warp<DIM, K>();
+  double* scratch = gws + (static_cast<int64_t>(blockIdx.x) * CPB + grp) * scratch_doubles_per_warp<DIM, K>();
   const uint32_t cnt = static_cast<uint32_t>(parity_count(A.m));
-  for (uint32_t t = blockIdx.x * kWarps + (threadIdx.x >> 5); t < cnt; t += gridDim.x * kWarps) {
+  // the loop bound is uniform over each group (a group never splits on it)
+  for (uint32_t t0 = blockIdx.x * CPB; t0 < cnt; t0 += gridDim.x * CPB) {
+    const uint32_t t = t0 + grp;
     int cc[3];
-    const int e = parity_cell32(A.m, parity, t, cc);
-    if (e < 0) continue;
-    warp_cell<DIM, K>(A, e, parity, lane, *sm, *cs, scratch);
+    const int e = t < cnt ? parity_cell32(A.m, parity, t, cc) : -1;
+    if (GT > 32) {  // one cell per CTA: skip together
+      if (e < 0) continue;
+    } else if (e < 0) {
+      continue;
+    }
+    warp_cell<DIM, K>(A, e, parity, tid, *sm, *cs, scratch);
   }
 }
 
 template <int DIM, int K>
 size_t smem_t() {
-  return ((sizeof(CtaShared<DIM, K>) + 15) & ~size_t(15)) + sizeof(WarpSmem<DIM, K>) * kWarps;
+  return ((sizeof(CtaShared<DIM, K>) + 15) & ~size_t(15)) + sizeof(WarpSmem<DIM, K>) * (32 * kWarps / Group<DIM, K>::GT);
 }
 
 template <int DIM, int K>
 int64_t scratch_doubles_t(int64_t grid) {
-  return grid * kWarps * scratch_doubles_per_warp<DIM, K>();
+  return grid * (32 * kWarps / Group<DIM, K>::GT) * scratch_doubles_per_warp<DIM, K>();
 }
 
 template <int DIM, int K>
@@ -351,7 +386,8 @@ int64_t grid_t(const HybArgs& a) {
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_hyb_warp<DIM, K>, 32 * kWarps, smem);
-  const int64_t want = (cnt + kWarps - 1) / kWarps;
+  const int64_t cpb = 32 * kWarps / Group<DIM, K>::GT;
+  const int64_t want = (cnt + cpb - 1) / cpb;
   return std::max<int64_t>(1, std::min<int64_t>(want, static_cast<int64_t>(sms) * std::max(per_sm, 1)));
 }
 
