@@ -122,6 +122,60 @@ __device__ __forceinline__ void warp_gemm(const T* at, int lda, const T* bm, int
   }
 }
 
+// C[M x NN] (+)= A[M x KK] * B[KK x NN] in fp32 with 4 x 4 register tiles and
+// 128-bit shared-memory loads, K split over SPLIT consecutive threads (reduced
+// with shuffles): at[k * lda + m] and bm[k * ldb + n] must be readable up to the
+// next multiple of 4 in m and n (padded rows), lda, ldb multiples of 4.
+template <int M, int NN, int KK, int SPLIT, int GT>
+__device__ __forceinline__ void gemm44(const float* at, int lda, const float* bm, int ldb, float* cm, int ldc, int tid,
+                                       float scale_in = 0.f, bool accumulate = false) {
+  constexpr int TMS = (M + 3) / 4, TNS = (NN + 3) / 4, KS = (KK + SPLIT - 1) / SPLIT;
+  static_assert(TMS * TNS * SPLIT <= GT, "tiles x split must fit the group (one pass)");
+  static_assert(SPLIT == 1 || SPLIT == 2 || SPLIT == 4, "split within aligned lane pairs / quads");
+  const bool active = tid < TMS * TNS * SPLIT;  // every thread reaches the shuffles
+  const int tile = tid / SPLIT, part = tid - tile * SPLIT;
+  const int m0 = (tile / TNS) * 4, n0 = (tile % TNS) * 4;
+  float acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
+  if (active) {
+    const int k0 = part * KS, k1 = min(KK, k0 + KS);
+#pragma unroll 4
+    for (int k = k0; k < k1; ++k) {
+      const float4 av = *reinterpret_cast<const float4*>(at + k * lda + m0);
+      const float4 bv = *reinterpret_cast<const float4*>(bm + k * ldb + n0);
+      const float a4[4] = {av.x, av.y, av.z, av.w}, b4[4] = {bv.x, bv.y, bv.z, bv.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a4[i], b4[j], acc[i][j]);
+    }
+  }
+  if (SPLIT > 1) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        float v = acc[i][j];
+        v += __shfl_xor_sync(0xffffffffu, v, 1);
+        if (SPLIT == 4) v += __shfl_xor_sync(0xffffffffu, v, 2);
+        acc[i][j] = v;
+      }
+  }
+  if (active && part == 0) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (m0 + i < M && n0 + j < NN) {
+          float* dst = cm + (m0 + i) * ldc + n0 + j;
+          *dst = accumulate ? fmaf(scale_in, acc[i][j], *dst) : acc[i][j];
+        }
+  }
+}
+
 // per-warp global scratch: the higher-order buffer T (N x NCP fp32), rarely used
 template <int DIM, int K>
 constexpr int64_t scratch_doubles_per_warp() {
@@ -212,10 +266,16 @@ __device__ __forceinline__ void warp_cell(const HybArgs& A, int e, int parity, i
   }
   gsync<GT>();
   // first order: Y = Delta32 [V | w];  C = V_F^T Y
-  warp_gemm<N, NC, N, TL::Y_M, TL::Y_N, GT>(sm.d32t, N, sm.v32, NCP, sm.y32, NCP, lane);
-  gsync<GT>();
   float* corr = sm.corr;
-  warp_gemm<NF, NC, N, TL::C_M, TL::C_N, GT>(sm.v32, NCP, sm.y32, NCP, corr, NCP, lane);
+  if constexpr (GT == 128) {
+    gemm44<N, NC, N, 2, GT>(sm.d32t, N, sm.v32, NCP, sm.y32, NCP, lane);
+    gsync<GT>();
+    gemm44<NF, NC, N, 2, GT>(sm.v32, NCP, sm.y32, NCP, corr, NCP, lane);
+  } else {
+    warp_gemm<N, NC, N, TL::Y_M, TL::Y_N, GT>(sm.d32t, N, sm.v32, NCP, sm.y32, NCP, lane);
+    gsync<GT>();
+    warp_gemm<NF, NC, N, TL::C_M, TL::C_N, GT>(sm.v32, NCP, sm.y32, NCP, corr, NCP, lane);
+  }
   gsync<GT>();
   // a-posteriori size of the first-order term: 10 (|C|/|H0|)^2 <= 1e-12 -> order 1 suffices
   float cmax = 0.f, hmax = 0.f;
