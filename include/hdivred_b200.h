@@ -280,6 +280,9 @@ int64_t hdr_launch_count(void);
 /* FP64 FMA throughput of device 0 in TFLOP/s (2 flops per DFMA), measured with
  * a register-resident DFMA chain kernel; the fp64 roofline denominator. */
 hdr_status hdr_measure_fp64_peak(double* tflops, double* ms);
+/* Self-test of the tcgen05 TF32 tensor-core path (kern_umma.cu): D (128 x n) =
+ * A (128 x k, row-major) * B^T (B: n x k, row-major), split = 1: 3xTF32.  Host arrays. */
+hdr_status hdr_umma_selftest(int n, int k, const float* a, const float* b, float* d, int split);
 /* Synchronize the space's stream. */
 hdr_status hdr_space_synchronize(hdr_space_t space);
 

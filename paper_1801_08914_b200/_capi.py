@@ -80,6 +80,7 @@ _SIGS = {
     "hdr_space_set_vertices": (_i32, [_vp, _vp]),
     "hdr_space_element_matrices": (_i32, [_vp, _vp]),
     "hdr_hybrid_symmetrize": (_i32, [_vp]),
+    "hdr_umma_selftest": (_i32, [_i32, _i32, _vp, _vp, _vp, _i32]),
     "hdr_last_error": (ctypes.c_char_p, []),
     "hdr_version": (ctypes.c_char_p, []),
     "hdr_launch_count": (_i64, []),

@@ -1,0 +1,98 @@
+// Minimal tcgen05 (5th-generation tensor core) helpers for sm_100a: TMEM
+// allocation, shared-memory matrix descriptors (no-swizzle K-major canonical
+// layout), the TF32 MMA, commit-to-mbarrier and TMEM -> register loads.
+//
+// Canonical K-major SWIZZLE_NONE layout of an (MN x K) fp32/tf32 operand tile:
+// 8-row x 16-byte core matrices (8 rows x 4 K-elements, 128 contiguous bytes);
+// core matrices adjacent in MN are SBO bytes apart, adjacent in K LBO bytes.
+// With MN-blocks contiguous:  byte(mn, k) = ((k/4) * (MN/8) + mn/8) * 128
+//                                          + (mn%8) * 16 + (k%4) * 4,
+// SBO = 128, LBO = MN/8 * 128; one K=8 MMA step spans two K chunks (2 LBO).
+#pragma once
+
+#include <cstdint>
+
+namespace hdr {
+namespace umma {
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+
+// byte offset of element (mn, k) in the canonical layout of an MN-row tile
+__device__ __forceinline__ uint32_t kmajor_offset(int mn, int k, int MN) {
+  return static_cast<uint32_t>((((k >> 2) * (MN >> 3) + (mn >> 3)) << 7) + ((mn & 7) << 4) + ((k & 3) << 2));
+}
+
+// shared-memory matrix descriptor (Blackwell version 1, no swizzle)
+__device__ __forceinline__ uint64_t smem_desc(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFFu);
+  d |= static_cast<uint64_t>((lbo_bytes >> 4) & 0x3FFFu) << 16;
+  d |= static_cast<uint64_t>((sbo_bytes >> 4) & 0x3FFFu) << 32;
+  d |= static_cast<uint64_t>(1) << 46;  // version
+  return d;                             // base offset 0, lbo mode 0, layout SWIZZLE_NONE (0)
+}
+
+// instruction descriptor: D f32, A/B tf32, both K-major, M x N
+__host__ __device__ constexpr uint32_t idesc_tf32(int M, int N) {
+  return (1u << 4)                                   // c_format F32
+         | (2u << 7) | (2u << 10)                    // a, b format TF32
+         | (static_cast<uint32_t>(N >> 3) << 17)     // n_dim
+         | (static_cast<uint32_t>(M >> 4) << 24);    // m_dim
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, bool acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc ? 1u : 0u));
+}
+
+__device__ __forceinline__ void commit(uint64_t* mbar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(mbar))
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* mbar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(mbar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* mbar, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred done;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1;\n\t"
+      "@!done bra WAIT_%=;\n\t}\n" ::"r"(smem_u32(mbar)),
+      "r"(phase)
+      : "memory");
+}
+
+__device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+// generic-proxy shared-memory writes -> visible to the tensor core's async proxy
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// one warp: allocate ncols (power of two >= 32) TMEM columns; address -> *slot
+__device__ __forceinline__ void tmem_alloc(uint32_t* slot, uint32_t ncols) {
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(slot)), "r"(ncols)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t ncols) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
+}
+
+// warp w reads TMEM lanes [32w, 32w + 32): thread t gets 8 consecutive 32-bit
+// columns of lane 32w + t starting at column col
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr_lane_col, float (&v)[8]) {
+  uint32_t r[8];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr_lane_col));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+}  // namespace umma
+}  // namespace hdr
