@@ -1,4 +1,4 @@
-// Structured element solve for RT2 / RT3 hexahedra: one 256-thread CTA per
+// Structured element solve for RT2 / RT3 hexahedra: one 512-thread CTA per
 // cell (n = 108 / 240 local dofs, nF = 54 / 96 face dofs).
 //
 // Same mathematics as kern_warp.cu (fp64 V = A0^-1 [E_F | f_T]; fp32 first-order
@@ -13,9 +13,11 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 
 #include "hdr_device.cuh"
 #include "kernels.hpp"
+#include "umma.cuh"
 
 namespace hdr {
 namespace {
@@ -36,9 +38,20 @@ struct Big {
   static constexpr int VT_M = (K == 3) ? 4 : 3, VT_N = (K == 3) ? 6 : 3;
   static constexpr int CT_M = (K == 3) ? 6 : 3, CT_N = (K == 3) ? 7 : 4;
   static constexpr int NS = 6;
+  // tensor-core (tcgen05, 3xTF32) shapes of the first-order correction:
+  //   Y (MP x NP, MT1 M-tiles of 128) = Delta (MP x KP) V (KP x NP);  C (128 x NP) = V_F^T Y
+  static constexpr int MT1 = (N + 127) / 128, MP = MT1 * 128;
+  static constexpr int NP = (NC + 15) / 16 * 16, KP = (N + 15) / 16 * 16;
+  static constexpr int KC = 16;  // K per operand chunk (two K=8 MMA steps)
+  static constexpr int TCOLS_USED = (MT1 + 1) * NP;
+  static constexpr int TCOLS = TCOLS_USED <= 32 ? 32 : TCOLS_USED <= 64 ? 64 : TCOLS_USED <= 128 ? 128 : TCOLS_USED <= 256 ? 256 : 512;
 };
 
-constexpr int kThreads = 256;
+#ifndef HDR_TC_TAU
+#define HDR_TC_TAU 1e-6
+#endif
+
+constexpr int kThreads = 512;
 
 template <int K>
 struct BigSmem {
@@ -53,12 +66,19 @@ struct BigSmem {
       float dt[B::N * B::IB];  // Delta32 block transposed: dt[l * IB + ii]
       float y[B::IB * B::NCP];
     } pc;
+    struct {  // tcgen05 operand chunks (canonical K-major, no swizzle), hi / lo tf32 parts
+      float ahi[B::MP * B::KC], alo[B::MP * B::KC];
+      float bhi[B::NP * B::KC], blo[B::NP * B::KC];
+    } tc;
+    float csm[B::NF * B::NCP];  // the correction C (NF x NC) for the scatter
   } u;
   double f[B::N], nf[B::N], s[B::R];
   long long rstart[B::NS];
   int rlen[B::NS], grow[B::NS], rank[B::NS * B::NS];
   float red[2 * kThreads / 32];
   int order;
+  uint64_t mbar;
+  uint32_t tmem;
 };
 
 template <int K>
@@ -68,14 +88,142 @@ constexpr int64_t big_scratch_doubles() {
   return static_cast<int64_t>(B::NF) * B::NC + static_cast<int64_t>(B::N) * B::NCP + 16;
 }
 
+__device__ __forceinline__ void tf32_split(float x, float& hi, float& lo) {
+  uint32_t h, l;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(x));
+  hi = __uint_as_float(h);
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(l) : "f"(x - hi));
+  lo = __uint_as_float(l);
+}
+
+// First-order correction on the tensor cores (3xTF32):
+//   Y = Delta V  (Y in TMEM, MT1 tiles of 128 rows),  C = V[:, F]^T Y  (C in TMEM),
+// operands generated chunk by chunk (K = 16) straight into the canonical
+// shared-memory layout; one thread issues the MMAs, everyone waits on the
+// commit mbarrier before the buffers are refilled.  C -> sm.u.csm.
 template <int K>
-__global__ void __launch_bounds__(kThreads, 1) k_hyb_big(HybArgs A, int parity, double* gws) {
+__device__ void correction_tc(BigSmem<K>& sm, const Fixed& fx, double a, double b, uint32_t& phase) {
+  using B = Big<K>;
+  constexpr int N = B::N, NF = B::NF, NC = B::NC, NCP = B::NCP, NINT = B::NINT;
+  constexpr int MP = B::MP, NP = B::NP, KP = B::KP, KC = B::KC, MT1 = B::MT1;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t tY = sm.tmem, tC = sm.tmem + MT1 * NP;
+  constexpr uint32_t idesc = umma::idesc_tf32(128, NP);
+  constexpr uint32_t lbo_a = (MP / 8) * 128, lbo_b = (NP / 8) * 128, lbo_a2 = (128 / 8) * 128;
+  auto& T = sm.u.tc;
+  // ---- Y = Delta V
+  for (int kc = 0; kc < KP; kc += KC) {
+    for (int idx = tid; idx < MP * KC; idx += kThreads) {
+      const int m = idx / KC, k = idx - m * KC, col = kc + k;
+      float x = 0.f;
+      if (m < N && col < N) {
+        const int64_t o = static_cast<int64_t>(m) * N + col;
+        x = static_cast<float>(delta_entry(a, b, __ldg(fx.D + o), __ldg(fx.M + o), __ldg(fx.E + o), __ldg(fx.Ma + o)));
+      }
+      const uint32_t off = umma::kmajor_offset(m, k, MP) >> 2;
+      tf32_split(x, T.ahi[off], T.alo[off]);
+    }
+    for (int idx = tid; idx < NP * KC; idx += kThreads) {
+      const int n = idx / KC, k = idx - n * KC, row = kc + k;
+      const float x = (n < NC && row < N) ? sm.v32[row * NCP + n] : 0.f;
+      const uint32_t off = umma::kmajor_offset(n, k, NP) >> 2;
+      tf32_split(x, T.bhi[off], T.blo[off]);
+    }
+    umma::fence_proxy_async();
+    __syncthreads();
+    if (tid == 0) {
+      umma::fence_after();
+      for (int ks = 0; ks < KC / 8; ++ks)
+        for (int t = 0; t < MT1; ++t)
+          for (int term = 0; term < 3; ++term) {
+            const float* aop = term == 2 ? T.alo : T.ahi;
+            const float* bop = term == 1 ? T.blo : T.bhi;
+            const uint64_t ad = umma::smem_desc(umma::smem_u32(aop) + t * 2048 + ks * 2 * lbo_a, lbo_a, 128);
+            const uint64_t bd = umma::smem_desc(umma::smem_u32(bop) + ks * 2 * lbo_b, lbo_b, 128);
+            umma::mma_tf32(tY + t * NP, ad, bd, idesc, kc > 0 || ks > 0 || term > 0);
+          }
+      umma::commit(&sm.mbar);
+    }
+    umma::mbar_wait(&sm.mbar, phase);
+    phase ^= 1u;
+    umma::fence_after();
+  }
+  // ---- C = V_F^T Y  (B operand: rows of Y read back from TMEM)
+  for (int kc = 0; kc < KP; kc += KC) {
+    for (int idx = tid; idx < 128 * KC; idx += kThreads) {
+      const int m = idx / KC, k = idx - m * KC, row = kc + k;
+      const float x = (m < NF && row < N) ? sm.v32[row * NCP + m] : 0.f;  // column m of V = A0^-1 E_F
+      const uint32_t off = umma::kmajor_offset(m, k, 128) >> 2;
+      tf32_split(x, T.ahi[off], T.alo[off]);
+    }
+    {
+      const int t = kc / 128, l0 = kc - t * 128, q = l0 >> 5, lo = l0 & 31;
+      if ((warp & 3) == q) {  // the warps of TMEM lane quadrant q share the columns, 8 at a time
+        for (int c = 8 * (warp >> 2); c < NP; c += 8 * (kThreads / 128)) {
+          float v[8];
+          umma::tmem_ld8(tY + t * NP + (static_cast<uint32_t>(32 * q) << 16) + c, v);
+          if (lane >= lo && lane < lo + KC) {
+            const int k = lane - lo;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const uint32_t off = umma::kmajor_offset(c + j, k, NP) >> 2;
+              tf32_split(v[j], T.bhi[off], T.blo[off]);
+            }
+          }
+        }
+      }
+    }
+    umma::fence_proxy_async();
+    umma::fence_before();
+    __syncthreads();
+    if (tid == 0) {
+      umma::fence_after();
+      for (int ks = 0; ks < KC / 8; ++ks)
+        for (int term = 0; term < 3; ++term) {
+          const float* aop = term == 2 ? T.alo : T.ahi;
+          const float* bop = term == 1 ? T.blo : T.bhi;
+          const uint64_t ad = umma::smem_desc(umma::smem_u32(aop) + ks * 2 * lbo_a2, lbo_a2, 128);
+          const uint64_t bd = umma::smem_desc(umma::smem_u32(bop) + ks * 2 * lbo_b, lbo_b, 128);
+          umma::mma_tf32(tC, ad, bd, idesc, kc > 0 || ks > 0 || term > 0);
+        }
+      umma::commit(&sm.mbar);
+    }
+    umma::mbar_wait(&sm.mbar, phase);
+    phase ^= 1u;
+    umma::fence_after();
+  }
+  // ---- C -> shared memory
+  {
+    const int q = warp & 3, m = 32 * q + lane;
+    for (int c = 8 * (warp >> 2); c < NP; c += 8 * (kThreads / 128)) {
+      float v[8];
+      umma::tmem_ld8(tC + (static_cast<uint32_t>(32 * q) << 16) + c, v);
+      if (m < NF)
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          if (c + j < NC) sm.u.csm[m * NCP + c + j] = v[j];
+    }
+  }
+  umma::fence_before();
+  __syncthreads();
+}
+
+template <int K>
+__global__ void __launch_bounds__(kThreads, 1) k_hyb_big(HybArgs A, int parity, double* gws, int use_tc) {
   using B = Big<K>;
   constexpr int N = B::N, NF = B::NF, NC = B::NC, NCP = B::NCP, R = B::R, NINT = B::NINT, DPF = B::DPF;
   constexpr int IB = B::IB, NS = B::NS;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   BigSmem<K>& sm = *reinterpret_cast<BigSmem<K>*>(smem_raw);
   const int tid = threadIdx.x;
+  uint32_t phase = 0;
+  if (use_tc) {
+    if (tid == 0) umma::mbar_init(&sm.mbar, 1);
+    if ((tid >> 5) == 0) umma::tmem_alloc(&sm.tmem, B::TCOLS);
+    umma::fence_before();
+    __syncthreads();
+    umma::fence_after();
+  }
   const Fixed& fx = A.fx;
   double* vf = gws + static_cast<int64_t>(blockIdx.x) * big_scratch_doubles<K>();  // NF x NC
   float* yg = reinterpret_cast<float*>(vf + NF * NC);                               // N x NCP (Y, higher orders)
@@ -153,136 +301,187 @@ __global__ void __launch_bounds__(kThreads, 1) k_hyb_big(HybArgs A, int parity, 
       }
       __syncthreads();
     }
-    // ---------------------------------------------------------------- phase C (fp32)
-    constexpr int CM = B::CT_M, CN = B::CT_N;
-    constexpr int CMS = (NF + CM - 1) / CM, CNS = (NC + CN - 1) / CN;
-    const bool cown = tid < CMS * CNS;
-    const int cm0 = cown ? (tid / CNS) * CM : 0, cn0 = cown ? (tid % CNS) * CN : 0;
-    float cacc[CM][CN];
-#pragma unroll
-    for (int i = 0; i < CM; ++i)
-#pragma unroll
-      for (int j = 0; j < CN; ++j) cacc[i][j] = 0.f;
-    int P = 1;
-    for (int pass = 1; pass <= P; ++pass) {
-      // right operand of this order: V32 (pass 1) or T = A0^-1 Y_prev (global, rare)
-      const float* rhs = (pass == 1) ? sm.v32 : yg + N * NCP;  // T staged behind Y in scratch
-      for (int i0 = 0; i0 < N; i0 += IB) {
-        for (int idx = tid; idx < IB * N; idx += kThreads) {
-          const int ii = idx / N, l = idx - ii * N;
-          const int64_t o = static_cast<int64_t>(i0 + ii) * N + l;
-          sm.u.pc.dt[l * IB + ii] = static_cast<float>(
-              delta_entry(a, b, __ldg(fx.D + o), __ldg(fx.M + o), __ldg(fx.E + o), __ldg(fx.Ma + o)));
+    // ---------------------------------------------------------------- phase C
+    // first order on the tensor cores; the CUDA-core path below is kept for
+    // the (rare) cells whose a-posteriori estimate asks for a second order
+    bool tc_done = false;
+    if (use_tc) {
+      correction_tc<K>(sm, fx, a, b, phase);
+      float cmax = 0.f, hmax = 0.f;
+      for (int idx = tid; idx < NF * NF; idx += kThreads) {
+        const int p = idx / NF, q = idx - p * NF;
+        cmax = fmaxf(cmax, fabsf(sm.u.csm[p * NCP + q]));
+        hmax = fmaxf(hmax, fabsf(sm.v32[(NINT + p) * NCP + q]));
+      }
+      for (int o = 16; o > 0; o >>= 1) {
+        cmax = fmaxf(cmax, __shfl_xor_sync(0xffffffffu, cmax, o));
+        hmax = fmaxf(hmax, __shfl_xor_sync(0xffffffffu, hmax, o));
+      }
+      if ((tid & 31) == 0) {
+        sm.red[tid >> 5] = cmax;
+        sm.red[kThreads / 32 + (tid >> 5)] = hmax;
+      }
+      __syncthreads();
+      if (tid == 0) {
+        float cm = 0.f, hm = 0.f;
+        for (int w = 0; w < kThreads / 32; ++w) {
+          cm = fmaxf(cm, sm.red[w]);
+          hm = fmaxf(hm, sm.red[kThreads / 32 + w]);
         }
-        __syncthreads();
-        {  // Y_I = Delta_I rhs
-          constexpr int TM = B::VT_M, TN = B::VT_N;
-          constexpr int TMS = (IB + TM - 1) / TM, TNS = (NC + TN - 1) / TN;
-          for (int tile = tid; tile < TMS * TNS; tile += kThreads) {
-            const int m0 = (tile / TNS) * TM, n0 = (tile % TNS) * TN;
-            float acc[TM][TN];
-#pragma unroll
-            for (int i = 0; i < TM; ++i)
-#pragma unroll
-              for (int jj = 0; jj < TN; ++jj) acc[i][jj] = 0.f;
-#pragma unroll 4
-            for (int l = 0; l < N; ++l) {
-              float dv[TM], rv[TN];
-#pragma unroll
-              for (int i = 0; i < TM; ++i) dv[i] = (m0 + i < IB) ? sm.u.pc.dt[l * IB + m0 + i] : 0.f;
-#pragma unroll
-              for (int jj = 0; jj < TN; ++jj) rv[jj] = (n0 + jj < NC) ? rhs[l * NCP + n0 + jj] : 0.f;
-#pragma unroll
+        const double ratio = hm > 0.f ? static_cast<double>(cm) / hm : 0.0;
+        int p = 1;
+        double tt = ratio * ratio * 10.0;
+        while (tt > 1e-12 && p < A.p_max) {
+          ++p;
+          tt *= ratio;
+        }
+        if (!(ratio < 0.25)) atomicOr(A.status, 1);
+        // the tensor core's fp32 accumulation is less accurate than fp32 FMA
+        // chains (~1e-6 of |C|): accept its C only where C itself is tiny
+        sm.order = (p == 1 && ratio <= HDR_TC_TAU) ? 1 : 0;
+      }
+      __syncthreads();
+      tc_done = sm.order == 1;
+    }
+    if (!tc_done) {
+      constexpr int CM = B::CT_M, CN = B::CT_N;
+      constexpr int CMS = (NF + CM - 1) / CM, CNS = (NC + CN - 1) / CN;
+      const bool cown = tid < CMS * CNS;
+      const int cm0 = cown ? (tid / CNS) * CM : 0, cn0 = cown ? (tid % CNS) * CN : 0;
+      float cacc[CM][CN];
+  #pragma unroll
+      for (int i = 0; i < CM; ++i)
+  #pragma unroll
+        for (int j = 0; j < CN; ++j) cacc[i][j] = 0.f;
+      int P = 1;
+      for (int pass = 1; pass <= P; ++pass) {
+        // right operand of this order: V32 (pass 1) or T = A0^-1 Y_prev (global, rare)
+        const float* rhs = (pass == 1) ? sm.v32 : yg + N * NCP;  // T staged behind Y in scratch
+        for (int i0 = 0; i0 < N; i0 += IB) {
+          for (int idx = tid; idx < IB * N; idx += kThreads) {
+            const int ii = idx / N, l = idx - ii * N;
+            const int64_t o = static_cast<int64_t>(i0 + ii) * N + l;
+            sm.u.pc.dt[l * IB + ii] = static_cast<float>(
+                delta_entry(a, b, __ldg(fx.D + o), __ldg(fx.M + o), __ldg(fx.E + o), __ldg(fx.Ma + o)));
+          }
+          __syncthreads();
+          {  // Y_I = Delta_I rhs
+            constexpr int TM = B::VT_M, TN = B::VT_N;
+            constexpr int TMS = (IB + TM - 1) / TM, TNS = (NC + TN - 1) / TN;
+            for (int tile = tid; tile < TMS * TNS; tile += kThreads) {
+              const int m0 = (tile / TNS) * TM, n0 = (tile % TNS) * TN;
+              float acc[TM][TN];
+  #pragma unroll
               for (int i = 0; i < TM; ++i)
-#pragma unroll
-                for (int jj = 0; jj < TN; ++jj) acc[i][jj] = fmaf(dv[i], rv[jj], acc[i][jj]);
-            }
-#pragma unroll
-            for (int i = 0; i < TM; ++i)
-#pragma unroll
-              for (int jj = 0; jj < TN; ++jj)
-                if (m0 + i < IB && n0 + jj < NC) {
-                  sm.u.pc.y[(m0 + i) * NCP + n0 + jj] = acc[i][jj];
-                  yg[(i0 + m0 + i) * NCP + n0 + jj] = acc[i][jj];
-                }
-          }
-        }
-        __syncthreads();
-        if (cown) {  // C (+/-)= V32_I^T Y_I
-          const float sg = (pass == 1) ? 1.f : ((pass & 1) ? 1.f : -1.f);
-#pragma unroll 4
-          for (int ii = 0; ii < IB; ++ii) {
-            float vv[CM], yv[CN];
-#pragma unroll
-            for (int i = 0; i < CM; ++i) vv[i] = (cm0 + i < NF) ? sg * sm.v32[(i0 + ii) * NCP + cm0 + i] : 0.f;
-#pragma unroll
-            for (int j = 0; j < CN; ++j) yv[j] = (cn0 + j < NC) ? sm.u.pc.y[ii * NCP + cn0 + j] : 0.f;
-#pragma unroll
-            for (int i = 0; i < CM; ++i)
-#pragma unroll
-              for (int j = 0; j < CN; ++j) cacc[i][j] = fmaf(vv[i], yv[j], cacc[i][j]);
-          }
-        }
-        __syncthreads();
-      }
-      if (pass == 1) {  // a-posteriori order control: 10 (|C| / |H0|)^2 <= 1e-12 -> order 1 suffices
-        float cmax = 0.f, hmax = 0.f;
-        if (cown)
-#pragma unroll
-          for (int i = 0; i < CM; ++i)
-#pragma unroll
-            for (int j = 0; j < CN; ++j)
-              if (cm0 + i < NF && cn0 + j < NF) {
-                cmax = fmaxf(cmax, fabsf(cacc[i][j]));
-                hmax = fmaxf(hmax, fabsf(sm.v32[(NINT + cm0 + i) * NCP + cn0 + j]));
+  #pragma unroll
+                for (int jj = 0; jj < TN; ++jj) acc[i][jj] = 0.f;
+  #pragma unroll 4
+              for (int l = 0; l < N; ++l) {
+                float dv[TM], rv[TN];
+  #pragma unroll
+                for (int i = 0; i < TM; ++i) dv[i] = (m0 + i < IB) ? sm.u.pc.dt[l * IB + m0 + i] : 0.f;
+  #pragma unroll
+                for (int jj = 0; jj < TN; ++jj) rv[jj] = (n0 + jj < NC) ? rhs[l * NCP + n0 + jj] : 0.f;
+  #pragma unroll
+                for (int i = 0; i < TM; ++i)
+  #pragma unroll
+                  for (int jj = 0; jj < TN; ++jj) acc[i][jj] = fmaf(dv[i], rv[jj], acc[i][jj]);
               }
-        for (int o = 16; o > 0; o >>= 1) {
-          cmax = fmaxf(cmax, __shfl_xor_sync(0xffffffffu, cmax, o));
-          hmax = fmaxf(hmax, __shfl_xor_sync(0xffffffffu, hmax, o));
-        }
-        if ((tid & 31) == 0) {
-          sm.red[tid >> 5] = cmax;
-          sm.red[kThreads / 32 + (tid >> 5)] = hmax;
-        }
-        __syncthreads();
-        if (tid == 0) {
-          float cm = 0.f, hm = 0.f;
-          for (int w = 0; w < kThreads / 32; ++w) {
-            cm = fmaxf(cm, sm.red[w]);
-            hm = fmaxf(hm, sm.red[kThreads / 32 + w]);
+  #pragma unroll
+              for (int i = 0; i < TM; ++i)
+  #pragma unroll
+                for (int jj = 0; jj < TN; ++jj)
+                  if (m0 + i < IB && n0 + jj < NC) {
+                    sm.u.pc.y[(m0 + i) * NCP + n0 + jj] = acc[i][jj];
+                    yg[(i0 + m0 + i) * NCP + n0 + jj] = acc[i][jj];
+                  }
+            }
           }
-          const double ratio = hm > 0.f ? static_cast<double>(cm) / hm : 0.0;
-          int p = 1;
-          double tt = ratio * ratio * 10.0;
-          while (tt > 1e-12 && p < A.p_max) {
-            ++p;
-            tt *= ratio;
+          __syncthreads();
+          if (cown) {  // C (+/-)= V32_I^T Y_I
+            const float sg = (pass == 1) ? 1.f : ((pass & 1) ? 1.f : -1.f);
+  #pragma unroll 4
+            for (int ii = 0; ii < IB; ++ii) {
+              float vv[CM], yv[CN];
+  #pragma unroll
+              for (int i = 0; i < CM; ++i) vv[i] = (cm0 + i < NF) ? sg * sm.v32[(i0 + ii) * NCP + cm0 + i] : 0.f;
+  #pragma unroll
+              for (int j = 0; j < CN; ++j) yv[j] = (cn0 + j < NC) ? sm.u.pc.y[ii * NCP + cn0 + j] : 0.f;
+  #pragma unroll
+              for (int i = 0; i < CM; ++i)
+  #pragma unroll
+                for (int j = 0; j < CN; ++j) cacc[i][j] = fmaf(vv[i], yv[j], cacc[i][j]);
+            }
           }
-          if (!(ratio < 0.25)) atomicOr(A.status, 1);
-          sm.order = p;
+          __syncthreads();
         }
-        __syncthreads();
-        P = sm.order;
+        if (pass == 1) {  // a-posteriori order control: 10 (|C| / |H0|)^2 <= 1e-12 -> order 1 suffices
+          float cmax = 0.f, hmax = 0.f;
+          if (cown)
+  #pragma unroll
+            for (int i = 0; i < CM; ++i)
+  #pragma unroll
+              for (int j = 0; j < CN; ++j)
+                if (cm0 + i < NF && cn0 + j < NF) {
+                  cmax = fmaxf(cmax, fabsf(cacc[i][j]));
+                  hmax = fmaxf(hmax, fabsf(sm.v32[(NINT + cm0 + i) * NCP + cn0 + j]));
+                }
+          for (int o = 16; o > 0; o >>= 1) {
+            cmax = fmaxf(cmax, __shfl_xor_sync(0xffffffffu, cmax, o));
+            hmax = fmaxf(hmax, __shfl_xor_sync(0xffffffffu, hmax, o));
+          }
+          if ((tid & 31) == 0) {
+            sm.red[tid >> 5] = cmax;
+            sm.red[kThreads / 32 + (tid >> 5)] = hmax;
+          }
+          __syncthreads();
+          if (tid == 0) {
+            float cm = 0.f, hm = 0.f;
+            for (int w = 0; w < kThreads / 32; ++w) {
+              cm = fmaxf(cm, sm.red[w]);
+              hm = fmaxf(hm, sm.red[kThreads / 32 + w]);
+            }
+            const double ratio = hm > 0.f ? static_cast<double>(cm) / hm : 0.0;
+            int p = 1;
+            double tt = ratio * ratio * 10.0;
+            while (tt > 1e-12 && p < A.p_max) {
+              ++p;
+              tt *= ratio;
+            }
+            if (!(ratio < 0.25)) atomicOr(A.status, 1);
+            sm.order = p;
+          }
+          __syncthreads();
+          P = sm.order;
+        }
+        if (pass < P) {  // T = A0^-1 Y (Y in yg) -> behind Y in the scratch; rare path, fp64 accumulation
+          float* tgl = yg + N * NCP;
+          for (int idx = tid; idx < R * NC; idx += kThreads) {
+            const int j = idx / NC, c = idx - j * NC;
+            double acc = 0.0;
+            for (int l = 0; l < N; ++l) acc = fma(__ldg(fx.X + l * R + j), static_cast<double>(yg[l * NCP + c]), acc);
+            sm.u.pv.z[idx] = sm.s[j] * acc;
+          }
+          __syncthreads();
+          for (int idx = tid; idx < N * NC; idx += kThreads) {
+            const int i = idx / NC, c = idx - i * NC;
+            double acc = 0.0;
+            for (int l = 0; l < N; ++l)
+              acc = fma(__ldg(fx.N0 + static_cast<int64_t>(i) * N + l), static_cast<double>(yg[l * NCP + c]), acc);
+            for (int j = 0; j < R; ++j) acc = fma(__ldg(fx.X + i * R + j), sm.u.pv.z[j * NC + c], acc);
+            tgl[i * NCP + c] = static_cast<float>(acc * ib);
+          }
+          __syncthreads();
+        }
       }
-      if (pass < P) {  // T = A0^-1 Y (Y in yg) -> behind Y in the scratch; rare path, fp64 accumulation
-        float* tgl = yg + N * NCP;
-        for (int idx = tid; idx < R * NC; idx += kThreads) {
-          const int j = idx / NC, c = idx - j * NC;
-          double acc = 0.0;
-          for (int l = 0; l < N; ++l) acc = fma(__ldg(fx.X + l * R + j), static_cast<double>(yg[l * NCP + c]), acc);
-          sm.u.pv.z[idx] = sm.s[j] * acc;
-        }
-        __syncthreads();
-        for (int idx = tid; idx < N * NC; idx += kThreads) {
-          const int i = idx / NC, c = idx - i * NC;
-          double acc = 0.0;
-          for (int l = 0; l < N; ++l)
-            acc = fma(__ldg(fx.N0 + static_cast<int64_t>(i) * N + l), static_cast<double>(yg[l * NCP + c]), acc);
-          for (int j = 0; j < R; ++j) acc = fma(__ldg(fx.X + i * R + j), sm.u.pv.z[j * NC + c], acc);
-          tgl[i * NCP + c] = static_cast<float>(acc * ib);
-        }
-        __syncthreads();
-      }
+
+      if (cown)
+#pragma unroll
+        for (int i = 0; i < CM; ++i)
+#pragma unroll
+          for (int j = 0; j < CN; ++j)
+            if (cm0 + i < NF && cn0 + j < NC) sm.u.csm[(cm0 + i) * NCP + cn0 + j] = cacc[i][j];
+      __syncthreads();
     }
     // ---------------------------------------------------------------- scatter
     {
@@ -319,41 +518,34 @@ __global__ void __launch_bounds__(kThreads, 1) k_hyb_big(HybArgs A, int parity, 
       }
     }
     __syncthreads();
-    if (cown) {
-#pragma unroll
-      for (int i = 0; i < CM; ++i) {
-        const int p = cm0 + i;
-        if (p >= NF) continue;
-        const int ps = p / DPF, sub = p - ps * DPF;
-        const int64_t rs = sm.rstart[ps];
-        if (rs < 0) continue;
-#pragma unroll
-        for (int j = 0; j < CN; ++j) {
-          const int c = cn0 + j;
-          if (c >= NC) continue;
-          const double v = vf[p * NC + c] - static_cast<double>(cacc[i][j]);
-          if (c == NF) {
-            double* gp = A.g + sm.grow[ps] + sub;
-            *gp = parity ? *gp + v : v;
-            continue;
-          }
-          const int qs = c / DPF, sj = c - qs * DPF;
-          const int rk = sm.rank[ps * NS + qs];
-          if (rk < 0) continue;
-          double* hp = A.hval + rs + static_cast<int64_t>(sub) * sm.rlen[ps] + rk * DPF + sj;
-          *hp = (parity == 1 && ps == qs) ? *hp + v : v;
-        }
+    for (int idx = tid; idx < NF * NC; idx += kThreads) {
+      const int p = idx / NC, c = idx - p * NC;
+      const int ps = p / DPF, sub = p - ps * DPF;
+      const int64_t rs = sm.rstart[ps];
+      if (rs < 0) continue;
+      const double v = vf[p * NC + c] - static_cast<double>(sm.u.csm[p * NCP + c]);
+      if (c == NF) {
+        double* gp = A.g + sm.grow[ps] + sub;
+        *gp = parity ? *gp + v : v;
+        continue;
       }
+      const int qs = c / DPF, sj = c - qs * DPF;
+      const int rk = sm.rank[ps * NS + qs];
+      if (rk < 0) continue;
+      double* hp = A.hval + rs + static_cast<int64_t>(sub) * sm.rlen[ps] + rk * DPF + sj;
+      *hp = (parity == 1 && ps == qs) ? *hp + v : v;
     }
     __syncthreads();
   }
+  if (use_tc && (tid >> 5) == 0) umma::tmem_dealloc(sm.tmem, B::TCOLS);
 }
 
 template <int K>
 void launch_big_t(const HybArgs& a, int parity, double* gws, int64_t grid, cudaStream_t st) {
   const size_t smem = sizeof(BigSmem<K>);
   cudaFuncSetAttribute(k_hyb_big<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-  k_hyb_big<K><<<static_cast<unsigned>(grid), kThreads, smem, st>>>(a, parity, gws);
+  static const int use_tc = getenv("HDR_NO_TC") ? 0 : 1;  // HDR_NO_TC=1: CUDA-core correction (A/B timing)
+  k_hyb_big<K><<<static_cast<unsigned>(grid), kThreads, smem, st>>>(a, parity, gws, use_tc);
 }
 
 template <int K>
