@@ -57,6 +57,7 @@ struct hdr_space_s {
   DBuf<double> fixed;  // D, M, E, Ma, N0 (n*n each), X (n*r), lam (r)
   std::vector<double> rt0_consts;  // packed constant block of the k = 0 kernel
   DBuf<uint64_t> rank_tab;         // k = 0 row-rank table
+  DBuf<double> premat;             // k >= 2 (3D): [N0 ; X^T] column-major ((n + r) x n)
   Fixed fx{};
   GeomState* geom = nullptr;  // mapped (trilinear) cells: hdr_space_set_vertices
   ~hdr_space_s() {
@@ -67,7 +68,7 @@ struct hdr_space_s {
 
 struct hdr_hybrid_s {
   hdr_space_t sp = nullptr;
-  DBuf<double> hval, g, alpha, beta, f, ws;
+  DBuf<double> hval, g, alpha, beta, f, ws, pre;
   DBuf<int> status;
   int64_t ws_doubles = 0;
   const double* a_ptr = nullptr;  // coefficients used by the last hybridize (owned copy or borrowed device input)
@@ -297,6 +298,17 @@ hdr_status hdr_space_create(int dim, const int64_t cells[3], const double h[3], 
     fx.lam = fx.X + static_cast<size_t>(n) * r;
     fx.r = r;
     fx.rho = sp->st.rho;
+    if (dim == 3 && order >= 2) {
+      const int npr = n + r;
+      std::vector<double> pm(static_cast<size_t>(npr) * n);
+      for (int l = 0; l < n; ++l)
+        for (int row = 0; row < npr; ++row)
+          pm[static_cast<size_t>(l) * npr + row] =
+              row < n ? sp->st.N0[static_cast<size_t>(row) * n + l] : sp->st.X[static_cast<size_t>(l) * r + (row - n)];
+      sp->premat.alloc(pm.size());
+      CK(cudaMemcpyAsync(sp->premat.p, pm.data(), pm.size() * 8, cudaMemcpyHostToDevice, st));
+      CK(cudaStreamSynchronize(st));
+    }
     if (order == 0) {  // constant block for the register kernel: D, M, E, Ma, N0, X, lam, rho
       sp->rt0_consts.assign(pack.begin(), pack.begin() + 5 * nn + n + 1);
       sp->rt0_consts.push_back(sp->st.rho);
@@ -505,7 +517,10 @@ static hdr_status run_hybridize(hdr_hybrid_t op, const double* alpha, const doub
         op->ws.alloc(static_cast<size_t>(need));
         op->ws_doubles = need;
       }
-      for (int parity = 0; parity < 2; ++parity) launch_hybridize_big(A, sp->k, parity, op->ws.p, st);
+      const int npr = sp->n + sp->r;  // [N0 ; X^T] f for every cell, one batched fp64 GEMM
+      if (!op->pre.p || op->pre.n < static_cast<size_t>(npr) * sp->ncells) op->pre.alloc(static_cast<size_t>(npr) * sp->ncells);
+      launch_gemm_f64_nn(npr, static_cast<int>(sp->ncells), sp->n, sp->premat.p, npr, df, sp->n, op->pre.p, npr, st);
+      for (int parity = 0; parity < 2; ++parity) launch_hybridize_big(A, sp->k, parity, op->ws.p, op->pre.p, st);
     } else if (hybridize_warp_supported(sp->dim, sp->k) && !getenv("HDR_CTA_PATH")) {
       const int64_t need = hybridize_warp_scratch_doubles(A);
       if (op->ws_doubles < need) {

@@ -209,7 +209,8 @@ __device__ void correction_tc(BigSmem<K>& sm, const Fixed& fx, double a, double 
 }
 
 template <int K>
-__global__ void __launch_bounds__(kThreads, 1) k_hyb_big(HybArgs A, int parity, double* gws, int use_tc) {
+__global__ void __launch_bounds__(kThreads, 1) k_hyb_big(HybArgs A, int parity, double* gws, int use_tc,
+                                                         const double* pre) {
   using B = Big<K>;
   constexpr int N = B::N, NF = B::NF, NC = B::NC, NCP = B::NCP, R = B::R, NINT = B::NINT, DPF = B::DPF;
   constexpr int IB = B::IB, NS = B::NS;
@@ -240,28 +241,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_hyb_big(HybArgs A, int parity, 
     for (int i = tid; i < N; i += kThreads) sm.f[i] = fe[i];
     for (int j = tid; j < R; j += kThreads) sm.s[j] = b / fma(a, __ldg(fx.lam + j), b);
     __syncthreads();
-    for (int i = tid; i < N; i += kThreads) {
-      double acc = 0.0;
-      const double* row = fx.N0 + static_cast<int64_t>(i) * N;
-#pragma unroll 8
-      for (int l = 0; l < N; ++l) acc = fma(__ldg(row + l), sm.f[l], acc);
-      sm.nf[i] = acc;
-    }
+    const double* pe = pre + static_cast<int64_t>(e) * (N + R);  // [N0 f_e ; X^T f_e], batched GEMM
+    for (int i = tid; i < N; i += kThreads) sm.nf[i] = pe[i];
     for (int idx = tid; idx < R * NF; idx += kThreads) {
       const int j = idx / NF, c = idx - j * NF;
       sm.u.pv.z[j * NC + c] = sm.s[j] * __ldg(fx.X + (NINT + c) * R + j);
     }
-    {  // z[:, NF] = s * X^T f : R dots of length N, 4 threads each
-      for (int j0 = 0; j0 < R; j0 += kThreads / 4) {
-        const int j = j0 + tid / 4, part = tid & 3;
-        double acc = 0.0;
-        if (j < R)
-          for (int l = part; l < N; l += 4) acc = fma(__ldg(fx.X + l * R + j), sm.f[l], acc);
-        acc += __shfl_xor_sync(0xffffffffu, acc, 1);
-        acc += __shfl_xor_sync(0xffffffffu, acc, 2);
-        if (j < R && part == 0) sm.u.pv.z[j * NC + NF] = sm.s[j] * acc;
-      }
-    }
+    for (int j = tid; j < R; j += kThreads) sm.u.pv.z[j * NC + NF] = sm.s[j] * pe[N + j];
     __syncthreads();
     for (int i0 = 0; i0 < N; i0 += IB) {
       for (int idx = tid; idx < IB * R; idx += kThreads) sm.u.pv.xi[idx] = __ldg(fx.X + i0 * R + idx);
@@ -541,11 +527,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_hyb_big(HybArgs A, int parity, 
 }
 
 template <int K>
-void launch_big_t(const HybArgs& a, int parity, double* gws, int64_t grid, cudaStream_t st) {
+void launch_big_t(const HybArgs& a, int parity, double* gws, const double* pre, int64_t grid, cudaStream_t st) {
   const size_t smem = sizeof(BigSmem<K>);
   cudaFuncSetAttribute(k_hyb_big<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   static const int use_tc = getenv("HDR_NO_TC") ? 0 : 1;  // HDR_NO_TC=1: CUDA-core correction (A/B timing)
-  k_hyb_big<K><<<static_cast<unsigned>(grid), kThreads, smem, st>>>(a, parity, gws, use_tc);
+  k_hyb_big<K><<<static_cast<unsigned>(grid), kThreads, smem, st>>>(a, parity, gws, use_tc, pre);
 }
 
 template <int K>
@@ -569,10 +555,65 @@ int64_t hybridize_big_scratch_doubles(const HybArgs& a, int k) {
   return grid_big_t<3>(a) * (big_scratch_doubles<3>() + static_cast<int64_t>(Big<3>::N) * Big<3>::NCP / 2 + 8);
 }
 
-void launch_hybridize_big(const HybArgs& a, int k, int parity, double* gws, cudaStream_t st) {
-  if (k == 2) launch_big_t<2>(a, parity, gws, grid_big_t<2>(a), st);
-  else launch_big_t<3>(a, parity, gws, grid_big_t<3>(a), st);
+void launch_hybridize_big(const HybArgs& a, int k, int parity, double* gws, const double* pre, cudaStream_t st) {
+  if (k == 2) launch_big_t<2>(a, parity, gws, pre, grid_big_t<2>(a), st);
+  else launch_big_t<3>(a, parity, gws, pre, grid_big_t<3>(a), st);
   count_launch();
 }
 
+}  // namespace hdr
+
+// ---------------------------------------------------------------------------
+// Per-cell products with fixed matrices, batched over all cells as one fp64
+// GEMM before the element kernel: pre(:, e) = [N0 ; X^T] f_e (column-major,
+// ld = N + R).  A tiled GEMM (64 x 64 output tile per 256-thread CTA, 4 x 4
+// fp64 register tiles, K staged in shared memory by 16).
+namespace hdr {
+namespace {
+__global__ void __launch_bounds__(256) k_gemm_f64_nn(int M, int Ncol, int Kd, const double* A, int lda,
+                                                     const double* B, int ldb, double* C, int ldc) {
+  __shared__ double As[16][64 + 1];
+  __shared__ double Bs[16][64 + 1];
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const int m0 = blockIdx.y * 64, n0 = blockIdx.x * 64;
+  double acc[4][4] = {};
+  for (int k0 = 0; k0 < Kd; k0 += 16) {
+    for (int t = threadIdx.x; t < 16 * 64; t += 256) {
+      const int kk = t / 64, mm = t % 64;
+      As[kk][mm] = (m0 + mm < M && k0 + kk < Kd) ? A[(m0 + mm) + static_cast<int64_t>(lda) * (k0 + kk)] : 0.0;
+      const int nn = t / 16, k2 = t % 16;
+      Bs[k2][nn] = (n0 + nn < Ncol && k0 + k2 < Kd) ? B[(k0 + k2) + static_cast<int64_t>(ldb) * (n0 + nn)] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) {
+      double a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = As[kk][ty * 4 + i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx * 4 + j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int m = m0 + ty * 4 + i, n = n0 + tx * 4 + j;
+      if (m < M && n < Ncol) C[m + static_cast<int64_t>(ldc) * n] = acc[i][j];
+    }
+}
+}  // namespace
+
+void launch_gemm_f64_nn(int M, int Ncol, int Kd, const double* A, int lda, const double* B, int ldb, double* C,
+                        int ldc, cudaStream_t st) {
+  if (M <= 0 || Ncol <= 0) return;
+  dim3 grid(static_cast<unsigned>((Ncol + 63) / 64), static_cast<unsigned>((M + 63) / 64));
+  k_gemm_f64_nn<<<grid, 256, 0, st>>>(M, Ncol, Kd, A, lda, B, ldb, C, ldc);
+  count_launch();
+}
 }  // namespace hdr

@@ -55,7 +55,11 @@ void launch_hybridize_warp(const HybArgs& a, int parity, double* gws, cudaStream
 // RT2 / RT3 hexahedra: one CTA per cell (kern_cta.cu)
 bool hybridize_big_supported(int dim, int k);
 int64_t hybridize_big_scratch_doubles(const HybArgs& a, int k);
-void launch_hybridize_big(const HybArgs& a, int k, int parity, double* gws, cudaStream_t st);
+// pre: (N + R) x ncells column-major [N0 f_e ; X^T f_e] (launch_gemm_f64_nn with A = [N0 ; X^T])
+void launch_hybridize_big(const HybArgs& a, int k, int parity, double* gws, const double* pre, cudaStream_t st);
+// C (M x Ncol) = A (M x Kd) B (Kd x Ncol), column-major fp64
+void launch_gemm_f64_nn(int M, int Ncol, int Kd, const double* A, int lda, const double* B, int ldb, double* C,
+                        int ldc, cudaStream_t st);
 // General path (k >= 1): one CTA per cell, shared-memory or global workspace.
 void launch_hybridize_cta(const HybArgs& a, int parity, double* gws, int64_t ws_doubles, cudaStream_t st);
 int64_t hybridize_cta_ws_doubles(const DevMesh& m, int nF, int r, int p_max, bool* use_smem);
