@@ -32,7 +32,7 @@ struct Big {
   static constexpr int R = (K + 1) * (K + 1) * (K + 1);
   static constexpr int NC = NF + 1;
   static constexpr int NCP = (NC + 3) & ~3;
-  static constexpr int IB = (K == 3) ? 60 : 36;  // rows per block, divides N
+  static constexpr int IB = (K == 3) ? 48 : 54;  // rows per block: divides N and NINT (interior / face blocks)
   static constexpr int NB = N / IB;
   // thread tiles: V / Y blocks (IB x NC), C (NF x NC)
   static constexpr int VT_M = (K == 3) ? 4 : 3, VT_N = (K == 3) ? 6 : 3;
@@ -61,6 +61,8 @@ struct BigSmem {
     struct {
       double z[B::R * B::NC];
       double xi[B::IB * B::R];
+      float z32[B::R * B::NC];   // fp32 copies for the interior-row blocks
+      float xi32[B::IB * B::R];
     } pv;
     struct {
       float dt[B::N * B::IB];  // Delta32 block transposed: dt[l * IB + ii]
@@ -69,7 +71,7 @@ struct BigSmem {
     struct {  // tcgen05 operand chunks (canonical K-major, no swizzle), hi / lo tf32 parts
       float ahi[B::MP * B::KC], alo[B::MP * B::KC];
       float bhi[B::NP * B::KC], blo[B::NP * B::KC];
-    } tc;
+    } tc[2];    // double-buffered: chunk c + 1 is generated while the MMAs of chunk c run
     float csm[B::NF * B::NCP];  // the correction C (NF x NC) for the scatter
   } u;
   double f[B::N], nf[B::N], s[B::R];
@@ -77,7 +79,7 @@ struct BigSmem {
   int rlen[B::NS], grow[B::NS], rank[B::NS * B::NS];
   float red[2 * kThreads / 32];
   int order;
-  uint64_t mbar;
+  uint64_t mbar[2];
   uint32_t tmem;
 };
 
@@ -96,23 +98,72 @@ __device__ __forceinline__ void tf32_split(float x, float& hi, float& lo) {
   lo = __uint_as_float(l);
 }
 
+// One row block [i0, i0 + IB) of [V | w] = (base + X z) / beta, register tiles
+// in T (double for the face rows, float for the interior rows).
+template <int K, class T>
+__device__ __forceinline__ void v_block(BigSmem<K>& sm, const T* xi, const T* z, const Fixed& fx, int i0, double ib,
+                                        double* vf, int tid) {
+  using B = Big<K>;
+  constexpr int N = B::N, NF = B::NF, NC = B::NC, NCP = B::NCP, R = B::R, NINT = B::NINT, IB = B::IB;
+  constexpr int TM = B::VT_M, TN = B::VT_N;
+  constexpr int TMS = (IB + TM - 1) / TM, TNS = (NC + TN - 1) / TN;
+  for (int tile = tid; tile < TMS * TNS; tile += kThreads) {
+    const int m0 = (tile / TNS) * TM, n0 = (tile % TNS) * TN;
+    T acc[TM][TN];
+#pragma unroll
+    for (int i = 0; i < TM; ++i)
+#pragma unroll
+      for (int jj = 0; jj < TN; ++jj) acc[i][jj] = T(0);
+#pragma unroll 4
+    for (int j = 0; j < R; ++j) {
+      T xv[TM], zv[TN];
+#pragma unroll
+      for (int i = 0; i < TM; ++i) xv[i] = (m0 + i < IB) ? xi[(m0 + i) * R + j] : T(0);
+#pragma unroll
+      for (int jj = 0; jj < TN; ++jj) zv[jj] = (n0 + jj < NC) ? z[j * NC + n0 + jj] : T(0);
+#pragma unroll
+      for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int jj = 0; jj < TN; ++jj) acc[i][jj] = fma(xv[i], zv[jj], acc[i][jj]);
+    }
+#pragma unroll
+    for (int i = 0; i < TM; ++i)
+#pragma unroll
+      for (int jj = 0; jj < TN; ++jj) {
+        const int row = i0 + m0 + i, col = n0 + jj;
+        if (m0 + i >= IB || col >= NC) continue;
+        const double base = (col < NF) ? __ldg(fx.N0 + static_cast<int64_t>(row) * N + NINT + col) : sm.nf[row];
+        const double v = (base + static_cast<double>(acc[i][jj])) * ib;
+        sm.v32[row * NCP + col] = static_cast<float>(v);
+        if (row >= NINT) vf[(row - NINT) * NC + col] = v;
+      }
+  }
+}
+
 // First-order correction on the tensor cores (3xTF32):
 //   Y = Delta V  (Y in TMEM, MT1 tiles of 128 rows),  C = V[:, F]^T Y  (C in TMEM),
 // operands generated chunk by chunk (K = 16) straight into the canonical
 // shared-memory layout; one thread issues the MMAs, everyone waits on the
 // commit mbarrier before the buffers are refilled.  C -> sm.u.csm.
 template <int K>
-__device__ void correction_tc(BigSmem<K>& sm, const Fixed& fx, double a, double b, uint32_t& phase) {
+__device__ void correction_tc(BigSmem<K>& sm, const Fixed& fx, double a, double b, uint32_t (&ph)[2]) {
   using B = Big<K>;
-  constexpr int N = B::N, NF = B::NF, NC = B::NC, NCP = B::NCP, NINT = B::NINT;
-  constexpr int MP = B::MP, NP = B::NP, KP = B::KP, KC = B::KC, MT1 = B::MT1;
+  constexpr int N = B::N, NF = B::NF, NC = B::NC, NCP = B::NCP;
+  constexpr int MP = B::MP, NP = B::NP, KP = B::KP, KC = B::KC, MT1 = B::MT1, NCH = KP / KC;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t tY = sm.tmem, tC = sm.tmem + MT1 * NP;
   constexpr uint32_t idesc = umma::idesc_tf32(128, NP);
   constexpr uint32_t lbo_a = (MP / 8) * 128, lbo_b = (NP / 8) * 128, lbo_a2 = (128 / 8) * 128;
-  auto& T = sm.u.tc;
+  auto wait_buf = [&](int bf) {  // the MMAs that last read buffer bf are done
+    umma::mbar_wait(&sm.mbar[bf], ph[bf]);
+    ph[bf] ^= 1u;
+    umma::fence_after();
+  };
   // ---- Y = Delta V
-  for (int kc = 0; kc < KP; kc += KC) {
+  for (int c = 0; c < NCH; ++c) {
+    const int bf = c & 1, kc = c * KC;
+    auto& T = sm.u.tc[bf];
+    if (c >= 2) wait_buf(bf);
     for (int idx = tid; idx < MP * KC; idx += kThreads) {
       const int m = idx / KC, k = idx - m * KC, col = kc + k;
       float x = 0.f;
@@ -140,16 +191,18 @@ __device__ void correction_tc(BigSmem<K>& sm, const Fixed& fx, double a, double 
             const float* bop = term == 1 ? T.blo : T.bhi;
             const uint64_t ad = umma::smem_desc(umma::smem_u32(aop) + t * 2048 + ks * 2 * lbo_a, lbo_a, 128);
             const uint64_t bd = umma::smem_desc(umma::smem_u32(bop) + ks * 2 * lbo_b, lbo_b, 128);
-            umma::mma_tf32(tY + t * NP, ad, bd, idesc, kc > 0 || ks > 0 || term > 0);
+            umma::mma_tf32(tY + t * NP, ad, bd, idesc, c > 0 || ks > 0 || term > 0);
           }
-      umma::commit(&sm.mbar);
+      umma::commit(&sm.mbar[bf]);
     }
-    umma::mbar_wait(&sm.mbar, phase);
-    phase ^= 1u;
-    umma::fence_after();
   }
-  // ---- C = V_F^T Y  (B operand: rows of Y read back from TMEM)
-  for (int kc = 0; kc < KP; kc += KC) {
+  wait_buf(NCH & 1);        // chunk NCH - 2
+  wait_buf((NCH - 1) & 1);  // chunk NCH - 1: Y complete
+  // ---- C = V[:, F]^T Y  (B operand: rows of Y read back from TMEM)
+  for (int c = 0; c < NCH; ++c) {
+    const int bf = c & 1, kc = c * KC;
+    auto& T = sm.u.tc[bf];
+    if (c >= 2) wait_buf(bf);
     for (int idx = tid; idx < 128 * KC; idx += kThreads) {
       const int m = idx / KC, k = idx - m * KC, row = kc + k;
       const float x = (m < NF && row < N) ? sm.v32[row * NCP + m] : 0.f;  // column m of V = A0^-1 E_F
@@ -159,14 +212,14 @@ __device__ void correction_tc(BigSmem<K>& sm, const Fixed& fx, double a, double 
     {
       const int t = kc / 128, l0 = kc - t * 128, q = l0 >> 5, lo = l0 & 31;
       if ((warp & 3) == q) {  // the warps of TMEM lane quadrant q share the columns, 8 at a time
-        for (int c = 8 * (warp >> 2); c < NP; c += 8 * (kThreads / 128)) {
+        for (int cc = 8 * (warp >> 2); cc < NP; cc += 8 * (kThreads / 128)) {
           float v[8];
-          umma::tmem_ld8(tY + t * NP + (static_cast<uint32_t>(32 * q) << 16) + c, v);
+          umma::tmem_ld8(tY + t * NP + (static_cast<uint32_t>(32 * q) << 16) + cc, v);
           if (lane >= lo && lane < lo + KC) {
             const int k = lane - lo;
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
-              const uint32_t off = umma::kmajor_offset(c + j, k, NP) >> 2;
+              const uint32_t off = umma::kmajor_offset(cc + j, k, NP) >> 2;
               tf32_split(v[j], T.bhi[off], T.blo[off]);
             }
           }
@@ -184,24 +237,23 @@ __device__ void correction_tc(BigSmem<K>& sm, const Fixed& fx, double a, double 
           const float* bop = term == 1 ? T.blo : T.bhi;
           const uint64_t ad = umma::smem_desc(umma::smem_u32(aop) + ks * 2 * lbo_a2, lbo_a2, 128);
           const uint64_t bd = umma::smem_desc(umma::smem_u32(bop) + ks * 2 * lbo_b, lbo_b, 128);
-          umma::mma_tf32(tC, ad, bd, idesc, kc > 0 || ks > 0 || term > 0);
+          umma::mma_tf32(tC, ad, bd, idesc, c > 0 || ks > 0 || term > 0);
         }
-      umma::commit(&sm.mbar);
+      umma::commit(&sm.mbar[bf]);
     }
-    umma::mbar_wait(&sm.mbar, phase);
-    phase ^= 1u;
-    umma::fence_after();
   }
+  wait_buf(NCH & 1);
+  wait_buf((NCH - 1) & 1);
   // ---- C -> shared memory
   {
     const int q = warp & 3, m = 32 * q + lane;
-    for (int c = 8 * (warp >> 2); c < NP; c += 8 * (kThreads / 128)) {
+    for (int cc = 8 * (warp >> 2); cc < NP; cc += 8 * (kThreads / 128)) {
       float v[8];
-      umma::tmem_ld8(tC + (static_cast<uint32_t>(32 * q) << 16) + c, v);
+      umma::tmem_ld8(tC + (static_cast<uint32_t>(32 * q) << 16) + cc, v);
       if (m < NF)
 #pragma unroll
         for (int j = 0; j < 8; ++j)
-          if (c + j < NC) sm.u.csm[m * NCP + c + j] = v[j];
+          if (cc + j < NC) sm.u.csm[m * NCP + cc + j] = v[j];
     }
   }
   umma::fence_before();
@@ -217,9 +269,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_hyb_big(HybArgs A, int parity, 
   extern __shared__ __align__(128) unsigned char smem_raw[];
   BigSmem<K>& sm = *reinterpret_cast<BigSmem<K>*>(smem_raw);
   const int tid = threadIdx.x;
-  uint32_t phase = 0;
+  uint32_t phase[2] = {0u, 0u};
   if (use_tc) {
-    if (tid == 0) umma::mbar_init(&sm.mbar, 1);
+    if (tid == 0) {
+      umma::mbar_init(&sm.mbar[0], 1);
+      umma::mbar_init(&sm.mbar[1], 1);
+    }
     if ((tid >> 5) == 0) umma::tmem_alloc(&sm.tmem, B::TCOLS);
     umma::fence_before();
     __syncthreads();
@@ -249,42 +304,19 @@ __global__ void __launch_bounds__(kThreads, 1) k_hyb_big(HybArgs A, int parity, 
     }
     for (int j = tid; j < R; j += kThreads) sm.u.pv.z[j * NC + NF] = sm.s[j] * pe[N + j];
     __syncthreads();
+    // rows below NINT (interior dofs) only feed the fp32 correction: fp32 tiles;
+    // the face rows (H0 = V_F, g0) in fp64
+    for (int idx = tid; idx < R * NC; idx += kThreads) sm.u.pv.z32[idx] = static_cast<float>(sm.u.pv.z[idx]);
     for (int i0 = 0; i0 < N; i0 += IB) {
-      for (int idx = tid; idx < IB * R; idx += kThreads) sm.u.pv.xi[idx] = __ldg(fx.X + i0 * R + idx);
-      __syncthreads();
-      constexpr int TM = B::VT_M, TN = B::VT_N;
-      constexpr int TMS = (IB + TM - 1) / TM, TNS = (NC + TN - 1) / TN;
-      for (int tile = tid; tile < TMS * TNS; tile += kThreads) {
-        const int m0 = (tile / TNS) * TM, n0 = (tile % TNS) * TN;
-        double acc[TM][TN];
-#pragma unroll
-        for (int i = 0; i < TM; ++i)
-#pragma unroll
-          for (int jj = 0; jj < TN; ++jj) acc[i][jj] = 0.0;
-#pragma unroll 4
-        for (int j = 0; j < R; ++j) {
-          double xv[TM], zv[TN];
-#pragma unroll
-          for (int i = 0; i < TM; ++i) xv[i] = (m0 + i < IB) ? sm.u.pv.xi[(m0 + i) * R + j] : 0.0;
-#pragma unroll
-          for (int jj = 0; jj < TN; ++jj) zv[jj] = (n0 + jj < NC) ? sm.u.pv.z[j * NC + n0 + jj] : 0.0;
-#pragma unroll
-          for (int i = 0; i < TM; ++i)
-#pragma unroll
-            for (int jj = 0; jj < TN; ++jj) acc[i][jj] = fma(xv[i], zv[jj], acc[i][jj]);
-        }
-#pragma unroll
-        for (int i = 0; i < TM; ++i)
-#pragma unroll
-          for (int jj = 0; jj < TN; ++jj) {
-            const int row = i0 + m0 + i, col = n0 + jj;
-            if (m0 + i >= IB || col >= NC) continue;
-            const double base = (col < NF) ? __ldg(fx.N0 + static_cast<int64_t>(row) * N + NINT + col) : sm.nf[row];
-            const double v = (base + acc[i][jj]) * ib;
-            sm.v32[row * NCP + col] = static_cast<float>(v);
-            if (row >= NINT) vf[(row - NINT) * NC + col] = v;
-          }
+      const bool face = i0 >= NINT;
+      for (int idx = tid; idx < IB * R; idx += kThreads) {
+        const double x = __ldg(fx.X + i0 * R + idx);
+        if (face) sm.u.pv.xi[idx] = x;
+        else sm.u.pv.xi32[idx] = static_cast<float>(x);
       }
+      __syncthreads();
+      if (face) v_block<K, double>(sm, sm.u.pv.xi, sm.u.pv.z, fx, i0, ib, vf, tid);
+      else v_block<K, float>(sm, sm.u.pv.xi32, sm.u.pv.z32, fx, i0, ib, vf, tid);
       __syncthreads();
     }
     // ---------------------------------------------------------------- phase C
