@@ -1,0 +1,63 @@
+#!/usr/bin/env python
+"""Summarise ncu --set full reports into markdown (python profiles/summarize.py r01)."""
+import csv
+import subprocess
+import sys
+from pathlib import Path
+
+KEYS = [
+    ("gpu__time_duration.sum", "duration"),
+    ("dram__bytes_read.sum", "DRAM read"),
+    ("dram__bytes_write.sum", "DRAM write"),
+    ("launch__grid_size", "grid"),
+    ("launch__block_size", "block"),
+    ("launch__registers_per_thread", "registers/thread"),
+    ("launch__shared_mem_per_block_dynamic", "dyn. smem/block"),
+    ("sm__warps_active.avg.pct_of_peak_sustained_active", "warps active %"),
+    ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue active %"),
+    ("smsp__inst_executed.sum", "warp instructions"),
+    ("sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active", "fp64 pipe %"),
+    ("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active", "fma pipe %"),
+    ("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active", "tensor pipe %"),
+    ("l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed", "L1 LSU wavefronts %"),
+    ("lts__throughput.avg.pct_of_peak_sustained_elapsed", "L2 throughput %"),
+    ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "DRAM throughput %"),
+]
+
+
+def raw(rep: Path):
+    out = subprocess.run(["ncu", "-i", str(rep), "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(out.splitlines()))
+    hdr, units = rows[0], rows[1]
+    return [(dict(zip(hdr, r)), dict(zip(hdr, units))) for r in rows[2:]]
+
+
+def main():
+    rnd = sys.argv[1] if len(sys.argv) > 1 else "r01"
+    src = Path("gpurun_out") / rnd
+    lines = [f"# {rnd} ncu summaries (B200, `ncu --set full --clock-control none --import-source on`)", "",
+             "Cold-cache, serialised replays (ncu flushes caches per pass): compare shares, not absolutes.",
+             "Reports: `gpurun_out/" + rnd + "/full_cfg*.ncu-rep` (not committed); commands in profiles/README.md.", ""]
+    for rep in sorted(src.glob("full_cfg*.ncu-rep")):
+        cfg = rep.stem.replace("full_", "")
+        for d, u in raw(rep):
+            lines.append(f"## {cfg}: `{d['Kernel Name'][:110]}`")
+            lines.append("")
+            lines.append("| metric | value |")
+            lines.append("|---|---|")
+            for k, name in KEYS:
+                if k in d and d[k] not in ("", "n/a"):
+                    lines.append(f"| {name} | {d[k]} {u.get(k, '')} |")
+            st = {k.replace("smsp__pcsamp_warps_issue_stalled_", ""): int(v.replace(",", ""))
+                  for k, v in d.items() if k.startswith("smsp__pcsamp_warps_issue_stalled")
+                  and not k.endswith("not_issued") and v.replace(",", "").isdigit()}
+            tot = sum(st.values()) or 1
+            top = sorted(st.items(), key=lambda x: -x[1])[:5]
+            lines.append("| top stall reasons (share of samples) | " +
+                         ", ".join(f"{k} {100 * v / tot:.0f}%" for k, v in top) + " |")
+            lines.append("")
+    Path("profiles") .joinpath(f"{rnd}_ncu_summary.md").write_text("\n".join(lines) + "\n")
+
+
+if __name__ == "__main__":
+    main()
