@@ -256,6 +256,37 @@ void hdr_alg_destroy(hdr_alg_t op);
  * unsymmetrized element-exact value the parity contract is stated on. */
 hdr_status hdr_alg_symmetrize(hdr_alg_t op);
 
+/* ---------------------------------------------------------- reduced solve
+ *
+ * pcg (src/solvers.cpp:109-163) on the device with the reference's "none"
+ * (precond = 0) and Jacobi (precond = 1, positive_inv_diag :32-44) options,
+ * x0 = 0, stop at ||r|| / ||b|| <= rtol or maxit iterations.
+ * b: the right-hand side (NULL: the operator's own g / f_s), x: the solution,
+ * both host (on_device = 0) or device arrays; residual_history: NULL or
+ * maxit + 1 host doubles (relative residuals, [0] = 1).  Errors: HDR_VALIDATION
+ * for a non-positive diagonal (ZeroDiagonal), <z, r> <= 0
+ * (IndefinitePreconditioner) or <p, Ap> <= 0 (matrix not positive definite).
+ * The reference also rejects |A - A^T| > 1e-10 max|A| before iterating; call
+ * hdr_hybrid_symmetrize / hdr_alg_symmetrize first where that is wanted. */
+typedef struct hdr_pcg_report {
+  int64_t iterations;
+  int32_t converged;
+  int32_t reserved;
+  double final_relative_residual;
+  double wall_ms;
+} hdr_pcg_report;
+
+hdr_status hdr_hybrid_pcg(hdr_hybrid_t op, const double* b, double* x, int on_device, double rtol, int64_t maxit,
+                          int precond, double* residual_history, hdr_pcg_report* report);
+hdr_status hdr_condensed_pcg(hdr_condensed_t op, const double* b, double* x, int on_device, double rtol,
+                             int64_t maxit, int precond, double* residual_history, hdr_pcg_report* report);
+hdr_status hdr_alg_pcg(hdr_alg_t op, const double* b, double* x, int on_device, double rtol, int64_t maxit,
+                       int precond, double* residual_history, hdr_pcg_report* report);
+/* Host-array form for a caller-owned CsrMatrix (copies in and out). */
+hdr_status hdr_csr_pcg_host(int64_t n, const int64_t* row_offsets, const int64_t* col_indices, const double* values,
+                            const double* b, double* x, double rtol, int64_t maxit, int precond,
+                            double* residual_history, hdr_pcg_report* report);
+
 /* ------------------------------------------------- host-only introspection */
 
 /* The reference element matrices of RT_k on an h[0] x h[1] (x h[2]) box,

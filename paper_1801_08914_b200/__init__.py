@@ -303,6 +303,10 @@ class HybridizedOperator:
         dev = _same_device([h_out, g_out])
         _check(_lib().hdr_hybrid_values_enqueue(self._h, _ptr(h_out)[0], _ptr(g_out)[0], dev))
 
+    def pcg(self, b=None, rtol: float = 1e-10, maxit: int = 1000, precond: Optional[str] = "jacobi"):
+        """Solve H lambda = b (default b = g) on the device: (lambda, report), see hdr_hybrid_pcg."""
+        return _pcg_call(_lib().hdr_hybrid_pcg, self._h, self.space.m, b, rtol, maxit, precond)
+
     def symmetrize(self) -> None:
         """In place H <- (H + H^T) / 2, the reference's symmetrize (reduction.cpp:316):
         exactly symmetric H for consumers such as its pcg (solvers.cpp:25-30)."""
@@ -375,6 +379,10 @@ class CondensedOperator:
         _check(_lib().hdr_condensed_values(self._h, sv.ctypes.data, fs.ctypes.data, 0))
         return sv, fs
 
+    def pcg(self, b=None, rtol: float = 1e-10, maxit: int = 1000, precond: Optional[str] = "jacobi"):
+        """Solve S x_b = b (default b = f_s) on the device: (x_b, report)."""
+        return _pcg_call(_lib().hdr_condensed_pcg, self._h, self.space.info["n_s"], b, rtol, maxit, precond)
+
     def s_mat(self):
         ro, ci = self.space.pattern("S")
         sv, _ = self.values()
@@ -408,6 +416,58 @@ class CondensedOperator:
             y = np.empty(sp.info["n_s"])
         _check(_lib().hdr_condensed_spmv(self._h, _ptr(x)[0], _ptr(y)[0], dev))
         return y
+
+
+_PRECOND = {None: 0, "none": 0, "jacobi": 1}
+
+
+def _pcg_call(fn, handle, n, b, rtol, maxit, precond):
+    """Shared driver of the device pcg entry points: returns (x, report)."""
+    if precond not in _PRECOND:
+        raise ValueError("precond must be None, 'none' or 'jacobi' (the device pcg's options)")
+    hist = np.zeros(int(maxit) + 1)
+    rep = _capi.PcgReport()
+    if b is None:
+        x = np.empty(n)
+        _check(fn(handle, None, x.ctypes.data, 0, float(rtol), int(maxit), _PRECOND[precond], hist.ctypes.data,
+                  ctypes.byref(rep)))
+    else:
+        bb = _as_f64(b, n, "b")
+        dev = _ptr(bb)[1]
+        if dev:
+            import torch
+
+            x = torch.empty(n, dtype=torch.float64, device=bb.device)
+        else:
+            x = np.empty(n)
+        _check(fn(handle, _ptr(bb)[0], _ptr(x)[0], dev, float(rtol), int(maxit), _PRECOND[precond],
+                  hist.ctypes.data, ctypes.byref(rep)))
+    it = int(rep.iterations)
+    report = {"iterations": it, "converged": bool(rep.converged), "relative_residuals": hist[: it + 1].tolist(),
+              "final_relative_residual": float(rep.final_relative_residual), "wall_time": rep.wall_ms * 1e-3}
+    return x, report
+
+
+def pcg(a, b, rtol: float = 1e-10, maxit: int = 1000, precond: Optional[str] = "jacobi"):
+    """pcg (src/solvers.cpp:109-163) on the device for a CSR tuple (nrows, ncols, row_offsets,
+    col_indices, values): returns (x, report)."""
+    nr, nc, ro, ci, v = a
+    ro = np.ascontiguousarray(ro, np.int64)
+    ci = np.ascontiguousarray(ci, np.int64)
+    v = np.ascontiguousarray(v, np.float64)
+    b = np.ascontiguousarray(b, np.float64)
+    if nr != nc or b.size != nr:
+        raise DimensionMismatch("pcg: matrix not square or rhs length")
+    if precond not in _PRECOND:
+        raise ValueError("precond must be None, 'none' or 'jacobi'")
+    x = np.empty(nr)
+    hist = np.zeros(int(maxit) + 1)
+    rep = _capi.PcgReport()
+    _check(_lib().hdr_csr_pcg_host(nr, ro.ctypes.data, ci.ctypes.data, v.ctypes.data, b.ctypes.data, x.ctypes.data,
+                                   float(rtol), int(maxit), _PRECOND[precond], hist.ctypes.data, ctypes.byref(rep)))
+    it = int(rep.iterations)
+    return x, {"iterations": it, "converged": bool(rep.converged), "relative_residuals": hist[: it + 1].tolist(),
+               "final_relative_residual": float(rep.final_relative_residual), "wall_time": rep.wall_ms * 1e-3}
 
 
 # ------------------------------------------------------------------ reference-mirroring front-end
@@ -542,5 +602,5 @@ from . import algebraic  # noqa: E402  (ReductionInputs-level API; needs _check/
 __all__ = [
     "algebraic", "CapExceededError", "FormatError", "SingularBlockError", "ValidationError", "DimensionMismatch",
     "UnsupportedError", "DeviceError", "Space", "HybridizedOperator", "CondensedOperator", "hybridized_matrix",
-    "space_info", "coefficients_from_config", "space_from_config", "launch_count", "__version__",
+    "space_info", "coefficients_from_config", "space_from_config", "launch_count", "pcg", "__version__",
 ]

@@ -22,6 +22,12 @@ INFO_NAMES = ["dim", "order", "ncells", "nfaces", "ndofs", "broken_ndofs", "elem
 
 _vp, _i32, _i64, _d = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_double
 
+class PcgReport(ctypes.Structure):
+    """hdr_pcg_report"""
+    _fields_ = [("iterations", _i64), ("converged", ctypes.c_int32), ("reserved", ctypes.c_int32),
+                ("final_relative_residual", _d), ("wall_ms", _d)]
+
+
 class AlgInputs(ctypes.Structure):
     """hdr_alg_inputs (include/hdivred_b200.h): a ReductionInputs as plain arrays."""
     _fields_ = [
@@ -81,6 +87,10 @@ _SIGS = {
     "hdr_space_element_matrices": (_i32, [_vp, _vp]),
     "hdr_hybrid_symmetrize": (_i32, [_vp]),
     "hdr_umma_selftest": (_i32, [_i32, _i32, _vp, _vp, _vp, _i32]),
+    "hdr_hybrid_pcg": (_i32, [_vp, _vp, _vp, _i32, _d, _i64, _i32, _vp, _vp]),
+    "hdr_condensed_pcg": (_i32, [_vp, _vp, _vp, _i32, _d, _i64, _i32, _vp, _vp]),
+    "hdr_alg_pcg": (_i32, [_vp, _vp, _vp, _i32, _d, _i64, _i32, _vp, _vp]),
+    "hdr_csr_pcg_host": (_i32, [_i64, _vp, _vp, _vp, _vp, _vp, _d, _i64, _i32, _vp, _vp]),
     "hdr_last_error": (ctypes.c_char_p, []),
     "hdr_version": (ctypes.c_char_p, []),
     "hdr_launch_count": (_i64, []),

@@ -22,7 +22,7 @@ from typing import Optional, Sequence
 import numpy as np
 
 from . import _capi
-from . import _check, _lib
+from . import _check, _lib, _pcg_call
 
 
 @dataclass
@@ -117,6 +117,10 @@ class _AlgOperator:
         if h:
             _lib().hdr_alg_destroy(h)
             self._h = None
+
+    def pcg(self, b=None, rtol: float = 1e-10, maxit: int = 1000, precond: Optional[str] = "jacobi"):
+        """Solve the reduced system (h_mat / s_mat, default rhs g / f_s) on the device: (x, report)."""
+        return _pcg_call(_lib().hdr_alg_pcg, self._h, self.info["nrows"], b, rtol, maxit, precond)
 
     def _matrix(self):
         n, nnz = self.info["nrows"], self.info["nnz"]

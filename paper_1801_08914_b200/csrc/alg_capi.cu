@@ -623,6 +623,30 @@ hdr_status hdr_alg_recover_condensed(hdr_alg_t op, const double* x_b, int64_t xb
 
 void hdr_alg_destroy(hdr_alg_t op) { delete op; }
 
+hdr_status hdr_alg_pcg(hdr_alg_t op, const double* b, double* x, int on_device, double rtol, int64_t maxit,
+                       int precond, double* hist, hdr_pcg_report* rep) {
+  if (!op || !x) return fail(HDR_INVALID_ARGUMENT, "null argument");
+  return catch_all([&]() -> hdr_status {
+    const int64_t n = op->nrows;
+    DBuf<double> db, dx;
+    const double* pb = b ? b : op->rhs.p;
+    if (b && !on_device) {
+      db.upload(b, static_cast<size_t>(n));
+      pb = db.p;
+    }
+    double* px = x;
+    if (!on_device) {
+      dx.alloc(static_cast<size_t>(n));
+      px = dx.p;
+    }
+    const hdr_status s = pcg_device(n, op->row_offsets.p, nullptr, op->col_indices.p, op->values.p, pb, px, rtol, maxit,
+                                    precond, hist, rep, op->st);
+    if (s != HDR_OK) return s;
+    if (!on_device && n) CK(cudaMemcpy(x, px, static_cast<size_t>(n) * 8, cudaMemcpyDeviceToHost));
+    return HDR_OK;
+  });
+}
+
 hdr_status hdr_alg_symmetrize(hdr_alg_t op) {
   if (!op) return fail(HDR_INVALID_ARGUMENT, "null operator");
   return catch_all([&]() -> hdr_status {

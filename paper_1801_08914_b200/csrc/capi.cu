@@ -849,6 +849,65 @@ hdr_status hdr_condensed_spmv(hdr_condensed_t op, const double* x, double* y, in
   return spmv_common(op->sp, 1, op->sval.p, x, y, on_device);
 }
 
+static hdr_status pcg_common(int64_t n, const int64_t* ro, const int32_t* ci, const double* vals, const double* own_rhs,
+                              const double* b, double* x, int on_device, double rtol, int64_t maxit, int precond,
+                              double* hist, hdr_pcg_report* rep, cudaStream_t st) {
+  return catch_all([&]() -> hdr_status {
+    DBuf<double> db, dx;
+    const double* pb = b ? b : own_rhs;
+    if (b && !on_device) {
+      db.upload(b, static_cast<size_t>(n));
+      pb = db.p;
+    }
+    double* px = x;
+    if (!on_device) {
+      dx.alloc(static_cast<size_t>(n));
+      px = dx.p;
+    }
+    const hdr_status s = pcg_device(n, ro, ci, nullptr, vals, pb, px, rtol, maxit, precond, hist, rep, st);
+    if (s != HDR_OK) return s;
+    if (!on_device && n) CK(cudaMemcpy(x, px, static_cast<size_t>(n) * 8, cudaMemcpyDeviceToHost));
+    return HDR_OK;
+  });
+}
+
+hdr_status hdr_hybrid_pcg(hdr_hybrid_t op, const double* b, double* x, int on_device, double rtol, int64_t maxit,
+                          int precond, double* hist, hdr_pcg_report* rep) {
+  if (!op || !x) return fail(HDR_INVALID_ARGUMENT, "null argument");
+  hdr_space_t sp = op->sp;
+  return pcg_common(sp->m, sp->row_h.p, sp->col_h.p, op->hval.p, op->g.p, b, x, on_device, rtol, maxit, precond, hist,
+                    rep, sp->stream);
+}
+
+hdr_status hdr_condensed_pcg(hdr_condensed_t op, const double* b, double* x, int on_device, double rtol,
+                             int64_t maxit, int precond, double* hist, hdr_pcg_report* rep) {
+  if (!op || !x) return fail(HDR_INVALID_ARGUMENT, "null argument");
+  hdr_space_t sp = op->sp;
+  return pcg_common(sp->ns, sp->row_s.p, sp->col_s.p, op->sval.p, op->fs.p, b, x, on_device, rtol, maxit, precond,
+                    hist, rep, sp->stream);
+}
+
+hdr_status hdr_csr_pcg_host(int64_t n, const int64_t* ro, const int64_t* ci, const double* v, const double* b,
+                            double* x, double rtol, int64_t maxit, int precond, double* hist, hdr_pcg_report* rep) {
+  if (n < 0 || !ro || !b || !x || (n > 0 && ro[n] > 0 && (!ci || !v))) return fail(HDR_INVALID_ARGUMENT, "null argument");
+  return catch_all([&]() -> hdr_status {
+    int devs = 0;
+    if (cudaGetDeviceCount(&devs) != cudaSuccess || devs == 0) return fail(HDR_CUDA_ERROR, "no CUDA device available");
+    const int64_t nnz = ro[n];
+    DBuf<int64_t> dro, dci;
+    DBuf<double> dv, db, dx;
+    dro.upload(ro, static_cast<size_t>(n) + 1);
+    dci.upload(ci, static_cast<size_t>(nnz));
+    dv.upload(v, static_cast<size_t>(nnz));
+    db.upload(b, static_cast<size_t>(n));
+    dx.alloc(static_cast<size_t>(n));
+    const hdr_status s = pcg_device(n, dro.p, nullptr, dci.p, dv.p, db.p, dx.p, rtol, maxit, precond, hist, rep, nullptr);
+    if (s != HDR_OK) return s;
+    if (n) CK(cudaMemcpy(x, dx.p, static_cast<size_t>(n) * 8, cudaMemcpyDeviceToHost));
+    return HDR_OK;
+  });
+}
+
 hdr_status hdr_csr_spmv_host(int64_t nrows, int64_t ncols, const int64_t* row_offsets, const int64_t* col_indices,
                              const double* values, const double* x, double* y) {
   if (nrows < 0 || ncols < 0 || !row_offsets || (nrows > 0 && (!col_indices || !values || !x || !y)))

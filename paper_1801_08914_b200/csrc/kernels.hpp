@@ -2,6 +2,8 @@
 #pragma once
 
 #include <cstdint>
+
+#include "../../include/hdivred_b200.h"
 #include <vector>
 
 #include <cuda_runtime.h>
@@ -192,6 +194,10 @@ size_t piola_smem_bytes(int n);
 void launch_affine_assemble(int64_t ncells, int n, const double* dm, const double* alpha, const double* beta,
                             double* out, cudaStream_t st);
 void launch_piola_assemble(const PiolaArgs& a, int grid, cudaStream_t st);
+// device pcg (kern_pcg.cu) on a CSR matrix with int32 (ci32) or int64 (ci64) columns
+hdr_status pcg_device(int64_t n, const int64_t* ro, const int32_t* ci32, const int64_t* ci64, const double* vals,
+                      const double* b, double* x, double rtol, int64_t maxit, int precond, double* hist,
+                      hdr_pcg_report* rep, cudaStream_t st);
 void launch_dot(int64_t n, const double* x, const double* y, double* part, double* out, cudaStream_t st);
 
 }  // namespace hdr
