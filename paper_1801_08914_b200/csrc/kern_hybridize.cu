@@ -288,6 +288,211 @@ __global__ void __launch_bounds__(128, HDR_ROWS_MINB) k_rt0_rows(HybArgs A, Rt0C
   A.g[row] = h[N] + nrow[N];
 }
 
+// ------------------------------------------------------------------ k = 0, thread-per-cell form
+//
+// The same arithmetic as rt0_row_math, one thread per cell: [V | w] in fp32
+// registers (fp64 entries recomputed where H is formed), Delta32 and the
+// correction in per-thread shared-memory columns, the Neumann terms column by
+// column (C_:q = V32 (Delta32 [V|w]_:q), higher orders continue the same
+// column), the order chosen per cell.  No shuffles, no warp barriers, ~1/5 of
+// the lane-per-row instructions; the staging layout and the pass-1 row merge
+// are those of k_rt0_rows.
+constexpr int kCT = 128;
+#ifndef HDR_CELL_MINB
+#define HDR_CELL_MINB 1
+#endif
+
+template <int DIM, int PASS>
+__global__ void __launch_bounds__(kCT, HDR_CELL_MINB) k_rt0_cell(HybArgs A, Rt0Const<2 * DIM> c, double* stage) {
+  constexpr int N = 2 * DIM;
+  constexpr int NC = N + 1;
+  __shared__ float dsm[N * N][kCT];   // Delta32 (row-major), this thread's column
+  __shared__ float csm[N * NC][kCT];  // correction C (row-major)
+  const int tid = threadIdx.x;
+  const uint32_t t = blockIdx.x * kCT + tid;
+  int cc[3] = {0, 0, 0};
+  if (t >= static_cast<uint32_t>(parity_count(A.m))) return;
+  const int e = parity_cell32(A.m, PASS, t, cc);
+  if (e < 0) return;
+  const double a = A.alpha[e], b = A.beta[e];
+  const double ib = 1.0 / b;
+  const double s = b / fma(a, c.lam, b);
+  double f[N];
+#pragma unroll
+  for (int j = 0; j < N; ++j) f[j] = A.f[static_cast<int64_t>(e) * N + j];
+  float v32[N][NC];
+#pragma unroll
+  for (int k = 0; k < N; ++k) {
+    const double xs = c.X[k] * s;
+    double wk = 0.0;
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+      const double vk = fma(xs, c.X[j], c.N0[k * N + j]) * ib;
+      v32[k][j] = static_cast<float>(vk);
+      wk = fma(vk, f[j], wk);
+    }
+    v32[k][N] = static_cast<float>(wk);
+  }
+#pragma unroll
+  for (int k = 0; k < N; ++k) {
+    const int k0 = k & ~1;
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {  // same axis: M_kl != 0
+      const int l = k0 + j;
+      dsm[k * N + l][tid] = static_cast<float>(delta_entry(a, b, c.D[k * N + l], c.M[k * N + l], c.E[k * N + l], c.Ma[k * N + l]));
+    }
+#pragma unroll
+    for (int j = 0; j < N - 2; ++j) {  // other axes: M_kl = Ma_kl = 0 exactly
+      int l = k0 + 2 + j;
+      l = l >= N ? l - N : l;
+      const double d = c.D[k * N + l];
+      const double p1 = __dmul_rn(a, d);
+      const double e1 = __fma_rn(a, d, -p1);
+      dsm[k * N + l][tid] = static_cast<float>(__fma_rn(a, c.E[k * N + l], -e1));
+    }
+  }
+  // first order, column by column: y = Delta32 v_:q, t = V32 y
+  float cm = 0.f, hm = 0.f;
+#pragma unroll
+  for (int q = 0; q <= N; ++q) {
+    float y[N];
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+      float acc = 0.f;
+#pragma unroll
+      for (int l = 0; l < N; ++l) acc = fmaf(dsm[k * N + l][tid], v32[l][q], acc);
+      y[k] = acc;
+    }
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+      float acc = 0.f;
+#pragma unroll
+      for (int j = 0; j < N; ++j) acc = fmaf(v32[k][j], y[j], acc);
+      const float cv = fmaf(1.f, acc, 0.f);
+      csm[k * NC + q][tid] = cv;
+      if (q < N) {
+        cm = fmaxf(cm, fabsf(cv));
+        hm = fmaxf(hm, fabsf(v32[k][q]));
+      }
+    }
+  }
+  // a-posteriori order control (as the lane-per-row kernel, per cell)
+  const double ratio = hm > 0.f ? static_cast<double>(cm) / hm : 0.0;
+  int P = 1;
+  {
+    double tt = ratio * ratio * 10.0;
+    while (tt > 1e-12 && P < A.p_max) {
+      ++P;
+      tt *= ratio;
+    }
+    if (!(ratio < 0.25)) atomicOr(A.status, 1);
+  }
+  if (P > 1) {  // rare: continue each column through the higher orders
+    for (int q = 0; q <= N; ++q) {
+      float tcol[N];
+#pragma unroll
+      for (int k = 0; k < N; ++k) tcol[k] = v32[k][q];
+      for (int p = 1; p <= P; ++p) {
+        float y[N], tn[N];
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+          float acc = 0.f;
+#pragma unroll
+          for (int l = 0; l < N; ++l) acc = fmaf(dsm[k * N + l][tid], tcol[l], acc);
+          y[k] = acc;
+        }
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+          float acc = 0.f;
+#pragma unroll
+          for (int j = 0; j < N; ++j) acc = fmaf(v32[k][j], y[j], acc);
+          tn[k] = acc;
+        }
+        if (p >= 2) {
+          const float sg = (p & 1) ? 1.f : -1.f;
+#pragma unroll
+          for (int k = 0; k < N; ++k) csm[k * NC + q][tid] = fmaf(sg, tn[k], csm[k * NC + q][tid]);
+        }
+#pragma unroll
+        for (int k = 0; k < N; ++k) tcol[k] = tn[k];
+      }
+    }
+  }
+  // h_kq = [V | w]_kq (fp64, recomputed exactly as above) - C_kq
+  auto hrow = [&](int k, double (&h)[NC]) {
+    const double xs = c.X[k] * s;
+    double wk = 0.0;
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+      const double vk = fma(xs, c.X[j], c.N0[k * N + j]) * ib;
+      wk = fma(vk, f[j], wk);
+      h[j] = vk - static_cast<double>(csm[k * NC + j][tid]);
+    }
+    h[N] = wk - static_cast<double>(csm[k * NC + N][tid]);
+  };
+  if (PASS == 0) {
+    double* slot = stage + static_cast<int64_t>(t) * (N * NC);
+    const uint64_t pol = l2_policy_evict_last();
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+      double h[NC];
+      hrow(k, h);
+#pragma unroll
+      for (int q = 0; q <= N; ++q) st_l2hint(slot + k * NC + q, h[q], pol);
+    }
+    return;
+  }
+  // pass 1: complete rows of this cell's interior faces
+  unsigned lo = 0, hi = 0;
+#pragma unroll
+  for (int x = 0; x < DIM; ++x) {
+    const int cx = x == 0 ? cc[0] : (x == 1 ? cc[1] : cc[2]);
+    const int Nx = static_cast<int>(x == 0 ? A.m.N[0] : (x == 1 ? A.m.N[1] : A.m.N[2]));
+    lo |= static_cast<unsigned>(cx > 0) << x;
+    hi |= static_cast<unsigned>(cx + 1 < Nx) << x;
+  }
+  const uint64_t pol = l2_policy_evict_first();
+  const uint32_t half = static_cast<uint32_t>((A.m.N[0] + 1) / 2);
+#pragma unroll
+  for (int k = 0; k < N; ++k) {
+    const int a_ = k >> 1, side = k & 1;
+    const int ca = a_ == 0 ? cc[0] : (a_ == 1 ? cc[1] : cc[2]);
+    const int na = static_cast<int>(a_ == 0 ? A.m.N[0] : (a_ == 1 ? A.m.N[1] : A.m.N[2]));
+    if (!(side ? (ca + 1 < na) : (ca > 0))) continue;
+    const int step = side ? 1 : -1;
+    const int nc0 = cc[0] + (a_ == 0 ? step : 0), nc1 = cc[1] + (a_ == 1 ? step : 0), nc2 = cc[2] + (a_ == 2 ? step : 0);
+    const uint32_t tn = (static_cast<uint32_t>(nc1) + static_cast<uint32_t>(A.m.N[1]) * nc2) * half + (nc0 >> 1);
+    const int kn = k ^ 1;
+    const double* nrow_p = stage + static_cast<int64_t>(tn) * (N * NC) + kn * NC;
+    double nrow[NC];
+#pragma unroll
+    for (int q = 0; q <= N; ++q) nrow[q] = nrow_p[q];
+    const int face = face_id32(A.m, a_, cc[0] + (a_ == 0 ? side : 0), cc[1] + (a_ == 1 ? side : 0), cc[2] + (a_ == 2 ? side : 0));
+    const int row = A.mbase[face];
+    const unsigned far = side ? static_cast<unsigned>(ca + 2 < na) : static_cast<unsigned>(ca >= 2);
+    const unsigned flags = lo | (hi << DIM) | (far << (2 * DIM));
+    const uint64_t* tab = A.rank_tab + ((static_cast<size_t>(k) << (2 * DIM + 1)) + flags) * 2;
+    const uint64_t own = __ldg(tab), nbr = __ldg(tab + 1);
+    double* out = A.hval + A.rowoff[row];
+    double h[NC];
+    hrow(k, h);
+#pragma unroll
+    for (int q = 0; q < N; ++q) {
+      const unsigned r = static_cast<unsigned>(own >> (4 * q)) & 15u;
+      if (r == 15u) continue;
+      const double v = q == k ? h[q] + nrow[kn] : h[q];
+      st_l2hint(out + r, v, pol);
+    }
+#pragma unroll
+    for (int q = 0; q < N; ++q) {
+      const unsigned r = static_cast<unsigned>(nbr >> (4 * q)) & 15u;
+      if (r == 15u) continue;
+      st_l2hint(out + r, nrow[q], pol);
+    }
+    A.g[row] = h[N] + nrow[N];
+  }
+}
+
 // ------------------------------------------------------------------ k >= 1
 
 constexpr int kIB = 8;   // rows of Delta per block
@@ -604,18 +809,31 @@ void launch_hybridize_rt0_rows(const HybArgs& a, const double* hc, double* stage
     c.lam = hc[5 * N * N + N];
     c.rho = hc[5 * N * N + N + 1];
   };
+  static const bool rows = getenv("HDR_RT0_ROWS") != nullptr;  // lane-per-row variant (A/B timing)
   if (a.m.dim == 3) {
     Rt0Const<6> c;
     fill(c, 6);
-    const unsigned nb = static_cast<unsigned>((cnt + 4 * 5 - 1) / (4 * 5));
-    k_rt0_rows<3, 0><<<nb, 128, 0, st>>>(a, c, stage);
-    k_rt0_rows<3, 1><<<nb, 128, 0, st>>>(a, c, stage);
+    if (rows) {
+      const unsigned nb = static_cast<unsigned>((cnt + 4 * 5 - 1) / (4 * 5));
+      k_rt0_rows<3, 0><<<nb, 128, 0, st>>>(a, c, stage);
+      k_rt0_rows<3, 1><<<nb, 128, 0, st>>>(a, c, stage);
+    } else {
+      const unsigned nb = static_cast<unsigned>((cnt + kCT - 1) / kCT);
+      k_rt0_cell<3, 0><<<nb, kCT, 0, st>>>(a, c, stage);
+      k_rt0_cell<3, 1><<<nb, kCT, 0, st>>>(a, c, stage);
+    }
   } else {
     Rt0Const<4> c;
     fill(c, 4);
-    const unsigned nb = static_cast<unsigned>((cnt + 4 * 8 - 1) / (4 * 8));
-    k_rt0_rows<2, 0><<<nb, 128, 0, st>>>(a, c, stage);
-    k_rt0_rows<2, 1><<<nb, 128, 0, st>>>(a, c, stage);
+    if (rows) {
+      const unsigned nb = static_cast<unsigned>((cnt + 4 * 8 - 1) / (4 * 8));
+      k_rt0_rows<2, 0><<<nb, 128, 0, st>>>(a, c, stage);
+      k_rt0_rows<2, 1><<<nb, 128, 0, st>>>(a, c, stage);
+    } else {
+      const unsigned nb = static_cast<unsigned>((cnt + kCT - 1) / kCT);
+      k_rt0_cell<2, 0><<<nb, kCT, 0, st>>>(a, c, stage);
+      k_rt0_cell<2, 1><<<nb, kCT, 0, st>>>(a, c, stage);
+    }
   }
   count_launch(2);
 }
