@@ -302,7 +302,7 @@ constexpr int kCT = 128;
 #define HDR_CELL_MINB 1
 #endif
 
-template <int DIM, int PASS>
+template <int DIM, int PASS, bool SIDE>
 __global__ void __launch_bounds__(kCT, HDR_CELL_MINB) k_rt0_cell(HybArgs A, Rt0Const<2 * DIM> c, double* stage) {
   constexpr int N = 2 * DIM;
   constexpr int NC = N + 1;
@@ -430,6 +430,51 @@ __global__ void __launch_bounds__(kCT, HDR_CELL_MINB) k_rt0_cell(HybArgs A, Rt0C
     }
     h[N] = wk - static_cast<double>(csm[k * NC + N][tid]);
   };
+  if (SIDE) {
+    // both colours write their own columns of their faces' rows straight into H;
+    // the two shared quantities of a row (diagonal, g) meet in a per-row side
+    // slot: colour 0 parks them, colour 1 adds its own (same bits as the
+    // staged merge: h(colour 1) + h(colour 0))
+    unsigned lo = 0, hi = 0;
+#pragma unroll
+    for (int x = 0; x < DIM; ++x) {
+      const int cx = x == 0 ? cc[0] : (x == 1 ? cc[1] : cc[2]);
+      const int Nx = static_cast<int>(x == 0 ? A.m.N[0] : (x == 1 ? A.m.N[1] : A.m.N[2]));
+      lo |= static_cast<unsigned>(cx > 0) << x;
+      hi |= static_cast<unsigned>(cx + 1 < Nx) << x;
+    }
+    const uint64_t pol = PASS == 0 ? l2_policy_evict_last() : l2_policy_evict_first();
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+      const int a_ = k >> 1, side = k & 1;
+      const int ca = a_ == 0 ? cc[0] : (a_ == 1 ? cc[1] : cc[2]);
+      const int na = static_cast<int>(a_ == 0 ? A.m.N[0] : (a_ == 1 ? A.m.N[1] : A.m.N[2]));
+      if (!(side ? (ca + 1 < na) : (ca > 0))) continue;
+      const int face = face_id32(A.m, a_, cc[0] + (a_ == 0 ? side : 0), cc[1] + (a_ == 1 ? side : 0), cc[2] + (a_ == 2 ? side : 0));
+      const int row = A.mbase[face];
+      const unsigned far = side ? static_cast<unsigned>(ca + 2 < na) : static_cast<unsigned>(ca >= 2);
+      const unsigned flags = lo | (hi << DIM) | (far << (2 * DIM));
+      const uint64_t own = __ldg(A.rank_tab + ((static_cast<size_t>(k) << (2 * DIM + 1)) + flags) * 2);
+      double* out = A.hval + A.rowoff[row];
+      double h[NC];
+      hrow(k, h);
+#pragma unroll
+      for (int q = 0; q < N; ++q) {
+        const unsigned r = static_cast<unsigned>(own >> (4 * q)) & 15u;
+        if (r == 15u || q == k) continue;
+        st_l2hint(out + r, h[q], pol);
+      }
+      double* sv = stage + 2 * static_cast<int64_t>(row);
+      if (PASS == 0) {
+        st_l2hint(sv, h[k], l2_policy_evict_last());
+        st_l2hint(sv + 1, h[N], l2_policy_evict_last());
+      } else {
+        out[(own >> (4 * k)) & 15u] = h[k] + sv[0];
+        A.g[row] = h[N] + sv[1];
+      }
+    }
+    return;
+  }
   if (PASS == 0) {
     double* slot = stage + static_cast<int64_t>(t) * (N * NC);
     const uint64_t pol = l2_policy_evict_last();
@@ -810,6 +855,7 @@ void launch_hybridize_rt0_rows(const HybArgs& a, const double* hc, double* stage
     c.rho = hc[5 * N * N + N + 1];
   };
   static const bool rows = getenv("HDR_RT0_ROWS") != nullptr;  // lane-per-row variant (A/B timing)
+  static const bool side = getenv("HDR_RT0_STAGE") == nullptr;  // default: per-row side slots; HDR_RT0_STAGE=1: row stage
   if (a.m.dim == 3) {
     Rt0Const<6> c;
     fill(c, 6);
@@ -817,10 +863,14 @@ void launch_hybridize_rt0_rows(const HybArgs& a, const double* hc, double* stage
       const unsigned nb = static_cast<unsigned>((cnt + 4 * 5 - 1) / (4 * 5));
       k_rt0_rows<3, 0><<<nb, 128, 0, st>>>(a, c, stage);
       k_rt0_rows<3, 1><<<nb, 128, 0, st>>>(a, c, stage);
+    } else if (side) {
+      const unsigned nb = static_cast<unsigned>((cnt + kCT - 1) / kCT);
+      k_rt0_cell<3, 0, true><<<nb, kCT, 0, st>>>(a, c, stage);
+      k_rt0_cell<3, 1, true><<<nb, kCT, 0, st>>>(a, c, stage);
     } else {
       const unsigned nb = static_cast<unsigned>((cnt + kCT - 1) / kCT);
-      k_rt0_cell<3, 0><<<nb, kCT, 0, st>>>(a, c, stage);
-      k_rt0_cell<3, 1><<<nb, kCT, 0, st>>>(a, c, stage);
+      k_rt0_cell<3, 0, false><<<nb, kCT, 0, st>>>(a, c, stage);
+      k_rt0_cell<3, 1, false><<<nb, kCT, 0, st>>>(a, c, stage);
     }
   } else {
     Rt0Const<4> c;
@@ -829,10 +879,14 @@ void launch_hybridize_rt0_rows(const HybArgs& a, const double* hc, double* stage
       const unsigned nb = static_cast<unsigned>((cnt + 4 * 8 - 1) / (4 * 8));
       k_rt0_rows<2, 0><<<nb, 128, 0, st>>>(a, c, stage);
       k_rt0_rows<2, 1><<<nb, 128, 0, st>>>(a, c, stage);
+    } else if (side) {
+      const unsigned nb = static_cast<unsigned>((cnt + kCT - 1) / kCT);
+      k_rt0_cell<2, 0, true><<<nb, kCT, 0, st>>>(a, c, stage);
+      k_rt0_cell<2, 1, true><<<nb, kCT, 0, st>>>(a, c, stage);
     } else {
       const unsigned nb = static_cast<unsigned>((cnt + kCT - 1) / kCT);
-      k_rt0_cell<2, 0><<<nb, kCT, 0, st>>>(a, c, stage);
-      k_rt0_cell<2, 1><<<nb, kCT, 0, st>>>(a, c, stage);
+      k_rt0_cell<2, 0, false><<<nb, kCT, 0, st>>>(a, c, stage);
+      k_rt0_cell<2, 1, false><<<nb, kCT, 0, st>>>(a, c, stage);
     }
   }
   count_launch(2);
