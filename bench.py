@@ -439,6 +439,93 @@ def ours(args):
     return 0
 
 
+def stage_bench(args):
+    """Timing of the other in-scope stages of the path (SURVEY.md §8(d) "other
+    stages"): static condensation, hybrid recovery, SpMV with H.  Device-resident
+    inputs, CUDA events on the library's stream, L2 flushed between steps;
+    roofline from the §8(d) cost models."""
+    import torch
+    import ctypes
+
+    import paper_1801_08914_b200 as hd
+
+    cfg = CONFIGS[args.config]
+    alpha, beta, f_hat = make_inputs(cfg, cfg["seed"])
+    sp = hd.Space(cfg["dim"], cfg["cells"], cfg["k"])
+    if cfg.get("perturb"):
+        sp.set_vertices(make_vertices(cfg, cfg["seed"]))
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    sp.set_stream(stream.cuda_stream)
+    a_d, b_d, f_d = (torch.from_numpy(x).cuda() for x in (alpha, beta, f_hat))
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float64, device="cuda")
+    n, nc, m = sp.n, sp.ncells, sp.m
+    dpf = sp.info["dofs_per_face"]
+    nint = sp.info["interior_dofs_per_cell"]
+    nb = n - nint
+    lib = hd._lib()
+    if args.stage == "condense":
+        cop = sp.static_condense(a_d, b_d, f_d)
+
+        def run():
+            st = lib.hdr_static_condense_fe_into(cop._h, a_d.data_ptr(), b_d.data_ptr(), f_d.data_ptr(), 1)
+            assert st == 0, hd._capi.last_error()
+        flops = nc * (2 * (nint ** 3 / 3 + nint ** 2 * nb + nint * nb ** 2) + 2 * (nint ** 2 + nint * nb) + 3 * n ** 2)
+        byts = nc * (16 + 8 * n) + 8 * (sp.info["nnz_s"] + sp.info["n_s"])
+        metric = "elements/s of static condensation (assemble+condense+scatter)"
+    elif args.stage == "recover":
+        op = sp.hybridize(a_d, b_d, f_d)
+        lam = torch.from_numpy(np.random.default_rng(3).uniform(-1, 1, m)).cuda()
+
+        def run():
+            op.recover(lam, f_d)
+        flops = nc * (2 * n ** 3 / 3 + 4 * n ** 2)
+        byts = nc * (16 + 16 * n) + 8 * m
+        metric = "elements/s of hybrid recovery (x_hat = A^-1 (f - C^T lambda), averaged x)"
+    else:  # spmv
+        op = sp.hybridize(a_d, b_d, f_d)
+        x = torch.from_numpy(np.random.default_rng(4).uniform(-1, 1, m)).cuda()
+        nnz = sp.info["nnz_h"]
+
+        def run():
+            op.spmv(x)
+        flops = 2 * nnz
+        byts = 12 * nnz + 8 * (m + 1) + 16 * m
+        metric = "rows/s of SpMV with H (reference row-sum order)"
+    for _ in range(args.warmup):
+        run()
+    torch.cuda.synchronize()
+    ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    l0 = hd.launch_count()
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        for i in range(args.steps):
+            flush.fill_(float(i))
+            ev0[i].record(stream)
+            run()
+            ev1[i].record(stream)
+        torch.cuda.synchronize()
+    launches = hd.launch_count() - l0
+    ms = float(np.mean([a.elapsed_time(b) for a, b in zip(ev0, ev1)]))
+    units = m if args.stage == "spmv" else nc
+    peak, kind = load_peaks()
+    tfl, _ = hd.measure_fp64_peak()
+    bw = byts / (ms * 1e-3) / 1e9
+    fl = flops / (ms * 1e-3) / 1e12
+    hbm_frac, fp_frac = bw / peak, fl / tfl
+    roof = ({"bound": "hbm", "achieved": bw, "peak": peak, "unit": "GB/s", "frac": hbm_frac, "traffic": None}
+            if hbm_frac >= fp_frac or args.stage == "spmv" else
+            {"bound": "fp64", "achieved": fl, "peak": tfl, "unit": "TFLOP/s", "frac": fp_frac, "traffic": None})
+    roof.update({"algorithmic_bytes_per_step": byts, "algorithmic_flops_per_step": flops})
+    print(json.dumps({"metric": metric, "value": units / (ms * 1e-3), "unit": "rows/s" if args.stage == "spmv" else UNIT,
+                      "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+                      "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                      "data": "synthetic", "config": {"workload": cfg["desc"], "stage": args.stage,
+                                                      "l2": "flushed between steps"},
+                      "roofline": roof, "gpu_launches": launches, "clocks": clk.summary()}))
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -450,11 +537,15 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--fp64", action="store_true", help="also report the fp64 roofline for k = 0")
     ap.add_argument("--no-graph", action="store_true", help="launch the step directly instead of replaying a CUDA graph")
+    ap.add_argument("--stage", default="hybridize", choices=["hybridize", "condense", "recover", "spmv"],
+                    help="time another stage of the path (not the headline metric)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":
         return reference_arm(args)
+    if args.stage != "hybridize":
+        return stage_bench(args)
     return ours(args)
 
 

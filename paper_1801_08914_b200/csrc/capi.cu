@@ -670,7 +670,8 @@ hdr_status hdr_recover_hybrid(hdr_hybrid_t op, const double* lambda, const doubl
     R.x_hat = pxh;
     R.x = px;
     R.status = op->status.p;
-    launch_recover_hybrid(R, nullptr, 0, st);
+    if (sp->k == 0) launch_recover_rt0(R, sp->rt0_consts.data(), st);
+    else launch_recover_hybrid(R, nullptr, 0, st);
     launch_average_faces(sp->dm, pxh, px, st);
     CK(cudaGetLastError());
     if (!on_device) {

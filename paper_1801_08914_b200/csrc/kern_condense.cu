@@ -184,7 +184,9 @@ __device__ void dd_refined_solve(const CondArgs& C, double a, double b, int ni, 
   }
 }
 
-__global__ void __launch_bounds__(kNT) k_sc_cta(CondArgs C, int parity, double* gws, int64_t stride, int use_smem) {
+// small interior blocks (ni <= 32, e.g. RT1 hexahedra): 128 threads per cell,
+// column-per-thread solves in shared memory (the layout uses nF columns)
+__global__ void __launch_bounds__(kNT) k_sc_small(CondArgs C, int parity, double* gws, int64_t stride, int use_smem) {
   extern __shared__ double smem[];
   double* ws = use_smem ? smem : gws + blockIdx.x * stride;
   const DevMesh& m = C.m;
@@ -280,6 +282,248 @@ __global__ void __launch_bounds__(kNT) k_sc_cta(CondArgs C, int parity, double* 
   (void)ns;
 }
 
+// One warp: y <- L^-T L^-1 y for CPW columns y_c (stride ys) with the
+// Cholesky factor L (row-major lower, leading dimension ni) and its inverse
+// diagonal.  The columns live in registers (lane owns rows lane + 32 s), y_j is
+// broadcast with a shuffle: no memory round trip and no barrier on the chain;
+// CPW independent columns interleave their chains.
+template <int S, int CPW>
+__device__ void warp_chol_solve(const double* l, const double* ld, int ni, double* const (&y)[CPW], int ys, int ncol,
+                                int lane) {
+  double v[CPW][S];
+#pragma unroll
+  for (int c = 0; c < CPW; ++c)
+#pragma unroll
+    for (int t = 0; t < S; ++t) {
+      const int i = 32 * t + lane;
+      v[c][t] = (c < ncol && i < ni) ? y[c][i * ys] : 0.0;
+    }
+#pragma unroll
+  for (int s = 0; s < S; ++s)
+    for (int jj = 0; jj < 32; ++jj) {  // forward: L z = y
+      const int j = 32 * s + jj;
+      if (j >= ni) break;
+      const double inv = ld[j];
+      double yj[CPW];
+#pragma unroll
+      for (int c = 0; c < CPW; ++c) {
+        if (lane == jj) v[c][s] *= inv;
+        yj[c] = __shfl_sync(0xffffffffu, v[c][s], jj);
+      }
+#pragma unroll
+      for (int t = s; t < S; ++t) {
+        const int i = 32 * t + lane;
+        if (i > j && i < ni) {
+          const double lij = l[i * ni + j];
+#pragma unroll
+          for (int c = 0; c < CPW; ++c) v[c][t] = fma(-lij, yj[c], v[c][t]);
+        }
+      }
+    }
+#pragma unroll
+  for (int s = S - 1; s >= 0; --s)
+    for (int jj = 31; jj >= 0; --jj) {  // backward: L^T x = z
+      const int j = 32 * s + jj;
+      if (j >= ni) continue;
+      const double inv = ld[j];
+      double yj[CPW];
+#pragma unroll
+      for (int c = 0; c < CPW; ++c) {
+        if (lane == jj) v[c][s] *= inv;
+        yj[c] = __shfl_sync(0xffffffffu, v[c][s], jj);
+      }
+#pragma unroll
+      for (int t = 0; t <= s; ++t) {
+        const int i = 32 * t + lane;
+        if (i < j) {
+          const double lji = l[j * ni + i];
+#pragma unroll
+          for (int c = 0; c < CPW; ++c) v[c][t] = fma(-lji, yj[c], v[c][t]);
+        }
+      }
+    }
+#pragma unroll
+  for (int c = 0; c < CPW; ++c)
+#pragma unroll
+    for (int t = 0; t < S; ++t) {
+      const int i = 32 * t + lane;
+      if (c < ncol && i < ni) y[c][i * ys] = v[c][t];
+    }
+}
+
+constexpr int kSC = 256;  // threads of the k >= 1 condensation CTA
+constexpr int kSK = 16;   // K chunk of the S GEMM
+
+// Per cell: Cholesky of A_ii; [W | x] = A_ii^-1 [A_iF | f_i] by warp-level
+// sweeps (one column per warp at a time); x refined to double-double (exact
+// residuals, warp sweep corrections); S = A_FF - A_Fi W as a tiled GEMM (A_Fi
+// assembled into shared memory by K chunks, 4 x 4 register tiles);
+// f_S = f_F - A_Fi x with error-free products; scatter as before.
+template <int S>
+__global__ void __launch_bounds__(kSC, 2) k_sc_cta(CondArgs C, int parity, double* gws, int64_t stride, int use_smem) {
+  extern __shared__ double smem[];
+  __shared__ double afs[96 * kSK];  // A_Fi chunk (p, k), nf <= 96
+  __shared__ double wks[kSK * 96];  // W chunk (k, q)
+  double* ws = use_smem ? smem : gws + blockIdx.x * stride;
+  const DevMesh& m = C.m;
+  const int n = m.n, ni = m.nint, nf = C.nF, dpf = m.dpf, dim = m.dim;
+  const int nc = nf + 1;  // [W | x] columns
+  const ScLayout L = sc_layout(ni, nc, n);
+  double* aii = ws + L.aii;
+  double* wx = ws + L.aif;  // ni x nc: [A_iF | f_i] -> [W | x]
+  double* xl = ws + L.xl;
+  double* r = ws + L.r;
+  double* ldi = ws + L.d;  // 1 / L_jj
+  double* fl = ws + L.f;
+  __shared__ int flag;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t cnt = static_cast<uint32_t>(parity_count(m));
+  for (uint32_t t = blockIdx.x; t < cnt; t += gridDim.x) {
+    int cc[3];
+    const int e = parity_cell32(m, parity, t, cc);
+    if (e < 0) continue;
+    const double a = C.alpha[e], b = C.beta[e];
+    if (tid == 0) flag = 0;
+    for (int i = tid; i < n; i += kSC) fl[i] = C.f[static_cast<int64_t>(e) * n + i];
+    for (int idx = tid; idx < ni * ni; idx += kSC) {
+      const int i = idx / ni, j = idx - i * ni;
+      aii[idx] = assemble_entry(a, b, C.fx.D[i * n + j], C.fx.M[i * n + j]);
+    }
+    for (int idx = tid; idx < ni * nc; idx += kSC) {
+      const int i = idx / nc, c = idx - i * nc;
+      wx[idx] = c < nf ? assemble_entry(a, b, C.fx.D[i * n + ni + c], C.fx.M[i * n + ni + c]) : C.f[static_cast<int64_t>(e) * n + i];
+    }
+    __syncthreads();
+    cta_cholesky(aii, ni, &flag);
+    if (flag && tid == 0) atomicOr(C.status, 2);
+    for (int i = tid; i < ni; i += kSC) {
+      ldi[i] = 1.0 / aii[i * ni + i];  // inverse diagonal of L
+      xl[i] = 0.0;
+    }
+    __syncthreads();
+    // [W | x] = A_ii^-1 [A_iF | f_i]: two columns per warp at a time
+    for (int c = 2 * warp; c < nc; c += 2 * (kSC / 32)) {
+      double* const cols[2] = {wx + c, wx + c + 1};
+      warp_chol_solve<S, 2>(aii, ldi, ni, cols, nc, min(2, nc - c), lane);
+    }
+    __syncthreads();
+    // x to double-double: r = f_i - A_ii (x + xl) exactly accumulated, x += A_ii^-1 r
+    for (int step = 0; step < 3; ++step) {
+      for (int i = tid; i < ni; i += kSC) {
+        ddv acc = {fl[i], 0.0};
+        for (int j = 0; j < ni; ++j) {
+          const double aij = assemble_entry(a, b, C.fx.D[i * n + j], C.fx.M[i * n + j]);
+          acc = dd_fma_sub(acc, aij, wx[j * nc + nf]);
+          acc.lo = fma(-aij, xl[j], acc.lo);
+        }
+        r[i] = acc.hi + acc.lo;
+      }
+      __syncthreads();
+      if (warp == 0) {
+        double* const rc[1] = {r};
+        warp_chol_solve<S, 1>(aii, ldi, ni, rc, 1, 1, lane);
+        for (int i = lane; i < ni; i += 32) {
+          const ddv v = dd_add_d({wx[i * nc + nf], xl[i]}, r[i]);
+          wx[i * nc + nf] = v.hi;
+          xl[i] = v.lo;
+        }
+      }
+      __syncthreads();
+    }
+    // scatter tables
+    unsigned lo = 0, hi = 0;
+    for (int x = 0; x < dim; ++x) {
+      const int cx = x == 0 ? cc[0] : (x == 1 ? cc[1] : cc[2]);
+      const int Nx = static_cast<int>(x == 0 ? m.N[0] : (x == 1 ? m.N[1] : m.N[2]));
+      lo |= static_cast<unsigned>(cx > 0) << x;
+      hi |= static_cast<unsigned>(cx + 1 < Nx) << x;
+    }
+    // f_S,p = f_F,p - A_Fi x  (x in double-double)
+    for (int p = tid; p < nf; p += kSC) {
+      const int ps = p / dpf, sub = p - ps * dpf;
+      const int ax = ps >> 1, side = ps & 1;
+      const bool pin = (((side) ? hi : lo) >> ax) & 1u;
+      const int face = face_id32(m, ax, cc[0] + (ax == 0 ? side : 0), cc[1] + (ax == 1 ? side : 0), cc[2] + (ax == 2 ? side : 0));
+      ddv acc = {fl[ni + p], 0.0};
+      for (int i = 0; i < ni; ++i) {
+        const double api = assemble_entry(a, b, C.fx.D[(ni + p) * n + i], C.fx.M[(ni + p) * n + i]);
+        acc = dd_fma_sub(acc, api, wx[i * nc + nf]);
+        acc.lo = fma(-api, xl[i], acc.lo);
+      }
+      const double v = (side ? 1.0 : -1.0) * (acc.hi + acc.lo);
+      const int row = face * dpf + sub;
+      C.fs[row] = (parity == 1 && pin) ? C.fs[row] + v : v;
+    }
+    // S = A_FF - A_Fi W: 4 x 4 register tiles over (p, q), K in chunks staged in shared memory
+    const int TS = (nf + 3) / 4;
+    for (int tile0 = 0; tile0 < TS * TS; tile0 += kSC) {
+      const int tile = tile0 + tid;
+      const bool own = tile < TS * TS;
+      const int p0 = own ? (tile / TS) * 4 : 0, q0 = own ? (tile % TS) * 4 : 0;
+      double acc[4][4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+      for (int k0 = 0; k0 < ni; k0 += kSK) {
+        const int kw = min(kSK, ni - k0);
+        __syncthreads();
+        for (int idx = tid; idx < nf * kSK; idx += kSC) {
+          const int p = idx / kSK, kk = idx - p * kSK;
+          afs[idx] = kk < kw ? assemble_entry(a, b, C.fx.D[(ni + p) * n + k0 + kk], C.fx.M[(ni + p) * n + k0 + kk]) : 0.0;
+        }
+        for (int idx = tid; idx < kSK * nf; idx += kSC) {
+          const int kk = idx / nf, q = idx - kk * nf;
+          wks[idx] = kk < kw ? wx[(k0 + kk) * nc + q] : 0.0;
+        }
+        __syncthreads();
+        if (own)
+          for (int kk = 0; kk < kw; ++kk) {
+            double av[4], wv[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) av[i] = p0 + i < nf ? afs[(p0 + i) * kSK + kk] : 0.0;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) wv[j] = q0 + j < nf ? wks[kk * nf + q0 + j] : 0.0;
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+              for (int j = 0; j < 4; ++j) acc[i][j] = fma(av[i], wv[j], acc[i][j]);
+          }
+      }
+      if (own)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int p = p0 + i;
+          if (p >= nf) continue;
+          const int ps = p / dpf, sub = p - ps * dpf;
+          const int ax = ps >> 1, side = ps & 1;
+          const bool pin = (((side) ? hi : lo) >> ax) & 1u;
+          const int face = face_id32(m, ax, cc[0] + (ax == 0 ? side : 0), cc[1] + (ax == 1 ? side : 0),
+                                     cc[2] + (ax == 2 ? side : 0));
+          const double sp = side ? 1.0 : -1.0;
+          const bool add = parity == 1 && pin;
+          const int row = face * dpf + sub;
+          const int64_t start = C.rowoff[row];
+          const int ca = ax == 0 ? cc[0] : (ax == 1 ? cc[1] : cc[2]);
+          const int na = static_cast<int>(ax == 0 ? m.N[0] : (ax == 1 ? m.N[1] : m.N[2]));
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int q = q0 + j;
+            if (q >= nf) continue;
+            const double sv = assemble_entry(a, b, C.fx.D[(ni + p) * n + ni + q], C.fx.M[(ni + p) * n + ni + q]) - acc[i][j];
+            const int qs = q / dpf, sj = q - qs * dpf;
+            const double sq = (qs & 1) ? 1.0 : -1.0;
+            const int rk = col_rank_fast(dim, ps, qs, lo, hi, ca, na, true);
+            double* dst = C.sval + start + static_cast<int64_t>(rk) * dpf + sj;
+            const double v = sp * sq * sv;
+            *dst = (add && ps == qs) ? *dst + v : v;
+          }
+        }
+    }
+    __syncthreads();
+  }
+}
+
 // recover_condensed: x_i = A_ii^-1 (f_i - A_iF x_b,T) (double-double), masters copied
 __global__ void __launch_bounds__(kNT) k_rc_cta(CondArgs C, double* gws, int64_t stride, int use_smem) {
   extern __shared__ double smem[];
@@ -343,20 +587,40 @@ void launch_condense(const CondArgs& c, int parity, double* gws, int64_t ws_doub
     count_launch();
     return;
   }
-  const ScLayout L = sc_layout(c.m.nint, c.nF, c.m.n);
+  if (c.m.nint <= 32) {  // small interior blocks: the 128-thread shared-memory kernel
+    const ScLayout Ls = sc_layout(c.m.nint, c.nF, c.m.n);
+    const bool sm_ok = Ls.total * 8 <= 96 * 1024;
+    const size_t smem_s = sm_ok ? static_cast<size_t>(Ls.total) * 8 : 0;
+    if (sm_ok) cudaFuncSetAttribute(k_sc_small, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_s));
+    const int64_t cnt_s = parity_count(c.m);
+    int64_t grid_s = sm_ok ? std::min<int64_t>(cnt_s, 148 * 16) : std::min<int64_t>(cnt_s, ws_doubles / Ls.total);
+    grid_s = std::max<int64_t>(grid_s, 1);
+    k_sc_small<<<static_cast<unsigned>(grid_s), kNT, smem_s, st>>>(c, parity, gws, Ls.total, sm_ok ? 1 : 0);
+    count_launch();
+    return;
+  }
+  const ScLayout L = sc_layout(c.m.nint, c.nF + 1, c.m.n);
   const bool use_smem = L.total * 8 <= 96 * 1024;
   const size_t smem = use_smem ? static_cast<size_t>(L.total) * 8 : 0;
-  if (use_smem) cudaFuncSetAttribute(k_sc_cta, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   const int64_t cnt = parity_count(c.m);
   int64_t grid = use_smem ? std::min<int64_t>(cnt, 148 * 16) : std::min<int64_t>(cnt, ws_doubles / L.total);
   grid = std::max<int64_t>(grid, 1);
-  k_sc_cta<<<static_cast<unsigned>(grid), kNT, smem, st>>>(c, parity, gws, L.total, use_smem ? 1 : 0);
+  auto go = [&](auto kern) {
+    if (use_smem) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    kern<<<static_cast<unsigned>(grid), kSC, smem, st>>>(c, parity, gws, L.total, use_smem ? 1 : 0);
+  };
+  const int ni = c.m.nint;  // rows per lane in the warp-level triangular sweeps
+  if (ni <= 32) go(k_sc_cta<1>);
+  else if (ni <= 64) go(k_sc_cta<2>);
+  else if (ni <= 96) go(k_sc_cta<3>);
+  else if (ni <= 128) go(k_sc_cta<4>);
+  else go(k_sc_cta<5>);
   count_launch();
 }
 
 int64_t condense_ws_doubles(const DevMesh& m, int nF) {
   if (m.nint == 0) return 0;
-  const ScLayout L = sc_layout(m.nint, nF, m.n);
+  const ScLayout L = sc_layout(m.nint, nF + 1, m.n);
   return L.total * 8 <= 96 * 1024 ? 0 : L.total * 148 * 2;
 }
 

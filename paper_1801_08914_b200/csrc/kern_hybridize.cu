@@ -813,6 +813,66 @@ __global__ void __launch_bounds__(kNT) k_recover_cta(RecArgs R, double* gws, int
   (void)nsl;
 }
 
+// k = 0 recovery, one thread per cell: x_hat = A_T^-1 r, r = f - C_T^T lambda,
+// by the structured solve in fp64 (A0^-1 = (N0 + s X X^T) / beta, Neumann
+// terms with the exact rounding errors Delta; order from the a-priori bound
+// rho alpha / beta as the CTA form).  Constants in the kernel-parameter bank.
+template <int DIM>
+__global__ void __launch_bounds__(128) k_rt0_recover(RecArgs R, Rt0Const<2 * DIM> c) {
+  constexpr int N = 2 * DIM;
+  const int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (e >= R.m.ncells) return;
+  const double a = R.alpha[e], b = R.beta[e];
+  const double ib = 1.0 / b;
+  const double s = b / fma(a, c.lam, b);
+  int cc[3];
+  cell_coords32(R.m, static_cast<uint32_t>(e), cc);
+  double y[N];
+#pragma unroll
+  for (int k = 0; k < N; ++k) {
+    double v = R.f[e * N + k];
+    const int a_ = k >> 1, side = k & 1;
+    const int ca = a_ == 0 ? cc[0] : (a_ == 1 ? cc[1] : cc[2]);
+    const int na = static_cast<int>(a_ == 0 ? R.m.N[0] : (a_ == 1 ? R.m.N[1] : R.m.N[2]));
+    if (side ? (ca + 1 < na) : (ca > 0)) {  // unit constraint rows: C_T^T lambda
+      const int face = face_id32(R.m, a_, cc[0] + (a_ == 0 ? side : 0), cc[1] + (a_ == 1 ? side : 0),
+                                 cc[2] + (a_ == 2 ? side : 0));
+      v -= R.lambda[R.mbase[face]];
+    }
+    y[k] = v;
+  }
+  const int P = neumann_order(c.rho * a * ib, R.p_max, R.status);
+  double acc[N];
+  for (int p = 0; p <= P; ++p) {
+    // t = A0^-1 y
+    double xty = 0.0;
+#pragma unroll
+    for (int l = 0; l < N; ++l) xty = fma(c.X[l], y[l], xty);
+    xty *= s;
+    double t[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      double u = 0.0;
+#pragma unroll
+      for (int l = 0; l < N; ++l) u = fma(c.N0[i * N + l], y[l], u);
+      u = fma(c.X[i], xty, u);
+      t[i] = u * ib;
+      acc[i] = (p == 0) ? t[i] : ((p & 1) ? acc[i] - t[i] : acc[i] + t[i]);
+    }
+    if (p == P) break;
+#pragma unroll
+    for (int i = 0; i < N; ++i) {  // y = Delta t
+      double u = 0.0;
+#pragma unroll
+      for (int l = 0; l < N; ++l)
+        u = fma(delta_entry(a, b, c.D[i * N + l], c.M[i * N + l], c.E[i * N + l], c.Ma[i * N + l]), t[l], u);
+      y[i] = u;
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < N; ++k) R.x_hat[e * N + k] = acc[k];
+}
+
 // x = (P^T P)^-1 P^T x_hat: signed average of the face copies, bubbles copied
 // (src/reduction.cpp:396-404; the Gram matrix of the FE P is diagonal)
 __global__ void k_average(DevMesh m, const double* x_hat, double* x) {
@@ -920,6 +980,30 @@ void launch_hybridize_cta(const HybArgs& a, int parity, double* gws, int64_t ws_
   if (grid > 1 << 30) grid = 1 << 30;
   (void)sm_count;
   k_hyb_cta<<<static_cast<unsigned>(grid), kNT, smem, st>>>(a, parity, gws, need, use_smem ? 1 : 0);
+  count_launch();
+}
+
+void launch_recover_rt0(const RecArgs& a, const double* hc, cudaStream_t st) {
+  auto fill = [&](auto& c, int N) {
+    memcpy(c.D, hc, sizeof(double) * N * N);
+    memcpy(c.M, hc + N * N, sizeof(double) * N * N);
+    memcpy(c.E, hc + 2 * N * N, sizeof(double) * N * N);
+    memcpy(c.Ma, hc + 3 * N * N, sizeof(double) * N * N);
+    memcpy(c.N0, hc + 4 * N * N, sizeof(double) * N * N);
+    memcpy(c.X, hc + 5 * N * N, sizeof(double) * N);
+    c.lam = hc[5 * N * N + N];
+    c.rho = hc[5 * N * N + N + 1];
+  };
+  const unsigned nb = static_cast<unsigned>((a.m.ncells + 127) / 128);
+  if (a.m.dim == 3) {
+    Rt0Const<6> c;
+    fill(c, 6);
+    k_rt0_recover<3><<<nb, 128, 0, st>>>(a, c);
+  } else {
+    Rt0Const<4> c;
+    fill(c, 4);
+    k_rt0_recover<2><<<nb, 128, 0, st>>>(a, c);
+  }
   count_launch();
 }
 

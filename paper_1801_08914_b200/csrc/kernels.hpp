@@ -78,6 +78,8 @@ struct RecArgs {
   int* status;
 };
 void launch_recover_hybrid(const RecArgs& a, double* gws, int64_t ws_doubles, cudaStream_t st);
+// k = 0: one thread per cell (host_consts as launch_hybridize_rt0_rows)
+void launch_recover_rt0(const RecArgs& a, const double* host_consts, cudaStream_t st);
 void launch_average_faces(const DevMesh& m, const double* x_hat, double* x, cudaStream_t st);
 
 // ---- static condensation / recover_condensed (kern_condense.cu)
