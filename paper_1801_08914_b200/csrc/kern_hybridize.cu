@@ -297,7 +297,13 @@ __global__ void __launch_bounds__(128, HDR_ROWS_MINB) k_rt0_rows(HybArgs A, Rt0C
 // column), the order chosen per cell.  No shuffles, no warp barriers, ~1/5 of
 // the lane-per-row instructions; the staging layout and the pass-1 row merge
 // are those of k_rt0_rows.
-constexpr int kCT = 128;
+#ifndef HDR_CELL_VSM
+#define HDR_CELL_VSM 0
+#endif
+#ifndef HDR_CELL_CT
+#define HDR_CELL_CT 64
+#endif
+constexpr int kCT = HDR_CELL_CT;
 #ifndef HDR_CELL_MINB
 #define HDR_CELL_MINB 1
 #endif
@@ -308,6 +314,12 @@ __global__ void __launch_bounds__(kCT, HDR_CELL_MINB) k_rt0_cell(HybArgs A, Rt0C
   constexpr int NC = N + 1;
   __shared__ float dsm[N * N][kCT];   // Delta32 (row-major), this thread's column
   __shared__ float csm[N * NC][kCT];  // correction C (row-major)
+#if HDR_CELL_VSM
+  __shared__ float vsm[N * NC][kCT];  // [V | w] fp32 (row-major)
+#define V32(k, q) vsm[(k) * NC + (q)][tid]
+#else
+#define V32(k, q) v32[k][q]
+#endif
   const int tid = threadIdx.x;
   const uint32_t t = blockIdx.x * kCT + tid;
   int cc[3] = {0, 0, 0};
@@ -320,7 +332,9 @@ __global__ void __launch_bounds__(kCT, HDR_CELL_MINB) k_rt0_cell(HybArgs A, Rt0C
   double f[N];
 #pragma unroll
   for (int j = 0; j < N; ++j) f[j] = A.f[static_cast<int64_t>(e) * N + j];
+#if !HDR_CELL_VSM
   float v32[N][NC];
+#endif
 #pragma unroll
   for (int k = 0; k < N; ++k) {
     const double xs = c.X[k] * s;
@@ -328,10 +342,10 @@ __global__ void __launch_bounds__(kCT, HDR_CELL_MINB) k_rt0_cell(HybArgs A, Rt0C
 #pragma unroll
     for (int j = 0; j < N; ++j) {
       const double vk = fma(xs, c.X[j], c.N0[k * N + j]) * ib;
-      v32[k][j] = static_cast<float>(vk);
+      V32(k, j) = static_cast<float>(vk);
       wk = fma(vk, f[j], wk);
     }
-    v32[k][N] = static_cast<float>(wk);
+    V32(k, N) = static_cast<float>(wk);
   }
 #pragma unroll
   for (int k = 0; k < N; ++k) {
@@ -360,19 +374,19 @@ __global__ void __launch_bounds__(kCT, HDR_CELL_MINB) k_rt0_cell(HybArgs A, Rt0C
     for (int k = 0; k < N; ++k) {
       float acc = 0.f;
 #pragma unroll
-      for (int l = 0; l < N; ++l) acc = fmaf(dsm[k * N + l][tid], v32[l][q], acc);
+      for (int l = 0; l < N; ++l) acc = fmaf(dsm[k * N + l][tid], V32(l, q), acc);
       y[k] = acc;
     }
 #pragma unroll
     for (int k = 0; k < N; ++k) {
       float acc = 0.f;
 #pragma unroll
-      for (int j = 0; j < N; ++j) acc = fmaf(v32[k][j], y[j], acc);
+      for (int j = 0; j < N; ++j) acc = fmaf(V32(k, j), y[j], acc);
       const float cv = fmaf(1.f, acc, 0.f);
       csm[k * NC + q][tid] = cv;
       if (q < N) {
         cm = fmaxf(cm, fabsf(cv));
-        hm = fmaxf(hm, fabsf(v32[k][q]));
+        hm = fmaxf(hm, fabsf(V32(k, q)));
       }
     }
   }
@@ -391,7 +405,7 @@ __global__ void __launch_bounds__(kCT, HDR_CELL_MINB) k_rt0_cell(HybArgs A, Rt0C
     for (int q = 0; q <= N; ++q) {
       float tcol[N];
 #pragma unroll
-      for (int k = 0; k < N; ++k) tcol[k] = v32[k][q];
+      for (int k = 0; k < N; ++k) tcol[k] = V32(k, q);
       for (int p = 1; p <= P; ++p) {
         float y[N], tn[N];
 #pragma unroll
@@ -405,7 +419,7 @@ __global__ void __launch_bounds__(kCT, HDR_CELL_MINB) k_rt0_cell(HybArgs A, Rt0C
         for (int k = 0; k < N; ++k) {
           float acc = 0.f;
 #pragma unroll
-          for (int j = 0; j < N; ++j) acc = fmaf(v32[k][j], y[j], acc);
+          for (int j = 0; j < N; ++j) acc = fmaf(V32(k, j), y[j], acc);
           tn[k] = acc;
         }
         if (p >= 2) {
