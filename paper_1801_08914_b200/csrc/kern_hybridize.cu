@@ -760,20 +760,28 @@ __global__ void __launch_bounds__(kNT) k_hyb_cta(HybArgs A, int parity, double* 
 
 // ------------------------------------------------------------------ recovery
 
-// x_hat_T = A_T^-1 (f_T - C_T^T lambda) by the same structured solve (one CTA per cell)
+// x_hat_T = A_T^-1 (f_T - C_T^T lambda) by the same structured solve (one CTA per cell):
+// the Neumann series of A0^-1 Delta in fp64 with the a-priori order; every
+// matrix-vector product is done warp-per-row with the lanes striding along the
+// row (coalesced loads of the fixed factors) and a shuffle reduction.
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
 __global__ void __launch_bounds__(kNT) k_recover_cta(RecArgs R, double* gws, int64_t ws_stride, int use_smem) {
   extern __shared__ double smem[];
   double* ws = use_smem ? smem : gws + blockIdx.x * ws_stride;
   const DevMesh& m = R.m;
-  const int n = m.n, r = R.fx.r, dpf = m.dpf, nsl = 2 * m.dim, nint = m.nint;
+  const int n = m.n, r = R.fx.r, dpf = m.dpf, nint = m.nint;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const bool wide = n > 64;       // long rows: warp per row; short rows: thread per row
   double* s = ws;                 // r
   double* y = ws + 64;            // n: current rhs
   double* t = y + kMaxN;          // n: current term
   double* acc = t + kMaxN;        // n: sum
   double* xty = acc + kMaxN;      // r
-  HybArgs A;
-  A.m = R.m;
-  A.fx = R.fx;
   for (int64_t e = blockIdx.x; e < m.ncells; e += gridDim.x) {
     const double a = R.alpha[e], b = R.beta[e];
     const double ib = 1.0 / b;
@@ -793,38 +801,73 @@ __global__ void __launch_bounds__(kNT) k_recover_cta(RecArgs R, double* gws, int
     __syncthreads();
     const int P = neumann_order(R.fx.rho * a * ib, R.p_max, R.status);
     for (int p = 0; p <= P; ++p) {
-      // t = A0^-1 y
-      for (int j = threadIdx.x; j < r; j += blockDim.x) {
-        double u = 0.0;
-        for (int l = 0; l < n; ++l) u = fma(__ldg(R.fx.X + static_cast<int64_t>(l) * r + j), y[l], u);
-        xty[j] = u * s[j];
+      // t = A0^-1 y = (N0 y + X diag(s) X^T y) / beta
+      if (wide) {  // warp per row, lanes along the row
+        for (int j = warp; j < r; j += nw) {
+          double u = 0.0;
+          for (int l = lane; l < n; l += 32) u = fma(__ldg(R.fx.X + static_cast<int64_t>(l) * r + j), y[l], u);
+          u = warp_sum(u);
+          if (lane == 0) xty[j] = u * s[j];
+        }
+      } else {  // small elements: thread per row
+        for (int j = threadIdx.x; j < r; j += blockDim.x) {
+          double u = 0.0;
+          for (int l = 0; l < n; ++l) u = fma(__ldg(R.fx.X + static_cast<int64_t>(l) * r + j), y[l], u);
+          xty[j] = u * s[j];
+        }
       }
       __syncthreads();
-      for (int i = threadIdx.x; i < n; i += blockDim.x) {
-        double u = 0.0;
-        for (int l = 0; l < n; ++l) u = fma(__ldg(R.fx.N0 + static_cast<int64_t>(i) * n + l), y[l], u);
-        for (int j = 0; j < r; ++j) u = fma(__ldg(R.fx.X + static_cast<int64_t>(i) * r + j), xty[j], u);
-        u *= ib;
-        t[i] = u;
-        acc[i] = (p == 0) ? u : ((p & 1) ? acc[i] - u : acc[i] + u);
+      if (wide) {
+        for (int i = warp; i < n; i += nw) {
+          const double* row = R.fx.N0 + static_cast<int64_t>(i) * n;
+          double u = 0.0;
+          for (int l = lane; l < n; l += 32) u = fma(__ldg(row + l), y[l], u);
+          for (int j = lane; j < r; j += 32) u = fma(__ldg(R.fx.X + static_cast<int64_t>(i) * r + j), xty[j], u);
+          u = warp_sum(u);
+          if (lane == 0) {
+            u *= ib;
+            t[i] = u;
+            acc[i] = (p == 0) ? u : ((p & 1) ? acc[i] - u : acc[i] + u);
+          }
+        }
+      } else {
+        for (int i = threadIdx.x; i < n; i += blockDim.x) {
+          double u = 0.0;
+          for (int l = 0; l < n; ++l) u = fma(__ldg(R.fx.N0 + static_cast<int64_t>(i) * n + l), y[l], u);
+          for (int j = 0; j < r; ++j) u = fma(__ldg(R.fx.X + static_cast<int64_t>(i) * r + j), xty[j], u);
+          u *= ib;
+          t[i] = u;
+          acc[i] = (p == 0) ? u : ((p & 1) ? acc[i] - u : acc[i] + u);
+        }
       }
       __syncthreads();
       if (p == P) break;
       // y = Delta t
-      for (int i = threadIdx.x; i < n; i += blockDim.x) {
-        double u = 0.0;
-        for (int l = 0; l < n; ++l) {
-          const int64_t o = static_cast<int64_t>(i) * n + l;
-          u = fma(delta_entry(a, b, __ldg(R.fx.D + o), __ldg(R.fx.M + o), __ldg(R.fx.E + o), __ldg(R.fx.Ma + o)), t[l], u);
+      if (wide) {
+        for (int i = warp; i < n; i += nw) {
+          double u = 0.0;
+          for (int l = lane; l < n; l += 32) {
+            const int64_t o = static_cast<int64_t>(i) * n + l;
+            u = fma(delta_entry(a, b, __ldg(R.fx.D + o), __ldg(R.fx.M + o), __ldg(R.fx.E + o), __ldg(R.fx.Ma + o)), t[l], u);
+          }
+          u = warp_sum(u);
+          if (lane == 0) y[i] = u;
         }
-        y[i] = u;
+      } else {
+        for (int i = threadIdx.x; i < n; i += blockDim.x) {
+          double u = 0.0;
+          for (int l = 0; l < n; ++l) {
+            const int64_t o = static_cast<int64_t>(i) * n + l;
+            u = fma(delta_entry(a, b, __ldg(R.fx.D + o), __ldg(R.fx.M + o), __ldg(R.fx.E + o), __ldg(R.fx.Ma + o)), t[l], u);
+          }
+          y[i] = u;
+        }
       }
       __syncthreads();
     }
     for (int i = threadIdx.x; i < n; i += blockDim.x) R.x_hat[e * n + i] = acc[i];
     __syncthreads();
   }
-  (void)nsl;
 }
 
 // k = 0 recovery, one thread per cell: x_hat = A_T^-1 r, r = f - C_T^T lambda,
