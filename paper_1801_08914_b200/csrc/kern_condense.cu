@@ -113,21 +113,27 @@ __host__ __device__ inline ScLayout sc_layout(int ni, int nf, int n) {
 }
 
 // Cholesky of ni x ni (row-major, lower) in place; returns false if not SPD
-__device__ bool cta_cholesky(double* a, int ni, int* flag) {
+__device__ bool cta_cholesky(double* a, int ni, int* flag, int ld = 0) {
+  if (ld == 0) ld = ni;
+  __shared__ double colk[256];  // column k of the factor (ni <= 256)
   for (int k = 0; k < ni; ++k) {
     if (threadIdx.x == 0) {
-      const double dkk = a[k * ni + k];
+      const double dkk = a[k * ld + k];
       if (!(dkk > 0.0)) *flag = 1;
-      a[k * ni + k] = sqrt(fmax(dkk, 0.0));
+      a[k * ld + k] = sqrt(fmax(dkk, 0.0));
     }
     __syncthreads();
-    const double lkk = a[k * ni + k];
-    for (int i = k + 1 + threadIdx.x; i < ni; i += blockDim.x) a[i * ni + k] = lkk > 0.0 ? a[i * ni + k] / lkk : 0.0;
+    const double lkk = a[k * ld + k];
+    for (int i = k + 1 + threadIdx.x; i < ni; i += blockDim.x) a[i * ld + k] = lkk > 0.0 ? a[i * ld + k] / lkk : 0.0;
     __syncthreads();
-    const int rem = ni - k - 1;
-    for (int idx = threadIdx.x; idx < rem * rem; idx += blockDim.x) {
-      const int i = k + 1 + idx / rem, j = k + 1 + idx % rem;
-      if (j <= i) a[i * ni + j] = fma(-a[i * ni + k], a[j * ni + k], a[i * ni + j]);
+    // trailing update of the lower triangle: warps over rows i, lanes over columns j <= i
+    // (contiguous in the row-major factor); column k read from a contiguous copy
+    for (int i = k + 1 + threadIdx.x; i < ni; i += blockDim.x) colk[i] = a[i * ld + k];
+    __syncthreads();
+    const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    for (int i = k + 1 + (threadIdx.x >> 5); i < ni; i += nw) {
+      const double lik = colk[i];
+      for (int j = k + 1 + lane; j <= i; j += 32) a[i * ld + j] = fma(-lik, colk[j], a[i * ld + j]);
     }
     __syncthreads();
   }
@@ -288,8 +294,8 @@ __global__ void __launch_bounds__(kNT) k_sc_small(CondArgs C, int parity, double
 // broadcast with a shuffle: no memory round trip and no barrier on the chain;
 // CPW independent columns interleave their chains.
 template <int S, int CPW>
-__device__ void warp_chol_solve(const double* l, const double* ld, int ni, double* const (&y)[CPW], int ys, int ncol,
-                                int lane) {
+__device__ void warp_chol_solve(const double* l, int lda, const double* ld, int ni, double* const (&y)[CPW], int ys,
+                                int ncol, int lane) {
   double v[CPW][S];
 #pragma unroll
   for (int c = 0; c < CPW; ++c)
@@ -314,7 +320,7 @@ __device__ void warp_chol_solve(const double* l, const double* ld, int ni, doubl
       for (int t = s; t < S; ++t) {
         const int i = 32 * t + lane;
         if (i > j && i < ni) {
-          const double lij = l[i * ni + j];
+          const double lij = l[i * lda + j];
 #pragma unroll
           for (int c = 0; c < CPW; ++c) v[c][t] = fma(-lij, yj[c], v[c][t]);
         }
@@ -336,7 +342,7 @@ __device__ void warp_chol_solve(const double* l, const double* ld, int ni, doubl
       for (int t = 0; t <= s; ++t) {
         const int i = 32 * t + lane;
         if (i < j) {
-          const double lji = l[j * ni + i];
+          const double lji = l[j * lda + i];
 #pragma unroll
           for (int c = 0; c < CPW; ++c) v[c][t] = fma(-lji, yj[c], v[c][t]);
         }
@@ -360,16 +366,18 @@ constexpr int kSK = 16;   // K chunk of the S GEMM
 // assembled into shared memory by K chunks, 4 x 4 register tiles);
 // f_S = f_F - A_Fi x with error-free products; scatter as before.
 template <int S>
-__global__ void __launch_bounds__(kSC, 2) k_sc_cta(CondArgs C, int parity, double* gws, int64_t stride, int use_smem) {
+__global__ void __launch_bounds__(kSC, 1) k_sc_cta(CondArgs C, int parity, double* gws, int64_t stride, int use_smem) {
   extern __shared__ double smem[];
   __shared__ double afs[96 * kSK];  // A_Fi chunk (p, k), nf <= 96
   __shared__ double wks[kSK * 96];  // W chunk (k, q)
-  double* ws = use_smem ? smem : gws + blockIdx.x * stride;
+  // use_smem: 1 = whole workspace in shared memory, 2 = only A_ii / its factor
+  double* ws = use_smem == 1 ? smem : gws + blockIdx.x * stride;
   const DevMesh& m = C.m;
   const int n = m.n, ni = m.nint, nf = C.nF, dpf = m.dpf, dim = m.dim;
   const int nc = nf + 1;  // [W | x] columns
   const ScLayout L = sc_layout(ni, nc, n);
-  double* aii = ws + L.aii;
+  double* aii = use_smem == 2 ? smem : ws + L.aii;
+  const int lda = use_smem == 2 ? (ni | 1) : ni;  // odd row stride: conflict-free column reads of the factor
   double* wx = ws + L.aif;  // ni x nc: [A_iF | f_i] -> [W | x]
   double* xl = ws + L.xl;
   double* r = ws + L.r;
@@ -387,24 +395,24 @@ __global__ void __launch_bounds__(kSC, 2) k_sc_cta(CondArgs C, int parity, doubl
     for (int i = tid; i < n; i += kSC) fl[i] = C.f[static_cast<int64_t>(e) * n + i];
     for (int idx = tid; idx < ni * ni; idx += kSC) {
       const int i = idx / ni, j = idx - i * ni;
-      aii[idx] = assemble_entry(a, b, C.fx.D[i * n + j], C.fx.M[i * n + j]);
+      aii[i * lda + j] = assemble_entry(a, b, C.fx.D[i * n + j], C.fx.M[i * n + j]);
     }
     for (int idx = tid; idx < ni * nc; idx += kSC) {
       const int i = idx / nc, c = idx - i * nc;
       wx[idx] = c < nf ? assemble_entry(a, b, C.fx.D[i * n + ni + c], C.fx.M[i * n + ni + c]) : C.f[static_cast<int64_t>(e) * n + i];
     }
     __syncthreads();
-    cta_cholesky(aii, ni, &flag);
+    cta_cholesky(aii, ni, &flag, lda);
     if (flag && tid == 0) atomicOr(C.status, 2);
     for (int i = tid; i < ni; i += kSC) {
-      ldi[i] = 1.0 / aii[i * ni + i];  // inverse diagonal of L
+      ldi[i] = 1.0 / aii[i * lda + i];  // inverse diagonal of L
       xl[i] = 0.0;
     }
     __syncthreads();
     // [W | x] = A_ii^-1 [A_iF | f_i]: two columns per warp at a time
     for (int c = 2 * warp; c < nc; c += 2 * (kSC / 32)) {
       double* const cols[2] = {wx + c, wx + c + 1};
-      warp_chol_solve<S, 2>(aii, ldi, ni, cols, nc, min(2, nc - c), lane);
+      warp_chol_solve<S, 2>(aii, lda, ldi, ni, cols, nc, min(2, nc - c), lane);
     }
     __syncthreads();
     // x to double-double: r = f_i - A_ii (x + xl) exactly accumulated, x += A_ii^-1 r
@@ -421,7 +429,7 @@ __global__ void __launch_bounds__(kSC, 2) k_sc_cta(CondArgs C, int parity, doubl
       __syncthreads();
       if (warp == 0) {
         double* const rc[1] = {r};
-        warp_chol_solve<S, 1>(aii, ldi, ni, rc, 1, 1, lane);
+        warp_chol_solve<S, 1>(aii, lda, ldi, ni, rc, 1, 1, lane);
         for (int i = lane; i < ni; i += 32) {
           const ddv v = dd_add_d({wx[i * nc + nf], xl[i]}, r[i]);
           wx[i * nc + nf] = v.hi;
@@ -601,13 +609,17 @@ void launch_condense(const CondArgs& c, int parity, double* gws, int64_t ws_doub
   }
   const ScLayout L = sc_layout(c.m.nint, c.nF + 1, c.m.n);
   const bool use_smem = L.total * 8 <= 96 * 1024;
-  const size_t smem = use_smem ? static_cast<size_t>(L.total) * 8 : 0;
+  // otherwise keep at least the factor of A_ii on chip (the sweeps read it ni^2 times)
+  const bool aii_smem = !use_smem && static_cast<int64_t>(c.m.nint) * (c.m.nint | 1) * 8 <= 190 * 1024;
+  const size_t smem = use_smem ? static_cast<size_t>(L.total) * 8
+                               : (aii_smem ? static_cast<size_t>(c.m.nint) * (c.m.nint | 1) * 8 : 0);
+  const int mode = use_smem ? 1 : (aii_smem ? 2 : 0);
   const int64_t cnt = parity_count(c.m);
   int64_t grid = use_smem ? std::min<int64_t>(cnt, 148 * 16) : std::min<int64_t>(cnt, ws_doubles / L.total);
   grid = std::max<int64_t>(grid, 1);
   auto go = [&](auto kern) {
-    if (use_smem) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    kern<<<static_cast<unsigned>(grid), kSC, smem, st>>>(c, parity, gws, L.total, use_smem ? 1 : 0);
+    if (smem) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    kern<<<static_cast<unsigned>(grid), kSC, smem, st>>>(c, parity, gws, L.total, mode);
   };
   const int ni = c.m.nint;  // rows per lane in the warp-level triangular sweeps
   if (ni <= 32) go(k_sc_cta<1>);
