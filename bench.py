@@ -219,7 +219,7 @@ def kernel_name(cfg: dict) -> str:
     if cfg.get("perturb"):
         return "k_piola_assemble + k_alg<HYB> + k_run_sum"
     if cfg["k"] == 0:
-        return "k_rt0_rows<dim,0> + k_rt0_rows<dim,1> (colour passes)"
+        return "k_rt0_cell<dim,0> + k_rt0_cell<dim,1> (colour passes)"
     if cfg["dim"] == 3 and cfg["k"] >= 2:
         return "k_hyb_big<k> x2 colours"
     return "k_hyb_warp x2 colours"

@@ -7,6 +7,7 @@
 // point returns HDR_CUDA_ERROR.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <atomic>
 #include <functional>
 #include <cmath>
@@ -57,6 +58,7 @@ struct hdr_space_s {
   DBuf<double> fixed;  // D, M, E, Ma, N0 (n*n each), X (n*r), lam (r)
   std::vector<double> rt0_consts;  // packed constant block of the k = 0 kernel
   DBuf<uint64_t> rank_tab;         // k = 0 row-rank table
+  DBuf<longlong2> frs;             // k = 0 per-face {row start, row}
   DBuf<double> premat;             // k >= 2 (3D): [N0 ; X^T] column-major ((n + r) x n)
   Fixed fx{};
   GeomState* geom = nullptr;  // mapped (trilinear) cells: hdr_space_set_vertices
@@ -315,6 +317,8 @@ hdr_status hdr_space_create(int dim, const int64_t cells[3], const double h[3], 
       const std::vector<uint64_t> tab = rank_table_rt0(dim);
       sp->rank_tab.alloc(tab.size());
       CK(cudaMemcpyAsync(sp->rank_tab.p, tab.data(), tab.size() * 8, cudaMemcpyHostToDevice, st));
+      sp->frs.alloc(static_cast<size_t>(sp->nfaces));
+      launch_face_rows(sp->nfaces, sp->mbase.p, sp->row_h.p, sp->frs.p, st);
     }
     if (sp->weighted) {  // weighted constraint rows: the per-cell elimination path (geom.cu, affine cells)
       std::vector<int> mb(static_cast<size_t>(sp->nfaces));
@@ -504,8 +508,10 @@ static hdr_status run_hybridize(hdr_hybrid_t op, const double* alpha, const doub
     A.g = op->g.p;
     A.status = op->status.p;
     A.rank_tab = sp->rank_tab.p;
+    A.frs = sp->frs.p;
     if (sp->k == 0) {
-      const int64_t need = parity_count(sp->dm) * sp->n * (sp->n + 1);  // colour-0 staging
+      // colour-0 staging: per cell slot (row-stage variant), per face (side slots; brick: N+1 per face)
+      const int64_t need = std::max<int64_t>(parity_count(sp->dm) * sp->n * (sp->n + 1), (sp->n + 1) * sp->nfaces);
       if (op->ws_doubles < need) {
         op->ws.alloc(static_cast<size_t>(need));
         op->ws_doubles = need;

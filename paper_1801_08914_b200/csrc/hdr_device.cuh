@@ -234,6 +234,20 @@ __device__ __forceinline__ double ld_l2hint(const double* a, uint64_t pol) {
   return v;
 }
 
+// ------------------------------------------------------------ asynchronous global -> shared copies
+// (cp.async: the loads are in flight while the thread computes, no registers held)
+__device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(sdst))),
+               "l"(gsrc)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* sdst, const void* gsrc) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(sdst))),
+               "l"(gsrc)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 // ------------------------------------------------------------ error-free transforms
 
 __device__ __forceinline__ void two_prod(double a, double b, double& p, double& e) {

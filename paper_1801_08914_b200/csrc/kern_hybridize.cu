@@ -20,6 +20,7 @@
 // item 7) and fl(a+b) = fl(b+a), so the result is deterministic without atomics.
 #include <algorithm>
 #include <cstdio>
+#include <type_traits>
 #include <cstdlib>
 #include <cstring>
 
@@ -295,11 +296,7 @@ __global__ void __launch_bounds__(128, HDR_ROWS_MINB) k_rt0_rows(HybArgs A, Rt0C
 // correction in per-thread shared-memory columns, the Neumann terms column by
 // column (C_:q = V32 (Delta32 [V|w]_:q), higher orders continue the same
 // column), the order chosen per cell.  No shuffles, no warp barriers, ~1/5 of
-// the lane-per-row instructions; the staging layout and the pass-1 row merge
-// are those of k_rt0_rows.
-#ifndef HDR_CELL_VSM
-#define HDR_CELL_VSM 0
-#endif
+// the lane-per-row instructions.
 #ifndef HDR_CELL_CT
 #define HDR_CELL_CT 64
 #endif
@@ -308,33 +305,14 @@ constexpr int kCT = HDR_CELL_CT;
 #define HDR_CELL_MINB 1
 #endif
 
-template <int DIM, int PASS, bool SIDE>
-__global__ void __launch_bounds__(kCT, HDR_CELL_MINB) k_rt0_cell(HybArgs A, Rt0Const<2 * DIM> c, double* stage) {
+// correction C (N x (N+1), row-major) of one cell into csm[.][tid]
+template <int DIM, int CT>
+__device__ __forceinline__ void rt0_cell_correction(const HybArgs& A, const Rt0Const<2 * DIM>& c, double a, double b,
+                                                    double s, double ib, const double (&f)[2 * DIM],
+                                                    float (*dsm)[CT], float (*csm)[CT], int tid) {
   constexpr int N = 2 * DIM;
   constexpr int NC = N + 1;
-  __shared__ float dsm[N * N][kCT];   // Delta32 (row-major), this thread's column
-  __shared__ float csm[N * NC][kCT];  // correction C (row-major)
-#if HDR_CELL_VSM
-  __shared__ float vsm[N * NC][kCT];  // [V | w] fp32 (row-major)
-#define V32(k, q) vsm[(k) * NC + (q)][tid]
-#else
-#define V32(k, q) v32[k][q]
-#endif
-  const int tid = threadIdx.x;
-  const uint32_t t = blockIdx.x * kCT + tid;
-  int cc[3] = {0, 0, 0};
-  if (t >= static_cast<uint32_t>(parity_count(A.m))) return;
-  const int e = parity_cell32(A.m, PASS, t, cc);
-  if (e < 0) return;
-  const double a = A.alpha[e], b = A.beta[e];
-  const double ib = 1.0 / b;
-  const double s = b / fma(a, c.lam, b);
-  double f[N];
-#pragma unroll
-  for (int j = 0; j < N; ++j) f[j] = A.f[static_cast<int64_t>(e) * N + j];
-#if !HDR_CELL_VSM
   float v32[N][NC];
-#endif
 #pragma unroll
   for (int k = 0; k < N; ++k) {
     const double xs = c.X[k] * s;
@@ -342,10 +320,10 @@ __global__ void __launch_bounds__(kCT, HDR_CELL_MINB) k_rt0_cell(HybArgs A, Rt0C
 #pragma unroll
     for (int j = 0; j < N; ++j) {
       const double vk = fma(xs, c.X[j], c.N0[k * N + j]) * ib;
-      V32(k, j) = static_cast<float>(vk);
+      v32[k][j] = static_cast<float>(vk);
       wk = fma(vk, f[j], wk);
     }
-    V32(k, N) = static_cast<float>(wk);
+    v32[k][N] = static_cast<float>(wk);
   }
 #pragma unroll
   for (int k = 0; k < N; ++k) {
@@ -374,19 +352,19 @@ __global__ void __launch_bounds__(kCT, HDR_CELL_MINB) k_rt0_cell(HybArgs A, Rt0C
     for (int k = 0; k < N; ++k) {
       float acc = 0.f;
 #pragma unroll
-      for (int l = 0; l < N; ++l) acc = fmaf(dsm[k * N + l][tid], V32(l, q), acc);
+      for (int l = 0; l < N; ++l) acc = fmaf(dsm[k * N + l][tid], v32[l][q], acc);
       y[k] = acc;
     }
 #pragma unroll
     for (int k = 0; k < N; ++k) {
       float acc = 0.f;
 #pragma unroll
-      for (int j = 0; j < N; ++j) acc = fmaf(V32(k, j), y[j], acc);
+      for (int j = 0; j < N; ++j) acc = fmaf(v32[k][j], y[j], acc);
       const float cv = fmaf(1.f, acc, 0.f);
       csm[k * NC + q][tid] = cv;
       if (q < N) {
         cm = fmaxf(cm, fabsf(cv));
-        hm = fmaxf(hm, fabsf(V32(k, q)));
+        hm = fmaxf(hm, fabsf(v32[k][q]));
       }
     }
   }
@@ -405,7 +383,7 @@ __global__ void __launch_bounds__(kCT, HDR_CELL_MINB) k_rt0_cell(HybArgs A, Rt0C
     for (int q = 0; q <= N; ++q) {
       float tcol[N];
 #pragma unroll
-      for (int k = 0; k < N; ++k) tcol[k] = V32(k, q);
+      for (int k = 0; k < N; ++k) tcol[k] = v32[k][q];
       for (int p = 1; p <= P; ++p) {
         float y[N], tn[N];
 #pragma unroll
@@ -419,7 +397,7 @@ __global__ void __launch_bounds__(kCT, HDR_CELL_MINB) k_rt0_cell(HybArgs A, Rt0C
         for (int k = 0; k < N; ++k) {
           float acc = 0.f;
 #pragma unroll
-          for (int j = 0; j < N; ++j) acc = fmaf(V32(k, j), y[j], acc);
+          for (int j = 0; j < N; ++j) acc = fmaf(v32[k][j], y[j], acc);
           tn[k] = acc;
         }
         if (p >= 2) {
@@ -432,24 +410,46 @@ __global__ void __launch_bounds__(kCT, HDR_CELL_MINB) k_rt0_cell(HybArgs A, Rt0C
       }
     }
   }
-  // h_kq = [V | w]_kq (fp64, recomputed exactly as above) - C_kq
-  auto hrow = [&](int k, double (&h)[NC]) {
-    const double xs = c.X[k] * s;
-    double wk = 0.0;
+}
+
+// row k of [H_T | g_T]: [V | w]_k,: (fp64, recomputed exactly) - C_k,:
+template <int DIM, int CT>
+__device__ __forceinline__ void rt0_hrow(const Rt0Const<2 * DIM>& c, double s, double ib, const double (&f)[2 * DIM],
+                                         const float (*csm)[CT], int tid, int k, double (&h)[2 * DIM + 1]) {
+  constexpr int N = 2 * DIM;
+  constexpr int NC = N + 1;
+  const double xs = c.X[k] * s;
+  double wk = 0.0;
 #pragma unroll
-    for (int j = 0; j < N; ++j) {
-      const double vk = fma(xs, c.X[j], c.N0[k * N + j]) * ib;
-      wk = fma(vk, f[j], wk);
-      h[j] = vk - static_cast<double>(csm[k * NC + j][tid]);
-    }
-    h[N] = wk - static_cast<double>(csm[k * NC + N][tid]);
-  };
+  for (int j = 0; j < N; ++j) {
+    const double vk = fma(xs, c.X[j], c.N0[k * N + j]) * ib;
+    wk = fma(vk, f[j], wk);
+    h[j] = vk - static_cast<double>(csm[k * NC + j][tid]);
+  }
+  h[N] = wk - static_cast<double>(csm[k * NC + N][tid]);
+}
+
+template <int DIM, int PASS, bool SIDE>
+__global__ void __launch_bounds__(kCT, HDR_CELL_MINB) k_rt0_cell(HybArgs A, Rt0Const<2 * DIM> c, double* stage) {
+  constexpr int N = 2 * DIM;
+  constexpr int NC = N + 1;
+  __shared__ float dsm[N * N][kCT];   // Delta32 (row-major), this thread's column
+  __shared__ float csm[N * NC][kCT];  // correction C (row-major)
+  __shared__ longlong2 pf_rs[SIDE ? N : 1][kCT];                       // {row start, row} per slot
+  __shared__ unsigned long long pf_tab[SIDE ? N : 1][kCT];             // packed column ranks
+  __shared__ double2 pf_sv[(SIDE && PASS == 1) ? N : 1][kCT];          // colour 0's {diagonal, g}
+  const int tid = threadIdx.x;
+  const uint32_t t = blockIdx.x * kCT + tid;
+  int cc[3] = {0, 0, 0};
+  if (t >= static_cast<uint32_t>(parity_count(A.m))) return;
+  const int e = parity_cell32(A.m, PASS, t, cc);
+  if (e < 0) return;
+  const double a = A.alpha[e], b = A.beta[e];
+  // SIDE: the scatter metadata of the cell's interior faces (row start + row, the
+  // packed column ranks, colour 1: colour 0's parked side slot) is fetched into
+  // shared memory now, so its latency hides behind the element solve
+  unsigned lo = 0, hi = 0, inmask = 0;
   if (SIDE) {
-    // both colours write their own columns of their faces' rows straight into H;
-    // the two shared quantities of a row (diagonal, g) meet in a per-row side
-    // slot: colour 0 parks them, colour 1 adds its own (same bits as the
-    // staged merge: h(colour 1) + h(colour 0))
-    unsigned lo = 0, hi = 0;
 #pragma unroll
     for (int x = 0; x < DIM; ++x) {
       const int cx = x == 0 ? cc[0] : (x == 1 ? cc[1] : cc[2]);
@@ -457,19 +457,42 @@ __global__ void __launch_bounds__(kCT, HDR_CELL_MINB) k_rt0_cell(HybArgs A, Rt0C
       lo |= static_cast<unsigned>(cx > 0) << x;
       hi |= static_cast<unsigned>(cx + 1 < Nx) << x;
     }
-    const uint64_t pol = PASS == 0 ? l2_policy_evict_last() : l2_policy_evict_first();
 #pragma unroll
     for (int k = 0; k < N; ++k) {
       const int a_ = k >> 1, side = k & 1;
       const int ca = a_ == 0 ? cc[0] : (a_ == 1 ? cc[1] : cc[2]);
       const int na = static_cast<int>(a_ == 0 ? A.m.N[0] : (a_ == 1 ? A.m.N[1] : A.m.N[2]));
       if (!(side ? (ca + 1 < na) : (ca > 0))) continue;
+      inmask |= 1u << k;
       const int face = face_id32(A.m, a_, cc[0] + (a_ == 0 ? side : 0), cc[1] + (a_ == 1 ? side : 0), cc[2] + (a_ == 2 ? side : 0));
-      const int row = A.mbase[face];
       const unsigned far = side ? static_cast<unsigned>(ca + 2 < na) : static_cast<unsigned>(ca >= 2);
       const unsigned flags = lo | (hi << DIM) | (far << (2 * DIM));
-      const uint64_t own = __ldg(A.rank_tab + ((static_cast<size_t>(k) << (2 * DIM + 1)) + flags) * 2);
-      double* out = A.hval + A.rowoff[row];
+      cp_async16(&pf_rs[k][tid], A.frs + face);
+      cp_async8(&pf_tab[k][tid], A.rank_tab + ((static_cast<size_t>(k) << (2 * DIM + 1)) + flags) * 2);
+      if (PASS == 1) cp_async16(&pf_sv[k][tid], stage + 2 * static_cast<int64_t>(face));
+    }
+  }
+  const double ib = 1.0 / b;
+  const double s = b / fma(a, c.lam, b);
+  double f[N];
+#pragma unroll
+  for (int j = 0; j < N; ++j) f[j] = A.f[static_cast<int64_t>(e) * N + j];
+  rt0_cell_correction<DIM, kCT>(A, c, a, b, s, ib, f, dsm, csm, tid);
+  auto hrow = [&](int k, double (&h)[NC]) { rt0_hrow<DIM, kCT>(c, s, ib, f, csm, tid, k, h); };
+  if (SIDE) {
+    // both colours write their own columns of their faces' rows straight into H;
+    // the two shared quantities of a row (diagonal, g) meet in a per-row side
+    // slot: colour 0 parks them, colour 1 adds its own (same bits as the
+    // staged merge: h(colour 1) + h(colour 0)); side slots indexed by face
+    const uint64_t pol = PASS == 0 ? l2_policy_evict_last() : l2_policy_evict_first();
+    cp_async_wait_all();
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+      if (!((inmask >> k) & 1u)) continue;
+      const longlong2 rs = pf_rs[k][tid];
+      const uint64_t own = pf_tab[k][tid];
+      const int row = static_cast<int>(rs.y);
+      double* out = A.hval + rs.x;
       double h[NC];
       hrow(k, h);
 #pragma unroll
@@ -478,13 +501,16 @@ __global__ void __launch_bounds__(kCT, HDR_CELL_MINB) k_rt0_cell(HybArgs A, Rt0C
         if (r == 15u || q == k) continue;
         st_l2hint(out + r, h[q], pol);
       }
-      double* sv = stage + 2 * static_cast<int64_t>(row);
       if (PASS == 0) {
+        const int a_ = k >> 1, side = k & 1;
+        const int face = face_id32(A.m, a_, cc[0] + (a_ == 0 ? side : 0), cc[1] + (a_ == 1 ? side : 0), cc[2] + (a_ == 2 ? side : 0));
+        double* sv = stage + 2 * static_cast<int64_t>(face);
         st_l2hint(sv, h[k], l2_policy_evict_last());
         st_l2hint(sv + 1, h[N], l2_policy_evict_last());
       } else {
-        out[(own >> (4 * k)) & 15u] = h[k] + sv[0];
-        A.g[row] = h[N] + sv[1];
+        const double2 sv = pf_sv[k][tid];
+        out[(own >> (4 * k)) & 15u] = h[k] + sv.x;
+        A.g[row] = h[N] + sv.y;
       }
     }
     return;
@@ -501,8 +527,7 @@ __global__ void __launch_bounds__(kCT, HDR_CELL_MINB) k_rt0_cell(HybArgs A, Rt0C
     }
     return;
   }
-  // pass 1: complete rows of this cell's interior faces
-  unsigned lo = 0, hi = 0;
+  // pass 1: complete rows of this cell's interior faces (lo, hi still 0: SIDE is false)
 #pragma unroll
   for (int x = 0; x < DIM; ++x) {
     const int cx = x == 0 ? cc[0] : (x == 1 ? cc[1] : cc[2]);
@@ -549,6 +574,258 @@ __global__ void __launch_bounds__(kCT, HDR_CELL_MINB) k_rt0_cell(HybArgs A, Rt0C
       st_l2hint(out + r, nrow[q], pol);
     }
     A.g[row] = h[N] + nrow[N];
+  }
+}
+
+// ------------------------------------------------------------------ k = 0, brick form (default)
+//
+// The thread-per-cell kernels above store each H entry as an isolated 8-byte
+// write; with HBM3e ECC every partially written 32-byte sector costs a DRAM
+// read-fill, and those fills, not the arithmetic, set their time (measured:
+// the same kernel without its H stores runs in half the time).  Here a CTA
+// owns a brick of BX x BY x BZ cells (one thread per cell, the element solve
+// of rt0_cell_correction) and assembles the H rows of the brick's faces in
+// shared memory.  The rows of the faces of one axis along one x-line of the
+// brick are consecutive in H (faces are numbered x-fastest, rows follow the
+// interior faces in face order), so each such line is one contiguous segment,
+// written out with coalesced full-sector stores, together with its g entries.
+// Faces on a brick boundary are shared with the neighbouring brick: bricks are
+// two-coloured (bx + by + bz parity, face-adjacent bricks differ); colour 0
+// parks its row of such a face in a face-indexed stage (structure of arrays,
+// coalesced) and colour 1 completes and writes it.  Every H row and g entry is
+// written once; the two contributions to a diagonal entry / g entry meet as
+// fl(h_minus + h_plus), the reference's two-term sum.
+template <int DIM>
+struct Brick;
+template <>
+struct Brick<3> {
+  static constexpr int X = 32, Y = 2, Z = 2;
+};
+template <>
+struct Brick<2> {
+  static constexpr int X = 32, Y = 4, Z = 1;
+};
+
+template <int DIM>
+struct BrickDims {
+  static constexpr int X = Brick<DIM>::X, Y = Brick<DIM>::Y, Z = Brick<DIM>::Z;
+  static constexpr int CT = X * Y * Z;
+  static constexpr int NL0 = Y * Z, NL1 = (Y + 1) * Z, NL2 = DIM == 3 ? Y * (Z + 1) : 0;
+  static constexpr int NL = NL0 + NL1 + NL2;  // x-lines of faces of each axis
+  static constexpr int RL = 4 * DIM - 1;      // longest H row
+  static constexpr int CAP = (X + 1) * RL;    // entries of one line segment
+  static constexpr size_t smem_bytes() { return static_cast<size_t>(NL) * (CAP + X + 1) * sizeof(double); }
+};
+
+// interior faces of a cell (its row-length contribution)
+template <int DIM>
+__device__ __forceinline__ int interior_faces(const DevMesh& m, int x, int y, int z) {
+  int n = (x > 0) + (x + 1 < static_cast<int>(m.N[0])) + (y > 0) + (y + 1 < static_cast<int>(m.N[1]));
+  if (DIM == 3) n += (z > 0) + (z + 1 < static_cast<int>(m.N[2]));
+  return n;
+}
+
+template <int DIM, int COL>
+__global__ void __launch_bounds__(BrickDims<DIM>::CT) k_rt0_brick(HybArgs A, Rt0Const<2 * DIM> c, double* stage,
+                                                                  int nbx, int nby, int nbz) {
+  using B = BrickDims<DIM>;
+  constexpr int N = 2 * DIM;
+  constexpr int NC = N + 1;
+  constexpr int X = B::X, Y = B::Y, Z = B::Z, CT = B::CT, NL = B::NL, CAP = B::CAP;
+  static_assert(N * N * CT * sizeof(float) <= NL * CAP * sizeof(double), "Delta32 aliases the line buffers");
+  __shared__ float csm[N * NC][CT];
+  extern __shared__ double bsm[];
+  double* hbuf = bsm;              // NL x CAP: H line segments
+  double* gbuf = bsm + NL * CAP;   // NL x (X + 1): g of the line's faces
+  float(*dsm)[CT] = reinterpret_cast<float(*)[CT]>(bsm);  // Delta32: dead before the segments are filled
+  __shared__ long long l_base[NL];  // H offset of the line's first row
+  __shared__ int l_row0[NL], l_pa[NL], l_oa[NL], l_ob[NL], l_olo[NL], l_ohi[NL];
+  const DevMesh& m = A.m;
+  const int N0 = static_cast<int>(m.N[0]), N1 = static_cast<int>(m.N[1]), N2 = DIM == 3 ? static_cast<int>(m.N[2]) : 1;
+  // this colour's bricks: x index alternates within a (by, bz) row
+  const int nbxh = (nbx + 1) >> 1;
+  const int row_ = blockIdx.x / nbxh;
+  const int by = row_ % nby, bz = row_ / nby;
+  const int bx = 2 * (blockIdx.x - row_ * nbxh) + ((by + bz + COL) & 1);
+  if (bx >= nbx || bz >= nbz) return;
+  const int x0 = bx * X, y0 = by * Y, z0 = bz * Z;
+  const int ex = min(X, N0 - x0), ey = min(Y, N1 - y0), ez = DIM == 3 ? min(Z, N2 - z0) : 1;
+  const int tid = threadIdx.x;
+  // face p of line (ax, jj, kk): x = x0 + p, y = y0 + jj, z = z0 + kk (ax 1: jj in [0, ey], ax 2: kk in [0, ez])
+  auto line_face = [&](int ax, int jj, int kk, int p) { return face_id32(m, ax, x0 + p, y0 + jj, z0 + kk); };
+  if (tid < NL) {  // line metadata
+    int ax, jj, kk;
+    if (tid < B::NL0) {
+      ax = 0, jj = tid % Y, kk = tid / Y;
+    } else if (tid < B::NL0 + B::NL1) {
+      const int u = tid - B::NL0;
+      ax = 1, jj = u % (Y + 1), kk = u / (Y + 1);
+    } else {
+      const int u = tid - B::NL0 - B::NL1;
+      ax = 2, jj = u % Y, kk = u / Y;
+    }
+    int pa = 0, pb = -1, oa = 0, ob = -1;
+    if (ax == 0) {
+      if (jj < ey && kk < ez) {
+        pa = x0 == 0 ? 1 : 0;
+        pb = x0 + ex == N0 ? ex - 1 : ex;
+        oa = COL == 1 ? pa : 1;
+        ob = COL == 1 ? pb : ex - 1;
+      }
+    } else if (ax == 1) {
+      const int j = y0 + jj;
+      if (jj <= ey && kk < ez && j > 0 && j < N1) {
+        pa = 0, pb = ex - 1;
+        const bool edge = jj == 0 || jj == ey;
+        oa = pa, ob = (COL == 0 && edge) ? -1 : pb;
+      }
+    } else {
+      const int k = z0 + kk;
+      if (jj < ey && kk <= ez && k > 0 && k < N2) {
+        pa = 0, pb = ex - 1;
+        const bool edge = kk == 0 || kk == ez;
+        oa = pa, ob = (COL == 0 && edge) ? -1 : pb;
+      }
+    }
+    long long base = 0, lo_ = 0, hi_ = 0;
+    int row0 = 0;
+    if (pb >= pa) {
+      const longlong2 fa = A.frs[line_face(ax, jj, kk, pa)];
+      base = fa.x;
+      row0 = static_cast<int>(fa.y);
+      if (ob >= oa) {
+        const longlong2 fo = A.frs[line_face(ax, jj, kk, oa)];
+        const longlong2 fb = A.frs[line_face(ax, jj, kk, ob)];
+        // length of the last owned row: interior faces of its two cells - 1
+        const int bxp = x0 + ob, byp = y0 + jj, bzp = z0 + kk;  // the plus cell of face ob
+        int len;
+        if (ax == 0)
+          len = interior_faces<DIM>(m, bxp - 1, byp, bzp) + interior_faces<DIM>(m, bxp, byp, bzp) - 1;
+        else if (ax == 1)
+          len = interior_faces<DIM>(m, bxp, byp - 1, bzp) + interior_faces<DIM>(m, bxp, byp, bzp) - 1;
+        else
+          len = interior_faces<DIM>(m, bxp, byp, bzp - 1) + interior_faces<DIM>(m, bxp, byp, bzp) - 1;
+        lo_ = fo.x - base;
+        hi_ = fb.x + len - base;
+      }
+    }
+    l_base[tid] = base;
+    l_row0[tid] = row0;
+    l_pa[tid] = pa;
+    l_oa[tid] = oa;
+    l_ob[tid] = ob;
+    l_olo[tid] = static_cast<int>(lo_);
+    l_ohi[tid] = static_cast<int>(hi_);
+  }
+  // the cell
+  const int lx = tid % X, ly = (tid / X) % Y, lz = tid / (X * Y);
+  const int cc[3] = {x0 + lx, y0 + ly, z0 + lz};
+  const bool valid = lx < ex && ly < ey && lz < ez;
+  double a = 1.0, b = 1.0, s = 1.0, ib = 1.0;
+  double f[N];
+#pragma unroll
+  for (int j = 0; j < N; ++j) f[j] = 0.0;
+  if (valid) {
+    const int64_t e = cc[0] + static_cast<int64_t>(N0) * (cc[1] + static_cast<int64_t>(N1) * cc[2]);
+    a = A.alpha[e];
+    b = A.beta[e];
+#pragma unroll
+    for (int j = 0; j < N; ++j) f[j] = A.f[e * N + j];
+    ib = 1.0 / b;
+    s = b / fma(a, c.lam, b);
+    rt0_cell_correction<DIM, CT>(A, c, a, b, s, ib, f, dsm, csm, tid);
+  }
+  __syncthreads();  // line metadata
+  unsigned lo = 0, hi = 0;
+#pragma unroll
+  for (int x = 0; x < DIM; ++x) {
+    const int Nx = x == 0 ? N0 : (x == 1 ? N1 : N2);
+    lo |= static_cast<unsigned>(cc[x] > 0) << x;
+    hi |= static_cast<unsigned>(cc[x] + 1 < Nx) << x;
+  }
+  const int lc[3] = {lx, ly, lz}, ec[3] = {ex, ey, ez};
+  const int64_t nfaces = m.nfaces;
+  // pass 1: own columns; the first contribution of diagonals / g (minus cell, or
+  // the completed value on a colour-1 brick boundary); colour 0 parks boundary rows
+  if (valid) {
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+      const int ax = k >> 1, side = k & 1;
+      const int ca = cc[ax], na = ax == 0 ? N0 : (ax == 1 ? N1 : N2);
+      if (!(side ? (ca + 1 < na) : (ca > 0))) continue;
+      const int face = face_id32(m, ax, cc[0] + (ax == 0 ? side : 0), cc[1] + (ax == 1 ? side : 0), cc[2] + (ax == 2 ? side : 0));
+      const bool bb = side ? lc[ax] == ec[ax] - 1 : lc[ax] == 0;  // neighbour in the adjacent brick
+      double h[NC];
+      rt0_hrow<DIM, CT>(c, s, ib, f, csm, tid, k, h);
+      if (COL == 0 && bb) {
+#pragma unroll
+        for (int q = 0; q <= N; ++q) stage[q * nfaces + face] = h[q];
+        continue;
+      }
+      const int l = ax == 0 ? ly + Y * lz : (ax == 1 ? B::NL0 + (ly + side) + (Y + 1) * lz : B::NL0 + B::NL1 + ly + Y * (lz + side));
+      const int p = ax == 0 ? lx + side : lx;
+      const unsigned far = side ? static_cast<unsigned>(ca + 2 < na) : static_cast<unsigned>(ca >= 2);
+      const unsigned flags = lo | (hi << DIM) | (far << (2 * DIM));
+      const uint64_t* tab = A.rank_tab + ((static_cast<size_t>(k) << (2 * DIM + 1)) + flags) * 2;
+      const uint64_t own = __ldg(tab);
+      double* rowp = hbuf + l * CAP + (A.frs[face].x - l_base[l]);
+#pragma unroll
+      for (int q = 0; q < N; ++q) {
+        const unsigned r = static_cast<unsigned>(own >> (4 * q)) & 15u;
+        if (r == 15u || q == k) continue;
+        rowp[r] = h[q];
+      }
+      const unsigned rd = static_cast<unsigned>(own >> (4 * k)) & 15u;
+      if (bb) {  // colour 1: the neighbour's parked row (its slot k ^ 1)
+        const uint64_t nbr = __ldg(tab + 1);
+        double nv[NC];
+#pragma unroll
+        for (int q = 0; q <= N; ++q) nv[q] = stage[q * nfaces + face];
+#pragma unroll
+        for (int q = 0; q < N; ++q) {
+          const unsigned r = static_cast<unsigned>(nbr >> (4 * q)) & 15u;
+          if (r != 15u) rowp[r] = nv[q];
+        }
+        rowp[rd] = side ? h[k] + nv[k ^ 1] : nv[k ^ 1] + h[k];
+        gbuf[l * (X + 1) + p] = side ? h[N] + nv[N] : nv[N] + h[N];
+      } else if (side) {  // this cell is the face's minus cell
+        rowp[rd] = h[k];
+        gbuf[l * (X + 1) + p] = h[N];
+      }
+    }
+  }
+  __syncthreads();
+  // pass 2: the plus cell adds its diagonal / g contribution to brick-interior faces
+  if (valid) {
+#pragma unroll
+    for (int ax = 0; ax < DIM; ++ax) {
+      const int k = 2 * ax;  // low face of the cell
+      if (!(cc[ax] > 0) || lc[ax] == 0) continue;
+      const int face = face_id32(m, ax, cc[0], cc[1], cc[2]);
+      const int l = ax == 0 ? ly + Y * lz : (ax == 1 ? B::NL0 + ly + (Y + 1) * lz : B::NL0 + B::NL1 + ly + Y * lz);
+      const int p = lx;
+      const unsigned far = static_cast<unsigned>(cc[ax] >= 2);
+      const unsigned flags = lo | (hi << DIM) | (far << (2 * DIM));
+      const uint64_t own = __ldg(A.rank_tab + ((static_cast<size_t>(k) << (2 * DIM + 1)) + flags) * 2);
+      const unsigned rd = static_cast<unsigned>(own >> (4 * k)) & 15u;
+      double h[NC];
+      rt0_hrow<DIM, CT>(c, s, ib, f, csm, tid, k, h);
+      double* dp = hbuf + l * CAP + (A.frs[face].x - l_base[l]) + rd;
+      *dp = *dp + h[k];
+      gbuf[l * (X + 1) + p] = gbuf[l * (X + 1) + p] + h[N];
+    }
+  }
+  __syncthreads();
+  // write-out: one warp per line segment, coalesced
+  const int lane = tid & 31, warp = tid >> 5;
+  const uint64_t pol = l2_policy_evict_first();
+  for (int l = warp; l < NL; l += CT / 32) {
+    const int lo_ = l_olo[l], hi_ = l_ohi[l];
+    double* dst = A.hval + l_base[l];
+    const double* src = hbuf + l * CAP;
+    for (int i = lo_ + lane; i < hi_; i += 32) st_l2hint(dst + i, src[i], pol);
+    const int pa = l_pa[l], oa = l_oa[l], ob = l_ob[l];
+    for (int p = oa + lane; p <= ob; p += 32) A.g[l_row0[l] + (p - pa)] = gbuf[l * (X + 1) + p];
   }
 }
 
@@ -972,11 +1249,28 @@ void launch_hybridize_rt0_rows(const HybArgs& a, const double* hc, double* stage
     c.rho = hc[5 * N * N + N + 1];
   };
   static const bool rows = getenv("HDR_RT0_ROWS") != nullptr;  // lane-per-row variant (A/B timing)
+  // thread-per-cell scattered-store variant: forced, or for meshes too small to
+  // give each SM a few bricks per colour (e.g. 64 x 64 quads: 16 bricks a colour)
+  const bool cell = getenv("HDR_RT0_CELL") != nullptr || a.m.ncells < 148 * 128 * 4;
   static const bool side = getenv("HDR_RT0_STAGE") == nullptr;  // default: per-row side slots; HDR_RT0_STAGE=1: row stage
+  auto brick = [&](auto dimc, auto& c) {
+    constexpr int D = decltype(dimc)::value;
+    using B = BrickDims<D>;
+    const int nbx = static_cast<int>((a.m.N[0] + B::X - 1) / B::X), nby = static_cast<int>((a.m.N[1] + B::Y - 1) / B::Y);
+    const int nbz = D == 3 ? static_cast<int>((a.m.N[2] + B::Z - 1) / B::Z) : 1;
+    const unsigned grid = static_cast<unsigned>(((nbx + 1) / 2) * nby * nbz);
+    const size_t smem = B::smem_bytes();
+    cudaFuncSetAttribute(k_rt0_brick<D, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    cudaFuncSetAttribute(k_rt0_brick<D, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    k_rt0_brick<D, 0><<<grid, B::CT, smem, st>>>(a, c, stage, nbx, nby, nbz);
+    k_rt0_brick<D, 1><<<grid, B::CT, smem, st>>>(a, c, stage, nbx, nby, nbz);
+  };
   if (a.m.dim == 3) {
     Rt0Const<6> c;
     fill(c, 6);
-    if (rows) {
+    if (!rows && !cell) {
+      brick(std::integral_constant<int, 3>{}, c);
+    } else if (rows) {
       const unsigned nb = static_cast<unsigned>((cnt + 4 * 5 - 1) / (4 * 5));
       k_rt0_rows<3, 0><<<nb, 128, 0, st>>>(a, c, stage);
       k_rt0_rows<3, 1><<<nb, 128, 0, st>>>(a, c, stage);
@@ -992,7 +1286,9 @@ void launch_hybridize_rt0_rows(const HybArgs& a, const double* hc, double* stage
   } else {
     Rt0Const<4> c;
     fill(c, 4);
-    if (rows) {
+    if (!rows && !cell) {
+      brick(std::integral_constant<int, 2>{}, c);
+    } else if (rows) {
       const unsigned nb = static_cast<unsigned>((cnt + 4 * 8 - 1) / (4 * 8));
       k_rt0_rows<2, 0><<<nb, 128, 0, st>>>(a, c, stage);
       k_rt0_rows<2, 1><<<nb, 128, 0, st>>>(a, c, stage);

@@ -110,7 +110,22 @@ __global__ void k_fill_patterns(DevMesh m, const int* mbase, const int64_t* fbas
   }
 }
 
+// k = 0 scatter metadata: per face {start of its H row, row} in one 16-byte word
+// (row = -1 and start = 0 on the boundary), so the hybridize kernel reaches a
+// row with one load instead of the mbase -> rowoff chain
+__global__ void k_face_rows(int64_t nfaces, const int* mbase, const int64_t* rowoff, longlong2* frs) {
+  const int64_t f = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (f >= nfaces) return;
+  const int mb = mbase[f];
+  frs[f] = make_longlong2(mb >= 0 ? rowoff[mb] : 0, mb);
+}
+
 }  // namespace
+
+void launch_face_rows(int64_t nfaces, const int* mbase, const int64_t* rowoff, longlong2* frs, cudaStream_t st) {
+  k_face_rows<<<static_cast<unsigned>((nfaces + 255) / 256), 256, 0, st>>>(nfaces, mbase, rowoff, frs);
+  count_launch();
+}
 
 void launch_face_counts(const DevMesh& m, int* flag, int64_t* fnnz_h, int64_t* fnnz_s, cudaStream_t st) {
   const int64_t nb = (m.nfaces + 255) / 256;

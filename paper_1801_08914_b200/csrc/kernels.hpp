@@ -41,7 +41,9 @@ struct HybArgs {
   double* g;     // reduced rhs (m)
   int* status;   // device flag: bit 0 = Neumann ratio out of range
   const uint64_t* rank_tab;  // k = 0 row-rank table (rank_table_rt0)
+  const longlong2* frs;      // k = 0: per face {rowoff[mbase[face]], mbase[face]} (launch_face_rows)
 };
+void launch_face_rows(int64_t nfaces, const int* mbase, const int64_t* rowoff, longlong2* frs, cudaStream_t st);
 
 // Row-rank table of the k = 0 kernel: for row slot k and boundary flags
 // (own lo bits | own hi bits << dim | neighbour far face << 2 dim), two words of
