@@ -1251,7 +1251,8 @@ void launch_hybridize_rt0_rows(const HybArgs& a, const double* hc, double* stage
   static const bool rows = getenv("HDR_RT0_ROWS") != nullptr;  // lane-per-row variant (A/B timing)
   // thread-per-cell scattered-store variant: forced, or for meshes too small to
   // give each SM a few bricks per colour (e.g. 64 x 64 quads: 16 bricks a colour)
-  const bool cell = getenv("HDR_RT0_CELL") != nullptr || a.m.ncells < 148 * 128 * 4;
+  // (HDR_RT0_BRICK forces the brick kernel at any size: tests)
+  const bool cell = getenv("HDR_RT0_CELL") != nullptr || (a.m.ncells < 148 * 128 * 4 && !getenv("HDR_RT0_BRICK"));
   static const bool side = getenv("HDR_RT0_STAGE") == nullptr;  // default: per-row side slots; HDR_RT0_STAGE=1: row stage
   auto brick = [&](auto dimc, auto& c) {
     constexpr int D = decltype(dimc)::value;

@@ -101,6 +101,30 @@ def test_hybridize_moderate_meshes_vs_dd(dim, cells, k, coef):
     assert rel_err(gv, o.get("g_dd")) <= TOL
 
 
+@pytest.mark.parametrize("dim,cells,coef", [
+    (3, (8, 8, 8), "logu:1e-2:1e2"), (3, (37, 5, 7), "logu:1e-3:1e3"), (3, (70, 3, 2), "checker:1e-2:1e2"),
+    (3, (1, 1, 9), "logu:1e-2:1e2"), (2, (64, 64), "uniform:1:1"), (2, (75, 9), "logu:1e-2:1e2"), (2, (1, 13), "logu:1e-2:1e2"),
+])
+def test_rt0_brick_kernel_matches_cell_kernel_bitwise(dim, cells, coef, monkeypatch):
+    """The k = 0 brick kernel (shared-memory line segments, coalesced stores,
+    staged brick-boundary faces) against the thread-per-cell kernel: the same
+    element arithmetic and the same two-term sums, so identical bits, on meshes
+    with partial bricks in every direction; plus the DD oracle."""
+    o = Oracle(dim, cells, 0)
+    o.gen_inputs(coef, 77)
+    a, b, f = o.get("alpha"), o.get("beta"), o.get("f_hat")
+    sp = hd.Space(dim, cells, 0)
+    monkeypatch.setenv("HDR_RT0_BRICK", "1")
+    hb = sp.hybridize(a, b, f).values()
+    monkeypatch.delenv("HDR_RT0_BRICK")
+    monkeypatch.setenv("HDR_RT0_CELL", "1")
+    hc = sp.hybridize(a, b, f).values()
+    assert np.array_equal(hb[0], hc[0]) and np.array_equal(hb[1], hc[1])
+    o.run("port_hybridize")
+    o.run("dd_hybridize")
+    assert rel_err(hb[0], o.get("H.values_dd")) <= TOL and rel_err(hb[1], o.get("g_dd")) <= TOL
+
+
 def test_deterministic_and_device_inputs():
     import torch
 
