@@ -314,6 +314,7 @@ hdr_status hdr_space_create(int dim, const int64_t cells[3], const double h[3], 
     if (order == 0) {  // constant block for the register kernel: D, M, E, Ma, N0, X, lam, rho
       sp->rt0_consts.assign(pack.begin(), pack.begin() + 5 * nn + n + 1);
       sp->rt0_consts.push_back(sp->st.rho);
+      sp->rt0_consts.insert(sp->rt0_consts.end(), sp->st.Minv.begin(), sp->st.Minv.end());  // for Rt0Fast
       const std::vector<uint64_t> tab = rank_table_rt0(dim);
       sp->rank_tab.alloc(tab.size());
       CK(cudaMemcpyAsync(sp->rank_tab.p, tab.data(), tab.size() * 8, cudaMemcpyHostToDevice, st));

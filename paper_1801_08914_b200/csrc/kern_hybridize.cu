@@ -21,6 +21,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <type_traits>
+#include <vector>
 #include <cstdlib>
 #include <cstring>
 
@@ -305,136 +306,214 @@ constexpr int kCT = HDR_CELL_CT;
 #define HDR_CELL_MINB 1
 #endif
 
-// correction C (N x (N+1), row-major) of one cell into csm[.][tid]
-template <int DIM, int CT>
-__device__ __forceinline__ void rt0_cell_correction(const HybArgs& A, const Rt0Const<2 * DIM>& c, double a, double b,
-                                                    double s, double ib, const double (&f)[2 * DIM],
-                                                    float (*dsm)[CT], float (*csm)[CT], int tid) {
+// ------------------------------------------------------------------ k = 0, structured first-order correction
+//
+// V = A0^-1 = (N0 + s X X^T) / beta = W / beta, W = M^-1 + t X X^T (t = s - 1),
+// with M^-1 block-diagonal (2 x 2 per axis: RT0 basis functions of different
+// axes are orthogonal) and Delta = alpha E + beta Ma + delta, so the first-order
+// correction splits as
+//   C = V Delta V = [ alpha (P0 + t P1 + t^2 P2) + beta (Q0 + t Q1 + t^2 Q2)
+//                     + W delta W ] / beta^2
+// with P. / Q. the constant t-polynomial coefficients of W E W
+// (resp. Ma), precomputed on the host, and only the per-cell rounding errors
+// delta (symmetric, exact error-free transforms) multiplied per cell.  C is
+// symmetric (21 entries in 3D), lives in registers, and C_w = C f.  About 380
+// fp32 FMAs per cell instead of 504, no shared-memory Delta / correction
+// columns.  Cells whose order control asks for P > 1 (rare) run the general
+// Neumann loop (rt0_general_correction) in shared-memory scratch.
+template <int N>
+struct Rt0Fast {
+  static constexpr int NS = N * (N + 1) / 2;
+  float n0[N][2];            // M^-1 row k on its axis pair (k & ~1, k | 1)
+  float x[N];                // X (rank-one direction of the divergence)
+  float p[3][NS], q[3][NS];  // s-polynomial coefficients (E part, Ma part), symmetric packed
+};
+
+__host__ __device__ constexpr int sym_idx(int k, int l, int n) {
+  return k <= l ? k * n - k * (k - 1) / 2 + (l - k) : l * n - l * (l - 1) / 2 + (k - l);
+}
+
+// returns max |C| (q < N); hm = max |V| (the order control's reference size)
+template <int DIM>
+__device__ __forceinline__ float rt0_fast_correction(const Rt0Const<2 * DIM>& c, const Rt0Fast<2 * DIM>& F, double a,
+                                                     double b, double s, double ib,
+                                                     float (&C)[Rt0Fast<2 * DIM>::NS], float& hm) {
   constexpr int N = 2 * DIM;
-  constexpr int NC = N + 1;
-  float v32[N][NC];
+  constexpr int NS = Rt0Fast<N>::NS;
+  float dl[NS];  // delta: the exact rounding error of the reference's combine
+#pragma unroll
+  for (int k = 0; k < N; ++k)
+#pragma unroll
+    for (int l = k; l < N; ++l) {
+      double p1, e1;
+      two_prod(a, c.D[k * N + l], p1, e1);
+      if ((k >> 1) == (l >> 1)) {
+        double p2, e2, s_, e3;
+        two_prod(b, c.M[k * N + l], p2, e2);
+        two_sum(p1, p2, s_, e3);
+        dl[sym_idx(k, l, N)] = static_cast<float>(-((e1 + e2) + e3));
+      } else {
+        dl[sym_idx(k, l, N)] = static_cast<float>(-e1);  // M_kl = 0: A_kl = fl(alpha D_kl)
+      }
+    }
+  float u[N], nu[N], gam = 0.f;
 #pragma unroll
   for (int k = 0; k < N; ++k) {
-    const double xs = c.X[k] * s;
-    double wk = 0.0;
+    float acc = 0.f;
 #pragma unroll
-    for (int j = 0; j < N; ++j) {
-      const double vk = fma(xs, c.X[j], c.N0[k * N + j]) * ib;
-      v32[k][j] = static_cast<float>(vk);
-      wk = fma(vk, f[j], wk);
-    }
-    v32[k][N] = static_cast<float>(wk);
+    for (int l = 0; l < N; ++l) acc = fmaf(dl[sym_idx(k, l, N)], F.x[l], acc);
+    u[k] = acc;
+    gam = fmaf(F.x[k], acc, gam);
   }
 #pragma unroll
   for (int k = 0; k < N; ++k) {
     const int k0 = k & ~1;
+    nu[k] = fmaf(F.n0[k][0], u[k0], F.n0[k][1] * u[k0 + 1]);
+  }
+  // W = N0 + s XX^T = M^-1 + (s - 1) XX^T: F.n0 holds the block-diagonal M^-1
+  const float sf = static_cast<float>(s - 1.0), af = static_cast<float>(a), bf = static_cast<float>(b);
+  const float ibf = static_cast<float>(ib), ib2 = static_cast<float>(ib * ib);
+  const float s2g = sf * sf * gam;
+  float cm = 0.f;
+  hm = 0.f;
 #pragma unroll
-    for (int j = 0; j < 2; ++j) {  // same axis: M_kl != 0
-      const int l = k0 + j;
-      dsm[k * N + l][tid] = static_cast<float>(delta_entry(a, b, c.D[k * N + l], c.M[k * N + l], c.E[k * N + l], c.Ma[k * N + l]));
+  for (int k = 0; k < N; ++k)
+#pragma unroll
+    for (int l = k; l < N; ++l) {
+      const int i = sym_idx(k, l, N);
+      // (N0 delta N0)_kl: N0 couples only the axis pairs of k and l
+      const int k0 = k & ~1, l0 = l & ~1;
+      float Bkl = F.n0[k][0] * F.n0[l][0] * dl[sym_idx(k0, l0, N)];
+      Bkl = fmaf(F.n0[k][0] * F.n0[l][1], dl[sym_idx(k0, l0 + 1, N)], Bkl);
+      Bkl = fmaf(F.n0[k][1] * F.n0[l][0], dl[sym_idx(k0 + 1, l0, N)], Bkl);
+      Bkl = fmaf(F.n0[k][1] * F.n0[l][1], dl[sym_idx(k0 + 1, l0 + 1, N)], Bkl);
+      float R = fmaf(sf, fmaf(nu[k], F.x[l], F.x[k] * nu[l]), Bkl);
+      R = fmaf(s2g * F.x[k], F.x[l], R);
+      const float Pm = fmaf(fmaf(F.p[2][i], sf, F.p[1][i]), sf, F.p[0][i]);
+      const float Qm = fmaf(fmaf(F.q[2][i], sf, F.q[1][i]), sf, F.q[0][i]);
+      const float v = fmaf(af, Pm, fmaf(bf, Qm, R)) * ib2;
+      C[i] = v;
+      cm = fmaxf(cm, fabsf(v));
+      const float n0kl = (k >> 1) == (l >> 1) ? F.n0[k][l & 1] : 0.f;
+      hm = fmaxf(hm, fabsf(fmaf(sf * F.x[k], F.x[l], n0kl) * ibf));
     }
+  return cm;
+}
+
+// general Neumann correction through order P (the rare cells the order control
+// sends here): Delta and V (fp32, full) in per-thread shared-memory scratch
+// columns (stride = threads of the block), C (symmetric) written back there
+template <int DIM>
+__device__ __noinline__ void rt0_general_correction(const double* Dg, const double* Mg, const double* Eg,
+                                                    const double* Mag, const double* N0g, const double* Xg, double a,
+                                                    double b, double s, double ib, int P, float* scr, int stride) {
+  constexpr int N = 2 * DIM;
+  struct {
+    const double *D, *M, *E, *Ma, *N0, *X;
+  } c{Dg, Mg, Eg, Mag, N0g, Xg};
+  float* dm = scr;
+  float* vm = scr + N * N * stride;
+  float* cw = scr + 2 * N * N * stride;
+#pragma unroll 1
+  for (int k = 0; k < N; ++k) {
+    const double xs = c.X[k] * s;
 #pragma unroll
-    for (int j = 0; j < N - 2; ++j) {  // other axes: M_kl = Ma_kl = 0 exactly
-      int l = k0 + 2 + j;
-      l = l >= N ? l - N : l;
-      const double d = c.D[k * N + l];
-      const double p1 = __dmul_rn(a, d);
-      const double e1 = __fma_rn(a, d, -p1);
-      dsm[k * N + l][tid] = static_cast<float>(__fma_rn(a, c.E[k * N + l], -e1));
+    for (int l = 0; l < N; ++l) {
+      vm[(k * N + l) * stride] = static_cast<float>(fma(xs, c.X[l], c.N0[k * N + l]) * ib);
+      double d;
+      if ((k >> 1) == (l >> 1)) {
+        d = delta_entry(a, b, c.D[k * N + l], c.M[k * N + l], c.E[k * N + l], c.Ma[k * N + l]);
+      } else {
+        const double p1 = __dmul_rn(a, c.D[k * N + l]);
+        const double e1 = __fma_rn(a, c.D[k * N + l], -p1);
+        d = __fma_rn(a, c.E[k * N + l], -e1);
+      }
+      dm[(k * N + l) * stride] = static_cast<float>(d);
     }
   }
-  // first order, column by column: y = Delta32 v_:q, t = V32 y
-  float cm = 0.f, hm = 0.f;
-#pragma unroll
-  for (int q = 0; q <= N; ++q) {
-    float y[N];
+#pragma unroll 1
+  for (int q = 0; q < N; ++q) {
+    float t[N], acc[N];
 #pragma unroll
     for (int k = 0; k < N; ++k) {
-      float acc = 0.f;
-#pragma unroll
-      for (int l = 0; l < N; ++l) acc = fmaf(dsm[k * N + l][tid], v32[l][q], acc);
-      y[k] = acc;
+      t[k] = vm[(k * N + q) * stride];
+      acc[k] = 0.f;
     }
+#pragma unroll 1
+    for (int p = 1; p <= P; ++p) {
+      float y[N];
 #pragma unroll
-    for (int k = 0; k < N; ++k) {
-      float acc = 0.f;
+      for (int k = 0; k < N; ++k) {
+        float v = 0.f;
 #pragma unroll
-      for (int j = 0; j < N; ++j) acc = fmaf(v32[k][j], y[j], acc);
-      const float cv = fmaf(1.f, acc, 0.f);
-      csm[k * NC + q][tid] = cv;
-      if (q < N) {
-        cm = fmaxf(cm, fabsf(cv));
-        hm = fmaxf(hm, fabsf(v32[k][q]));
+        for (int l = 0; l < N; ++l) v = fmaf(dm[(k * N + l) * stride], t[l], v);
+        y[k] = v;
+      }
+      const float sg = (p & 1) ? 1.f : -1.f;
+#pragma unroll
+      for (int k = 0; k < N; ++k) {
+        float v = 0.f;
+#pragma unroll
+        for (int j = 0; j < N; ++j) v = fmaf(vm[(k * N + j) * stride], y[j], v);
+        t[k] = v;
+        acc[k] = fmaf(sg, v, acc[k]);
       }
     }
-  }
-  // a-posteriori order control (as the lane-per-row kernel, per cell)
-  const double ratio = hm > 0.f ? static_cast<double>(cm) / hm : 0.0;
-  int P = 1;
-  {
-    double tt = ratio * ratio * 10.0;
-    while (tt > 1e-12 && P < A.p_max) {
-      ++P;
-      tt *= ratio;
-    }
-    if (!(ratio < 0.25)) atomicOr(A.status, 1);
-  }
-  if (P > 1) {  // rare: continue each column through the higher orders
-    for (int q = 0; q <= N; ++q) {
-      float tcol[N];
 #pragma unroll
-      for (int k = 0; k < N; ++k) tcol[k] = v32[k][q];
-      for (int p = 1; p <= P; ++p) {
-        float y[N], tn[N];
-#pragma unroll
-        for (int k = 0; k < N; ++k) {
-          float acc = 0.f;
-#pragma unroll
-          for (int l = 0; l < N; ++l) acc = fmaf(dsm[k * N + l][tid], tcol[l], acc);
-          y[k] = acc;
-        }
-#pragma unroll
-        for (int k = 0; k < N; ++k) {
-          float acc = 0.f;
-#pragma unroll
-          for (int j = 0; j < N; ++j) acc = fmaf(v32[k][j], y[j], acc);
-          tn[k] = acc;
-        }
-        if (p >= 2) {
-          const float sg = (p & 1) ? 1.f : -1.f;
-#pragma unroll
-          for (int k = 0; k < N; ++k) csm[k * NC + q][tid] = fmaf(sg, tn[k], csm[k * NC + q][tid]);
-        }
-#pragma unroll
-        for (int k = 0; k < N; ++k) tcol[k] = tn[k];
-      }
-    }
+    for (int k = 0; k < N; ++k)
+      if (k <= q) cw[sym_idx(k, q, N) * stride] = acc[k];
   }
 }
 
-// row k of [H_T | g_T]: [V | w]_k,: (fp64, recomputed exactly) - C_k,:
-template <int DIM, int CT>
-__device__ __forceinline__ void rt0_hrow(const Rt0Const<2 * DIM>& c, double s, double ib, const double (&f)[2 * DIM],
-                                         const float (*csm)[CT], int tid, int k, double (&h)[2 * DIM + 1]) {
+// the cell's correction C (registers): structured first order, general loop if needed
+template <int DIM>
+__device__ __forceinline__ void rt0_correction(const HybArgs& A, const Rt0Const<2 * DIM>& c, const Rt0Fast<2 * DIM>& F,
+                                               double a, double b, double s, double ib, float* scr, int stride,
+                                               float (&C)[Rt0Fast<2 * DIM>::NS]) {
   constexpr int N = 2 * DIM;
-  constexpr int NC = N + 1;
+  float hm;
+  const float cm = rt0_fast_correction<DIM>(c, F, a, b, s, ib, C, hm);
+  // a-posteriori order control (as the other k = 0 kernels)
+  const double ratio = hm > 0.f ? static_cast<double>(cm) / hm : 0.0;
+  int P = 1;
+  double tt = ratio * ratio * 10.0;
+  while (tt > 1e-12 && P < A.p_max) {
+    ++P;
+    tt *= ratio;
+  }
+  if (!(ratio < 0.25)) atomicOr(A.status, 1);
+  if (P > 1) {
+    rt0_general_correction<DIM>(A.fx.D, A.fx.M, A.fx.E, A.fx.Ma, A.fx.N0, A.fx.X, a, b, s, ib, P, scr, stride);
+#pragma unroll
+    for (int i = 0; i < Rt0Fast<N>::NS; ++i) C[i] = scr[(2 * N * N + i) * stride];
+  }
+}
+
+// row k of [H_T | g_T] = [V | w]_k,: (fp64) - [C | C f]_k,:
+template <int DIM>
+__device__ __forceinline__ void rt0_hrow_c(const Rt0Const<2 * DIM>& c, double s, double ib, const double (&f)[2 * DIM],
+                                           const float (&C)[Rt0Fast<2 * DIM>::NS], int k, double (&h)[2 * DIM + 1]) {
+  constexpr int N = 2 * DIM;
   const double xs = c.X[k] * s;
   double wk = 0.0;
+  float cw = 0.f;
 #pragma unroll
   for (int j = 0; j < N; ++j) {
     const double vk = fma(xs, c.X[j], c.N0[k * N + j]) * ib;
     wk = fma(vk, f[j], wk);
-    h[j] = vk - static_cast<double>(csm[k * NC + j][tid]);
+    const float ckj = C[sym_idx(k, j, N)];
+    h[j] = vk - static_cast<double>(ckj);
+    cw = fmaf(ckj, static_cast<float>(f[j]), cw);
   }
-  h[N] = wk - static_cast<double>(csm[k * NC + N][tid]);
+  h[N] = wk - static_cast<double>(cw);
 }
 
 template <int DIM, int PASS, bool SIDE>
-__global__ void __launch_bounds__(kCT, HDR_CELL_MINB) k_rt0_cell(HybArgs A, Rt0Const<2 * DIM> c, double* stage) {
+__global__ void __launch_bounds__(kCT, HDR_CELL_MINB) k_rt0_cell(HybArgs A, Rt0Const<2 * DIM> c, Rt0Fast<2 * DIM> F,
+                                                               double* stage) {
   constexpr int N = 2 * DIM;
   constexpr int NC = N + 1;
-  __shared__ float dsm[N * N][kCT];   // Delta32 (row-major), this thread's column
-  __shared__ float csm[N * NC][kCT];  // correction C (row-major)
+  __shared__ float scr[2 * N * N + Rt0Fast<N>::NS][kCT];  // general-correction scratch (rare cells)
   __shared__ longlong2 pf_rs[SIDE ? N : 1][kCT];                       // {row start, row} per slot
   __shared__ unsigned long long pf_tab[SIDE ? N : 1][kCT];             // packed column ranks
   __shared__ double2 pf_sv[(SIDE && PASS == 1) ? N : 1][kCT];          // colour 0's {diagonal, g}
@@ -477,8 +556,9 @@ __global__ void __launch_bounds__(kCT, HDR_CELL_MINB) k_rt0_cell(HybArgs A, Rt0C
   double f[N];
 #pragma unroll
   for (int j = 0; j < N; ++j) f[j] = A.f[static_cast<int64_t>(e) * N + j];
-  rt0_cell_correction<DIM, kCT>(A, c, a, b, s, ib, f, dsm, csm, tid);
-  auto hrow = [&](int k, double (&h)[NC]) { rt0_hrow<DIM, kCT>(c, s, ib, f, csm, tid, k, h); };
+  float C[Rt0Fast<N>::NS];
+  rt0_correction<DIM>(A, c, F, a, b, s, ib, &scr[0][tid], kCT, C);
+  auto hrow = [&](int k, double (&h)[NC]) { rt0_hrow_c<DIM>(c, s, ib, f, C, k, h); };
   if (SIDE) {
     // both colours write their own columns of their faces' rows straight into H;
     // the two shared quantities of a row (diagonal, g) meet in a per-row side
@@ -595,11 +675,19 @@ __global__ void __launch_bounds__(kCT, HDR_CELL_MINB) k_rt0_cell(HybArgs A, Rt0C
 // coalesced) and colour 1 completes and writes it.  Every H row and g entry is
 // written once; the two contributions to a diagonal entry / g entry meet as
 // fl(h_minus + h_plus), the reference's two-term sum.
+#ifndef HDR_BRICK_MINB
+#define HDR_BRICK_MINB 4
+#endif
 template <int DIM>
 struct Brick;
+#ifndef HDR_BX
+#define HDR_BX 32
+#define HDR_BY 2
+#define HDR_BZ 2
+#endif
 template <>
 struct Brick<3> {
-  static constexpr int X = 32, Y = 2, Z = 2;
+  static constexpr int X = HDR_BX, Y = HDR_BY, Z = HDR_BZ;
 };
 template <>
 struct Brick<2> {
@@ -614,7 +702,9 @@ struct BrickDims {
   static constexpr int NL = NL0 + NL1 + NL2;  // x-lines of faces of each axis
   static constexpr int RL = 4 * DIM - 1;      // longest H row
   static constexpr int CAP = (X + 1) * RL;    // entries of one line segment
-  static constexpr size_t smem_bytes() { return static_cast<size_t>(NL) * (CAP + X + 1) * sizeof(double); }
+  static constexpr size_t line_bytes = static_cast<size_t>(NL) * (CAP + X + 1) * sizeof(double);
+  static constexpr size_t scratch_bytes = static_cast<size_t>(2 * 4 * DIM * DIM + DIM * (2 * DIM + 1)) * CT * sizeof(float);
+  static constexpr size_t smem_bytes() { return line_bytes > scratch_bytes ? line_bytes : scratch_bytes; }
 };
 
 // interior faces of a cell (its row-length contribution)
@@ -626,18 +716,17 @@ __device__ __forceinline__ int interior_faces(const DevMesh& m, int x, int y, in
 }
 
 template <int DIM, int COL>
-__global__ void __launch_bounds__(BrickDims<DIM>::CT) k_rt0_brick(HybArgs A, Rt0Const<2 * DIM> c, double* stage,
-                                                                  int nbx, int nby, int nbz) {
+__global__ void __launch_bounds__(BrickDims<DIM>::CT, HDR_BRICK_MINB) k_rt0_brick(HybArgs A, Rt0Const<2 * DIM> c, Rt0Fast<2 * DIM> F,
+                                                                  double* stage, int nbx, int nby, int nbz) {
   using B = BrickDims<DIM>;
   constexpr int N = 2 * DIM;
   constexpr int NC = N + 1;
   constexpr int X = B::X, Y = B::Y, Z = B::Z, CT = B::CT, NL = B::NL, CAP = B::CAP;
-  static_assert(N * N * CT * sizeof(float) <= NL * CAP * sizeof(double), "Delta32 aliases the line buffers");
-  __shared__ float csm[N * NC][CT];
   extern __shared__ double bsm[];
   double* hbuf = bsm;              // NL x CAP: H line segments
   double* gbuf = bsm + NL * CAP;   // NL x (X + 1): g of the line's faces
-  float(*dsm)[CT] = reinterpret_cast<float(*)[CT]>(bsm);  // Delta32: dead before the segments are filled
+  // general-correction scratch of the rare P > 1 cells: dead before the segments are filled
+  float* scr = reinterpret_cast<float*>(bsm) + threadIdx.x;
   __shared__ long long l_base[NL];  // H offset of the line's first row
   __shared__ int l_row0[NL], l_pa[NL], l_oa[NL], l_ob[NL], l_olo[NL], l_ohi[NL];
   const DevMesh& m = A.m;
@@ -722,6 +811,7 @@ __global__ void __launch_bounds__(BrickDims<DIM>::CT) k_rt0_brick(HybArgs A, Rt0
   const int cc[3] = {x0 + lx, y0 + ly, z0 + lz};
   const bool valid = lx < ex && ly < ey && lz < ez;
   double a = 1.0, b = 1.0, s = 1.0, ib = 1.0;
+  float C[Rt0Fast<N>::NS];
   double f[N];
 #pragma unroll
   for (int j = 0; j < N; ++j) f[j] = 0.0;
@@ -733,7 +823,7 @@ __global__ void __launch_bounds__(BrickDims<DIM>::CT) k_rt0_brick(HybArgs A, Rt0
     for (int j = 0; j < N; ++j) f[j] = A.f[e * N + j];
     ib = 1.0 / b;
     s = b / fma(a, c.lam, b);
-    rt0_cell_correction<DIM, CT>(A, c, a, b, s, ib, f, dsm, csm, tid);
+    rt0_correction<DIM>(A, c, F, a, b, s, ib, scr, CT, C);
   }
   __syncthreads();  // line metadata
   unsigned lo = 0, hi = 0;
@@ -756,7 +846,7 @@ __global__ void __launch_bounds__(BrickDims<DIM>::CT) k_rt0_brick(HybArgs A, Rt0
       const int face = face_id32(m, ax, cc[0] + (ax == 0 ? side : 0), cc[1] + (ax == 1 ? side : 0), cc[2] + (ax == 2 ? side : 0));
       const bool bb = side ? lc[ax] == ec[ax] - 1 : lc[ax] == 0;  // neighbour in the adjacent brick
       double h[NC];
-      rt0_hrow<DIM, CT>(c, s, ib, f, csm, tid, k, h);
+      rt0_hrow_c<DIM>(c, s, ib, f, C, k, h);
       if (COL == 0 && bb) {
 #pragma unroll
         for (int q = 0; q <= N; ++q) stage[q * nfaces + face] = h[q];
@@ -809,7 +899,7 @@ __global__ void __launch_bounds__(BrickDims<DIM>::CT) k_rt0_brick(HybArgs A, Rt0
       const uint64_t own = __ldg(A.rank_tab + ((static_cast<size_t>(k) << (2 * DIM + 1)) + flags) * 2);
       const unsigned rd = static_cast<unsigned>(own >> (4 * k)) & 15u;
       double h[NC];
-      rt0_hrow<DIM, CT>(c, s, ib, f, csm, tid, k, h);
+      rt0_hrow_c<DIM>(c, s, ib, f, C, k, h);
       double* dp = hbuf + l * CAP + (A.frs[face].x - l_base[l]) + rd;
       *dp = *dp + h[k];
       gbuf[l * (X + 1) + p] = gbuf[l * (X + 1) + p] + h[N];
@@ -1236,6 +1326,53 @@ __global__ void k_average(DevMesh m, const double* x_hat, double* x) {
 
 }  // namespace
 
+// Rt0Fast from the constant block; false when the structure it relies on is absent
+// (M^-1 not block-diagonal per axis, or D / M / E / Ma not bitwise symmetric).
+// Constant block: D, M, E, Ma, N0 (n*n each), X (n), lambda, rho, M^-1 (n*n).
+template <int N>
+static bool rt0_fast_setup(const double* hc, Rt0Fast<N>& F) {
+  const double *D = hc, *M = hc + N * N, *E = hc + 2 * N * N, *Ma = hc + 3 * N * N, *X = hc + 5 * N * N;
+  const double* N0 = hc + 5 * N * N + N + 2;  // M^-1 (named N0 below: the block-diagonal factor of W)
+  for (int k = 0; k < N; ++k)
+    for (int l = 0; l < N; ++l) {
+      for (const double* m : {D, M, E, Ma, N0})
+        if (m[k * N + l] != m[l * N + k]) return false;
+      if ((k >> 1) != (l >> 1) && (N0[k * N + l] != 0.0 || M[k * N + l] != 0.0 || Ma[k * N + l] != 0.0)) return false;
+    }
+  // W(t) = M^-1 + t XX^T (t = s - 1, W = N0 + s XX^T);
+  // W E W = Mi E Mi + t (Mi E XX^T + XX^T E Mi) + t^2 XX^T E XX^T
+  auto poly = [&](const double* Em, float (*out)[Rt0Fast<N>::NS]) {
+    std::vector<double> NE(N * N, 0.0), NEN(N * N, 0.0), EX(N, 0.0), NEX(N, 0.0);
+    double xex = 0.0;
+    for (int k = 0; k < N; ++k)
+      for (int l = 0; l < N; ++l) {
+        for (int j = 0; j < N; ++j) NE[k * N + l] += N0[k * N + j] * Em[j * N + l];
+        EX[k] += Em[k * N + l] * X[l];
+      }
+    for (int k = 0; k < N; ++k) {
+      for (int l = 0; l < N; ++l)
+        for (int j = 0; j < N; ++j) NEN[k * N + l] += NE[k * N + j] * N0[j * N + l];
+      for (int j = 0; j < N; ++j) NEX[k] += N0[k * N + j] * EX[j];
+      xex += X[k] * EX[k];
+    }
+    for (int k = 0; k < N; ++k)
+      for (int l = k; l < N; ++l) {
+        const int i = sym_idx(k, l, N);
+        out[0][i] = static_cast<float>(NEN[k * N + l]);
+        out[1][i] = static_cast<float>(NEX[k] * X[l] + X[k] * NEX[l]);
+        out[2][i] = static_cast<float>(xex * X[k] * X[l]);
+      }
+  };
+  for (int k = 0; k < N; ++k) {
+    F.n0[k][0] = static_cast<float>(N0[k * N + (k & ~1)]);
+    F.n0[k][1] = static_cast<float>(N0[k * N + (k | 1)]);
+    F.x[k] = static_cast<float>(X[k]);
+  }
+  poly(E, F.p);
+  poly(Ma, F.q);
+  return true;
+}
+
 void launch_hybridize_rt0_rows(const HybArgs& a, const double* hc, double* stage, cudaStream_t st) {
   const int64_t cnt = parity_count(a.m);
   auto fill = [&](auto& c, int N) {
@@ -1248,13 +1385,17 @@ void launch_hybridize_rt0_rows(const HybArgs& a, const double* hc, double* stage
     c.lam = hc[5 * N * N + N];
     c.rho = hc[5 * N * N + N + 1];
   };
-  static const bool rows = getenv("HDR_RT0_ROWS") != nullptr;  // lane-per-row variant (A/B timing)
+  // lane-per-row variant: A/B timing, or when the element lacks the structure of Rt0Fast
+  bool rows = getenv("HDR_RT0_ROWS") != nullptr;
+  Rt0Fast<6> f3{};
+  Rt0Fast<4> f2{};
+  if (!(a.m.dim == 3 ? rt0_fast_setup<6>(hc, f3) : rt0_fast_setup<4>(hc, f2))) rows = true;
   // thread-per-cell scattered-store variant: forced, or for meshes too small to
   // give each SM a few bricks per colour (e.g. 64 x 64 quads: 16 bricks a colour)
   // (HDR_RT0_BRICK forces the brick kernel at any size: tests)
   const bool cell = getenv("HDR_RT0_CELL") != nullptr || (a.m.ncells < 148 * 128 * 4 && !getenv("HDR_RT0_BRICK"));
   static const bool side = getenv("HDR_RT0_STAGE") == nullptr;  // default: per-row side slots; HDR_RT0_STAGE=1: row stage
-  auto brick = [&](auto dimc, auto& c) {
+  auto brick = [&](auto dimc, auto& c, auto& F) {
     constexpr int D = decltype(dimc)::value;
     using B = BrickDims<D>;
     const int nbx = static_cast<int>((a.m.N[0] + B::X - 1) / B::X), nby = static_cast<int>((a.m.N[1] + B::Y - 1) / B::Y);
@@ -1263,44 +1404,44 @@ void launch_hybridize_rt0_rows(const HybArgs& a, const double* hc, double* stage
     const size_t smem = B::smem_bytes();
     cudaFuncSetAttribute(k_rt0_brick<D, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     cudaFuncSetAttribute(k_rt0_brick<D, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    k_rt0_brick<D, 0><<<grid, B::CT, smem, st>>>(a, c, stage, nbx, nby, nbz);
-    k_rt0_brick<D, 1><<<grid, B::CT, smem, st>>>(a, c, stage, nbx, nby, nbz);
+    k_rt0_brick<D, 0><<<grid, B::CT, smem, st>>>(a, c, F, stage, nbx, nby, nbz);
+    k_rt0_brick<D, 1><<<grid, B::CT, smem, st>>>(a, c, F, stage, nbx, nby, nbz);
   };
   if (a.m.dim == 3) {
     Rt0Const<6> c;
     fill(c, 6);
     if (!rows && !cell) {
-      brick(std::integral_constant<int, 3>{}, c);
+      brick(std::integral_constant<int, 3>{}, c, f3);
     } else if (rows) {
       const unsigned nb = static_cast<unsigned>((cnt + 4 * 5 - 1) / (4 * 5));
       k_rt0_rows<3, 0><<<nb, 128, 0, st>>>(a, c, stage);
       k_rt0_rows<3, 1><<<nb, 128, 0, st>>>(a, c, stage);
     } else if (side) {
       const unsigned nb = static_cast<unsigned>((cnt + kCT - 1) / kCT);
-      k_rt0_cell<3, 0, true><<<nb, kCT, 0, st>>>(a, c, stage);
-      k_rt0_cell<3, 1, true><<<nb, kCT, 0, st>>>(a, c, stage);
+      k_rt0_cell<3, 0, true><<<nb, kCT, 0, st>>>(a, c, f3, stage);
+      k_rt0_cell<3, 1, true><<<nb, kCT, 0, st>>>(a, c, f3, stage);
     } else {
       const unsigned nb = static_cast<unsigned>((cnt + kCT - 1) / kCT);
-      k_rt0_cell<3, 0, false><<<nb, kCT, 0, st>>>(a, c, stage);
-      k_rt0_cell<3, 1, false><<<nb, kCT, 0, st>>>(a, c, stage);
+      k_rt0_cell<3, 0, false><<<nb, kCT, 0, st>>>(a, c, f3, stage);
+      k_rt0_cell<3, 1, false><<<nb, kCT, 0, st>>>(a, c, f3, stage);
     }
   } else {
     Rt0Const<4> c;
     fill(c, 4);
     if (!rows && !cell) {
-      brick(std::integral_constant<int, 2>{}, c);
+      brick(std::integral_constant<int, 2>{}, c, f2);
     } else if (rows) {
       const unsigned nb = static_cast<unsigned>((cnt + 4 * 8 - 1) / (4 * 8));
       k_rt0_rows<2, 0><<<nb, 128, 0, st>>>(a, c, stage);
       k_rt0_rows<2, 1><<<nb, 128, 0, st>>>(a, c, stage);
     } else if (side) {
       const unsigned nb = static_cast<unsigned>((cnt + kCT - 1) / kCT);
-      k_rt0_cell<2, 0, true><<<nb, kCT, 0, st>>>(a, c, stage);
-      k_rt0_cell<2, 1, true><<<nb, kCT, 0, st>>>(a, c, stage);
+      k_rt0_cell<2, 0, true><<<nb, kCT, 0, st>>>(a, c, f2, stage);
+      k_rt0_cell<2, 1, true><<<nb, kCT, 0, st>>>(a, c, f2, stage);
     } else {
       const unsigned nb = static_cast<unsigned>((cnt + kCT - 1) / kCT);
-      k_rt0_cell<2, 0, false><<<nb, kCT, 0, st>>>(a, c, stage);
-      k_rt0_cell<2, 1, false><<<nb, kCT, 0, st>>>(a, c, stage);
+      k_rt0_cell<2, 0, false><<<nb, kCT, 0, st>>>(a, c, f2, stage);
+      k_rt0_cell<2, 1, false><<<nb, kCT, 0, st>>>(a, c, f2, stage);
     }
   }
   count_launch(2);
