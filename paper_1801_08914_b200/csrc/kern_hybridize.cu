@@ -707,6 +707,23 @@ struct BrickDims {
   static constexpr size_t smem_bytes() { return line_bytes > scratch_bytes ? line_bytes : scratch_bytes; }
 };
 
+// entries of the H rows of faces x in [xa, x) of one x-line of axis-ax faces
+// (x-faces: x is the face index; y / z faces: the cell column): row length =
+// interior faces of the face's two cells - 1, in closed form
+__device__ __forceinline__ int cnt_in(int lo, int hi, int a, int b) { return max(0, min(hi, b) - max(lo, a)); }
+template <int DIM>
+__device__ __forceinline__ int line_entries(const DevMesh& m, int ax, int xa, int x, int y, int z) {
+  const int N0 = static_cast<int>(m.N[0]), N1 = static_cast<int>(m.N[1]), N2 = DIM == 3 ? static_cast<int>(m.N[2]) : 1;
+  auto f = [](int c, int n) { return (c > 0) + (c + 1 < n); };
+  const int big = 1 << 30;
+  const int sx = cnt_in(xa, x, 1, big) + cnt_in(xa, x, -big, N0 - 1);  // sum of f(x', N0) over [xa, x)
+  const int fz = DIM == 3 ? f(z, N2) : 0;
+  if (ax == 0)
+    return sx + cnt_in(xa, x, 2, big) + cnt_in(xa, x, -big, N0) + (x - xa) * (2 * (f(y, N1) + fz) - 1);
+  if (ax == 1) return 2 * sx + (x - xa) * (f(y - 1, N1) + f(y, N1) + 2 * fz - 1);
+  return 2 * sx + (x - xa) * (2 * f(y, N1) + f(z - 1, N2) + fz - 1);
+}
+
 // interior faces of a cell (its row-length contribution)
 template <int DIM>
 __device__ __forceinline__ int interior_faces(const DevMesh& m, int x, int y, int z) {
@@ -776,26 +793,16 @@ __global__ void __launch_bounds__(BrickDims<DIM>::CT, HDR_BRICK_MINB) k_rt0_bric
         oa = pa, ob = (COL == 0 && edge) ? -1 : pb;
       }
     }
-    long long base = 0, lo_ = 0, hi_ = 0;
-    int row0 = 0;
+    long long base = 0;
+    int row0 = 0, lo_ = 0, hi_ = 0;
     if (pb >= pa) {
       const longlong2 fa = A.frs[line_face(ax, jj, kk, pa)];
       base = fa.x;
       row0 = static_cast<int>(fa.y);
       if (ob >= oa) {
-        const longlong2 fo = A.frs[line_face(ax, jj, kk, oa)];
-        const longlong2 fb = A.frs[line_face(ax, jj, kk, ob)];
-        // length of the last owned row: interior faces of its two cells - 1
-        const int bxp = x0 + ob, byp = y0 + jj, bzp = z0 + kk;  // the plus cell of face ob
-        int len;
-        if (ax == 0)
-          len = interior_faces<DIM>(m, bxp - 1, byp, bzp) + interior_faces<DIM>(m, bxp, byp, bzp) - 1;
-        else if (ax == 1)
-          len = interior_faces<DIM>(m, bxp, byp - 1, bzp) + interior_faces<DIM>(m, bxp, byp, bzp) - 1;
-        else
-          len = interior_faces<DIM>(m, bxp, byp, bzp - 1) + interior_faces<DIM>(m, bxp, byp, bzp) - 1;
-        lo_ = fo.x - base;
-        hi_ = fb.x + len - base;
+        const int y = y0 + jj, z = z0 + kk;
+        lo_ = line_entries<DIM>(m, ax, x0 + pa, x0 + oa, y, z);
+        hi_ = line_entries<DIM>(m, ax, x0 + pa, x0 + ob + 1, y, z);
       }
     }
     l_base[tid] = base;
@@ -803,8 +810,8 @@ __global__ void __launch_bounds__(BrickDims<DIM>::CT, HDR_BRICK_MINB) k_rt0_bric
     l_pa[tid] = pa;
     l_oa[tid] = oa;
     l_ob[tid] = ob;
-    l_olo[tid] = static_cast<int>(lo_);
-    l_ohi[tid] = static_cast<int>(hi_);
+    l_olo[tid] = lo_;
+    l_ohi[tid] = hi_;
   }
   // the cell
   const int lx = tid % X, ly = (tid / X) % Y, lz = tid / (X * Y);
@@ -858,7 +865,7 @@ __global__ void __launch_bounds__(BrickDims<DIM>::CT, HDR_BRICK_MINB) k_rt0_bric
       const unsigned flags = lo | (hi << DIM) | (far << (2 * DIM));
       const uint64_t* tab = A.rank_tab + ((static_cast<size_t>(k) << (2 * DIM + 1)) + flags) * 2;
       const uint64_t own = __ldg(tab);
-      double* rowp = hbuf + l * CAP + (A.frs[face].x - l_base[l]);
+      double* rowp = hbuf + l * CAP + line_entries<DIM>(m, ax, x0 + l_pa[l], x0 + p, cc[1] + (ax == 1 ? side : 0), cc[2] + (ax == 2 ? side : 0));
 #pragma unroll
       for (int q = 0; q < N; ++q) {
         const unsigned r = static_cast<unsigned>(own >> (4 * q)) & 15u;
@@ -900,7 +907,7 @@ __global__ void __launch_bounds__(BrickDims<DIM>::CT, HDR_BRICK_MINB) k_rt0_bric
       const unsigned rd = static_cast<unsigned>(own >> (4 * k)) & 15u;
       double h[NC];
       rt0_hrow_c<DIM>(c, s, ib, f, C, k, h);
-      double* dp = hbuf + l * CAP + (A.frs[face].x - l_base[l]) + rd;
+      double* dp = hbuf + l * CAP + line_entries<DIM>(m, ax, x0 + l_pa[l], x0 + p, cc[1], cc[2]) + rd;
       *dp = *dp + h[k];
       gbuf[l * (X + 1) + p] = gbuf[l * (X + 1) + p] + h[N];
     }
