@@ -675,29 +675,18 @@ __global__ void __launch_bounds__(kCT, HDR_CELL_MINB) k_rt0_cell(HybArgs A, Rt0C
 // coalesced) and colour 1 completes and writes it.  Every H row and g entry is
 // written once; the two contributions to a diagonal entry / g entry meet as
 // fl(h_minus + h_plus), the reference's two-term sum.
-#ifndef HDR_BRICK_MINB
-#define HDR_BRICK_MINB 4
-#endif
-template <int DIM>
-struct Brick;
-#ifndef HDR_BX
-#define HDR_BX 32
-#define HDR_BY 2
-#define HDR_BZ 2
-#endif
-template <>
-struct Brick<3> {
-  static constexpr int X = HDR_BX, Y = HDR_BY, Z = HDR_BZ;
-};
-template <>
-struct Brick<2> {
-  static constexpr int X = 32, Y = 4, Z = 1;
+// brick shapes: BX cells along x (64 when the mesh is at least 48 cells wide,
+// else 32) by 2 x 2 (3D) / 4 (2D); 512 threads per SM either way
+template <int DIM, int BX>
+struct Brick {
+  static constexpr int X = BX, Y = DIM == 3 ? 2 : 4, Z = DIM == 3 ? 2 : 1;
 };
 
-template <int DIM>
+template <int DIM, int BX>
 struct BrickDims {
-  static constexpr int X = Brick<DIM>::X, Y = Brick<DIM>::Y, Z = Brick<DIM>::Z;
+  static constexpr int X = Brick<DIM, BX>::X, Y = Brick<DIM, BX>::Y, Z = Brick<DIM, BX>::Z;
   static constexpr int CT = X * Y * Z;
+  static constexpr int MINB = 512 / CT;
   static constexpr int NL0 = Y * Z, NL1 = (Y + 1) * Z, NL2 = DIM == 3 ? Y * (Z + 1) : 0;
   static constexpr int NL = NL0 + NL1 + NL2;  // x-lines of faces of each axis
   static constexpr int RL = 4 * DIM - 1;      // longest H row
@@ -732,10 +721,10 @@ __device__ __forceinline__ int interior_faces(const DevMesh& m, int x, int y, in
   return n;
 }
 
-template <int DIM, int COL>
-__global__ void __launch_bounds__(BrickDims<DIM>::CT, HDR_BRICK_MINB) k_rt0_brick(HybArgs A, Rt0Const<2 * DIM> c, Rt0Fast<2 * DIM> F,
-                                                                  double* stage, int nbx, int nby, int nbz) {
-  using B = BrickDims<DIM>;
+template <int DIM, int COL, int BX>
+__global__ void __launch_bounds__(BrickDims<DIM, BX>::CT, BrickDims<DIM, BX>::MINB)
+    k_rt0_brick(HybArgs A, Rt0Const<2 * DIM> c, Rt0Fast<2 * DIM> F, double* stage, int nbx, int nby, int nbz) {
+  using B = BrickDims<DIM, BX>;
   constexpr int N = 2 * DIM;
   constexpr int NC = N + 1;
   constexpr int X = B::X, Y = B::Y, Z = B::Z, CT = B::CT, NL = B::NL, CAP = B::CAP;
@@ -1402,23 +1391,25 @@ void launch_hybridize_rt0_rows(const HybArgs& a, const double* hc, double* stage
   // (HDR_RT0_BRICK forces the brick kernel at any size: tests)
   const bool cell = getenv("HDR_RT0_CELL") != nullptr || (a.m.ncells < 148 * 128 * 4 && !getenv("HDR_RT0_BRICK"));
   static const bool side = getenv("HDR_RT0_STAGE") == nullptr;  // default: per-row side slots; HDR_RT0_STAGE=1: row stage
-  auto brick = [&](auto dimc, auto& c, auto& F) {
-    constexpr int D = decltype(dimc)::value;
-    using B = BrickDims<D>;
+  auto brick = [&](auto dimc, auto bxc, auto& c, auto& F) {
+    constexpr int D = decltype(dimc)::value, BXv = decltype(bxc)::value;
+    using B = BrickDims<D, BXv>;
     const int nbx = static_cast<int>((a.m.N[0] + B::X - 1) / B::X), nby = static_cast<int>((a.m.N[1] + B::Y - 1) / B::Y);
     const int nbz = D == 3 ? static_cast<int>((a.m.N[2] + B::Z - 1) / B::Z) : 1;
     const unsigned grid = static_cast<unsigned>(((nbx + 1) / 2) * nby * nbz);
     const size_t smem = B::smem_bytes();
-    cudaFuncSetAttribute(k_rt0_brick<D, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    cudaFuncSetAttribute(k_rt0_brick<D, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    k_rt0_brick<D, 0><<<grid, B::CT, smem, st>>>(a, c, F, stage, nbx, nby, nbz);
-    k_rt0_brick<D, 1><<<grid, B::CT, smem, st>>>(a, c, F, stage, nbx, nby, nbz);
+    cudaFuncSetAttribute(k_rt0_brick<D, 0, BXv>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    cudaFuncSetAttribute(k_rt0_brick<D, 1, BXv>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    k_rt0_brick<D, 0, BXv><<<grid, B::CT, smem, st>>>(a, c, F, stage, nbx, nby, nbz);
+    k_rt0_brick<D, 1, BXv><<<grid, B::CT, smem, st>>>(a, c, F, stage, nbx, nby, nbz);
   };
+  const bool wide = a.m.N[0] >= 48 && !getenv("HDR_RT0_BRICK32");
   if (a.m.dim == 3) {
     Rt0Const<6> c;
     fill(c, 6);
     if (!rows && !cell) {
-      brick(std::integral_constant<int, 3>{}, c, f3);
+      if (wide) brick(std::integral_constant<int, 3>{}, std::integral_constant<int, 64>{}, c, f3);
+      else brick(std::integral_constant<int, 3>{}, std::integral_constant<int, 32>{}, c, f3);
     } else if (rows) {
       const unsigned nb = static_cast<unsigned>((cnt + 4 * 5 - 1) / (4 * 5));
       k_rt0_rows<3, 0><<<nb, 128, 0, st>>>(a, c, stage);
@@ -1436,7 +1427,8 @@ void launch_hybridize_rt0_rows(const HybArgs& a, const double* hc, double* stage
     Rt0Const<4> c;
     fill(c, 4);
     if (!rows && !cell) {
-      brick(std::integral_constant<int, 2>{}, c, f2);
+      if (wide) brick(std::integral_constant<int, 2>{}, std::integral_constant<int, 64>{}, c, f2);
+      else brick(std::integral_constant<int, 2>{}, std::integral_constant<int, 32>{}, c, f2);
     } else if (rows) {
       const unsigned nb = static_cast<unsigned>((cnt + 4 * 8 - 1) / (4 * 8));
       k_rt0_rows<2, 0><<<nb, 128, 0, st>>>(a, c, stage);
