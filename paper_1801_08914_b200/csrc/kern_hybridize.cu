@@ -746,6 +746,9 @@ __global__ void __launch_bounds__(BrickDims<DIM, BX>::CT, BrickDims<DIM, BX>::MI
   const int x0 = bx * X, y0 = by * Y, z0 = bz * Z;
   const int ex = min(X, N0 - x0), ey = min(Y, N1 - y0), ez = DIM == 3 ? min(Z, N2 - z0) : 1;
   const int tid = threadIdx.x;
+  // programmatic dependent launch: colour 1 may start (line metadata, element
+  // solves) while colour 0's last wave runs; it waits before touching the stage
+  if (COL == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   // face p of line (ax, jj, kk): x = x0 + p, y = y0 + jj, z = z0 + kk (ax 1: jj in [0, ey], ax 2: kk in [0, ez])
   auto line_face = [&](int ax, int jj, int kk, int p) { return face_id32(m, ax, x0 + p, y0 + jj, z0 + kk); };
   if (tid < NL) {  // line metadata
@@ -822,6 +825,7 @@ __global__ void __launch_bounds__(BrickDims<DIM, BX>::CT, BrickDims<DIM, BX>::MI
     rt0_correction<DIM>(A, c, F, a, b, s, ib, scr, CT, C);
   }
   __syncthreads();  // line metadata
+  if (COL == 1) asm volatile("griddepcontrol.wait;" ::: "memory");  // colour 0 complete, stage visible
   unsigned lo = 0, hi = 0;
 #pragma unroll
   for (int x = 0; x < DIM; ++x) {
@@ -1401,7 +1405,17 @@ void launch_hybridize_rt0_rows(const HybArgs& a, const double* hc, double* stage
     cudaFuncSetAttribute(k_rt0_brick<D, 0, BXv>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     cudaFuncSetAttribute(k_rt0_brick<D, 1, BXv>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     k_rt0_brick<D, 0, BXv><<<grid, B::CT, smem, st>>>(a, c, F, stage, nbx, nby, nbz);
-    k_rt0_brick<D, 1, BXv><<<grid, B::CT, smem, st>>>(a, c, F, stage, nbx, nby, nbz);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(B::CT);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = getenv("HDR_NO_PDL") ? 0 : 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, k_rt0_brick<D, 1, BXv>, a, c, F, stage, nbx, nby, nbz);
   };
   const bool wide = a.m.N[0] >= 48 && !getenv("HDR_RT0_BRICK32");
   if (a.m.dim == 3) {
