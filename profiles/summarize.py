@@ -57,6 +57,39 @@ def main():
                          ", ".join(f"{k} {100 * v / tot:.0f}%" for k, v in top) + " |")
             lines.append("")
     Path("profiles") .joinpath(f"{rnd}_ncu_summary.md").write_text("\n".join(lines) + "\n")
+    traffic_json(src)
+
+
+# per step DRAM bytes (read + write) of the dominant kernels, from the traffic launch lists;
+# the number of steps captured = launches of the step's anchor kernel / its launches per step
+ANCHOR = {"cfg2": ("k_rt0_brick", 2), "cfg3": ("k_hyb_warp", 2), "cfg4": ("k_piola_assemble", 1), "cfg5": ("k_hyb_big", 2)}
+
+
+def traffic_json(src: Path):
+    import json
+    out = {}
+    for cfg, (anchor, per_step) in ANCHOR.items():
+        f = src / f"traffic_{cfg}.csv"
+        if not f.exists():
+            continue
+        rows = [r for r in csv.reader(f.read_text().splitlines()) if r]
+        hdr = next((r for r in rows if "Kernel Name" in r), None)
+        if hdr is None:
+            continue
+        tot, launches = 0.0, set()
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+        for r in rows:
+            if len(r) != len(hdr) or r is hdr:
+                continue
+            d = dict(zip(hdr, r))
+            if d["Metric Name"] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+                tot += float(d["Metric Value"].replace(",", "")) * scale.get(d["Metric Unit"], 1)
+            if anchor in d["Kernel Name"]:
+                launches.add(d["ID"])
+        if launches:
+            out[cfg] = tot / (len(launches) / per_step)
+    if out:
+        Path("profiles").joinpath("ncu_traffic.json").write_text(json.dumps(out, indent=1) + "\n")
 
 
 if __name__ == "__main__":
