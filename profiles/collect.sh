@@ -21,7 +21,7 @@ timeout 600 python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu > "$OUT/plain
 # DRAM traffic of the dominant kernels, one step per config
 for c in 2 3 4 5; do
   case $c in
-    2) K='regex:k_rt0_cell' ;;
+    2) K='regex:k_rt0_brick|k_rt0_cell|k_rt0_rows' ;;
     3) K='regex:k_hyb_warp' ;;
     4) K='regex:k_piola_assemble|k_alg<|k_run_sum' ;;
     5) K='regex:k_hyb_big|k_gemm_f64' ;;
