@@ -943,6 +943,18 @@ int hdo_element_matrix(hdo_ctx* c, long long cell, double* a_t) {
     memcpy(a_t, ahat + cell * n * n, (size_t)(n * n) * 8);
     return 0;
   }
+  /* a_sel / a_sel_blocks: explicit blocks for a few cells (test-scale parity on
+   * full-size meshes: the device's A_T of the sampled cells) */
+  const double* sel = get_d(c, "a_sel");
+  const double* sblk = get_d(c, "a_sel_blocks");
+  if (sel && sblk) {
+    const long long ns = hdo_count(c, "a_sel");
+    for (long long q = 0; q < ns; ++q)
+      if ((long long)sel[q] == cell && hdo_count(c, "a_sel_blocks") >= (q + 1) * n * n) {
+        memcpy(a_t, sblk + q * n * n, (size_t)(n * n) * 8);
+        return 0;
+      }
+  }
   if (!al || !be) {
     set_err(c, "alpha/beta not set");
     return 1;

@@ -12,6 +12,7 @@
 // The per-cell descriptors (partition, multiplier rows, constraint slice) are
 // the FE structure of reduction.cpp:236-258 / :31-57, built once here.
 #include <algorithm>
+#include <cstdlib>
 #include <memory>
 #include <vector>
 
@@ -29,6 +30,9 @@ struct GeomState {
   DevMesh dm{};
   double h[3] = {1, 1, 1}, det0 = 1;
   DBuf<double> verts, qs, bq_val, bq_div, bq_w;
+  bool gemm = false;            // k_piola_gemm (component-separable basis) instead of k_piola_assemble
+  DBuf<double> tphi, tdiv;      // np x n tables in the component-sorted order
+  DBuf<int> perm;
   bool mapped = false;   // trilinear cells (vertices attached); else the affine reference element
   DBuf<double> ref_dm;   // affine: D_ref, M_ref (n x n each)
   // hybrid descriptors
@@ -48,6 +52,8 @@ struct GeomState {
   DBuf<double> ablk, hbuf, gbuf, sbuf, fsbuf, gws;
   int64_t gws_doubles = 0;
   DBuf<int> status;
+  int max_nr = 0;
+  bool spd = false;  // hybridize through kern_spd.cu (SPD blocks small enough for shared memory)
   DBuf<unsigned long long> bad;
 };
 
@@ -92,7 +98,8 @@ void assemble(GeomState* G, const double* alpha, const double* beta, cudaStream_
   P.beta = beta;
   P.ablk = G->ablk.p;
   const int grid = static_cast<int>(std::min<int64_t>(G->ncells, static_cast<int64_t>(sms())));
-  launch_piola_assemble(P, grid > 0 ? grid : 1, st);
+  if (G->gemm) launch_piola_gemm(P, G->tphi.p, G->tdiv.p, G->perm.p, grid > 0 ? grid : 1, st);
+  else launch_piola_assemble(P, grid > 0 ? grid : 1, st);
 }
 
 AlgArgs hyb_args(GeomState* G, const double* f) {
@@ -128,6 +135,9 @@ hdr_status read_geom_status(GeomState* G, cudaStream_t st, const char* who) {
     CK(cudaMemsetAsync(G->status.p, 0, sizeof(int), st));
     CK(cudaMemsetAsync(G->bad.p, 0xff, sizeof(unsigned long long), st));
     CK(cudaStreamSynchronize(st));
+    if (status & 4)
+      return fail(HDR_UNSUPPORTED, std::string(who) + ": element block not positive definite (element " +
+                                       std::to_string(bad) + ")");
     return fail(HDR_SINGULAR_BLOCK,
                 std::string(who) + ": singular block (element " + std::to_string(bad) + ", pivot <= 1e-14 max|block|)");
   }
@@ -269,6 +279,38 @@ GeomState* geom_create(const RefElement& re, const DevMesh& dm, const std::vecto
     G->bq_val.upload(re.bq_val);
     G->bq_div.upload(re.bq_div);
     G->bq_w.upload(re.bq_w);
+    // component-separable basis (every phi_j has one nonzero component): sorted
+    // tables for the GEMM-form assembly
+    const int n = re.n, np = static_cast<int>(re.bq_w.size());
+    std::vector<int> comp(static_cast<size_t>(n), -1);
+    bool sep = piola_gemm_supported(n, np) && !getenv("HDR_PIOLA_DIRECT");
+    for (int j = 0; j < n && sep; ++j)
+      for (int p = 0; p < np && sep; ++p)
+        for (int c = 0; c < 3; ++c)
+          if (re.bq_val[(static_cast<size_t>(p) * n + j) * 3 + c] != 0.0) {
+            if (comp[j] >= 0 && comp[j] != c) sep = false;
+            comp[j] = c;
+          }
+    std::vector<int> perm;
+    for (int c = 0; c < 3 && sep; ++c)
+      for (int j = 0; j < n; ++j)
+        if (comp[j] == c) perm.push_back(j);
+    sep = sep && static_cast<int>(perm.size()) == n;
+    for (int c = 0; c < 3 && sep; ++c)
+      sep = std::count(comp.begin(), comp.end(), c) == n / 3;
+    if (sep) {
+      std::vector<double> tp(static_cast<size_t>(np) * n), td(static_cast<size_t>(np) * n);
+      for (int p = 0; p < np; ++p)
+        for (int jj = 0; jj < n; ++jj) {
+          const int j = perm[jj];
+          tp[static_cast<size_t>(p) * n + jj] = re.bq_val[(static_cast<size_t>(p) * n + j) * 3 + comp[j]];
+          td[static_cast<size_t>(p) * n + jj] = re.bq_div[static_cast<size_t>(p) * n + j];
+        }
+      G->tphi.upload(tp);
+      G->tdiv.upload(td);
+      G->perm.upload(perm);
+      G->gemm = true;
+    }
   } else {
     std::vector<double> dmv(re.divdiv);
     dmv.insert(dmv.end(), re.mass.begin(), re.mass.end());
@@ -344,6 +386,16 @@ GeomState* geom_create(const RefElement& re, const DevMesh& dm, const std::vecto
   G->cent_v.upload(cent_v);
   G->plan_h = alg_plan(ne, n, max_nr + 1);
   ensure_ws(G.get(), G->plan_h);
+  G->max_nr = max_nr;
+  G->spd = !getenv("HDR_NO_SPD") && spd_supported(n, max_nr + 1);
+  if (G->spd) {
+    int grid = 1;
+    const int64_t need = spd_gws_doubles(ne, n, max_nr + 1, &grid);
+    if (need > G->gws_doubles) {
+      G->gws.alloc(static_cast<size_t>(need));
+      G->gws_doubles = need;
+    }
+  }
   G->hbuf.alloc(static_cast<size_t>(hoff.back()));
   G->gbuf.alloc(static_cast<size_t>(goff.back()));
   // from_triplets order of H and g, once
@@ -375,7 +427,8 @@ hdr_status geom_hybridize(GeomState* G, const double* alpha, const double* beta,
   AlgArgs a = hyb_args(G, f);
   a.hbuf = G->hbuf.p;
   a.gbuf = G->gbuf.p;
-  launch_alg(a, ALG_HYB, G->plan_h, G->gws.p, st);
+  if (G->spd) launch_spd_hyb(a, G->n, G->max_nr + 1, G->gws.p, st);
+  else launch_alg(a, ALG_HYB, G->plan_h, G->gws.p, st);
   launch_run_sum(G->HR.nruns, G->HR.start.p, G->HR.src.p, nullptr, G->hbuf.p, hval, nullptr, 0, st);
   CK(cudaMemsetAsync(g, 0, static_cast<size_t>(G->m) * 8, st));
   launch_run_sum(G->GR.nruns, G->GR.start.p, G->GR.src.p, nullptr, G->gbuf.p, g, G->GR.index.p, 1, st);

@@ -159,6 +159,10 @@ struct AlgPlan {
 AlgPlan alg_plan(int64_t ne, int dmax, int ncmax);
 int64_t alg_gws_doubles(const AlgPlan& p);  // global scratch the plan needs
 void launch_alg(const AlgArgs& a, int mode, const AlgPlan& p, double* gws, cudaStream_t st);
+// SPD element blocks (kern_spd.cu): LDL^T + exact-residual refinement, hybridize mode
+bool spd_supported(int nmax, int ncmax);
+int64_t spd_gws_doubles(int64_t ne, int nmax, int ncmax, int* grid);
+void launch_spd_hyb(const AlgArgs& a, int nmax, int ncmax, double* gws, cudaStream_t st);
 void launch_alg_hkeys(const AlgArgs& a, uint64_t* hkeys, int64_t* hsrc, uint64_t* gkeys, int64_t* gsrc, cudaStream_t st);
 void launch_alg_skeys(const AlgArgs& a, const int64_t* trip_off, const int64_t* ftrip_off, uint64_t* skeys,
                       int64_t* ssrc, double* sw, uint64_t* fkeys, int64_t* fsrc, double* fw, cudaStream_t st);
@@ -198,6 +202,11 @@ size_t piola_smem_bytes(int n);
 void launch_affine_assemble(int64_t ncells, int n, const double* dm, const double* alpha, const double* beta,
                             double* out, cudaStream_t st);
 void launch_piola_assemble(const PiolaArgs& a, int grid, cudaStream_t st);
+// GEMM form for component-separable bases (tphi / tdiv: np x n tables in the
+// component-sorted dof order perm; n % 12 == 0)
+bool piola_gemm_supported(int n, int np);
+void launch_piola_gemm(const PiolaArgs& a, const double* tphi, const double* tdiv, const int* perm, int grid,
+                       cudaStream_t st);
 // device pcg (kern_pcg.cu) on a CSR matrix with int32 (ci32) or int64 (ci64) columns
 hdr_status pcg_device(int64_t n, const int64_t* ro, const int32_t* ci32, const int64_t* ci64, const double* vals,
                       const double* b, double* x, double rtol, int64_t maxit, int precond, double* hist,
