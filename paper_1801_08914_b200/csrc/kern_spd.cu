@@ -4,19 +4,22 @@
 // for element blocks that are SPD (every A_T = alpha D_T + beta M_T is).
 //
 // One 384-thread CTA per element (persistent), everything in shared memory:
-//   W   n x n, column-major (ld odd): the block in the [i | b] order, factored in
-//       place as A = L D L^T (unscaled columns, one barrier per step; pivots are
-//       checked with the reference's SingularBlock rule, dense.cpp:61-97: the
-//       first ni pivots against 1e-14 max|A_ii|, the rest against 1e-14 max|S_b|)
+//   W   n x n: the block in the [i | b] order (its lower triangle, mirrored),
+//       swept in place by pivot blocks of <= 8 (block Gauss-Jordan in the
+//       symmetric "sweep" form: W -> -A^-1, symmetric at every step).  The
+//       scalar pivots are the LDL^T pivots and are checked with the reference's
+//       SingularBlock rule (dense.cpp:61-97): the first ni against 1e-14
+//       max|A_ii|, the rest against 1e-14 max|S_b| (a block boundary at ni,
+//       where the unswept block is exactly S_b)
 //   Z   n x nc: Z = A^-1 [C_T^T | f_T]
-//   R   n x nc: residuals / corrections
-// The fp64 factorization is only a preconditioner: A_T is ill conditioned
-// (alpha / beta up to 1e6, h^-2), so Z is refined with residuals B - A Z whose
-// products are exact (two_prod) and whose sums are compensated (two_sum), until
-// the correction times its observed contraction rate is below 2^-55 of |Z|.
-// This gives the element-exact H_e = C_b Z, g_e like the reference's own
-// double-double oracle (src/reference.cpp:137-235), at about a quarter of the
-// work of kern_alg.cu's general LU + double-double solution.
+//   R   n x nc: right-hand sides / residuals
+// The fp64 inverse is only a preconditioner: A_T is ill conditioned (alpha /
+// beta up to 1e6, h^-2), so Z is refined with residuals B - A Z whose products
+// are exact (two_prod) and whose sums are compensated (two_sum), until the
+// correction times its observed contraction rate is below 2^-47 of |Z|.  This
+// gives the element-exact H_e = C_b Z, g_e like the reference's own
+// double-double oracle (src/reference.cpp:137-235).  Every product here is a
+// 4 x 4 register-tiled GEMM over shared memory (128-bit loads).
 #include <algorithm>
 
 #include "hdr_device.cuh"
@@ -26,181 +29,38 @@ namespace hdr {
 
 namespace {
 
+#ifdef HDR_SPD_TIMING  // phase cycle counters of CTA 0 (variant builds only: make EXTRA=-DHDR_SPD_TIMING)
+__device__ unsigned long long g_spd_prof[16];
+#define SPD_T(slot)                                                         \
+  do {                                                                      \
+    if (blockIdx.x == 0 && threadIdx.x == 0) {                              \
+      const long long now_ = clock64();                                     \
+      g_spd_prof[slot] += static_cast<unsigned long long>(now_ - t_last_); \
+      t_last_ = now_;                                                       \
+    }                                                                       \
+  } while (0)
+#else
+#define SPD_T(slot) \
+  do {              \
+  } while (0)
+#endif
+
 constexpr int kST = 384;
 constexpr int kSW = kST / 32;
 
 struct SpdSmem {
-  double* W;
-  double* Z;
-  double* R;
-  double* dinv;
+  double* W;   // n x ld
+  double* Z;   // n x ldz
+  double* R;   // n x ldz
+  double* T;   // 8 x ld: A_iB P^-1 of the current pivot block
+  double* C;   // 8 x ld: A_iB (the block's columns before the step)
+  double* P;   // 2 x 8 x 8: swept pivot blocks (-P^-1), double-buffered
+  double* piv; // n scalar pivots
   double* red;
   int* sidx;
   int* flag;
   int ld, ldz;
 };
-
-// L (unit lower, scaled in place; the diagonal of W keeps the pivots d) ->
-// L^-1 in place, by blocks of 8 columns from the right:
-//   Ib = L_bb^-1;  T = L[rest, b] Ib;  Linv[rest, b] = -Linv[rest, rest] T.
-// T: scratch of >= 8 (n - 8) doubles; Ib: 64 doubles.
-__device__ void tri_invert(int n, double* W, int ld, double* T, double* Ib) {
-  const int tid = threadIdx.x;
-  for (int jb = ((n - 1) / 8) * 8; jb >= 0; jb -= 8) {
-    const int je = min(jb + 8, n), w = je - jb, rest = n - je;
-    if (tid < w) {  // column tid of L_bb^-1 (unit lower), forward substitution
-      double x[8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        double v = (i == tid) ? 1.0 : 0.0;
-#pragma unroll
-        for (int k = 0; k < i; ++k)
-          if (i > tid && k >= tid && i < w) v = fma(-W[(jb + k) * ld + jb + i], x[k], v);
-        x[i] = v;
-      }
-#pragma unroll
-      for (int i = 0; i < 8; ++i) Ib[i * 8 + tid] = x[i];
-    }
-    __syncthreads();
-    for (int t = tid; t < rest * 8; t += kST) {  // T = L[rest, b] Ib  (w == 8 whenever rest > 0)
-      const int i = je + (t >> 3), c = t & 7;
-      double acc = W[(jb + c) * ld + i];
-      for (int k = c + 1; k < 8; ++k) acc = fma(W[(jb + k) * ld + i], Ib[k * 8 + c], acc);
-      T[t] = acc;
-    }
-    __syncthreads();
-    for (int t = tid; t < rest * 8; t += kST) {  // Linv[rest, b] = -Linv[rest, rest] T
-      const int ii = t >> 3, c = t & 7, i = je + ii;
-      double acc = T[t];
-      for (int kk = 0; kk < ii; ++kk) acc = fma(W[(je + kk) * ld + i], T[kk * 8 + c], acc);
-      W[(jb + c) * ld + i] = -acc;
-    }
-    for (int t = tid; t < w * w; t += kST) {
-      const int i = t / w, c = t - (t / w) * w;
-      if (i > c) W[(jb + c) * ld + jb + i] = Ib[i * 8 + c];
-    }
-    __syncthreads();
-  }
-}
-
-// Register tiles of TM rows x TN columns over n x nc outputs.  The triangular
-// products are load-balanced by giving each thread the row-tile pair (t, last - t)
-// (n = 108, nc = 55 -> 378 pairs).
-constexpr int TM = 2, TN = 4;
-
-// acc = Linv[r0:r0+TM, :] Y[:, c0:c0+TN]  (Linv unit lower in W)
-__device__ __forceinline__ void lower_tile(int n, const double* W, int ld, const double* Y, int ldy, int r0, int c0,
-                                           double (&acc)[TM][TN]) {
-#pragma unroll
-  for (int a = 0; a < TM; ++a)
-#pragma unroll
-    for (int b = 0; b < TN; ++b) acc[a][b] = 0.0;
-#pragma unroll 4
-  for (int k = 0; k < r0; ++k) {
-    const double2 yv0 = *reinterpret_cast<const double2*>(Y + k * ldy + c0);
-    const double2 yv1 = *reinterpret_cast<const double2*>(Y + k * ldy + c0 + 2);
-    const double yv[TN] = {yv0.x, yv0.y, yv1.x, yv1.y};
-    double lv[TM];
-#pragma unroll
-    for (int a = 0; a < TM; ++a) lv[a] = W[k * ld + r0 + a];
-#pragma unroll
-    for (int a = 0; a < TM; ++a)
-#pragma unroll
-      for (int b = 0; b < TN; ++b) acc[a][b] = fma(lv[a], yv[b], acc[a][b]);
-  }
-#pragma unroll
-  for (int kk = 0; kk < TM; ++kk) {
-    const int k = r0 + kk;
-    if (k >= n) break;
-    double yv[TN];
-#pragma unroll
-    for (int b = 0; b < TN; ++b) yv[b] = Y[k * ldy + c0 + b];
-#pragma unroll
-    for (int a = kk; a < TM; ++a) {
-      const double l = (a == kk) ? 1.0 : W[k * ld + r0 + a];
-#pragma unroll
-      for (int b = 0; b < TN; ++b) acc[a][b] = fma(l, yv[b], acc[a][b]);
-    }
-  }
-}
-
-// acc = Linv^T[r0:r0+TM, :] Y[:, c0:c0+TN]
-__device__ __forceinline__ void upper_tile(int n, const double* W, int ld, const double* Y, int ldy, int r0, int c0,
-                                           double (&acc)[TM][TN]) {
-#pragma unroll
-  for (int a = 0; a < TM; ++a)
-#pragma unroll
-    for (int b = 0; b < TN; ++b) acc[a][b] = 0.0;
-#pragma unroll
-  for (int kk = 0; kk < TM; ++kk) {
-    const int k = r0 + kk;
-    if (k >= n) break;
-    double yv[TN];
-#pragma unroll
-    for (int b = 0; b < TN; ++b) yv[b] = Y[k * ldy + c0 + b];
-#pragma unroll
-    for (int a = 0; a <= kk; ++a) {
-      const double l = (a == kk) ? 1.0 : W[(r0 + a) * ld + k];
-#pragma unroll
-      for (int b = 0; b < TN; ++b) acc[a][b] = fma(l, yv[b], acc[a][b]);
-    }
-  }
-#pragma unroll 4
-  for (int k = r0 + TM; k < n; ++k) {
-    const double2 yv0 = *reinterpret_cast<const double2*>(Y + k * ldy + c0);
-    const double2 yv1 = *reinterpret_cast<const double2*>(Y + k * ldy + c0 + 2);
-    const double yv[TN] = {yv0.x, yv0.y, yv1.x, yv1.y};
-    double lv[TM];
-#pragma unroll
-    for (int a = 0; a < TM; ++a) lv[a] = W[(r0 + a) * ld + k];
-#pragma unroll
-    for (int a = 0; a < TM; ++a)
-#pragma unroll
-      for (int b = 0; b < TN; ++b) acc[a][b] = fma(lv[a], yv[b], acc[a][b]);
-  }
-}
-
-// the (up to) two row tiles and the column tile of work unit u
-struct PairTiles {
-  int r0a, r0b, c0;  // r0b < 0: single tile
-  bool ok;
-};
-__device__ __forceinline__ PairTiles pair_tiles(int u, int n, int nc) {
-  const int tn = (nc + TN - 1) / TN, nrt = (n + TM - 1) / TM, npair = (nrt + 1) / 2;
-  PairTiles p;
-  p.ok = u < npair * tn;
-  const int pr = u / tn;
-  p.c0 = (u - pr * tn) * TN;
-  p.r0a = pr * TM;
-  p.r0b = (nrt - 1 - pr) != pr ? (nrt - 1 - pr) * TM : -1;
-  return p;
-}
-
-template <class F>
-__device__ __forceinline__ void store_tile(int n, int nc, int r0, int c0, const double (&acc)[TM][TN], F f) {
-#pragma unroll
-  for (int a = 0; a < TM; ++a)
-#pragma unroll
-    for (int b = 0; b < TN; ++b)
-      if (r0 + a < n && c0 + b < nc) f(r0 + a, c0 + b, acc[a][b]);
-}
-
-// Y <- D^-1 Linv Y in place (two-phase: products to registers, barrier, store)
-__device__ void lower_inplace(int n, int nc, const double* W, int ld, const double* dinv, double* Y, int ldy) {
-  const PairTiles p = pair_tiles(threadIdx.x, n, nc);
-  double acc0[TM][TN], acc1[TM][TN];
-  if (p.ok) {
-    lower_tile(n, W, ld, Y, ldy, p.r0a, p.c0, acc0);
-    if (p.r0b >= 0) lower_tile(n, W, ld, Y, ldy, p.r0b, p.c0, acc1);
-  }
-  __syncthreads();
-  if (p.ok) {
-    auto st = [&](int i, int c, double v) { Y[i * ldy + c] = v * dinv[i]; };
-    store_tile(n, nc, p.r0a, p.c0, acc0, st);
-    if (p.r0b >= 0) store_tile(n, nc, p.r0b, p.c0, acc1, st);
-  }
-  __syncthreads();
-}
 
 // block max of two values at once
 __device__ void blk_max2(double& v0, double& v1, double* red) {
@@ -222,6 +82,127 @@ __device__ void blk_max2(double& v0, double& v1, double* red) {
   for (int w = 1; w < kSW; ++w) {
     v0 = fmax(v0, red[w]);
     v1 = fmax(v1, red[kSW + w]);
+  }
+}
+
+// One warp: sweep the 8 x 8 block P (row-major; a w x w pivot block padded with
+// the identity) in registers, P <- -P^-1.  Lane l holds (l/8, l%8) and
+// (l/8 + 4, l%8).  The scalar pivots go to piv[0, w) (checked later).
+__device__ void sweep8(double* P, int w, double* piv) {
+  const int lane = threadIdx.x & 31, r = lane >> 3, c = lane & 7;
+  double v0 = P[r * 8 + c], v1 = P[(r + 4) * 8 + c];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const double akk = __shfl_sync(0xffffffffu, k < 4 ? v0 : v1, ((k & 3) << 3) | k);
+    const double aik0 = __shfl_sync(0xffffffffu, v0, (r << 3) | k);
+    const double aik1 = __shfl_sync(0xffffffffu, v1, (r << 3) | k);
+    const double akj = __shfl_sync(0xffffffffu, k < 4 ? v0 : v1, ((k & 3) << 3) | c);
+    if (lane == 0 && k < w) piv[k] = akk;
+    // reciprocal for the preconditioner (refinement absorbs its last-bit error):
+    // fp32 seed + two Newton steps
+    double inv = static_cast<double>(__frcp_rn(static_cast<float>(akk)));
+    inv = inv * fma(-akk, inv, 2.0);
+    inv = inv * fma(-akk, inv, 2.0);
+    auto upd = [&](int i, double v, double aik) {
+      if (i == k) return c == k ? -inv : akj * inv;
+      if (c == k) return aik * inv;
+      return fma(-aik * inv, akj, v);
+    };
+    v0 = upd(r, v0, aik0);
+    v1 = upd(r + 4, v1, aik1);
+  }
+  P[r * 8 + c] = v0;
+  P[(r + 4) * 8 + c] = v1;
+}
+
+// warp 0: the pivot block [kb, kb + w) of W (padded with the identity) -> P, swept
+__device__ void load_sweep(const double* W, int ld, int kb, int w, double* P, double* piv) {
+  for (int t = threadIdx.x & 31; t < 64; t += 32) {
+    const int r = t >> 3, c = t & 7;
+    const int hi = r > c ? r : c, lo = r > c ? c : r;  // lower triangle holds the block
+    P[t] = (r < w && c < w) ? W[(kb + hi) * ld + kb + lo] : (r == c ? 1.0 : 0.0);
+  }
+  __syncwarp();
+  sweep8(P, w, piv + kb);
+  __syncwarp();
+}
+
+__device__ __forceinline__ int block_end(int kb, int n, int ni) { return min(kb + 8, (kb < ni) ? ni : n); }
+
+// lower 4 x 4 tile index t -> (ti, tj), tj <= ti
+__device__ __forceinline__ void tri_tile(int t, int& ti, int& tj) {
+  ti = static_cast<int>((sqrtf(8.f * t + 1.f) - 1.f) * 0.5f);
+  while ((ti + 1) * (ti + 2) / 2 <= t) ++ti;
+  while (ti * (ti + 1) / 2 > t) --ti;
+  tj = t - ti * (ti + 1) / 2;
+}
+
+// W[i][j] -= sum_k T[k][i] C[k][j] for the tile's (i, j) outside B, i >= j
+// (lower triangle only; C = the block's columns before the step, T = C P^-1)
+__device__ __forceinline__ void sweep_tile(double* W, int ld, const double* T, const double* C, int n, int kb, int ke,
+                                           int ti, int tj) {
+  const int i0 = 4 * ti, j0 = 4 * tj, w = ke - kb;
+  double cur[4][4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {  // the tile's current values, early (latency)
+    const double2 a0 = *reinterpret_cast<const double2*>(W + (i0 + r) * ld + j0);
+    const double2 a1 = *reinterpret_cast<const double2*>(W + (i0 + r) * ld + j0 + 2);
+    cur[r][0] = a0.x;
+    cur[r][1] = a0.y;
+    cur[r][2] = a1.x;
+    cur[r][3] = a1.y;
+  }
+  double acc[4][4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) acc[r][c] = 0.0;
+#pragma unroll 4
+  for (int k = 0; k < w; ++k) {
+    const double2 t0 = *reinterpret_cast<const double2*>(T + k * ld + i0);
+    const double2 t1 = *reinterpret_cast<const double2*>(T + k * ld + i0 + 2);
+    const double2 c0v = *reinterpret_cast<const double2*>(C + k * ld + j0);
+    const double2 c1v = *reinterpret_cast<const double2*>(C + k * ld + j0 + 2);
+    const double tv[4] = {t0.x, t0.y, t1.x, t1.y}, cv[4] = {c0v.x, c0v.y, c1v.x, c1v.y};
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) acc[r][c] = fma(tv[r], cv[c], acc[r][c]);
+  }
+  const bool full = i0 + 4 <= n && (ti != tj) && !(i0 + 4 > kb && i0 < ke) && !(j0 + 4 > kb && j0 < ke);
+  if (full) {
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      *reinterpret_cast<double2*>(W + (i0 + r) * ld + j0) = make_double2(cur[r][0] - acc[r][0], cur[r][1] - acc[r][1]);
+      *reinterpret_cast<double2*>(W + (i0 + r) * ld + j0 + 2) =
+          make_double2(cur[r][2] - acc[r][2], cur[r][3] - acc[r][3]);
+    }
+  } else {
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int i = i0 + r, j = j0 + c;
+        if (i >= n || j > i || (i >= kb && i < ke) || (j >= kb && j < ke)) continue;
+        W[i * ld + j] = cur[r][c] - acc[r][c];
+      }
+  }
+}
+
+// acc (+)= sign * W[i0:i0+4, :] Y[:, c0:c0+4] over k < n (W symmetric: read as rows)
+__device__ __forceinline__ void gemm_tile(int n, const double* W, int ld, const double* Y, int ldy, int i0, int c0,
+                                          double (&acc)[4][4]) {
+#pragma unroll 2
+  for (int k = 0; k < n; ++k) {
+    const double2 w0 = *reinterpret_cast<const double2*>(W + k * ld + i0);
+    const double2 w1 = *reinterpret_cast<const double2*>(W + k * ld + i0 + 2);
+    const double2 y0 = *reinterpret_cast<const double2*>(Y + k * ldy + c0);
+    const double2 y1 = *reinterpret_cast<const double2*>(Y + k * ldy + c0 + 2);
+    const double wv[4] = {w0.x, w0.y, w1.x, w1.y}, yv[4] = {y0.x, y0.y, y1.x, y1.y};
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) acc[a][b] = fma(wv[a], yv[b], acc[a][b]);
   }
 }
 
@@ -251,7 +232,7 @@ __device__ void residual(int n, int nc, const double* A, const SpdSmem& s, const
 #pragma unroll
       for (int a = 0; a < TM; ++a) av[a] = -__ldg(arow[a] + cj);
 #pragma unroll
-      for (int b = 0; b < TN; ++b) zv[b] = s.Z[j * s.ldz + c0 + b];  // padded columns hold 0
+      for (int b = 0; b < TN; ++b) zv[b] = s.Z[j * s.ldz + c0 + b];
 #pragma unroll
       for (int a = 0; a < TM; ++a)
 #pragma unroll
@@ -274,18 +255,26 @@ __device__ void residual(int n, int nc, const double* A, const SpdSmem& s, const
 __global__ void __launch_bounds__(kST, 1) k_spd_hyb(AlgArgs a, double* gws, int64_t slot, int nmax, int ncmax) {
   extern __shared__ __align__(16) double smem[];
   SpdSmem s;
-  s.ld = nmax | 1;
-  s.ldz = (ncmax + 1) & ~1;
+  s.ld = (nmax + 1) & ~1;
+  s.ldz = (ncmax + 3) & ~3;
   s.W = smem;
-  s.Z = s.W + ((nmax * s.ld + 1) & ~1);
+  s.Z = s.W + nmax * s.ld;
   s.R = s.Z + nmax * s.ldz;
-  s.dinv = s.R + max(nmax * s.ldz, 8 * nmax + 64);
-  s.red = s.dinv + nmax;
+  s.T = s.R + nmax * s.ldz;
+  s.C = s.T + 8 * s.ld;
+  s.P = s.C + 8 * s.ld;
+  s.piv = s.P + 128;
+  s.red = s.piv + nmax;
   s.sidx = reinterpret_cast<int*>(s.red + 2 * kSW);
   s.flag = s.sidx + nmax;
   double* Bg = gws + static_cast<int64_t>(blockIdx.x) * slot;  // n x ldz right-hand sides
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int ld = s.ld, ldz = s.ldz;
+#ifdef HDR_SPD_TIMING
+  long long t_last_ = clock64();
+#endif
   for (int64_t e = blockIdx.x; e < a.ne; e += gridDim.x) {
+    SPD_T(0);
     const int64_t boff = a.boff[e];
     const int n = static_cast<int>(a.boff[e + 1] - boff), ni = a.ni[e];
     const int64_t g0 = a.goff[e];
@@ -293,105 +282,134 @@ __global__ void __launch_bounds__(kST, 1) k_spd_hyb(AlgArgs a, double* gws, int6
     const double* A = a.blocks + a.aoff[e];
     for (int i = tid; i < n; i += kST) s.sidx[i] = a.idx[boff + i];
     __syncthreads();
-    // permuted block, column-major; max |A_ii|
+    // permuted block: lower triangle, mirrored; max |A_ii|
     double mx = 0.0;
-    for (int t = tid; t < n * n; t += kST) {
-      const int i = t / n, k = t - i * n;  // consecutive threads: consecutive columns of row i
-      const double v = __ldg(A + static_cast<int64_t>(s.sidx[i]) * n + s.sidx[k]);
-      s.W[k * s.ld + i] = v;
-      if (ni == 0 || (i < ni && k < ni)) mx = fmax(mx, fabs(v));
+    for (int t0 = tid; t0 < n * n; t0 += 4 * kST) {  // 4 loads in flight per thread
+      double v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int t = t0 + u * kST, i = t / n, k = t - i * n;
+        v[u] = (t < n * n && k <= i) ? __ldg(A + static_cast<int64_t>(s.sidx[i]) * n + s.sidx[k]) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int t = t0 + u * kST, i = t / n, k = t - i * n;
+        if (t >= n * n || k > i) continue;
+        s.W[i * ld + k] = v[u];
+        if (ni == 0 || i < ni) mx = fmax(mx, fabs(v[u]));
+      }
     }
     // right-hand sides [C_T^T | f_T] (global slot, row-major n x ldz, padding 0)
-    for (int t = tid; t < n * s.ldz; t += kST) {
-      const int i = t / s.ldz, c = t - i * s.ldz;
+    for (int t = tid; t < n * ldz; t += kST) {
+      const int i = t / ldz, c = t - i * ldz;
       Bg[t] = c == nr ? a.f[boff + s.sidx[i]] : 0.0;
     }
     double dummy0 = 0.0;
     blk_max2(mx, dummy0, s.red);
     double thr = 1e-14 * mx;
     for (int64_t q = a.cptr[g0] + tid; q < a.cptr[g0 + nr]; q += kST)
-      Bg[a.cent_a[q] * s.ldz + a.cent_r[q]] = a.cent_v[q];
-    // ---- A = L D L^T, right-looking by panels of <= 8 columns (a panel
-    // boundary at ni, where the trailing matrix is exactly S_b):
-    //   1. warp 0 factors the panel's diagonal block (pivot checks)
-    //   2. rows below the block: their panel columns (one thread per row)
-    //   3. trailing lower triangle -= (panel) D^-1 (panel)^T, 4 x 4 register tiles
-    int fail = 0;
+      Bg[a.cent_a[q] * ldz + a.cent_r[q]] = a.cent_v[q];
+    SPD_T(1);
+    // ---- sweep: W -> -A^-1 by pivot blocks B = [kb, kb + w).  Look-ahead:
+    // warp 0 updates the next pivot block's tiles first and sweeps it while
+    // the other warps finish the trailing update.  Pivots are checked at the end.
+    const int nb4 = (n + 3) / 4, ntl = nb4 * (nb4 + 1) / 2;
+    double thr2 = thr;
+    if (warp == 0) load_sweep(s.W, ld, 0, block_end(0, n, ni), s.P, s.piv);
+    __syncthreads();
+    int cur = 0;
     for (int kb = 0; kb < n;) {
-      const int ke = min(kb + 8, (kb < ni) ? ni : n);
-      if (kb == ni && ni > 0) {  // Schur block S_b = trailing matrix: its own threshold
-        double m2 = 0.0, dummy = 0.0;
-        const int w = n - kb;
-        for (int t = tid; t < w * w; t += kST) {
-          const int i = t / w, j = t - i * w;
-          if (j <= i) m2 = fmax(m2, fabs(s.W[(kb + j) * s.ld + kb + i]));
+      const int ke = block_end(kb, n, ni), w = ke - kb;
+      const int kn = ke < n ? block_end(ke, n, ni) : ke;  // next block [ke, kn)
+      const double* P = s.P + 64 * cur;
+      // C[m][i] = A_i,kb+m (lower triangle), T[k][i] = (A_iB P^-1)_k = -sum_m C[m][i] Sw[m][k]  (i outside B)
+      for (int t = tid; t < w * n; t += kST) {
+        const int k = t / n, i = t - k * n;
+        if (i >= kb && i < ke) continue;
+        double acc = 0.0;
+        for (int m = 0; m < w; ++m) {
+          const double c = (i > kb + m) ? s.W[i * ld + kb + m] : s.W[(kb + m) * ld + i];
+          if (k == 0) s.C[m * ld + i] = c;
+          acc = fma(c, P[m * 8 + k], acc);
         }
-        blk_max2(m2, dummy, s.red);
-        thr = 1e-14 * m2;
+        s.T[k * ld + i] = -acc;
       }
+      __syncthreads();
+      SPD_T(2);
+      // trailing update over the tiles not inside B (tile rows/cols tb0..tb1-1
+      // lie fully in B); the tiles touching the next pivot block go to warp 0
+      const int a0 = ke >> 2, a1 = (kn - 1) >> 2;  // tile rows of the next block
+      const int tb0 = (kb + 3) >> 2, tb1 = max(tb0, ke >> 2), nskip = tb1 - tb0;
+      const int nr4 = nb4 - nskip, ntr = nr4 * (nr4 + 1) / 2;
+#ifdef HDR_SPD_TIMING
+      const long long tw0 = clock64();
+#endif
       if (warp == 0) {
-        int f = 0;
-        for (int k = kb; k < ke; ++k) {
-          const double d = s.W[k * s.ld + k];
-          if (!(d > thr)) {
-            f = (fabs(d) > thr) ? 4 : 2;  // 4: not positive definite, 2: singular
-            break;
-          }
-          const double dk = 1.0 / d;
-          if (lane == 0) s.dinv[k] = dk;
-          const int w = ke - k - 1;
-          for (int t = lane; t < w * w; t += 32) {
-            const int i = k + 1 + t / w, j = k + 1 + t % w;
-            if (j <= i) s.W[j * s.ld + i] = fma(-s.W[k * s.ld + i], s.W[k * s.ld + j] * dk, s.W[j * s.ld + i]);
+        if (kn > ke) {
+          const int nt = a1 - a0 + 1;
+          for (int q = threadIdx.x; q < nt * (nt + 1) / 2; q += 32) {
+            int qi, qj;
+            tri_tile(q, qi, qj);
+            sweep_tile(s.W, ld, s.T, s.C, n, kb, ke, a0 + qi, a0 + qj);
           }
           __syncwarp();
+#ifdef HDR_SPD_TIMING
+          if (blockIdx.x == 0 && threadIdx.x == 0) g_spd_prof[11] += clock64() - tw0;
+#endif
+          load_sweep(s.W, ld, ke, kn - ke, s.P + 64 * (cur ^ 1), s.piv);
+#ifdef HDR_SPD_TIMING
+          if (blockIdx.x == 0 && threadIdx.x == 0) g_spd_prof[12] += clock64() - tw0;
+#endif
         }
-        if (lane == 0) *s.flag = f;
+      } else {
+        for (int t = tid - 32; t < ntr; t += kST - 32) {
+          int ti, tj;
+          tri_tile(t, ti, tj);
+          ti += (ti >= tb0) ? nskip : 0;
+          tj += (tj >= tb0) ? nskip : 0;
+          if (kn > ke && ti >= a0 && ti <= a1 && tj >= a0 && tj <= a1) continue;
+          sweep_tile(s.W, ld, s.T, s.C, n, kb, ke, ti, tj);
+        }
+#ifdef HDR_SPD_TIMING
+        if (blockIdx.x == 0 && threadIdx.x == 32) g_spd_prof[13] += clock64() - tw0;
+#endif
       }
       __syncthreads();
-      fail = *s.flag;
-      if (fail) break;
-      for (int i = ke + tid; i < n; i += kST)
-        for (int k = kb; k < ke; ++k) {
-          const double c = s.W[k * s.ld + i] * s.dinv[k];
-          for (int j = k + 1; j < ke; ++j) s.W[j * s.ld + i] = fma(-c, s.W[k * s.ld + j], s.W[j * s.ld + i]);
+      SPD_T(3);
+      for (int t = tid; t < w * n; t += kST) {
+        const int k = t / n, i = t - k * n, col = kb + k;
+        if (i < col) s.W[col * ld + i] = (i >= kb) ? P[k * 8 + (i - kb)] : s.T[k * ld + i];
+        else s.W[i * ld + col] = (i < ke) ? P[(i - kb) * 8 + k] : s.T[k * ld + i];
+      }
+      if (ke == ni && ni > 0) {  // the unswept block is now S_b: its own threshold
+        double m2 = 0.0, dummy = 0.0;
+        const int m = n - ke;
+        for (int t = tid; t < m * m; t += kST) {
+          const int i = t / m, j = t - i * m;
+          if (j <= i) m2 = fmax(m2, fabs(s.W[(ke + i) * ld + ke + j]));
         }
-      __syncthreads();
-      {
-        const int m = n - ke, tb = (m + 3) / 4, nt = tb * (tb + 1) / 2, w = ke - kb;
-        for (int t = tid; t < nt; t += kST) {
-          int ti = static_cast<int>((sqrtf(8.f * t + 1.f) - 1.f) * 0.5f);
-          while ((ti + 1) * (ti + 2) / 2 <= t) ++ti;
-          while (ti * (ti + 1) / 2 > t) --ti;
-          const int tj = t - ti * (ti + 1) / 2;
-          const int i0 = ke + 4 * ti, j0 = ke + 4 * tj;
-          double acc[4][4];
-#pragma unroll
-          for (int r = 0; r < 4; ++r)
-#pragma unroll
-            for (int c = 0; c < 4; ++c) acc[r][c] = 0.0;
-          for (int k = kb; k < kb + w; ++k) {
-            const double dk = s.dinv[k];
-            double pi[4], pj[4];
-#pragma unroll
-            for (int r = 0; r < 4; ++r) {
-              pi[r] = (i0 + r < n) ? s.W[k * s.ld + i0 + r] : 0.0;
-              pj[r] = (j0 + r < n) ? s.W[k * s.ld + j0 + r] * dk : 0.0;
-            }
-#pragma unroll
-            for (int r = 0; r < 4; ++r)
-#pragma unroll
-              for (int c = 0; c < 4; ++c) acc[r][c] = fma(pi[r], pj[c], acc[r][c]);
-          }
-#pragma unroll
-          for (int r = 0; r < 4; ++r)
-#pragma unroll
-            for (int c = 0; c < 4; ++c)
-              if (i0 + r < n && j0 + c <= i0 + r) s.W[(j0 + c) * s.ld + i0 + r] -= acc[r][c];
-        }
+        blk_max2(m2, dummy, s.red);
+        thr2 = 1e-14 * m2;
       }
       __syncthreads();
+      SPD_T(4);
+      cur ^= 1;
       kb = ke;
+    }
+    for (int t = tid; t < n * n; t += kST) {  // the full matrix for the products below
+      const int i = t / n, j = t - i * n;
+      if (j > i) s.W[i * ld + j] = s.W[j * ld + i];
+    }
+    // pivot checks (the reference's SingularBlock rule)
+    int fail = 0;
+    for (int k = tid; k < n; k += kST) {
+      const double d = s.piv[k], t2 = (k < ni || ni == 0) ? thr : thr2;
+      if (!(d > t2)) fail = max(fail, (fabs(d) > t2) ? 4 : 2);
+    }
+    {
+      double f0 = fail, dummy = 0.0;
+      blk_max2(f0, dummy, s.red);
+      fail = static_cast<int>(f0);
     }
     if (fail) {
       if (tid == 0) {
@@ -401,60 +419,80 @@ __global__ void __launch_bounds__(kST, 1) k_spd_hyb(AlgArgs a, double* gws, int6
       __syncthreads();
       continue;
     }
-    // ---- L (unit) and L^-1 in place; R is the scratch of the inversion
-    for (int k = warp; k < n; k += kSW) {
-      const double dk = s.dinv[k];
-      for (int i = k + 1 + lane; i < n; i += 32) s.W[k * s.ld + i] *= dk;
-    }
+    SPD_T(5);
+    // ---- Z = A^-1 B = -W B, refined with exact residuals; one 4 x 4 tile per thread
+    const int tn = (nc + 3) / 4, ntz = nb4 * tn;
+    for (int t = tid; t < n * ldz; t += kST) s.R[t] = Bg[t];
+    bool unit = a.cptr[g0 + nr] - a.cptr[g0] == nr;  // one entry per row: C_T^T columns are (scaled) unit vectors
     __syncthreads();
-    tri_invert(n, s.W, s.ld, s.R, s.R + 8 * nmax);
-    // ---- Z = A^-1 B = Linv^T D^-1 Linv B, refined with exact residuals
-    const PairTiles pt = pair_tiles(tid, n, nc);
-    for (int t = tid; t < n * s.ldz; t += kST) s.Z[t] = Bg[t];
-    __syncthreads();
-    lower_inplace(n, nc, s.W, s.ld, s.dinv, s.Z, s.ldz);
-    if (pt.ok) {  // R = Linv^T Z
-      double acc[TM][TN];
-      auto st = [&](int i, int c, double v) { s.R[i * s.ldz + c] = v; };
-      upper_tile(n, s.W, s.ld, s.Z, s.ldz, pt.r0a, pt.c0, acc);
-      store_tile(n, nc, pt.r0a, pt.c0, acc, st);
-      if (pt.r0b >= 0) {
-        upper_tile(n, s.W, s.ld, s.Z, s.ldz, pt.r0b, pt.c0, acc);
-        store_tile(n, nc, pt.r0b, pt.c0, acc, st);
+    if (unit) {  // Z[:, r] = -W[:, a_r] v_r (exact), Z[:, nr] = -W f
+      for (int t = tid; t < n * nr; t += kST) {
+        const int r = t / n, i = t - r * n;
+        const int64_t q = a.cptr[g0 + r];
+        s.Z[i * ldz + a.cent_r[q]] = -s.W[a.cent_a[q] * ld + i] * a.cent_v[q];
+      }
+      for (int i = tid; i < n; i += kST) {
+        double acc = 0.0;
+        for (int k = 0; k < n; ++k) acc = fma(s.W[k * ld + i], s.R[k * ldz + nr], acc);
+        s.Z[i * ldz + nr] = -acc;
+        for (int c = nc; c < ldz; ++c) s.Z[i * ldz + c] = 0.0;
+      }
+    } else {
+      for (int t = tid; t < ntz; t += kST) {
+        const int i0 = (t / tn) * 4, c0 = (t % tn) * 4;
+        double acc[4][4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) acc[r][c] = 0.0;
+        gemm_tile(n, s.W, ld, s.R, ldz, i0, c0, acc);
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+            if (i0 + r < n) s.Z[(i0 + r) * ldz + c0 + c] = (c0 + c < nc) ? -acc[r][c] : 0.0;
       }
     }
     __syncthreads();
-    for (int t = tid; t < n * s.ldz; t += kST) s.Z[t] = (t % s.ldz < nc) ? s.R[t] : 0.0;
-    __syncthreads();
+    SPD_T(6);
     double prev = 0.0;
     for (int step = 0; step < 6; ++step) {
       residual(n, nc, A, s, Bg);
       __syncthreads();
-      lower_inplace(n, nc, s.W, s.ld, s.dinv, s.R, s.ldz);
+      SPD_T(7);
+#ifdef HDR_SPD_TIMING
+      if (blockIdx.x == 0 && threadIdx.x == 0) g_spd_prof[15] += 1;  // residual count
+#endif
       double cm = 0.0, zm = 0.0;
-      if (pt.ok) {  // Z += Linv^T R
-        double acc[TM][TN];
-        auto st = [&](int i, int c, double v) {
-          const int o = i * s.ldz + c;
-          const double z = s.Z[o] + v;
-          s.Z[o] = z;
-          cm = fmax(cm, fabs(v));
-          zm = fmax(zm, fabs(z));
-        };
-        upper_tile(n, s.W, s.ld, s.R, s.ldz, pt.r0a, pt.c0, acc);
-        store_tile(n, nc, pt.r0a, pt.c0, acc, st);
-        if (pt.r0b >= 0) {
-          upper_tile(n, s.W, s.ld, s.R, s.ldz, pt.r0b, pt.c0, acc);
-          store_tile(n, nc, pt.r0b, pt.c0, acc, st);
-        }
+      for (int t = tid; t < ntz; t += kST) {  // Z -= W R
+        const int i0 = (t / tn) * 4, c0 = (t % tn) * 4;
+        double acc[4][4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) acc[r][c] = 0.0;
+        gemm_tile(n, s.W, ld, s.R, ldz, i0, c0, acc);
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+            if (i0 + r < n && c0 + c < nc) {
+              const int o = (i0 + r) * ldz + c0 + c;
+              const double z = s.Z[o] - acc[r][c];
+              s.Z[o] = z;
+              cm = fmax(cm, fabs(acc[r][c]));
+              zm = fmax(zm, fabs(z));
+            }
       }
       blk_max2(cm, zm, s.red);
       // the next correction is about rho * cm; rho = observed contraction (first
       // step: the relative size of the correction itself)
       const double rho = step > 0 ? fmin(1.0, prev > 0.0 ? cm / prev : 1.0) : (zm > 0.0 ? cm / zm : 0.0);
       prev = cm;
+      SPD_T(8);
       if (!(cm * fmax(rho, 0x1p-52) > 0x1p-47 * zm)) break;
     }
+    SPD_T(9);
     // ---- epilogue: H_e = C_b Z[:, :nr], g_e = C_b Z[:, nr]
     double* he = a.hbuf + a.hoff[e];
     double* ge = a.gbuf + g0;
@@ -472,21 +510,28 @@ __global__ void __launch_bounds__(kST, 1) k_spd_hyb(AlgArgs a, double* gws, int6
       else ge[r] = hi + lo;
     }
     __syncthreads();
+    SPD_T(10);
+#ifdef HDR_SPD_TIMING
+    if (blockIdx.x == 0 && threadIdx.x == 0) g_spd_prof[14] += 1;  // cells
+#endif
   }
 }
 
 size_t spd_smem_bytes(int nmax, int ncmax) {
-  const size_t ld = nmax | 1, ldz = (ncmax + 1) & ~1;
-  const size_t r = std::max(nmax * ldz, 8 * static_cast<size_t>(nmax) + 64);
-  return (((nmax * ld + 1) & ~size_t(1)) + nmax * ldz + r + nmax + 2 * kSW + 2) * 8 + static_cast<size_t>(nmax) * 4 + 16;
+  const size_t ld = (nmax + 1) & ~1, ldz = (ncmax + 3) & ~3;
+  return (nmax * ld + 2 * nmax * ldz + 16 * ld + 128 + nmax + 2 * kSW) * 8 + static_cast<size_t>(nmax + 2) * 4;
 }
 
 }  // namespace
 
-bool spd_supported(int nmax, int ncmax) {
-  const int units = (((nmax + TM - 1) / TM + 1) / 2) * ((ncmax + TN - 1) / TN);  // one row-tile pair per thread
-  return units <= kST && spd_smem_bytes(nmax, ncmax) <= 227 * 1024;
+#ifdef HDR_SPD_TIMING
+extern "C" int hdr_debug_spd_prof(unsigned long long* out) {
+  cudaMemcpyFromSymbol(out, g_spd_prof, sizeof(g_spd_prof));
+  return 0;
 }
+#endif
+
+bool spd_supported(int nmax, int ncmax) { return spd_smem_bytes(nmax, ncmax) <= 227 * 1024; }
 
 int64_t spd_gws_doubles(int64_t ne, int nmax, int ncmax, int* grid) {
   int dev = 0, sms = 148;
@@ -494,7 +539,7 @@ int64_t spd_gws_doubles(int64_t ne, int nmax, int ncmax, int* grid) {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   if (sms <= 0) sms = 148;
   *grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ne, sms)));
-  return static_cast<int64_t>(*grid) * nmax * ((ncmax + 1) & ~1);
+  return static_cast<int64_t>(*grid) * nmax * ((ncmax + 3) & ~3);
 }
 
 void launch_spd_hyb(const AlgArgs& a, int nmax, int ncmax, double* gws, cudaStream_t st) {
@@ -502,7 +547,7 @@ void launch_spd_hyb(const AlgArgs& a, int nmax, int ncmax, double* gws, cudaStre
   spd_gws_doubles(a.ne, nmax, ncmax, &grid);
   const size_t smem = spd_smem_bytes(nmax, ncmax);
   cudaFuncSetAttribute(k_spd_hyb, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-  k_spd_hyb<<<grid, kST, smem, st>>>(a, gws, static_cast<int64_t>(nmax) * ((ncmax + 1) & ~1), nmax, ncmax);
+  k_spd_hyb<<<grid, kST, smem, st>>>(a, gws, static_cast<int64_t>(nmax) * ((ncmax + 3) & ~3), nmax, ncmax);
   count_launch();
 }
 
