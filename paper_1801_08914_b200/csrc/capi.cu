@@ -60,6 +60,8 @@ struct hdr_space_s {
   DBuf<uint64_t> rank_tab;         // k = 0 row-rank table
   DBuf<longlong2> frs;             // k = 0 per-face {row start, row}
   DBuf<double> premat;             // k >= 2 (3D): [N0 ; X^T] column-major ((n + r) x n)
+  DBuf<double> dtab;               // k >= 2 (3D): {D, M} in the tensor-core chunk order
+  DBuf<float> etab;                // k >= 2 (3D): {E, Ma} (fp32) likewise
   Fixed fx{};
   GeomState* geom = nullptr;  // mapped (trilinear) cells: hdr_space_set_vertices
   ~hdr_space_s() {
@@ -309,6 +311,30 @@ hdr_status hdr_space_create(int dim, const int64_t cells[3], const double h[3], 
               row < n ? sp->st.N0[static_cast<size_t>(row) * n + l] : sp->st.X[static_cast<size_t>(l) * r + (row - n)];
       sp->premat.alloc(pm.size());
       CK(cudaMemcpyAsync(sp->premat.p, pm.data(), pm.size() * 8, cudaMemcpyHostToDevice, st));
+      // chunk-ordered Delta tables of the tensor-core correction (kern_cta.cu)
+      // entry order = the kernel's (chunk, iteration i, thread) order, thread
+      // (warp w, lane l) -> row 8 (g / 4) + l / 4, column 16 c + 4 (g % 4) + l % 4, g = w + 16 i
+      const int MP = (n + 127) / 128 * 128, KC = 16, nch = (n + 15) / 16, per = MP * KC / 512;
+      std::vector<double> dt(static_cast<size_t>(nch) * MP * KC * 2, 0.0);
+      std::vector<float> et(static_cast<size_t>(nch) * MP * KC * 2, 0.0f);
+      for (int c = 0; c < nch; ++c)
+        for (int i = 0; i < per; ++i)
+          for (int tid = 0; tid < 512; ++tid) {
+            const int g = tid / 32 + 16 * i, lane = tid % 32;
+            const int mrow = 8 * (g / 4) + lane / 4, col = c * KC + 4 * (g % 4) + lane % 4;
+            if (mrow >= n || col >= n) continue;
+            const size_t q = (static_cast<size_t>(c) * per + i) * 512 + tid, o = static_cast<size_t>(mrow) * n + col;
+            dt[2 * q] = sp->re.divdiv[o];
+            dt[2 * q + 1] = sp->re.mass[o];
+            et[2 * q] = static_cast<float>(sp->st.E[o]);
+            et[2 * q + 1] = static_cast<float>(sp->st.Ma[o]);
+          }
+      sp->dtab.alloc(dt.size());
+      sp->etab.alloc(et.size());
+      CK(cudaMemcpyAsync(sp->dtab.p, dt.data(), dt.size() * 8, cudaMemcpyHostToDevice, st));
+      CK(cudaMemcpyAsync(sp->etab.p, et.data(), et.size() * 4, cudaMemcpyHostToDevice, st));
+      fx.dtab = reinterpret_cast<const double2*>(sp->dtab.p);
+      fx.etab = reinterpret_cast<const float2*>(sp->etab.p);
       CK(cudaStreamSynchronize(st));
     }
     if (order == 0) {  // constant block for the register kernel: D, M, E, Ma, N0, X, lam, rho

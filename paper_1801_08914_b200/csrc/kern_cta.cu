@@ -14,6 +14,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstdlib>
+#include <type_traits>
 
 #include "hdr_device.cuh"
 #include "kernels.hpp"
@@ -34,6 +35,13 @@ struct Big {
   static constexpr int NCP = (NC + 3) & ~3;
   static constexpr int IB = (K == 3) ? 48 : 54;  // rows per block: divides N and NINT (interior / face blocks)
   static constexpr int NB = N / IB;
+  // fp64 tensor-core (DMMA m8n8k4) phase V: row strides chosen so that the 32
+  // lanes' fragment loads hit every bank pair exactly twice (2 wavefronts)
+  static constexpr int NZ = (NC + 7) / 16 * 16 + 8;  // z (RP x NZ), NZ = 8 mod 16
+  static constexpr int RP = (R + 3) & ~3;            // K of the V product, padded to the MMA's 4
+  static constexpr int RS = (RP + 11) / 16 * 16 + 4; // xi (IBP x RS), RS = 4 mod 16
+  static constexpr int IBP = (IB + 7) & ~7;          // row block padded to the MMA's 8
+
   // thread tiles: V / Y blocks (IB x NC), C (NF x NC)
   static constexpr int VT_M = (K == 3) ? 4 : 3, VT_N = (K == 3) ? 6 : 3;
   static constexpr int CT_M = (K == 3) ? 6 : 3, CT_N = (K == 3) ? 7 : 4;
@@ -53,16 +61,30 @@ struct Big {
 
 constexpr int kThreads = 512;
 
+#ifdef HDR_BIG_TIMING  // phase cycle counters of CTA 0 (variant builds only: make EXTRA=-DHDR_BIG_TIMING)
+__device__ unsigned long long g_big_prof[32];
+#define BIG_T(slot)                                                         \
+  do {                                                                      \
+    if (blockIdx.x == 0 && threadIdx.x == 0) {                              \
+      const long long now_ = clock64();                                     \
+      g_big_prof[slot] += static_cast<unsigned long long>(now_ - t_last_); \
+      t_last_ = now_;                                                       \
+    }                                                                       \
+  } while (0)
+#else
+#define BIG_T(slot) \
+  do {              \
+  } while (0)
+#endif
+
 template <int K>
 struct BigSmem {
   using B = Big<K>;
   float v32[B::N * B::NCP];
   union U {
     struct {
-      double z[B::R * B::NC];
-      double xi[B::IB * B::R];
-      float z32[B::R * B::NC];   // fp32 copies for the interior-row blocks
-      float xi32[B::IB * B::R];
+      double z[B::RP * B::NZ];
+      double xi[B::IBP * B::RS];
     } pv;
     struct {
       float dt[B::N * B::IB];  // Delta32 block transposed: dt[l * IB + ii]
@@ -100,43 +122,63 @@ __device__ __forceinline__ void tf32_split(float x, float& hi, float& lo) {
 
 // One row block [i0, i0 + IB) of [V | w] = (base + X z) / beta, register tiles
 // in T (double for the face rows, float for the interior rows).
-template <int K, class T>
-__device__ __forceinline__ void v_block(BigSmem<K>& sm, const T* xi, const T* z, const Fixed& fx, int i0, double ib,
-                                        double* vf, int tid) {
+__device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+// One row block [i0, i0 + IB) of [V | w] = (base + X z) / beta on the fp64
+// tensor cores: warp tiles of 8 rows x 8 columns, K = RP in steps of 4
+// (fragments: a = xi[row = lane/4][k = lane%4], b = z[k = lane%4][col = lane/4],
+// d = (row lane/4, cols 2 (lane%4) + {0, 1})).  Face blocks: V_FF is symmetric,
+// only tiles reaching the lower triangle are computed, the rest mirrored.
+template <int K>
+__device__ __forceinline__ void v_block(BigSmem<K>& sm, const Fixed& fx, int i0, double ib, double* vf) {
   using B = Big<K>;
-  constexpr int N = B::N, NF = B::NF, NC = B::NC, NCP = B::NCP, R = B::R, NINT = B::NINT, IB = B::IB;
-  constexpr int TM = B::VT_M, TN = B::VT_N;
-  constexpr int TMS = (IB + TM - 1) / TM, TNS = (NC + TN - 1) / TN;
-  for (int tile = tid; tile < TMS * TNS; tile += kThreads) {
-    const int m0 = (tile / TNS) * TM, n0 = (tile % TNS) * TN;
-    T acc[TM][TN];
+  constexpr int N = B::N, NF = B::NF, NC = B::NC, NCP = B::NCP, NINT = B::NINT, IB = B::IB, NZ = B::NZ, RS = B::RS;
+  constexpr int RT = B::IBP / 8, CT = (NC + 7) / 8;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const bool face = i0 >= NINT;
+  const int pb = i0 - NINT;
+  const double* xi = sm.u.pv.xi;
+  const double* z = sm.u.pv.z;
+  for (int t = warp; t < RT * CT; t += kThreads / 32) {
+    const int rt = t / CT, ct = t - rt * CT;
+    if (face && ct * 8 + 7 < NF && ct * 8 > pb + rt * 8 + 7) continue;  // strictly above the diagonal (no w column)
+    const int r = rt * 8 + (lane >> 2), c0 = ct * 8 + 2 * (lane & 3);
+    const int row = i0 + r;
+    const bool rok = r < IB;
+    double base[2];
 #pragma unroll
-    for (int i = 0; i < TM; ++i)
-#pragma unroll
-      for (int jj = 0; jj < TN; ++jj) acc[i][jj] = T(0);
-#pragma unroll 4
-    for (int j = 0; j < R; ++j) {
-      T xv[TM], zv[TN];
-#pragma unroll
-      for (int i = 0; i < TM; ++i) xv[i] = (m0 + i < IB) ? xi[(m0 + i) * R + j] : T(0);
-#pragma unroll
-      for (int jj = 0; jj < TN; ++jj) zv[jj] = (n0 + jj < NC) ? z[j * NC + n0 + jj] : T(0);
-#pragma unroll
-      for (int i = 0; i < TM; ++i)
-#pragma unroll
-        for (int jj = 0; jj < TN; ++jj) acc[i][jj] = fma(xv[i], zv[jj], acc[i][jj]);
+    for (int q = 0; q < 2; ++q) {
+      const int col = c0 + q;
+      base[q] = !rok || col >= NC ? 0.0
+                : (col < NF ? __ldg(fx.N0 + static_cast<int64_t>(row) * N + NINT + col) : sm.nf[row]);
     }
+    double d0 = 0.0, d1 = 0.0;
+    const double* ap = xi + (rt * 8 + (lane >> 2)) * RS + (lane & 3);
+    const double* bp = z + (lane & 3) * NZ + ct * 8 + (lane >> 2);
+#pragma unroll 4
+    for (int kk = 0; kk < B::RP / 4; ++kk) dmma_8x8x4(d0, d1, ap[4 * kk], bp[4 * kk * NZ]);
+    if (!rok) continue;
+    const double dv[2] = {d0, d1};
 #pragma unroll
-    for (int i = 0; i < TM; ++i)
-#pragma unroll
-      for (int jj = 0; jj < TN; ++jj) {
-        const int row = i0 + m0 + i, col = n0 + jj;
-        if (m0 + i >= IB || col >= NC) continue;
-        const double base = (col < NF) ? __ldg(fx.N0 + static_cast<int64_t>(row) * N + NINT + col) : sm.nf[row];
-        const double v = (base + static_cast<double>(acc[i][jj])) * ib;
-        sm.v32[row * NCP + col] = static_cast<float>(v);
-        if (row >= NINT) vf[(row - NINT) * NC + col] = v;
+    for (int q = 0; q < 2; ++q) {
+      const int col = c0 + q;
+      if (col >= NC) continue;
+      if (face && col < NF && col > pb + r) continue;
+      const double v = (base[q] + dv[q]) * ib;
+      sm.v32[row * NCP + col] = static_cast<float>(v);
+      if (face) {
+        vf[(row - NINT) * NC + col] = v;
+        if (col < NF && col < pb + r) {  // mirror (col, row) of the symmetric face block
+          const int p = pb + r;
+          sm.v32[(NINT + col) * NCP + p] = static_cast<float>(v);
+          vf[col * NC + p] = v;
+        }
       }
+    }
   }
 }
 
@@ -159,29 +201,62 @@ __device__ void correction_tc(BigSmem<K>& sm, const Fixed& fx, double a, double 
     ph[bf] ^= 1u;
     umma::fence_after();
   };
-  // ---- Y = Delta V
+  // ---- Y = Delta V.  Delta's inputs come from the chunk-ordered tables
+  // (dtab: {D, M} fp64, etab: {E, Ma} fp32; zero padded), coalesced, and the
+  // next chunk's loads are issued as soon as the current chunk is generated
+  // (their latency overlaps the B fill, the barrier and the MMA issue).
+  constexpr int PER = MP * KC / kThreads;
+  static_assert(PER * kThreads == MP * KC, "chunk entries per thread");
+  double2 dm[PER];
+  float2 em[PER];
+#pragma unroll
+  for (int i = 0; i < PER; ++i) {
+    dm[i] = __ldg(fx.dtab + tid + i * kThreads);
+    em[i] = __ldg(fx.etab + tid + i * kThreads);
+  }
   for (int c = 0; c < NCH; ++c) {
     const int bf = c & 1, kc = c * KC;
     auto& T = sm.u.tc[bf];
+#ifdef HDR_BIG_TIMING
+    long long tq = clock64();
+#define BIG_Q(slot)                                                      \
+  if (blockIdx.x == 0 && threadIdx.x == 0) {                             \
+    const long long nq_ = clock64();                                     \
+    g_big_prof[slot] += static_cast<unsigned long long>(nq_ - tq);       \
+    tq = nq_;                                                            \
+  }
+#else
+#define BIG_Q(slot)
+#endif
     if (c >= 2) wait_buf(bf);
-    for (int idx = tid; idx < MP * KC; idx += kThreads) {
-      const int m = idx / KC, k = idx - m * KC, col = kc + k;
-      float x = 0.f;
-      if (m < N && col < N) {
-        const int64_t o = static_cast<int64_t>(m) * N + col;
-        x = static_cast<float>(delta_entry(a, b, __ldg(fx.D + o), __ldg(fx.M + o), __ldg(fx.E + o), __ldg(fx.Ma + o)));
-      }
+    BIG_Q(8);
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {  // lane -> (m % 8, k % 4): the 32 lanes store to 32 banks
+      const int g = warp + 16 * i, m = 8 * (g >> 2) + (lane >> 2), k = 4 * (g & 3) + (lane & 3);
+      const float x = static_cast<float>(
+          delta_entry(a, b, dm[i].x, dm[i].y, static_cast<double>(em[i].x), static_cast<double>(em[i].y)));
       const uint32_t off = umma::kmajor_offset(m, k, MP) >> 2;
       tf32_split(x, T.ahi[off], T.alo[off]);
     }
-    for (int idx = tid; idx < NP * KC; idx += kThreads) {
-      const int n = idx / KC, k = idx - n * KC, row = kc + k;
+    if (c + 1 < NCH) {
+      const int64_t q0 = static_cast<int64_t>(c + 1) * MP * KC + tid;
+#pragma unroll
+      for (int i = 0; i < PER; ++i) {
+        dm[i] = __ldg(fx.dtab + q0 + i * kThreads);
+        em[i] = __ldg(fx.etab + q0 + i * kThreads);
+      }
+    }
+    BIG_Q(9);
+    for (int g = warp; g < NP / 2; g += 16) {  // NP / 8 x 4 groups of (n % 8, k % 4) lane patterns
+      const int n = 8 * (g >> 2) + (lane >> 2), k = 4 * (g & 3) + (lane & 3), row = kc + k;
       const float x = (n < NC && row < N) ? sm.v32[row * NCP + n] : 0.f;
       const uint32_t off = umma::kmajor_offset(n, k, NP) >> 2;
       tf32_split(x, T.bhi[off], T.blo[off]);
     }
+    BIG_Q(10);
     umma::fence_proxy_async();
     __syncthreads();
+    BIG_Q(11);
     if (tid == 0) {
       umma::fence_after();
       for (int ks = 0; ks < KC / 8; ++ks)
@@ -198,6 +273,9 @@ __device__ void correction_tc(BigSmem<K>& sm, const Fixed& fx, double a, double 
   }
   wait_buf(NCH & 1);        // chunk NCH - 2
   wait_buf((NCH - 1) & 1);  // chunk NCH - 1: Y complete
+#ifdef HDR_BIG_TIMING
+  if (blockIdx.x == 0 && threadIdx.x == 0) g_big_prof[13] = clock64();
+#endif
   // ---- C = V[:, F]^T Y  (B operand: rows of Y read back from TMEM)
   for (int c = 0; c < NCH; ++c) {
     const int bf = c & 1, kc = c * KC;
@@ -285,10 +363,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_hyb_big(HybArgs A, int parity, 
   float* yg = reinterpret_cast<float*>(vf + NF * NC);                               // N x NCP (Y, higher orders)
   const uint32_t cnt = static_cast<uint32_t>(parity_count(A.m));
 
+#ifdef HDR_BIG_TIMING
+  long long t_last_ = clock64();
+#endif
   for (uint32_t t = blockIdx.x; t < cnt; t += gridDim.x) {
     int cc[3];
     const int e = parity_cell32(A.m, parity, t, cc);
     if (e < 0) continue;
+    BIG_T(0);
     const double a = A.alpha[e], b = A.beta[e];
     const double ib = 1.0 / b;
     const double* fe = A.f + static_cast<int64_t>(e) * N;
@@ -300,31 +382,35 @@ __global__ void __launch_bounds__(kThreads, 1) k_hyb_big(HybArgs A, int parity, 
     for (int i = tid; i < N; i += kThreads) sm.nf[i] = pe[i];
     for (int idx = tid; idx < R * NF; idx += kThreads) {
       const int j = idx / NF, c = idx - j * NF;
-      sm.u.pv.z[j * NC + c] = sm.s[j] * __ldg(fx.X + (NINT + c) * R + j);
+      sm.u.pv.z[j * B::NZ + c] = sm.s[j] * __ldg(fx.X + (NINT + c) * R + j);
     }
-    for (int j = tid; j < R; j += kThreads) sm.u.pv.z[j * NC + NF] = sm.s[j] * pe[N + j];
-    __syncthreads();
-    // rows below NINT (interior dofs) only feed the fp32 correction: fp32 tiles;
-    // the face rows (H0 = V_F, g0) in fp64
-    for (int idx = tid; idx < R * NC; idx += kThreads) sm.u.pv.z32[idx] = static_cast<float>(sm.u.pv.z[idx]);
+    for (int j = tid; j < B::RP; j += kThreads) {
+      sm.u.pv.z[j * B::NZ + NF] = j < R ? sm.s[j] * pe[N + j] : 0.0;
+      for (int c = (j < R ? NC : 0); c < B::NZ; ++c) sm.u.pv.z[j * B::NZ + c] = 0.0;
+    }
+    BIG_T(1);
+    // row blocks on the fp64 tensor cores (the interior rows only feed the
+    // fp32 correction and are rounded to fp32; the face rows give H0 = V_F, g0)
     for (int i0 = 0; i0 < N; i0 += IB) {
-      const bool face = i0 >= NINT;
-      for (int idx = tid; idx < IB * R; idx += kThreads) {
-        const double x = __ldg(fx.X + i0 * R + idx);
-        if (face) sm.u.pv.xi[idx] = x;
-        else sm.u.pv.xi32[idx] = static_cast<float>(x);
+      for (int idx = tid; idx < B::IBP * B::RS; idx += kThreads) {
+        const int r = idx / B::RS, j = idx - r * B::RS;
+        sm.u.pv.xi[idx] = (r < IB && j < R && i0 + r < N) ? __ldg(fx.X + (i0 + r) * R + j) : 0.0;
       }
       __syncthreads();
-      if (face) v_block<K, double>(sm, sm.u.pv.xi, sm.u.pv.z, fx, i0, ib, vf, tid);
-      else v_block<K, float>(sm, sm.u.pv.xi32, sm.u.pv.z32, fx, i0, ib, vf, tid);
+      v_block<K>(sm, fx, i0, ib, vf);
       __syncthreads();
     }
     // ---------------------------------------------------------------- phase C
     // first order on the tensor cores; the CUDA-core path below is kept for
     // the (rare) cells whose a-posteriori estimate asks for a second order
+    BIG_T(2);
     bool tc_done = false;
     if (use_tc) {
       correction_tc<K>(sm, fx, a, b, phase);
+#ifdef HDR_BIG_TIMING
+      if (blockIdx.x == 0 && threadIdx.x == 0) { g_big_prof[3] += g_big_prof[13] - t_last_; t_last_ = g_big_prof[13]; }
+#endif
+      BIG_T(4);
       float cmax = 0.f, hmax = 0.f;
       for (int idx = tid; idx < NF * NF; idx += kThreads) {
         const int p = idx / NF, q = idx - p * NF;
@@ -361,6 +447,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_hyb_big(HybArgs A, int parity, 
       __syncthreads();
       tc_done = sm.order == 1;
     }
+    BIG_T(5);
     if (!tc_done) {
       constexpr int CM = B::CT_M, CN = B::CT_N;
       constexpr int CMS = (NF + CM - 1) / CM, CNS = (NC + CN - 1) / CN;
@@ -501,6 +588,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_hyb_big(HybArgs A, int parity, 
             if (cm0 + i < NF && cn0 + j < NC) sm.u.csm[(cm0 + i) * NCP + cn0 + j] = cacc[i][j];
       __syncthreads();
     }
+    BIG_T(6);
     // ---------------------------------------------------------------- scatter
     {
       unsigned lo = 0, hi = 0;
@@ -554,6 +642,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_hyb_big(HybArgs A, int parity, 
       *hp = (parity == 1 && ps == qs) ? *hp + v : v;
     }
     __syncthreads();
+    BIG_T(7);
+#ifdef HDR_BIG_TIMING
+    if (blockIdx.x == 0 && threadIdx.x == 0) g_big_prof[14] += 1;
+    if (blockIdx.x == 0 && threadIdx.x == 0 && !tc_done) g_big_prof[15] += 1;
+#endif
   }
   if (use_tc && (tid >> 5) == 0) umma::tmem_dealloc(sm.tmem, B::TCOLS);
 }
@@ -579,6 +672,13 @@ int64_t grid_big_t(const HybArgs& a) {
 }
 
 }  // namespace
+
+#ifdef HDR_BIG_TIMING
+extern "C" int hdr_debug_big_prof(unsigned long long* out) {
+  cudaMemcpyFromSymbol(out, g_big_prof, sizeof(g_big_prof));  // 32 counters
+  return 0;
+}
+#endif
 
 bool hybridize_big_supported(int dim, int k) { return dim == 3 && (k == 2 || k == 3); }
 

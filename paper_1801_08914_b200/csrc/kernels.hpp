@@ -25,6 +25,10 @@ void launch_fill_patterns(const DevMesh& m, const int* mbase, const int64_t* fba
 // ---- structured element solve (kern_hybridize.cu)
 struct Fixed {  // device pointers to the per-space fixed factors (see hdr_internal.hpp)
   const double *D, *M, *E, *Ma, *N0, *X, *lam;
+  // RT2 / RT3 hexes: Delta's inputs in the tensor-core chunk order of
+  // kern_cta.cu (chunk c, row m < MP, k < 16 -> column 16 c + k; zero padded)
+  const double2* dtab;  // {D, M}
+  const float2* etab;   // {E, Ma} (tiny: fp32 carries them to 6e-8 relative)
   int r;
   double rho;
 };
