@@ -84,7 +84,7 @@ struct BigSmem {
   union U {
     struct {
       double z[B::RP * B::NZ];
-      double xi[B::IBP * B::RS];
+      double xi[2][B::IBP * B::RS];  // double-buffered row blocks of X
     } pv;
     struct {
       float dt[B::N * B::IB];  // Delta32 block transposed: dt[l * IB + ii]
@@ -141,7 +141,7 @@ __device__ __forceinline__ void v_block(BigSmem<K>& sm, const Fixed& fx, int i0,
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const bool face = i0 >= NINT;
   const int pb = i0 - NINT;
-  const double* xi = sm.u.pv.xi;
+  const double* xi = sm.u.pv.xi[(i0 / IB) & 1];
   const double* z = sm.u.pv.z;
   for (int t = warp; t < RT * CT; t += kThreads / 32) {
     const int rt = t / CT, ct = t - rt * CT;
@@ -207,6 +207,7 @@ __device__ void correction_tc(BigSmem<K>& sm, const Fixed& fx, double a, double 
   // (their latency overlaps the B fill, the barrier and the MMA issue).
   constexpr int PER = MP * KC / kThreads;
   static_assert(PER * kThreads == MP * KC, "chunk entries per thread");
+  const float af = static_cast<float>(a), bf32 = static_cast<float>(b);
   double2 dm[PER];
   float2 em[PER];
 #pragma unroll
@@ -233,8 +234,12 @@ __device__ void correction_tc(BigSmem<K>& sm, const Fixed& fx, double a, double 
 #pragma unroll
     for (int i = 0; i < PER; ++i) {  // lane -> (m % 8, k % 4): the 32 lanes store to 32 banks
       const int g = warp + 16 * i, m = 8 * (g >> 2) + (lane >> 2), k = 4 * (g & 3) + (lane & 3);
-      const float x = static_cast<float>(
-          delta_entry(a, b, dm[i].x, dm[i].y, static_cast<double>(em[i].x), static_cast<double>(em[i].y)));
+      // delta (exact rounding error of the combine) in fp64; alpha E + beta Ma in fp32
+      double p1, e1, p2, e2, sm_, e3;
+      two_prod(a, dm[i].x, p1, e1);
+      two_prod(b, dm[i].y, p2, e2);
+      two_sum(p1, p2, sm_, e3);
+      const float x = fmaf(af, em[i].x, fmaf(bf32, em[i].y, static_cast<float>(-((e1 + e2) + e3))));
       const uint32_t off = umma::kmajor_offset(m, k, MP) >> 2;
       tf32_split(x, T.ahi[off], T.alo[off]);
     }
@@ -281,8 +286,8 @@ __device__ void correction_tc(BigSmem<K>& sm, const Fixed& fx, double a, double 
     const int bf = c & 1, kc = c * KC;
     auto& T = sm.u.tc[bf];
     if (c >= 2) wait_buf(bf);
-    for (int idx = tid; idx < 128 * KC; idx += kThreads) {
-      const int m = idx / KC, k = idx - m * KC, row = kc + k;
+    for (int g = warp; g < 64; g += 16) {  // lane -> (m % 8, k % 4) patterns: conflict-free stores
+      const int m = 8 * (g >> 2) + (lane >> 2), k = 4 * (g & 3) + (lane & 3), row = kc + k;
       const float x = (m < NF && row < N) ? sm.v32[row * NCP + m] : 0.f;  // column m of V = A0^-1 E_F
       const uint32_t off = umma::kmajor_offset(m, k, 128) >> 2;
       tf32_split(x, T.ahi[off], T.alo[off]);
@@ -391,14 +396,31 @@ __global__ void __launch_bounds__(kThreads, 1) k_hyb_big(HybArgs A, int parity, 
     BIG_T(1);
     // row blocks on the fp64 tensor cores (the interior rows only feed the
     // fp32 correction and are rounded to fp32; the face rows give H0 = V_F, g0)
-    for (int i0 = 0; i0 < N; i0 += IB) {
-      for (int idx = tid; idx < B::IBP * B::RS; idx += kThreads) {
-        const int r = idx / B::RS, j = idx - r * B::RS;
-        sm.u.pv.xi[idx] = (r < IB && j < R && i0 + r < N) ? __ldg(fx.X + (i0 + r) * R + j) : 0.0;
+    {
+      constexpr int XE = B::IBP * B::RS, XPT = (XE + kThreads - 1) / kThreads;
+      auto xload = [&](int i0, double (&reg)[XPT]) {
+#pragma unroll
+        for (int u = 0; u < XPT; ++u) {
+          const int idx = tid + u * kThreads, r = idx / B::RS, j = idx - r * B::RS;
+          reg[u] = (idx < XE && r < IB && j < R && i0 + r < N) ? __ldg(fx.X + (i0 + r) * R + j) : 0.0;
+        }
+      };
+      auto xstore = [&](int buf, const double (&reg)[XPT]) {
+#pragma unroll
+        for (int u = 0; u < XPT; ++u)
+          if (tid + u * kThreads < XE) sm.u.pv.xi[buf][tid + u * kThreads] = reg[u];
+      };
+      double xr[XPT];
+      xload(0, xr);
+      xstore(0, xr);
+      __syncthreads();
+      for (int i0 = 0; i0 < N; i0 += IB) {
+        const bool more = i0 + IB < N;
+        if (more) xload(i0 + IB, xr);  // next block's X rows in flight during this block
+        v_block<K>(sm, fx, i0, ib, vf);
+        if (more) xstore(((i0 / IB) + 1) & 1, xr);
+        __syncthreads();
       }
-      __syncthreads();
-      v_block<K>(sm, fx, i0, ib, vf);
-      __syncthreads();
     }
     // ---------------------------------------------------------------- phase C
     // first order on the tensor cores; the CUDA-core path below is kept for
@@ -624,22 +646,40 @@ __global__ void __launch_bounds__(kThreads, 1) k_hyb_big(HybArgs A, int parity, 
       }
     }
     __syncthreads();
-    for (int idx = tid; idx < NF * NC; idx += kThreads) {
-      const int p = idx / NC, c = idx - p * NC;
-      const int ps = p / DPF, sub = p - ps * DPF;
-      const int64_t rs = sm.rstart[ps];
-      if (rs < 0) continue;
-      const double v = vf[p * NC + c] - static_cast<double>(sm.u.csm[p * NCP + c]);
-      if (c == NF) {
-        double* gp = A.g + sm.grow[ps] + sub;
-        *gp = parity ? *gp + v : v;
-        continue;
+    // four entries per thread per pass: every load (vf, csm, the shared diagonal
+    // blocks' partial sums) issued before the first store
+    for (int base = tid; base < NF * NC; base += 4 * kThreads) {
+      double val[4], old[4];
+      double* dst[4];
+      bool acc[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int idx = base + u * kThreads;
+        dst[u] = nullptr;
+        acc[u] = false;
+        val[u] = 0.0;
+        if (idx >= NF * NC) continue;
+        const int p = idx / NC, c = idx - p * NC;
+        const int ps = p / DPF, sub = p - ps * DPF;
+        const int64_t rs = sm.rstart[ps];
+        if (rs < 0) continue;
+        val[u] = vf[p * NC + c] - static_cast<double>(sm.u.csm[p * NCP + c]);
+        if (c == NF) {
+          dst[u] = A.g + sm.grow[ps] + sub;
+          acc[u] = parity != 0;
+          continue;
+        }
+        const int qs = c / DPF, sj = c - qs * DPF;
+        const int rk = sm.rank[ps * NS + qs];
+        if (rk < 0) continue;
+        dst[u] = A.hval + rs + static_cast<int64_t>(sub) * sm.rlen[ps] + rk * DPF + sj;
+        acc[u] = parity == 1 && ps == qs;
       }
-      const int qs = c / DPF, sj = c - qs * DPF;
-      const int rk = sm.rank[ps * NS + qs];
-      if (rk < 0) continue;
-      double* hp = A.hval + rs + static_cast<int64_t>(sub) * sm.rlen[ps] + rk * DPF + sj;
-      *hp = (parity == 1 && ps == qs) ? *hp + v : v;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) old[u] = (dst[u] && acc[u]) ? *dst[u] : 0.0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (dst[u]) *dst[u] = acc[u] ? old[u] + val[u] : val[u];
     }
     __syncthreads();
     BIG_T(7);
