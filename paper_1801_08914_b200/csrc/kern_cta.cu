@@ -379,14 +379,61 @@ __global__ void __launch_bounds__(kThreads, 1) k_hyb_big(HybArgs A, int parity, 
     const double a = A.alpha[e], b = A.beta[e];
     const double ib = 1.0 / b;
     const double* fe = A.f + static_cast<int64_t>(e) * N;
+    // scatter tables (cell geometry only), computed up front; the shared
+    // diagonal blocks' partial sums (colour 1 adds to colour 0's) are prefetched
+    // into L2 now and read back by the scatter
+    {
+      unsigned lo = 0, hi = 0;
+#pragma unroll
+      for (int x = 0; x < 3; ++x) {
+        const int cx = x == 0 ? cc[0] : (x == 1 ? cc[1] : cc[2]);
+        const int Nx = static_cast<int>(x == 0 ? A.m.N[0] : (x == 1 ? A.m.N[1] : A.m.N[2]));
+        lo |= static_cast<unsigned>(cx > 0) << x;
+        hi |= static_cast<unsigned>(cx + 1 < Nx) << x;
+      }
+      for (int idx = tid; idx < NS * NS; idx += kThreads) {
+        const int ps = idx / NS, qs = idx - ps * NS;
+        const int a_ = ps >> 1;
+        const bool pin = (((ps & 1) ? hi : lo) >> a_) & 1u;
+        const bool qin = (((qs & 1) ? hi : lo) >> (qs >> 1)) & 1u;
+        const int ca = a_ == 0 ? cc[0] : (a_ == 1 ? cc[1] : cc[2]);
+        const int na = static_cast<int>(a_ == 0 ? A.m.N[0] : (a_ == 1 ? A.m.N[1] : A.m.N[2]));
+        sm.rank[idx] = (pin && qin) ? col_rank_fast(3, ps, qs, lo, hi, ca, na, false) : -1;
+        if (qs == 0) {
+          const int side = ps & 1;
+          if (pin) {
+            const int face = face_id32(A.m, a_, cc[0] + (a_ == 0 ? side : 0), cc[1] + (a_ == 1 ? side : 0),
+                                       cc[2] + (a_ == 2 ? side : 0));
+            const int row = A.mbase[face];
+            const int64_t r0s = A.rowoff[row];
+            sm.rstart[ps] = r0s;
+            sm.rlen[ps] = static_cast<int>(A.rowoff[row + 1] - r0s);
+            sm.grow[ps] = row;
+          } else {
+            sm.rstart[ps] = -1;
+          }
+        }
+      }
+    }
+    __syncthreads();
+    if (parity == 1)
+      for (int q = tid; q < NS * DPF * (DPF * 8 / 128 + 1); q += kThreads) {
+        const int ps = q / (DPF * (DPF * 8 / 128 + 1)), rem = q - ps * (DPF * (DPF * 8 / 128 + 1));
+        const int sub = rem / (DPF * 8 / 128 + 1), part = rem - sub * (DPF * 8 / 128 + 1);
+        const int64_t rs = sm.rstart[ps];
+        const int rk = sm.rank[ps * NS + ps];
+        if (rs < 0 || rk < 0) continue;
+        const double* line = A.hval + rs + static_cast<int64_t>(sub) * sm.rlen[ps] + rk * DPF + part * 16;
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(line));
+      }
     // ---------------------------------------------------------------- phase V (fp64)
     for (int i = tid; i < N; i += kThreads) sm.f[i] = fe[i];
     for (int j = tid; j < R; j += kThreads) sm.s[j] = b / fma(a, __ldg(fx.lam + j), b);
     __syncthreads();
     const double* pe = pre + static_cast<int64_t>(e) * (N + R);  // [N0 f_e ; X^T f_e], batched GEMM
     for (int i = tid; i < N; i += kThreads) sm.nf[i] = pe[i];
-    for (int idx = tid; idx < R * NF; idx += kThreads) {
-      const int j = idx / NF, c = idx - j * NF;
+    for (int idx = tid; idx < R * NF; idx += kThreads) {  // j fastest: coalesced rows of X
+      const int c = idx / R, j = idx - c * R;
       sm.u.pv.z[j * B::NZ + c] = sm.s[j] * __ldg(fx.X + (NINT + c) * R + j);
     }
     for (int j = tid; j < B::RP; j += kThreads) {
@@ -612,48 +659,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_hyb_big(HybArgs A, int parity, 
     }
     BIG_T(6);
     // ---------------------------------------------------------------- scatter
-    {
-      unsigned lo = 0, hi = 0;
-#pragma unroll
-      for (int x = 0; x < 3; ++x) {
-        const int cx = x == 0 ? cc[0] : (x == 1 ? cc[1] : cc[2]);
-        const int Nx = static_cast<int>(x == 0 ? A.m.N[0] : (x == 1 ? A.m.N[1] : A.m.N[2]));
-        lo |= static_cast<unsigned>(cx > 0) << x;
-        hi |= static_cast<unsigned>(cx + 1 < Nx) << x;
-      }
-      for (int idx = tid; idx < NS * NS; idx += kThreads) {
-        const int ps = idx / NS, qs = idx - ps * NS;
-        const int a_ = ps >> 1;
-        const bool pin = (((ps & 1) ? hi : lo) >> a_) & 1u;
-        const bool qin = (((qs & 1) ? hi : lo) >> (qs >> 1)) & 1u;
-        const int ca = a_ == 0 ? cc[0] : (a_ == 1 ? cc[1] : cc[2]);
-        const int na = static_cast<int>(a_ == 0 ? A.m.N[0] : (a_ == 1 ? A.m.N[1] : A.m.N[2]));
-        sm.rank[idx] = (pin && qin) ? col_rank_fast(3, ps, qs, lo, hi, ca, na, false) : -1;
-        if (qs == 0) {
-          const int side = ps & 1;
-          if (pin) {
-            const int face = face_id32(A.m, a_, cc[0] + (a_ == 0 ? side : 0), cc[1] + (a_ == 1 ? side : 0),
-                                       cc[2] + (a_ == 2 ? side : 0));
-            const int row = A.mbase[face];
-            const int64_t r0s = A.rowoff[row];
-            sm.rstart[ps] = r0s;
-            sm.rlen[ps] = static_cast<int>(A.rowoff[row + 1] - r0s);
-            sm.grow[ps] = row;
-          } else {
-            sm.rstart[ps] = -1;
-          }
-        }
-      }
-    }
-    __syncthreads();
     // four entries per thread per pass: every load (vf, csm, the shared diagonal
     // blocks' partial sums) issued before the first store
-    for (int base = tid; base < NF * NC; base += 4 * kThreads) {
-      double val[4], old[4];
-      double* dst[4];
-      bool acc[4];
+    constexpr int SB = 8;
+    for (int base = tid; base < NF * NC; base += SB * kThreads) {
+      double val[SB], old[SB];
+      double* dst[SB];
+      bool acc[SB];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < SB; ++u) {
         const int idx = base + u * kThreads;
         dst[u] = nullptr;
         acc[u] = false;
@@ -676,9 +690,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_hyb_big(HybArgs A, int parity, 
         acc[u] = parity == 1 && ps == qs;
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) old[u] = (dst[u] && acc[u]) ? *dst[u] : 0.0;
+      for (int u = 0; u < SB; ++u) old[u] = (dst[u] && acc[u]) ? *dst[u] : 0.0;
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
+      for (int u = 0; u < SB; ++u)
         if (dst[u]) *dst[u] = acc[u] ? old[u] + val[u] : val[u];
     }
     __syncthreads();

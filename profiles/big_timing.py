@@ -15,6 +15,7 @@ names = ["loop-top", "f/s/z setup", "V blocks", "TC: Y=Delta V", "TC: C=V^T Y", 
 cells = v[14]
 tot = sum(v[:8])
 print(f"cells {cells} fallback cells {v[15]} cycles/cell {tot / max(cells, 1):.0f}")
+print(f"  scatter tables (part of scatter) {v[12] / max(cells, 1):.0f}")
 print(f"  Y loop (thread 0): wait {v[8] / max(cells, 1):.0f}  A fill {v[9] / max(cells, 1):.0f}  B fill {v[10] / max(cells, 1):.0f}  barrier {v[11] / max(cells, 1):.0f}  MMA issue {v[12] / max(cells, 1):.0f}")
 print("  V rounds (face tid 0 / interior tid 256):", [round(v[16 + q] / max(cells, 1)) for q in range(6)],
       "barrier wait", round(v[24] / max(cells, 1)), round(v[25] / max(cells, 1)))
