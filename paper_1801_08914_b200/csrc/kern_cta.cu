@@ -47,11 +47,13 @@ struct Big {
   static constexpr int CT_M = (K == 3) ? 6 : 3, CT_N = (K == 3) ? 7 : 4;
   static constexpr int NS = 6;
   // tensor-core (tcgen05, 3xTF32) shapes of the first-order correction:
-  //   Y (MP x NP, MT1 M-tiles of 128) = Delta (MP x KP) V (KP x NP);  C (128 x NP) = V_F^T Y
+  //   Y^T (128 x NY) = V^T (128 x KP) Delta^T (KP x NY);  C^T (128 x NFP) = Y^T (128 x KP) V_F (KP x NFP)
+  //   (the Delta tables keep MP = MT1 * 128 rows per chunk; rows >= N are zero)
   static constexpr int MT1 = (N + 127) / 128, MP = MT1 * 128;
   static constexpr int NP = (NC + 15) / 16 * 16, KP = (N + 15) / 16 * 16;
+  static constexpr int NY = KP, NFP = (NF + 15) / 16 * 16;
   static constexpr int KC = 16;  // K per operand chunk (two K=8 MMA steps)
-  static constexpr int TCOLS_USED = (MT1 + 1) * NP;
+  static constexpr int TCOLS_USED = NY + NFP;
   static constexpr int TCOLS = TCOLS_USED <= 32 ? 32 : TCOLS_USED <= 64 ? 64 : TCOLS_USED <= 128 ? 128 : TCOLS_USED <= 256 ? 256 : 512;
 };
 
@@ -91,8 +93,8 @@ struct BigSmem {
       float y[B::IB * B::NCP];
     } pc;
     struct {  // tcgen05 operand chunks (canonical K-major, no swizzle), hi / lo tf32 parts
-      float ahi[B::MP * B::KC], alo[B::MP * B::KC];
-      float bhi[B::NP * B::KC], blo[B::NP * B::KC];
+      float ahi[128 * B::KC], alo[128 * B::KC];    // V^T / Y^T chunk (M = 128)
+      float bhi[B::NY * B::KC], blo[B::NY * B::KC];  // Delta chunk (N = NY) / V_F chunk (N = NFP)
     } tc[2];    // double-buffered: chunk c + 1 is generated while the MMAs of chunk c run
     float csm[B::NF * B::NCP];  // the correction C (NF x NC) for the scatter
   } u;
@@ -182,8 +184,11 @@ __device__ __forceinline__ void v_block(BigSmem<K>& sm, const Fixed& fx, int i0,
   }
 }
 
-// First-order correction on the tensor cores (3xTF32):
-//   Y = Delta V  (Y in TMEM, MT1 tiles of 128 rows),  C = V[:, F]^T Y  (C in TMEM),
+// First-order correction on the tensor cores (3xTF32), in transposed form so
+// that the intermediate never has to be transposed:
+//   Y^T = V^T Delta^T  (M = 128 columns c of [V | w], N = NY rows of Delta, in TMEM)
+//   C^T = Y^T V_F      (M = 128, N = NFP face columns; A = Y^T chunks copied from
+//                       TMEM: lane c holds row c, i.e. exactly the A layout)
 // operands generated chunk by chunk (K = 16) straight into the canonical
 // shared-memory layout; one thread issues the MMAs, everyone waits on the
 // commit mbarrier before the buffers are refilled.  C -> sm.u.csm.
@@ -191,20 +196,30 @@ template <int K>
 __device__ void correction_tc(BigSmem<K>& sm, const Fixed& fx, double a, double b, uint32_t (&ph)[2]) {
   using B = Big<K>;
   constexpr int N = B::N, NF = B::NF, NC = B::NC, NCP = B::NCP;
-  constexpr int MP = B::MP, NP = B::NP, KP = B::KP, KC = B::KC, MT1 = B::MT1, NCH = KP / KC;
+  constexpr int MP = B::MP, KP = B::KP, KC = B::KC, NY = B::NY, NFP = B::NFP, NCH = KP / KC;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const uint32_t tY = sm.tmem, tC = sm.tmem + MT1 * NP;
-  constexpr uint32_t idesc = umma::idesc_tf32(128, NP);
-  constexpr uint32_t lbo_a = (MP / 8) * 128, lbo_b = (NP / 8) * 128, lbo_a2 = (128 / 8) * 128;
+  const uint32_t tY = sm.tmem, tC = sm.tmem + NY;
+  constexpr uint32_t idesc1 = umma::idesc_tf32(128, NY), idesc2 = umma::idesc_tf32(128, NFP);
+  constexpr uint32_t lbo_a = (128 / 8) * 128, lbo_b1 = (NY / 8) * 128, lbo_b2 = (NFP / 8) * 128;
   auto wait_buf = [&](int bf) {  // the MMAs that last read buffer bf are done
     umma::mbar_wait(&sm.mbar[bf], ph[bf]);
     ph[bf] ^= 1u;
     umma::fence_after();
   };
-  // ---- Y = Delta V.  Delta's inputs come from the chunk-ordered tables
+  auto issue = [&](auto& T, int c, uint32_t tD, uint32_t idesc, uint32_t lbo_b) {
+    umma::fence_after();
+    for (int ks = 0; ks < KC / 8; ++ks)
+      for (int term = 0; term < 3; ++term) {
+        const float* aop = term == 2 ? T.alo : T.ahi;
+        const float* bop = term == 1 ? T.blo : T.bhi;
+        const uint64_t ad = umma::smem_desc(umma::smem_u32(aop) + ks * 2 * lbo_a, lbo_a, 128);
+        const uint64_t bd = umma::smem_desc(umma::smem_u32(bop) + ks * 2 * lbo_b, lbo_b, 128);
+        umma::mma_tf32(tD, ad, bd, idesc, c > 0 || ks > 0 || term > 0);
+      }
+  };
+  // ---- Y^T = V^T Delta^T.  Delta's inputs come from the chunk-ordered tables
   // (dtab: {D, M} fp64, etab: {E, Ma} fp32; zero padded), coalesced, and the
-  // next chunk's loads are issued as soon as the current chunk is generated
-  // (their latency overlaps the B fill, the barrier and the MMA issue).
+  // next chunk's loads are issued as soon as the current chunk is generated.
   constexpr int PER = MP * KC / kThreads;
   static_assert(PER * kThreads == MP * KC, "chunk entries per thread");
   const float af = static_cast<float>(a), bf32 = static_cast<float>(b);
@@ -232,7 +247,7 @@ __device__ void correction_tc(BigSmem<K>& sm, const Fixed& fx, double a, double 
     if (c >= 2) wait_buf(bf);
     BIG_Q(8);
 #pragma unroll
-    for (int i = 0; i < PER; ++i) {  // lane -> (m % 8, k % 4): the 32 lanes store to 32 banks
+    for (int i = 0; i < PER; ++i) {  // lane -> (n % 8, k % 4): the 32 lanes store to 32 banks
       const int g = warp + 16 * i, m = 8 * (g >> 2) + (lane >> 2), k = 4 * (g & 3) + (lane & 3);
       // delta (exact rounding error of the combine) in fp64; alpha E + beta Ma in fp32
       double p1, e1, p2, e2, sm_, e3;
@@ -240,8 +255,10 @@ __device__ void correction_tc(BigSmem<K>& sm, const Fixed& fx, double a, double 
       two_prod(b, dm[i].y, p2, e2);
       two_sum(p1, p2, sm_, e3);
       const float x = fmaf(af, em[i].x, fmaf(bf32, em[i].y, static_cast<float>(-((e1 + e2) + e3))));
-      const uint32_t off = umma::kmajor_offset(m, k, MP) >> 2;
-      tf32_split(x, T.ahi[off], T.alo[off]);
+      if (m < NY) {
+        const uint32_t off = umma::kmajor_offset(m, k, NY) >> 2;
+        tf32_split(x, T.bhi[off], T.blo[off]);
+      }
     }
     if (c + 1 < NCH) {
       const int64_t q0 = static_cast<int64_t>(c + 1) * MP * KC + tid;
@@ -252,91 +269,68 @@ __device__ void correction_tc(BigSmem<K>& sm, const Fixed& fx, double a, double 
       }
     }
     BIG_Q(9);
-    for (int g = warp; g < NP / 2; g += 16) {  // NP / 8 x 4 groups of (n % 8, k % 4) lane patterns
-      const int n = 8 * (g >> 2) + (lane >> 2), k = 4 * (g & 3) + (lane & 3), row = kc + k;
-      const float x = (n < NC && row < N) ? sm.v32[row * NCP + n] : 0.f;
-      const uint32_t off = umma::kmajor_offset(n, k, NP) >> 2;
-      tf32_split(x, T.bhi[off], T.blo[off]);
+    for (int g = warp; g < 64; g += 16) {  // V^T chunk: lane -> (c % 8, k % 4)
+      const int m = 8 * (g >> 2) + (lane >> 2), k = 4 * (g & 3) + (lane & 3), row = kc + k;
+      const float x = (m < NC && row < N) ? sm.v32[row * NCP + m] : 0.f;
+      const uint32_t off = umma::kmajor_offset(m, k, 128) >> 2;
+      tf32_split(x, T.ahi[off], T.alo[off]);
     }
     BIG_Q(10);
     umma::fence_proxy_async();
     __syncthreads();
     BIG_Q(11);
     if (tid == 0) {
-      umma::fence_after();
-      for (int ks = 0; ks < KC / 8; ++ks)
-        for (int t = 0; t < MT1; ++t)
-          for (int term = 0; term < 3; ++term) {
-            const float* aop = term == 2 ? T.alo : T.ahi;
-            const float* bop = term == 1 ? T.blo : T.bhi;
-            const uint64_t ad = umma::smem_desc(umma::smem_u32(aop) + t * 2048 + ks * 2 * lbo_a, lbo_a, 128);
-            const uint64_t bd = umma::smem_desc(umma::smem_u32(bop) + ks * 2 * lbo_b, lbo_b, 128);
-            umma::mma_tf32(tY + t * NP, ad, bd, idesc, c > 0 || ks > 0 || term > 0);
-          }
+      issue(T, c, tY, idesc1, lbo_b1);
       umma::commit(&sm.mbar[bf]);
     }
   }
   wait_buf(NCH & 1);        // chunk NCH - 2
-  wait_buf((NCH - 1) & 1);  // chunk NCH - 1: Y complete
+  wait_buf((NCH - 1) & 1);  // chunk NCH - 1: Y^T complete
 #ifdef HDR_BIG_TIMING
   if (blockIdx.x == 0 && threadIdx.x == 0) g_big_prof[13] = clock64();
 #endif
-  // ---- C = V[:, F]^T Y  (B operand: rows of Y read back from TMEM)
+  // ---- C^T = Y^T V_F  (A operand: Y^T chunk from TMEM; lane c holds row c)
   for (int c = 0; c < NCH; ++c) {
     const int bf = c & 1, kc = c * KC;
     auto& T = sm.u.tc[bf];
     if (c >= 2) wait_buf(bf);
-    for (int g = warp; g < 64; g += 16) {  // lane -> (m % 8, k % 4) patterns: conflict-free stores
-      const int m = 8 * (g >> 2) + (lane >> 2), k = 4 * (g & 3) + (lane & 3), row = kc + k;
-      const float x = (m < NF && row < N) ? sm.v32[row * NCP + m] : 0.f;  // column m of V = A0^-1 E_F
-      const uint32_t off = umma::kmajor_offset(m, k, 128) >> 2;
-      tf32_split(x, T.ahi[off], T.alo[off]);
-    }
-    {
-      const int t = kc / 128, l0 = kc - t * 128, q = l0 >> 5, lo = l0 & 31;
-      if ((warp & 3) == q) {  // the warps of TMEM lane quadrant q share the columns, 8 at a time
-        for (int cc = 8 * (warp >> 2); cc < NP; cc += 8 * (kThreads / 128)) {
-          float v[8];
-          umma::tmem_ld8(tY + t * NP + (static_cast<uint32_t>(32 * q) << 16) + cc, v);
-          if (lane >= lo && lane < lo + KC) {
-            const int k = lane - lo;
+    {  // the 4 warps of lane quadrant q = warp % 4 take 4 columns each
+      const int q = warp & 3, k0 = 4 * (warp >> 2), m = 32 * q + lane;
+      float v[4];
+      umma::tmem_ld4(tY + (static_cast<uint32_t>(32 * q) << 16) + kc + k0, v);
+      float hi[4], lo[4];
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-              const uint32_t off = umma::kmajor_offset(cc + j, k, NP) >> 2;
-              tf32_split(v[j], T.bhi[off], T.blo[off]);
-            }
-          }
-        }
-      }
+      for (int j = 0; j < 4; ++j) tf32_split(v[j], hi[j], lo[j]);
+      const uint32_t off = umma::kmajor_offset(m, k0, 128) >> 2;  // 4 consecutive k: 16 bytes
+      *reinterpret_cast<float4*>(T.ahi + off) = make_float4(hi[0], hi[1], hi[2], hi[3]);
+      *reinterpret_cast<float4*>(T.alo + off) = make_float4(lo[0], lo[1], lo[2], lo[3]);
+    }
+    for (int g = warp; g < NFP / 2; g += 16) {  // V_F chunk: lane -> (f % 8, k % 4)
+      const int f = 8 * (g >> 2) + (lane >> 2), k = 4 * (g & 3) + (lane & 3), row = kc + k;
+      const float x = (f < NF && row < N) ? sm.v32[row * NCP + f] : 0.f;
+      const uint32_t off = umma::kmajor_offset(f, k, NFP) >> 2;
+      tf32_split(x, T.bhi[off], T.blo[off]);
     }
     umma::fence_proxy_async();
     umma::fence_before();
     __syncthreads();
     if (tid == 0) {
-      umma::fence_after();
-      for (int ks = 0; ks < KC / 8; ++ks)
-        for (int term = 0; term < 3; ++term) {
-          const float* aop = term == 2 ? T.alo : T.ahi;
-          const float* bop = term == 1 ? T.blo : T.bhi;
-          const uint64_t ad = umma::smem_desc(umma::smem_u32(aop) + ks * 2 * lbo_a2, lbo_a2, 128);
-          const uint64_t bd = umma::smem_desc(umma::smem_u32(bop) + ks * 2 * lbo_b, lbo_b, 128);
-          umma::mma_tf32(tC, ad, bd, idesc, c > 0 || ks > 0 || term > 0);
-        }
+      issue(T, c, tC, idesc2, lbo_b2);
       umma::commit(&sm.mbar[bf]);
     }
   }
   wait_buf(NCH & 1);
   wait_buf((NCH - 1) & 1);
-  // ---- C -> shared memory
+  // ---- C^T -> C in shared memory: lane c holds C^T[c][f] = C[f][c]
   {
     const int q = warp & 3, m = 32 * q + lane;
-    for (int cc = 8 * (warp >> 2); cc < NP; cc += 8 * (kThreads / 128)) {
+    for (int cc = 8 * (warp >> 2); cc < NFP; cc += 8 * (kThreads / 128)) {
       float v[8];
       umma::tmem_ld8(tC + (static_cast<uint32_t>(32 * q) << 16) + cc, v);
-      if (m < NF)
+      if (m < NC)
 #pragma unroll
         for (int j = 0; j < 8; ++j)
-          if (cc + j < NC) sm.u.csm[m * NCP + cc + j] = v[j];
+          if (cc + j < NF) sm.u.csm[(cc + j) * NCP + m] = v[j];
     }
   }
   umma::fence_before();

@@ -94,5 +94,16 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr_lane_col, float (&v)[8])
   for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// warp w reads TMEM lanes [32 (w % 4), +32): thread t gets 4 consecutive columns
+__device__ __forceinline__ void tmem_ld4(uint32_t taddr_lane_col, float (&v)[4]) {
+  uint32_t r[4];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(taddr_lane_col));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 4; ++i) v[i] = __uint_as_float(r[i]);
+}
+
 }  // namespace umma
 }  // namespace hdr
