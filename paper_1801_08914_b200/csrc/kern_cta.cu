@@ -114,12 +114,13 @@ constexpr int64_t big_scratch_doubles() {
   return static_cast<int64_t>(B::NF) * B::NC + static_cast<int64_t>(B::N) * B::NCP + 16;
 }
 
+// x = hi + lo with hi, lo tf32 (low 13 mantissa bits zero; hi rounded half away
+// from zero like cvt.rna): integer ops only (the tensor core reads the top 19
+// bits; x - hi is exact in fp32)
 __device__ __forceinline__ void tf32_split(float x, float& hi, float& lo) {
-  uint32_t h, l;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(x));
-  hi = __uint_as_float(h);
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(l) : "f"(x - hi));
-  lo = __uint_as_float(l);
+  hi = __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
+  const float r = x - hi;
+  lo = __uint_as_float((__float_as_uint(r) + 0x1000u) & 0xFFFFE000u);
 }
 
 // One row block [i0, i0 + IB) of [V | w] = (base + X z) / beta, register tiles
@@ -249,16 +250,15 @@ __device__ void correction_tc(BigSmem<K>& sm, const Fixed& fx, double a, double 
 #pragma unroll
     for (int i = 0; i < PER; ++i) {  // lane -> (n % 8, k % 4): the 32 lanes store to 32 banks
       const int g = warp + 16 * i, m = 8 * (g >> 2) + (lane >> 2), k = 4 * (g & 3) + (lane & 3);
+      if (8 * (g >> 2) >= NY) continue;  // padding rows of the table (warp-uniform)
       // delta (exact rounding error of the combine) in fp64; alpha E + beta Ma in fp32
       double p1, e1, p2, e2, sm_, e3;
       two_prod(a, dm[i].x, p1, e1);
       two_prod(b, dm[i].y, p2, e2);
       two_sum(p1, p2, sm_, e3);
       const float x = fmaf(af, em[i].x, fmaf(bf32, em[i].y, static_cast<float>(-((e1 + e2) + e3))));
-      if (m < NY) {
-        const uint32_t off = umma::kmajor_offset(m, k, NY) >> 2;
-        tf32_split(x, T.bhi[off], T.blo[off]);
-      }
+      const uint32_t off = umma::kmajor_offset(m, k, NY) >> 2;
+      tf32_split(x, T.bhi[off], T.blo[off]);
     }
     if (c + 1 < NCH) {
       const int64_t q0 = static_cast<int64_t>(c + 1) * MP * KC + tid;
