@@ -159,11 +159,28 @@ __device__ __forceinline__ void v_block(BigSmem<K>& sm, const Fixed& fx, int i0,
       base[q] = !rok || col >= NC ? 0.0
                 : (col < NF ? __ldg(fx.N0 + static_cast<int64_t>(row) * N + NINT + col) : sm.nf[row]);
     }
-    double d0 = 0.0, d1 = 0.0;
     const double* ap = xi + (rt * 8 + (lane >> 2)) * RS + (lane & 3);
     const double* bp = z + (lane & 3) * NZ + ct * 8 + (lane >> 2);
-#pragma unroll 4
-    for (int kk = 0; kk < B::RP / 4; ++kk) dmma_8x8x4(d0, d1, ap[4 * kk], bp[4 * kk * NZ]);
+    // fragments loaded in batches of 8 k-steps ahead of their MMAs; two
+    // accumulator pairs (even / odd k-steps) halve the dependent MMA chain
+    constexpr int KS = B::RP / 4, KB = KS < 8 ? KS : 8;
+    double d0 = 0.0, d1 = 0.0, e0 = 0.0, e1 = 0.0;
+#pragma unroll
+    for (int k0 = 0; k0 < KS; k0 += KB) {
+      double av[KB], bv[KB];
+#pragma unroll
+      for (int u = 0; u < KB; ++u) {
+        av[u] = k0 + u < KS ? ap[4 * (k0 + u)] : 0.0;
+        bv[u] = k0 + u < KS ? bp[4 * (k0 + u) * NZ] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < KB; ++u) {
+        if (u & 1) dmma_8x8x4(e0, e1, av[u], bv[u]);
+        else dmma_8x8x4(d0, d1, av[u], bv[u]);
+      }
+    }
+    d0 += e0;
+    d1 += e1;
     if (!rok) continue;
     const double dv[2] = {d0, d1};
 #pragma unroll
