@@ -217,9 +217,9 @@ def cpu_baseline(cfg_id: int):
 
 def kernel_name(cfg: dict) -> str:
     if cfg.get("perturb"):
-        return "k_piola_assemble + k_alg<HYB> + k_run_sum"
+        return "k_piola_gemm + k_spd_hyb + k_run_sum"
     if cfg["k"] == 0:
-        return "k_rt0_cell<dim,0> + k_rt0_cell<dim,1> (colour passes)"
+        return "k_rt0_brick<dim,0> + k_rt0_brick<dim,1> (colour passes; k_rt0_cell below the brick size)"
     if cfg["dim"] == 3 and cfg["k"] >= 2:
         return "k_hyb_big<k> x2 colours"
     return "k_hyb_warp x2 colours"

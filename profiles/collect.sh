@@ -23,7 +23,7 @@ for c in 2 3 4 5; do
   case $c in
     2) K='regex:k_rt0_brick|k_rt0_cell|k_rt0_rows' ;;
     3) K='regex:k_hyb_warp' ;;
-    4) K='regex:k_piola_assemble|k_alg<|k_run_sum' ;;
+    4) K='regex:k_piola_gemm|k_spd_hyb|k_run_sum' ;;
     5) K='regex:k_hyb_big|k_gemm_f64' ;;
   esac
   timeout 900 ncu --clock-control none --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum \
@@ -36,7 +36,7 @@ timeout 900 ncu --set full --import-source on --clock-control none -k regex:k_rt
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:k_hyb_warp -c 1 \
   -o "$OUT/full_cfg3" python bench.py --config 3 --steps 1 --warmup 3 --no-e2e --no-cpu --no-graph > "$OUT/full3.log" 2>&1
 timeout 900 ncu --set full --import-source on --clock-control none --kernel-name-base function \
-  -k regex:'^(k_piola_assemble|k_alg)$' -c 2 \
+  -k regex:'^(k_piola_gemm|k_spd_hyb)$' -c 2 \
   -o "$OUT/full_cfg4" python bench.py --config 4 --steps 1 --warmup 3 --no-e2e --no-cpu --no-graph > "$OUT/full4.log" 2>&1
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:k_hyb_big -c 1 \
   -o "$OUT/full_cfg5" python bench.py --config 5 --steps 1 --warmup 3 --no-e2e --no-cpu --no-graph > "$OUT/full5.log" 2>&1

@@ -62,7 +62,7 @@ def main():
 
 # per step DRAM bytes (read + write) of the dominant kernels, from the traffic launch lists;
 # the number of steps captured = launches of the step's anchor kernel / its launches per step
-ANCHOR = {"cfg2": ("k_rt0_brick", 2), "cfg3": ("k_hyb_warp", 2), "cfg4": ("k_piola_assemble", 1), "cfg5": ("k_hyb_big", 2)}
+ANCHOR = {"cfg2": ("k_rt0_brick", 2), "cfg3": ("k_hyb_warp", 2), "cfg4": ("k_piola_gemm", 1), "cfg5": ("k_hyb_big", 2)}
 
 
 def traffic_json(src: Path):
