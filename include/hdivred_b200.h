@@ -135,6 +135,18 @@ hdr_status hdr_hybridize_fe_into(hdr_hybrid_t op, const double* alpha, const dou
  * Errors detected on the device are reported by the next hdr_hybrid_check. */
 hdr_status hdr_hybridize_fe_enqueue(hdr_hybrid_t op, const double* alpha, const double* beta, const double* f_hat,
                                     int on_device);
+/* Pipelined batch of count independent hybridizations on one space (new
+ * coefficients / right-hand sides per item: parameter sweeps, time steps):
+ * item i reads alpha[i], beta[i], f_hat[i] (host memory; pinned for overlap)
+ * and writes its H values (nnz_H, pattern order) and g (m) to h_values[i] /
+ * g[i] (host; NULL skips).  Uploads, kernels and downloads run on three
+ * streams with two alternating device operators, so item i's download overlaps
+ * item i+1's kernels and item i+2's upload.  Same bits as count separate
+ * hdr_hybridize_fe + hdr_hybrid_values calls (reduction.cpp:262-354 each).
+ * Returns after the last download; the space's stream is ordered after it. */
+hdr_status hdr_hybridize_fe_batch(hdr_space_t space, int count, const double* const* alpha,
+                                  const double* const* beta, const double* const* f_hat, double* const* h_values,
+                                  double* const* g);
 /* Synchronizes the stream and reports device-side status of enqueued work. */
 hdr_status hdr_hybrid_check(hdr_hybrid_t op);
 /* In-place symmetrization of the operator's H values (see hdr_alg_symmetrize). */

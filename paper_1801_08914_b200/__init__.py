@@ -259,6 +259,40 @@ class Space:
         _check(_lib().hdr_hybridize_fe(self._h, _ptr(a)[0], _ptr(b)[0], _ptr(f)[0], dev, ctypes.byref(h)))
         return HybridizedOperator(self, h)
 
+    def hybridize_batch(self, alphas, betas, f_hats, h_outs=None, g_outs=None) -> None:
+        """Pipelined batch of independent hybridizations (hdr_hybridize_fe_batch):
+        item i's host inputs (alphas[i], betas[i], f_hats[i]; pinned for overlap)
+        give H values / g in the host arrays h_outs[i] / g_outs[i] (None skips).
+        Uploads, kernels and downloads of consecutive items overlap."""
+        count = len(alphas)
+        if len(betas) != count or len(f_hats) != count:
+            raise DimensionMismatch("hybridize_batch: alphas, betas, f_hats differ in length")
+
+        def ptrs(arrs, n, name, out=False):
+            if arrs is None:
+                return None
+            if len(arrs) != count:
+                raise DimensionMismatch(f"hybridize_batch: {name} has {len(arrs)} items, expected {count}")
+            vals = []
+            for a in arrs:
+                if a is None:
+                    vals.append(None)
+                    continue
+                if not out:
+                    a = _as_f64(a, n, name)
+                elif (a.size if isinstance(a, np.ndarray) else a.numel()) != n:
+                    raise DimensionMismatch(f"{name}: expected {n} values")
+                p_, dev = _ptr(a)
+                if dev:
+                    raise ValueError(f"{name}: hybridize_batch takes host arrays")
+                vals.append(p_)
+            return (ctypes.c_void_p * count)(*vals)
+
+        keep = [ptrs(alphas, self.ncells, "alpha"), ptrs(betas, self.ncells, "beta"),
+                ptrs(f_hats, self.broken_ndofs, "f_hat"), ptrs(h_outs, self.info["nnz_h"], "h_outs", True),
+                ptrs(g_outs, self.m, "g_outs", True)]
+        _check(_lib().hdr_hybridize_fe_batch(self._h, count, *keep))
+
     def static_condense(self, alpha, beta, f_hat) -> "CondensedOperator":
         """static_condense (src/reduction.cpp:448-557) of the FE inputs."""
         a = _as_f64(alpha, self.ncells, "alpha")

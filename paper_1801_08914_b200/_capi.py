@@ -55,6 +55,7 @@ _SIGS = {
     "hdr_hybridize_fe": (_i32, [_vp, _vp, _vp, _vp, _i32, _vp]),
     "hdr_hybridize_fe_into": (_i32, [_vp, _vp, _vp, _vp, _i32]),
     "hdr_hybridize_fe_enqueue": (_i32, [_vp, _vp, _vp, _vp, _i32]),
+    "hdr_hybridize_fe_batch": (_i32, [_vp, _i32, _vp, _vp, _vp, _vp, _vp]),
     "hdr_hybrid_check": (_i32, [_vp]),
     "hdr_hybrid_values_enqueue": (_i32, [_vp, _vp, _vp, _i32]),
     "hdr_measure_fp64_peak": (_i32, [_vp, _vp]),

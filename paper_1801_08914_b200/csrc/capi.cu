@@ -64,10 +64,8 @@ struct hdr_space_s {
   DBuf<float> etab;                // k >= 2 (3D): {E, Ma} (fp32) likewise
   Fixed fx{};
   GeomState* geom = nullptr;  // mapped (trilinear) cells: hdr_space_set_vertices
-  ~hdr_space_s() {
-    if (geom) geom_destroy(geom);
-    if (own_stream && stream) cudaStreamDestroy(stream);
-  }
+  struct BatchCtx* batch = nullptr;  // hdr_hybridize_fe_batch: streams, events, two operators
+  ~hdr_space_s();
 };
 
 struct hdr_hybrid_s {
@@ -78,6 +76,30 @@ struct hdr_hybrid_s {
   const double* a_ptr = nullptr;  // coefficients used by the last hybridize (owned copy or borrowed device input)
   const double* b_ptr = nullptr;
 };
+
+// pipelined batch (hdr_hybridize_fe_batch): uploads on cs, kernels on the space's
+// stream, downloads on ds; two operators alternate (double-buffered inputs and
+// H values)
+struct BatchCtx {
+  cudaStream_t cs = nullptr, ds = nullptr;
+  cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_comp[2] = {nullptr, nullptr}, ev_d2h[2] = {nullptr, nullptr};
+  hdr_hybrid_s op[2];
+  ~BatchCtx() {
+    for (int b = 0; b < 2; ++b) {
+      if (ev_in[b]) cudaEventDestroy(ev_in[b]);
+      if (ev_comp[b]) cudaEventDestroy(ev_comp[b]);
+      if (ev_d2h[b]) cudaEventDestroy(ev_d2h[b]);
+    }
+    if (cs) cudaStreamDestroy(cs);
+    if (ds) cudaStreamDestroy(ds);
+  }
+};
+
+hdr_space_s::~hdr_space_s() {
+  delete batch;
+  if (geom) geom_destroy(geom);
+  if (own_stream && stream) cudaStreamDestroy(stream);
+}
 
 struct hdr_condensed_s {
   hdr_space_t sp = nullptr;
@@ -598,6 +620,66 @@ hdr_status hdr_hybridize_fe_enqueue(hdr_hybrid_t op, const double* alpha, const 
                                    int on_device) {
   if (!op || !alpha || !beta || !f_hat) return fail(HDR_INVALID_ARGUMENT, "null argument");
   return run_hybridize(op, alpha, beta, f_hat, on_device, false);
+}
+
+hdr_status hdr_hybridize_fe_batch(hdr_space_t sp, int count, const double* const* alpha, const double* const* beta,
+                                  const double* const* f_hat, double* const* h_values, double* const* g) {
+  if (!sp || count < 0 || (count > 0 && (!alpha || !beta || !f_hat))) return fail(HDR_INVALID_ARGUMENT, "null argument");
+  for (int i = 0; i < count; ++i)
+    if (!alpha[i] || !beta[i] || !f_hat[i]) return fail(HDR_INVALID_ARGUMENT, "null input of a batch item");
+  return catch_all([&]() -> hdr_status {
+    cudaStream_t st = sp->stream;
+    if (!sp->batch) {
+      auto ctx = std::make_unique<BatchCtx>();
+      CK(cudaStreamCreateWithFlags(&ctx->cs, cudaStreamNonBlocking));
+      CK(cudaStreamCreateWithFlags(&ctx->ds, cudaStreamNonBlocking));
+      for (int b = 0; b < 2; ++b) {
+        CK(cudaEventCreateWithFlags(&ctx->ev_in[b], cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&ctx->ev_comp[b], cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&ctx->ev_d2h[b], cudaEventDisableTiming));
+        ctx->op[b].sp = sp;
+        ctx->op[b].alpha.alloc(static_cast<size_t>(sp->ncells));
+        ctx->op[b].beta.alloc(static_cast<size_t>(sp->ncells));
+        ctx->op[b].f.alloc(static_cast<size_t>(sp->broken));
+      }
+      sp->batch = ctx.release();
+    }
+    BatchCtx& B = *sp->batch;
+    // the previous batch (and anything else on the space's stream) completes first
+    CK(cudaEventRecord(B.ev_comp[0], st));
+    CK(cudaStreamWaitEvent(B.cs, B.ev_comp[0], 0));
+    CK(cudaStreamWaitEvent(B.ds, B.ev_comp[0], 0));
+    for (int i = 0; i < count; ++i) {
+      const int b = i & 1;
+      hdr_hybrid_s* op = &B.op[b];
+      if (i >= 2) CK(cudaStreamWaitEvent(B.cs, B.ev_comp[b], 0));  // item i - 2's kernels done with the inputs
+      CK(cudaMemcpyAsync(op->alpha.p, alpha[i], static_cast<size_t>(sp->ncells) * 8, cudaMemcpyHostToDevice, B.cs));
+      CK(cudaMemcpyAsync(op->beta.p, beta[i], static_cast<size_t>(sp->ncells) * 8, cudaMemcpyHostToDevice, B.cs));
+      CK(cudaMemcpyAsync(op->f.p, f_hat[i], static_cast<size_t>(sp->broken) * 8, cudaMemcpyHostToDevice, B.cs));
+      CK(cudaEventRecord(B.ev_in[b], B.cs));
+      CK(cudaStreamWaitEvent(st, B.ev_in[b], 0));
+      if (i >= 2) CK(cudaStreamWaitEvent(st, B.ev_d2h[b], 0));  // item i - 2's download of these H values done
+      const hdr_status s = run_hybridize(op, op->alpha.p, op->beta.p, op->f.p, 1, false);
+      if (s != HDR_OK) return s;
+      CK(cudaEventRecord(B.ev_comp[b], st));
+      CK(cudaStreamWaitEvent(B.ds, B.ev_comp[b], 0));
+      if (h_values && h_values[i] && sp->nnz_h)
+        CK(cudaMemcpyAsync(h_values[i], op->hval.p, static_cast<size_t>(sp->nnz_h) * 8, cudaMemcpyDeviceToHost, B.ds));
+      if (g && g[i] && sp->m)
+        CK(cudaMemcpyAsync(g[i], op->g.p, static_cast<size_t>(sp->m) * 8, cudaMemcpyDeviceToHost, B.ds));
+      CK(cudaEventRecord(B.ev_d2h[b], B.ds));
+    }
+    // the space's stream is ordered after the last download (callers time on it)
+    if (count > 0) CK(cudaStreamWaitEvent(st, B.ev_d2h[(count - 1) & 1], 0));
+    CK(cudaStreamSynchronize(B.ds));
+    CK(cudaStreamSynchronize(B.cs));
+    for (int b = 0; b < 2 && b < count; ++b) {
+      const hdr_status s = check_status(B.op[b].status.p, st);
+      if (s != HDR_OK) return s;
+    }
+    CK(cudaStreamSynchronize(st));
+    return HDR_OK;
+  });
 }
 
 hdr_status hdr_hybrid_check(hdr_hybrid_t op) {

@@ -224,3 +224,23 @@ def test_full_size_sampled_rows_vs_dd(dim, cells, k, coef, seed, nnz):
     assert checked > 0
     assert worst_h <= TOL * scale_h, worst_h / scale_h
     assert worst_g <= TOL * scale_g, worst_g / scale_g
+
+
+@pytest.mark.parametrize("dim,cells,k", [(3, (6, 5, 4), 0), (3, (5, 4, 3), 1), (3, (3, 3, 2), 3), (2, (9, 7), 2)])
+def test_batch_pipeline_matches_single_calls(dim, cells, k):
+    """hdr_hybridize_fe_batch (three streams, two alternating operators) gives
+    the same bits as separate hybridize calls, item by item."""
+    sp = hd.Space(dim, cells, k)
+    rng = np.random.default_rng(7)
+    items = []
+    for _ in range(5):
+        a = 10.0 ** rng.uniform(-2, 2, sp.ncells)
+        b = 10.0 ** rng.uniform(-2, 2, sp.ncells)
+        f = rng.uniform(-1, 1, sp.broken_ndofs)
+        items.append((a, b, f))
+    h_outs = [np.full(sp.info["nnz_h"], np.nan) for _ in items]
+    g_outs = [np.full(sp.m, np.nan) for _ in items]
+    sp.hybridize_batch([x[0] for x in items], [x[1] for x in items], [x[2] for x in items], h_outs, g_outs)
+    for (a, b, f), hv, gv in zip(items, h_outs, g_outs):
+        h_ref, g_ref = sp.hybridize(a, b, f).values()
+        assert np.array_equal(hv, h_ref) and np.array_equal(gv, g_ref)
