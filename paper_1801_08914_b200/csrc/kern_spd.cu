@@ -56,6 +56,7 @@ struct SpdSmem {
   double* C;   // 8 x ld: A_iB (the block's columns before the step)
   double* P;   // 2 x 8 x 8: swept pivot blocks (-P^-1), double-buffered
   double* piv; // n scalar pivots
+  double* rsum;  // n: row sums of |A| (residual anchors)
   double* red;
   int* sidx;
   int* flag;
@@ -206,23 +207,33 @@ __device__ __forceinline__ void gemm_tile(int n, const double* W, int ld, const 
   }
 }
 
-// R = B - A Z with exact products and compensated sums (rounded once).
+// R = B - A Z to ~2^-99 of sum |B| + |A||Z| (rounded once), five fp64 ops per
+// term instead of a double-double dot product: with a per-row anchor
+// C = 1.5 * 2^q, 2^(q-1) > |B| + rowsum|A| * max|Z| (every product and partial
+// sum fits below 2^(q-1)):
+//   t = fma(a, z, C); p_hi = t - C (exact, Sterbenz: a z rounded to ulp(C));
+//   p_lo = fma(a, z, -p_hi) (the remainder, rounded: <= u ulp(C) / 2);
+//   S_hi += p_hi (exact: multiples of ulp(C) below 2^(q+1)), S_lo += p_lo.
 // Thread tiles of TM rows x TN columns; A read through the [i | b] permutation.
-__device__ void residual(int n, int nc, const double* A, const SpdSmem& s, const double* Bg) {
+__device__ void residual(int n, int nc, const double* A, const SpdSmem& s, const double* Bg, double bound_z,
+                         double bmax) {
   constexpr int TM = 4, TN = 4;
   const int tn = (nc + TN - 1) / TN, tm = (n + TM - 1) / TM;
   for (int tile = threadIdx.x; tile < tm * tn; tile += kST) {
     const int r0 = (tile / tn) * TM, c0 = (tile % tn) * TN;
-    double hi[TM][TN], lo[TM][TN];
+    double hi[TM][TN], lo[TM][TN], anc[TM];
     const double* arow[TM];
 #pragma unroll
     for (int a = 0; a < TM; ++a) {
       const int r = min(r0 + a, n - 1);
       arow[a] = A + static_cast<int64_t>(s.sidx[r]) * n;
+      const double x = fmax(s.rsum[r] * bound_z + bmax, 1e-280);
+      anc[a] = scalbn(1.5, ilogb(x) + 2);
 #pragma unroll
       for (int b = 0; b < TN; ++b) {
-        hi[a][b] = (r0 + a < n && c0 + b < nc) ? Bg[(r0 + a) * s.ldz + c0 + b] : 0.0;
-        lo[a][b] = 0.0;
+        const double bv = (r0 + a < n && c0 + b < nc) ? Bg[(r0 + a) * s.ldz + c0 + b] : 0.0;
+        hi[a][b] = (bv + anc[a]) - anc[a];
+        lo[a][b] = bv - hi[a][b];
       }
     }
 #pragma unroll 2
@@ -237,11 +248,10 @@ __device__ void residual(int n, int nc, const double* A, const SpdSmem& s, const
       for (int a = 0; a < TM; ++a)
 #pragma unroll
         for (int b = 0; b < TN; ++b) {
-          double p, e, sm, t;
-          two_prod(av[a], zv[b], p, e);
-          two_sum(hi[a][b], p, sm, t);
-          hi[a][b] = sm;
-          lo[a][b] = lo[a][b] + (t + e);
+          const double t = fma(av[a], zv[b], anc[a]);
+          const double ph = t - anc[a];
+          hi[a][b] += ph;
+          lo[a][b] += fma(av[a], zv[b], -ph);
         }
     }
 #pragma unroll
@@ -264,7 +274,8 @@ __global__ void __launch_bounds__(kST, 1) k_spd_hyb(AlgArgs a, double* gws, int6
   s.C = s.T + 8 * s.ld;
   s.P = s.C + 8 * s.ld;
   s.piv = s.P + 128;
-  s.red = s.piv + nmax;
+  s.rsum = s.piv + nmax;
+  s.red = s.rsum + nmax;
   s.sidx = reinterpret_cast<int*>(s.red + 2 * kSW);
   s.flag = s.sidx + nmax;
   double* Bg = gws + static_cast<int64_t>(blockIdx.x) * slot;  // n x ldz right-hand sides
@@ -304,9 +315,16 @@ __global__ void __launch_bounds__(kST, 1) k_spd_hyb(AlgArgs a, double* gws, int6
       const int i = t / ldz, c = t - i * ldz;
       Bg[t] = c == nr ? a.f[boff + s.sidx[i]] : 0.0;
     }
-    double dummy0 = 0.0;
-    blk_max2(mx, dummy0, s.red);
+    double bmax = 1.0;  // max |B|: unit / weighted constraint columns and f_T
+    for (int i = tid; i < n; i += kST) bmax = fmax(bmax, fabs(a.f[boff + s.sidx[i]]));
+    for (int64_t q = a.cptr[g0] + tid; q < a.cptr[g0 + nr]; q += kST) bmax = fmax(bmax, fabs(a.cent_v[q]));
+    blk_max2(mx, bmax, s.red);
     double thr = 1e-14 * mx;
+    for (int i = tid; i < n; i += kST) {  // row sums of |A| (the block, symmetric lower triangle loaded)
+      double rs = 0.0;
+      for (int k = 0; k < n; ++k) rs += fabs(k <= i ? s.W[i * ld + k] : s.W[k * ld + i]);
+      s.rsum[i] = rs;
+    }
     for (int64_t q = a.cptr[g0] + tid; q < a.cptr[g0 + nr]; q += kST)
       Bg[a.cent_a[q] * ldz + a.cent_r[q]] = a.cent_v[q];
     SPD_T(1);
@@ -455,9 +473,12 @@ __global__ void __launch_bounds__(kST, 1) k_spd_hyb(AlgArgs a, double* gws, int6
     }
     __syncthreads();
     SPD_T(6);
+    double zb = 0.0, dummy1 = 0.0;  // max |Z|: the residual anchors' bound
+    for (int t = tid; t < n * ldz; t += kST) zb = fmax(zb, fabs(s.Z[t]));
+    blk_max2(zb, dummy1, s.red);
     double prev = 0.0;
     for (int step = 0; step < 6; ++step) {
-      residual(n, nc, A, s, Bg);
+      residual(n, nc, A, s, Bg, zb, bmax);
       __syncthreads();
       SPD_T(7);
 #ifdef HDR_SPD_TIMING
@@ -485,6 +506,7 @@ __global__ void __launch_bounds__(kST, 1) k_spd_hyb(AlgArgs a, double* gws, int6
             }
       }
       blk_max2(cm, zm, s.red);
+      zb = zm;
       // the next correction is about rho * cm; rho = observed contraction (first
       // step: the relative size of the correction itself)
       const double rho = step > 0 ? fmin(1.0, prev > 0.0 ? cm / prev : 1.0) : (zm > 0.0 ? cm / zm : 0.0);
@@ -519,7 +541,7 @@ __global__ void __launch_bounds__(kST, 1) k_spd_hyb(AlgArgs a, double* gws, int6
 
 size_t spd_smem_bytes(int nmax, int ncmax) {
   const size_t ld = (nmax + 1) & ~1, ldz = (ncmax + 3) & ~3;
-  return (nmax * ld + 2 * nmax * ldz + 16 * ld + 128 + nmax + 2 * kSW) * 8 + static_cast<size_t>(nmax + 2) * 4;
+  return (nmax * ld + 2 * nmax * ldz + 16 * ld + 128 + 2 * nmax + 2 * kSW) * 8 + static_cast<size_t>(nmax + 2) * 4;
 }
 
 }  // namespace
