@@ -340,17 +340,28 @@ __global__ void __launch_bounds__(kST, 1) k_spd_hyb(AlgArgs a, double* gws, int6
       const int ke = block_end(kb, n, ni), w = ke - kb;
       const int kn = ke < n ? block_end(ke, n, ni) : ke;  // next block [ke, kn)
       const double* P = s.P + 64 * cur;
-      // C[m][i] = A_i,kb+m (lower triangle), T[k][i] = (A_iB P^-1)_k = -sum_m C[m][i] Sw[m][k]  (i outside B)
-      for (int t = tid; t < w * n; t += kST) {
-        const int k = t / n, i = t - k * n;
+      // C[m][i] = A_i,kb+m (lower triangle), T[k][i] = (A_iB P^-1)_k = -sum_m C[m][i] Sw[m][k]  (i outside B):
+      // thread (i, kq) loads row i's block entries once and makes T for k in [3 kq, 3 kq + 3)
+      for (int t = tid; t < 3 * n; t += kST) {
+        const int kq = t / n, i = t - kq * n;
         if (i >= kb && i < ke) continue;
-        double acc = 0.0;
-        for (int m = 0; m < w; ++m) {
-          const double c = (i > kb + m) ? s.W[i * ld + kb + m] : s.W[(kb + m) * ld + i];
-          if (k == 0) s.C[m * ld + i] = c;
-          acc = fma(c, P[m * 8 + k], acc);
+        double cv[8];
+#pragma unroll
+        for (int m = 0; m < 8; ++m)
+          cv[m] = m < w ? ((i > kb + m) ? s.W[i * ld + kb + m] : s.W[(kb + m) * ld + i]) : 0.0;
+        if (kq == 0)
+#pragma unroll
+          for (int m = 0; m < 8; ++m)
+            if (m < w) s.C[m * ld + i] = cv[m];
+#pragma unroll
+        for (int kk = 0; kk < 3; ++kk) {
+          const int k = 3 * kq + kk;
+          if (k >= w) break;
+          double acc = 0.0;
+#pragma unroll
+          for (int m = 0; m < 8; ++m) acc = fma(cv[m], P[m * 8 + k], acc);
+          s.T[k * ld + i] = -acc;
         }
-        s.T[k * ld + i] = -acc;
       }
       __syncthreads();
       SPD_T(2);
