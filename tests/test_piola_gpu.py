@@ -152,3 +152,34 @@ def test_config4_full_size_sampled_rows_vs_dd():
     e_h, e_g = worst_h / np.max(np.abs(hv)), worst_g / np.max(np.abs(gv))
     print(f"config 4 full size: {checked} sampled H entries, H {e_h:.1e} g {e_g:.1e}")
     assert e_h <= TOL and e_g <= TOL
+
+
+def test_mapped_blocks_not_positive_definite_or_singular_are_reported():
+    """The SPD elimination of mapped cells checks every LDL^T pivot with the
+    reference's SingularBlock rule (dense.cpp:61-97): a cell with alpha = beta = 0
+    (zero block) raises SingularBlockError, one with a negative coefficient pair
+    (negative definite block) is not SPD and raises UnsupportedError; both name
+    the element, and the space stays usable afterwards."""
+    o, sp = _setup((3, 2, 2), 2, 1004)
+    a, b, f = o.get("alpha").copy(), o.get("beta").copy(), o.get("f_hat")
+    a0, b0 = a.copy(), b.copy()
+    a[5] = b[5] = 0.0
+    with pytest.raises(hd.SingularBlockError, match="element 5"):
+        sp.hybridize(a, b, f)
+    a, b = a0.copy(), b0.copy()
+    a[7], b[7] = -a[7], -b[7]
+    with pytest.raises(hd.UnsupportedError, match="element 7"):
+        sp.hybridize(a, b, f)
+    hv, g = sp.hybridize(a0, b0, f).values()
+    assert np.all(np.isfinite(hv)) and np.all(np.isfinite(g))
+
+
+def test_batch_empty_and_partial_outputs():
+    """hdr_hybridize_fe_batch: count 0 is a no-op; NULL outputs skip the download."""
+    sp = hd.Space(3, (4, 3, 2), 1)
+    sp.hybridize_batch([], [], [])
+    rng = np.random.default_rng(3)
+    a, b, f = rng.uniform(1, 2, sp.ncells), rng.uniform(1, 2, sp.ncells), rng.uniform(-1, 1, sp.broken_ndofs)
+    g_out = [np.full(sp.m, np.nan)]
+    sp.hybridize_batch([a], [b], [f], None, g_out)
+    assert np.array_equal(g_out[0], sp.hybridize(a, b, f).values()[1])
