@@ -763,46 +763,75 @@ void launch_hybridize_big(const HybArgs& a, int k, int parity, double* gws, cons
 // ---------------------------------------------------------------------------
 // Per-cell products with fixed matrices, batched over all cells as one fp64
 // GEMM before the element kernel: pre(:, e) = [N0 ; X^T] f_e (column-major,
-// ld = N + R).  A tiled GEMM (64 x 64 output tile per 256-thread CTA, 4 x 4
-// fp64 register tiles, K staged in shared memory by 16).
+// ld = N + R), on the fp64 tensor cores: a 128-thread CTA owns a 64 x 64 output
+// tile (warp tiles of 32 x 32 = 4 x 4 DMMA m8n8k4 blocks); K staged in shared
+// memory by 16, double-buffered, with row strides = 4 mod 16 so the fragment
+// loads (8 rows x 4 k) hit every bank pair twice.
 namespace hdr {
 namespace {
-__global__ void __launch_bounds__(256) k_gemm_f64_nn(int M, int Ncol, int Kd, const double* A, int lda,
+constexpr int kGS = 68;  // shared row stride (doubles) of the staged tiles
+__global__ void __launch_bounds__(128) k_gemm_f64_nn(int M, int Ncol, int Kd, const double* A, int lda,
                                                      const double* B, int ldb, double* C, int ldc) {
-  __shared__ double As[16][64 + 1];
-  __shared__ double Bs[16][64 + 1];
-  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  __shared__ __align__(16) double As[2][16][kGS];  // As[k][m]
+  __shared__ __align__(16) double Bs[2][16][kGS];  // Bs[k][n]
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
   const int m0 = blockIdx.y * 64, n0 = blockIdx.x * 64;
-  double acc[4][4] = {};
-  for (int k0 = 0; k0 < Kd; k0 += 16) {
-    for (int t = threadIdx.x; t < 16 * 64; t += 256) {
-      const int kk = t / 64, mm = t % 64;
-      As[kk][mm] = (m0 + mm < M && k0 + kk < Kd) ? A[(m0 + mm) + static_cast<int64_t>(lda) * (k0 + kk)] : 0.0;
-      const int nn = t / 16, k2 = t % 16;
-      Bs[k2][nn] = (n0 + nn < Ncol && k0 + k2 < Kd) ? B[(k0 + k2) + static_cast<int64_t>(ldb) * (n0 + nn)] : 0.0;
+  const int wm = (warp & 1) * 32, wn = (warp >> 1) * 32;
+  double d[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) d[i][j][0] = d[i][j][1] = 0.0;
+  double ra[8], rb[8];  // the next chunk's tiles in flight (global -> registers) during this chunk's MMAs
+  auto fetch = [&](int k0) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {  // 16 x 64 each: 1024 entries / 128 threads
+      const int q = tid + u * 128;
+      const int kk = q >> 6, mm = q & 63;  // A: k-major rows of 64 consecutive m
+      ra[u] = (m0 + mm < M && k0 + kk < Kd) ? A[(m0 + mm) + static_cast<int64_t>(lda) * (k0 + kk)] : 0.0;
+      const int nn = q >> 4, k2 = q & 15;  // B: column nn holds 16 consecutive k
+      rb[u] = (n0 + nn < Ncol && k0 + k2 < Kd) ? B[(k0 + k2) + static_cast<int64_t>(ldb) * (n0 + nn)] : 0.0;
     }
-    __syncthreads();
+  };
+  auto stash = [&](int buf) {
 #pragma unroll
-    for (int kk = 0; kk < 16; ++kk) {
-      double a[4], b[4];
+    for (int u = 0; u < 8; ++u) {
+      const int q = tid + u * 128;
+      As[buf][q >> 6][q & 63] = ra[u];
+      Bs[buf][q & 15][q >> 4] = rb[u];
+    }
+  };
+  fetch(0);
+  stash(0);
+  __syncthreads();
+  const int nk = (Kd + 15) / 16;
+  for (int c = 0; c < nk; ++c) {
+    const int buf = c & 1;
+    if (c + 1 < nk) fetch((c + 1) * 16);
 #pragma unroll
-      for (int i = 0; i < 4; ++i) a[i] = As[kk][ty * 4 + i];
+    for (int ks = 0; ks < 4; ++ks) {
+      double af[4], bf[4];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx * 4 + j];
+      for (int i = 0; i < 4; ++i) af[i] = As[buf][4 * ks + t][wm + 8 * i + g];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bf[j] = Bs[buf][4 * ks + t][wn + 8 * j + g];
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+        for (int j = 0; j < 4; ++j) dmma_8x8x4(d[i][j][0], d[i][j][1], af[i], bf[j]);
     }
+    if (c + 1 < nk) stash(buf ^ 1);
     __syncthreads();
   }
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int m = m0 + ty * 4 + i, n = n0 + tx * 4 + j;
-      if (m < M && n < Ncol) C[m + static_cast<int64_t>(ldc) * n] = acc[i][j];
-    }
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int m = m0 + wm + 8 * i + g, n = n0 + wn + 8 * j + 2 * t + q;
+        if (m < M && n < Ncol) C[m + static_cast<int64_t>(ldc) * n] = d[i][j][q];
+      }
 }
 }  // namespace
 
@@ -810,7 +839,7 @@ void launch_gemm_f64_nn(int M, int Ncol, int Kd, const double* A, int lda, const
                         int ldc, cudaStream_t st) {
   if (M <= 0 || Ncol <= 0) return;
   dim3 grid(static_cast<unsigned>((Ncol + 63) / 64), static_cast<unsigned>((M + 63) / 64));
-  k_gemm_f64_nn<<<grid, 256, 0, st>>>(M, Ncol, Kd, A, lda, B, ldb, C, ldc);
+  k_gemm_f64_nn<<<grid, 128, 0, st>>>(M, Ncol, Kd, A, lda, B, ldb, C, ldc);
   count_launch();
 }
 }  // namespace hdr
