@@ -390,9 +390,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_hyb_big(HybArgs A, int parity, 
     const double a = A.alpha[e], b = A.beta[e];
     const double ib = 1.0 / b;
     const double* fe = A.f + static_cast<int64_t>(e) * N;
-    // scatter tables (cell geometry only), computed up front; the shared
-    // diagonal blocks' partial sums (colour 1 adds to colour 0's) are prefetched
-    // into L2 now and read back by the scatter
+    // scatter tables (cell geometry only) and an L2 prefetch of the shared
+    // diagonal blocks' partial sums (colour 1 adds to colour 0's): made by warp 15
+    // during the first V block, where it has one tile fewer than warps 0..13
+    auto scatter_tables = [&](int lane_) {
     {
       unsigned lo = 0, hi = 0;
 #pragma unroll
@@ -402,7 +403,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_hyb_big(HybArgs A, int parity, 
         lo |= static_cast<unsigned>(cx > 0) << x;
         hi |= static_cast<unsigned>(cx + 1 < Nx) << x;
       }
-      for (int idx = tid; idx < NS * NS; idx += kThreads) {
+      for (int idx = lane_; idx < NS * NS; idx += 32) {
         const int ps = idx / NS, qs = idx - ps * NS;
         const int a_ = ps >> 1;
         const bool pin = (((ps & 1) ? hi : lo) >> a_) & 1u;
@@ -426,9 +427,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_hyb_big(HybArgs A, int parity, 
         }
       }
     }
-    __syncthreads();
+    __syncwarp();
     if (parity == 1)
-      for (int q = tid; q < NS * DPF * (DPF * 8 / 128 + 1); q += kThreads) {
+      for (int q = lane_; q < NS * DPF * (DPF * 8 / 128 + 1); q += 32) {
         const int ps = q / (DPF * (DPF * 8 / 128 + 1)), rem = q - ps * (DPF * (DPF * 8 / 128 + 1));
         const int sub = rem / (DPF * 8 / 128 + 1), part = rem - sub * (DPF * 8 / 128 + 1);
         const int64_t rs = sm.rstart[ps];
@@ -437,15 +438,25 @@ __global__ void __launch_bounds__(kThreads, 1) k_hyb_big(HybArgs A, int parity, 
         const double* line = A.hval + rs + static_cast<int64_t>(sub) * sm.rlen[ps] + rk * DPF + part * 16;
         asm volatile("prefetch.global.L2 [%0];" ::"l"(line));
       }
+    };
     // ---------------------------------------------------------------- phase V (fp64)
+    // X_F (rows of the face dofs) for z = s X_F^T: all loads in flight before the barrier
+    constexpr int ZPT = (R * NF + kThreads - 1) / kThreads;
+    double xz[ZPT];
+#pragma unroll
+    for (int u = 0; u < ZPT; ++u) {  // j fastest: coalesced rows of X
+      const int idx = tid + u * kThreads, c = idx / R, j = idx - c * R;
+      xz[u] = idx < R * NF ? __ldg(fx.X + (NINT + c) * R + j) : 0.0;
+    }
     for (int i = tid; i < N; i += kThreads) sm.f[i] = fe[i];
     for (int j = tid; j < R; j += kThreads) sm.s[j] = b / fma(a, __ldg(fx.lam + j), b);
-    __syncthreads();
     const double* pe = pre + static_cast<int64_t>(e) * (N + R);  // [N0 f_e ; X^T f_e], batched GEMM
     for (int i = tid; i < N; i += kThreads) sm.nf[i] = pe[i];
-    for (int idx = tid; idx < R * NF; idx += kThreads) {  // j fastest: coalesced rows of X
-      const int c = idx / R, j = idx - c * R;
-      sm.u.pv.z[j * B::NZ + c] = sm.s[j] * __ldg(fx.X + (NINT + c) * R + j);
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < ZPT; ++u) {
+      const int idx = tid + u * kThreads, c = idx / R, j = idx - c * R;
+      if (idx < R * NF) sm.u.pv.z[j * B::NZ + c] = sm.s[j] * xz[u];
     }
     for (int j = tid; j < B::RP; j += kThreads) {
       sm.u.pv.z[j * B::NZ + NF] = j < R ? sm.s[j] * pe[N + j] : 0.0;
@@ -476,6 +487,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_hyb_big(HybArgs A, int parity, 
         const bool more = i0 + IB < N;
         if (more) xload(i0 + IB, xr);  // next block's X rows in flight during this block
         v_block<K>(sm, fx, i0, ib, vf);
+        if (i0 == 0 && (tid >> 5) == kThreads / 32 - 1) scatter_tables(tid & 31);
         if (more) xstore(((i0 / IB) + 1) & 1, xr);
         __syncthreads();
       }
