@@ -45,6 +45,9 @@ __device__ unsigned long long g_spd_prof[16];
   } while (0)
 #endif
 
+#ifndef HDR_SPD_UB
+#define HDR_SPD_UB 1  // measured: 1 -> 18.9 ms, 2 -> 19.0, 4 -> 19.6 (cfg4)
+#endif
 constexpr int kST = 384;
 constexpr int kSW = kST / 32;
 
@@ -138,56 +141,57 @@ __device__ __forceinline__ void tri_tile(int t, int& ti, int& tj) {
   tj = t - ti * (ti + 1) / 2;
 }
 
-// W[i][j] -= sum_k T[k][i] C[k][j] for the tile's (i, j) outside B, i >= j
-// (lower triangle only; C = the block's columns before the step, T = C P^-1)
-__device__ __forceinline__ void sweep_tile(double* W, int ld, const double* T, const double* C, int n, int kb, int ke,
-                                           int ti, int tj) {
-  const int i0 = 4 * ti, j0 = 4 * tj, w = ke - kb;
-  double cur[4][4];
+__device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+// W[i][j] -= sum_k T[k][i] C[k][j] on the 8 x 8 block (bi, bj), bi >= bj, by one
+// warp on the fp64 tensor cores (two DMMA m8n8k4; fragments a = (row g, k t),
+// b = (k t, col g), d = (row g, cols 2t, 2t + 1) with g = lane / 4, t = lane % 4).
+// Rows / columns >= n are left alone.  Entries in the pivot block's rows or
+// columns and above the diagonal are updated too: the write-back rewrites the
+// former, the latter are dead until the final mirror.
+template <int NB>
+__device__ __forceinline__ void sweep_blocks(double* W, int ld, const double* T, const double* C, int n, int w,
+                                             const int (&bi)[NB], const int (&bj)[NB]) {
+  // NB independent blocks per call: their loads and MMAs interleave (latency)
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  double d0[NB], d1[NB];
 #pragma unroll
-  for (int r = 0; r < 4; ++r) {  // the tile's current values, early (latency)
-    const double2 a0 = *reinterpret_cast<const double2*>(W + (i0 + r) * ld + j0);
-    const double2 a1 = *reinterpret_cast<const double2*>(W + (i0 + r) * ld + j0 + 2);
-    cur[r][0] = a0.x;
-    cur[r][1] = a0.y;
-    cur[r][2] = a1.x;
-    cur[r][3] = a1.y;
+  for (int q = 0; q < NB; ++q) {
+    const int r = 8 * bi[q] + g, c = 8 * bj[q] + 2 * t;
+    const bool rok = bi[q] >= 0 && r < n;
+    d0[q] = rok && c < n ? W[r * ld + c] : 0.0;
+    d1[q] = rok && c + 1 < n ? W[r * ld + c + 1] : 0.0;
   }
-  double acc[4][4];
 #pragma unroll
-  for (int r = 0; r < 4; ++r)
+  for (int ks = 0; ks < 2; ++ks) {
+    const int k = 4 * ks + t;
+    double av[NB], bv[NB];
 #pragma unroll
-    for (int c = 0; c < 4; ++c) acc[r][c] = 0.0;
-#pragma unroll 4
-  for (int k = 0; k < w; ++k) {
-    const double2 t0 = *reinterpret_cast<const double2*>(T + k * ld + i0);
-    const double2 t1 = *reinterpret_cast<const double2*>(T + k * ld + i0 + 2);
-    const double2 c0v = *reinterpret_cast<const double2*>(C + k * ld + j0);
-    const double2 c1v = *reinterpret_cast<const double2*>(C + k * ld + j0 + 2);
-    const double tv[4] = {t0.x, t0.y, t1.x, t1.y}, cv[4] = {c0v.x, c0v.y, c1v.x, c1v.y};
-#pragma unroll
-    for (int r = 0; r < 4; ++r)
-#pragma unroll
-      for (int c = 0; c < 4; ++c) acc[r][c] = fma(tv[r], cv[c], acc[r][c]);
-  }
-  const bool full = i0 + 4 <= n && (ti != tj) && !(i0 + 4 > kb && i0 < ke) && !(j0 + 4 > kb && j0 < ke);
-  if (full) {
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      *reinterpret_cast<double2*>(W + (i0 + r) * ld + j0) = make_double2(cur[r][0] - acc[r][0], cur[r][1] - acc[r][1]);
-      *reinterpret_cast<double2*>(W + (i0 + r) * ld + j0 + 2) =
-          make_double2(cur[r][2] - acc[r][2], cur[r][3] - acc[r][3]);
+    for (int q = 0; q < NB; ++q) {
+      const int i = 8 * bi[q] + g, j = 8 * bj[q] + g;
+      av[q] = (bi[q] >= 0 && k < w && i < n) ? -T[k * ld + i] : 0.0;
+      bv[q] = (bi[q] >= 0 && k < w && j < n) ? C[k * ld + j] : 0.0;
     }
-  } else {
 #pragma unroll
-    for (int r = 0; r < 4; ++r)
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const int i = i0 + r, j = j0 + c;
-        if (i >= n || j > i || (i >= kb && i < ke) || (j >= kb && j < ke)) continue;
-        W[i * ld + j] = cur[r][c] - acc[r][c];
-      }
+    for (int q = 0; q < NB; ++q) dmma_8x8x4(d0[q], d1[q], av[q], bv[q]);
   }
+#pragma unroll
+  for (int q = 0; q < NB; ++q) {
+    const int r = 8 * bi[q] + g, c = 8 * bj[q] + 2 * t;
+    if (bi[q] < 0 || r >= n) continue;
+    if (c < n) W[r * ld + c] = d0[q];
+    if (c + 1 < n) W[r * ld + c + 1] = d1[q];
+  }
+}
+
+__device__ __forceinline__ void sweep_block(double* W, int ld, const double* T, const double* C, int n, int w, int bi,
+                                            int bj) {
+  const int ri[1] = {bi}, rj[1] = {bj};
+  sweep_blocks<1>(W, ld, T, C, n, w, ri, rj);
 }
 
 // acc (+)= sign * W[i0:i0+4, :] Y[:, c0:c0+4] over k < n (W symmetric: read as rows)
@@ -365,22 +369,19 @@ __global__ void __launch_bounds__(kST, 1) k_spd_hyb(AlgArgs a, double* gws, int6
       }
       __syncthreads();
       SPD_T(2);
-      // trailing update over the tiles not inside B (tile rows/cols tb0..tb1-1
-      // lie fully in B); the tiles touching the next pivot block go to warp 0
-      const int a0 = ke >> 2, a1 = (kn - 1) >> 2;  // tile rows of the next block
-      const int tb0 = (kb + 3) >> 2, tb1 = max(tb0, ke >> 2), nskip = tb1 - tb0;
-      const int nr4 = nb4 - nskip, ntr = nr4 * (nr4 + 1) / 2;
+      // trailing update on 8 x 8 blocks (fp64 tensor cores), lower triangle, blocks
+      // lying fully in B's rows or columns skipped; the blocks of the next pivot
+      // block go to warp 0, which then sweeps it
+      const int nb8 = (n + 7) / 8, a0 = ke >> 3, a1 = (kn - 1) >> 3;
+      const int sb = (kb % 8 == 0 && w == 8) ? kb >> 3 : -1;  // block row / column fully inside B
+      const int nr8 = nb8 - (sb >= 0 ? 1 : 0), ntr = nr8 * (nr8 + 1) / 2;
 #ifdef HDR_SPD_TIMING
       const long long tw0 = clock64();
 #endif
       if (warp == 0) {
         if (kn > ke) {
-          const int nt = a1 - a0 + 1;
-          for (int q = threadIdx.x; q < nt * (nt + 1) / 2; q += 32) {
-            int qi, qj;
-            tri_tile(q, qi, qj);
-            sweep_tile(s.W, ld, s.T, s.C, n, kb, ke, a0 + qi, a0 + qj);
-          }
+          for (int bi = a0; bi <= a1; ++bi)
+            for (int bj = a0; bj <= bi; ++bj) sweep_block(s.W, ld, s.T, s.C, n, w, bi, bj);
           __syncwarp();
 #ifdef HDR_SPD_TIMING
           if (blockIdx.x == 0 && threadIdx.x == 0) g_spd_prof[11] += clock64() - tw0;
@@ -391,13 +392,24 @@ __global__ void __launch_bounds__(kST, 1) k_spd_hyb(AlgArgs a, double* gws, int6
 #endif
         }
       } else {
-        for (int t = tid - 32; t < ntr; t += kST - 32) {
-          int ti, tj;
-          tri_tile(t, ti, tj);
-          ti += (ti >= tb0) ? nskip : 0;
-          tj += (tj >= tb0) ? nskip : 0;
-          if (kn > ke && ti >= a0 && ti <= a1 && tj >= a0 && tj <= a1) continue;
-          sweep_tile(s.W, ld, s.T, s.C, n, kb, ke, ti, tj);
+        constexpr int UB = HDR_SPD_UB;  // blocks per warp in flight
+        for (int q0 = warp - 1; q0 < ntr; q0 += UB * (kSW - 1)) {
+          int bi[UB], bj[UB];
+#pragma unroll
+          for (int u = 0; u < UB; ++u) {
+            const int q = q0 + u * (kSW - 1);
+            bi[u] = -1;
+            bj[u] = 0;
+            if (q >= ntr) continue;
+            int ti, tj;
+            tri_tile(q, ti, tj);
+            ti += (sb >= 0 && ti >= sb) ? 1 : 0;
+            tj += (sb >= 0 && tj >= sb) ? 1 : 0;
+            if (kn > ke && ti >= a0 && ti <= a1 && tj >= a0 && tj <= a1) continue;
+            bi[u] = ti;
+            bj[u] = tj;
+          }
+          sweep_blocks<UB>(s.W, ld, s.T, s.C, n, w, bi, bj);
         }
 #ifdef HDR_SPD_TIMING
         if (blockIdx.x == 0 && threadIdx.x == 32) g_spd_prof[13] += clock64() - tw0;
