@@ -52,6 +52,7 @@ struct Big {
   static constexpr int MT1 = (N + 127) / 128, MP = MT1 * 128;
   static constexpr int NP = (NC + 15) / 16 * 16, KP = (N + 15) / 16 * 16;
   static constexpr int NY = KP, NFP = (NF + 15) / 16 * 16;
+  static constexpr int KC2 = 32, NCH2 = (KP + KC2 - 1) / KC2;  // C^T product chunks
   static constexpr int KC = 16;  // K per operand chunk (two K=8 MMA steps)
   static constexpr int TCOLS_USED = NY + NFP;
   static constexpr int TCOLS = TCOLS_USED <= 32 ? 32 : TCOLS_USED <= 64 ? 64 : TCOLS_USED <= 128 ? 128 : TCOLS_USED <= 256 ? 256 : 512;
@@ -96,6 +97,10 @@ struct BigSmem {
       float ahi[128 * B::KC], alo[128 * B::KC];    // V^T / Y^T chunk (M = 128)
       float bhi[B::NY * B::KC], blo[B::NY * B::KC];  // Delta chunk (N = NY) / V_F chunk (N = NFP)
     } tc[2];    // double-buffered: chunk c + 1 is generated while the MMAs of chunk c run
+    struct {  // the C^T product's operand chunks, K = KC2 (fewer, longer chunks)
+      float ahi[128 * B::KC2], alo[128 * B::KC2];    // Y^T chunk (from TMEM)
+      float bhi[B::NFP * B::KC2], blo[B::NFP * B::KC2];  // V_F chunk
+    } tc2[2];
     float csm[B::NF * B::NCP];  // the correction C (NF x NC) for the scatter
   } u;
   double f[B::N], nf[B::N], s[B::R];
@@ -306,24 +311,32 @@ __device__ void correction_tc(BigSmem<K>& sm, const Fixed& fx, double a, double 
 #ifdef HDR_BIG_TIMING
   if (blockIdx.x == 0 && threadIdx.x == 0) g_big_prof[13] = clock64();
 #endif
-  // ---- C^T = Y^T V_F  (A operand: Y^T chunk from TMEM; lane c holds row c)
-  for (int c = 0; c < NCH; ++c) {
-    const int bf = c & 1, kc = c * KC;
-    auto& T = sm.u.tc[bf];
+  // ---- C^T = Y^T V_F  (A operand: Y^T chunk from TMEM; lane c holds row c), K = 32 per chunk
+  constexpr int KC2 = B::KC2, NCH2 = B::NCH2;
+  for (int c = 0; c < NCH2; ++c) {
+    const int bf = c & 1, kc = c * KC2;
+    auto& T = sm.u.tc2[bf];
     if (c >= 2) wait_buf(bf);
-    {  // the 4 warps of lane quadrant q = warp % 4 take 4 columns each
-      const int q = warp & 3, k0 = 4 * (warp >> 2), m = 32 * q + lane;
-      float v[4];
-      umma::tmem_ld4(tY + (static_cast<uint32_t>(32 * q) << 16) + kc + k0, v);
-      float hi[4], lo[4];
+    {  // the 4 warps of lane quadrant q = warp % 4 take 8 columns each (columns >= N: zero)
+      const int q = warp & 3, k0 = 8 * (warp >> 2), m = 32 * q + lane;
+      float v[8];
+      if (kc + k0 < N) {
+        umma::tmem_ld8(tY + (static_cast<uint32_t>(32 * q) << 16) + kc + k0, v);
+      } else {
 #pragma unroll
-      for (int j = 0; j < 4; ++j) tf32_split(v[j], hi[j], lo[j]);
-      const uint32_t off = umma::kmajor_offset(m, k0, 128) >> 2;  // 4 consecutive k: 16 bytes
-      *reinterpret_cast<float4*>(T.ahi + off) = make_float4(hi[0], hi[1], hi[2], hi[3]);
-      *reinterpret_cast<float4*>(T.alo + off) = make_float4(lo[0], lo[1], lo[2], lo[3]);
+        for (int j = 0; j < 8; ++j) v[j] = 0.f;
+      }
+      float hi[8], lo[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) tf32_split(kc + k0 + j < N ? v[j] : 0.f, hi[j], lo[j]);
+      const uint32_t off0 = umma::kmajor_offset(m, k0, 128) >> 2, off1 = umma::kmajor_offset(m, k0 + 4, 128) >> 2;
+      *reinterpret_cast<float4*>(T.ahi + off0) = make_float4(hi[0], hi[1], hi[2], hi[3]);
+      *reinterpret_cast<float4*>(T.alo + off0) = make_float4(lo[0], lo[1], lo[2], lo[3]);
+      *reinterpret_cast<float4*>(T.ahi + off1) = make_float4(hi[4], hi[5], hi[6], hi[7]);
+      *reinterpret_cast<float4*>(T.alo + off1) = make_float4(lo[4], lo[5], lo[6], lo[7]);
     }
-    for (int g = warp; g < NFP / 2; g += 16) {  // V_F chunk: lane -> (f % 8, k % 4)
-      const int f = 8 * (g >> 2) + (lane >> 2), k = 4 * (g & 3) + (lane & 3), row = kc + k;
+    for (int g = warp; g < NFP / 8 * (KC2 / 4); g += 16) {  // V_F chunk: lane -> (f % 8, k % 4)
+      const int f = 8 * (g / (KC2 / 4)) + (lane >> 2), k = 4 * (g % (KC2 / 4)) + (lane & 3), row = kc + k;
       const float x = (f < NF && row < N) ? sm.v32[row * NCP + f] : 0.f;
       const uint32_t off = umma::kmajor_offset(f, k, NFP) >> 2;
       tf32_split(x, T.bhi[off], T.blo[off]);
@@ -332,12 +345,20 @@ __device__ void correction_tc(BigSmem<K>& sm, const Fixed& fx, double a, double 
     umma::fence_before();
     __syncthreads();
     if (tid == 0) {
-      issue(T, c, tC, idesc2, lbo_b2);
+      umma::fence_after();
+      for (int ks = 0; ks < KC2 / 8; ++ks)
+        for (int term = 0; term < 3; ++term) {
+          const float* aop = term == 2 ? T.alo : T.ahi;
+          const float* bop = term == 1 ? T.blo : T.bhi;
+          const uint64_t ad = umma::smem_desc(umma::smem_u32(aop) + ks * 2 * lbo_a, lbo_a, 128);
+          const uint64_t bd = umma::smem_desc(umma::smem_u32(bop) + ks * 2 * lbo_b2, lbo_b2, 128);
+          umma::mma_tf32(tC, ad, bd, idesc2, c > 0 || ks > 0 || term > 0);
+        }
       umma::commit(&sm.mbar[bf]);
     }
   }
-  wait_buf(NCH & 1);
-  wait_buf((NCH - 1) & 1);
+  wait_buf(NCH2 & 1);
+  wait_buf((NCH2 - 1) & 1);
   // ---- C^T -> C in shared memory: lane c holds C^T[c][f] = C[f][c]
   {
     const int q = warp & 3, m = 32 * q + lane;
