@@ -62,6 +62,8 @@ struct hdr_space_s {
   DBuf<double> premat;             // k >= 2 (3D): [N0 ; X^T] column-major ((n + r) x n)
   DBuf<double> dtab;               // k >= 2 (3D): {D, M} in the tensor-core chunk order
   DBuf<float> etab;                // k >= 2 (3D): {E, Ma} (fp32) likewise
+  DBuf<double> tdm;                // warp-kernel spaces: {D, M} transposed ((i, l) at l * n + i)
+  DBuf<float> tem;                 // warp-kernel spaces: {E, Ma} (fp32) transposed
   Fixed fx{};
   GeomState* geom = nullptr;  // mapped (trilinear) cells: hdr_space_set_vertices
   struct BatchCtx* batch = nullptr;  // hdr_hybridize_fe_batch: streams, events, two operators
@@ -358,6 +360,22 @@ hdr_status hdr_space_create(int dim, const int64_t cells[3], const double h[3], 
       fx.dtab = reinterpret_cast<const double2*>(sp->dtab.p);
       fx.etab = reinterpret_cast<const float2*>(sp->etab.p);
       CK(cudaStreamSynchronize(st));
+    }
+    if ((dim == 3 && order == 1) || (dim == 2 && order >= 1)) {  // transposed Delta inputs (kern_warp.cu)
+      std::vector<double> td(2 * nn);
+      std::vector<float> te(2 * nn);
+      for (int i = 0; i < n; ++i)
+        for (int l = 0; l < n; ++l) {
+          const size_t q = static_cast<size_t>(l) * n + i, o = static_cast<size_t>(i) * n + l;
+          td[2 * q] = sp->re.divdiv[o];
+          td[2 * q + 1] = sp->re.mass[o];
+          te[2 * q] = static_cast<float>(sp->st.E[o]);
+          te[2 * q + 1] = static_cast<float>(sp->st.Ma[o]);
+        }
+      sp->tdm.upload(td);
+      sp->tem.upload(te);
+      fx.tdm = reinterpret_cast<const double2*>(sp->tdm.p);
+      fx.tem = reinterpret_cast<const float2*>(sp->tem.p);
     }
     if (order == 0) {  // constant block for the register kernel: D, M, E, Ma, N0, X, lam, rho
       sp->rt0_consts.assign(pack.begin(), pack.begin() + 5 * nn + n + 1);

@@ -259,10 +259,16 @@ __device__ __forceinline__ void warp_cell(const HybArgs& A, int e, int parity, i
     }
   }
   // Delta32^T (fp64 exact rounding errors -> fp32)
+  // (transposed input tables: contiguous loads and stores; alpha E + beta Ma in fp32)
+  const float af = static_cast<float>(a), bfl = static_cast<float>(b);
   for (int idx = lane; idx < N * N; idx += GT) {
-    const int i = idx / N, l = idx - i * N;
-    sm.d32t[l * N + i] = static_cast<float>(
-        delta_entry(a, b, __ldg(fx.D + idx), __ldg(fx.M + idx), __ldg(fx.E + idx), __ldg(fx.Ma + idx)));
+    const double2 dm = __ldg(fx.tdm + idx);
+    const float2 em = __ldg(fx.tem + idx);
+    double p1, e1, p2, e2, s_, e3;
+    two_prod(a, dm.x, p1, e1);
+    two_prod(b, dm.y, p2, e2);
+    two_sum(p1, p2, s_, e3);
+    sm.d32t[idx] = fmaf(af, em.x, fmaf(bfl, em.y, static_cast<float>(-((e1 + e2) + e3))));
   }
   gsync<GT>();
   // first order: Y = Delta32 [V | w];  C = V_F^T Y

@@ -29,6 +29,10 @@ struct Fixed {  // device pointers to the per-space fixed factors (see hdr_inter
   // kern_cta.cu (chunk c, row m < MP, k < 16 -> column 16 c + k; zero padded)
   const double2* dtab;  // {D, M}
   const float2* etab;   // {E, Ma} (tiny: fp32 carries them to 6e-8 relative)
+  // warp-kernel spaces (RT1 hexes, RT1-3 quads): the same inputs transposed,
+  // entry l * n + i = (i, l), so Delta^T is generated with contiguous loads and stores
+  const double2* tdm;   // {D, M}
+  const float2* tem;    // {E, Ma}
   int r;
   double rho;
 };
