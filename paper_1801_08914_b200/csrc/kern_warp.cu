@@ -200,11 +200,16 @@ __device__ __forceinline__ void warp_cell(const HybArgs& A, int e, int parity, i
   for (int i = lane; i < N; i += GT) sm.f[i] = fe[i];
   for (int j = lane; j < R; j += GT) sm.s[j] = b / fma(a, __ldg(fx.lam + j), b);
   gsync<GT>();
-  for (int i = lane; i < N; i += GT) {
+  // nf = N0 f: each row's dot product split over 4 consecutive lanes (l = part mod 4)
+  for (int i0 = 0; i0 < N; i0 += GT / 4) {
+    const int i = i0 + (lane >> 2), part = lane & 3;
     double acc = 0.0;
-#pragma unroll 6
-    for (int l = 0; l < N; ++l) acc = fma(cs.n0[i * N + l], sm.f[l], acc);
-    sm.nf[i] = acc;
+    if (i < N)
+#pragma unroll 3
+      for (int l = part; l < N; l += 4) acc = fma(cs.n0[i * N + l], sm.f[l], acc);
+    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+    acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+    if (i < N && part == 0) sm.nf[i] = acc;
   }
   // z = [s X_F^T | s X^T f]; the X^T f dots are split over 4 lanes each
   for (int idx = lane; idx < R * NF; idx += GT) {
