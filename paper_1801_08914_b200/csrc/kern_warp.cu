@@ -82,7 +82,8 @@ template <int DIM, int K>
 struct CtaShared {  // fixed per space, staged once per CTA
   using S = Shape<DIM, K>;
   double xt[S::R * S::N];  // X^T
-  double n0[S::N * S::N];  // N0
+  // (N0 is read through the read-only cache: 10 KB, L1-resident; keeping it out of
+  // shared memory lets more cell groups reside per SM)
 };
 
 // C[M x NN] = A[M x KK] * B[KK x NN] on one warp, operands in shared memory:
@@ -206,7 +207,7 @@ __device__ __forceinline__ void warp_cell(const HybArgs& A, int e, int parity, i
     double acc = 0.0;
     if (i < N)
 #pragma unroll 3
-      for (int l = part; l < N; l += 4) acc = fma(cs.n0[i * N + l], sm.f[l], acc);
+      for (int l = part; l < N; l += 4) acc = fma(__ldg(fx.N0 + i * N + l), sm.f[l], acc);
     acc += __shfl_xor_sync(0xffffffffu, acc, 1);
     acc += __shfl_xor_sync(0xffffffffu, acc, 2);
     if (i < N && part == 0) sm.nf[i] = acc;
@@ -256,7 +257,7 @@ __device__ __forceinline__ void warp_cell(const HybArgs& A, int e, int parity, i
         for (int jj = 0; jj < TN; ++jj) {
           const int row = m0 + i, col = n0 + jj;
           if (row >= N || col >= NC) continue;
-          const double base = (col < NF) ? cs.n0[row * N + NINT + col] : sm.nf[row];
+          const double base = (col < NF) ? __ldg(fx.N0 + row * N + NINT + col) : sm.nf[row];
           const double v = (base + acc[i][jj]) * ib;
           sm.v32[row * NCP + col] = static_cast<float>(v);
           if (row >= NINT) sm.vf[(row - NINT) * NC + col] = v;
@@ -333,7 +334,7 @@ __device__ __forceinline__ void warp_cell(const HybArgs& A, int e, int parity, i
     for (int idx = lane; idx < N * NC; idx += GT) {
       const int i = idx / NC, c = idx - i * NC;
       double acc = 0.0;
-      for (int l = 0; l < N; ++l) acc = fma(cs.n0[i * N + l], static_cast<double>(sm.y32[l * NCP + c]), acc);
+      for (int l = 0; l < N; ++l) acc = fma(__ldg(fx.N0 + i * N + l), static_cast<double>(sm.y32[l * NCP + c]), acc);
       for (int j = 0; j < R; ++j) acc = fma(cs.xt[j * N + i], sm.z[j * NC + c], acc);
       tbuf[i * NCP + c] = static_cast<float>(acc * ib);
     }
@@ -420,7 +421,6 @@ __global__ void __launch_bounds__(32 * kWarps) k_hyb_warp(HybArgs A, int parity,
     const int j = idx / S::N, i = idx - j * S::N;
     cs->xt[idx] = __ldg(A.fx.X + i * S::R + j);
   }
-  for (int idx = threadIdx.x; idx < S::N * S::N; idx += blockDim.x) cs->n0[idx] = __ldg(A.fx.N0 + idx);
   __syncthreads();
   double* scratch = gws + (static_cast<int64_t>(blockIdx.x) * CPB + grp) * scratch_doubles_per_warp<DIM, K>();
   const uint32_t cnt = static_cast<uint32_t>(parity_count(A.m));
