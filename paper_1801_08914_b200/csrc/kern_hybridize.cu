@@ -738,10 +738,8 @@ __global__ void __launch_bounds__(BrickDims<DIM, BX>::CT, BrickDims<DIM, BX>::MI
   const DevMesh& m = A.m;
   const int N0 = static_cast<int>(m.N[0]), N1 = static_cast<int>(m.N[1]), N2 = DIM == 3 ? static_cast<int>(m.N[2]) : 1;
   // this colour's bricks: x index alternates within a (by, bz) row
-  const int nbxh = (nbx + 1) >> 1;
-  const int row_ = blockIdx.x / nbxh;
-  const int by = row_ % nby, bz = row_ / nby;
-  const int bx = 2 * (blockIdx.x - row_ * nbxh) + ((by + bz + COL) & 1);
+  const int by = static_cast<int>(blockIdx.y), bz = static_cast<int>(blockIdx.z);  // grid (ceil(nbx / 2), nby, nbz)
+  const int bx = 2 * static_cast<int>(blockIdx.x) + ((by + bz + COL) & 1);
   if (bx >= nbx || bz >= nbz) return;
   const int x0 = bx * X, y0 = by * Y, z0 = bz * Z;
   const int ex = min(X, N0 - x0), ey = min(Y, N1 - y0), ez = DIM == 3 ? min(Z, N2 - z0) : 1;
@@ -1400,13 +1398,13 @@ void launch_hybridize_rt0_rows(const HybArgs& a, const double* hc, double* stage
     using B = BrickDims<D, BXv>;
     const int nbx = static_cast<int>((a.m.N[0] + B::X - 1) / B::X), nby = static_cast<int>((a.m.N[1] + B::Y - 1) / B::Y);
     const int nbz = D == 3 ? static_cast<int>((a.m.N[2] + B::Z - 1) / B::Z) : 1;
-    const unsigned grid = static_cast<unsigned>(((nbx + 1) / 2) * nby * nbz);
+    const dim3 grid(static_cast<unsigned>((nbx + 1) / 2), static_cast<unsigned>(nby), static_cast<unsigned>(nbz));
     const size_t smem = B::smem_bytes();
     cudaFuncSetAttribute(k_rt0_brick<D, 0, BXv>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     cudaFuncSetAttribute(k_rt0_brick<D, 1, BXv>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     k_rt0_brick<D, 0, BXv><<<grid, B::CT, smem, st>>>(a, c, F, stage, nbx, nby, nbz);
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(grid);
+    cfg.gridDim = grid;
     cfg.blockDim = dim3(B::CT);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
