@@ -177,6 +177,55 @@ __device__ __forceinline__ void gemm44(const float* at, int lda, const float* bm
   }
 }
 
+// gemm44 with the K split across the two halves of a 128-thread group instead
+// of across lane pairs: the lanes of a warp then all read the same k row of B,
+// so the 128-bit loads of B are conflict-free (split lane pairs read rows KK/2
+// apart, which share banks).  The upper half parks its partial sums in C, the
+// lower half adds them: (lower + upper), the same sum as the shuffle version.
+template <int M, int NN, int KK, int GT>
+__device__ __forceinline__ void gemm44h(const float* at, int lda, const float* bm, int ldb, float* cm, int ldc,
+                                        int tid) {
+  constexpr int HALF = GT / 2, TMS = (M + 3) / 4, TNS = (NN + 3) / 4, KS = (KK + 1) / 2;
+  static_assert(TMS * TNS <= HALF, "tiles must fit half the group");
+  const int part = tid / HALF, tile = tid - part * HALF;
+  const bool active = tile < TMS * TNS;
+  const int m0 = (tile / TNS) * 4, n0 = (tile % TNS) * 4;
+  float acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
+  if (active) {
+    const int k0 = part * KS, k1 = min(KK, k0 + KS);
+#pragma unroll 4
+    for (int k = k0; k < k1; ++k) {
+      const float4 av = *reinterpret_cast<const float4*>(at + k * lda + m0);
+      const float4 bv = *reinterpret_cast<const float4*>(bm + k * ldb + n0);
+      const float a4[4] = {av.x, av.y, av.z, av.w}, b4[4] = {bv.x, bv.y, bv.z, bv.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a4[i], b4[j], acc[i][j]);
+    }
+    if (part == 1)
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (m0 + i < M && n0 + j < NN) cm[(m0 + i) * ldc + n0 + j] = acc[i][j];
+  }
+  __syncthreads();
+  if (active && part == 0)
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (m0 + i < M && n0 + j < NN) {
+          float* dst = cm + (m0 + i) * ldc + n0 + j;
+          *dst = acc[i][j] + *dst;
+        }
+}
+
 // per-warp global scratch: the higher-order buffer T (N x NCP fp32), rarely used
 template <int DIM, int K>
 constexpr int64_t scratch_doubles_per_warp() {
@@ -280,9 +329,9 @@ __device__ __forceinline__ void warp_cell(const HybArgs& A, int e, int parity, i
   // first order: Y = Delta32 [V | w];  C = V_F^T Y
   float* corr = sm.corr;
   if constexpr (GT == 128) {
-    gemm44<N, NC, N, 2, GT>(sm.d32t, N, sm.v32, NCP, sm.y32, NCP, lane);
+    gemm44h<N, NC, N, GT>(sm.d32t, N, sm.v32, NCP, sm.y32, NCP, lane);
     gsync<GT>();
-    gemm44<NF, NC, N, 2, GT>(sm.v32, NCP, sm.y32, NCP, corr, NCP, lane);
+    gemm44h<NF, NC, N, GT>(sm.v32, NCP, sm.y32, NCP, corr, NCP, lane);
   } else {
     warp_gemm<N, NC, N, TL::Y_M, TL::Y_N, GT>(sm.d32t, N, sm.v32, NCP, sm.y32, NCP, lane);
     gsync<GT>();
