@@ -437,22 +437,56 @@ __device__ __forceinline__ void warp_cell(const HybArgs& A, int e, int parity, i
     }
   }
   gsync<GT>();
-  for (int idx = lane; idx < NF * NC; idx += GT) {
-    const int p = idx / NC, c = idx - p * NC;
-    const int ps = p / DPF, sub = p - ps * DPF;
-    const int64_t rs = sm.rstart[ps];
-    if (rs < 0) continue;
-    const double v = sm.vf[p * NC + c] - static_cast<double>(corr[p * NCP + c]);
-    if (c == NF) {
+  if constexpr (DPF % 2 == 0) {
+    // one (row, face block) run of DPF consecutive doubles per work item, stored
+    // as double2 (H rows start at multiples of DPF doubles, cudaMalloc'd base);
+    // then the g column
+    for (int idx = lane; idx < NF * NS; idx += GT) {
+      const int p = idx / NS, qs = idx - p * NS;
+      const int ps = p / DPF, sub = p - ps * DPF;
+      const int64_t rs = sm.rstart[ps];
+      const int rk = sm.rank[ps * NS + qs];
+      if (rs < 0 || rk < 0) continue;
+      double2* hp = reinterpret_cast<double2*>(A.hval + rs + static_cast<int64_t>(sub) * sm.rlen[ps] + rk * DPF);
+      const bool add = parity == 1 && ps == qs;
+#pragma unroll
+      for (int j = 0; j < DPF; j += 2) {
+        const int c = qs * DPF + j;
+        double2 v = make_double2(sm.vf[p * NC + c] - static_cast<double>(corr[p * NCP + c]),
+                                 sm.vf[p * NC + c + 1] - static_cast<double>(corr[p * NCP + c + 1]));
+        if (add) {
+          const double2 o = hp[j / 2];
+          v.x += o.x;
+          v.y += o.y;
+        }
+        hp[j / 2] = v;
+      }
+    }
+    for (int p = lane; p < NF; p += GT) {
+      const int ps = p / DPF, sub = p - ps * DPF;
+      if (sm.rstart[ps] < 0) continue;
+      const double v = sm.vf[p * NC + NF] - static_cast<double>(corr[p * NCP + NF]);
       double* gp = A.g + sm.grow[ps] + sub;
       *gp = parity ? *gp + v : v;
-      continue;
     }
-    const int qs = c / DPF, sj = c - qs * DPF;
-    const int rk = sm.rank[ps * NS + qs];
-    if (rk < 0) continue;
-    double* hp = A.hval + rs + static_cast<int64_t>(sub) * sm.rlen[ps] + rk * DPF + sj;
-    *hp = (parity == 1 && ps == qs) ? *hp + v : v;
+  } else {
+    for (int idx = lane; idx < NF * NC; idx += GT) {
+      const int p = idx / NC, c = idx - p * NC;
+      const int ps = p / DPF, sub = p - ps * DPF;
+      const int64_t rs = sm.rstart[ps];
+      if (rs < 0) continue;
+      const double v = sm.vf[p * NC + c] - static_cast<double>(corr[p * NCP + c]);
+      if (c == NF) {
+        double* gp = A.g + sm.grow[ps] + sub;
+        *gp = parity ? *gp + v : v;
+        continue;
+      }
+      const int qs = c / DPF, sj = c - qs * DPF;
+      const int rk = sm.rank[ps * NS + qs];
+      if (rk < 0) continue;
+      double* hp = A.hval + rs + static_cast<int64_t>(sub) * sm.rlen[ps] + rk * DPF + sj;
+      *hp = (parity == 1 && ps == qs) ? *hp + v : v;
+    }
   }
   gsync<GT>();
 }
