@@ -705,6 +705,48 @@ __global__ void __launch_bounds__(kThreads, 1) k_hyb_big(HybArgs A, int parity, 
     // ---------------------------------------------------------------- scatter
     // four entries per thread per pass: every load (vf, csm, the shared diagonal
     // blocks' partial sums) issued before the first store
+    if constexpr (DPF % 2 == 0) {
+      // even face dof counts: double2 work items, consecutive threads along one
+      // (row, face block) run of DPF doubles (H rows start at multiples of DPF);
+      // the g column after
+      constexpr int H2 = DPF / 2, NIT = NF * NS * H2, SB2 = 5;
+      for (int base = tid; base < NIT; base += SB2 * kThreads) {
+        double2 val[SB2], old[SB2];
+        double2* dst[SB2];
+        bool acc[SB2];
+#pragma unroll
+        for (int u = 0; u < SB2; ++u) {
+          const int idx = base + u * kThreads;
+          dst[u] = nullptr;
+          acc[u] = false;
+          val[u] = make_double2(0.0, 0.0);
+          if (idx >= NIT) continue;
+          const int run = idx / H2, j2 = idx - run * H2;
+          const int p = run / NS, qs = run - p * NS;
+          const int ps = p / DPF, sub = p - ps * DPF;
+          const int64_t rs = sm.rstart[ps];
+          const int rk = sm.rank[ps * NS + qs];
+          if (rs < 0 || rk < 0) continue;
+          const int c = qs * DPF + 2 * j2;
+          val[u] = make_double2(vf[p * NC + c] - static_cast<double>(sm.u.csm[p * NCP + c]),
+                                vf[p * NC + c + 1] - static_cast<double>(sm.u.csm[p * NCP + c + 1]));
+          dst[u] = reinterpret_cast<double2*>(A.hval + rs + static_cast<int64_t>(sub) * sm.rlen[ps] + rk * DPF) + j2;
+          acc[u] = parity == 1 && ps == qs;
+        }
+#pragma unroll
+        for (int u = 0; u < SB2; ++u) old[u] = (dst[u] && acc[u]) ? *dst[u] : make_double2(0.0, 0.0);
+#pragma unroll
+        for (int u = 0; u < SB2; ++u)
+          if (dst[u]) *dst[u] = acc[u] ? make_double2(old[u].x + val[u].x, old[u].y + val[u].y) : val[u];
+      }
+      for (int p = tid; p < NF; p += kThreads) {
+        const int ps = p / DPF, sub = p - ps * DPF;
+        if (sm.rstart[ps] < 0) continue;
+        const double v = vf[p * NC + NF] - static_cast<double>(sm.u.csm[p * NCP + NF]);
+        double* gp = A.g + sm.grow[ps] + sub;
+        *gp = parity ? *gp + v : v;
+      }
+    } else {
     constexpr int SB = 8;
     for (int base = tid; base < NF * NC; base += SB * kThreads) {
       double val[SB], old[SB];
@@ -738,6 +780,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_hyb_big(HybArgs A, int parity, 
 #pragma unroll
       for (int u = 0; u < SB; ++u)
         if (dst[u]) *dst[u] = acc[u] ? old[u] + val[u] : val[u];
+    }
     }
     __syncthreads();
     BIG_T(7);
