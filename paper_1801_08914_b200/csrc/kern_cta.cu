@@ -216,7 +216,7 @@ __device__ __forceinline__ void v_block(BigSmem<K>& sm, const Fixed& fx, int i0,
 // shared-memory layout; one thread issues the MMAs, everyone waits on the
 // commit mbarrier before the buffers are refilled.  C -> sm.u.csm.
 template <int K>
-__device__ void correction_tc(BigSmem<K>& sm, const Fixed& fx, double a, double b, uint32_t (&ph)[2]) {
+__device__ void correction_tc(BigSmem<K>& sm, const Fixed& fx, double a, double b, uint32_t& ph) {
   using B = Big<K>;
   constexpr int N = B::N, NF = B::NF, NC = B::NC, NCP = B::NCP;
   constexpr int MP = B::MP, KP = B::KP, KC = B::KC, NY = B::NY, NFP = B::NFP, NCH = KP / KC;
@@ -225,8 +225,8 @@ __device__ void correction_tc(BigSmem<K>& sm, const Fixed& fx, double a, double 
   constexpr uint32_t idesc1 = umma::idesc_tf32(128, NY), idesc2 = umma::idesc_tf32(128, NFP);
   constexpr uint32_t lbo_a = (128 / 8) * 128, lbo_b1 = (NY / 8) * 128, lbo_b2 = (NFP / 8) * 128;
   auto wait_buf = [&](int bf) {  // the MMAs that last read buffer bf are done
-    umma::mbar_wait(&sm.mbar[bf], ph[bf]);
-    ph[bf] ^= 1u;
+    umma::mbar_wait(&sm.mbar[bf], (ph >> bf) & 1u);  // phase bits in a register (no local memory)
+    ph ^= 1u << bf;
     umma::fence_after();
   };
   auto issue = [&](auto& T, int c, uint32_t tD, uint32_t idesc, uint32_t lbo_b) {
@@ -269,23 +269,21 @@ __device__ void correction_tc(BigSmem<K>& sm, const Fixed& fx, double a, double 
 #endif
     if (c >= 2) wait_buf(bf);
     BIG_Q(8);
+    const int64_t q0 = static_cast<int64_t>(c + 1) * MP * KC + tid;
 #pragma unroll
     for (int i = 0; i < PER; ++i) {  // lane -> (n % 8, k % 4): the 32 lanes store to 32 banks
       const int g = warp + 16 * i, m = 8 * (g >> 2) + (lane >> 2), k = 4 * (g & 3) + (lane & 3);
-      if (8 * (g >> 2) >= NY) continue;  // padding rows of the table (warp-uniform)
-      // delta (exact rounding error of the combine) in fp64; alpha E + beta Ma in fp32
-      double p1, e1, p2, e2, sm_, e3;
-      two_prod(a, dm[i].x, p1, e1);
-      two_prod(b, dm[i].y, p2, e2);
-      two_sum(p1, p2, sm_, e3);
-      const float x = fmaf(af, em[i].x, fmaf(bf32, em[i].y, static_cast<float>(-((e1 + e2) + e3))));
-      const uint32_t off = umma::kmajor_offset(m, k, NY) >> 2;
-      tf32_split(x, T.bhi[off], T.blo[off]);
-    }
-    if (c + 1 < NCH) {
-      const int64_t q0 = static_cast<int64_t>(c + 1) * MP * KC + tid;
-#pragma unroll
-      for (int i = 0; i < PER; ++i) {
+      if (8 * (g >> 2) < NY) {  // else padding rows of the table (warp-uniform)
+        // delta (exact rounding error of the combine) in fp64; alpha E + beta Ma in fp32
+        double p1, e1, p2, e2, sm_, e3;
+        two_prod(a, dm[i].x, p1, e1);
+        two_prod(b, dm[i].y, p2, e2);
+        two_sum(p1, p2, sm_, e3);
+        const float x = fmaf(af, em[i].x, fmaf(bf32, em[i].y, static_cast<float>(-((e1 + e2) + e3))));
+        const uint32_t off = umma::kmajor_offset(m, k, NY) >> 2;
+        tf32_split(x, T.bhi[off], T.blo[off]);
+      }
+      if (c + 1 < NCH) {  // entry i of the next chunk in flight as soon as its registers are free
         dm[i] = __ldg(fx.dtab + q0 + i * kThreads);
         em[i] = __ldg(fx.etab + q0 + i * kThreads);
       }
@@ -384,7 +382,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_hyb_big(HybArgs A, int parity, 
   extern __shared__ __align__(128) unsigned char smem_raw[];
   BigSmem<K>& sm = *reinterpret_cast<BigSmem<K>*>(smem_raw);
   const int tid = threadIdx.x;
-  uint32_t phase[2] = {0u, 0u};
+  uint32_t phase = 0u;  // bit b: parity of mbar[b]
   if (use_tc) {
     if (tid == 0) {
       umma::mbar_init(&sm.mbar[0], 1);
