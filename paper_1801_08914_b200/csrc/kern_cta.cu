@@ -35,9 +35,9 @@ struct Big {
   static constexpr int NCP = (NC + 3) & ~3;
   static constexpr int IB = (K == 3) ? 48 : 54;  // rows per block: divides N and NINT (interior / face blocks)
   static constexpr int NB = N / IB;
-  // fp64 tensor-core (DMMA m8n8k4) phase V: row strides chosen so that the 32
-  // lanes' fragment loads hit every bank pair exactly twice (2 wavefronts)
-  static constexpr int NZ = (NC + 7) / 16 * 16 + 8;  // z (RP x NZ), NZ = 8 mod 16
+  // fp64 tensor-core (DMMA m8n8k4) phase V: row strides chosen so that each
+  // half-warp's fragment loads hit 16 distinct bank pairs (2 wavefronts per load)
+  static constexpr int NZ = ((NC + 7) / 8 * 8 + 11) / 16 * 16 + 4;  // z (RP x NZ), NZ = 4 mod 16, >= 8 CT
   static constexpr int RP = (R + 3) & ~3;            // K of the V product, padded to the MMA's 4
   static constexpr int RS = (RP + 11) / 16 * 16 + 4; // xi (IBP x RS), RS = 4 mod 16
   static constexpr int IBP = (IB + 7) & ~7;          // row block padded to the MMA's 8
