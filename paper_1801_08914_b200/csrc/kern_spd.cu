@@ -194,15 +194,20 @@ __device__ __forceinline__ void sweep_block(double* W, int ld, const double* T, 
   sweep_blocks<1>(W, ld, T, C, n, w, ri, rj);
 }
 
-// acc (+)= sign * W[i0:i0+4, :] Y[:, c0:c0+4] over k < n (W symmetric: read as rows)
+// acc (+)= sign * W[i0:i0+4, :] Y[:, c0:c0+4] over k < n (W symmetric: read as rows).
+// Column order swizzled: acc[.][b] is column c0 + (b ^ tile_swz()) -- lanes 4..7
+// of each quarter-warp read the upper half of their 32-byte Y segment first, so
+// the 128-bit loads of 8 lanes at a 32-byte stride cover 32 distinct banks.
+__device__ __forceinline__ int tile_swz() { return threadIdx.x & 4 ? 2 : 0; }
 __device__ __forceinline__ void gemm_tile(int n, const double* W, int ld, const double* Y, int ldy, int i0, int c0,
                                           double (&acc)[4][4]) {
+  const int ya = c0 + tile_swz(), yb = c0 + (tile_swz() ^ 2);
 #pragma unroll 2
   for (int k = 0; k < n; ++k) {
     const double2 w0 = *reinterpret_cast<const double2*>(W + k * ld + i0);
     const double2 w1 = *reinterpret_cast<const double2*>(W + k * ld + i0 + 2);
-    const double2 y0 = *reinterpret_cast<const double2*>(Y + k * ldy + c0);
-    const double2 y1 = *reinterpret_cast<const double2*>(Y + k * ldy + c0 + 2);
+    const double2 y0 = *reinterpret_cast<const double2*>(Y + k * ldy + ya);
+    const double2 y1 = *reinterpret_cast<const double2*>(Y + k * ldy + yb);
     const double wv[4] = {w0.x, w0.y, w1.x, w1.y}, yv[4] = {y0.x, y0.y, y1.x, y1.y};
 #pragma unroll
     for (int a = 0; a < 4; ++a)
@@ -491,7 +496,7 @@ __global__ void __launch_bounds__(kST, 1) k_spd_hyb(AlgArgs a, double* gws, int6
         for (int r = 0; r < 4; ++r)
 #pragma unroll
           for (int c = 0; c < 4; ++c)
-            if (i0 + r < n) s.Z[(i0 + r) * ldz + c0 + c] = (c0 + c < nc) ? -acc[r][c] : 0.0;
+            if (i0 + r < n) s.Z[(i0 + r) * ldz + c0 + (c ^ tile_swz())] = (c0 + (c ^ tile_swz()) < nc) ? -acc[r][c] : 0.0;
       }
     }
     __syncthreads();
@@ -520,8 +525,8 @@ __global__ void __launch_bounds__(kST, 1) k_spd_hyb(AlgArgs a, double* gws, int6
         for (int r = 0; r < 4; ++r)
 #pragma unroll
           for (int c = 0; c < 4; ++c)
-            if (i0 + r < n && c0 + c < nc) {
-              const int o = (i0 + r) * ldz + c0 + c;
+            if (i0 + r < n && c0 + (c ^ tile_swz()) < nc) {
+              const int o = (i0 + r) * ldz + c0 + (c ^ tile_swz());
               const double z = s.Z[o] - acc[r][c];
               s.Z[o] = z;
               cm = fmax(cm, fabs(acc[r][c]));
