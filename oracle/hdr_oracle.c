@@ -811,6 +811,15 @@ static void free_port(hdo_ctx* c) {
   }
 }
 
+/* Cell sizes other than the unit cube's 1/N (a z-slab sub-mesh keeps the global
+   mesh's h, paper_1801_08914_b200/slab.py): the reference matrices are rebuilt
+   and any per-element state dropped. */
+int hdo_set_h(hdo_ctx* c, const double h[3]) {
+  for (int a = 0; a < c->dim; ++a) c->h[a] = h[a];
+  free_port(c);
+  return hdo_build_reference(c->dim, c->k, c->h, c->k + 2, c->divdiv, c->mass, c->face_moments, c->unit_load);
+}
+
 void hdo_destroy(hdo_ctx* c) {
   if (!c) return;
   free_port(c);

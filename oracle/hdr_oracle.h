@@ -38,6 +38,7 @@ typedef struct hdo_ctx hdo_ctx;
 /* dim 2|3, cells[3] (cells[2] ignored in 2D), RT order k in 0..3,
  * weighted: 0 = unit constraint rows (build_C weighted=false). */
 hdo_ctx* hdo_create(int dim, const long long cells[3], int k, int weighted);
+int hdo_set_h(hdo_ctx* c, const double h[3]); /* cell sizes (default 1 / cells) */
 void hdo_destroy(hdo_ctx* ctx);
 
 /* Scalar sizes: "dim","k","n","dpf","nint","ncells","nfaces","ndofs",

@@ -31,6 +31,7 @@ def lib():
         L.hdo_create.restype = ctypes.c_void_p
         L.hdo_create.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_longlong), ctypes.c_int, ctypes.c_int]
         L.hdo_destroy.argtypes = [ctypes.c_void_p]
+        L.hdo_set_h.argtypes = [ctypes.c_void_p, ctypes.POINTER(ctypes.c_double)]
         L.hdo_size.restype = ctypes.c_longlong
         L.hdo_size.argtypes = [ctypes.c_void_p, ctypes.c_char_p]
         L.hdo_count.restype = ctypes.c_longlong
@@ -92,6 +93,11 @@ class Oracle:
 
     def getq(self, name: str) -> np.ndarray:
         return self.get(name, np.int64)
+
+    def set_h(self, h) -> None:
+        arr = (ctypes.c_double * 3)(*(list(h) + [1.0] * (3 - len(h))))
+        if lib().hdo_set_h(self._h, arr) != 0:
+            raise OracleError("hdo_set_h failed")
 
     def set(self, name: str, data) -> None:
         a = np.ascontiguousarray(data, dtype=np.float64)
