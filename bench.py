@@ -10,8 +10,10 @@ element solve and deterministic CSR scatter of H and g, inputs resident in HBM.
   python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--config 2]
 
 Under torchrun (N > 1) every rank hybridizes its own independent replica mesh
-(the path shards by cells with no data-path exchange: weak scaling); timing is
-the max over ranks.  --impl reference times the reference's own CPU
+(the path shards by cells with no data-path exchange: weak scaling); with
+--partition slab the ranks instead split ONE mesh into ghosted z-slabs
+(paper_1801_08914_b200/slab.py: strong scaling, value = the mesh's cells / time,
+ghost cells not counted).  Timing is the max over ranks.  --impl reference times the reference's own CPU
 implementation (oracle/_ref/ref_harness, built from /root/reference) on a
 bounded sample of the same workload, on rank 0 only.
 """
@@ -284,8 +286,20 @@ def ours(args):
     from paper_1801_08914_b200 import dist as hdist
 
     cfg = CONFIGS[args.config]
-    alpha, beta, f_hat = make_inputs(cfg, hdist.replica_seed(cfg["seed"], rank))
-    sp = hd.Space(cfg["dim"], cfg["cells"], cfg["k"])
+    slab_plan = None
+    if args.partition == "slab":
+        # one mesh over the ranks: each hybridizes its ghosted z-slab (slab.py), no exchange
+        from paper_1801_08914_b200 import slab
+        if cfg["dim"] != 3 or cfg.get("perturb"):
+            raise SystemExit("--partition slab: affine 3D configs")
+        slab_plan = slab.SlabPlan(cfg["cells"], cfg["k"], world, rank)
+        alpha, beta, f_hat = make_inputs(cfg, cfg["seed"])  # the global inputs, identical on every rank
+        n_loc = f_hat.size // int(np.prod(cfg["cells"]))
+        alpha, beta, f_hat = (np.ascontiguousarray(x) for x in slab_plan.inputs(alpha, beta, f_hat, n_loc))
+        sp = hd.Space(3, slab_plan.sub_cells, cfg["k"], sizes=slab_plan.sizes)
+    else:
+        alpha, beta, f_hat = make_inputs(cfg, hdist.replica_seed(cfg["seed"], rank))
+        sp = hd.Space(cfg["dim"], cfg["cells"], cfg["k"])
     if cfg.get("perturb"):
         sp.set_vertices(make_vertices(cfg, hdist.replica_seed(cfg["seed"], rank)))
     stream = torch.cuda.Stream()  # one non-default stream for the library, the events and the flush
@@ -351,7 +365,9 @@ def ours(args):
     step_ms = [a.elapsed_time(b) for a, b in zip(ev0, ev1)]
     total_ms = hdist.reduce_max(float(np.sum(step_ms)))  # device time, max over ranks
     ncells = sp.ncells
-    value = ncells * world * args.steps / (total_ms * 1e-3)
+    # units of the whole job: replicas process world meshes; slabs one mesh (ghost cells not counted)
+    job_cells = int(np.prod(cfg["cells"])) if slab_plan is not None else ncells * world
+    value = job_cells * args.steps / (total_ms * 1e-3)
     ms_per_step = total_ms / args.steps
 
     # ---- e2e: the public pipelined batch call (hdr_hybridize_fe_batch) from pinned
@@ -376,7 +392,7 @@ def ours(args):
         e1.record(stream)  # the space's stream is ordered after the last download
         torch.cuda.synchronize()
         e2e_ms = hdist.reduce_max(float(e0.elapsed_time(e1)))
-        e2e = {"value": ncells * world * args.steps / (e2e_ms * 1e-3), "unit": UNIT,
+        e2e = {"value": job_cells * args.steps / (e2e_ms * 1e-3), "unit": UNIT,
                "h2d_bytes_per_step": 8 * (2 * ncells + sp.broken_ndofs),
                "d2h_bytes_per_step": 8 * (sp.info["nnz_h"] + sp.m),
                "note": "hdr_hybridize_fe_batch over the K timed steps: pinned host alpha/beta/f_hat in, H values + g "
@@ -419,10 +435,13 @@ def ours(args):
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "strong" if slab_plan is not None else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": cfg["desc"], "cells": ncells, "order": cfg["k"], "dim": cfg["dim"],
-                   "nnz_h": sp.info["nnz_h"], "m": sp.m, "parallelism": f"replicas x{world} (cells shard; no exchange)",
+                   "nnz_h": sp.info["nnz_h"], "m": sp.m,
+                   "parallelism": (f"z-slabs x{world} of one mesh (ghosted sub-meshes, no exchange)" if slab_plan is not None
+                                   else f"replicas x{world} (cells shard; no exchange)"),
                    "l2": "flushed between steps (512 MiB write); inputs resident in HBM",
                    "cuda_graph": graph is not None},
         "roofline": roof,
@@ -535,6 +554,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
+    ap.add_argument("--partition", default="replica", choices=["replica", "slab"],
+                    help="N > 1: independent replica meshes (weak scaling) or z-slabs of one mesh (strong scaling)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--fp64", action="store_true", help="also report the fp64 roofline for k = 0")
