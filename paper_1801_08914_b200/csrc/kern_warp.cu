@@ -62,10 +62,9 @@ template <int DIM, int K>
 struct WarpSmem {
   using S = Shape<DIM, K>;
   static constexpr int NCP = (S::NC + 3) & ~3;  // padded row length of [V | w] and Y
-  float d32t[S::N * S::N];     // Delta32 transposed: d32t[l * N + i] = Delta_il
+  float d32t[S::N * S::N];     // Delta32 transposed: d32t[l * N + i] = Delta_il; then C = V_F^T Y (NF x NCP)
   float v32[S::N * NCP];       // [V | w] row-major (fp32 operand)
   float y32[S::N * NCP];       // Y = Delta V
-  float corr[S::NF * NCP];     // C = V_F^T Y (+ higher orders)
   double vf[S::NF * S::NC];    // fp64 face rows of [V | w]: H0 and g0
   double z[S::R * S::NC];      // z[j][c] = s_j X_F_c,j (c < NF), s_j (X^T f)_j (c = NF)
   double f[S::N];              // f_T
@@ -226,12 +225,12 @@ __device__ __forceinline__ void gemm44h(const float* at, int lda, const float* b
         }
 }
 
-// per-warp global scratch: the higher-order buffer T (N x NCP fp32), rarely used
+// per-warp global scratch: the higher-order buffers T (N x NCP fp32) and Delta32 (N x N), rarely used
 template <int DIM, int K>
 constexpr int64_t scratch_doubles_per_warp() {
   using S = Shape<DIM, K>;
   constexpr int NCP = WarpSmem<DIM, K>::NCP;
-  return (S::N * NCP + 1) / 2 + 8;
+  return (S::N * NCP + S::N * S::N + 1) / 2 + 8;  // T, then a Delta32 copy for orders >= 2
 }
 
 template <int DIM, int K>
@@ -316,18 +315,25 @@ __device__ __forceinline__ void warp_cell(const HybArgs& A, int e, int parity, i
   // Delta32^T (fp64 exact rounding errors -> fp32)
   // (transposed input tables: contiguous loads and stores; alpha E + beta Ma in fp32)
   const float af = static_cast<float>(a), bfl = static_cast<float>(b);
-  for (int idx = lane; idx < N * N; idx += GT) {
-    const double2 dm = __ldg(fx.tdm + idx);
-    const float2 em = __ldg(fx.tem + idx);
-    double p1, e1, p2, e2, s_, e3;
-    two_prod(a, dm.x, p1, e1);
-    two_prod(b, dm.y, p2, e2);
-    two_sum(p1, p2, s_, e3);
-    sm.d32t[idx] = fmaf(af, em.x, fmaf(bfl, em.y, static_cast<float>(-((e1 + e2) + e3))));
-  }
+  auto fill_delta = [&](float* dst) {
+    for (int idx = lane; idx < N * N; idx += GT) {
+      const double2 dm = __ldg(fx.tdm + idx);
+      const float2 em = __ldg(fx.tem + idx);
+      double p1, e1, p2, e2, s_, e3;
+      two_prod(a, dm.x, p1, e1);
+      two_prod(b, dm.y, p2, e2);
+      two_sum(p1, p2, s_, e3);
+      dst[idx] = fmaf(af, em.x, fmaf(bfl, em.y, static_cast<float>(-((e1 + e2) + e3))));
+    }
+  };
+  fill_delta(sm.d32t);
   gsync<GT>();
-  // first order: Y = Delta32 [V | w];  C = V_F^T Y
-  float* corr = sm.corr;
+  // first order: Y = Delta32 [V | w];  C = V_F^T Y, C over Delta32's storage (dead
+  // after Y: fewer bytes per cell group, more groups per SM; orders >= 2 regenerate
+  // Delta32 in the global scratch)
+  static_assert(NF * NCP <= N * N, "C fits Delta32's storage");
+  float* corr = sm.d32t;
+  float* dglob = tbuf + N * NCP;
   if constexpr (GT == 128) {
     gemm44h<N, NC, N, GT>(sm.d32t, N, sm.v32, NCP, sm.y32, NCP, lane);
     gsync<GT>();
@@ -372,6 +378,10 @@ __device__ __forceinline__ void warp_cell(const HybArgs& A, int e, int parity, i
     if (!(ratio < 0.25) && lane == 0) atomicOr(A.status, 1);
   }
   // higher orders (rare): T = A0^-1 Y, Y <- Delta32 T, C += (-1)^(p+1) V_F^T Y (C is subtracted)
+  if (P >= 2) {
+    fill_delta(dglob);
+    gsync<GT>();
+  }
   for (int p = 2; p <= P; ++p) {
     for (int idx = lane; idx < R * NC; idx += GT) {
       const int j = idx / NC, c = idx - j * NC;
@@ -388,7 +398,7 @@ __device__ __forceinline__ void warp_cell(const HybArgs& A, int e, int parity, i
       tbuf[i * NCP + c] = static_cast<float>(acc * ib);
     }
     gsync<GT>();
-    warp_gemm<N, NC, N, TL::Y_M, TL::Y_N, GT>(sm.d32t, N, tbuf, NCP, sm.y32, NCP, lane);
+    warp_gemm<N, NC, N, TL::Y_M, TL::Y_N, GT>(dglob, N, tbuf, NCP, sm.y32, NCP, lane);
     gsync<GT>();
     warp_gemm<NF, NC, N, TL::C_M, TL::C_N, GT>(sm.v32, NCP, sm.y32, NCP, corr, NCP, lane, (p & 1) ? 1.f : -1.f, true);
     gsync<GT>();
@@ -492,7 +502,7 @@ __device__ __forceinline__ void warp_cell(const HybArgs& A, int e, int parity, i
 }
 
 template <int DIM, int K>
-__global__ void __launch_bounds__(32 * kWarps) k_hyb_warp(HybArgs A, int parity, double* gws) {
+__global__ void __launch_bounds__(32 * kWarps, (DIM == 3 && K == 1) ? 9 : 1) k_hyb_warp(HybArgs A, int parity, double* gws) {
   constexpr int GT = Group<DIM, K>::GT;
   constexpr int CPB = 32 * kWarps / GT;  // cells per CTA iteration
   extern __shared__ __align__(16) unsigned char smem_raw[];
