@@ -5,7 +5,14 @@ elements/s of hybridization = assemble + eliminate + scatter).
 Default workload: BASELINE config 2 (3D unit-cube 64^3 hexes, RT_0, alpha/beta
 log-uniform in [1e-2, 1e2], f_hat uniform [-1, 1]); --config picks another.
 One "step" = one hybridize of the whole mesh: element assembly, structured
-element solve and deterministic CSR scatter of H and g, inputs resident in HBM.
+element solve (with its fail-safe exact path) and deterministic CSR scatter of
+H and g, inputs resident in HBM.  Inputs are the SURVEY.md §8(d) stream (the
+reference's Xorshift, seed 1000 + config id: paper_1801_08914_b200/inputs.py),
+bit-identical to the parity tests' inputs (tests/test_inputs.py).
+
+At N = 1 the line also carries "configs": every BASELINE config (1-5) timed
+the same way in the same run (value, ms/step, roofline fraction with the
+boundary-aware b_T flop count of §8(d), cells sent to the exact path).
 
   python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--config 2]
 
@@ -13,9 +20,10 @@ Under torchrun (N > 1) every rank hybridizes its own independent replica mesh
 (the path shards by cells with no data-path exchange: weak scaling); with
 --partition slab the ranks instead split ONE mesh into ghosted z-slabs
 (paper_1801_08914_b200/slab.py: strong scaling, value = the mesh's cells / time,
-ghost cells not counted).  Timing is the max over ranks.  --impl reference times the reference's own CPU
-implementation (oracle/_ref/ref_harness, built from /root/reference) on a
-bounded sample of the same workload, on rank 0 only.
+ghost cells not counted).  Timing is the max over ranks.  --impl reference
+times the reference's own CPU implementation (oracle/_ref/ref_harness, built
+from /root/reference: build_reduction_inputs + hybridize) on the same full
+mesh and inputs law with all host threads, on rank 0 only.
 """
 from __future__ import annotations
 
@@ -36,59 +44,71 @@ sys.path.insert(0, str(ROOT))
 METRIC = "elements/s of hybridization (assemble+eliminate+scatter), % of fp64/HBM roofline"
 UNIT = "elements/s"
 
-# BASELINE.json configs
-CONFIGS = {
-    1: dict(dim=2, cells=(64, 64), k=0, coef=("uniform", 1.0, 1.0), seed=1001,
-            desc="cfg1: 2D unit-square 64x64 quads, RT_0, alpha=beta=1"),
-    2: dict(dim=3, cells=(64, 64, 64), k=0, coef=("logu", 1e-2, 1e2), seed=1002,
-            desc="cfg2: 3D unit-cube 64^3 hexes (262,144 elems), RT_0, alpha,beta log-uniform [1e-2,1e2]"),
-    3: dict(dim=3, cells=(48, 48, 48), k=1, coef=("logu", 1e-2, 1e2), seed=1003,
-            desc="cfg3: 3D unit-cube 48^3 hexes (110,592 elems), RT_1, alpha,beta log-uniform [1e-2,1e2]"),
-    4: dict(dim=3, cells=(24, 24, 24), k=2, coef=("logu", 1e-3, 1e3), seed=1004, perturb=0.2,
-            desc="cfg4: 3D 24^3 perturbed trilinear hexes (13,824 elems, interior vertices moved U[-0.2h,0.2h]), "
-                 "RT_2 (Piola), alpha,beta log-uniform [1e-3,1e3]"),
-    5: dict(dim=3, cells=(32, 32, 32), k=3, coef=("checker", 1e-2, 1e2), seed=1005,
-            desc="cfg5: 3D unit-cube 32^3 hexes (32,768 elems), RT_3, 4^3 checkerboard sigma_t in {1e-2,1e2}"),
-}
-# bounded CPU samples of each workload for the reference / cpu_baseline legs
-CPU_SAMPLE = {1: (2, (64, 64)), 2: (3, (32, 32, 32)), 3: (3, (16, 16, 16)), 4: (3, (3, 3, 3)), 5: (3, (4, 4, 4))}
+# BASELINE.json configs (dims, order, coefficient law, seed 1000 + id): paper_1801_08914_b200/inputs.py
+from paper_1801_08914_b200.inputs import CONFIGS, config_inputs  # noqa: E402  (numpy only; no library load)
+
+# --impl reference / cpu_baseline on configs too large for a few minutes of host
+# time per step: the reference on a sub-mesh with the SAME element (cell size of
+# the full mesh) and coefficient law, elements/s extrapolated by the §8(d) flop
+# ratio of the full mesh to the sub-mesh (boundary-aware b_T)
+CPU_SUBMESH = {3: (16, 16, 16), 5: (6, 6, 6)}
+CPU_PORT_SAMPLE = {4: (3, 3, 3)}  # config 4: no reference (trilinear cells): the oracle's port on a sample
 
 
-def make_inputs(cfg: dict, seed: int):
-    """Seeded synthetic inputs with the workload's distributions (host numpy)."""
-    rng = np.random.default_rng(seed)
-    cells = cfg["cells"]
-    nc = int(np.prod(cells))
-    kind, lo, hi = cfg["coef"]
-    if kind == "uniform":
-        alpha, beta = np.full(nc, lo), np.full(nc, hi)
-    elif kind == "logu":
-        alpha = np.exp(rng.uniform(np.log(lo), np.log(hi), nc))
-        beta = np.exp(rng.uniform(np.log(lo), np.log(hi), nc))
-    else:  # checkerboard: alpha_ref = 1 (divdiv), beta_ref = 1/(3 sigma_t) (mass), SURVEY.md §8(d)
-        idx = np.arange(nc)
-        co = [idx % cells[0], (idx // cells[0]) % cells[1], idx // (cells[0] * cells[1])]
-        reg = sum(np.floor(4.0 * (co[a] + 0.5) / cells[a]).astype(np.int64) for a in range(cfg["dim"]))
-        sigma = np.where(reg % 2 == 0, lo, hi)
-        alpha, beta = np.ones(nc), 1.0 / (3.0 * sigma)
-    dpf = (cfg["k"] + 1) ** (cfg["dim"] - 1)
-    n = 2 * cfg["dim"] * dpf + cfg["dim"] * cfg["k"] * dpf
-    f_hat = rng.uniform(-1.0, 1.0, nc * n)
-    return alpha, beta, f_hat
+def analytic_shape(dim: int, cells, k: int) -> dict:
+    """ncells, n, b_T per cell, m, nnz(H) of a structured mesh (probe P11)."""
+    c = list(cells) + [1] * (3 - len(cells))
+    dpf = (k + 1) ** (dim - 1)
+    n = 2 * dim * dpf + dim * k * dpf
+    idx = np.arange(c[0] * c[1] * c[2])
+    co = [idx % c[0], (idx // c[0]) % c[1], idx // (c[0] * c[1])]
+    nfi = np.zeros(idx.size, dtype=np.int64)
+    for a in range(dim):
+        nfi += (co[a] > 0).astype(np.int64) + (co[a] + 1 < c[a]).astype(np.int64)
+    b = nfi * dpf
+    n_int_faces = sum((c[a] - 1) * int(np.prod([c[x] for x in range(dim) if x != a])) for a in range(dim))
+    return {"ncells": int(idx.size), "n": n, "dpf": dpf, "b": b, "m": n_int_faces * dpf,
+            "nnz_h": int(np.sum(b.astype(np.int64) ** 2) - n_int_faces * dpf * dpf)}
 
 
-def make_vertices(cfg: dict, seed: int):
-    """Config 4 geometry: unit-cube grid, every interior vertex coordinate moved by
-    U[-f h, f h] (boundary vertices fixed), vertices lexicographic x fastest."""
-    cells = cfg["cells"]
-    h = [1.0 / c for c in cells]
-    g = np.stack(np.meshgrid(*[np.arange(c + 1) * hh for c, hh in zip(cells, h)], indexing="ij"), -1)
-    g = g.transpose(2, 1, 0, 3).copy()  # (z, y, x, coord)
-    rng = np.random.default_rng(seed + 17)
-    inner = (slice(1, -1),) * 3
-    f = cfg["perturb"]
-    g[inner] += rng.uniform(-f, f, g[inner].shape) * np.array(h)
-    return g.reshape(-1, 3)
+def flops_per_step(cfg: dict, cells=None) -> float:
+    """§8(d) algorithmic flops: sum over cells of 2n^3/3 + 4 b_T^3/3 + 2n^2 + 3n^2 (b_T the
+    cell's actual multiplier count), + the mapped-cell assembly for config 4."""
+    sh = analytic_shape(cfg["dim"], cells or cfg["cells"], cfg["k"])
+    n = sh["n"]
+    b = sh["b"].astype(np.float64)
+    f = float(np.sum(2 * n ** 3 / 3 + 4 * b ** 3 / 3 + 5 * n ** 2))
+    if cfg.get("perturb"):
+        f += sh["ncells"] * 2 * (n * (n + 1) / 2) * (cfg["k"] + 2) ** 3 * 2
+    return f
+
+
+def bytes_per_step(cfg: dict) -> float:
+    """§8(d) compulsory bytes: 16 (alpha, beta) + 8 n (f_hat) per cell [+ 8 vertices x 3 x 8 for
+    config 4] + 8 nnz(H) + 8 m."""
+    sh = analytic_shape(cfg["dim"], cfg["cells"], cfg["k"])
+    by = sh["ncells"] * (16 + 8 * sh["n"]) + 8 * (sh["nnz_h"] + sh["m"])
+    if cfg.get("perturb"):
+        by += 8 * 3 * 8 * sh["ncells"]
+    return float(by)
+
+
+def config_record(cfg_id: int) -> dict:
+    """The workload description both arms print (identical dicts: same config)."""
+    cfg = CONFIGS[cfg_id]
+    sh = analytic_shape(cfg["dim"], cfg["cells"], cfg["k"])
+    return {"workload": cfg["desc"], "cells": sh["ncells"], "order": cfg["k"], "dim": cfg["dim"],
+            "nnz_h": sh["nnz_h"], "m": sh["m"], "inputs": f"SURVEY.md §8(d) Xorshift stream, seed {cfg['seed']}"}
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 def load_peaks():
@@ -152,69 +172,85 @@ def ref_harness_path():
     return ROOT / "oracle" / "_ref" / "ref_harness"
 
 
-def run_reference_sample(cfg_id: int, reps: int, threads: int):
-    """Times the reference (oracle/_ref/ref_harness: build_reduction_inputs +
-    hybridize, src/reduction.cpp:200-354) on the bounded sample of the workload."""
+def run_reference(cfg_id: int, reps: int, threads: int, cells=None):
+    """The reference (oracle/_ref/ref_harness: build_reduction_inputs + hybridize,
+    src/reduction.cpp:200-354) on the config's inputs law; cells = a sub-mesh with
+    the full mesh's cell size (CPU_SUBMESH) or None for the full mesh."""
     cfg = CONFIGS[cfg_id]
-    dim, cells = CPU_SAMPLE[cfg_id]
     kind, lo, hi = cfg["coef"]
-    coef = f"{kind}:{lo}:{hi}"
-    cmd = [str(ref_harness_path()), "bench", f"dim={dim}", "cells=" + ",".join(map(str, cells)), f"k={cfg['k']}",
-           f"coef={coef}", f"seed={cfg['seed']}", f"reps={reps}", "sc=0", "rec=0"]
+    full = list(cfg["cells"])
+    cells = list(cells or full)
+    cmd = [str(ref_harness_path()), "bench", f"dim={cfg['dim']}", "cells=" + ",".join(map(str, cells)),
+           f"k={cfg['k']}", f"coef={kind}:{lo}:{hi}", f"seed={cfg['seed']}", f"reps={reps}", "sc=0", "rec=0"]
+    if cells != full:
+        cmd.append("h=" + ",".join(repr(1.0 / c) for c in full))
     env = dict(os.environ, HDIVRED_NUM_THREADS=str(threads))
     out = subprocess.run(cmd, capture_output=True, text=True, env=env, check=True).stdout
-    recs = [json.loads(line) for line in out.splitlines() if line.startswith("{")]
-    ncells = int(np.prod(cells))
-    sample = f"{'x'.join(map(str, cells))} mesh ({ncells} cells) of the {cfg['desc'].split(':')[0]} workload, same element and coefficient law"
-    return recs, ncells, sample
+    return [json.loads(line) for line in out.splitlines() if line.startswith("{")]
+
+
+def cpu_throughput(cfg_id: int, reps: int, threads: int):
+    """(elements/s of the full config, seconds per step, sample note) of the reference at
+    `threads` host threads; sub-mesh configs are extrapolated by the §8(d) flop ratio."""
+    cfg = CONFIGS[cfg_id]
+    sub = CPU_SUBMESH.get(cfg_id)
+    recs = run_reference(cfg_id, reps, threads, sub)
+    t = float(np.median([r["metric_s"] for r in recs]))
+    full_cells = int(np.prod(cfg["cells"]))
+    if sub is None:
+        return full_cells / t, t, f"full {'x'.join(map(str, cfg['cells']))} mesh, median of {reps}"
+    scale = flops_per_step(cfg) / flops_per_step(cfg, sub)
+    t_full = t * scale
+    note = (f"{'x'.join(map(str, sub))} sub-mesh with the full mesh's cell size (h = 1/{cfg['cells'][0]}), "
+            f"{t:.3f} s, extrapolated x{scale:.1f} by the §8(d) flop ratio (boundary-aware b_T) to the full "
+            f"{'x'.join(map(str, cfg['cells']))} mesh")
+    return full_cells / t_full, t_full, note
 
 
 def port_sample(cfg_id: int, reps: int = 1):
-    """The oracle's port of hybridize (single thread) on the bounded sample; for
-    config 4 the only CPU implementation of the path (the reference has affine
-    boxes only)."""
+    """The oracle's port of hybridize (single thread) on a sample; for config 4 the
+    only CPU implementation of the path (the reference has affine boxes only,
+    SURVEY.md §8(c)), per-element cost extrapolated by the flop ratio."""
     sys.path.insert(0, str(ROOT / "tests"))
     from oracle_lib import Oracle
 
     cfg = CONFIGS[cfg_id]
-    dim, cells = CPU_SAMPLE[cfg_id]
+    cells = CPU_PORT_SAMPLE.get(cfg_id, cfg["cells"])
     kind, lo, hi = cfg["coef"]
     spec = f"{kind}:{lo}:{hi}" + (f";perturb={cfg['perturb']}" if cfg.get("perturb") else "")
     times = []
     for _ in range(reps):
-        o = Oracle(dim, cells, cfg["k"])
+        o = Oracle(cfg["dim"], cells, cfg["k"])
+        o.set_h([1.0 / c for c in cfg["cells"]])
         o.gen_inputs(spec, cfg["seed"])
         t0 = time.perf_counter()
         o.run("port_hybridize")
         times.append(time.perf_counter() - t0)
-    sample = (f"{'x'.join(map(str, cells))} mesh ({int(np.prod(cells))} cells) of the {cfg['desc'].split(':')[0]} "
-              f"workload, oracle port of the reference hybridize (element assembly included)")
-    return times, int(np.prod(cells)), sample
+    scale = flops_per_step(cfg) / flops_per_step(cfg, cells)
+    note = (f"{'x'.join(map(str, cells))} sample (cell size of the full mesh) of the {cfg['desc'].split(':')[0]} "
+            f"workload, oracle port of the reference hybridize incl. the Piola assembly, 1 thread, extrapolated "
+            f"x{scale:.1f} by the §8(d) flop ratio to the full mesh")
+    return [t * scale for t in times], note
 
 
 def cpu_baseline(cfg_id: int):
+    """Reference on the box's host cores: nproc threads (value) and 1 thread."""
     threads = os.cpu_count() or 1
-    if CONFIGS[cfg_id].get("perturb"):
-        times, ncells, sample = port_sample(cfg_id, 1)
-        return {"value": ncells / times[0], "unit": UNIT, "cores": 1, "kind": "port", "sample": sample}
-    if ref_harness_path().exists():
-        recs, ncells, sample = run_reference_sample(cfg_id, 3, threads)
-        t = float(np.median([r["metric_s"] for r in recs]))
-        return {"value": ncells / t, "unit": UNIT, "cores": threads, "kind": "reference",
-                "sample": sample + "; build_reduction_inputs + hybridize, median of 3, HDIVRED_NUM_THREADS=" + str(threads)}
-    # the oracle's port of the reference algorithm (single thread)
-    sys.path.insert(0, str(ROOT / "tests"))
-    from oracle_lib import Oracle
-
-    dim, cells = CPU_SAMPLE[cfg_id]
-    kind, lo, hi = CONFIGS[cfg_id]["coef"]
-    o = Oracle(dim, cells, CONFIGS[cfg_id]["k"])
-    o.gen_inputs(f"{kind}:{lo}:{hi}", CONFIGS[cfg_id]["seed"])
-    t0 = time.perf_counter()
-    o.run("port_hybridize")
-    t = time.perf_counter() - t0
-    return {"value": int(np.prod(cells)) / t, "unit": UNIT, "cores": 1, "kind": "port",
-            "sample": f"{'x'.join(map(str, cells))} mesh, oracle port of hybridize (reference build unavailable)"}
+    cfg = CONFIGS[cfg_id]
+    ncells = int(np.prod(cfg["cells"]))
+    if cfg.get("perturb"):
+        times, note = port_sample(cfg_id, 1)
+        return {"value": ncells / times[0], "unit": UNIT, "cores": 1, "kind": "port", "sample": note,
+                "cpu_model": cpu_model()}
+    if not ref_harness_path().exists():
+        return {"value": None, "unit": UNIT, "cores": threads, "kind": "reference",
+                "error": "oracle/_ref/ref_harness not built"}
+    v, t, note = cpu_throughput(cfg_id, 3, threads)
+    v1, t1, _ = cpu_throughput(cfg_id, 1, 1)
+    return {"value": v, "unit": UNIT, "cores": threads, "kind": "reference",
+            "sample": note + f"; build_reduction_inputs + hybridize (the metric), HDIVRED_NUM_THREADS={threads}",
+            "s_per_step": t, "single_thread": {"value": v1, "s_per_step": t1, "cores": 1},
+            "cpu_model": cpu_model(), "nproc": threads}
 
 
 def kernel_name(cfg: dict) -> str:
@@ -241,36 +277,129 @@ def reference_arm(args):
     cfg_id = args.config
     threads = os.cpu_count() or 1
     cfg = CONFIGS[cfg_id]
+    base = {"impl": "reference", "metric": METRIC, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (SURVEY.md §8(d) Xorshift stream, the parity tests' inputs)",
+            "config": config_record(cfg_id)}
     if cfg.get("perturb"):  # no reference implementation of mapped cells: the oracle port stands in
-        times, ncells, sample = port_sample(cfg_id, args.warmup + args.steps)
+        times, note = port_sample(cfg_id, args.warmup + args.steps)
         timed = times[args.warmup:]
-        value = ncells * len(timed) / float(np.sum(timed))
-        print(json.dumps({
-            "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * float(np.mean(timed)),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": cfg["desc"], "sample": sample, "threads": 1},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "port", "sample": sample},
-            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
+        value = int(np.prod(cfg["cells"])) * len(timed) / float(np.sum(timed))
+        base.update({"value": value, "ms_per_step": 1e3 * float(np.mean(timed)),
+                     "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "port", "sample": note,
+                                      "cpu_model": cpu_model()},
+                     "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}})
+        print(json.dumps(base))
         return 0
     if not ref_harness_path().exists():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/ref_harness not built (needs /root/reference at build time)"}))
         return 0
-    recs, ncells, sample = run_reference_sample(cfg_id, args.warmup + args.steps, threads)
-    timed = recs[args.warmup:]
-    t = float(np.sum([r["metric_s"] for r in timed]))
-    value = ncells * len(timed) / t
-    line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": 1e3 * t / len(timed), "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": cfg["desc"], "sample": sample, "threads": threads},
+    sub = CPU_SUBMESH.get(cfg_id)
+    recs = run_reference(cfg_id, args.warmup + args.steps, threads, sub)
+    timed = [r["metric_s"] for r in recs[args.warmup:]]
+    scale = 1.0 if sub is None else flops_per_step(cfg) / flops_per_step(cfg, sub)
+    t = float(np.sum(timed)) * scale
+    value = int(np.prod(cfg["cells"])) * len(timed) / t
+    note = (f"full {'x'.join(map(str, cfg['cells']))} mesh" if sub is None else
+            f"{'x'.join(map(str, sub))} sub-mesh with the full mesh's cell size, extrapolated x{scale:.1f} by the "
+            f"§8(d) flop ratio to the full mesh")
+    base.update({
+        "value": value, "ms_per_step": 1e3 * t / len(timed),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
-                         "sample": sample + "; build_reduction_inputs + hybridize per step"},
+                         "sample": note + "; build_reduction_inputs + hybridize per step, HDIVRED_NUM_THREADS="
+                         + str(threads), "cpu_model": cpu_model()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-    }
-    print(json.dumps(line))
+    })
+    print(json.dumps(base))
     return 0
+
+
+class Timer:
+    """Device time of K steps (W warm-up), L2 flushed before each step, CUDA events
+    on the library's stream; the step replayed from a CUDA graph when it captures."""
+
+    def __init__(self, torch, stream, flush, use_graph: bool):
+        self.torch, self.stream, self.flush, self.use_graph = torch, stream, flush, use_graph
+
+    def run(self, step, check, steps: int, warmup: int, clocks=None):
+        torch = self.torch
+        for _ in range(warmup):
+            step()
+        check()
+        torch.cuda.synchronize()
+        graph = None
+        if self.use_graph:
+            try:
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=self.stream):
+                    step()
+                g.replay()
+                torch.cuda.synchronize()
+                check()
+                graph = g
+            except Exception:
+                graph = None
+                torch.cuda.synchronize()
+        fn = graph.replay if graph is not None else step
+        ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+        ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+        torch.cuda.synchronize()
+        for i in range(steps):
+            self.flush.fill_(float(i))
+            ev0[i].record(self.stream)
+            fn()
+            ev1[i].record(self.stream)
+        torch.cuda.synchronize()
+        check()
+        return [a.elapsed_time(b) for a, b in zip(ev0, ev1)], graph is not None
+
+
+def roofline_for(cfg: dict, ms: float, hbm_peak: float, fp64: tuple) -> dict:
+    """Roofline of one config's step: HBM (k = 0) or fp64 (k >= 1) bound, with the
+    §8(d) algorithmic bytes / boundary-aware flops; fp64 fractions against both the
+    DFMA and the DMMA (fp64 tensor core) peaks measured in this run."""
+    by = bytes_per_step(cfg)
+    fl = flops_per_step(cfg)
+    hbm = {"bound": "hbm", "achieved": by / (ms * 1e-3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
+           "algorithmic_bytes_per_step": by}
+    hbm["frac"] = hbm["achieved"] / hbm_peak
+    dfma, dmma = fp64
+    ach = fl / (ms * 1e-3) / 1e12
+    f64 = {"bound": "fp64", "achieved": ach, "peak": dfma, "unit": "TFLOP/s", "frac": ach / dfma,
+           "peak_dmma": dmma, "frac_dmma": ach / dmma if dmma else None, "flops_per_step": fl,
+           "flops_model": "§8(d): sum over cells of 2n^3/3 + 4 b_T^3/3 + 5 n^2 (b_T = the cell's multipliers)"
+                          + (" + Piola assembly" if cfg.get("perturb") else "")}
+    if cfg["k"] == 0:
+        hbm["fp64"] = f64
+        return hbm
+    f64["hbm"] = hbm
+    return f64
+
+
+def measure_config(hd, torch, timer, cfg_id: int, steps: int, warmup: int, hbm_peak: float, fp64: tuple,
+                   seed=None) -> dict:
+    """One BASELINE config timed like the headline (device-resident inputs)."""
+    cfg = CONFIGS[cfg_id]
+    alpha, beta, f_hat, verts = config_inputs(cfg_id, seed)
+    sp = hd.Space(cfg["dim"], cfg["cells"], cfg["k"])
+    if verts is not None:
+        sp.set_vertices(verts)
+    sp.set_stream(timer.stream.cuda_stream)
+    a_d, b_d, f_d = (torch.from_numpy(x).cuda() for x in (alpha, beta, f_hat))
+    op = sp.hybridize(a_d, b_d, f_d)
+    exact = op.exact_cells()
+    l0 = hd.launch_count()
+    op.enqueue(a_d, b_d, f_d)
+    op.check()
+    per_step = hd.launch_count() - l0
+    ms_list, graphed = timer.run(lambda: op.enqueue(a_d, b_d, f_d), op.check, steps, warmup)
+    ms = float(np.mean(ms_list))
+    rec = {"workload": cfg["desc"], "value": sp.ncells / (ms * 1e-3), "unit": UNIT, "ms_per_step": ms,
+           "roofline": roofline_for(cfg, ms, hbm_peak, fp64), "exact_cells": exact,
+           "gpu_launches_per_step": per_step, "cuda_graph": graphed}
+    del op, sp
+    torch.cuda.synchronize()
+    return rec
 
 
 def ours(args):
@@ -287,82 +416,46 @@ def ours(args):
 
     cfg = CONFIGS[args.config]
     slab_plan = None
+    verts = None
     if args.partition == "slab":
         # one mesh over the ranks: each hybridizes its ghosted z-slab (slab.py), no exchange
         from paper_1801_08914_b200 import slab
         if cfg["dim"] != 3 or cfg.get("perturb"):
             raise SystemExit("--partition slab: affine 3D configs")
         slab_plan = slab.SlabPlan(cfg["cells"], cfg["k"], world, rank)
-        alpha, beta, f_hat = make_inputs(cfg, cfg["seed"])  # the global inputs, identical on every rank
+        alpha, beta, f_hat, _ = config_inputs(args.config)  # the global inputs, identical on every rank
         n_loc = f_hat.size // int(np.prod(cfg["cells"]))
         alpha, beta, f_hat = (np.ascontiguousarray(x) for x in slab_plan.inputs(alpha, beta, f_hat, n_loc))
         sp = hd.Space(3, slab_plan.sub_cells, cfg["k"], sizes=slab_plan.sizes)
     else:
-        alpha, beta, f_hat = make_inputs(cfg, hdist.replica_seed(cfg["seed"], rank))
+        # rank 0 times exactly the parity-tested stream; other replicas reseed
+        seed = cfg["seed"] if rank == 0 else hdist.replica_seed(cfg["seed"], rank)
+        alpha, beta, f_hat, verts = config_inputs(args.config, seed)
         sp = hd.Space(cfg["dim"], cfg["cells"], cfg["k"])
-    if cfg.get("perturb"):
-        sp.set_vertices(make_vertices(cfg, hdist.replica_seed(cfg["seed"], rank)))
+    if verts is not None:
+        sp.set_vertices(verts)
     stream = torch.cuda.Stream()  # one non-default stream for the library, the events and the flush
     torch.cuda.set_stream(stream)
     sp.set_stream(stream.cuda_stream)
     a_d, b_d, f_d = (torch.from_numpy(x).cuda() for x in (alpha, beta, f_hat))
     op = sp.hybridize(a_d, b_d, f_d)
+    exact_cells = op.exact_cells()
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float64, device="cuda")  # 512 MiB > 126 MB L2
+    timer = Timer(torch, stream, flush, not args.no_graph)
 
     barrier = hdist.barrier
-
-    # warmup (device-resident inputs)
-    for i in range(args.warmup):
-        op.enqueue(a_d, b_d, f_d)
+    l0 = hd.launch_count()
+    op.enqueue(a_d, b_d, f_d)
     op.check()
-    torch.cuda.synchronize()
-
-    # the step's launches captured once into a CUDA graph (launch-bound small
-    # configs); paths that synchronise inside (mapped geometry) run directly
-    graph = None
-    if not args.no_graph:
-        try:
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g, stream=stream):
-                op.enqueue(a_d, b_d, f_d)
-            g.replay()
-            torch.cuda.synchronize()
-            op.check()
-            graph = g
-        except Exception:
-            graph = None
-            torch.cuda.synchronize()
-
-    def step():
-        if graph is not None:
-            graph.replay()
-        else:
-            op.enqueue(a_d, b_d, f_d)
+    launches_per_step = hd.launch_count() - l0
 
     # ---- value: inputs resident in HBM, L2 flushed between steps, CUDA events per step
-    ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    if graph is not None:
-        l0 = hd.launch_count()
-        op.enqueue(a_d, b_d, f_d)
-        torch.cuda.synchronize()
-        launches_per_step = hd.launch_count() - l0
-    launches0 = hd.launch_count()
     barrier()
     torch.cuda.synchronize()
     with ClockSampler(torch.cuda.current_device()) as clk:
-        for i in range(args.steps):
-            flush.fill_(float(i))
-            ev0[i].record(stream)
-            step()
-            ev1[i].record(stream)
-        torch.cuda.synchronize()
+        step_ms, graphed = timer.run(lambda: op.enqueue(a_d, b_d, f_d), op.check, args.steps, args.warmup)
     barrier()
-    op.check()
-    launches = hd.launch_count() - launches0
-    if graph is not None:  # replays do not pass through the library's launch counter
-        launches = launches_per_step * args.steps
-    step_ms = [a.elapsed_time(b) for a, b in zip(ev0, ev1)]
+    launches = launches_per_step * args.steps
     total_ms = hdist.reduce_max(float(np.sum(step_ms)))  # device time, max over ranks
     ncells = sp.ncells
     # units of the whole job: replicas process world meshes; slabs one mesh (ghost cells not counted)
@@ -404,51 +497,42 @@ def ours(args):
             torch.distributed.destroy_process_group()
         return 0
 
-    # ---- roofline of the dominant kernel (the fused hybridize kernel; one launch per colour)
+    # ---- roofline of the dominant kernel (the fused hybridize kernels of the step)
     peak, peak_kind = load_peaks()
-    alg_bytes = 8 * (2 * ncells + sp.broken_ndofs + sp.info["nnz_h"] + sp.m)
-    if cfg.get("perturb"):
-        alg_bytes += 8 * 3 * 8 * ncells  # the cell's vertex coordinates
-    achieved = alg_bytes / (ms_per_step * 1e-3) / 1e9
-    traffic = None
+    dfma, _ = hd.measure_fp64_peak()
+    dmma, _ = hd.measure_dmma_peak()
+    roof = roofline_for(cfg, ms_per_step, peak, (dfma, dmma)) if slab_plan is None else {
+        "bound": "n/a (slab partition)", "achieved": None, "peak": None, "unit": None, "frac": None, "traffic": None}
+    roof["peak_source"] = (f"HBM: {peak_kind} (MEASURED_PEAKS.json hbm_gbs); fp64: DFMA / DMMA m8n8k4 chains "
+                           "measured in this run (hdr_measure_fp64_peak / hdr_measure_dmma_peak)")
+    roof["kernel"] = kernel_name(cfg)
     tf = ROOT / "profiles" / "ncu_traffic.json"
-    if tf.exists():
-        traffic = json.loads(tf.read_text()).get(f"cfg{args.config}")
-    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-            "traffic": traffic, "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
-            "algorithmic_bytes_per_step": alg_bytes,
-            "kernel": kernel_name(cfg)}
-    if cfg["k"] > 0 or args.fp64:
-        tfl, _ = hd.measure_fp64_peak()
-        n = sp.n
-        b = sp.info["dofs_per_face"] * 2 * cfg["dim"]
-        flop_cell = 2 * n ** 3 / 3 + 4 * b ** 3 / 3 + 2 * n ** 2 + 3 * n ** 2
-        if cfg.get("perturb"):  # + mapped-element assembly (mass and divdiv, symmetric halves)
-            flop_cell += 2 * (n * (n + 1) / 2) * (cfg["k"] + 2) ** 3 * 2
-        fl = flop_cell * ncells / (ms_per_step * 1e-3) / 1e12
-        roof_fp64 = {"bound": "fp64", "achieved": fl, "peak": tfl, "unit": "TFLOP/s", "frac": fl / tfl,
-                     "peak_source": "measured DFMA (hdr_measure_fp64_peak)", "flops_per_cell": flop_cell}
-        if cfg["k"] > 0:
-            roof, roof_fp64["hbm"] = roof_fp64, roof
-        else:
-            roof["fp64"] = roof_fp64
+    traffic = json.loads(tf.read_text()).get(f"cfg{args.config}") if tf.exists() else None
+    roof["traffic"] = traffic
+    roof["traffic_source"] = ("dram__bytes_read.sum + dram__bytes_write.sum of the step's kernels from the committed "
+                              "ncu capture (profiles/ncu_traffic.json), not measured in this run")
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
         "scaling": "strong" if slab_plan is not None else "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": cfg["desc"], "cells": ncells, "order": cfg["k"], "dim": cfg["dim"],
-                   "nnz_h": sp.info["nnz_h"], "m": sp.m,
-                   "parallelism": (f"z-slabs x{world} of one mesh (ghosted sub-meshes, no exchange)" if slab_plan is not None
-                                   else f"replicas x{world} (cells shard; no exchange)"),
-                   "l2": "flushed between steps (512 MiB write); inputs resident in HBM",
-                   "cuda_graph": graph is not None},
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (SURVEY.md §8(d) Xorshift stream, the parity tests' inputs)",
+        "config": config_record(args.config),
+        "setup": {"parallelism": (f"z-slabs x{world} of one mesh (ghosted sub-meshes, no exchange)" if slab_plan is not None
+                                  else f"replicas x{world} (cells shard; no exchange)"),
+                  "l2": "flushed between steps (512 MiB write); inputs resident in HBM",
+                  "cuda_graph": graphed, "exact_cells": exact_cells},
         "roofline": roof,
         "e2e": e2e,
         "gpu_launches": launches,
         "clocks": clk.summary(),
     }
+    # every BASELINE config in the same run (N = 1): the north-star config 5 among them
+    if world == 1 and not args.no_configs and slab_plan is None:
+        line["configs"] = {}
+        for cid in sorted(CONFIGS):
+            line["configs"][str(cid)] = measure_config(hd, torch, timer, cid, args.steps, args.warmup, peak,
+                                                       (dfma, dmma))
     if world == 1 and not args.no_cpu:
         try:
             line["cpu_baseline"] = cpu_baseline(args.config)
@@ -471,10 +555,10 @@ def stage_bench(args):
     import paper_1801_08914_b200 as hd
 
     cfg = CONFIGS[args.config]
-    alpha, beta, f_hat = make_inputs(cfg, cfg["seed"])
+    alpha, beta, f_hat, verts = config_inputs(args.config)
     sp = hd.Space(cfg["dim"], cfg["cells"], cfg["k"])
-    if cfg.get("perturb"):
-        sp.set_vertices(make_vertices(cfg, cfg["seed"]))
+    if verts is not None:
+        sp.set_vertices(verts)
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
     sp.set_stream(stream.cuda_stream)
@@ -558,6 +642,7 @@ def main():
                     help="N > 1: independent replica meshes (weak scaling) or z-slabs of one mesh (strong scaling)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-configs", action="store_true", help="skip the per-config block (all BASELINE configs)")
     ap.add_argument("--fp64", action="store_true", help="also report the fp64 roofline for k = 0")
     ap.add_argument("--no-graph", action="store_true", help="launch the step directly instead of replaying a CUDA graph")
     ap.add_argument("--stage", default="hybridize", choices=["hybridize", "condense", "recover", "spmv"],

@@ -149,6 +149,19 @@ hdr_status hdr_hybridize_fe_batch(hdr_space_t space, int count, const double* co
                                   double* const* g);
 /* Synchronizes the stream and reports device-side status of enqueued work. */
 hdr_status hdr_hybrid_check(hdr_hybrid_t op);
+/* Fail-safe of the structured element solve: cells whose
+ * a-posteriori error estimate exceeds 1e-12 of |H_T| (extreme alpha/beta
+ * ratios, e.g. the reference's soft-hard preset p = -8, src/mesh.cpp:168-191)
+ * are solved on the exact double-double path instead.  *count = the number of
+ * such cells in the operator's last synchronous hybridize / recover call
+ * (k = 0: cells since that call, enqueued calls included). */
+hdr_status hdr_hybrid_exact_cells(hdr_hybrid_t op, int64_t* count);
+/* Testing / tuning: force_exact = 1 sends every cell of later calls to the
+ * exact path; eps32 / eps_tc (<= 0: defaults) = relative accuracy assumed for
+ * the fp32 / tcgen05 correction arithmetic in the acceptance test; q_log
+ * (device float[ncells] or NULL) receives each cell's measured ratio
+ * q = |first-order term| / |zero-order term| on later hybridize calls. */
+hdr_status hdr_space_set_exact_policy(hdr_space_t space, int force_exact, double eps32, double eps_tc, float* q_log);
 /* In-place symmetrization of the operator's H values (see hdr_alg_symmetrize). */
 hdr_status hdr_hybrid_symmetrize(hdr_hybrid_t op);
 void hdr_hybrid_destroy(hdr_hybrid_t op);
@@ -323,6 +336,9 @@ int64_t hdr_launch_count(void);
 /* FP64 FMA throughput of device 0 in TFLOP/s (2 flops per DFMA), measured with
  * a register-resident DFMA chain kernel; the fp64 roofline denominator. */
 hdr_status hdr_measure_fp64_peak(double* tflops, double* ms);
+/* fp64 tensor-core (DMMA m8n8k4) throughput of the device, TFLOP/s (the peak the
+ * k >= 2 kernels' DMMA phases run against). */
+hdr_status hdr_measure_dmma_peak(double* tflops, double* ms);
 /* Self-test of the tcgen05 TF32 tensor-core path (kern_umma.cu): D (128 x n) =
  * A (128 x k, row-major) * B^T (B: n x k, row-major), split = 1: 3xTF32.  Host arrays. */
 hdr_status hdr_umma_selftest(int n, int k, const float* a, const float* b, float* d, int split);

@@ -879,7 +879,7 @@ int hdo_gen_inputs(hdo_ctx* c, const char* coef, unsigned long long seed) {
     return 1;
   }
   memcpy(kind, coef, (size_t)(colon - coef));
-  if (sscanf(colon + 1, "%lf:%lf", &p0, &p1) != 2) {
+  if (sscanf(colon + 1, "%lf:%lf", &p0, &p1) < 1) {
     set_err(c, "bad coef spec %s", coef);
     return 1;
   }
@@ -905,6 +905,22 @@ int hdo_gen_inputs(hdo_ctx* c, const char* coef, unsigned long long seed) {
       const double sigma = (reg % 2 == 0) ? p0 : p1;
       al[e] = 1.0;
       be[e] = 1.0 / (3.0 * sigma);
+    } else if (!strcmp(kind, "softhard")) {
+      /* soft_hard_coefficients (src/mesh.cpp:168-191): beta = 10^p on the cells whose
+       * centre lies in [1/4, 1/2]^d or [1/2, 3/4]^d, alpha = beta = 1 elsewhere */
+      long long co[3];
+      co[0] = e % c->N[0];
+      long long rr = e / c->N[0];
+      co[1] = rr % c->N[1];
+      co[2] = rr / c->N[1];
+      int in_lo = 1, in_hi = 1;
+      for (int a = 0; a < c->dim; ++a) {
+        const double t = 0.0 + ((double)co[a] + 0.5) * c->h[a];
+        in_lo = in_lo && (t >= 0.25 && t <= 0.5);
+        in_hi = in_hi && (t >= 0.5 && t <= 0.75);
+      }
+      al[e] = 1.0;
+      be[e] = (in_lo || in_hi) ? pow(10.0, (double)(int)p0) : 1.0;
     } else {
       set_err(c, "unknown coef kind %s", kind);
       return 1;
@@ -1912,6 +1928,88 @@ static int run_assemble(hdo_ctx* c) {
   return 0;
 }
 
+/* ------------------------------------------------ structure-only patterns
+ * The CSR patterns from_triplets (csr.cpp:43-75: sorted by (row, col),
+ * duplicates merged, explicit zeros kept) produces from the triplet sets of
+ *   hybridize        (reduction.cpp:308-337): every pair (r, c) of an element's
+ *                    sorted multiplier rows (constraint_slice, :31-57);
+ *   static_condense  (reduction.cpp:509-555): every pair of master ordinals of
+ *                    an element's b dofs (for FE inputs every face dof is a
+ *                    master, ordinal = global face dof),
+ * built row by row (a row's columns are the union of the lists of the <= 2
+ * elements that reach it) without values, so full BASELINE sizes fit in memory:
+ * "Hp.*" / "Sp.*" row_offsets + col_indices. */
+static int cmp_ll(const void* a, const void* b) {
+  const long long x = *(const long long*)a, y = *(const long long*)b;
+  return x < y ? -1 : (x > y);
+}
+static long long merge_unique(const long long* a, long long na, const long long* b, long long nb, long long* out) {
+  long long i = 0, j = 0, k = 0;
+  while (i < na || j < nb) {
+    long long v;
+    if (j >= nb || (i < na && a[i] <= b[j])) v = a[i++];
+    else v = b[j++];
+    if (k == 0 || out[k - 1] != v) out[k++] = v;
+  }
+  return k;
+}
+/* the element's sorted list: multiplier rows (which = 0) or master ordinals (1) */
+static long long elem_list(hdo_ctx* c, long long e, int which, long long* out) {
+  long long faces[6];
+  double fs[6];
+  cell_faces(c, e, faces, fs);
+  long long* base = mult_base(c);
+  long long k = 0;
+  for (int s = 0; s < 2 * c->dim; ++s) {
+    if (which == 0) {
+      if (base[faces[s]] < 0) continue;
+      for (long long sub = 0; sub < c->dpf; ++sub) out[k++] = base[faces[s]] + sub;
+    } else {
+      for (long long sub = 0; sub < c->dpf; ++sub) out[k++] = faces[s] * c->dpf + sub;
+    }
+  }
+  qsort(out, (size_t)k, sizeof *out, cmp_ll);
+  return k;
+}
+static int run_pattern(hdo_ctx* c, int which) {
+  const long long nrows = which == 0 ? c->m : c->face_dof_count;
+  long long* base = mult_base(c);
+  /* owner elements of each row's face */
+  long long* rcell = malloc((size_t)(2 * nrows + 2) * sizeof(long long));
+  for (long long r = 0; r < 2 * nrows; ++r) rcell[r] = -1;
+  for (long long f = 0; f < c->nfaces; ++f) {
+    int ax;
+    long long cm, cp;
+    face_info(c, f, &ax, &cm, &cp);
+    if (which == 0 && base[f] < 0) continue;
+    for (long long sub = 0; sub < c->dpf; ++sub) {
+      const long long r = which == 0 ? base[f] + sub : f * c->dpf + sub;
+      rcell[2 * r] = cm;
+      rcell[2 * r + 1] = cp;
+    }
+  }
+  long long la[96], lb[96], tmp[192];
+  const char* pre = which == 0 ? "Hp" : "Sp";
+  char nm[64];
+  snprintf(nm, sizeof nm, "%s.row_offsets", pre);
+  long long* ro = put_arr(c, nm, 'q', nrows + 1);
+  ro[0] = 0;
+  for (long long r = 0; r < nrows; ++r) {
+    const long long na = rcell[2 * r] >= 0 ? elem_list(c, rcell[2 * r], which, la) : 0;
+    const long long nb = rcell[2 * r + 1] >= 0 ? elem_list(c, rcell[2 * r + 1], which, lb) : 0;
+    ro[r + 1] = ro[r] + merge_unique(la, na, lb, nb, tmp);
+  }
+  snprintf(nm, sizeof nm, "%s.col_indices", pre);
+  long long* ci = put_arr(c, nm, 'q', ro[nrows]);
+  for (long long r = 0; r < nrows; ++r) {
+    const long long na = rcell[2 * r] >= 0 ? elem_list(c, rcell[2 * r], which, la) : 0;
+    const long long nb = rcell[2 * r + 1] >= 0 ? elem_list(c, rcell[2 * r + 1], which, lb) : 0;
+    merge_unique(la, na, lb, nb, ci + ro[r]);
+  }
+  free(rcell);
+  return 0;
+}
+
 int hdo_run(hdo_ctx* c, const char* what) {
   c->err[0] = 0;
   if (!strcmp(what, "assemble")) return run_assemble(c);
@@ -1926,6 +2024,8 @@ int hdo_run(hdo_ctx* c, const char* what) {
   if (!strcmp(what, "dd_recover_condensed")) return run_dd_condense(c, 1);
   if (!strcmp(what, "spmv_H")) return run_spmv(c, "H", "lambda", "H_lambda");
   if (!strcmp(what, "spmv_S")) return run_spmv(c, "S", "x_b", "S_x_b");
+  if (!strcmp(what, "pattern_H")) return run_pattern(c, 0);
+  if (!strcmp(what, "pattern_S")) return run_pattern(c, 1);
   set_err(c, "unknown stage %s", what);
   return 1;
 }

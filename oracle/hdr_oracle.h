@@ -72,6 +72,9 @@ int hdo_gen_inputs(hdo_ctx* ctx, const char* coef, unsigned long long seed);
  *  "dd_recover_condensed" x_cond_dd
  *  "spmv_H"          H_lambda (y = H lambda, reference spmv order)
  *  "spmv_S"          S_x_b
+ *  "pattern_H"       Hp.row_offsets / Hp.col_indices: hybridize's H pattern,
+ *                    structure only (no values; full BASELINE sizes)
+ *  "pattern_S"       Sp.*: static_condense's S pattern likewise
  * Returns 0 on success, nonzero error code (see hdo_last_error). */
 int hdo_run(hdo_ctx* ctx, const char* what);
 

@@ -79,7 +79,7 @@ struct Problem {
   Rng rng{1};
 };
 
-// coef = "uniform:a:b" | "logu:lo:hi" | "checker:sig_lo:sig_hi" (cfg5: alpha_ref = 1
+// coef = "uniform:a:b" | "logu:lo:hi" | "softhard:p" | "checker:sig_lo:sig_hi" (cfg5: alpha_ref = 1
 // divdiv, beta_ref = 1/(3 sigma_t) mass, regions (floor(4x)+floor(4y)+floor(4z)) mod 2)
 Problem make_problem(const std::map<std::string, std::string>& kv) {
   const int dim = std::stoi(kv.at("dim"));
@@ -89,6 +89,10 @@ Problem make_problem(const std::map<std::string, std::string>& kv) {
   for (int a = 0; a < dim; ++a) {
     cells[a] = static_cast<index_t>(cells_d.at(a));
     h[a] = 1.0 / static_cast<double>(cells[a]);
+  }
+  if (kv.count("h")) {  // cell sizes of a sub-mesh that keeps the full mesh's element
+    const auto hs = split_d(kv.at("h"), ',');
+    for (int a = 0; a < dim; ++a) h[a] = hs.at(a);
   }
   const int k = std::stoi(kv.at("k"));
   const std::uint64_t seed = std::stoull(kv.at("seed"));
@@ -122,6 +126,8 @@ Problem make_problem(const std::map<std::string, std::string>& kv) {
       pb.coeffs.alpha[c] = 1.0;
       pb.coeffs.beta[c] = 1.0 / (3.0 * sigma);
     }
+  } else if (kind == "softhard") {  // the reference's own preset (src/mesh.cpp:168-191)
+    pb.coeffs = soft_hard_coefficients(mesh, static_cast<int>(par.at(0)));
   } else {
     throw std::invalid_argument("unknown coef kind " + kind);
   }

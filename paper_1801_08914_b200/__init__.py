@@ -153,8 +153,8 @@ class Space:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h:
-            _lib().hdr_space_destroy(h)
+        if h and _capi is not None and _capi._lib is not None:  # (not during interpreter teardown)
+            _capi._lib.hdr_space_destroy(h)
             self._h = None
 
     # sizes
@@ -248,6 +248,20 @@ class Space:
     def synchronize(self) -> None:
         _check(_lib().hdr_space_synchronize(self._h))
 
+    def set_exact_policy(self, force: bool = False, eps32: float = 0.0, eps_tc: float = 0.0, q_log=None) -> None:
+        """Fail-safe controls of the structured solve (hdr_space_set_exact_policy):
+        force=True sends every cell to the exact double-double path (testing);
+        eps32 / eps_tc override the assumed correction accuracy (0: defaults);
+        q_log: a CUDA float32 tensor (ncells) receiving each cell's measured
+        first-order ratio q on later hybridize calls (None: off)."""
+        qp = None
+        if q_log is not None:
+            if not getattr(q_log, "is_cuda", False) or str(q_log.dtype) != "torch.float32" or q_log.numel() < self.ncells:
+                raise ValueError("q_log: CUDA float32 tensor of ncells entries")
+            qp = q_log.data_ptr()
+        _check(_lib().hdr_space_set_exact_policy(self._h, 1 if force else 0, float(eps32), float(eps_tc), qp))
+        self._qlog = q_log
+
     # ---- hot path
     def hybridize(self, alpha, beta, f_hat) -> "HybridizedOperator":
         """hybridize (src/reduction.cpp:262-354) of the FE inputs (alpha, beta per cell, f_hat)."""
@@ -257,7 +271,9 @@ class Space:
         dev = _same_device([a, b, f])
         h = ctypes.c_void_p()
         _check(_lib().hdr_hybridize_fe(self._h, _ptr(a)[0], _ptr(b)[0], _ptr(f)[0], dev, ctypes.byref(h)))
-        return HybridizedOperator(self, h)
+        op = HybridizedOperator(self, h)
+        op._keep = (a, b) if dev else None  # the C operator borrows device alpha / beta for recovery
+        return op
 
     def hybridize_batch(self, alphas, betas, f_hats, h_outs=None, g_outs=None) -> None:
         """Pipelined batch of independent hybridizations (hdr_hybridize_fe_batch):
@@ -301,7 +317,9 @@ class Space:
         dev = _same_device([a, b, f])
         h = ctypes.c_void_p()
         _check(_lib().hdr_static_condense_fe(self._h, _ptr(a)[0], _ptr(b)[0], _ptr(f)[0], dev, ctypes.byref(h)))
-        return CondensedOperator(self, h)
+        op = CondensedOperator(self, h)
+        op._keep = (a, b) if dev else None  # borrowed device alpha / beta (recover_condensed re-reads them)
+        return op
 
 
 class HybridizedOperator:
@@ -310,11 +328,12 @@ class HybridizedOperator:
     def __init__(self, space: Space, handle):
         self.space = space
         self._h = handle
+        self._keep = None
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h:
-            _lib().hdr_hybrid_destroy(h)
+        if h and _capi is not None and _capi._lib is not None:
+            _capi._lib.hdr_hybrid_destroy(h)
             self._h = None
 
     def rehybridize(self, alpha, beta, f_hat) -> None:
@@ -324,6 +343,7 @@ class HybridizedOperator:
         f = _as_f64(f_hat, sp.broken_ndofs, "f_hat")
         dev = _same_device([a, b, f])
         _check(_lib().hdr_hybridize_fe_into(self._h, _ptr(a)[0], _ptr(b)[0], _ptr(f)[0], dev))
+        self._keep = (a, b) if dev else None
 
     def enqueue(self, alpha, beta, f_hat) -> None:
         """Asynchronous hybridize on the space's stream (no host sync); host
@@ -331,6 +351,14 @@ class HybridizedOperator:
         sp = self.space
         dev = _same_device([alpha, beta, f_hat])
         _check(_lib().hdr_hybridize_fe_enqueue(self._h, _ptr(alpha)[0], _ptr(beta)[0], _ptr(f_hat)[0], dev))
+        self._keep = (alpha, beta) if dev else None
+
+    def exact_cells(self) -> int:
+        """Cells the last synchronous call solved on the exact double-double path
+        (the structured solve's estimate rejected them; hdr_hybrid_exact_cells)."""
+        n = ctypes.c_int64()
+        _check(_lib().hdr_hybrid_exact_cells(self._h, ctypes.byref(n)))
+        return int(n.value)
 
     def values_enqueue(self, h_out, g_out) -> None:
         """Asynchronous copy of H values / g into caller buffers (host pinned or device)."""
@@ -400,11 +428,12 @@ class CondensedOperator:
     def __init__(self, space: Space, handle):
         self.space = space
         self._h = handle
+        self._keep = None
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h:
-            _lib().hdr_condensed_destroy(h)
+        if h and _capi is not None and _capi._lib is not None:
+            _capi._lib.hdr_condensed_destroy(h)
             self._h = None
 
     def values(self):
@@ -593,6 +622,7 @@ def hybridized_matrix(config: dict):
     g = _axes(g, 3, [1.0, 1.0, 1.0])
     f_hat = space.load_vector(g)
     op = space.hybridize(alpha, beta, f_hat)
+    op.symmetrize()  # the reference symmetrizes every element block (src/reduction.cpp:316)
     nr, nc, ro, ci, hv = op.h_mat()
     _, gv = op.values()
     return (nr, nc, list(ro), list(ci), list(hv)), list(gv)
@@ -623,6 +653,14 @@ def measure_fp64_peak() -> tuple[float, float]:
     t = ctypes.c_double()
     ms = ctypes.c_double()
     _check(_lib().hdr_measure_fp64_peak(ctypes.byref(t), ctypes.byref(ms)))
+    return t.value, ms.value
+
+
+def measure_dmma_peak() -> tuple[float, float]:
+    """(TFLOP/s, ms) of the device's fp64 tensor-core (DMMA m8n8k4) throughput."""
+    t = ctypes.c_double()
+    ms = ctypes.c_double()
+    _check(_lib().hdr_measure_dmma_peak(ctypes.byref(t), ctypes.byref(ms)))
     return t.value, ms.value
 
 

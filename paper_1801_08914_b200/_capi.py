@@ -57,8 +57,11 @@ _SIGS = {
     "hdr_hybridize_fe_enqueue": (_i32, [_vp, _vp, _vp, _vp, _i32]),
     "hdr_hybridize_fe_batch": (_i32, [_vp, _i32, _vp, _vp, _vp, _vp, _vp]),
     "hdr_hybrid_check": (_i32, [_vp]),
+    "hdr_hybrid_exact_cells": (_i32, [_vp, _vp]),
+    "hdr_space_set_exact_policy": (_i32, [_vp, _i32, _d, _d, _vp]),
     "hdr_hybrid_values_enqueue": (_i32, [_vp, _vp, _vp, _i32]),
     "hdr_measure_fp64_peak": (_i32, [_vp, _vp]),
+    "hdr_measure_dmma_peak": (_i32, [_vp, _vp]),
     "hdr_hybrid_destroy": (None, [_vp]),
     "hdr_hybrid_values": (_i32, [_vp, _vp, _vp, _i32]),
     "hdr_hybrid_device_ptrs": (_i32, [_vp, _vp, _vp, _vp, _vp]),

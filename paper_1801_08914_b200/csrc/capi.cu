@@ -67,6 +67,11 @@ struct hdr_space_s {
   Fixed fx{};
   GeomState* geom = nullptr;  // mapped (trilinear) cells: hdr_space_set_vertices
   struct BatchCtx* batch = nullptr;  // hdr_hybridize_fe_batch: streams, events, two operators
+  // fail-safe of the structured solve (hdr_device.cuh struct_order, kern_exact.cu)
+  DBuf<double> xws;            // exact-path scratch (exact_grid x exact_ws_doubles), on first use
+  double eps32 = 0, eps_tc = 1e-6;
+  int force_exact = 0;
+  float* qlog = nullptr;
   ~hdr_space_s();
 };
 
@@ -74,6 +79,11 @@ struct hdr_hybrid_s {
   hdr_space_t sp = nullptr;
   DBuf<double> hval, g, alpha, beta, f, ws, pre;
   DBuf<int> status;
+  // cells sent to the exact path: xcount = [count (k >= 1: list length), -,
+  // k = 0 brick kernels' list length, k = 0 recovery count]
+  DBuf<int> xlist, xcount;
+  int last_call = 0;  // 0: hybridize, 1: recover (which count exact_cells reports)
+  DBuf<unsigned long long> xbad;  // smallest singular cell of the exact path
   int64_t ws_doubles = 0;
   const double* a_ptr = nullptr;  // coefficients used by the last hybridize (owned copy or borrowed device input)
   const double* b_ptr = nullptr;
@@ -139,15 +149,63 @@ void stage(DBuf<double>& dst, const double* src, int64_t count, int on_device, c
 }
 
 // Synchronizes the stream and reports (then clears) the sticky device status.
-hdr_status check_status(int* d_status, cudaStream_t st) {
+hdr_status check_status(int* d_status, cudaStream_t st, unsigned long long* d_bad = nullptr) {
   int status = 0;
+  unsigned long long bad = ~0ull;
   CK(cudaMemcpyAsync(&status, d_status, sizeof(int), cudaMemcpyDeviceToHost, st));
+  if (d_bad) CK(cudaMemcpyAsync(&bad, d_bad, sizeof(bad), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   if (status) CK(cudaMemsetAsync(d_status, 0, sizeof(int), st));
-  if (status & 1)
-    return fail(HDR_UNSUPPORTED, "coefficient ratio alpha/beta outside the structured solve's range on some cell");
+  if (d_bad && bad != ~0ull) CK(cudaMemsetAsync(d_bad, 0xff, sizeof(bad), st));
+  if (status & 4)
+    return fail(HDR_SINGULAR_BLOCK, "SingularBlock: element " + (bad != ~0ull ? std::to_string(bad) : std::string("?")) +
+                                        " (pivot <= 1e-14 max|block| of A_ii or S_b)");
+  if (status & 1) return fail(HDR_UNSUPPORTED, "structured element solve: unsupported input");
   return HDR_OK;
 }
+
+// exact-path bookkeeping of an operator (list capacity = cells) and the space's scratch
+void exact_prepare(hdr_space_t sp, hdr_hybrid_s* op, cudaStream_t st) {
+  if (!op->xlist.p) op->xlist.alloc(static_cast<size_t>(std::max<int64_t>(sp->ncells, 1)));
+  if (!op->xcount.p) {
+    op->xcount.alloc(4);
+    CK(cudaMemsetAsync(op->xcount.p, 0, 4 * sizeof(int), st));
+    op->xbad.alloc(1);
+    CK(cudaMemsetAsync(op->xbad.p, 0xff, sizeof(unsigned long long), st));
+  }
+  if (sp->k > 0 && !sp->xws.p)
+    sp->xws.alloc(static_cast<size_t>(exact_grid(sp->n)) * static_cast<size_t>(exact_ws_doubles(sp->n, 0)));
+}
+
+ExactArgs exact_args(hdr_space_t sp, hdr_hybrid_s* op, int mode, const double* a, const double* b, const double* f) {
+  ExactArgs X{};
+  X.m = sp->dm;
+  X.n = sp->n;
+  X.nF = sp->nF;
+  X.mode = mode;
+  X.D = sp->fx.D;
+  X.M = sp->fx.M;
+  X.alpha = a;
+  X.beta = b;
+  X.f = f;
+  X.mbase = sp->mbase.p;
+  X.rowoff = sp->row_h.p;
+  X.hval = op->hval.p;
+  X.g = op->g.p;
+  X.xlist = op->xlist.p;
+  X.xcount = op->xcount.p;
+  X.status = op->status.p;
+  X.bad = op->xbad.p;
+  return X;
+}
+
+// Relative accuracy assumed for the correction terms in the acceptance test
+// (struct_order): fp32 products of fp32-rounded operands accumulated over n terms
+// in two chained GEMMs, in the probabilistic rounding-error model
+// sqrt(2n) * 2^-24; the tcgen05 3xTF32 form (fp32 accumulation in TMEM,
+// k_hyb_big) measured at ~1e-6 of |C|.
+double default_eps32(int n) { return std::sqrt(2.0 * n) * 0x1p-24; }
+constexpr double kDefaultEpsTc = 1e-6;
 
 }  // namespace
 
@@ -233,6 +291,8 @@ hdr_status hdr_space_create(int dim, const int64_t cells[3], const double h[3], 
     if (!precompute_structured(sp->re, static_cast<int>(ipow(order + 1, dim)), &sp->st, &err))
       return fail(HDR_UNSUPPORTED, err);
     sp->r = sp->st.r;
+    sp->eps32 = default_eps32(n);
+    sp->eps_tc = kDefaultEpsTc;
 
     // mesh numbering
     DevMesh& m = sp->dm;
@@ -561,11 +621,23 @@ static hdr_status run_hybridize(hdr_hybrid_t op, const double* alpha, const doub
       CK(cudaMemsetAsync(op->status.p, 0, sizeof(int), st));
     }
     if (sp->geom) return geom_hybridize(sp->geom, da, db, df, op->hval.p, op->g.p, st);
+    exact_prepare(sp, op, st);
+    // k >= 1: the exact-path list is rebuilt every call (kern_exact.cu); k = 0: the
+    // kernels solve rejected cells themselves (the brick kernels' list, xcount[2],
+    // is reset by k_rt0_exact); the count is reset here for the synchronous calls
+    if (sp->k > 0 || sync) CK(cudaMemsetAsync(op->xcount.p, 0, sizeof(int), st));
+    op->last_call = 0;
     HybArgs A{};
     A.m = sp->dm;
     A.fx = sp->fx;
     A.nF = sp->nF;
     A.p_max = 4;
+    A.xlist = op->xlist.p;
+    A.xcount = op->xcount.p;
+    A.eps32 = sp->eps32;
+    A.eps_tc = sp->eps_tc;
+    A.force_exact = sp->force_exact;
+    A.qlog = sp->qlog;
     A.alpha = da;
     A.beta = db;
     A.f = df;
@@ -584,7 +656,7 @@ static hdr_status run_hybridize(hdr_hybrid_t op, const double* alpha, const doub
         op->ws_doubles = need;
       }
       launch_hybridize_rt0_rows(A, sp->rt0_consts.data(), op->ws.p, st);
-    } else if (hybridize_big_supported(sp->dim, sp->k) && !getenv("HDR_CTA_PATH")) {
+    } else if (hybridize_big_supported(sp->dim, sp->k)) {
       const int64_t need = hybridize_big_scratch_doubles(A, sp->k);
       if (op->ws_doubles < need) {
         op->ws.alloc(static_cast<size_t>(need));
@@ -594,7 +666,7 @@ static hdr_status run_hybridize(hdr_hybrid_t op, const double* alpha, const doub
       if (!op->pre.p || op->pre.n < static_cast<size_t>(npr) * sp->ncells) op->pre.alloc(static_cast<size_t>(npr) * sp->ncells);
       launch_gemm_f64_nn(npr, static_cast<int>(sp->ncells), sp->n, sp->premat.p, npr, df, sp->n, op->pre.p, npr, st);
       for (int parity = 0; parity < 2; ++parity) launch_hybridize_big(A, sp->k, parity, op->ws.p, op->pre.p, st);
-    } else if (hybridize_warp_supported(sp->dim, sp->k) && !getenv("HDR_CTA_PATH")) {
+    } else if (hybridize_warp_supported(sp->dim, sp->k)) {
       const int64_t need = hybridize_warp_scratch_doubles(A);
       if (op->ws_doubles < need) {
         op->ws.alloc(static_cast<size_t>(need));
@@ -602,17 +674,15 @@ static hdr_status run_hybridize(hdr_hybrid_t op, const double* alpha, const doub
       }
       for (int parity = 0; parity < 2; ++parity) launch_hybridize_warp(A, parity, op->ws.p, st);
     } else {
-      bool use_smem = false;
-      const int64_t need = hybridize_cta_ws_doubles(sp->dm, sp->nF, sp->r, A.p_max, &use_smem);
-      if (!use_smem && !op->ws.p) {
-        op->ws_doubles = need * 148 * 4;
-        op->ws.alloc(static_cast<size_t>(op->ws_doubles));
-      }
-      for (int parity = 0; parity < 2; ++parity) launch_hybridize_cta(A, parity, op->ws.p, op->ws_doubles, st);
+      return fail(HDR_UNSUPPORTED, "hybridize: no structured kernel for this dim / order");
+    }
+    if (sp->k > 0) {  // the rejected cells of each colour, after both colours' fast passes
+      const ExactArgs X = exact_args(sp, op, EXACT_HYB, da, db, df);
+      for (int parity = 0; parity < 2; ++parity) launch_exact(X, parity, sp->xws.p, st);
     }
     CK(cudaGetLastError());
     if (!sync) return HDR_OK;
-    return check_status(op->status.p, st);
+    return check_status(op->status.p, st, op->xbad.p);
   });
 }
 
@@ -702,7 +772,30 @@ hdr_status hdr_hybridize_fe_batch(hdr_space_t sp, int count, const double* const
 
 hdr_status hdr_hybrid_check(hdr_hybrid_t op) {
   if (!op) return fail(HDR_INVALID_ARGUMENT, "null operator");
-  return catch_all([&]() -> hdr_status { return check_status(op->status.p, op->sp->stream); });
+  return catch_all([&]() -> hdr_status { return check_status(op->status.p, op->sp->stream, op->xbad.p); });
+}
+
+hdr_status hdr_hybrid_exact_cells(hdr_hybrid_t op, int64_t* count) {
+  if (!op || !count) return fail(HDR_INVALID_ARGUMENT, "null argument");
+  return catch_all([&]() -> hdr_status {
+    int c = 0;
+    if (op->xcount.p) {
+      const int slot = (op->sp->k == 0 && op->last_call == 1) ? 3 : 0;
+      CK(cudaMemcpyAsync(&c, op->xcount.p + slot, sizeof(int), cudaMemcpyDeviceToHost, op->sp->stream));
+      CK(cudaStreamSynchronize(op->sp->stream));
+    }
+    *count = c;
+    return HDR_OK;
+  });
+}
+
+hdr_status hdr_space_set_exact_policy(hdr_space_t sp, int force_exact, double eps32, double eps_tc, float* q_log) {
+  if (!sp) return fail(HDR_INVALID_ARGUMENT, "null space");
+  sp->force_exact = force_exact ? 1 : 0;
+  sp->eps32 = eps32 > 0 ? eps32 : default_eps32(sp->n);
+  sp->eps_tc = eps_tc > 0 ? eps_tc : kDefaultEpsTc;
+  sp->qlog = q_log;
+  return HDR_OK;
 }
 
 hdr_status hdr_hybrid_symmetrize(hdr_hybrid_t op) {
@@ -790,11 +883,18 @@ hdr_status hdr_recover_hybrid(hdr_hybrid_t op, const double* lambda, const doubl
       CK(cudaStreamSynchronize(st));
       return HDR_OK;
     }
+    exact_prepare(sp, op, st);
+    int* rcount = sp->k > 0 ? op->xcount.p : op->xcount.p + 3;  // k = 0 keeps the hybridize list intact
+    CK(cudaMemsetAsync(rcount, 0, sizeof(int), st));
+    op->last_call = 1;
     RecArgs R{};
     R.m = sp->dm;
     R.fx = sp->fx;
     R.nF = sp->nF;
-    R.p_max = 4;
+    R.p_max = 8;  // fp64 Neumann terms: a-priori order control (struct_order_apriori)
+    R.xlist = op->xlist.p;
+    R.xcount = rcount;
+    R.force_exact = sp->force_exact;
     R.alpha = op->a_ptr;
     R.beta = op->b_ptr;
     R.f = pf;
@@ -803,15 +903,22 @@ hdr_status hdr_recover_hybrid(hdr_hybrid_t op, const double* lambda, const doubl
     R.x_hat = pxh;
     R.x = px;
     R.status = op->status.p;
-    if (sp->k == 0) launch_recover_rt0(R, sp->rt0_consts.data(), st);
-    else launch_recover_hybrid(R, nullptr, 0, st);
+    if (sp->k == 0) {
+      launch_recover_rt0(R, sp->rt0_consts.data(), st);
+    } else {
+      launch_recover_hybrid(R, nullptr, 0, st);
+      ExactArgs X = exact_args(sp, op, EXACT_REC, op->a_ptr, op->b_ptr, pf);
+      X.lambda = pl;
+      X.x_hat = pxh;
+      launch_exact(X, 0, sp->xws.p, st);
+    }
     launch_average_faces(sp->dm, pxh, px, st);
     CK(cudaGetLastError());
     if (!on_device) {
       if (x_hat) CK(cudaMemcpyAsync(x_hat, pxh, static_cast<size_t>(sp->broken) * 8, cudaMemcpyDeviceToHost, st));
       if (x) CK(cudaMemcpyAsync(x, px, static_cast<size_t>(sp->ndofs) * 8, cudaMemcpyDeviceToHost, st));
     }
-    return check_status(op->status.p, st);
+    return check_status(op->status.p, st, op->xbad.p);
   });
 }
 

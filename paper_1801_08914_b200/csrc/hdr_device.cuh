@@ -277,4 +277,89 @@ __device__ __forceinline__ double delta_entry(double alpha, double beta, double 
   return __fma_rn(alpha, e, __fma_rn(beta, ma, delta));
 }
 
+
+// ------------------------------------------------------------ double-double arithmetic (exact path)
+// (hi, lo) pairs with |lo| <= ulp(hi) / 2; every step through the rounding
+// intrinsics so no contraction can break an error-free transform.
+struct ddr {
+  double hi, lo;
+};
+__device__ __forceinline__ ddr dd_quick(double s, double e) {
+  const double h = __dadd_rn(s, e);
+  return {h, __dsub_rn(e, __dsub_rn(h, s))};
+}
+__device__ __forceinline__ ddr dd_from(double a) { return {a, 0.0}; }
+__device__ __forceinline__ ddr dd_add(ddr a, ddr b) {  // accurate sum (both parts two-summed)
+  double s, e, t, f;
+  two_sum(a.hi, b.hi, s, e);
+  two_sum(a.lo, b.lo, t, f);
+  e = __dadd_rn(e, t);
+  ddr r = dd_quick(s, e);
+  return dd_quick(r.hi, __dadd_rn(r.lo, f));
+}
+__device__ __forceinline__ ddr dd_neg(ddr a) { return {-a.hi, -a.lo}; }
+__device__ __forceinline__ ddr dd_mul(ddr a, ddr b) {
+  double p, e;
+  two_prod(a.hi, b.hi, p, e);
+  e = __fma_rn(a.hi, b.lo, e);
+  e = __fma_rn(a.lo, b.hi, e);
+  return dd_quick(p, e);
+}
+__device__ __forceinline__ ddr dd_div(ddr a, ddr b) {  // three-term long division
+  const double q1 = __ddiv_rn(a.hi, b.hi);
+  ddr r = dd_add(a, dd_neg(dd_mul(b, dd_from(q1))));
+  const double q2 = __ddiv_rn(r.hi, b.hi);
+  r = dd_add(r, dd_neg(dd_mul(b, dd_from(q2))));
+  const double q3 = __ddiv_rn(r.hi, b.hi);
+  return dd_add(dd_quick(q1, q2), dd_from(q3));
+}
+// a - b * c
+__device__ __forceinline__ ddr dd_fms(ddr a, ddr b, ddr c) { return dd_add(a, dd_neg(dd_mul(b, c))); }
+
+// ------------------------------------------------------------ structured-solve order control
+// (DESIGN.md §2 "Fail-safe").  q = max|first-order term| / max|zero-order term|
+// of the cell, measured a posteriori.  After P Neumann orders the remainder is
+// estimated as 10 q^(P+1) (geometric tail, q < 0.25); the fp32 / TF32 evaluation
+// of the correction terms adds about q * eps of |H_T| (eps: the relative
+// accuracy of the correction arithmetic, set per kernel by the host,
+// kStructEps*).  A cell whose estimated error exceeds kStructTol of its own
+// |H_T|, or whose q is not < 0.25, is not accepted: it is marked for the exact
+// path (double-double LU of A_T, kern_exact.cu) and contributes nothing here.
+constexpr double kStructTol = 1e-12;
+__device__ __forceinline__ int struct_order(double q, int p_max, double eps, bool& exact) {
+  if (!(q < 0.25)) {
+    exact = true;
+    return 1;
+  }
+  int P = 1;
+  double t = 10.0 * q * q;
+  while (t > kStructTol && P < p_max) {
+    ++P;
+    t *= q;
+  }
+  exact = t > kStructTol || q * eps > kStructTol;
+  return P;
+}
+// a-priori form (fp64 corrections: recovery): tau = rho alpha / beta bounds the
+// Neumann ratio; remainder tau^(P+1)
+__device__ __forceinline__ int struct_order_apriori(double tau, int p_max, bool& exact) {
+  if (!(tau < 0.25)) {
+    exact = true;
+    return 1;
+  }
+  int P = 1;
+  double t = tau * tau;
+  while (t > 1e-14 && P < p_max) {
+    ++P;
+    t *= tau;
+  }
+  exact = t > 1e-14;
+  return P;
+}
+// appends cell e to the exact-path list (capacity = cells of the mesh)
+__device__ __forceinline__ void exact_push(int* list, int* count, int e) {
+  const int s = atomicAdd(count, 1);
+  list[s] = e;
+}
+
 }  // namespace hdr

@@ -58,10 +58,6 @@ struct Big {
   static constexpr int TCOLS = TCOLS_USED <= 32 ? 32 : TCOLS_USED <= 64 ? 64 : TCOLS_USED <= 128 ? 128 : TCOLS_USED <= 256 ? 256 : 512;
 };
 
-#ifndef HDR_TC_TAU
-#define HDR_TC_TAU 1e-6
-#endif
-
 constexpr int kThreads = 512;
 
 #ifdef HDR_BIG_TIMING  // phase cycle counters of CTA 0 (variant builds only: make EXTRA=-DHDR_BIG_TIMING)
@@ -108,6 +104,7 @@ struct BigSmem {
   int rlen[B::NS], grow[B::NS], rank[B::NS * B::NS];
   float red[2 * kThreads / 32];
   int order;
+  int exact;  // the cell is rejected: zeros here, the exact path (kern_exact.cu) adds it
   uint64_t mbar[2];
   uint32_t tmem;
 };
@@ -544,19 +541,22 @@ __global__ void __launch_bounds__(kThreads, 1) k_hyb_big(HybArgs A, int parity, 
           hm = fmaxf(hm, sm.red[kThreads / 32 + w]);
         }
         const double ratio = hm > 0.f ? static_cast<double>(cm) / hm : 0.0;
-        int p = 1;
-        double tt = ratio * ratio * 10.0;
-        while (tt > 1e-12 && p < A.p_max) {
-          ++p;
-          tt *= ratio;
-        }
-        if (!(ratio < 0.25)) atomicOr(A.status, 1);
         // the tensor core's fp32 accumulation is less accurate than fp32 FMA
-        // chains (~1e-6 of |C|): accept its C only where C itself is tiny
-        sm.order = (p == 1 && ratio <= HDR_TC_TAU) ? 1 : 0;
+        // chains (eps_tc ~ 1e-6 of |C|): its C is accepted only where the
+        // estimate allows it at order 1 (hdr_device.cuh struct_order); cells the
+        // CUDA-core form cannot accept either go straight to the exact path
+        bool ex_tc = false, ex32 = false;
+        const int p = struct_order(ratio, A.p_max, A.eps_tc, ex_tc);
+        struct_order(ratio, A.p_max, A.eps32, ex32);
+        sm.exact = (ex32 || A.force_exact) ? 1 : 0;
+        sm.order = (!ex_tc && p == 1) ? 1 : 0;
+        if (A.qlog) A.qlog[e] = static_cast<float>(ratio);
+        if (sm.exact) exact_push(A.xlist, A.xcount, e);
       }
       __syncthreads();
-      tc_done = sm.order == 1;
+      tc_done = sm.order == 1 || sm.exact;
+    } else if (tid == 0) {
+      sm.exact = 0;
     }
     BIG_T(5);
     if (!tc_done) {
@@ -658,14 +658,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_hyb_big(HybArgs A, int parity, 
               hm = fmaxf(hm, sm.red[kThreads / 32 + w]);
             }
             const double ratio = hm > 0.f ? static_cast<double>(cm) / hm : 0.0;
-            int p = 1;
-            double tt = ratio * ratio * 10.0;
-            while (tt > 1e-12 && p < A.p_max) {
-              ++p;
-              tt *= ratio;
-            }
-            if (!(ratio < 0.25)) atomicOr(A.status, 1);
-            sm.order = p;
+            bool ex = false;
+            const int p = struct_order(ratio, A.p_max, A.eps32, ex);
+            ex = ex || A.force_exact;
+            sm.order = ex ? 1 : p;
+            if (A.qlog && !use_tc) A.qlog[e] = static_cast<float>(ratio);
+            if (ex) exact_push(A.xlist, A.xcount, e);  // (reached only for cells not yet rejected)
+            sm.exact = ex ? 1 : 0;
           }
           __syncthreads();
           P = sm.order;
@@ -700,6 +699,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_hyb_big(HybArgs A, int parity, 
       __syncthreads();
     }
     BIG_T(6);
+    const bool cell_exact = sm.exact != 0;
     // ---------------------------------------------------------------- scatter
     // four entries per thread per pass: every load (vf, csm, the shared diagonal
     // blocks' partial sums) issued before the first store
@@ -728,6 +728,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_hyb_big(HybArgs A, int parity, 
           const int c = qs * DPF + 2 * j2;
           val[u] = make_double2(vf[p * NC + c] - static_cast<double>(sm.u.csm[p * NCP + c]),
                                 vf[p * NC + c + 1] - static_cast<double>(sm.u.csm[p * NCP + c + 1]));
+          if (cell_exact) val[u] = make_double2(0.0, 0.0);
           dst[u] = reinterpret_cast<double2*>(A.hval + rs + static_cast<int64_t>(sub) * sm.rlen[ps] + rk * DPF) + j2;
           acc[u] = parity == 1 && ps == qs;
         }
@@ -740,7 +741,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_hyb_big(HybArgs A, int parity, 
       for (int p = tid; p < NF; p += kThreads) {
         const int ps = p / DPF, sub = p - ps * DPF;
         if (sm.rstart[ps] < 0) continue;
-        const double v = vf[p * NC + NF] - static_cast<double>(sm.u.csm[p * NCP + NF]);
+        const double v = cell_exact ? 0.0 : vf[p * NC + NF] - static_cast<double>(sm.u.csm[p * NCP + NF]);
         double* gp = A.g + sm.grow[ps] + sub;
         *gp = parity ? *gp + v : v;
       }
@@ -761,7 +762,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_hyb_big(HybArgs A, int parity, 
         const int ps = p / DPF, sub = p - ps * DPF;
         const int64_t rs = sm.rstart[ps];
         if (rs < 0) continue;
-        val[u] = vf[p * NC + c] - static_cast<double>(sm.u.csm[p * NCP + c]);
+        val[u] = cell_exact ? 0.0 : vf[p * NC + c] - static_cast<double>(sm.u.csm[p * NCP + c]);
         if (c == NF) {
           dst[u] = A.g + sm.grow[ps] + sub;
           acc[u] = parity != 0;

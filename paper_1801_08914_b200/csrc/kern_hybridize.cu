@@ -39,18 +39,103 @@ namespace hdr {
 
 namespace {
 
-__device__ inline int neumann_order(double tau, int p_max, int* status) {
-  if (!(tau < 0.25)) {
-    atomicOr(status, 1);
-    return p_max;
+// Exact path of one cell in one thread (k = 0 kernels; the structured
+// estimate rejected the cell, hdr_device.cuh struct_order): double-double
+// Gaussian elimination on the reference's A_T = fl(fl(alpha D) + fl(beta M)) in
+// its [i | b] partition (bmask bit l: local dof l is an interior-face (b) dof),
+// pivoting restricted to the i rows for the first n_i steps so that the
+// reference's SingularBlock rule sees the pivots of A_ii and of S_b
+// (src/reduction.cpp:279-302, src/dense.cpp:61-97; kern_exact.cu does the same
+// for k >= 1), applied to [I | r] (IDENT, NC = N + 1: rows of A_T^-1 and
+// A_T^-1 f, i.e. [H_T | g_T] rows) or to r alone (NC = 1: the recovery
+// x_hat = A_T^-1 (f - C^T lambda), r given as (rh, rl)).  out: N x NC row-major
+// in the local dof order, rounded once.  Local-memory arrays: only the rare
+// rejected cells run this.
+template <int N, int NC, bool IDENT>
+__device__ __forceinline__ void rt0_exact(const double* D, const double* M, double a, double b, unsigned bmask,
+                                          const double* rh, const double* rl, double* out, int* status) {
+  ddr A[N][N], B[N][NC];
+  int perm[N];  // partitioned position -> local dof
+  int ni = 0;
+  for (int l = 0; l < N; ++l)
+    if (!((bmask >> l) & 1u)) perm[ni++] = l;
+  for (int l = 0, q = ni; l < N; ++l)
+    if ((bmask >> l) & 1u) perm[q++] = l;
+  double amax = 0.0;
+  for (int i = 0; i < N; ++i) {
+    const int li = perm[i];
+    for (int j = 0; j < N; ++j) {
+      const int lj = perm[j];
+      A[i][j] = dd_from(assemble_entry(a, b, D[li * N + lj], M[li * N + lj]));
+      if (i < ni && j < ni) amax = fmax(amax, fabs(A[i][j].hi));
+    }
+    for (int c = 0; c < NC; ++c) {
+      if (IDENT) B[i][c] = c < N ? dd_from(li == c ? 1.0 : 0.0) : dd_from(rh[li]);
+      else B[i][c] = {rh[li], rl ? rl[li] : 0.0};
+    }
   }
-  int p = 1;
-  double t = tau * tau;
-  while (t > 1e-14 && p < p_max) {
-    ++p;
-    t *= tau;
+  for (int k = 0; k < N; ++k) {
+    if (k == ni) {  // max |S_b| of the trailing block
+      amax = 0.0;
+      for (int i = ni; i < N; ++i)
+        for (int j = ni; j < N; ++j) amax = fmax(amax, fabs(A[i][j].hi));
+    }
+    const int kend = k < ni ? ni : N;
+    int p = k;
+    for (int i = k + 1; i < kend; ++i)
+      if (fabs(A[i][k].hi) > fabs(A[p][k].hi)) p = i;
+    if (p != k) {
+      for (int j = 0; j < N; ++j) {
+        const ddr t = A[k][j];
+        A[k][j] = A[p][j];
+        A[p][j] = t;
+      }
+      for (int c = 0; c < NC; ++c) {
+        const ddr t = B[k][c];
+        B[k][c] = B[p][c];
+        B[p][c] = t;
+      }
+    }
+    if (!(fabs(A[k][k].hi) > 1e-14 * amax)) {
+      atomicOr(status, 4);
+      return;
+    }
+    for (int i = k + 1; i < N; ++i) {
+      const ddr l = dd_div(A[i][k], A[k][k]);
+      for (int j = k + 1; j < N; ++j) A[i][j] = dd_fms(A[i][j], l, A[k][j]);
+      for (int c = 0; c < NC; ++c) B[i][c] = dd_fms(B[i][c], l, B[k][c]);
+    }
   }
-  return p;
+  for (int k = N - 1; k >= 0; --k) {
+    for (int c = 0; c < NC; ++c) {
+      ddr v = B[k][c];
+      for (int j = k + 1; j < N; ++j) v = dd_fms(v, A[k][j], B[j][c]);
+      B[k][c] = dd_div(v, A[k][k]);
+    }
+  }
+  for (int i = 0; i < N; ++i)
+    for (int c = 0; c < NC; ++c) out[perm[i] * NC + c] = B[i][c].hi;
+}
+
+// out-of-line form (the recovery kernel keeps its registers for the fast path)
+template <int N, int NC, bool IDENT>
+__device__ __noinline__ void rt0_exact_ool(const double* D, const double* M, double a, double b, unsigned bmask,
+                                           const double* rh, const double* rl, double* out, int* status) {
+  rt0_exact<N, NC, IDENT>(D, M, a, b, bmask, rh, rl, out, status);
+}
+
+// interior-face mask of a k = 0 cell (bit s: slot s's face is interior = a b dof)
+template <int DIM>
+__device__ __forceinline__ unsigned rt0_bmask(const DevMesh& m, const int (&cc)[3]) {
+  unsigned mask = 0;
+#pragma unroll
+  for (int s = 0; s < 2 * DIM; ++s) {
+    const int ax = s >> 1, side = s & 1;
+    const int ca = ax == 0 ? cc[0] : (ax == 1 ? cc[1] : cc[2]);
+    const int na = static_cast<int>(ax == 0 ? m.N[0] : (ax == 1 ? m.N[1] : m.N[2]));
+    mask |= static_cast<unsigned>(side ? (ca + 1 < na) : (ca > 0)) << s;
+  }
+  return mask;
 }
 
 // ------------------------------------------------------------------ k = 0
@@ -81,7 +166,7 @@ struct Rt0Const {
 template <int DIM>
 __device__ __forceinline__ void rt0_row_math(const HybArgs& A, const Rt0Const<2 * DIM>& c, int e, int k, int& P,
                                              bool real, float* vsh, float* ysh, float* tsh, float* dsh,
-                                             double (&h)[2 * DIM + 1]) {
+                                             double (&h)[2 * DIM + 1], bool& exact) {
   constexpr int N = 2 * DIM;
   constexpr int NC = N + 1;
   const double* Dk = A.fx.D + k * N;
@@ -166,14 +251,12 @@ __device__ __forceinline__ void rt0_row_math(const HybArgs& A, const Rt0Const<2 
         hm = fmaxf(hm, __shfl_sync(0xffffffffu, hm, base + j));
       }
       const double ratio = hm > 0.f ? static_cast<double>(cm) / hm : 0.0;
-      int pc = 1;
-      double tt = ratio * ratio * 10.0;
-      while (tt > 1e-12 && pc < A.p_max) {
-        ++pc;
-        tt *= ratio;
-      }
-      if (!real) pc = 1;
-      else if (!(ratio < 0.25) && k == 0) atomicOr(A.status, 1);
+      bool ex = false;
+      int pc = struct_order(ratio, A.p_max, A.eps32, ex);
+      ex = real && (ex || A.force_exact);
+      if (ex || !real) pc = 1;
+      exact = ex;
+      if (real && k == 0 && A.qlog) A.qlog[e] = static_cast<float>(ratio);
       P = __reduce_max_sync(0xffffffffu, pc);
     }
     if (p == P) break;
@@ -198,7 +281,8 @@ __device__ __forceinline__ void rt0_row_math(const HybArgs& A, const Rt0Const<2 
 }
 
 template <int DIM, int PASS>
-__global__ void __launch_bounds__(128, HDR_ROWS_MINB) k_rt0_rows(HybArgs A, Rt0Const<2 * DIM> c, double* stage) {
+__device__ __forceinline__ bool rt0_rows_body(const HybArgs& A, const Rt0Const<2 * DIM>& c, double* stage) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // the exact-path kernel may launch
   constexpr int N = 2 * DIM;
   constexpr int NC = N + 1;
   constexpr int G = 32 / N;  // cells per warp
@@ -221,8 +305,18 @@ __global__ void __launch_bounds__(128, HDR_ROWS_MINB) k_rt0_rows(HybArgs A, Rt0C
   const int ee = valid ? e : 0;
   int P = 1;
   double h[N + 1];
-  rt0_row_math<DIM>(A, c, ee, kk, P, valid, vbuf[warp][gi], ybuf[warp][gi], tbuf[warp][gi], dbuf[warp][gi], h);
-  if (!valid) return;
+  bool exact = false;
+  const bool& rejected = exact;
+  rt0_row_math<DIM>(A, c, ee, kk, P, valid, vbuf[warp][gi], ybuf[warp][gi], tbuf[warp][gi], dbuf[warp][gi], h, exact);
+  if (!valid) return rejected;
+  if (exact) {  // rejected by the estimate: this lane's row from the exact solve
+    if (k == 0) atomicAdd(A.xcount, 1);
+    double hx[N * NC];
+    rt0_exact_ool<N, NC, true>(A.fx.D, A.fx.M, A.alpha[e], A.beta[e], rt0_bmask<DIM>(A.m, cc),
+                               A.f + static_cast<int64_t>(e) * N, nullptr, hx, A.status);
+#pragma unroll
+    for (int q = 0; q <= N; ++q) h[q] = hx[k * NC + q];
+  }
   if (PASS == 0) {
     double* slot = stage + static_cast<int64_t>(t) * (N * NC) + k * NC;
     if (HDR_L2HINT >= 1) {
@@ -233,14 +327,14 @@ __global__ void __launch_bounds__(128, HDR_ROWS_MINB) k_rt0_rows(HybArgs A, Rt0C
 #pragma unroll
       for (int q = 0; q <= N; ++q) slot[q] = h[q];
     }
-    return;
+    return rejected;
   }
   // pass 1: complete rows of this cell's interior faces
   const int a = k >> 1, side = k & 1;
   const int ca = a == 0 ? cc[0] : (a == 1 ? cc[1] : cc[2]);
   const int na = static_cast<int>(a == 0 ? A.m.N[0] : (a == 1 ? A.m.N[1] : A.m.N[2]));
   const bool kin = side ? (ca + 1 < na) : (ca > 0);
-  if (!kin) return;
+  if (!kin) return rejected;
   const int step = side ? 1 : -1;
   const int nc[3] = {cc[0] + (a == 0 ? step : 0), cc[1] + (a == 1 ? step : 0), cc[2] + (a == 2 ? step : 0)};
   const int kn = k ^ 1;  // the shared face's slot in the neighbour
@@ -288,6 +382,12 @@ __global__ void __launch_bounds__(128, HDR_ROWS_MINB) k_rt0_rows(HybArgs A, Rt0C
     else out[r] = nrow[q];
   }
   A.g[row] = h[N] + nrow[N];
+  return rejected;
+}
+
+template <int DIM, int PASS>
+__global__ void __launch_bounds__(128, HDR_ROWS_MINB) k_rt0_rows(HybArgs A, Rt0Const<2 * DIM> c, double* stage) {
+  rt0_rows_body<DIM, PASS>(A, c, stage);
 }
 
 // ------------------------------------------------------------------ k = 0, thread-per-cell form
@@ -466,28 +566,37 @@ __device__ __noinline__ void rt0_general_correction(const double* Dg, const doub
 }
 
 // the cell's correction C (registers): structured first order, general loop if needed
+// returns true when the cell is rejected: then C = 0 and the caller sets 1 / beta
+// = 0, so every row of [H_T | g_T] comes out exactly 0 (no branch in the row
+// code); the kernel then adds the cell's exact rows (rt0_exact) where its rows
+// were assembled
 template <int DIM>
-__device__ __forceinline__ void rt0_correction(const HybArgs& A, const Rt0Const<2 * DIM>& c, const Rt0Fast<2 * DIM>& F,
+__device__ __forceinline__ bool rt0_correction(const HybArgs& A, const Rt0Const<2 * DIM>& c, const Rt0Fast<2 * DIM>& F,
                                                double a, double b, double s, double ib, float* scr, int stride,
-                                               float (&C)[Rt0Fast<2 * DIM>::NS]) {
+                                               float (&C)[Rt0Fast<2 * DIM>::NS], int64_t e) {
   constexpr int N = 2 * DIM;
   float hm;
   const float cm = rt0_fast_correction<DIM>(c, F, a, b, s, ib, C, hm);
-  // a-posteriori order control (as the other k = 0 kernels)
+  // a-posteriori order control and acceptance (hdr_device.cuh struct_order)
   const double ratio = hm > 0.f ? static_cast<double>(cm) / hm : 0.0;
-  int P = 1;
-  double tt = ratio * ratio * 10.0;
-  while (tt > 1e-12 && P < A.p_max) {
-    ++P;
-    tt *= ratio;
+  if (A.qlog) A.qlog[e] = static_cast<float>(ratio);
+  bool exact = false;
+  const int P = struct_order(ratio, A.p_max, A.eps32, exact);
+  if (exact || A.force_exact) {  // rejected: zero contribution (the caller zeroes 1 / beta too)
+#pragma unroll
+    for (int i = 0; i < Rt0Fast<N>::NS; ++i) C[i] = 0.f;
+    atomicAdd(A.xcount, 1);
+    return true;
   }
-  if (!(ratio < 0.25)) atomicOr(A.status, 1);
   if (P > 1) {
     rt0_general_correction<DIM>(A.fx.D, A.fx.M, A.fx.E, A.fx.Ma, A.fx.N0, A.fx.X, a, b, s, ib, P, scr, stride);
 #pragma unroll
     for (int i = 0; i < Rt0Fast<N>::NS; ++i) C[i] = scr[(2 * N * N + i) * stride];
   }
+  return false;
 }
+
+
 
 // row k of [H_T | g_T] = [V | w]_k,: (fp64) - [C | C f]_k,:
 template <int DIM>
@@ -509,8 +618,9 @@ __device__ __forceinline__ void rt0_hrow_c(const Rt0Const<2 * DIM>& c, double s,
 }
 
 template <int DIM, int PASS, bool SIDE>
-__global__ void __launch_bounds__(kCT, HDR_CELL_MINB) k_rt0_cell(HybArgs A, Rt0Const<2 * DIM> c, Rt0Fast<2 * DIM> F,
-                                                               double* stage) {
+__device__ __forceinline__ bool rt0_cell_body(const HybArgs& A, const Rt0Const<2 * DIM>& c, const Rt0Fast<2 * DIM>& F,
+                                              double* stage) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // the exact-path kernel may launch
   constexpr int N = 2 * DIM;
   constexpr int NC = N + 1;
   __shared__ float scr[2 * N * N + Rt0Fast<N>::NS][kCT];  // general-correction scratch (rare cells)
@@ -520,9 +630,9 @@ __global__ void __launch_bounds__(kCT, HDR_CELL_MINB) k_rt0_cell(HybArgs A, Rt0C
   const int tid = threadIdx.x;
   const uint32_t t = blockIdx.x * kCT + tid;
   int cc[3] = {0, 0, 0};
-  if (t >= static_cast<uint32_t>(parity_count(A.m))) return;
+  if (t >= static_cast<uint32_t>(parity_count(A.m))) return false;
   const int e = parity_cell32(A.m, PASS, t, cc);
-  if (e < 0) return;
+  if (e < 0) return false;
   const double a = A.alpha[e], b = A.beta[e];
   // SIDE: the scatter metadata of the cell's interior faces (row start + row, the
   // packed column ranks, colour 1: colour 0's parked side slot) is fetched into
@@ -557,8 +667,9 @@ __global__ void __launch_bounds__(kCT, HDR_CELL_MINB) k_rt0_cell(HybArgs A, Rt0C
 #pragma unroll
   for (int j = 0; j < N; ++j) f[j] = A.f[static_cast<int64_t>(e) * N + j];
   float C[Rt0Fast<N>::NS];
-  rt0_correction<DIM>(A, c, F, a, b, s, ib, &scr[0][tid], kCT, C);
-  auto hrow = [&](int k, double (&h)[NC]) { rt0_hrow_c<DIM>(c, s, ib, f, C, k, h); };
+  const bool rejected = rt0_correction<DIM>(A, c, F, a, b, s, ib, &scr[0][tid], kCT, C, e);
+  const double ibr = rejected ? 0.0 : ib;
+  auto hrow = [&](int k, double (&h)[NC]) { rt0_hrow_c<DIM>(c, s, ibr, f, C, k, h); };
   if (SIDE) {
     // both colours write their own columns of their faces' rows straight into H;
     // the two shared quantities of a row (diagonal, g) meet in a per-row side
@@ -593,68 +704,41 @@ __global__ void __launch_bounds__(kCT, HDR_CELL_MINB) k_rt0_cell(HybArgs A, Rt0C
         A.g[row] = h[N] + sv.y;
       }
     }
-    return;
-  }
-  if (PASS == 0) {
-    double* slot = stage + static_cast<int64_t>(t) * (N * NC);
-    const uint64_t pol = l2_policy_evict_last();
-#pragma unroll
-    for (int k = 0; k < N; ++k) {
-      double h[NC];
-      hrow(k, h);
-#pragma unroll
-      for (int q = 0; q <= N; ++q) st_l2hint(slot + k * NC + q, h[q], pol);
+    if (rejected) {  // rare: the cell's exact rows over its zero ones (same positions, same sums)
+      double hx[N * NC];
+      rt0_exact_ool<N, NC, true>(A.fx.D, A.fx.M, a, b, inmask, A.f + static_cast<int64_t>(e) * N, nullptr, hx,
+                                 A.status);
+      for (int k = 0; k < N; ++k) {
+        if (!((inmask >> k) & 1u)) continue;
+        const longlong2 rs = pf_rs[k][tid];
+        const uint64_t own = pf_tab[k][tid];
+        double* out = A.hval + rs.x;
+        for (int q = 0; q < N; ++q) {
+          const unsigned r = static_cast<unsigned>(own >> (4 * q)) & 15u;
+          if (r != 15u && q != k) out[r] = hx[k * NC + q];
+        }
+        if (PASS == 0) {
+          const int a_ = k >> 1, side = k & 1;
+          const int face = face_id32(A.m, a_, cc[0] + (a_ == 0 ? side : 0), cc[1] + (a_ == 1 ? side : 0),
+                                     cc[2] + (a_ == 2 ? side : 0));
+          stage[2 * static_cast<int64_t>(face)] = hx[k * NC + k];
+          stage[2 * static_cast<int64_t>(face) + 1] = hx[k * NC + N];
+        } else {
+          const double2 sv = pf_sv[k][tid];
+          out[(own >> (4 * k)) & 15u] = hx[k * NC + k] + sv.x;
+          A.g[static_cast<int>(rs.y)] = hx[k * NC + N] + sv.y;
+        }
+      }
     }
-    return;
+    return rejected;
   }
-  // pass 1: complete rows of this cell's interior faces (lo, hi still 0: SIDE is false)
-#pragma unroll
-  for (int x = 0; x < DIM; ++x) {
-    const int cx = x == 0 ? cc[0] : (x == 1 ? cc[1] : cc[2]);
-    const int Nx = static_cast<int>(x == 0 ? A.m.N[0] : (x == 1 ? A.m.N[1] : A.m.N[2]));
-    lo |= static_cast<unsigned>(cx > 0) << x;
-    hi |= static_cast<unsigned>(cx + 1 < Nx) << x;
-  }
-  const uint64_t pol = l2_policy_evict_first();
-  const uint32_t half = static_cast<uint32_t>((A.m.N[0] + 1) / 2);
-#pragma unroll
-  for (int k = 0; k < N; ++k) {
-    const int a_ = k >> 1, side = k & 1;
-    const int ca = a_ == 0 ? cc[0] : (a_ == 1 ? cc[1] : cc[2]);
-    const int na = static_cast<int>(a_ == 0 ? A.m.N[0] : (a_ == 1 ? A.m.N[1] : A.m.N[2]));
-    if (!(side ? (ca + 1 < na) : (ca > 0))) continue;
-    const int step = side ? 1 : -1;
-    const int nc0 = cc[0] + (a_ == 0 ? step : 0), nc1 = cc[1] + (a_ == 1 ? step : 0), nc2 = cc[2] + (a_ == 2 ? step : 0);
-    const uint32_t tn = (static_cast<uint32_t>(nc1) + static_cast<uint32_t>(A.m.N[1]) * nc2) * half + (nc0 >> 1);
-    const int kn = k ^ 1;
-    const double* nrow_p = stage + static_cast<int64_t>(tn) * (N * NC) + kn * NC;
-    double nrow[NC];
-#pragma unroll
-    for (int q = 0; q <= N; ++q) nrow[q] = nrow_p[q];
-    const int face = face_id32(A.m, a_, cc[0] + (a_ == 0 ? side : 0), cc[1] + (a_ == 1 ? side : 0), cc[2] + (a_ == 2 ? side : 0));
-    const int row = A.mbase[face];
-    const unsigned far = side ? static_cast<unsigned>(ca + 2 < na) : static_cast<unsigned>(ca >= 2);
-    const unsigned flags = lo | (hi << DIM) | (far << (2 * DIM));
-    const uint64_t* tab = A.rank_tab + ((static_cast<size_t>(k) << (2 * DIM + 1)) + flags) * 2;
-    const uint64_t own = __ldg(tab), nbr = __ldg(tab + 1);
-    double* out = A.hval + A.rowoff[row];
-    double h[NC];
-    hrow(k, h);
-#pragma unroll
-    for (int q = 0; q < N; ++q) {
-      const unsigned r = static_cast<unsigned>(own >> (4 * q)) & 15u;
-      if (r == 15u) continue;
-      const double v = q == k ? h[q] + nrow[kn] : h[q];
-      st_l2hint(out + r, v, pol);
-    }
-#pragma unroll
-    for (int q = 0; q < N; ++q) {
-      const unsigned r = static_cast<unsigned>(nbr >> (4 * q)) & 15u;
-      if (r == 15u) continue;
-      st_l2hint(out + r, nrow[q], pol);
-    }
-    A.g[row] = h[N] + nrow[N];
-  }
+  return rejected;  // (SIDE is the only form)
+}
+
+template <int DIM, int PASS, bool SIDE>
+__global__ void __launch_bounds__(kCT, HDR_CELL_MINB) k_rt0_cell(HybArgs A, Rt0Const<2 * DIM> c, Rt0Fast<2 * DIM> F,
+                                                               double* stage) {
+  rt0_cell_body<DIM, PASS, SIDE>(A, c, F, stage);
 }
 
 // ------------------------------------------------------------------ k = 0, brick form (default)
@@ -721,9 +805,62 @@ __device__ __forceinline__ int interior_faces(const DevMesh& m, int x, int y, in
   return n;
 }
 
+// Exact path of the brick kernels: one CTA launched after the colour-1 brick
+// kernel (programmatic dependent launch: its launch overlaps colour 1's tail; it
+// returns at once when no cell was rejected).  The listed cells' [H_T | g_T] by
+// rt0_exact (one thread per cell, colour 0 first, then colour 1, so no two cells
+// of one round share an H entry) added into H and g at the positions of the
+// row-rank table: their own columns held 0, the diagonal and g the neighbour's
+// term.  The list length (xcount[2]) is reset for the next call.
+template <int DIM>
+__global__ void __launch_bounds__(256) k_rt0_exact(HybArgs A) {
+  constexpr int N = 2 * DIM, NC = N + 1;
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // both colours complete, their writes visible
+  const int cnt = A.xcount[2];
+  const DevMesh& m = A.m;
+  for (int colour = 0; colour < 2 && cnt > 0; ++colour) {
+    for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+      const int e = A.xlist[i];
+      int cc[3];
+      cell_coords32(m, static_cast<uint32_t>(e), cc);
+      if (DIM == 2) cc[2] = 0;
+      if (((cc[0] + cc[1] + cc[2]) & 1) != colour) continue;
+      const unsigned bm = rt0_bmask<DIM>(m, cc);
+      double hx[N * NC];
+      rt0_exact<N, NC, true>(A.fx.D, A.fx.M, A.alpha[e], A.beta[e], bm, A.f + static_cast<int64_t>(e) * N, nullptr,
+                             hx, A.status);
+      unsigned lo = 0, hi = 0;
+      for (int x = 0; x < DIM; ++x) {
+        lo |= ((bm >> (2 * x)) & 1u) << x;
+        hi |= ((bm >> (2 * x + 1)) & 1u) << x;
+      }
+      for (int k = 0; k < N; ++k) {
+        if (!((bm >> k) & 1u)) continue;
+        const int ax = k >> 1, side = k & 1;
+        const int ca = ax == 0 ? cc[0] : (ax == 1 ? cc[1] : cc[2]);
+        const int na = static_cast<int>(ax == 0 ? m.N[0] : (ax == 1 ? m.N[1] : m.N[2]));
+        const int face = face_id32(m, ax, cc[0] + (ax == 0 ? side : 0), cc[1] + (ax == 1 ? side : 0),
+                                   cc[2] + (ax == 2 ? side : 0));
+        const longlong2 rs = A.frs[face];  // {row start, row}
+        const unsigned far = side ? static_cast<unsigned>(ca + 2 < na) : static_cast<unsigned>(ca >= 2);
+        const unsigned flags = lo | (hi << DIM) | (far << (2 * DIM));
+        const uint64_t own = A.rank_tab[((static_cast<size_t>(k) << (2 * DIM + 1)) + flags) * 2];
+        double* out = A.hval + rs.x;
+        for (int q = 0; q < N; ++q) {
+          const unsigned r = static_cast<unsigned>(own >> (4 * q)) & 15u;
+          if (r != 15u) out[r] += hx[k * NC + q];
+        }
+        A.g[rs.y] += hx[k * NC + N];
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) A.xcount[2] = 0;
+}
+
 template <int DIM, int COL, int BX>
-__global__ void __launch_bounds__(BrickDims<DIM, BX>::CT, BrickDims<DIM, BX>::MINB)
-    k_rt0_brick(HybArgs A, Rt0Const<2 * DIM> c, Rt0Fast<2 * DIM> F, double* stage, int nbx, int nby, int nbz) {
+__device__ __forceinline__ bool rt0_brick_body(const HybArgs& A, const Rt0Const<2 * DIM>& c, const Rt0Fast<2 * DIM>& F,
+                                               double* stage, int nbx, int nby, int nbz) {
   using B = BrickDims<DIM, BX>;
   constexpr int N = 2 * DIM;
   constexpr int NC = N + 1;
@@ -740,13 +877,13 @@ __global__ void __launch_bounds__(BrickDims<DIM, BX>::CT, BrickDims<DIM, BX>::MI
   // this colour's bricks: x index alternates within a (by, bz) row
   const int by = static_cast<int>(blockIdx.y), bz = static_cast<int>(blockIdx.z);  // grid (ceil(nbx / 2), nby, nbz)
   const int bx = 2 * static_cast<int>(blockIdx.x) + ((by + bz + COL) & 1);
-  if (bx >= nbx || bz >= nbz) return;
+  if (bx >= nbx || bz >= nbz) return false;
   const int x0 = bx * X, y0 = by * Y, z0 = bz * Z;
   const int ex = min(X, N0 - x0), ey = min(Y, N1 - y0), ez = DIM == 3 ? min(Z, N2 - z0) : 1;
   const int tid = threadIdx.x;
   // programmatic dependent launch: colour 1 may start (line metadata, element
   // solves) while colour 0's last wave runs; it waits before touching the stage
-  if (COL == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // colour 1, resp. the exact-path kernel
   // face p of line (ax, jj, kk): x = x0 + p, y = y0 + jj, z = z0 + kk (ax 1: jj in [0, ey], ax 2: kk in [0, ez])
   auto line_face = [&](int ax, int jj, int kk, int p) { return face_id32(m, ax, x0 + p, y0 + jj, z0 + kk); };
   if (tid < NL) {  // line metadata
@@ -808,6 +945,7 @@ __global__ void __launch_bounds__(BrickDims<DIM, BX>::CT, BrickDims<DIM, BX>::MI
   const int cc[3] = {x0 + lx, y0 + ly, z0 + lz};
   const bool valid = lx < ex && ly < ey && lz < ez;
   double a = 1.0, b = 1.0, s = 1.0, ib = 1.0;
+  bool rejected = false;
   float C[Rt0Fast<N>::NS];
   double f[N];
 #pragma unroll
@@ -820,8 +958,13 @@ __global__ void __launch_bounds__(BrickDims<DIM, BX>::CT, BrickDims<DIM, BX>::MI
     for (int j = 0; j < N; ++j) f[j] = A.f[e * N + j];
     ib = 1.0 / b;
     s = b / fma(a, c.lam, b);
-    rt0_correction<DIM>(A, c, F, a, b, s, ib, scr, CT, C);
+    rejected = rt0_correction<DIM>(A, c, F, a, b, s, ib, scr, CT, C, e);
+    if (rejected) {  // zero rows here; k_rt0_exact adds the exact ones after both colours
+      ib = 0.0;
+      A.xlist[atomicAdd(A.xcount + 2, 1)] = static_cast<int>(e);
+    }
   }
+  auto hrow = [&](int k, double (&h)[NC]) { rt0_hrow_c<DIM>(c, s, ib, f, C, k, h); };
   __syncthreads();  // line metadata
   if (COL == 1) asm volatile("griddepcontrol.wait;" ::: "memory");  // colour 0 complete, stage visible
   unsigned lo = 0, hi = 0;
@@ -844,7 +987,7 @@ __global__ void __launch_bounds__(BrickDims<DIM, BX>::CT, BrickDims<DIM, BX>::MI
       const int face = face_id32(m, ax, cc[0] + (ax == 0 ? side : 0), cc[1] + (ax == 1 ? side : 0), cc[2] + (ax == 2 ? side : 0));
       const bool bb = side ? lc[ax] == ec[ax] - 1 : lc[ax] == 0;  // neighbour in the adjacent brick
       double h[NC];
-      rt0_hrow_c<DIM>(c, s, ib, f, C, k, h);
+      hrow(k, h);
       if (COL == 0 && bb) {
 #pragma unroll
         for (int q = 0; q <= N; ++q) stage[q * nfaces + face] = h[q];
@@ -897,7 +1040,7 @@ __global__ void __launch_bounds__(BrickDims<DIM, BX>::CT, BrickDims<DIM, BX>::MI
       const uint64_t own = __ldg(A.rank_tab + ((static_cast<size_t>(k) << (2 * DIM + 1)) + flags) * 2);
       const unsigned rd = static_cast<unsigned>(own >> (4 * k)) & 15u;
       double h[NC];
-      rt0_hrow_c<DIM>(c, s, ib, f, C, k, h);
+      hrow(k, h);
       double* dp = hbuf + l * CAP + line_entries<DIM>(m, ax, x0 + l_pa[l], x0 + p, cc[1], cc[2]) + rd;
       *dp = *dp + h[k];
       gbuf[l * (X + 1) + p] = gbuf[l * (X + 1) + p] + h[N];
@@ -915,215 +1058,19 @@ __global__ void __launch_bounds__(BrickDims<DIM, BX>::CT, BrickDims<DIM, BX>::MI
     const int pa = l_pa[l], oa = l_oa[l], ob = l_ob[l];
     for (int p = oa + lane; p <= ob; p += 32) A.g[l_row0[l] + (p - pa)] = gbuf[l * (X + 1) + p];
   }
+  return rejected;
 }
 
-// ------------------------------------------------------------------ k >= 1
-
-constexpr int kIB = 8;   // rows of Delta per block
-constexpr int kNT = 256; // threads per CTA
-
-struct CtaLayout {
-  int64_t s, xs, xf, v, dblk, yblk, h, yfull, t, xty, rank, rows, total;
-};
-
-__host__ __device__ inline CtaLayout cta_layout(int n, int nF, int r, int p_max) {
-  CtaLayout L;
-  const int64_t nc = nF + 1;
-  int64_t o = 0;
-  auto take = [&o](int64_t cnt) {
-    const int64_t at = o;
-    o += (cnt + 3) & ~int64_t(3);
-    return at;
-  };
-  L.s = take(r);
-  L.xs = take(static_cast<int64_t>(nF) * r);
-  L.xf = take(r);
-  L.v = take(static_cast<int64_t>(n) * nc);
-  L.dblk = take(static_cast<int64_t>(kIB) * n);
-  L.yblk = take(static_cast<int64_t>(kIB) * nc);
-  L.h = take(static_cast<int64_t>(nF) * nc);
-  if (p_max >= 2) {
-    L.yfull = take(static_cast<int64_t>(n) * nc);
-    L.t = take(static_cast<int64_t>(n) * nc);
-    L.xty = take(static_cast<int64_t>(r) * nc);
-  } else {
-    L.yfull = L.t = L.xty = -1;
-  }
-  L.rank = take(64);       // 6x6 col ranks (ints stored in doubles' space)
-  L.rows = take(128);      // row starts per face dof (int64 in doubles' space)
-  L.total = o;
-  return L;
+template <int DIM, int COL, int BX>
+__global__ void __launch_bounds__(BrickDims<DIM, BX>::CT, BrickDims<DIM, BX>::MINB)
+    k_rt0_brick(HybArgs A, Rt0Const<2 * DIM> c, Rt0Fast<2 * DIM> F, double* stage, int nbx, int nby, int nbz) {
+  rt0_brick_body<DIM, COL, BX>(A, c, F, stage, nbx, nby, nbz);
 }
 
-// y (rows i0..i0+ib) = Delta[i0:i0+ib, :] * Src   (Src n x nc), optionally kept in yfull
-__device__ inline void delta_block(const HybArgs& A, double a, double b, int n, int nc, int i0, int ib, const double* src,
-                                   double* dblk, double* yblk) {
-  const Fixed& fx = A.fx;
-  for (int idx = threadIdx.x; idx < ib * n; idx += blockDim.x) {
-    const int ii = idx / n, l = idx - ii * n;
-    const int64_t o = static_cast<int64_t>(i0 + ii) * n + l;
-    dblk[ii * n + l] = delta_entry(a, b, __ldg(fx.D + o), __ldg(fx.M + o), __ldg(fx.E + o), __ldg(fx.Ma + o));
-  }
-  __syncthreads();
-  for (int idx = threadIdx.x; idx < ib * nc; idx += blockDim.x) {
-    const int ii = idx / nc, c = idx - ii * nc;
-    double acc = 0.0;
-    for (int l = 0; l < n; ++l) acc = fma(dblk[ii * n + l], src[static_cast<int64_t>(l) * nc + c], acc);
-    yblk[ii * nc + c] = acc;
-  }
-  __syncthreads();
-}
+// ------------------------------------------------------------------ k >= 1 recovery
 
-// H[p][q] += sg * sum_ii V[i0+ii][p] * Y[ii][q]
-__device__ inline void accumulate_h(int nF, int nc, int nint, int i0, int ib, const double* V, const double* yblk,
-                                    double* H, double sg) {
-  (void)nint;
-  for (int idx = threadIdx.x; idx < nF * nc; idx += blockDim.x) {
-    const int p = idx / nc, q = idx - p * nc;
-    double acc = 0.0;
-    for (int ii = 0; ii < ib; ++ii) acc = fma(V[static_cast<int64_t>(i0 + ii) * nc + p], yblk[ii * nc + q], acc);
-    H[idx] = fma(sg, acc, H[idx]);
-  }
-  __syncthreads();
-}
+constexpr int kNT = 256;  // threads per CTA
 
-// dst = A0^-1 src = (N0 src + X diag(s) (X^T src)) / beta, src/dst n x nc
-__device__ inline void apply_a0inv(const HybArgs& A, int n, int nc, const double* s, double ib, const double* src,
-                                   double* xty, double* dst) {
-  const Fixed& fx = A.fx;
-  const int r = fx.r;
-  for (int idx = threadIdx.x; idx < r * nc; idx += blockDim.x) {
-    const int j = idx / nc, c = idx - j * nc;
-    double acc = 0.0;
-    for (int l = 0; l < n; ++l) acc = fma(__ldg(fx.X + static_cast<int64_t>(l) * r + j), src[static_cast<int64_t>(l) * nc + c], acc);
-    xty[idx] = acc * s[j];
-  }
-  __syncthreads();
-  for (int idx = threadIdx.x; idx < n * nc; idx += blockDim.x) {
-    const int i = idx / nc, c = idx - i * nc;
-    double acc = 0.0;
-    for (int l = 0; l < n; ++l) acc = fma(__ldg(fx.N0 + static_cast<int64_t>(i) * n + l), src[static_cast<int64_t>(l) * nc + c], acc);
-    for (int j = 0; j < r; ++j) acc = fma(__ldg(fx.X + static_cast<int64_t>(i) * r + j), xty[j * nc + c], acc);
-    dst[idx] = acc * ib;
-  }
-  __syncthreads();
-}
-
-__global__ void __launch_bounds__(kNT) k_hyb_cta(HybArgs A, int parity, double* gws, int64_t ws_stride, int use_smem) {
-  extern __shared__ double smem[];
-  double* ws = use_smem ? smem : gws + blockIdx.x * ws_stride;
-  const DevMesh& m = A.m;
-  const int n = m.n, nint = m.nint, nF = A.nF, nc = nF + 1, r = A.fx.r, dpf = m.dpf, nsl = 2 * m.dim;
-  const CtaLayout L = cta_layout(n, nF, r, A.p_max);
-  double* s = ws + L.s;
-  double* xs = ws + L.xs;
-  double* xf = ws + L.xf;
-  double* V = ws + L.v;
-  double* dblk = ws + L.dblk;
-  double* yblk = ws + L.yblk;
-  double* H = ws + L.h;
-  int* rank = reinterpret_cast<int*>(ws + L.rank);
-  int64_t* rows = reinterpret_cast<int64_t*>(ws + L.rows);
-  const int64_t cnt = parity_count(m);
-
-  for (int64_t tt = blockIdx.x; tt < cnt; tt += gridDim.x) {
-    const int64_t e = parity_cell(m, parity, tt);
-    if (e < 0) continue;
-    const double a = A.alpha[e], b = A.beta[e];
-    const double ib = 1.0 / b;
-    const double* fe = A.f + e * n;
-    // s_j and X^T f
-    for (int j = threadIdx.x; j < r; j += blockDim.x) {
-      const double sj = b / fma(a, __ldg(A.fx.lam + j), b);
-      s[j] = sj;
-      double acc = 0.0;
-      for (int l = 0; l < n; ++l) acc = fma(__ldg(A.fx.X + static_cast<int64_t>(l) * r + j), fe[l], acc);
-      xf[j] = acc * sj;
-    }
-    __syncthreads();
-    for (int idx = threadIdx.x; idx < nF * r; idx += blockDim.x) {
-      const int c = idx / r, j = idx - c * r;
-      xs[idx] = s[j] * __ldg(A.fx.X + static_cast<int64_t>(nint + c) * r + j);
-    }
-    __syncthreads();
-    // V = A0^-1 [E_F | f]
-    for (int idx = threadIdx.x; idx < n * nc; idx += blockDim.x) {
-      const int i = idx / nc, c = idx - i * nc;
-      const double* xi = A.fx.X + static_cast<int64_t>(i) * r;
-      double acc;
-      if (c < nF) {
-        acc = __ldg(A.fx.N0 + static_cast<int64_t>(i) * n + nint + c);
-        for (int j = 0; j < r; ++j) acc = fma(__ldg(xi + j), xs[c * r + j], acc);
-      } else {
-        acc = 0.0;
-        for (int l = 0; l < n; ++l) acc = fma(__ldg(A.fx.N0 + static_cast<int64_t>(i) * n + l), fe[l], acc);
-        for (int j = 0; j < r; ++j) acc = fma(__ldg(xi + j), xf[j], acc);
-      }
-      V[idx] = acc * ib;
-    }
-    __syncthreads();
-    for (int idx = threadIdx.x; idx < nF * nc; idx += blockDim.x) {
-      const int p = idx / nc, q = idx - p * nc;
-      H[idx] = V[static_cast<int64_t>(nint + p) * nc + q];
-    }
-    const int P = neumann_order(A.fx.rho * a * ib, A.p_max, A.status);
-    double* yfull = (P >= 2) ? ws + L.yfull : nullptr;
-    __syncthreads();
-    // first order
-    for (int i0 = 0; i0 < n; i0 += kIB) {
-      const int blk = min(kIB, n - i0);
-      delta_block(A, a, b, n, nc, i0, blk, V, dblk, yblk);
-      if (yfull)
-        for (int idx = threadIdx.x; idx < blk * nc; idx += blockDim.x) yfull[static_cast<int64_t>(i0) * nc + idx] = yblk[idx];
-      accumulate_h(nF, nc, nint, i0, blk, V, yblk, H, -1.0);
-    }
-    // higher orders: T = A0^-1 Y, Y <- Delta T
-    for (int p = 2; p <= P; ++p) {
-      double* T = ws + L.t;
-      apply_a0inv(A, n, nc, s, ib, yfull, ws + L.xty, T);
-      const double sg = (p & 1) ? -1.0 : 1.0;
-      for (int i0 = 0; i0 < n; i0 += kIB) {
-        const int blk = min(kIB, n - i0);
-        delta_block(A, a, b, n, nc, i0, blk, T, dblk, yblk);
-        for (int idx = threadIdx.x; idx < blk * nc; idx += blockDim.x) yfull[static_cast<int64_t>(i0) * nc + idx] = yblk[idx];
-        accumulate_h(nF, nc, nint, i0, blk, V, yblk, H, sg);
-      }
-    }
-    // scatter: col ranks and row starts of the interior face slots
-    int64_t cc[3], own_f[6];
-    bool own_in[6];
-    cell_coords(m, e, cc);
-    for (int q = 0; q < nsl; ++q) own_f[q] = slot_face(m, cc, q, &own_in[q]);
-    for (int idx = threadIdx.x; idx < nsl * nsl; idx += blockDim.x) {
-      const int p = idx / nsl, q = idx - p * nsl;
-      rank[idx] = (own_in[p] && own_in[q]) ? col_rank(m, cc, p, q, own_f, own_in) : -1;
-    }
-    for (int idx = threadIdx.x; idx < nsl * dpf; idx += blockDim.x) {
-      const int p = idx / dpf, sub = idx - p * dpf;
-      rows[idx] = own_in[p] ? A.rowoff[A.mbase[own_f[p]] + sub] : -1;
-    }
-    __syncthreads();
-    for (int idx = threadIdx.x; idx < nF * nc; idx += blockDim.x) {
-      const int i = idx / nc, q = idx - i * nc;
-      const int p = i / dpf;
-      if (!own_in[p]) continue;
-      const double v = H[idx];
-      if (q == nF) {
-        const int64_t row = A.mbase[own_f[p]] + (i - p * dpf);
-        A.g[row] = parity ? A.g[row] + v : v;
-        continue;
-      }
-      const int qs = q / dpf, sj = q - qs * dpf;
-      const int rk = rank[p * nsl + qs];
-      if (rk < 0) continue;
-      const int64_t pos = rows[i] + static_cast<int64_t>(rk) * dpf + sj;
-      A.hval[pos] = (parity == 1 && p == qs) ? A.hval[pos] + v : v;
-    }
-    __syncthreads();
-  }
-}
-
-// ------------------------------------------------------------------ recovery
 
 // x_hat_T = A_T^-1 (f_T - C_T^T lambda) by the same structured solve (one CTA per cell):
 // the Neumann series of A0^-1 Delta in fp64 with the a-priori order; every
@@ -1164,7 +1111,12 @@ __global__ void __launch_bounds__(kNT) k_recover_cta(RecArgs R, double* gws, int
       y[i] = v;
     }
     __syncthreads();
-    const int P = neumann_order(R.fx.rho * a * ib, R.p_max, R.status);
+    bool exact = false;
+    const int P = struct_order_apriori(R.fx.rho * a * ib, R.p_max, exact);
+    if (exact || R.force_exact) {  // rejected: x_hat of this cell from the exact path (kern_exact.cu)
+      if (threadIdx.x == 0) exact_push(R.xlist, R.xcount, static_cast<int>(e));
+      continue;
+    }
     for (int p = 0; p <= P; ++p) {
       // t = A0^-1 y = (N0 y + X diag(s) X^T y) / beta
       if (wide) {  // warp per row, lanes along the row
@@ -1249,21 +1201,31 @@ __global__ void __launch_bounds__(128) k_rt0_recover(RecArgs R, Rt0Const<2 * DIM
   const double s = b / fma(a, c.lam, b);
   int cc[3];
   cell_coords32(R.m, static_cast<uint32_t>(e), cc);
-  double y[N];
+  double y[N], yl[N];
 #pragma unroll
   for (int k = 0; k < N; ++k) {
-    double v = R.f[e * N + k];
+    double v = R.f[e * N + k], vl = 0.0;
     const int a_ = k >> 1, side = k & 1;
     const int ca = a_ == 0 ? cc[0] : (a_ == 1 ? cc[1] : cc[2]);
     const int na = static_cast<int>(a_ == 0 ? R.m.N[0] : (a_ == 1 ? R.m.N[1] : R.m.N[2]));
     if (side ? (ca + 1 < na) : (ca > 0)) {  // unit constraint rows: C_T^T lambda
       const int face = face_id32(R.m, a_, cc[0] + (a_ == 0 ? side : 0), cc[1] + (a_ == 1 ? side : 0),
                                  cc[2] + (a_ == 2 ? side : 0));
-      v -= R.lambda[R.mbase[face]];
+      two_sum(v, -R.lambda[R.mbase[face]], v, vl);  // v = fl(f - lambda), vl its rounding error
     }
     y[k] = v;
+    yl[k] = vl;
   }
-  const int P = neumann_order(c.rho * a * ib, R.p_max, R.status);
+  bool exact = false;
+  const int P = struct_order_apriori(c.rho * a * ib, R.p_max, exact);
+  if (exact || R.force_exact) {  // rejected: the exact solve in this thread
+    if (R.xcount) atomicAdd(R.xcount, 1);
+    double xo[N];
+    rt0_exact_ool<N, 1, false>(R.fx.D, R.fx.M, a, b, rt0_bmask<DIM>(R.m, cc), y, yl, xo, R.status);
+#pragma unroll
+    for (int k = 0; k < N; ++k) R.x_hat[e * N + k] = xo[k];
+    return;
+  }
   double acc[N];
   for (int p = 0; p <= P; ++p) {
     // t = A0^-1 y
@@ -1392,7 +1354,6 @@ void launch_hybridize_rt0_rows(const HybArgs& a, const double* hc, double* stage
   // give each SM a few bricks per colour (e.g. 64 x 64 quads: 16 bricks a colour)
   // (HDR_RT0_BRICK forces the brick kernel at any size: tests)
   const bool cell = getenv("HDR_RT0_CELL") != nullptr || (a.m.ncells < 148 * 128 * 4 && !getenv("HDR_RT0_BRICK"));
-  static const bool side = getenv("HDR_RT0_STAGE") == nullptr;  // default: per-row side slots; HDR_RT0_STAGE=1: row stage
   auto brick = [&](auto dimc, auto bxc, auto& c, auto& F) {
     constexpr int D = decltype(dimc)::value, BXv = decltype(bxc)::value;
     using B = BrickDims<D, BXv>;
@@ -1414,6 +1375,15 @@ void launch_hybridize_rt0_rows(const HybArgs& a, const double* hc, double* stage
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     cudaLaunchKernelEx(&cfg, k_rt0_brick<D, 1, BXv>, a, c, F, stage, nbx, nby, nbz);
+    // the exact path of rejected cells (usually none: the kernel returns at once)
+    cudaLaunchConfig_t xc{};
+    xc.gridDim = dim3(1);
+    xc.blockDim = dim3(256);
+    xc.stream = st;
+    xc.attrs = attr;
+    xc.numAttrs = 1;
+    cudaLaunchKernelEx(&xc, k_rt0_exact<D>, a);
+    count_launch();
   };
   const bool wide = a.m.N[0] >= 48 && !getenv("HDR_RT0_BRICK32");
   if (a.m.dim == 3) {
@@ -1426,14 +1396,10 @@ void launch_hybridize_rt0_rows(const HybArgs& a, const double* hc, double* stage
       const unsigned nb = static_cast<unsigned>((cnt + 4 * 5 - 1) / (4 * 5));
       k_rt0_rows<3, 0><<<nb, 128, 0, st>>>(a, c, stage);
       k_rt0_rows<3, 1><<<nb, 128, 0, st>>>(a, c, stage);
-    } else if (side) {
+    } else {
       const unsigned nb = static_cast<unsigned>((cnt + kCT - 1) / kCT);
       k_rt0_cell<3, 0, true><<<nb, kCT, 0, st>>>(a, c, f3, stage);
       k_rt0_cell<3, 1, true><<<nb, kCT, 0, st>>>(a, c, f3, stage);
-    } else {
-      const unsigned nb = static_cast<unsigned>((cnt + kCT - 1) / kCT);
-      k_rt0_cell<3, 0, false><<<nb, kCT, 0, st>>>(a, c, f3, stage);
-      k_rt0_cell<3, 1, false><<<nb, kCT, 0, st>>>(a, c, f3, stage);
     }
   } else {
     Rt0Const<4> c;
@@ -1445,48 +1411,13 @@ void launch_hybridize_rt0_rows(const HybArgs& a, const double* hc, double* stage
       const unsigned nb = static_cast<unsigned>((cnt + 4 * 8 - 1) / (4 * 8));
       k_rt0_rows<2, 0><<<nb, 128, 0, st>>>(a, c, stage);
       k_rt0_rows<2, 1><<<nb, 128, 0, st>>>(a, c, stage);
-    } else if (side) {
+    } else {
       const unsigned nb = static_cast<unsigned>((cnt + kCT - 1) / kCT);
       k_rt0_cell<2, 0, true><<<nb, kCT, 0, st>>>(a, c, f2, stage);
       k_rt0_cell<2, 1, true><<<nb, kCT, 0, st>>>(a, c, f2, stage);
-    } else {
-      const unsigned nb = static_cast<unsigned>((cnt + kCT - 1) / kCT);
-      k_rt0_cell<2, 0, false><<<nb, kCT, 0, st>>>(a, c, f2, stage);
-      k_rt0_cell<2, 1, false><<<nb, kCT, 0, st>>>(a, c, f2, stage);
     }
   }
   count_launch(2);
-}
-
-int64_t hybridize_cta_ws_doubles(const DevMesh& m, int nF, int r, int p_max, bool* use_smem) {
-  const CtaLayout L = cta_layout(m.n, nF, r, p_max);
-  *use_smem = L.total * 8 <= 200 * 1024;
-  return L.total;
-}
-
-static int sm_count() {
-  static int n = 0;
-  if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
-  }
-  return n;
-}
-
-void launch_hybridize_cta(const HybArgs& a, int parity, double* gws, int64_t ws_doubles, cudaStream_t st) {
-  bool use_smem = false;
-  const int64_t need = hybridize_cta_ws_doubles(a.m, a.nF, a.fx.r, a.p_max, &use_smem);
-  const size_t smem = use_smem ? static_cast<size_t>(need) * 8 : 0;
-  if (use_smem) cudaFuncSetAttribute(k_hyb_cta, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-  const int64_t cnt = parity_count(a.m);
-  int64_t grid = use_smem ? cnt : std::min<int64_t>(cnt, ws_doubles / need);
-  if (grid < 1) grid = 1;
-  if (grid > 1 << 30) grid = 1 << 30;
-  (void)sm_count;
-  k_hyb_cta<<<static_cast<unsigned>(grid), kNT, smem, st>>>(a, parity, gws, need, use_smem ? 1 : 0);
-  count_launch();
 }
 
 void launch_recover_rt0(const RecArgs& a, const double* hc, cudaStream_t st) {

@@ -8,8 +8,9 @@
 //          C = V_F^T Y  (first-order Neumann term; orders >= 2 the same way)
 // The correction is <= ~2e-7 |H| on every BASELINE config, so
 // fp32 arithmetic on it keeps the result within 1e-13 of the double-double
-// truth; the bound is re-checked per cell a posteriori (|C| / |H0|) and a
-// second order is added where the estimate asks for it.
+// truth; the bound is re-checked per cell a posteriori (|C| / |H0|): a second
+// order is added where the estimate asks for it, and a cell whose estimated
+// error stays above 1e-12 of |H_T| goes to the exact path (kern_exact.cu).
 //
 // Lane c owns column c: Y_:c = Delta32 V_:c and C_:c = V_F^T Y_:c need only the
 // warp-shared Delta32 / V32 (broadcast reads) and the lane's own column.
@@ -368,14 +369,15 @@ __device__ __forceinline__ void warp_cell(const HybArgs& A, int e, int parity, i
     gsync<GT>();
   }
   const double ratio = hmax > 0.f ? static_cast<double>(cmax) / hmax : 0.0;
-  int P = 1;
-  {
-    double t = ratio * ratio * 10.0;
-    while (t > 1e-12 && P < A.p_max) {
-      ++P;
-      t *= ratio;
-    }
-    if (!(ratio < 0.25) && lane == 0) atomicOr(A.status, 1);
+  // order control and acceptance (hdr_device.cuh struct_order); a rejected cell
+  // contributes zeros here and is solved on the exact path (kern_exact.cu)
+  bool exact = false;
+  int P = struct_order(ratio, A.p_max, A.eps32, exact);
+  exact = exact || A.force_exact;
+  if (exact) P = 1;
+  if (lane == 0) {
+    if (A.qlog) A.qlog[e] = static_cast<float>(ratio);
+    if (exact) exact_push(A.xlist, A.xcount, e);
   }
   // higher orders (rare): T = A0^-1 Y, Y <- Delta32 T, C += (-1)^(p+1) V_F^T Y (C is subtracted)
   if (P >= 2) {
@@ -464,6 +466,7 @@ __device__ __forceinline__ void warp_cell(const HybArgs& A, int e, int parity, i
         const int c = qs * DPF + j;
         double2 v = make_double2(sm.vf[p * NC + c] - static_cast<double>(corr[p * NCP + c]),
                                  sm.vf[p * NC + c + 1] - static_cast<double>(corr[p * NCP + c + 1]));
+        if (exact) v = make_double2(0.0, 0.0);
         if (add) {
           const double2 o = hp[j / 2];
           v.x += o.x;
@@ -475,7 +478,7 @@ __device__ __forceinline__ void warp_cell(const HybArgs& A, int e, int parity, i
     for (int p = lane; p < NF; p += GT) {
       const int ps = p / DPF, sub = p - ps * DPF;
       if (sm.rstart[ps] < 0) continue;
-      const double v = sm.vf[p * NC + NF] - static_cast<double>(corr[p * NCP + NF]);
+      const double v = exact ? 0.0 : sm.vf[p * NC + NF] - static_cast<double>(corr[p * NCP + NF]);
       double* gp = A.g + sm.grow[ps] + sub;
       *gp = parity ? *gp + v : v;
     }
@@ -485,7 +488,7 @@ __device__ __forceinline__ void warp_cell(const HybArgs& A, int e, int parity, i
       const int ps = p / DPF, sub = p - ps * DPF;
       const int64_t rs = sm.rstart[ps];
       if (rs < 0) continue;
-      const double v = sm.vf[p * NC + c] - static_cast<double>(corr[p * NCP + c]);
+      const double v = exact ? 0.0 : sm.vf[p * NC + c] - static_cast<double>(corr[p * NCP + c]);
       if (c == NF) {
         double* gp = A.g + sm.grow[ps] + sub;
         *gp = parity ? *gp + v : v;

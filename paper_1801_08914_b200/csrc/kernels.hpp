@@ -47,9 +47,18 @@ struct HybArgs {
   const int64_t* rowoff;
   double* hval;  // H values (pattern order)
   double* g;     // reduced rhs (m)
-  int* status;   // device flag: bit 0 = Neumann ratio out of range
+  int* status;   // device flag (bit 2: singular block on the exact path)
   const uint64_t* rank_tab;  // k = 0 row-rank table (rank_table_rt0)
   const longlong2* frs;      // k = 0: per face {rowoff[mbase[face]], mbase[face]} (launch_face_rows)
+  // fail-safe (hdr_device.cuh struct_order): cells the structured solve does not
+  // accept contribute nothing and are listed for the exact path (kern_exact.cu);
+  // k = 0 kernels solve them in place instead (double-double, per thread)
+  int* xlist;    // exact-path cells (capacity ncells)
+  int* xcount;   // [0]: their number (reset before each call); [2]: k = 0 brick kernels' list length
+  double eps32;  // relative accuracy of the fp32 correction arithmetic of this kernel
+  double eps_tc; // same for the tcgen05 3xTF32 form (k_hyb_big)
+  int force_exact;  // testing: send every cell to the exact path
+  float* qlog;      // optional per-cell q (diagnostics)
 };
 void launch_face_rows(int64_t nfaces, const int* mbase, const int64_t* rowoff, longlong2* frs, cudaStream_t st);
 
@@ -72,9 +81,6 @@ void launch_hybridize_big(const HybArgs& a, int k, int parity, double* gws, cons
 // C (M x Ncol) = A (M x Kd) B (Kd x Ncol), column-major fp64
 void launch_gemm_f64_nn(int M, int Ncol, int Kd, const double* A, int lda, const double* B, int ldb, double* C,
                         int ldc, cudaStream_t st);
-// General path (k >= 1): one CTA per cell, shared-memory or global workspace.
-void launch_hybridize_cta(const HybArgs& a, int parity, double* gws, int64_t ws_doubles, cudaStream_t st);
-int64_t hybridize_cta_ws_doubles(const DevMesh& m, int nF, int r, int p_max, bool* use_smem);
 
 // ---- hybrid recovery: x_hat = A^-1 (f - C^T lambda) per cell (kern_hybridize.cu)
 struct RecArgs {
@@ -86,11 +92,36 @@ struct RecArgs {
   double* x_hat;  // broken
   double* x;      // global (ndofs): face dofs averaged, bubbles copied
   int* status;
+  int* xlist;     // exact-path cells (see HybArgs)
+  int* xcount;
+  int force_exact;
 };
 void launch_recover_hybrid(const RecArgs& a, double* gws, int64_t ws_doubles, cudaStream_t st);
 // k = 0: one thread per cell (host_consts as launch_hybridize_rt0_rows)
 void launch_recover_rt0(const RecArgs& a, const double* host_consts, cudaStream_t st);
 void launch_average_faces(const DevMesh& m, const double* x_hat, double* x, cudaStream_t st);
+
+// ---- exact path (kern_exact.cu): double-double LU of A_T = fl(fl(alpha D) + fl(beta M))
+// for the cells the structured solve did not accept (xlist / xcount), one CTA per cell
+enum { EXACT_HYB = 0, EXACT_REC = 1 };
+struct ExactArgs {
+  DevMesh m;
+  int n, nF, mode;
+  const double *D, *M;  // reference element (n x n row-major)
+  const double *alpha, *beta, *f, *lambda;
+  const int* mbase;
+  const int64_t* rowoff;
+  double *hval, *g, *x_hat;
+  const int* xlist;
+  const int* xcount;
+  int* status;  // bit 2: singular block (the reference's rule)
+  unsigned long long* bad;  // smallest singular cell
+};
+int exact_grid(int n);                   // CTAs of one exact launch
+int64_t exact_ws_doubles(int n, int nF);  // global scratch of one launch
+// HYB: adds the listed cells of colour `parity` to H, g (their fast-path contributions are zero)
+// REC: writes x_hat of the listed cells (before k_average)
+void launch_exact(const ExactArgs& a, int parity, double* ws, cudaStream_t st);
 
 // ---- static condensation / recover_condensed (kern_condense.cu)
 struct CondArgs {

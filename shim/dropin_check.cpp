@@ -8,7 +8,31 @@
 #include <string>
 
 #include "hdivred/reduction.hpp"
+#include "hdivred/solvers.hpp"
 #include "hdivred_b200_shim.hpp"
+
+// The reference's solve_reduction sequences (src/driver.cpp:241-254), written
+// inside namespace hdivred exactly as there: the caller changes only the
+// hybridize / static_condense line; the unqualified recover_* calls then reach
+// the shim's overloads by argument-dependent lookup.
+namespace hdivred {
+template <class HybFn>
+std::vector<double> solve_hybridization(const ReductionInputs& inputs, HybFn hyb_fn, index_t* its) {
+  const auto [hyb, g] = hyb_fn(inputs);
+  const std::unique_ptr<Preconditioner> pc = jacobi_setup(hyb.h_mat);
+  auto [lambda, rep] = pcg(hyb.h_mat, pc.get(), g, 1e-12, 5000);
+  *its = rep.iterations;
+  return recover_hybrid(hyb, lambda, inputs.f_hat).second;
+}
+template <class CondFn>
+std::vector<double> solve_condensation(const ReductionInputs& inputs, CondFn cond_fn, index_t* its) {
+  const auto [cond, f_s] = cond_fn(inputs);
+  const std::unique_ptr<Preconditioner> pc = jacobi_setup(cond.s_mat);
+  auto [x_b, rep] = pcg(cond.s_mat, pc.get(), f_s, 1e-12, 5000);
+  *its = rep.iterations;
+  return recover_condensed(cond, x_b, inputs.f_hat);
+}
+}  // namespace hdivred
 
 using namespace hdivred;
 
@@ -56,12 +80,12 @@ int main(int argc, char** argv) {
     return d / (m > 0 ? m : 1.0);
   };
   auto [ahyb, g_alg] = hdivred_b200::hybridize(in);
-  const bool apat = ref.h_mat.row_offsets == ahyb.op.h_mat.row_offsets &&
-                    ref.h_mat.col_indices == ahyb.op.h_mat.col_indices;
+  const bool apat = ref.h_mat.row_offsets == ahyb.h_mat.row_offsets &&
+                    ref.h_mat.col_indices == ahyb.h_mat.col_indices;
   bool asym = true;
   {
-    const CsrMatrix t = transpose(ahyb.op.h_mat);
-    asym = t.values == ahyb.op.h_mat.values && t.col_indices == ahyb.op.h_mat.col_indices;
+    const CsrMatrix t = transpose(ahyb.h_mat);
+    asym = t.values == ahyb.h_mat.values && t.col_indices == ahyb.h_mat.col_indices;
   }
   std::vector<double> lam(g_ref.size());
   for (auto& v : lam) {
@@ -71,9 +95,8 @@ int main(int argc, char** argv) {
   auto [xh_ref, x_ref] = recover_hybrid(ref, lam, in.f_hat);
   auto [xh_alg, x_alg] = hdivred_b200::recover_hybrid(ahyb, lam, in.f_hat);
   auto [acond, fs_alg] = hdivred_b200::static_condense(in);
-  const bool acpat = cref.s_mat.row_offsets == acond.op.s_mat.row_offsets &&
-                     cref.s_mat.col_indices == acond.op.s_mat.col_indices &&
-                     cref.master_globals == acond.op.master_globals;
+  const bool acpat = cref.s_mat.row_offsets == acond.s_mat.row_offsets &&
+                     cref.s_mat.col_indices == acond.s_mat.col_indices && cref.master_globals == acond.master_globals;
   std::vector<double> xb(fs_ref.size());
   for (auto& v : xb) {
     s ^= s << 13; s ^= s >> 7; s ^= s << 17;
@@ -81,17 +104,38 @@ int main(int argc, char** argv) {
   }
   const std::vector<double> xc_ref = recover_condensed(cref, xb, in.f_hat);
   const std::vector<double> xc_alg = hdivred_b200::recover_condensed(acond, xb, in.f_hat);
+  // FE operators: recovery on the retained device state (no re-hybridize)
+  auto [xh_fe, x_fe] = hdivred_b200::recover_hybrid(gpu, lam, in.f_hat);
+  const std::vector<double> xc_fe = hdivred_b200::recover_condensed(cgpu, xb, in.f_hat);
+  // the solve_reduction sequences: reference, shim on ReductionInputs, shim FE path
+  index_t it_ref = 0, it_alg = 0, it_fe = 0, itc_ref = 0, itc_alg = 0, itc_fe = 0;
+  const std::vector<double> xs_ref = solve_hybridization(in, [](const ReductionInputs& r) { return hybridize(r); }, &it_ref);
+  const std::vector<double> xs_alg = solve_hybridization(
+      in, [](const ReductionInputs& r) { return hdivred_b200::hybridize(r); }, &it_alg);
+  const std::vector<double> xs_fe = solve_hybridization(
+      in, [&](const ReductionInputs& r) { return hdivred_b200::hybridize(sp, co, r.f_hat); }, &it_fe);
+  const std::vector<double> xsc_ref =
+      solve_condensation(in, [](const ReductionInputs& r) { return static_condense(r); }, &itc_ref);
+  const std::vector<double> xsc_alg = solve_condensation(
+      in, [](const ReductionInputs& r) { return hdivred_b200::static_condense(r); }, &itc_alg);
+  const std::vector<double> xsc_fe = solve_condensation(
+      in, [&](const ReductionInputs& r) { return hdivred_b200::static_condense(sp, co, r.f_hat); }, &itc_fe);
   const std::vector<double> y_ref = spmv(ref.h_mat, g_ref);
   const std::vector<double> y_gpu = hdivred_b200::spmv(ref.h_mat, g_ref);
   std::printf("{\"n\": %d, \"k\": %d, \"h_pattern_identical\": %s, \"h_rel\": %.3e, \"g_rel\": %.3e, "
               "\"s_pattern_identical\": %s, \"s_rel\": %.3e, \"spmv_identical\": %s, "
               "\"alg_h_pattern_identical\": %s, \"alg_h_symmetric\": %s, \"alg_h_rel\": %.3e, \"alg_g_rel\": %.3e, "
               "\"alg_x_hat_rel\": %.3e, \"alg_x_rel\": %.3e, \"alg_s_pattern_identical\": %s, \"alg_s_rel\": %.3e, "
-              "\"alg_f_s_rel\": %.3e, \"alg_x_cond_rel\": %.3e}\n",
+              "\"alg_f_s_rel\": %.3e, \"alg_x_cond_rel\": %.3e, \"fe_x_hat_rel\": %.3e, \"fe_x_rel\": %.3e, "
+              "\"fe_x_cond_rel\": %.3e, \"solve_hyb_alg_rel\": %.3e, \"solve_hyb_fe_rel\": %.3e, "
+              "\"solve_cond_alg_rel\": %.3e, \"solve_cond_fe_rel\": %.3e, \"pcg_iterations\": [%lld, %lld, %lld, %lld, %lld, %lld]}\n",
               n, k, pattern ? "true" : "false", dh / mh, dg / (mg > 0 ? mg : 1), spat ? "true" : "false", ds / ms,
               y_ref == y_gpu ? "true" : "false", apat ? "true" : "false", asym ? "true" : "false",
-              rel(ref.h_mat.values, ahyb.op.h_mat.values), rel(g_ref, g_alg), rel(xh_ref, xh_alg), rel(x_ref, x_alg),
-              acpat ? "true" : "false", rel(cref.s_mat.values, acond.op.s_mat.values), rel(fs_ref, fs_alg),
-              rel(xc_ref, xc_alg));
+              rel(ref.h_mat.values, ahyb.h_mat.values), rel(g_ref, g_alg), rel(xh_ref, xh_alg), rel(x_ref, x_alg),
+              acpat ? "true" : "false", rel(cref.s_mat.values, acond.s_mat.values), rel(fs_ref, fs_alg),
+              rel(xc_ref, xc_alg), rel(xh_ref, xh_fe), rel(x_ref, x_fe), rel(xc_ref, xc_fe), rel(xs_ref, xs_alg),
+              rel(xs_ref, xs_fe), rel(xsc_ref, xsc_alg), rel(xsc_ref, xsc_fe), static_cast<long long>(it_ref),
+              static_cast<long long>(it_alg), static_cast<long long>(it_fe), static_cast<long long>(itc_ref),
+              static_cast<long long>(itc_alg), static_cast<long long>(itc_fe));
   return (pattern && spat && y_ref == y_gpu && apat && asym && acpat) ? 0 : 1;
 }

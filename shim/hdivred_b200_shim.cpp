@@ -51,23 +51,44 @@ std::vector<hdivred::index_t> block_offsets(const hdivred::RtSpace& sp) {
   return off;
 }
 
-}  // namespace
-
-std::pair<hdivred::HybridizedOperator, std::vector<double>> hybridize(const hdivred::RtSpace& space,
-                                                                      const hdivred::CellCoefficients& coeffs,
-                                                                      const std::vector<double>& f_hat,
-                                                                      bool symmetric) {
+void check_fe_sizes(const hdivred::RtSpace& space, const hdivred::CellCoefficients& coeffs,
+                    const std::vector<double>& f_hat, const char* who) {
   if (static_cast<hdivred::index_t>(f_hat.size()) != space.broken_ndofs ||
       static_cast<hdivred::index_t>(coeffs.alpha.size()) != space.mesh.ncells() ||
       static_cast<hdivred::index_t>(coeffs.beta.size()) != space.mesh.ncells())
-    throw hdivred::DimensionMismatch("hybridize: inconsistent input dimensions");
+    throw hdivred::DimensionMismatch(std::string(who) + ": inconsistent input dimensions");
+}
+
+std::shared_ptr<void> own_space(SpacePtr s) {
+  return std::shared_ptr<void>(s.release(), [](void* p) { hdr_space_destroy(static_cast<hdr_space_t>(p)); });
+}
+
+// the FE P (build_P, src/reduction.cpp:136-150): one signed entry per broken dof
+hdivred::CsrMatrix fe_p_mat(hdr_space_t s, const hdivred::RtSpace& space, std::vector<int64_t>& gl,
+                            std::vector<double>& sg) {
+  gl.resize(static_cast<size_t>(space.broken_ndofs));
+  sg.resize(static_cast<size_t>(space.broken_ndofs));
+  check(hdr_space_dof_map(s, gl.data(), sg.data()));
+  hdivred::CsrMatrix p(space.broken_ndofs, space.ndofs);
+  p.col_indices.assign(gl.begin(), gl.end());
+  p.values.assign(sg.begin(), sg.end());
+  for (hdivred::index_t r = 0; r <= space.broken_ndofs; ++r) p.row_offsets[static_cast<size_t>(r)] = r;
+  return p;
+}
+
+}  // namespace
+
+std::pair<FeHybridized, std::vector<double>> hybridize(const hdivred::RtSpace& space,
+                                                       const hdivred::CellCoefficients& coeffs,
+                                                       const std::vector<double>& f_hat, bool symmetric) {
+  check_fe_sizes(space, coeffs, f_hat, "hybridize");
   SpacePtr s = make_space(space);
   const auto in = info(s.get());
   hdr_hybrid_t op = nullptr;
   check(hdr_hybridize_fe(s.get(), coeffs.alpha.data(), coeffs.beta.data(), f_hat.data(), 0, &op));
-  std::unique_ptr<hdr_hybrid_s, void (*)(hdr_hybrid_s*)> guard(op, hdr_hybrid_destroy);
+  FeHybridized out;
+  out.device = std::shared_ptr<void>(op, [](void* p) { hdr_hybrid_destroy(static_cast<hdr_hybrid_t>(p)); });
   if (symmetric) check(hdr_hybrid_symmetrize(op));
-  hdivred::HybridizedOperator out;
   const int64_t m = in[HDR_INFO_M], nnz = in[HDR_INFO_NNZ_H];
   out.h_mat = hdivred::CsrMatrix(m, m);
   out.h_mat.col_indices.resize(static_cast<size_t>(nnz));
@@ -76,30 +97,45 @@ std::pair<hdivred::HybridizedOperator, std::vector<double>> hybridize(const hdiv
   check(hdr_space_pattern(s.get(), 0, out.h_mat.row_offsets.data(), out.h_mat.col_indices.data()));
   check(hdr_hybrid_values(op, out.h_mat.values.data(), g.data(), 0));
   out.block_offsets = block_offsets(space);
-  // diag(P^T P): 1 for bubbles and boundary faces, 2 for interior faces
+  // p_mat and recovery_scale = 1 / diag(P^T P) (reduction.cpp:339-352): 1 for
+  // bubbles and boundary faces, 1/2 for interior faces
+  std::vector<int64_t> gl;
+  std::vector<double> sg;
+  out.p_mat = fe_p_mat(s.get(), space, gl, sg);
   const int64_t nd = space.ndofs;
-  out.recovery_scale.assign(static_cast<size_t>(nd), 1.0);
-  std::vector<int64_t> gl(static_cast<size_t>(space.broken_ndofs));
-  std::vector<double> sg(static_cast<size_t>(space.broken_ndofs));
-  check(hdr_space_dof_map(s.get(), gl.data(), sg.data()));
   std::vector<double> cnt(static_cast<size_t>(nd), 0.0);
   for (size_t r = 0; r < gl.size(); ++r) cnt[static_cast<size_t>(gl[r])] += sg[r] * sg[r];
+  out.recovery_scale.resize(static_cast<size_t>(nd));
   for (int64_t i = 0; i < nd; ++i) out.recovery_scale[static_cast<size_t>(i)] = 1.0 / cnt[static_cast<size_t>(i)];
   out.diagonal_gram = true;
+  out.space = own_space(std::move(s));  // released last: the operator borrows the space
   return {std::move(out), std::move(g)};
 }
 
-std::pair<hdivred::CondensedOperator, std::vector<double>> static_condense(const hdivred::RtSpace& space,
-                                                                          const hdivred::CellCoefficients& coeffs,
-                                                                          const std::vector<double>& f_hat) {
-  if (static_cast<hdivred::index_t>(f_hat.size()) != space.broken_ndofs)
-    throw hdivred::DimensionMismatch("static_condense: inconsistent input dimensions");
+std::pair<std::vector<double>, std::vector<double>> recover_hybrid(const FeHybridized& op,
+                                                                   const std::vector<double>& lambda,
+                                                                   const std::vector<double>& f_hat) {
+  if (!op.device) throw std::invalid_argument("recover_hybrid: operator without device state");
+  if (static_cast<hdivred::index_t>(lambda.size()) != op.h_mat.nrows)
+    throw hdivred::DimensionMismatch("recover_hybrid: lambda length != multiplier count");
+  if (static_cast<hdivred::index_t>(f_hat.size()) != op.p_mat.nrows)
+    throw hdivred::DimensionMismatch("recover_hybrid: f_hat length != broken dofs");
+  std::vector<double> x_hat(static_cast<size_t>(op.p_mat.nrows)), x(static_cast<size_t>(op.p_mat.ncols));
+  check(hdr_recover_hybrid(static_cast<hdr_hybrid_t>(op.device.get()), lambda.data(), f_hat.data(), 0, x_hat.data(),
+                           x.data()));
+  return {std::move(x_hat), std::move(x)};
+}
+
+std::pair<FeCondensed, std::vector<double>> static_condense(const hdivred::RtSpace& space,
+                                                            const hdivred::CellCoefficients& coeffs,
+                                                            const std::vector<double>& f_hat) {
+  check_fe_sizes(space, coeffs, f_hat, "static_condense");
   SpacePtr s = make_space(space);
   const auto in = info(s.get());
   hdr_condensed_t op = nullptr;
   check(hdr_static_condense_fe(s.get(), coeffs.alpha.data(), coeffs.beta.data(), f_hat.data(), 0, &op));
-  std::unique_ptr<hdr_condensed_s, void (*)(hdr_condensed_s*)> guard(op, hdr_condensed_destroy);
-  hdivred::CondensedOperator out;
+  FeCondensed out;
+  out.device = std::shared_ptr<void>(op, [](void* p) { hdr_condensed_destroy(static_cast<hdr_condensed_t>(p)); });
   const int64_t ns = in[HDR_INFO_NS], nnz = in[HDR_INFO_NNZ_S];
   out.s_mat = hdivred::CsrMatrix(ns, ns);
   out.s_mat.col_indices.resize(static_cast<size_t>(nnz));
@@ -111,22 +147,20 @@ std::pair<hdivred::CondensedOperator, std::vector<double>> static_condense(const
   check(hdr_space_master_globals(s.get(), out.master_globals.data()));
   out.block_offsets = block_offsets(space);
   out.n_global = space.ndofs;
+  out.space = own_space(std::move(s));
   return {std::move(out), std::move(f_s)};
 }
 
-std::pair<std::vector<double>, std::vector<double>> recover_hybrid(const hdivred::RtSpace& space,
-                                                                   const hdivred::CellCoefficients& coeffs,
-                                                                   const std::vector<double>& lambda,
-                                                                   const std::vector<double>& f_hat) {
-  SpacePtr s = make_space(space);
-  hdr_hybrid_t op = nullptr;
-  check(hdr_hybridize_fe(s.get(), coeffs.alpha.data(), coeffs.beta.data(), f_hat.data(), 0, &op));
-  std::unique_ptr<hdr_hybrid_s, void (*)(hdr_hybrid_s*)> guard(op, hdr_hybrid_destroy);
-  std::vector<double> x_hat(static_cast<size_t>(space.broken_ndofs)), x(static_cast<size_t>(space.ndofs));
-  if (static_cast<hdivred::index_t>(lambda.size()) != info(s.get())[HDR_INFO_M])
-    throw hdivred::DimensionMismatch("recover_hybrid: lambda length");
-  check(hdr_recover_hybrid(op, lambda.data(), f_hat.data(), 0, x_hat.data(), x.data()));
-  return {std::move(x_hat), std::move(x)};
+std::vector<double> recover_condensed(const FeCondensed& op, const std::vector<double>& x_b,
+                                      const std::vector<double>& f_hat) {
+  if (!op.device) throw std::invalid_argument("recover_condensed: operator without device state");
+  if (static_cast<hdivred::index_t>(x_b.size()) != op.s_mat.nrows)
+    throw hdivred::DimensionMismatch("recover_condensed: x_b length != master count");
+  if (static_cast<hdivred::index_t>(f_hat.size()) != op.block_offsets.back())
+    throw hdivred::DimensionMismatch("recover_condensed: f_hat length != broken dofs");
+  std::vector<double> x(static_cast<size_t>(op.n_global));
+  check(hdr_recover_condensed(static_cast<hdr_condensed_t>(op.device.get()), x_b.data(), f_hat.data(), 0, x.data()));
+  return x;
 }
 
 namespace {
@@ -212,13 +246,13 @@ std::pair<AlgHybridized, std::vector<double>> hybridize(const hdivred::Reduction
   out.device = own(h);
   if (symmetric) check(hdr_alg_symmetrize(h));
   std::vector<double> g;
-  out.op.h_mat = alg_matrix(h, g);
-  out.op.p_mat = inputs.p_mat;
-  out.op.block_offsets = offsets_of(inputs);
+  out.h_mat = alg_matrix(h, g);
+  out.p_mat = inputs.p_mat;
+  out.block_offsets = offsets_of(inputs);
   const auto o = alg_info(h);
-  out.op.diagonal_gram = o[HDR_ALG_DIAGONAL_GRAM] != 0;
-  out.op.recovery_scale.resize(static_cast<size_t>(o[HDR_ALG_N_GLOBAL]));
-  check(hdr_alg_recovery_scale(h, out.op.recovery_scale.data()));
+  out.diagonal_gram = o[HDR_ALG_DIAGONAL_GRAM] != 0;
+  out.recovery_scale.resize(static_cast<size_t>(o[HDR_ALG_N_GLOBAL]));
+  check(hdr_alg_recovery_scale(h, out.recovery_scale.data()));
   return {std::move(out), std::move(g)};
 }
 
@@ -242,18 +276,18 @@ std::pair<AlgCondensed, std::vector<double>> static_condense(const hdivred::Redu
   out.device = own(h);
   if (symmetric) check(hdr_alg_symmetrize(h));
   std::vector<double> f_s;
-  out.op.s_mat = alg_matrix(h, f_s);
-  out.op.master_globals.resize(static_cast<size_t>(out.op.s_mat.nrows));
-  check(hdr_alg_master_globals(h, out.op.master_globals.data()));
-  out.op.block_offsets = offsets_of(inputs);
-  out.op.n_global = inputs.p_mat.ncols;
+  out.s_mat = alg_matrix(h, f_s);
+  out.master_globals.resize(static_cast<size_t>(out.s_mat.nrows));
+  check(hdr_alg_master_globals(h, out.master_globals.data()));
+  out.block_offsets = offsets_of(inputs);
+  out.n_global = inputs.p_mat.ncols;
   return {std::move(out), std::move(f_s)};
 }
 
 std::vector<double> recover_condensed(const AlgCondensed& op, const std::vector<double>& x_b,
                                       const std::vector<double>& f_hat) {
   hdr_alg_t h = static_cast<hdr_alg_t>(op.device.get());
-  std::vector<double> x(static_cast<size_t>(op.op.n_global));
+  std::vector<double> x(static_cast<size_t>(op.n_global));
   check(hdr_alg_recover_condensed(h, x_b.data(), static_cast<int64_t>(x_b.size()), f_hat.data(),
                                   static_cast<int64_t>(f_hat.size()), x.data()));
   return x;

@@ -21,43 +21,60 @@
 
 namespace hdivred_b200 {
 
-// hybridize (src/reduction.cpp:262-354) of the FE inputs.  Fills h_mat,
-// block_offsets and recovery_scale/diagonal_gram like the reference; the
-// per-element factorizations stay on the device (HybridizedOperator::elements
-// is private to reduction.cpp and left empty).
-// symmetric = true (default) applies the reference's symmetrize to H (its
-// production output is exactly symmetric and its pcg requires that); false
-// returns the element-exact values the parity contract is stated on.
-std::pair<hdivred::HybridizedOperator, std::vector<double>> hybridize(const hdivred::RtSpace& space,
-                                                                      const hdivred::CellCoefficients& coeffs,
-                                                                      const std::vector<double>& f_hat,
-                                                                      bool symmetric = true);
+// ---- operators: the reference's own types plus the device state
+//
+// Each derives from the reference's operator, so its public fields (h_mat,
+// p_mat, block_offsets, recovery_scale, diagonal_gram / s_mat, master_globals,
+// n_global) are read exactly as before, and carries a shared_ptr to the device
+// handle that holds the per-element state (the reference keeps it in the private
+// `elements` vector, reduction.hpp:49-68 / 78-95, which stays empty here).
+// recover_hybrid / recover_condensed below take these types; an unqualified call
+// `recover_hybrid(op, lambda, f_hat)` inside namespace hdivred (src/driver.cpp:244)
+// finds them by argument-dependent lookup and prefers them over the reference's
+// overload (exact match of the derived type), so the caller changes only the
+// hybridize / static_condense line.
+struct FeHybridized : hdivred::HybridizedOperator {
+  std::shared_ptr<void> space, device;  // hdr_space_t, hdr_hybrid_t
+};
+struct FeCondensed : hdivred::CondensedOperator {
+  std::shared_ptr<void> space, device;  // hdr_space_t, hdr_condensed_t
+};
+struct AlgHybridized : hdivred::HybridizedOperator {
+  std::shared_ptr<void> device;  // hdr_alg_t
+};
+struct AlgCondensed : hdivred::CondensedOperator {
+  std::shared_ptr<void> device;  // hdr_alg_t
+};
 
-// static_condense (src/reduction.cpp:448-557) of the FE inputs: s_mat,
-// master_globals, n_global, block_offsets and f_S.
-std::pair<hdivred::CondensedOperator, std::vector<double>> static_condense(const hdivred::RtSpace& space,
-                                                                          const hdivred::CellCoefficients& coeffs,
-                                                                          const std::vector<double>& f_hat);
+// ---- FE fast path (the structured kernels): the space + coefficients + broken
+// load that build_reduction_inputs (src/reduction.cpp:200-222) would assemble;
+// the element matrices are formed on the device, bit-identically.
 
-// recover_hybrid (src/reduction.cpp:356-446): (x_hat, x)
-std::pair<std::vector<double>, std::vector<double>> recover_hybrid(const hdivred::RtSpace& space,
-                                                                   const hdivred::CellCoefficients& coeffs,
+// hybridize (src/reduction.cpp:262-354).  symmetric = true (default) applies the
+// reference's symmetrize to H (its production output is exactly symmetric and its
+// pcg requires that); false returns the element-exact values the parity contract
+// is stated on.
+std::pair<FeHybridized, std::vector<double>> hybridize(const hdivred::RtSpace& space,
+                                                       const hdivred::CellCoefficients& coeffs,
+                                                       const std::vector<double>& f_hat, bool symmetric = true);
+// recover_hybrid (src/reduction.cpp:356-446) on the retained device operator: (x_hat, x)
+std::pair<std::vector<double>, std::vector<double>> recover_hybrid(const FeHybridized& op,
                                                                    const std::vector<double>& lambda,
                                                                    const std::vector<double>& f_hat);
+// static_condense (src/reduction.cpp:448-557): s_mat, master_globals, n_global, block_offsets, f_S
+std::pair<FeCondensed, std::vector<double>> static_condense(const hdivred::RtSpace& space,
+                                                            const hdivred::CellCoefficients& coeffs,
+                                                            const std::vector<double>& f_hat);
+// recover_condensed (src/reduction.cpp:559-587) on the retained device operator
+std::vector<double> recover_condensed(const FeCondensed& op, const std::vector<double>& x_b,
+                                      const std::vector<double>& f_hat);
 
-// ---- algebraic drop-ins on the reference's own ReductionInputs (reduction.hpp:16-33)
-//
-// The operator handles carry the reference's public fields (h_mat, p_mat,
-// block_offsets, recovery_scale, diagonal_gram / s_mat, master_globals,
-// n_global); the per-element state lives on the device behind `device`.
-struct AlgHybridized {
-  hdivred::HybridizedOperator op;
-  std::shared_ptr<void> device;
-};
-struct AlgCondensed {
-  hdivred::CondensedOperator op;
-  std::shared_ptr<void> device;
-};
+// ---- algebraic drop-ins on the reference's own ReductionInputs (reduction.hpp:16-33).
+// General element blocks (any size, any C and P): double-double-refined LU per
+// element (kern_alg.cu).  NOTE: FE inputs reaching this entry point do NOT use
+// the structured FE kernels (the coefficients and the mesh are not part of a
+// ReductionInputs); callers that hold the RtSpace and CellCoefficients should use
+// the FE overloads above.
 
 // hybridize(const ReductionInputs&)            reduction.hpp:70, reduction.cpp:262-354
 std::pair<AlgHybridized, std::vector<double>> hybridize(const hdivred::ReductionInputs& inputs, bool symmetric = true);

@@ -203,6 +203,38 @@ def run_ref_dump(out_path, dim, cells, k, coef, seed, weighted=False, blocks=Tru
     return read_dump(out_path)
 
 
+def sampled_rows_vs_dd(o: "Oracle", ro, ci, hv, gv, n: int, nx: int, base) -> tuple[float, float]:
+    """H / g rows of the cells in `base` and their +x neighbours (so shared-face
+    blocks are complete) against the element-wise DD oracle (hdo_dd_element);
+    needs o.run("structure").  Returns (max|dH| / max|H|, max|dg| / max|g|)."""
+    have = set(int(e) for e in base) | {int(e) + 1 for e in base}
+    row_vals, row_g = {}, {}
+    for cell in sorted(have):
+        rows, h, gt, _ = o.dd_element(cell)
+        for a_, r in enumerate(rows):
+            row_g.setdefault(int(r), []).append(gt[a_])
+            for b_, c in enumerate(rows):
+                row_vals.setdefault((int(r), int(c)), []).append(h[a_, b_])
+    C = o.getq("C.col_indices").reshape(-1, 2)
+
+    def cells_of(row):
+        return {int(C[row, 0]) // n, int(C[row, 1]) // n}
+
+    worst_h, worst_g, checked = 0.0, 0.0, 0
+    for (r, c), parts in row_vals.items():
+        if not (cells_of(r) & cells_of(c)) <= have:
+            continue
+        p = ro[r] + np.searchsorted(ci[ro[r]:ro[r + 1]], c)
+        assert ci[p] == c
+        worst_h = max(worst_h, abs(hv[p] - sum(parts)))
+        checked += 1
+    for r, parts in row_g.items():
+        if cells_of(r) <= have:
+            worst_g = max(worst_g, abs(gv[r] - sum(parts)))
+    assert checked > 0
+    return worst_h / max(np.max(np.abs(hv)), 1e-300), worst_g / max(np.max(np.abs(gv)), 1e-300)
+
+
 def rel_err(a, b, scale=None) -> float:
     a = np.asarray(a, dtype=np.float64)
     b = np.asarray(b, dtype=np.float64)

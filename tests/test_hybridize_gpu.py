@@ -13,7 +13,7 @@ import numpy as np
 import pytest
 
 from conftest import has_cuda, load_golden, GOLDEN_CASES
-from oracle_lib import Oracle, rel_err
+from oracle_lib import Oracle, rel_err, sampled_rows_vs_dd
 
 pytestmark = pytest.mark.gpu
 
@@ -192,38 +192,10 @@ def test_full_size_sampled_rows_vs_dd(dim, cells, k, coef, seed, nnz):
     ro, ci = sp.pattern("H")
     assert ro[-1] == nnz and np.all(np.diff(ro) > 0)
     assert np.all(np.isfinite(hv)) and np.all(np.isfinite(gv))
-    n = sp.n
     rng = np.random.default_rng(seed)
-    # sampled cells and their +x neighbours, so shared-face blocks are complete
     base = [int(e) for e in rng.choice(sp.ncells, 3 if k == 3 else 16, replace=False) if int(e) % cells[0] < cells[0] - 1]
-    have = set(base) | {e + 1 for e in base}
-    row_vals, row_g = {}, {}
-    for cell in sorted(have):
-        rows, h, gt, _ = o.dd_element(cell)
-        for a_, r in enumerate(rows):
-            row_g.setdefault(int(r), []).append(gt[a_])
-            for b_, c in enumerate(rows):
-                row_vals.setdefault((int(r), int(c)), []).append(h[a_, b_])
-    C = o.getq("C.col_indices").reshape(-1, 2)
-
-    def cells_of(row):
-        return {int(C[row, 0]) // n, int(C[row, 1]) // n}
-
-    worst_h, scale_h, worst_g, scale_g = 0.0, np.max(np.abs(hv)), 0.0, np.max(np.abs(gv))
-    checked = 0
-    for (r, c), parts in row_vals.items():
-        if not (cells_of(r) & cells_of(c)) <= have:
-            continue
-        p = ro[r] + np.searchsorted(ci[ro[r]:ro[r + 1]], c)
-        assert ci[p] == c
-        worst_h = max(worst_h, abs(hv[p] - sum(parts)))
-        checked += 1
-    for r, parts in row_g.items():
-        if cells_of(r) <= have:
-            worst_g = max(worst_g, abs(gv[r] - sum(parts)))
-    assert checked > 0
-    assert worst_h <= TOL * scale_h, worst_h / scale_h
-    assert worst_g <= TOL * scale_g, worst_g / scale_g
+    eh, eg = sampled_rows_vs_dd(o, ro, ci, hv, gv, sp.n, cells[0], base)
+    assert eh <= TOL and eg <= TOL, (eh, eg)
 
 
 @pytest.mark.parametrize("dim,cells,k", [(3, (6, 5, 4), 0), (3, (5, 4, 3), 1), (3, (3, 3, 2), 3), (2, (9, 7), 2)])

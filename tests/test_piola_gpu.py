@@ -114,7 +114,8 @@ def test_config4_full_size_sampled_rows_vs_dd():
     ro, ci = sp.pattern("H")
     assert ro[-1] == 34058880 and np.all(np.isfinite(hv)) and np.all(np.isfinite(gv))
     rng = np.random.default_rng(1004)
-    base = [int(e) for e in rng.choice(sp.ncells, 12, replace=False) if int(e) % cells[0] < cells[0] - 1]
+    pool = [e for e in range(sp.ncells) if e % cells[0] < cells[0] - 1]
+    base = [int(e) for e in rng.choice(pool, 128, replace=False)]  # + their +x neighbours: >= 256 cells
     have = sorted(set(base) | {e + 1 for e in base})
     A = sp.element_matrices()
     n = sp.n
