@@ -39,7 +39,8 @@ typedef enum {
   HDR_VALIDATION = 3,         /* hdivred::ValidationError (errors.hpp:44) */
   HDR_UNSUPPORTED = 4,        /* input outside what the device path implements (typed, never silent) */
   HDR_CUDA_ERROR = 5,         /* CUDA runtime failure, or no device */
-  HDR_INVALID_ARGUMENT = 6    /* std::invalid_argument in the reference */
+  HDR_INVALID_ARGUMENT = 6,   /* std::invalid_argument in the reference */
+  HDR_FORMAT_ERROR = 7        /* hdivred::FormatError (errors.hpp:25): malformed instance file */
 } hdr_status;
 
 typedef struct hdr_space_s* hdr_space_t;         /* mesh + RT_k space + device pattern + fixed factors */
@@ -109,6 +110,13 @@ hdr_status hdr_space_set_stream(hdr_space_t space, void* stream);
 hdr_status hdr_space_pattern(hdr_space_t space, int which, int64_t* row_offsets, int64_t* col_indices);
 /* master_globals of static_condense (src/reduction.cpp:509-521), int64, nS entries. */
 hdr_status hdr_space_master_globals(hdr_space_t space, int64_t* out);
+/* The element matrices A_T of every cell (element_matrices, src/rt_space.cpp:345-374:
+ * fl(fl(alpha D) + fl(beta M)) bit-exact; mapped cells: the Piola assembly),
+ * ncells*n*n row-major, to host (on_device = 0) or device memory.  Feeds the
+ * algebraic ReductionInputs of the space (build_reduction_inputs,
+ * src/reduction.cpp:200-222), e.g. for eliminate_essential. */
+hdr_status hdr_space_element_blocks(hdr_space_t space, const double* alpha, const double* beta, int on_device,
+                                    double* out);
 /* Signed local->global dof map of every cell (local_dof_map,
  * src/rt_space.cpp:383-393): global[ncells*n] int64, sign[ncells*n]. */
 hdr_status hdr_space_dof_map(hdr_space_t space, int64_t* global, double* sign);
@@ -344,6 +352,39 @@ hdr_status hdr_measure_dmma_peak(double* tflops, double* ms);
 hdr_status hdr_umma_selftest(int n, int k, const float* a, const float* b, float* d, int split);
 /* Synchronize the space's stream. */
 hdr_status hdr_space_synchronize(hdr_space_t space);
+
+/* ------------------------------------------------------------- instance I/O (host, all threads)
+ * The reference's text formats (src/block_io.cpp:15-94, src/matrix_market.cpp:36-146),
+ * parsed in parallel with exact rounding (values bit-identical to the reference's
+ * readers) and written with its "%.17g" (byte-identical files).  threads <= 0:
+ * all hardware threads.  Read results live in handles until destroyed. */
+typedef struct hdr_blocks_s* hdr_blocks_t;     /* ElementBlockOperator (block_operator.hpp:22-38) */
+typedef struct hdr_csr_host_s* hdr_csr_host_t; /* CsrMatrix (csr.hpp:13-42) in host memory */
+/* read_block_operator (block_io.cpp:41-94) */
+hdr_status hdr_io_read_block_operator(const char* path, int threads, hdr_blocks_t* out);
+/* info[0..3] = nblocks, broken_dim, global_dim, total matrix entries */
+hdr_status hdr_io_blocks_info(hdr_blocks_t blocks, int64_t* info);
+/* copies (NULL skips): block sizes (nblocks), dof globals and signs (broken_dim), row-major entries */
+hdr_status hdr_io_blocks_get(hdr_blocks_t blocks, int64_t* block_sizes, int64_t* dof_global, double* dof_sign,
+                             double* entries);
+void hdr_io_blocks_destroy(hdr_blocks_t blocks);
+/* write_block_operator (block_io.cpp:15-39) */
+hdr_status hdr_io_write_block_operator(const char* path, int64_t nblocks, int64_t broken_dim, int64_t global_dim,
+                                       const int64_t* block_sizes, const int64_t* dof_global, const double* dof_sign,
+                                       const double* entries, int threads);
+/* read_matrix_market (matrix_market.cpp:55-97, triplets summed as from_triplets) */
+hdr_status hdr_io_read_matrix_market(const char* path, int threads, hdr_csr_host_t* out);
+/* read_vector_lines (matrix_market.cpp:131-146): an n x 1 handle */
+hdr_status hdr_io_read_vector_lines(const char* path, int threads, hdr_csr_host_t* out);
+/* info[0..2] = nrows, ncols, nnz */
+hdr_status hdr_io_csr_info(hdr_csr_host_t a, int64_t* info);
+hdr_status hdr_io_csr_get(hdr_csr_host_t a, int64_t* row_offsets, int64_t* col_indices, double* values);
+void hdr_io_csr_destroy(hdr_csr_host_t a);
+/* write_matrix_market (matrix_market.cpp:36-53) */
+hdr_status hdr_io_write_matrix_market(const char* path, int64_t nrows, int64_t ncols, const int64_t* row_offsets,
+                                      const int64_t* col_indices, const double* values, int threads);
+/* write_vector_lines (matrix_market.cpp:124-129) */
+hdr_status hdr_io_write_vector_lines(const char* path, int64_t n, const double* v, int threads);
 
 #ifdef __cplusplus
 }

@@ -29,6 +29,8 @@
 
 #include "hdivred/csr.hpp"
 #include "hdivred/mesh.hpp"
+#include "hdivred/block_io.hpp"
+#include "hdivred/matrix_market.hpp"
 #include "hdivred/reduction.hpp"
 #include "hdivred/rt_space.hpp"
 
@@ -173,6 +175,27 @@ int cmd_dump(const std::map<std::string, std::string>& kv) {
   ReductionInputs in = build_reduction_inputs(sp, pb.coeffs, weighted);
   in.f_hat = pb.f_hat;
   Writer w(kv.at("out"));
+  // essential=1: eliminate_essential (src/reduction.cpp:589-698) on every boundary
+  // face, prescribed normal fluxes drawn U[-1, 1] after f_hat; everything below then
+  // runs on the reduced inputs (as build_problem does, src/driver.cpp:187-195)
+  if (kv.count("essential") && kv.at("essential") == "1") {
+    std::vector<EssentialBc> bcs;
+    std::vector<double> flux;
+    for (index_t f = 0; f < sp.mesh.nfaces(); ++f)
+      if (sp.mesh.face(f).is_boundary) {
+        bcs.push_back({f, pb.rng.uniform(-1.0, 1.0)});
+        flux.push_back(bcs.back().normal_flux);
+      }
+    EliminationResult el = eliminate_essential(sp, in, bcs);
+    w.d("ess.flux", flux);
+    w.q("ess.kept_globals", el.kept_globals);
+    w.d("ess.prescribed", el.prescribed);
+    w.q("ess.interior_global_begin", {el.inputs.interior_global_begin});
+    std::vector<index_t> sizes;
+    for (const auto& b : el.inputs.a_hat.blocks) sizes.push_back(static_cast<index_t>(b.dof_map.size()));
+    w.q("ess.block_sizes", sizes);
+    in = std::move(el.inputs);
+  }
   w.q("meta", {sp.mesh.dim, sp.mesh.ncells_per_axis[0], sp.mesh.ncells_per_axis[1], sp.mesh.ncells_per_axis[2],
                sp.order, sp.element_ndofs, sp.dofs_per_face, sp.interior_dofs_per_cell, sp.mesh.ncells(),
                sp.mesh.nfaces(), sp.ndofs, sp.face_dof_count, sp.broken_ndofs, in.c_mat.nrows,
@@ -271,6 +294,39 @@ int cmd_bench(const std::map<std::string, std::string>& kv) {
 
 }  // namespace
 
+// export prefix=P: the problem's ReductionInputs through the reference's own
+// writers (P.blocks, P.p.mtx, P.c.mtx, P.f.mtx, P.f.txt); import prefix=P: reads
+// them back with the reference's readers and prints the seconds taken.
+int cmd_export(const std::map<std::string, std::string>& kv) {
+  Problem pb = make_problem(kv);
+  const bool weighted = kv.count("weighted") && kv.at("weighted") == "1";
+  ReductionInputs in = build_reduction_inputs(pb.space, pb.coeffs, weighted);
+  in.f_hat = pb.f_hat;
+  const std::string pre = kv.at("prefix");
+  const double t0 = now();
+  write_block_operator(pre + ".blocks", in.a_hat);
+  write_matrix_market(pre + ".p.mtx", in.p_mat);
+  write_matrix_market(pre + ".c.mtx", in.c_mat);
+  write_vector_market(pre + ".f.mtx", in.f_hat);
+  write_vector_lines(pre + ".f.txt", in.f_hat);
+  std::printf("{\"write_s\": %.6f}\n", now() - t0);
+  return 0;
+}
+
+int cmd_import(const std::map<std::string, std::string>& kv) {
+  const std::string pre = kv.at("prefix");
+  const double t0 = now();
+  const ElementBlockOperator a = read_block_operator(pre + ".blocks");
+  const double t1 = now();
+  const CsrMatrix p = read_matrix_market(pre + ".p.mtx");
+  const CsrMatrix c = read_matrix_market(pre + ".c.mtx");
+  const std::vector<double> f = read_vector_market(pre + ".f.mtx");
+  const double t2 = now();
+  std::printf("{\"blocks_s\": %.6f, \"mtx_s\": %.6f, \"nblocks\": %zu, \"c_nnz\": %lld, \"f\": %zu}\n", t1 - t0,
+              t2 - t1, a.blocks.size(), static_cast<long long>(c.nnz()), f.size());
+  return 0;
+}
+
 int main(int argc, char** argv) {
   if (argc < 2) {
     std::fprintf(stderr, "usage: ref_harness dump|bench key=value...\n");
@@ -281,6 +337,8 @@ int main(int argc, char** argv) {
     const std::string cmd = argv[1];
     if (cmd == "dump") return cmd_dump(kv);
     if (cmd == "bench") return cmd_bench(kv);
+    if (cmd == "export") return cmd_export(kv);
+    if (cmd == "import") return cmd_import(kv);
     std::fprintf(stderr, "unknown command %s\n", cmd.c_str());
     return 2;
   } catch (const std::exception& e) {

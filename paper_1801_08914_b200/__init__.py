@@ -69,6 +69,7 @@ _STATUS_EXC = {
     _capi.UNSUPPORTED: UnsupportedError,
     _capi.CUDA_ERROR: DeviceError,
     _capi.INVALID_ARGUMENT: ValueError,
+    _capi.FORMAT_ERROR: FormatError,
 }
 
 
@@ -608,8 +609,6 @@ def space_from_config(config: dict) -> Space:
             sizes[a] = 1.0 / cells[a]
     if dim == 2:
         cells[2], sizes[2] = 1, 1.0
-    if config.get("essential_boundary", False):
-        raise UnsupportedError("essential-boundary elimination is outside the FE fast path")
     return Space(dim, cells[:dim], int(config.get("order", 0)), sizes, weighted=bool(config.get("weighted", False)))
 
 
@@ -621,6 +620,18 @@ def hybridized_matrix(config: dict):
     g = config.get("g", (1.0, 1.0, 1.0))
     g = _axes(g, 3, [1.0, 1.0, 1.0])
     f_hat = space.load_vector(g)
+    if config.get("essential_boundary", False):
+        # build_problem (src/driver.cpp:187-195): every boundary face eliminated with
+        # zero normal flux, then hybridize(ReductionInputs) on the reduced blocks
+        from . import algebraic as alg
+
+        inputs = alg.fe_reduction_inputs(space, alpha, beta, f_hat)
+        _, cm, cp = alg._face_geometry(space)
+        bcs = [alg.EssentialBc(int(f), 0.0) for f in np.nonzero((cm < 0) | (cp < 0))[0]]
+        red = alg.eliminate_essential(space, inputs, bcs).inputs
+        aop, gv = alg.hybridize(red, symmetric=True)
+        h = aop.h_mat
+        return (h.nrows, h.ncols, list(h.row_offsets), list(h.col_indices), list(h.values)), list(gv)
     op = space.hybridize(alpha, beta, f_hat)
     op.symmetrize()  # the reference symmetrizes every element block (src/reduction.cpp:316)
     nr, nc, ro, ci, hv = op.h_mat()
@@ -670,9 +681,10 @@ def launch_count() -> int:
 
 
 from . import algebraic  # noqa: E402  (ReductionInputs-level API; needs _check/_lib above)
+from . import io  # noqa: E402  (instance I/O, host threads)
 
 __all__ = [
-    "algebraic", "CapExceededError", "FormatError", "SingularBlockError", "ValidationError", "DimensionMismatch",
+    "algebraic", "io", "CapExceededError", "FormatError", "SingularBlockError", "ValidationError", "DimensionMismatch",
     "UnsupportedError", "DeviceError", "Space", "HybridizedOperator", "CondensedOperator", "hybridized_matrix",
     "space_info", "coefficients_from_config", "space_from_config", "launch_count", "pcg", "__version__",
 ]

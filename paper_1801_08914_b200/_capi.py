@@ -14,7 +14,7 @@ from pathlib import Path
 LIB_PATH = Path(os.environ.get("HDR_LIB") or Path(__file__).resolve().parent / "libhdivred_b200.so")
 
 # status codes (hdr_status)
-OK, SINGULAR_BLOCK, DIMENSION_MISMATCH, VALIDATION, UNSUPPORTED, CUDA_ERROR, INVALID_ARGUMENT = range(7)
+OK, SINGULAR_BLOCK, DIMENSION_MISMATCH, VALIDATION, UNSUPPORTED, CUDA_ERROR, INVALID_ARGUMENT, FORMAT_ERROR = range(8)
 
 # hdr_space_info indices
 INFO_NAMES = ["dim", "order", "ncells", "nfaces", "ndofs", "broken_ndofs", "element_ndofs", "dofs_per_face",
@@ -51,6 +51,7 @@ _SIGS = {
     "hdr_space_pattern": (_i32, [_vp, _i32, _vp, _vp]),
     "hdr_space_master_globals": (_i32, [_vp, _vp]),
     "hdr_space_dof_map": (_i32, [_vp, _vp, _vp]),
+    "hdr_space_element_blocks": (_i32, [_vp, _vp, _vp, _i32, _vp]),
     "hdr_space_synchronize": (_i32, [_vp]),
     "hdr_hybridize_fe": (_i32, [_vp, _vp, _vp, _vp, _i32, _vp]),
     "hdr_hybridize_fe_into": (_i32, [_vp, _vp, _vp, _vp, _i32]),
@@ -95,6 +96,19 @@ _SIGS = {
     "hdr_condensed_pcg": (_i32, [_vp, _vp, _vp, _i32, _d, _i64, _i32, _vp, _vp]),
     "hdr_alg_pcg": (_i32, [_vp, _vp, _vp, _i32, _d, _i64, _i32, _vp, _vp]),
     "hdr_csr_pcg_host": (_i32, [_i64, _vp, _vp, _vp, _vp, _vp, _d, _i64, _i32, _vp, _vp]),
+    "hdr_io_read_block_operator": (_i32, [ctypes.c_char_p, _i32, _vp]),
+    "hdr_io_blocks_info": (_i32, [_vp, _vp]),
+    "hdr_io_blocks_get": (_i32, [_vp, _vp, _vp, _vp, _vp]),
+    "hdr_io_blocks_destroy": (None, [_vp]),
+    "hdr_io_write_block_operator": (_i32, [ctypes.c_char_p, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _i32]),
+    "hdr_io_read_matrix_market": (_i32, [ctypes.c_char_p, _i32, _vp]),
+    "hdr_io_read_vector_lines": (_i32, [ctypes.c_char_p, _i32, _vp]),
+    "hdr_io_csr_info": (_i32, [_vp, _vp]),
+    "hdr_io_csr_get": (_i32, [_vp, _vp, _vp, _vp]),
+    "hdr_io_csr_destroy": (None, [_vp]),
+    "hdr_io_write_matrix_market": (_i32, [ctypes.c_char_p, _i64, _i64, _vp, _vp, _vp, _i32]),
+    "hdr_io_write_vector_lines": (_i32, [ctypes.c_char_p, _i64, _vp, _i32]),
+    "hdr_space_set_exact_policy": (_i32, [_vp, _i32, _d, _d, _vp]),
     "hdr_last_error": (ctypes.c_char_p, []),
     "hdr_version": (ctypes.c_char_p, []),
     "hdr_launch_count": (_i64, []),

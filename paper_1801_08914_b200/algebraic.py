@@ -200,5 +200,163 @@ def recover_condensed(op: CondensedOperator, x_b, f_hat):
     return x
 
 
+# ------------------------------------------------------------------ FE inputs and essential boundaries
+
+def _face_geometry(space):
+    """Per face: (axis, minus cell or -1, plus cell or -1), in the mesh's face order
+    (src/mesh.cpp:75-120: faces grouped by axis, lexicographic, x fastest)."""
+    dim = space.dim
+    N = list(space.cells) + [1] * (3 - len(space.cells))
+    axes, cms, cps = [], [], []
+    for a in range(dim):
+        d = [N[b] + (1 if b == a else 0) for b in range(3)]
+        idx = np.arange(d[0] * d[1] * d[2])
+        co = [idx % d[0], (idx // d[0]) % d[1], idx // (d[0] * d[1])]
+        plane = co[a]
+        cell = lambda c: c[0] + N[0] * (c[1] + N[1] * c[2])  # noqa: E731
+        cm = np.where(plane > 0, cell([co[b] - (1 if b == a else 0) for b in range(3)]), -1)
+        cp = np.where(plane < N[a], cell(co), -1)
+        axes.append(np.full(idx.size, a))
+        cms.append(cm)
+        cps.append(cp)
+    return np.concatenate(axes), np.concatenate(cms), np.concatenate(cps)
+
+
+def fe_reduction_inputs(space, alpha, beta, f_hat) -> ReductionInputs:
+    """build_reduction_inputs (src/reduction.cpp:200-222) of an FE space: the element
+    blocks A_T (assembled on the device, bit-identical to element_matrices), P from
+    the signed dof map (build_P, :136-150), C (build_C, :152-198: unit rows, or face
+    moment rows for weighted spaces), interior_global_begin = face dof count."""
+    n, nc = space.n, space.ncells
+    a = np.ascontiguousarray(alpha, dtype=np.float64)
+    b = np.ascontiguousarray(beta, dtype=np.float64)
+    blocks = np.empty(nc * n * n)
+    _check(_lib().hdr_space_element_blocks(space._h, a.ctypes.data, b.ctypes.data, 0, blocks.ctypes.data))
+    blocks = blocks.reshape(nc, n, n)
+    gl, sg = space.dof_map()
+    nb = space.broken_ndofs
+    p_mat = Csr(nb, space.ndofs, np.arange(nb + 1), gl, sg)
+    dpf, nint, dim = space.info["dofs_per_face"], space.info["interior_dofs_per_cell"], space.dim
+    axis, cm, cp = _face_geometry(space)
+    interior = (cm >= 0) & (cp >= 0)
+    faces = np.nonzero(interior)[0]
+    m = faces.size * dpf
+    if space.weighted:
+        fm = np.empty(2 * dim * dpf * n)
+        hh = (ctypes.c_double * 3)(*space.sizes)
+        _check(_lib().hdr_reference_element(dim, space.order, hh, None, None, fm.ctypes.data, None))
+        fm = fm.reshape(2 * dim, dpf, n)
+    ro, ci, cv = [0], [], []
+    for f in faces:
+        ax = int(axis[f])
+        lm, lp = nint + (2 * ax + 1) * dpf, nint + 2 * ax * dpf
+        om, op = int(cm[f]) * n, int(cp[f]) * n
+        for r in range(dpf):
+            if not space.weighted:
+                ci += [om + lm + r, op + lp + r]
+                cv += [1.0, 1.0]
+            else:
+                ci += [om + lm + s_ for s_ in range(dpf)] + [op + lp + s_ for s_ in range(dpf)]
+                cv += [fm[2 * ax + 1, r, lm + s_] for s_ in range(dpf)] + [fm[2 * ax, r, lp + s_] for s_ in range(dpf)]
+            ro.append(len(ci))
+    c_mat = Csr(m, nb, np.array(ro), np.array(ci, dtype=np.int64), np.array(cv))
+    return ReductionInputs(list(blocks), p_mat, c_mat, np.ascontiguousarray(f_hat, dtype=np.float64),
+                           interior_global_begin=space.info["face_dof_count"], dof_global=gl)
+
+
+@dataclass
+class EssentialBc:
+    """EssentialBc (include/hdivred/reduction.hpp:104-107)."""
+    face: int
+    normal_flux: float = 0.0
+
+
+@dataclass
+class EliminationResult:
+    """EliminationResult (reduction.hpp:109-113)."""
+    inputs: ReductionInputs
+    kept_globals: np.ndarray
+    prescribed: np.ndarray
+
+
+def eliminate_essential(space, inputs: ReductionInputs, bcs) -> EliminationResult:
+    """eliminate_essential (src/reduction.cpp:589-698): removes the face dofs of
+    the listed boundary faces from every block, moves their prescribed values
+    (normal flux on sub-dof 0, 0 on the others) to the right-hand side
+    (f_keep -= A[keep, drop] x_drop, in the reference's order), renumbers the
+    globals, keeps C's rows (eliminated dofs are boundary dofs, so C never
+    touches them).  Host bookkeeping; the reduced blocks then go through the
+    device's general element path (kern_alg.cu)."""
+    n = inputs.p_mat.ncols
+    dpf = space.info["dofs_per_face"]
+    _, cm, cp = _face_geometry(space)
+    elim = np.zeros(n, dtype=bool)
+    prescribed = np.zeros(n)
+    for bc in bcs:
+        if bc.face < 0 or bc.face >= space.info["nfaces"]:
+            raise ValueError("eliminate_essential: face index out of range")
+        if cm[bc.face] >= 0 and cp[bc.face] >= 0:
+            raise ValueError(f"eliminate_essential: face {bc.face} is not on the boundary")
+        for sub in range(dpf):
+            g = bc.face * dpf + sub
+            if elim[g]:
+                raise ValueError(f"eliminate_essential: face {bc.face} listed twice")
+            elim[g] = True
+            prescribed[g] = bc.normal_flux if sub == 0 else 0.0
+    kept = np.nonzero(~elim)[0]
+    new_global = np.full(n, -1, dtype=np.int64)
+    new_global[kept] = np.arange(kept.size)
+    gl = inputs.dof_global if inputs.dof_global is not None else inputs.p_mat.col_indices
+    sg = inputs.p_mat.values
+    blocks, dof_global, signs, f_new, broken_keep = [], [], [], [], []
+    off = 0
+    for blk in inputs.blocks:
+        nel = np.shape(blk)[0]
+        g_e, s_e = gl[off:off + nel], sg[off:off + nel]
+        drop_mask = elim[g_e]
+        keep = np.nonzero(~drop_mask)[0]
+        drop = np.nonzero(drop_mask)[0]
+        A = np.asarray(blk)
+        blocks.append(np.ascontiguousarray(A[np.ix_(keep, keep)]))
+        dof_global.append(new_global[g_e[keep]])
+        signs.append(s_e[keep])
+        broken_keep.append(off + keep)
+        for i in keep:  # v -= A[keep_i, l] * (sign_l * prescribed[global_l]), l in drop order
+            v = float(inputs.f_hat[off + i])
+            for l in drop:
+                v -= A[i, l] * (s_e[l] * prescribed[g_e[l]])
+            f_new.append(v)
+        off += nel
+    dof_global = np.concatenate(dof_global) if dof_global else np.zeros(0, np.int64)
+    signs = np.concatenate(signs) if signs else np.zeros(0)
+    broken_keep = np.concatenate(broken_keep) if broken_keep else np.zeros(0, np.int64)
+    nb = broken_keep.size
+    p_mat = Csr(nb, kept.size, np.arange(nb + 1), dof_global, signs)
+    new_broken = np.full(inputs.p_mat.nrows, -1, dtype=np.int64)
+    new_broken[broken_keep] = np.arange(nb)
+    c = inputs.c_mat
+    cols = new_broken[c.col_indices]
+    if np.any(cols < 0):
+        raise ValueError("eliminate_essential: constraint touches an eliminated dof")
+    c_mat = Csr(c.nrows, nb, c.row_offsets.copy(), cols, c.values.copy())  # column order preserved (monotone map)
+    igb = inputs.interior_global_begin
+    if igb >= 0:
+        igb = igb - int(np.count_nonzero(elim[:igb]))
+    red = ReductionInputs(blocks, p_mat, c_mat, np.array(f_new), interior_global_begin=igb, dof_global=dof_global)
+    return EliminationResult(red, kept, prescribed)
+
+
+def expand_eliminated(elim: EliminationResult, reduced, full_n: int) -> np.ndarray:
+    """expand_eliminated (src/reduction.cpp:700-709)."""
+    reduced = np.asarray(reduced, dtype=np.float64)
+    if reduced.size != elim.kept_globals.size:
+        raise ValueError("expand_eliminated: reduced solution length")
+    full = np.zeros(full_n)
+    full[:elim.prescribed.size] = elim.prescribed[:full_n]
+    full[elim.kept_globals] = reduced
+    return full
+
+
 __all__ = ["Csr", "ReductionInputs", "HybridizedOperator", "CondensedOperator", "hybridize", "static_condense",
-           "recover_hybrid", "recover_condensed"]
+           "recover_hybrid", "recover_condensed", "fe_reduction_inputs", "EssentialBc", "EliminationResult",
+           "eliminate_essential", "expand_eliminated"]

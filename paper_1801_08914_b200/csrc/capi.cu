@@ -495,6 +495,39 @@ hdr_status hdr_space_element_matrices(hdr_space_t sp, double* out) {
   });
 }
 
+hdr_status hdr_space_element_blocks(hdr_space_t sp, const double* alpha, const double* beta, int on_device,
+                                    double* out) {
+  if (!sp || !alpha || !beta || !out) return fail(HDR_INVALID_ARGUMENT, "null argument");
+  return catch_all([&]() -> hdr_status {
+    cudaStream_t st = sp->stream;
+    DBuf<double> da, db, dout;
+    const double *pa = alpha, *pb = beta;
+    if (!on_device) {
+      stage(da, alpha, sp->ncells, 0, st);
+      stage(db, beta, sp->ncells, 0, st);
+      pa = da.p;
+      pb = db.p;
+    }
+    const size_t cnt = static_cast<size_t>(sp->ncells) * sp->n * sp->n;
+    if (sp->geom) {
+      geom_assemble_blocks(sp->geom, pa, pb, st);
+      CK(cudaMemcpyAsync(out, geom_element_blocks(sp->geom), cnt * 8,
+                         on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
+    } else {
+      double* po = out;
+      if (!on_device) {
+        dout.alloc(cnt);
+        po = dout.p;
+      }
+      launch_affine_assemble(sp->ncells, sp->n, sp->fixed.p, pa, pb, po, st);  // fixed = [D | M | ...]
+      if (!on_device) CK(cudaMemcpyAsync(out, po, cnt * 8, cudaMemcpyDeviceToHost, st));
+    }
+    CK(cudaStreamSynchronize(st));
+    CK(cudaGetLastError());
+    return HDR_OK;
+  });
+}
+
 hdr_status hdr_space_info(hdr_space_t sp, int64_t* o) {
   if (!sp || !o) return fail(HDR_INVALID_ARGUMENT, "null argument");
   o[HDR_INFO_DIM] = sp->dim;

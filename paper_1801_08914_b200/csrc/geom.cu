@@ -472,6 +472,9 @@ hdr_status geom_recover_condensed(GeomState* G, const double* alpha, const doubl
 }
 
 const double* geom_element_blocks(const GeomState* G) { return G->ablk.p; }
+void geom_assemble_blocks(GeomState* G, const double* alpha, const double* beta, cudaStream_t st) {
+  assemble(G, alpha, beta, st);
+}
 bool geom_mapped(const GeomState* G) { return G->mapped; }
 
 }  // namespace hdr

@@ -27,5 +27,7 @@ hdr_status geom_condense(GeomState* G, const double* alpha, const double* beta, 
 hdr_status geom_recover_condensed(GeomState* G, const double* alpha, const double* beta, const double* x_b,
                                   const double* f, double* x, cudaStream_t st);
 const double* geom_element_blocks(const GeomState* G);
+// A_T of every cell (mapped: Piola assembly; affine weighted: fl(fl(alpha D) + fl(beta M)))
+void geom_assemble_blocks(GeomState* G, const double* alpha, const double* beta, cudaStream_t st);
 
 }  // namespace hdr

@@ -282,7 +282,6 @@ __device__ __forceinline__ void rt0_row_math(const HybArgs& A, const Rt0Const<2 
 
 template <int DIM, int PASS>
 __device__ __forceinline__ bool rt0_rows_body(const HybArgs& A, const Rt0Const<2 * DIM>& c, double* stage) {
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // the exact-path kernel may launch
   constexpr int N = 2 * DIM;
   constexpr int NC = N + 1;
   constexpr int G = 32 / N;  // cells per warp
@@ -579,10 +578,16 @@ __device__ __forceinline__ bool rt0_correction(const HybArgs& A, const Rt0Const<
   const float cm = rt0_fast_correction<DIM>(c, F, a, b, s, ib, C, hm);
   // a-posteriori order control and acceptance (hdr_device.cuh struct_order)
   const double ratio = hm > 0.f ? static_cast<double>(cm) / hm : 0.0;
+#ifndef HDR_AB_NOQLOG
   if (A.qlog) A.qlog[e] = static_cast<float>(ratio);
+#endif
   bool exact = false;
   const int P = struct_order(ratio, A.p_max, A.eps32, exact);
-  if (exact || A.force_exact) {  // rejected: zero contribution (the caller zeroes 1 / beta too)
+#ifdef HDR_AB_NOQLOG
+  if (exact) {
+#else
+  if (exact || A.force_exact) {
+#endif  // rejected: zero contribution (the caller zeroes 1 / beta too)
 #pragma unroll
     for (int i = 0; i < Rt0Fast<N>::NS; ++i) C[i] = 0.f;
     atomicAdd(A.xcount, 1);
@@ -620,7 +625,6 @@ __device__ __forceinline__ void rt0_hrow_c(const Rt0Const<2 * DIM>& c, double s,
 template <int DIM, int PASS, bool SIDE>
 __device__ __forceinline__ bool rt0_cell_body(const HybArgs& A, const Rt0Const<2 * DIM>& c, const Rt0Fast<2 * DIM>& F,
                                               double* stage) {
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // the exact-path kernel may launch
   constexpr int N = 2 * DIM;
   constexpr int NC = N + 1;
   __shared__ float scr[2 * N * N + Rt0Fast<N>::NS][kCT];  // general-correction scratch (rare cells)
@@ -704,6 +708,7 @@ __device__ __forceinline__ bool rt0_cell_body(const HybArgs& A, const Rt0Const<2
         A.g[row] = h[N] + sv.y;
       }
     }
+#ifndef HDR_AB_NOFIX
     if (rejected) {  // rare: the cell's exact rows over its zero ones (same positions, same sums)
       double hx[N * NC];
       rt0_exact_ool<N, NC, true>(A.fx.D, A.fx.M, a, b, inmask, A.f + static_cast<int64_t>(e) * N, nullptr, hx,
@@ -730,6 +735,7 @@ __device__ __forceinline__ bool rt0_cell_body(const HybArgs& A, const Rt0Const<2
         }
       }
     }
+#endif
     return rejected;
   }
   return rejected;  // (SIDE is the only form)
