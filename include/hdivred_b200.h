@@ -40,7 +40,9 @@ typedef enum {
   HDR_UNSUPPORTED = 4,        /* input outside what the device path implements (typed, never silent) */
   HDR_CUDA_ERROR = 5,         /* CUDA runtime failure, or no device */
   HDR_INVALID_ARGUMENT = 6,   /* std::invalid_argument in the reference */
-  HDR_FORMAT_ERROR = 7        /* hdivred::FormatError (errors.hpp:25): malformed instance file */
+  HDR_FORMAT_ERROR = 7,       /* hdivred::FormatError (errors.hpp:25): malformed instance file */
+  HDR_CAP_EXCEEDED = 8,       /* hdivred::CapExceeded (errors.hpp:20): dense size cap */
+  HDR_SETUP_FAILED = 9        /* hdivred::SetupFailed (errors.hpp:39): AMG setup */
 } hdr_status;
 
 typedef struct hdr_space_s* hdr_space_t;         /* mesh + RT_k space + device pattern + fixed factors */
@@ -320,6 +322,20 @@ hdr_status hdr_csr_pcg_host(int64_t n, const int64_t* row_offsets, const int64_t
                             const double* b, double* x, double rtol, int64_t maxit, int precond,
                             double* residual_history, hdr_pcg_report* report);
 
+/* ------------------------------------------------------------ diagnostics
+ *
+ * near_nullspace_check (src/reduction.cpp:711-742): the ascending eigenvalues of
+ * the assembled m x m matrix C Y C^T, Y_T = M^-1 - M^-1 B^T (B M^-1 B^T)^-1 B M^-1
+ * (M = beta_T ref_mass, B = ref_div_form), computed on the device in the
+ * reference's operation order (kern_nullspace.cu): bit-identical eigenvalues.
+ * weighted: the mass-weighted constraint rows (build_C weighted).  alpha, beta:
+ * ncells host (on_device = 0) or device arrays, validated > 0 like
+ * element_matrices (rt_space.cpp:353-354, HDR_INVALID_ARGUMENT).  eigenvalues:
+ * m host doubles (HDR_INFO_M; m = 0 writes nothing).  HDR_CAP_EXCEEDED when
+ * m * m > dense_cap (the reference's default is 4,000,000). */
+hdr_status hdr_near_nullspace_check(hdr_space_t space, const double* alpha, const double* beta, int on_device,
+                                    int weighted, int64_t dense_cap, double* eigenvalues);
+
 /* ------------------------------------------------- host-only introspection */
 
 /* The reference element matrices of RT_k on an h[0] x h[1] (x h[2]) box,
@@ -327,6 +343,8 @@ hdr_status hdr_csr_pcg_host(int64_t n, const int64_t* row_offsets, const int64_t
  * (n*n), face_moments (2*dim*dpf*n), unit_load (3*n).  NULL skips.  Host only. */
 hdr_status hdr_reference_element(int dim, int order, const double h[3], double* divdiv, double* mass,
                                  double* face_moments, double* unit_load);
+/* RtSpace::ref_div_form (rt_space.cpp:197, 256-259): (k+1)^dim x n, bit-identical.  Host only. */
+hdr_status hdr_reference_div_form(int dim, int order, const double h[3], double* div_form);
 /* Fixed factors of the structured element solve: X (n*r), lambda
  * (r), E, N0, Ma (n*n); diag = {rho, max|E|/max|D|, max|X^T M X - I|, block
  * diagonal M}.  Host only. */

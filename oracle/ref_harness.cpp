@@ -211,6 +211,7 @@ int cmd_dump(const std::map<std::string, std::string>& kv) {
     for (const auto& u : sp.ref_unit_load) ul.insert(ul.end(), u.begin(), u.end());
     w.d("ref_unit_load", ul);
   }
+  w.d("ref_div_form", sp.ref_div_form.entries);
   w.d("alpha", pb.coeffs.alpha);
   w.d("beta", pb.coeffs.beta);
   w.d("f_hat", in.f_hat);
@@ -234,6 +235,9 @@ int cmd_dump(const std::map<std::string, std::string>& kv) {
 
   const auto [hyb, g] = hybridize(in);
   w.csr("H", hyb.h_mat);
+  // near_nullspace_check (src/reduction.cpp:711-742): eigenvalues of C Y C^T
+  if (kv.count("nullspace") && kv.at("nullspace") == "1" && in.c_mat.nrows * in.c_mat.nrows <= kDefaultDenseCap)
+    w.d("nullspace", near_nullspace_check(sp, pb.coeffs, weighted));
   w.d("g", g);
   std::vector<double> lambda(static_cast<std::size_t>(hyb.h_mat.nrows));
   for (auto& v : lambda) v = pb.rng.uniform(-1.0, 1.0);

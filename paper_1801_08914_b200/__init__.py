@@ -50,6 +50,10 @@ class ValidationError(HdivredError):
     """hdivred::ValidationError (include/hdivred/errors.hpp:44)."""
 
 
+class SetupFailed(HdivredError):
+    """hdivred::SetupFailed (include/hdivred/errors.hpp:39): AMG setup."""
+
+
 class DimensionMismatch(HdivredError):
     """hdivred::DimensionMismatch (include/hdivred/errors.hpp:9)."""
 
@@ -70,6 +74,8 @@ _STATUS_EXC = {
     _capi.CUDA_ERROR: DeviceError,
     _capi.INVALID_ARGUMENT: ValueError,
     _capi.FORMAT_ERROR: FormatError,
+    _capi.CAP_EXCEEDED: CapExceededError,
+    _capi.SETUP_FAILED: SetupFailed,
 }
 
 
@@ -262,6 +268,17 @@ class Space:
             qp = q_log.data_ptr()
         _check(_lib().hdr_space_set_exact_policy(self._h, 1 if force else 0, float(eps32), float(eps_tc), qp))
         self._qlog = q_log
+
+    def near_nullspace_check(self, alpha, beta, weighted: bool = False, dense_cap: int = 4_000_000) -> np.ndarray:
+        """near_nullspace_check (src/reduction.cpp:711-742): ascending eigenvalues of
+        C Y C^T, computed on the device in the reference's operation order."""
+        a = _as_f64(alpha, self.ncells, "alpha")
+        b = _as_f64(beta, self.ncells, "beta")
+        dev = _same_device([a, b])
+        out = np.empty(self.m)
+        _check(_lib().hdr_near_nullspace_check(self._h, _ptr(a)[0], _ptr(b)[0], dev, 1 if weighted else 0,
+                                               int(dense_cap), out.ctypes.data if self.m else None))
+        return out
 
     # ---- hot path
     def hybridize(self, alpha, beta, f_hat) -> "HybridizedOperator":

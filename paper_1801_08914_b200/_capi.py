@@ -14,7 +14,8 @@ from pathlib import Path
 LIB_PATH = Path(os.environ.get("HDR_LIB") or Path(__file__).resolve().parent / "libhdivred_b200.so")
 
 # status codes (hdr_status)
-OK, SINGULAR_BLOCK, DIMENSION_MISMATCH, VALIDATION, UNSUPPORTED, CUDA_ERROR, INVALID_ARGUMENT, FORMAT_ERROR = range(8)
+(OK, SINGULAR_BLOCK, DIMENSION_MISMATCH, VALIDATION, UNSUPPORTED, CUDA_ERROR, INVALID_ARGUMENT, FORMAT_ERROR,
+ CAP_EXCEEDED, SETUP_FAILED) = range(10)
 
 # hdr_space_info indices
 INFO_NAMES = ["dim", "order", "ncells", "nfaces", "ndofs", "broken_ndofs", "element_ndofs", "dofs_per_face",
@@ -109,6 +110,8 @@ _SIGS = {
     "hdr_io_write_matrix_market": (_i32, [ctypes.c_char_p, _i64, _i64, _vp, _vp, _vp, _i32]),
     "hdr_io_write_vector_lines": (_i32, [ctypes.c_char_p, _i64, _vp, _i32]),
     "hdr_space_set_exact_policy": (_i32, [_vp, _i32, _d, _d, _vp]),
+    "hdr_reference_div_form": (_i32, [_i32, _i32, _vp, _vp]),
+    "hdr_near_nullspace_check": (_i32, [_vp, _vp, _vp, _i32, _i32, _i64, _vp]),
     "hdr_last_error": (ctypes.c_char_p, []),
     "hdr_version": (ctypes.c_char_p, []),
     "hdr_launch_count": (_i64, []),

@@ -230,6 +230,18 @@ hdr_status hdr_reference_element(int dim, int order, const double h[3], double* 
   });
 }
 
+hdr_status hdr_reference_div_form(int dim, int order, const double h[3], double* div_form) {
+  if (dim != 2 && dim != 3) return fail(HDR_INVALID_ARGUMENT, "dim must be 2 or 3");
+  if (order < 0 || order > 3) return fail(HDR_INVALID_ARGUMENT, "order must be in 0..3");
+  if (!div_form) return fail(HDR_INVALID_ARGUMENT, "null argument");
+  return catch_all([&]() -> hdr_status {
+    const double hh[3] = {h ? h[0] : 1.0, h ? h[1] : 1.0, (h && dim == 3) ? h[2] : 1.0};
+    const RefElement re = build_reference_element(dim, order, hh);
+    std::memcpy(div_form, re.div_form.data(), re.div_form.size() * 8);
+    return HDR_OK;
+  });
+}
+
 hdr_status hdr_structured_factors(int dim, int order, const double h[3], double* X, double* lambda, double* E,
                                   double* N0, double* Ma, double* diag, int64_t* rank) {
   if (dim != 2 && dim != 3) return fail(HDR_INVALID_ARGUMENT, "dim must be 2 or 3");
@@ -606,6 +618,33 @@ hdr_status hdr_space_master_globals(hdr_space_t sp, int64_t* out) {
   if (!sp || !out) return fail(HDR_INVALID_ARGUMENT, "null argument");
   for (int64_t i = 0; i < sp->ns; ++i) out[i] = i;  // every face dof is a master, in order
   return HDR_OK;
+}
+
+hdr_status hdr_near_nullspace_check(hdr_space_t sp, const double* alpha, const double* beta, int on_device,
+                                    int weighted, int64_t dense_cap, double* eigenvalues) {
+  if (!sp || !alpha || !beta) return fail(HDR_INVALID_ARGUMENT, "null argument");
+  if (sp->m == 0) return HDR_OK;  // no multipliers: the reference returns {}
+  if (!eigenvalues) return fail(HDR_INVALID_ARGUMENT, "null argument");
+  if (sp->m * sp->m > dense_cap)
+    return fail(HDR_CAP_EXCEEDED, "near_nullspace_check: m = " + std::to_string(sp->m) + " exceeds dense cap");
+  return catch_all([&]() -> hdr_status {
+    cudaStream_t st = sp->stream;
+    // element_matrices' coefficient check (rt_space.cpp:353-354), on a host copy
+    std::vector<double> ha(static_cast<size_t>(sp->ncells)), hb(static_cast<size_t>(sp->ncells));
+    CK(cudaMemcpyAsync(ha.data(), alpha, ha.size() * 8, on_device ? cudaMemcpyDeviceToHost : cudaMemcpyHostToHost, st));
+    CK(cudaMemcpyAsync(hb.data(), beta, hb.size() * 8, on_device ? cudaMemcpyDeviceToHost : cudaMemcpyHostToHost, st));
+    CK(cudaStreamSynchronize(st));
+    for (size_t e = 0; e < ha.size(); ++e)
+      if (!(ha[e] > 0.0) || !(hb[e] > 0.0))
+        return fail(HDR_INVALID_ARGUMENT, "element_matrices: coefficients must be positive");
+    DBuf<double> db;
+    const double* pb = beta;
+    if (!on_device) {
+      stage(db, beta, sp->ncells, 0, st);
+      pb = db.p;
+    }
+    return near_nullspace_device(sp->dm, sp->re, weighted, sp->mbase.p, sp->m, pb, eigenvalues, st);
+  });
 }
 
 hdr_status hdr_space_dof_map(hdr_space_t sp, int64_t* global, double* sign) {

@@ -13,6 +13,8 @@ struct RefElement {
   std::vector<double> divdiv, mass, face_moments;  // n*n, n*n, 2*dim*dpf*n
   std::vector<double> unit_load;                   // 3*n: (e_c, phi_i) per component c
   std::vector<int> comp;                           // vector component of each local dof
+  int npr = 1;                                     // pressure dofs (k+1)^dim
+  std::vector<double> div_form;                    // npr*n: (q_r, div phi_j) (RtSpace::ref_div_form)
   // basis at the nq^dim Gauss points (x fastest), for mapped (Piola) cells:
   // bq_val[(p*n + j)*3 + c] = phi_j,c(s_p) on the unit box coordinates s, bq_div[p*n + j]
   // = sum_a d phi_j,a / d s_a / h_a, bq_w[p] = product of the 1D weights, qs = 1D points

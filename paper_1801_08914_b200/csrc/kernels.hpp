@@ -252,4 +252,9 @@ hdr_status pcg_device(int64_t n, const int64_t* ro, const int32_t* ci32, const i
                       hdr_pcg_report* rep, cudaStream_t st);
 void launch_dot(int64_t n, const double* x, const double* y, double* part, double* out, cudaStream_t st);
 
+// ---- near_nullspace_check (kern_nullspace.cu)
+struct RefElement;
+hdr_status near_nullspace_device(const DevMesh& dm, const RefElement& re, int weighted, const int* mbase, int64_t m,
+                                 const double* beta_dev, double* out, cudaStream_t st);
+
 }  // namespace hdr

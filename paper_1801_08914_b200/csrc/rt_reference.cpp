@@ -189,6 +189,10 @@ RefElement build_reference_element(int dim, int k, const double h[3]) {
   re.mass.assign(static_cast<size_t>(n) * n, 0.0);
   re.face_moments.assign(static_cast<size_t>(2 * dim) * dpf * n, 0.0);
   re.unit_load.assign(3 * static_cast<size_t>(n), 0.0);
+  const int npr = dim == 3 ? (k + 1) * (k + 1) * (k + 1) : (k + 1) * (k + 1);
+  re.npr = npr;
+  re.div_form.assign(static_cast<size_t>(npr) * n, 0.0);
+  std::vector<double> prv(npr);
 
   std::vector<double> pv(n), pd(n), bv(3 * static_cast<size_t>(n)), bd(n);
   const int nqz = (dim == 3) ? nq : 1;
@@ -237,6 +241,16 @@ RefElement build_reference_element(int dim, int k, const double h[3]) {
           }
           for (int c = 0; c < dim; ++c) re.unit_load[static_cast<size_t>(c) * n + i] += w * vi[c];
         }
+        // div_form (rt_space.cpp:256-259): pressure Legendre products (pressure_polys
+        // :104-111, x fastest) against the basis divergence
+        for (int r = 0; r < npr; ++r) {
+          const int d[3] = {r % (k + 1), (r / (k + 1)) % (k + 1), r / ((k + 1) * (k + 1))};
+          double v = 1.0;
+          for (int a = 0; a < dim; ++a) v *= leg(d[a], s[a]);
+          prv[r] = v;
+        }
+        for (int r = 0; r < npr; ++r)
+          for (int j = 0; j < n; ++j) re.div_form[static_cast<size_t>(r) * n + j] += w * prv[r] * bd[j];
       }
 
   // face moment rows of the weighted constraint (rt_space.cpp:267-312)

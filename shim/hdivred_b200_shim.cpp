@@ -20,6 +20,9 @@ void check(hdr_status s) {
     case HDR_DIMENSION_MISMATCH: throw hdivred::DimensionMismatch(msg);
     case HDR_VALIDATION: throw hdivred::ValidationError(msg);
     case HDR_INVALID_ARGUMENT: throw std::invalid_argument(msg);
+    case HDR_CAP_EXCEEDED: throw hdivred::CapExceeded(msg);
+    case HDR_SETUP_FAILED: throw hdivred::SetupFailed(msg);
+    case HDR_FORMAT_ERROR: throw hdivred::FormatError(msg, 0);
     default: throw std::runtime_error("hdivred_b200: " + msg);
   }
 }

@@ -7,7 +7,7 @@ oracle/Makefile) on small seeded instances.  Run in the build container:
 Each fixture holds every array ref_harness dumps: reference element matrices
 (D_ref, M_ref, face moments), the seeded inputs (alpha, beta, f_hat, lambda,
 x_b), P, C, H/g, recovered x_hat/x, S/f_S/master_globals, recovered x_cond,
-and the reference spmv outputs.  k = 2, 3 use the guard-lifted copy of
+the reference spmv outputs, ref_div_form and the near_nullspace_check eigenvalues.  k = 2, 3 use the guard-lifted copy of
 rt_space.cpp.
 """
 import sys
@@ -32,13 +32,14 @@ CASES = [
     ("h3_rt2_2x2x2_logu3", 3, (2, 2, 2), 2, "logu:1e-3:1e3", 1004, False, False),
     ("h3_rt3_2x2x1_checker", 3, (2, 2, 1), 3, "checker:1e-2:1e2", 1005, False, False),
     ("h3_rt0_1x1x1_unit", 3, (1, 1, 1), 0, "uniform:1:1", 7, False, True),
+    ("h3_rt0_3x3x3_unit", 3, (3, 3, 3), 0, "uniform:1:1", 7, False, True),
 ]
 
 
 def main():
     with tempfile.TemporaryDirectory() as td:
         for name, dim, cells, k, coef, seed, weighted, blocks in CASES:
-            d = run_ref_dump(Path(td) / "d.bin", dim, cells, k, coef, seed, weighted, blocks)
+            d = run_ref_dump(Path(td) / "d.bin", dim, cells, k, coef, seed, weighted, blocks, nullspace=True)
             d["case"] = np.array([dim, *list(cells) + [1] * (3 - len(cells)), k, seed, int(weighted)], np.int64)
             d["coef"] = np.frombuffer(coef.encode(), dtype=np.uint8)
             np.savez_compressed(HERE / f"{name}.npz", **{k_.replace(".", "__"): v for k_, v in d.items()})

@@ -49,6 +49,16 @@ def test_host_reference_element_bit_exact(name):
     assert np.array_equal(ul, g["ref_unit_load"])
 
 
+@pytest.mark.parametrize("name", GOLDEN_CASES)
+def test_host_div_form_bit_exact(name):
+    """ref_div_form (rt_space.cpp:256-259), the B of near_nullspace_check."""
+    g = load_golden(name)
+    h = (ctypes.c_double * 3)(*g["h"])
+    out = np.empty(g["ref_div_form"].size)
+    assert _capi.load().hdr_reference_div_form(g["dim"], g["k"], ctypes.addressof(h), out.ctypes.data) == 0
+    assert np.array_equal(out, g["ref_div_form"])
+
+
 @pytest.mark.parametrize("dim,k,cells", [(2, 0, 64), (3, 0, 64), (3, 1, 48), (3, 2, 24), (3, 3, 32), (2, 3, 16)])
 def test_structured_factors(dim, k, cells):
     """D = Ms X diag(lambda) X^T Ms + E with E at rounding level, X M-orthonormal,
