@@ -317,10 +317,54 @@ hdr_status hdr_condensed_pcg(hdr_condensed_t op, const double* b, double* x, int
                              int64_t maxit, int precond, double* residual_history, hdr_pcg_report* report);
 hdr_status hdr_alg_pcg(hdr_alg_t op, const double* b, double* x, int on_device, double rtol, int64_t maxit,
                        int precond, double* residual_history, hdr_pcg_report* report);
+/* precond (all four of the reference's PrecondKind, include/hdivred/driver.hpp:15):
+ *   0 none, 1 jacobi (jacobi_setup), 2 sgs (ssgs_setup: one forward + one backward
+ *   Gauss-Seidel sweep, solvers.cpp:60-72), 3 amg (amg_setup with default
+ *   AmgOptions + one V(1,1) cycle per application, amg.cpp:189-266).
+ * The reference's check_symmetric (solvers.cpp:25-30) runs first on the device:
+ * |A - A^T| > 1e-10 max|A| or a non-square matrix -> HDR_INVALID_ARGUMENT. */
 /* Host-array form for a caller-owned CsrMatrix (copies in and out). */
 hdr_status hdr_csr_pcg_host(int64_t n, const int64_t* row_offsets, const int64_t* col_indices, const double* values,
                             const double* b, double* x, double rtol, int64_t maxit, int precond,
                             double* residual_history, hdr_pcg_report* report);
+
+/* ------------------------------------------------------------ AMG / SGS
+ *
+ * Smoothed-aggregation AMG on the device (kern_amg.cu): amg_setup
+ * (src/amg.cpp:189-244) and amg_apply (one V(1,1) cycle, :248-271).  Every step
+ * with arithmetic rounds like the reference, so for the same matrix the levels
+ * (A, P, R) and every application are bit-identical to it; the greedy
+ * aggregate() pass runs on the host over the device-built strength graph. */
+typedef struct hdr_amg_s* hdr_amg_t;
+typedef struct hdr_amg_options { /* AmgOptions (include/hdivred/amg.hpp:12-19) */
+  double strength_threshold;     /* 0.08 */
+  double omega_factor;           /* 1.0 */
+  int64_t coarse_cap;            /* 64 */
+  int32_t max_levels;            /* 25 */
+  int32_t power_iterations;      /* 10 */
+  double stall_ratio;            /* 0.9 */
+} hdr_amg_options;
+void hdr_amg_default_options(hdr_amg_options* out);
+/* CSR (row_offsets n+1, col_indices, values; int64 indices) host (on_device = 0)
+ * or device arrays; options NULL = defaults.  HDR_SETUP_FAILED as SetupFailed,
+ * HDR_SINGULAR_BLOCK from the coarsest LU, HDR_CAP_EXCEEDED from its to_dense. */
+hdr_status hdr_amg_setup(int64_t n, const int64_t* row_offsets, const int64_t* col_indices, const double* values,
+                         int on_device, const hdr_amg_options* options, hdr_amg_t* out);
+/* levels (AmgHierarchy::levels.size()); sizes / nnz: levels + 1 entries (the
+ * level matrices, then the coarse matrix); NULL skips. */
+hdr_status hdr_amg_info(hdr_amg_t amg, int64_t* levels, int64_t* sizes, int64_t* nnz);
+/* which: 0 the level's matrix (level == levels: the coarse matrix), 1 its
+ * prolongator, 2 its restriction.  dims[3] = {nrows, ncols, nnz}; the arrays
+ * (host, NULL skips) must hold nrows + 1 / nnz / nnz entries. */
+hdr_status hdr_amg_level_matrix(hdr_amg_t amg, int64_t level, int which, int64_t* dims, int64_t* row_offsets,
+                                int64_t* col_indices, double* values);
+/* z = V-cycle(r), both n, host or device */
+hdr_status hdr_amg_apply(hdr_amg_t amg, const double* r, double* z, int on_device);
+void hdr_amg_destroy(hdr_amg_t amg);
+/* One application of the jacobi (kind 1) or sgs (kind 2) preconditioner of a
+ * host CSR matrix to r (host arrays), as the reference's Preconditioner::apply. */
+hdr_status hdr_csr_precond_apply_host(int64_t n, const int64_t* row_offsets, const int64_t* col_indices,
+                                      const double* values, int kind, const double* r, double* z);
 
 /* ------------------------------------------------------------ diagnostics
  *

@@ -12,6 +12,7 @@
 //   recover_hybrid        src/reduction.cpp:356   static_condense    src/reduction.cpp:448
 //   recover_condensed     src/reduction.cpp:559   spmv               src/csr.cpp:77
 //   element_matrices      src/rt_space.cpp:370    local_dof_map      src/rt_space.cpp:383
+//   amg_setup / amg_apply src/amg.cpp:189, 268    ssgs_setup / pcg   src/solvers.cpp:185, 109
 //
 // Input generation follows SURVEY.md §8(d): xorshift64 (tests/test_support.hpp:79-92
 // semantics), draw order per cell alpha then beta, then f_hat in broken order,
@@ -27,8 +28,10 @@
 #include <string>
 #include <vector>
 
+#include "hdivred/amg.hpp"
 #include "hdivred/csr.hpp"
 #include "hdivred/mesh.hpp"
+#include "hdivred/solvers.hpp"
 #include "hdivred/block_io.hpp"
 #include "hdivred/matrix_market.hpp"
 #include "hdivred/reduction.hpp"
@@ -239,6 +242,32 @@ int cmd_dump(const std::map<std::string, std::string>& kv) {
   if (kv.count("nullspace") && kv.at("nullspace") == "1" && in.c_mat.nrows * in.c_mat.nrows <= kDefaultDenseCap)
     w.d("nullspace", near_nullspace_check(sp, pb.coeffs, weighted));
   w.d("g", g);
+  // amg=1: the reduced solve of solve_reduction (src/driver.cpp:203-247) on H:
+  // the AMG hierarchy, one V-cycle and one SGS application on g, and pcg
+  // (rtol, maxit of RunConfig) with each preconditioner
+  if (kv.count("amg") && kv.at("amg") == "1" && hyb.h_mat.nrows > 0) {
+    const double rtol = kv.count("rtol") ? std::stod(kv.at("rtol")) : 1e-12;
+    const AmgHierarchy ah = amg_setup(hyb.h_mat);
+    w.q("amg.levels", {static_cast<index_t>(ah.levels.size())});
+    for (std::size_t l = 0; l < ah.levels.size(); ++l) {
+      w.csr("amg.A" + std::to_string(l), ah.levels[l].matrix);
+      w.csr("amg.P" + std::to_string(l), ah.levels[l].prolongator);
+      w.csr("amg.R" + std::to_string(l), ah.levels[l].restriction);
+    }
+    w.csr("amg.coarse", ah.coarse_matrix);
+    w.d("amg.z", amg_apply(ah, g));
+    std::vector<double> zs;
+    ssgs_setup(hyb.h_mat)->apply(g, zs);
+    w.d("sgs.z", zs);
+    const std::pair<const char*, std::unique_ptr<Preconditioner>> pcs[] = {
+        {"amg", amg_preconditioner(hyb.h_mat)}, {"sgs", ssgs_setup(hyb.h_mat)}, {"jacobi", jacobi_setup(hyb.h_mat)}};
+    for (const auto& [name, pc] : pcs) {
+      auto [sol, rep] = pcg(hyb.h_mat, pc.get(), g, rtol, 2000);
+      w.q(std::string("pcg.") + name + ".iterations", {rep.iterations});
+      w.d(std::string("pcg.") + name + ".residuals", rep.relative_residuals);
+      w.d(std::string("pcg.") + name + ".x", sol);
+    }
+  }
   std::vector<double> lambda(static_cast<std::size_t>(hyb.h_mat.nrows));
   for (auto& v : lambda) v = pb.rng.uniform(-1.0, 1.0);
   w.d("lambda", lambda);

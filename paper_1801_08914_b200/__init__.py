@@ -499,13 +499,14 @@ class CondensedOperator:
         return y
 
 
-_PRECOND = {None: 0, "none": 0, "jacobi": 1}
+# the reference's PrecondKind (include/hdivred/driver.hpp:15)
+_PRECOND = {None: 0, "none": 0, "jacobi": 1, "sgs": 2, "amg": 3}
 
 
 def _pcg_call(fn, handle, n, b, rtol, maxit, precond):
     """Shared driver of the device pcg entry points: returns (x, report)."""
     if precond not in _PRECOND:
-        raise ValueError("precond must be None, 'none' or 'jacobi' (the device pcg's options)")
+        raise ValueError("precond must be None, 'none', 'jacobi', 'sgs' or 'amg'")
     hist = np.zeros(int(maxit) + 1)
     rep = _capi.PcgReport()
     if b is None:
@@ -540,7 +541,7 @@ def pcg(a, b, rtol: float = 1e-10, maxit: int = 1000, precond: Optional[str] = "
     if nr != nc or b.size != nr:
         raise DimensionMismatch("pcg: matrix not square or rhs length")
     if precond not in _PRECOND:
-        raise ValueError("precond must be None, 'none' or 'jacobi'")
+        raise ValueError("precond must be None, 'none', 'jacobi', 'sgs' or 'amg'")
     x = np.empty(nr)
     hist = np.zeros(int(maxit) + 1)
     rep = _capi.PcgReport()
@@ -549,6 +550,71 @@ def pcg(a, b, rtol: float = 1e-10, maxit: int = 1000, precond: Optional[str] = "
     it = int(rep.iterations)
     return x, {"iterations": it, "converged": bool(rep.converged), "relative_residuals": hist[: it + 1].tolist(),
                "final_relative_residual": float(rep.final_relative_residual), "wall_time": rep.wall_ms * 1e-3}
+
+
+def _host_csr(a):
+    nr, nc, ro, ci, v = a
+    if nr != nc:
+        raise DimensionMismatch("matrix not square")
+    return (int(nr), np.ascontiguousarray(ro, np.int64), np.ascontiguousarray(ci, np.int64),
+            np.ascontiguousarray(v, np.float64))
+
+
+class AmgHierarchy:
+    """amg_setup (src/amg.cpp:189-244) on the device: levels (A, P, R) bit-identical
+    to the reference's for the same matrix; apply() is one V(1,1) cycle (amg_apply)."""
+
+    def __init__(self, a, **options):
+        n, ro, ci, v = _host_csr(a)
+        o = _capi.AmgOptions()
+        _lib().hdr_amg_default_options(ctypes.byref(o))
+        for k_, val in options.items():
+            setattr(o, k_, val)
+        h = ctypes.c_void_p()
+        _check(_lib().hdr_amg_setup(n, ro.ctypes.data, ci.ctypes.data, v.ctypes.data, 0, ctypes.byref(o),
+                                    ctypes.byref(h)))
+        self._h = h
+        self.n = n
+        lv = ctypes.c_int64()
+        _check(_lib().hdr_amg_info(self._h, ctypes.byref(lv), None, None))
+        self.nlevels = int(lv.value)
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            _lib().hdr_amg_destroy(self._h)
+            self._h = None
+
+    def matrix(self, level: int, which: str = "A"):
+        """(nrows, ncols, row_offsets, col_indices, values) of a level's A / P / R
+        (level == nlevels: the coarse matrix)."""
+        w = {"A": 0, "P": 1, "R": 2}[which]
+        dims = np.zeros(3, np.int64)
+        _check(_lib().hdr_amg_level_matrix(self._h, level, w, dims.ctypes.data, None, None, None))
+        ro = np.empty(dims[0] + 1, np.int64)
+        ci = np.empty(dims[2], np.int64)
+        v = np.empty(dims[2])
+        _check(_lib().hdr_amg_level_matrix(self._h, level, w, dims.ctypes.data, ro.ctypes.data,
+                                           ci.ctypes.data if dims[2] else None, v.ctypes.data if dims[2] else None))
+        return int(dims[0]), int(dims[1]), ro, ci, v
+
+    def apply(self, r) -> np.ndarray:
+        r = np.ascontiguousarray(r, np.float64)
+        if r.size != self.n:
+            raise DimensionMismatch("amg_apply: vector length")
+        z = np.empty(self.n)
+        _check(_lib().hdr_amg_apply(self._h, r.ctypes.data, z.ctypes.data, 0))
+        return z
+
+
+def precond_apply(a, r, kind: str = "sgs") -> np.ndarray:
+    """One application of the jacobi / sgs preconditioner of a host CSR matrix
+    (jacobi_setup / ssgs_setup, src/solvers.cpp:46-72), on the device."""
+    n, ro, ci, v = _host_csr(a)
+    r = np.ascontiguousarray(r, np.float64)
+    z = np.empty(n)
+    _check(_lib().hdr_csr_precond_apply_host(n, ro.ctypes.data, ci.ctypes.data, v.ctypes.data,
+                                             {"jacobi": 1, "sgs": 2}[kind], r.ctypes.data, z.ctypes.data))
+    return z
 
 
 # ------------------------------------------------------------------ reference-mirroring front-end
@@ -701,7 +767,7 @@ from . import algebraic  # noqa: E402  (ReductionInputs-level API; needs _check/
 from . import io  # noqa: E402  (instance I/O, host threads)
 
 __all__ = [
-    "algebraic", "io", "CapExceededError", "FormatError", "SingularBlockError", "ValidationError", "DimensionMismatch",
+    "algebraic", "io", "AmgHierarchy", "precond_apply", "SetupFailed", "CapExceededError", "FormatError", "SingularBlockError", "ValidationError", "DimensionMismatch",
     "UnsupportedError", "DeviceError", "Space", "HybridizedOperator", "CondensedOperator", "hybridized_matrix",
     "space_info", "coefficients_from_config", "space_from_config", "launch_count", "pcg", "__version__",
 ]

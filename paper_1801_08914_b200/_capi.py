@@ -29,6 +29,12 @@ class PcgReport(ctypes.Structure):
                 ("final_relative_residual", _d), ("wall_ms", _d)]
 
 
+class AmgOptions(ctypes.Structure):
+    """hdr_amg_options (AmgOptions, include/hdivred/amg.hpp:12-19)"""
+    _fields_ = [("strength_threshold", _d), ("omega_factor", _d), ("coarse_cap", _i64), ("max_levels", ctypes.c_int32),
+                ("power_iterations", ctypes.c_int32), ("stall_ratio", _d)]
+
+
 class AlgInputs(ctypes.Structure):
     """hdr_alg_inputs (include/hdivred_b200.h): a ReductionInputs as plain arrays."""
     _fields_ = [
@@ -111,6 +117,13 @@ _SIGS = {
     "hdr_io_write_vector_lines": (_i32, [ctypes.c_char_p, _i64, _vp, _i32]),
     "hdr_space_set_exact_policy": (_i32, [_vp, _i32, _d, _d, _vp]),
     "hdr_reference_div_form": (_i32, [_i32, _i32, _vp, _vp]),
+    "hdr_amg_default_options": (None, [_vp]),
+    "hdr_amg_setup": (_i32, [_i64, _vp, _vp, _vp, _i32, _vp, _vp]),
+    "hdr_amg_info": (_i32, [_vp, _vp, _vp, _vp]),
+    "hdr_amg_level_matrix": (_i32, [_vp, _i64, _i32, _vp, _vp, _vp, _vp]),
+    "hdr_amg_apply": (_i32, [_vp, _vp, _vp, _i32]),
+    "hdr_amg_destroy": (None, [_vp]),
+    "hdr_csr_precond_apply_host": (_i32, [_i64, _vp, _vp, _vp, _i32, _vp, _vp]),
     "hdr_near_nullspace_check": (_i32, [_vp, _vp, _vp, _i32, _i32, _i64, _vp]),
     "hdr_last_error": (ctypes.c_char_p, []),
     "hdr_version": (ctypes.c_char_p, []),

@@ -194,14 +194,14 @@ def read_dump(path) -> dict:
 
 
 def run_ref_dump(out_path, dim, cells, k, coef, seed, weighted=False, blocks=True, essential=False,
-                 nullspace=False) -> dict:
+                 nullspace=False, amg=False) -> dict:
     """Runs the reference (oracle/_ref/ref_harness) and reads its dump (essential:
     every boundary face eliminated first, eliminate_essential)."""
     if not REF_HARNESS.exists():
         raise FileNotFoundError(REF_HARNESS)
     args = [str(REF_HARNESS), "dump", f"out={out_path}", f"dim={dim}", "cells=" + ",".join(map(str, cells)),
             f"k={k}", f"coef={coef}", f"seed={seed}", f"weighted={int(weighted)}", f"blocks={int(blocks)}",
-            f"essential={int(essential)}", f"nullspace={int(nullspace)}"]
+            f"essential={int(essential)}", f"nullspace={int(nullspace)}", f"amg={int(amg)}"]
     subprocess.run(args, check=True, env={**os.environ, "HDIVRED_NUM_THREADS": "1"})
     return read_dump(out_path)
 
