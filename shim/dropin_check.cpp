@@ -7,6 +7,7 @@
 #include <cstdlib>
 #include <string>
 
+#include "hdivred/amg.hpp"
 #include "hdivred/reduction.hpp"
 #include "hdivred/solvers.hpp"
 #include "hdivred_b200_shim.hpp"
@@ -31,6 +32,15 @@ std::vector<double> solve_condensation(const ReductionInputs& inputs, CondFn con
   auto [x_b, rep] = pcg(cond.s_mat, pc.get(), f_s, 1e-12, 5000);
   *its = rep.iterations;
   return recover_condensed(cond, x_b, inputs.f_hat);
+}
+// the same sequence with run_pcg's make_preconditioner + pcg replaced by the
+// device solve on the device-resident H (default preconditioner: amg)
+template <class HybFn, class PcgFn>
+std::vector<double> solve_hybridization_pc(const ReductionInputs& inputs, HybFn hyb_fn, PcgFn pcg_fn, index_t* its) {
+  const auto [hyb, g] = hyb_fn(inputs);
+  auto [lambda, rep] = pcg_fn(hyb, g);
+  *its = rep.iterations;
+  return recover_hybrid(hyb, lambda, inputs.f_hat).second;
 }
 }  // namespace hdivred
 
@@ -120,6 +130,29 @@ int main(int argc, char** argv) {
       in, [](const ReductionInputs& r) { return hdivred_b200::static_condense(r); }, &itc_alg);
   const std::vector<double> xsc_fe = solve_condensation(
       in, [&](const ReductionInputs& r) { return hdivred_b200::static_condense(sp, co, r.f_hat); }, &itc_fe);
+  // AMG-preconditioned solve: the reference's (host amg_setup + pcg) and the
+  // device one on the FE operator's device-resident H
+  index_t ita_ref = 0, ita_fe = 0;
+  const std::vector<double> xa_ref = solve_hybridization_pc(
+      in, [](const ReductionInputs& r) { return hybridize(r); },
+      [](const HybridizedOperator& h, const std::vector<double>& g) {
+        const std::unique_ptr<Preconditioner> pc = amg_preconditioner(h.h_mat);
+        return pcg(h.h_mat, pc.get(), g, 1e-12, 2000);
+      },
+      &ita_ref);
+  const std::vector<double> xa_fe = solve_hybridization_pc(
+      in, [&](const ReductionInputs& r) { return hdivred_b200::hybridize(sp, co, r.f_hat); },
+      [](const hdivred_b200::FeHybridized& h, const std::vector<double>& g) {
+        return hdivred_b200::pcg(h, PrecondKind::amg, g, 1e-12, 2000);
+      },
+      &ita_fe);
+  // the device pcg on the reference's own H (host CsrMatrix in, device solve)
+  const std::unique_ptr<Preconditioner> pc_ref = amg_preconditioner(ref.h_mat);
+  const auto ref_solve = pcg(ref.h_mat, pc_ref.get(), g_ref, 1e-12, 2000);
+  const auto dev_solve = hdivred_b200::pcg(ref.h_mat, PrecondKind::amg, g_ref, 1e-12, 2000);
+  // near_nullspace_check, bit-identical (small meshes: dense m x m)
+  bool ns_identical = true;
+  if (ref.h_mat.nrows <= 600) ns_identical = near_nullspace_check(sp, co) == hdivred_b200::near_nullspace_check(sp, co);
   const std::vector<double> y_ref = spmv(ref.h_mat, g_ref);
   const std::vector<double> y_gpu = hdivred_b200::spmv(ref.h_mat, g_ref);
   std::printf("{\"n\": %d, \"k\": %d, \"h_pattern_identical\": %s, \"h_rel\": %.3e, \"g_rel\": %.3e, "
@@ -128,7 +161,9 @@ int main(int argc, char** argv) {
               "\"alg_x_hat_rel\": %.3e, \"alg_x_rel\": %.3e, \"alg_s_pattern_identical\": %s, \"alg_s_rel\": %.3e, "
               "\"alg_f_s_rel\": %.3e, \"alg_x_cond_rel\": %.3e, \"fe_x_hat_rel\": %.3e, \"fe_x_rel\": %.3e, "
               "\"fe_x_cond_rel\": %.3e, \"solve_hyb_alg_rel\": %.3e, \"solve_hyb_fe_rel\": %.3e, "
-              "\"solve_cond_alg_rel\": %.3e, \"solve_cond_fe_rel\": %.3e, \"pcg_iterations\": [%lld, %lld, %lld, %lld, %lld, %lld]}\n",
+              "\"solve_cond_alg_rel\": %.3e, \"solve_cond_fe_rel\": %.3e, \"pcg_iterations\": [%lld, %lld, %lld, %lld, %lld, %lld], "
+              "\"amg_iterations\": [%lld, %lld], \"solve_amg_fe_rel\": %.3e, \"amg_ref_matrix_iterations\": [%lld, %lld], "
+              "\"amg_ref_matrix_x_rel\": %.3e, \"nullspace_identical\": %s}\n",
               n, k, pattern ? "true" : "false", dh / mh, dg / (mg > 0 ? mg : 1), spat ? "true" : "false", ds / ms,
               y_ref == y_gpu ? "true" : "false", apat ? "true" : "false", asym ? "true" : "false",
               rel(ref.h_mat.values, ahyb.h_mat.values), rel(g_ref, g_alg), rel(xh_ref, xh_alg), rel(x_ref, x_alg),
@@ -136,6 +171,9 @@ int main(int argc, char** argv) {
               rel(xc_ref, xc_alg), rel(xh_ref, xh_fe), rel(x_ref, x_fe), rel(xc_ref, xc_fe), rel(xs_ref, xs_alg),
               rel(xs_ref, xs_fe), rel(xsc_ref, xsc_alg), rel(xsc_ref, xsc_fe), static_cast<long long>(it_ref),
               static_cast<long long>(it_alg), static_cast<long long>(it_fe), static_cast<long long>(itc_ref),
-              static_cast<long long>(itc_alg), static_cast<long long>(itc_fe));
-  return (pattern && spat && y_ref == y_gpu && apat && asym && acpat) ? 0 : 1;
+              static_cast<long long>(itc_alg), static_cast<long long>(itc_fe), static_cast<long long>(ita_ref),
+              static_cast<long long>(ita_fe), rel(xa_ref, xa_fe), static_cast<long long>(ref_solve.second.iterations),
+              static_cast<long long>(dev_solve.second.iterations), rel(ref_solve.first, dev_solve.first),
+              ns_identical ? "true" : "false");
+  return (pattern && spat && y_ref == y_gpu && apat && asym && acpat && ns_identical) ? 0 : 1;
 }

@@ -304,4 +304,62 @@ std::vector<double> spmv(const hdivred::CsrMatrix& a, const std::vector<double>&
   return y;
 }
 
+namespace {
+int precond_code(hdivred::PrecondKind p) {
+  switch (p) {
+    case hdivred::PrecondKind::none: return 0;
+    case hdivred::PrecondKind::jacobi: return 1;
+    case hdivred::PrecondKind::sgs: return 2;
+    case hdivred::PrecondKind::amg: return 3;
+  }
+  return 0;
+}
+
+hdivred::PcgReport to_report(const hdr_pcg_report& r, const std::vector<double>& hist) {
+  hdivred::PcgReport out;
+  out.iterations = r.iterations;
+  out.converged = r.converged != 0;
+  out.relative_residuals.assign(hist.begin(), hist.begin() + static_cast<std::ptrdiff_t>(r.iterations) + 1);
+  out.wall_time = r.wall_ms * 1e-3;
+  return out;
+}
+}  // namespace
+
+std::pair<std::vector<double>, hdivred::PcgReport> pcg(const hdivred::CsrMatrix& a, hdivred::PrecondKind precond,
+                                                       const std::vector<double>& b, double rtol,
+                                                       hdivred::index_t maxit) {
+  if (a.nrows != a.ncols) throw std::invalid_argument("pcg: matrix not square");
+  if (static_cast<hdivred::index_t>(b.size()) != a.nrows) throw hdivred::DimensionMismatch("pcg: rhs length");
+  std::vector<double> x(b.size()), hist(static_cast<size_t>(maxit) + 1, 0.0);
+  hdr_pcg_report rep{};
+  check(hdr_csr_pcg_host(a.nrows, a.row_offsets.data(), a.col_indices.data(), a.values.data(), b.data(), x.data(),
+                         rtol, maxit, precond_code(precond), hist.data(), &rep));
+  return {std::move(x), to_report(rep, hist)};
+}
+
+std::pair<std::vector<double>, hdivred::PcgReport> pcg(const FeHybridized& op, hdivred::PrecondKind precond,
+                                                       const std::vector<double>& b, double rtol,
+                                                       hdivred::index_t maxit) {
+  if (!op.device) throw std::invalid_argument("pcg: operator without device state");
+  if (static_cast<hdivred::index_t>(b.size()) != op.h_mat.nrows) throw hdivred::DimensionMismatch("pcg: rhs length");
+  std::vector<double> x(b.size()), hist(static_cast<size_t>(maxit) + 1, 0.0);
+  hdr_pcg_report rep{};
+  check(hdr_hybrid_pcg(static_cast<hdr_hybrid_t>(op.device.get()), b.data(), x.data(), 0, rtol, maxit,
+                       precond_code(precond), hist.data(), &rep));
+  return {std::move(x), to_report(rep, hist)};
+}
+
+std::vector<double> near_nullspace_check(const hdivred::RtSpace& space, const hdivred::CellCoefficients& coeffs,
+                                         bool weighted, hdivred::index_t dense_cap) {
+  if (static_cast<hdivred::index_t>(coeffs.alpha.size()) != space.mesh.ncells() ||
+      static_cast<hdivred::index_t>(coeffs.beta.size()) != space.mesh.ncells())
+    throw hdivred::DimensionMismatch("near_nullspace_check: coefficient count");
+  SpacePtr s = make_space(space);
+  const auto in = info(s.get());
+  std::vector<double> ev(static_cast<size_t>(in[HDR_INFO_M]));
+  check(hdr_near_nullspace_check(s.get(), coeffs.alpha.data(), coeffs.beta.data(), 0, weighted ? 1 : 0, dense_cap,
+                                 ev.empty() ? nullptr : ev.data()));
+  return ev;
+}
+
 }  // namespace hdivred_b200

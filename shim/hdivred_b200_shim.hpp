@@ -18,6 +18,8 @@
 #include "hdivred/mesh.hpp"
 #include "hdivred/reduction.hpp"
 #include "hdivred/rt_space.hpp"
+#include "hdivred/driver.hpp"
+#include "hdivred/solvers.hpp"
 
 namespace hdivred_b200 {
 
@@ -88,6 +90,22 @@ std::pair<AlgCondensed, std::vector<double>> static_condense(const hdivred::Redu
 // recover_condensed(op, x_b, f_hat)            reduction.hpp:101-102, reduction.cpp:559-587
 std::vector<double> recover_condensed(const AlgCondensed& op, const std::vector<double>& x_b,
                                       const std::vector<double>& f_hat);
+
+// ---- the reduced solve on the device (run_pcg in src/driver.cpp:220-231:
+// make_preconditioner + pcg, src/solvers.cpp:109-163).  All four PrecondKind
+// values; amg / sgs apply bit-identically to the reference's on the same matrix
+// (kern_amg.cu).  Same checks and exceptions as the reference's pcg.
+std::pair<std::vector<double>, hdivred::PcgReport> pcg(const hdivred::CsrMatrix& a, hdivred::PrecondKind precond,
+                                                       const std::vector<double>& b, double rtol,
+                                                       hdivred::index_t maxit);
+// on a device-resident H (no upload of the matrix)
+std::pair<std::vector<double>, hdivred::PcgReport> pcg(const FeHybridized& op, hdivred::PrecondKind precond,
+                                                       const std::vector<double>& b, double rtol,
+                                                       hdivred::index_t maxit);
+
+// near_nullspace_check (src/reduction.cpp:711-742) on the device, bit-identical.
+std::vector<double> near_nullspace_check(const hdivred::RtSpace& space, const hdivred::CellCoefficients& coeffs,
+                                         bool weighted = false, hdivred::index_t dense_cap = hdivred::kDefaultDenseCap);
 
 // spmv (src/csr.cpp:77-87) on the device, bit-identical to the reference.
 std::vector<double> spmv(const hdivred::CsrMatrix& a, const std::vector<double>& x);

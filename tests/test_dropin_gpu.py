@@ -40,4 +40,11 @@ def test_dropin_against_reference(n, k):
     # reference's x to the accuracy of its H (~1e-9) times the conditioning of H
     assert line["solve_hyb_alg_rel"] < 1e-6 and line["solve_hyb_fe_rel"] < 1e-6, line
     assert line["solve_cond_alg_rel"] < 1e-6 and line["solve_cond_fe_rel"] < 1e-6, line
+    # the default reduced solve (amg) on the device: on the device-resident H and on
+    # the reference's own H (where every V-cycle is bit-identical to the reference's)
+    ia_ref, ia_fe = line["amg_iterations"]
+    assert abs(ia_ref - ia_fe) <= 1 and line["solve_amg_fe_rel"] < 1e-6, line
+    ir_ref, ir_dev = line["amg_ref_matrix_iterations"]
+    assert abs(ir_ref - ir_dev) <= 1 and line["amg_ref_matrix_x_rel"] < 1e-8, line
+    assert line["nullspace_identical"], line
     print(line)
