@@ -398,7 +398,7 @@ hdr_status hdr_space_create(int dim, const int64_t cells[3], const double h[3], 
     fx.lam = fx.X + static_cast<size_t>(n) * r;
     fx.r = r;
     fx.rho = sp->st.rho;
-    if (dim == 3 && order >= 2) {
+    if (dim == 3 && order >= 1) {  // [N0 ; X^T] of the batched pre-GEMM (RT1..RT3 hexes)
       const int npr = n + r;
       std::vector<double> pm(static_cast<size_t>(npr) * n);
       for (int l = 0; l < n; ++l)
@@ -407,6 +407,8 @@ hdr_status hdr_space_create(int dim, const int64_t cells[3], const double h[3], 
               row < n ? sp->st.N0[static_cast<size_t>(row) * n + l] : sp->st.X[static_cast<size_t>(l) * r + (row - n)];
       sp->premat.alloc(pm.size());
       CK(cudaMemcpyAsync(sp->premat.p, pm.data(), pm.size() * 8, cudaMemcpyHostToDevice, st));
+    }
+    if (dim == 3 && order >= 2) {
       // chunk-ordered Delta tables of the tensor-core correction (kern_cta.cu)
       // entry order = the kernel's (chunk, iteration i, thread) order, thread
       // (warp w, lane l) -> row 8 (g / 4) + l / 4, column 16 c + 4 (g % 4) + l % 4, g = w + 16 i
@@ -744,7 +746,14 @@ static hdr_status run_hybridize(hdr_hybrid_t op, const double* alpha, const doub
         op->ws.alloc(static_cast<size_t>(need));
         op->ws_doubles = need;
       }
-      for (int parity = 0; parity < 2; ++parity) launch_hybridize_warp(A, parity, op->ws.p, st);
+      const double* pre = nullptr;
+      if (sp->dim == 3 && sp->premat.p) {  // [N0 f ; X^T f] for every cell, one batched fp64 GEMM
+        const int npr = sp->n + sp->r;
+        if (!op->pre.p || op->pre.n < static_cast<size_t>(npr) * sp->ncells) op->pre.alloc(static_cast<size_t>(npr) * sp->ncells);
+        launch_gemm_f64_nn(npr, static_cast<int>(sp->ncells), sp->n, sp->premat.p, npr, df, sp->n, op->pre.p, npr, st);
+        pre = op->pre.p;
+      }
+      for (int parity = 0; parity < 2; ++parity) launch_hybridize_warp(A, parity, op->ws.p, pre, st);
     } else {
       return fail(HDR_UNSUPPORTED, "hybridize: no structured kernel for this dim / order");
     }

@@ -62,10 +62,16 @@ __device__ __forceinline__ void gsync() {
 template <int DIM, int K>
 struct WarpSmem {
   using S = Shape<DIM, K>;
-  static constexpr int NCP = (S::NC + 3) & ~3;  // padded row length of [V | w] and Y
-  float d32t[S::N * S::N];     // Delta32 transposed: d32t[l * N + i] = Delta_il; then C = V_F^T Y (NF x NCP)
-  float v32[S::N * NCP];       // [V | w] row-major (fp32 operand)
-  float y32[S::N * NCP];       // Y = Delta V
+  // RT1 hexes: the correction GEMMs on the tensor cores (mma.sync m16n8k8, 3xTF32):
+  // operands padded to 40 x 40 (K and M multiples of 8 / 16, zero pads), row
+  // strides of 40 floats so every fragment load hits 32 distinct banks
+  static constexpr bool MMA = DIM == 3 && K == 1;
+  static constexpr int NCP = MMA ? 40 : (S::NC + 3) & ~3;  // padded row length of [V | w] and Y
+  static constexpr int NR = S::N;                           // rows of V32 / Y (the MMA's K pad is masked)
+  static constexpr int DT = MMA ? 40 : S::N;                // row stride of Delta32^T
+  float d32t[NR * DT];         // Delta32 transposed: d32t[l * DT + i] = Delta_il; then C = V_F^T Y (NF x NCP)
+  float v32[NR * NCP];         // [V | w] row-major (fp32 operand)
+  float y32[NR * NCP];         // Y = Delta V
   double vf[S::NF * S::NC];    // fp64 face rows of [V | w]: H0 and g0
   double z[S::R * S::NC];      // z[j][c] = s_j X_F_c,j (c < NF), s_j (X^T f)_j (c = NF)
   double f[S::N];              // f_T
@@ -226,17 +232,113 @@ __device__ __forceinline__ void gemm44h(const float* at, int lda, const float* b
         }
 }
 
+// x = hi + lo with hi, lo tf32 (cvt.rna: the tensor core reads the top 19 bits; x - hi is exact in fp32)
+__device__ __forceinline__ void tf32_split(float x, uint32_t& hi, uint32_t& lo) {
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(hi) : "f"(x));
+  const float r = x - __uint_as_float(hi);
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(lo) : "f"(r));
+}
+
+// d += a b on the tensor cores (m16n8k8, tf32 inputs, fp32 accumulate)
+__device__ __forceinline__ void mma_tf32(float (&d)[4], const uint32_t (&a)[4], const uint32_t (&b)[2]) {
+  asm volatile("mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+               : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+               : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
+}
+
+// 3xTF32 (fp32-accurate: the lo * lo term is below fp32 rounding): small terms first
+__device__ __forceinline__ void mma_3xtf32(float (&d)[4], const float (&a)[4], const float (&b)[2]) {
+  uint32_t ah[4], al[4], bh[2], bl[2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) tf32_split(a[i], ah[i], al[i]);
+  tf32_split(b[0], bh[0], bl[0]);
+  tf32_split(b[1], bh[1], bl[1]);
+  mma_tf32(d, al, bh);
+  mma_tf32(d, ah, bl);
+  mma_tf32(d, ah, bh);
+}
+
+// RT1 hexes: first-order correction on the tensor cores, four warps per cell.
+// Warp w owns columns [8w, 8w + 8) of Y = Delta32 [V | w] (three m16 tiles, five
+// k8 steps) and of C = V_F^T Y (two m16 tiles): C's B operand is the warp's own
+// Y columns, so only a warp barrier separates the two products.  C stays in
+// registers until the whole group has finished reading Delta32 (C's storage).
+// The K pad (rows 36..39 of the last k8 step) is masked to zero in the
+// fragments; rows / columns beyond the operands' extents only feed output rows
+// and columns that are never stored.
+template <class SM, int N, int NF, int NC, int NINT, int GT>
+__device__ __forceinline__ void correction_mma(SM& sm, float* corr, int tid) {
+  constexpr int NCP = SM::NCP, DT = SM::DT;
+  const int w = tid >> 5, l32 = tid & 31, g = l32 >> 2, t = l32 & 3, n0 = 8 * w;
+  float acc[3][4];
+#pragma unroll
+  for (int mt = 0; mt < 3; ++mt)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) acc[mt][i] = 0.f;
+#pragma unroll
+  for (int k0 = 0; k0 < N; k0 += 8) {
+    const bool k1ok = k0 + t + 4 < N;  // the first half (k0 + t) is always < N: N % 8 == 4
+    const float b[2] = {sm.v32[(k0 + t) * NCP + n0 + g], k1ok ? sm.v32[(k0 + t + 4) * NCP + n0 + g] : 0.f};
+#pragma unroll
+    for (int mt = 0; mt < 3; ++mt) {
+      const int m0 = 16 * mt;
+      const float a[4] = {sm.d32t[(k0 + t) * DT + m0 + g], sm.d32t[(k0 + t) * DT + m0 + g + 8],
+                          k1ok ? sm.d32t[(k0 + t + 4) * DT + m0 + g] : 0.f,
+                          k1ok ? sm.d32t[(k0 + t + 4) * DT + m0 + g + 8] : 0.f};
+      mma_3xtf32(acc[mt], a, b);
+    }
+  }
+#pragma unroll
+  for (int mt = 0; mt < 3; ++mt) {
+    const int r0 = 16 * mt + g, r1 = r0 + 8;
+    if (r0 < N) *reinterpret_cast<float2*>(sm.y32 + r0 * NCP + n0 + 2 * t) = make_float2(acc[mt][0], acc[mt][1]);
+    if (r1 < N) *reinterpret_cast<float2*>(sm.y32 + r1 * NCP + n0 + 2 * t) = make_float2(acc[mt][2], acc[mt][3]);
+  }
+  __syncwarp();
+  float cacc[2][4];
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) cacc[mt][i] = 0.f;
+#pragma unroll
+  for (int k0 = 0; k0 < N; k0 += 8) {
+    const bool k1ok = k0 + t + 4 < N;
+    const float b[2] = {sm.y32[(k0 + t) * NCP + n0 + g], k1ok ? sm.y32[(k0 + t + 4) * NCP + n0 + g] : 0.f};
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt) {
+      const int m0 = 16 * mt;  // A = V_F^T: A(p, k) = V(k, p), V_F = A0^-1 E_F the first NF columns
+      const float a[4] = {sm.v32[(k0 + t) * NCP + m0 + g], sm.v32[(k0 + t) * NCP + m0 + g + 8],
+                          k1ok ? sm.v32[(k0 + t + 4) * NCP + m0 + g] : 0.f,
+                          k1ok ? sm.v32[(k0 + t + 4) * NCP + m0 + g + 8] : 0.f};
+      mma_3xtf32(cacc[mt], a, b);
+    }
+  }
+  gsync<GT>();  // the group has finished reading Delta32 (C is stored over it)
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt) {
+    const int p0 = 16 * mt + g, p1 = p0 + 8, c0 = n0 + 2 * t;
+    if (p0 < NF) {
+      if (c0 < NC) corr[p0 * NCP + c0] = cacc[mt][0];
+      if (c0 + 1 < NC) corr[p0 * NCP + c0 + 1] = cacc[mt][1];
+    }
+    if (p1 < NF) {
+      if (c0 < NC) corr[p1 * NCP + c0] = cacc[mt][2];
+      if (c0 + 1 < NC) corr[p1 * NCP + c0 + 1] = cacc[mt][3];
+    }
+  }
+}
+
 // per-warp global scratch: the higher-order buffers T (N x NCP fp32) and Delta32 (N x N), rarely used
 template <int DIM, int K>
 constexpr int64_t scratch_doubles_per_warp() {
   using S = Shape<DIM, K>;
   constexpr int NCP = WarpSmem<DIM, K>::NCP;
-  return (S::N * NCP + S::N * S::N + 1) / 2 + 8;  // T, then a Delta32 copy for orders >= 2
+  return (WarpSmem<DIM, K>::NR * NCP + S::N * S::N + 1) / 2 + 8;  // T, then a Delta32 copy for orders >= 2
 }
 
 template <int DIM, int K>
 __device__ __forceinline__ void warp_cell(const HybArgs& A, int e, int parity, int lane, WarpSmem<DIM, K>& sm,
-                                          const CtaShared<DIM, K>& cs, double* scratch) {
+                                          const CtaShared<DIM, K>& cs, double* scratch, const double* pre) {
   constexpr int GT = Group<DIM, K>::GT;  // "lane" is the thread index within the cell's group
   using S = Shape<DIM, K>;
   using SM = WarpSmem<DIM, K>;
@@ -246,34 +348,88 @@ __device__ __forceinline__ void warp_cell(const HybArgs& A, int e, int parity, i
   float* tbuf = reinterpret_cast<float*>(scratch);  // N x NCP
   const double a = A.alpha[e], b = A.beta[e];
   const double ib = 1.0 / b;
-  const double* fe = A.f + static_cast<int64_t>(e) * N;
-  for (int i = lane; i < N; i += GT) sm.f[i] = fe[i];
+  constexpr int NS = 2 * DIM;
+  int cc[3];
+  unsigned lo = 0, hi = 0;
+  {
+    const uint32_t r0 = A.m.div_n0.div(static_cast<uint32_t>(e));
+    cc[0] = static_cast<int>(static_cast<uint32_t>(e) - r0 * static_cast<uint32_t>(A.m.N[0]));
+    const uint32_t z2 = A.m.div_n1.div(r0);
+    cc[1] = static_cast<int>(r0 - z2 * static_cast<uint32_t>(A.m.N[1]));
+    cc[2] = static_cast<int>(z2);
+#pragma unroll
+    for (int x = 0; x < DIM; ++x) {
+      const int cx = x == 0 ? cc[0] : (x == 1 ? cc[1] : cc[2]);
+      const int Nx = static_cast<int>(x == 0 ? A.m.N[0] : (x == 1 ? A.m.N[1] : A.m.N[2]));
+      lo |= static_cast<unsigned>(cx > 0) << x;
+      hi |= static_cast<unsigned>(cx + 1 < Nx) << x;
+    }
+  }
+  // scatter tables of the cell (row starts / lengths of each face slot, column-block
+  // ranks): their global loads are issued now, their latency hides behind the solve
+  for (int idx = lane; idx < NS * NS; idx += GT) {
+    const int ps = idx / NS, qs = idx - ps * NS;
+    const int a_ = ps >> 1;
+    const bool pin = (((ps & 1) ? hi : lo) >> a_) & 1u;
+    const bool qin = (((qs & 1) ? hi : lo) >> (qs >> 1)) & 1u;
+    const int ca = a_ == 0 ? cc[0] : (a_ == 1 ? cc[1] : cc[2]);
+    const int na = static_cast<int>(a_ == 0 ? A.m.N[0] : (a_ == 1 ? A.m.N[1] : A.m.N[2]));
+    sm.rank[idx] = (pin && qin) ? col_rank_fast(DIM, ps, qs, lo, hi, ca, na, false) : -1;
+    if (qs == 0) {
+      const int side = ps & 1;
+      if (pin) {
+        const int face = face_id32(A.m, a_, cc[0] + (a_ == 0 ? side : 0), cc[1] + (a_ == 1 ? side : 0),
+                                   cc[2] + (a_ == 2 ? side : 0));
+        const int row = A.mbase[face];
+        const int64_t r0s = A.rowoff[row];
+        sm.rstart[ps] = r0s;
+        sm.rlen[ps] = static_cast<int>(A.rowoff[row + 1] - r0s);
+        sm.grow[ps] = row;
+      } else {
+        sm.rstart[ps] = -1;
+      }
+    }
+  }
   for (int j = lane; j < R; j += GT) sm.s[j] = b / fma(a, __ldg(fx.lam + j), b);
-  gsync<GT>();
-  // nf = N0 f: each row's dot product split over 4 consecutive lanes (l = part mod 4)
-  for (int i0 = 0; i0 < N; i0 += GT / 4) {
-    const int i = i0 + (lane >> 2), part = lane & 3;
-    double acc = 0.0;
-    if (i < N)
+  if (pre) {
+    // [N0 f ; X^T f] of every cell from one batched fp64 GEMM before the launch
+    const double* pe = pre + static_cast<int64_t>(e) * (N + R);
+    for (int i = lane; i < N; i += GT) sm.nf[i] = pe[i];
+    gsync<GT>();
+    for (int idx = lane; idx < R * NF; idx += GT) {
+      const int j = idx / NF, c = idx - j * NF;
+      sm.z[j * NC + c] = sm.s[j] * cs.xt[j * N + NINT + c];
+    }
+    for (int j = lane; j < R; j += GT) sm.z[j * NC + NF] = sm.s[j] * pe[N + j];
+  } else {
+    const double* fe = A.f + static_cast<int64_t>(e) * N;
+    for (int i = lane; i < N; i += GT) sm.f[i] = fe[i];
+    gsync<GT>();
+    // nf = N0 f: each row's dot product split over 4 consecutive lanes (l = part mod 4)
+    for (int i0 = 0; i0 < N; i0 += GT / 4) {
+      const int i = i0 + (lane >> 2), part = lane & 3;
+      double acc = 0.0;
+      if (i < N)
 #pragma unroll 3
-      for (int l = part; l < N; l += 4) acc = fma(__ldg(fx.N0 + i * N + l), sm.f[l], acc);
-    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
-    acc += __shfl_xor_sync(0xffffffffu, acc, 2);
-    if (i < N && part == 0) sm.nf[i] = acc;
-  }
-  // z = [s X_F^T | s X^T f]; the X^T f dots are split over 4 lanes each
-  for (int idx = lane; idx < R * NF; idx += GT) {
-    const int j = idx / NF, c = idx - j * NF;
-    sm.z[j * NC + c] = sm.s[j] * cs.xt[j * N + NINT + c];
-  }
-  for (int j0 = 0; j0 < R; j0 += GT / 4) {
-    const int j = j0 + (lane >> 2), part = lane & 3;
-    double acc = 0.0;
-    if (j < R)
-      for (int l = part; l < N; l += 4) acc = fma(cs.xt[j * N + l], sm.f[l], acc);
-    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
-    acc += __shfl_xor_sync(0xffffffffu, acc, 2);
-    if (j < R && part == 0) sm.z[j * NC + NF] = sm.s[j] * acc;
+        for (int l = part; l < N; l += 4) acc = fma(__ldg(fx.N0 + i * N + l), sm.f[l], acc);
+      acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+      acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+      if (i < N && part == 0) sm.nf[i] = acc;
+    }
+    // z = [s X_F^T | s X^T f]; the X^T f dots are split over 4 lanes each
+    for (int idx = lane; idx < R * NF; idx += GT) {
+      const int j = idx / NF, c = idx - j * NF;
+      sm.z[j * NC + c] = sm.s[j] * cs.xt[j * N + NINT + c];
+    }
+    for (int j0 = 0; j0 < R; j0 += GT / 4) {
+      const int j = j0 + (lane >> 2), part = lane & 3;
+      double acc = 0.0;
+      if (j < R)
+        for (int l = part; l < N; l += 4) acc = fma(cs.xt[j * N + l], sm.f[l], acc);
+      acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+      acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+      if (j < R && part == 0) sm.z[j * NC + NF] = sm.s[j] * acc;
+    }
   }
   gsync<GT>();
   // [V | w] = (base + X z) / beta, base = N0_:,F | N0 f: register tiles over (rows, cols),
@@ -316,7 +472,7 @@ __device__ __forceinline__ void warp_cell(const HybArgs& A, int e, int parity, i
   // Delta32^T (fp64 exact rounding errors -> fp32)
   // (transposed input tables: contiguous loads and stores; alpha E + beta Ma in fp32)
   const float af = static_cast<float>(a), bfl = static_cast<float>(b);
-  auto fill_delta = [&](float* dst) {
+  auto fill_delta = [&](float* dst, int ld) {
     for (int idx = lane; idx < N * N; idx += GT) {
       const double2 dm = __ldg(fx.tdm + idx);
       const float2 em = __ldg(fx.tem + idx);
@@ -324,18 +480,21 @@ __device__ __forceinline__ void warp_cell(const HybArgs& A, int e, int parity, i
       two_prod(a, dm.x, p1, e1);
       two_prod(b, dm.y, p2, e2);
       two_sum(p1, p2, s_, e3);
-      dst[idx] = fmaf(af, em.x, fmaf(bfl, em.y, static_cast<float>(-((e1 + e2) + e3))));
+      const int l = idx / N, i = idx - l * N;  // entry (i, l), stored transposed
+      dst[l * ld + i] = fmaf(af, em.x, fmaf(bfl, em.y, static_cast<float>(-((e1 + e2) + e3))));
     }
   };
-  fill_delta(sm.d32t);
+  fill_delta(sm.d32t, SM::DT);
   gsync<GT>();
   // first order: Y = Delta32 [V | w];  C = V_F^T Y, C over Delta32's storage (dead
   // after Y: fewer bytes per cell group, more groups per SM; orders >= 2 regenerate
   // Delta32 in the global scratch)
-  static_assert(NF * NCP <= N * N, "C fits Delta32's storage");
+  static_assert(NF * NCP <= SM::NR * SM::DT, "C fits Delta32's storage");
   float* corr = sm.d32t;
   float* dglob = tbuf + N * NCP;
-  if constexpr (GT == 128) {
+  if constexpr (SM::MMA) {
+    correction_mma<SM, N, NF, NC, NINT, GT>(sm, corr, lane);
+  } else if constexpr (GT == 128) {
     gemm44h<N, NC, N, GT>(sm.d32t, N, sm.v32, NCP, sm.y32, NCP, lane);
     gsync<GT>();
     gemm44h<NF, NC, N, GT>(sm.v32, NCP, sm.y32, NCP, corr, NCP, lane);
@@ -372,7 +531,7 @@ __device__ __forceinline__ void warp_cell(const HybArgs& A, int e, int parity, i
   // order control and acceptance (hdr_device.cuh struct_order); a rejected cell
   // contributes zeros here and is solved on the exact path (kern_exact.cu)
   bool exact = false;
-  int P = struct_order(ratio, A.p_max, A.eps32, exact);
+  int P = struct_order(ratio, A.p_max, SM::MMA ? A.eps_tc : A.eps32, exact);  // 3xTF32: eps_tc
   exact = exact || A.force_exact;
   if (exact) P = 1;
   if (lane == 0) {
@@ -381,7 +540,7 @@ __device__ __forceinline__ void warp_cell(const HybArgs& A, int e, int parity, i
   }
   // higher orders (rare): T = A0^-1 Y, Y <- Delta32 T, C += (-1)^(p+1) V_F^T Y (C is subtracted)
   if (P >= 2) {
-    fill_delta(dglob);
+    fill_delta(dglob, N);
     gsync<GT>();
   }
   for (int p = 2; p <= P; ++p) {
@@ -405,50 +564,8 @@ __device__ __forceinline__ void warp_cell(const HybArgs& A, int e, int parity, i
     warp_gemm<NF, NC, N, TL::C_M, TL::C_N, GT>(sm.v32, NCP, sm.y32, NCP, corr, NCP, lane, (p & 1) ? 1.f : -1.f, true);
     gsync<GT>();
   }
-  // scatter: H_pc = V_F(p, c) (fp64) - C_pc ; g_p = w_F(p) - C_p,NF.  Per-cell tables
-  // (row starts / lengths of each face slot, column-block ranks) first, then one
-  // cheap position per entry; consecutive lanes write consecutive columns.
-  constexpr int NS = 2 * DIM;
-  {
-    int cc[3];
-    const uint32_t r0 = A.m.div_n0.div(static_cast<uint32_t>(e));
-    cc[0] = static_cast<int>(static_cast<uint32_t>(e) - r0 * static_cast<uint32_t>(A.m.N[0]));
-    const uint32_t z2 = A.m.div_n1.div(r0);
-    cc[1] = static_cast<int>(r0 - z2 * static_cast<uint32_t>(A.m.N[1]));
-    cc[2] = static_cast<int>(z2);
-    unsigned lo = 0, hi = 0;
-#pragma unroll
-    for (int x = 0; x < DIM; ++x) {
-      const int cx = x == 0 ? cc[0] : (x == 1 ? cc[1] : cc[2]);
-      const int Nx = static_cast<int>(x == 0 ? A.m.N[0] : (x == 1 ? A.m.N[1] : A.m.N[2]));
-      lo |= static_cast<unsigned>(cx > 0) << x;
-      hi |= static_cast<unsigned>(cx + 1 < Nx) << x;
-    }
-    for (int idx = lane; idx < NS * NS; idx += GT) {
-      const int ps = idx / NS, qs = idx - ps * NS;
-      const int a_ = ps >> 1;
-      const bool pin = (((ps & 1) ? hi : lo) >> a_) & 1u;
-      const bool qin = (((qs & 1) ? hi : lo) >> (qs >> 1)) & 1u;
-      const int ca = a_ == 0 ? cc[0] : (a_ == 1 ? cc[1] : cc[2]);
-      const int na = static_cast<int>(a_ == 0 ? A.m.N[0] : (a_ == 1 ? A.m.N[1] : A.m.N[2]));
-      sm.rank[idx] = (pin && qin) ? col_rank_fast(DIM, ps, qs, lo, hi, ca, na, false) : -1;
-      if (qs == 0) {
-        const int side = ps & 1;
-        if (pin) {
-          const int face = face_id32(A.m, a_, cc[0] + (a_ == 0 ? side : 0), cc[1] + (a_ == 1 ? side : 0),
-                                     cc[2] + (a_ == 2 ? side : 0));
-          const int row = A.mbase[face];
-          const int64_t r0s = A.rowoff[row];
-          sm.rstart[ps] = r0s;
-          sm.rlen[ps] = static_cast<int>(A.rowoff[row + 1] - r0s);
-          sm.grow[ps] = row;
-        } else {
-          sm.rstart[ps] = -1;
-        }
-      }
-    }
-  }
-  gsync<GT>();
+  // scatter: H_pc = V_F(p, c) (fp64) - C_pc ; g_p = w_F(p) - C_p,NF, through the
+  // per-cell tables built at the start; consecutive lanes write consecutive columns.
   if constexpr (DPF % 2 == 0) {
     // one (row, face block) run of DPF consecutive doubles per work item, stored
     // as double2 (H rows start at multiples of DPF doubles, cudaMalloc'd base);
@@ -505,7 +622,7 @@ __device__ __forceinline__ void warp_cell(const HybArgs& A, int e, int parity, i
 }
 
 template <int DIM, int K>
-__global__ void __launch_bounds__(32 * kWarps, (DIM == 3 && K == 1) ? 9 : 1) k_hyb_warp(HybArgs A, int parity, double* gws) {
+__global__ void __launch_bounds__(32 * kWarps, (DIM == 3 && K == 1) ? 8 : 1) k_hyb_warp(HybArgs A, int parity, double* gws, const double* pre) {
   constexpr int GT = Group<DIM, K>::GT;
   constexpr int CPB = 32 * kWarps / GT;  // cells per CTA iteration
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -530,7 +647,7 @@ __global__ void __launch_bounds__(32 * kWarps, (DIM == 3 && K == 1) ? 9 : 1) k_h
     } else if (e < 0) {
       continue;
     }
-    warp_cell<DIM, K>(A, e, parity, tid, *sm, *cs, scratch);
+    warp_cell<DIM, K>(A, e, parity, tid, *sm, *cs, scratch, pre);
   }
 }
 
@@ -559,10 +676,10 @@ int64_t grid_t(const HybArgs& a) {
 }
 
 template <int DIM, int K>
-void launch_t(const HybArgs& a, int parity, double* gws, cudaStream_t st) {
+void launch_t(const HybArgs& a, int parity, double* gws, const double* pre, cudaStream_t st) {
   const size_t smem = smem_t<DIM, K>();
   const int64_t grid = grid_t<DIM, K>(a);
-  k_hyb_warp<DIM, K><<<static_cast<unsigned>(grid), 32 * kWarps, smem, st>>>(a, parity, gws);
+  k_hyb_warp<DIM, K><<<static_cast<unsigned>(grid), 32 * kWarps, smem, st>>>(a, parity, gws, pre);
 }
 
 }  // namespace
@@ -583,12 +700,12 @@ int64_t hybridize_warp_scratch_doubles(const HybArgs& a) {
   return scratch_doubles_t<2, 3>(grid_t<2, 3>(a));
 }
 
-void launch_hybridize_warp(const HybArgs& a, int parity, double* gws, cudaStream_t st) {
+void launch_hybridize_warp(const HybArgs& a, int parity, double* gws, const double* pre, cudaStream_t st) {
   const int dim = a.m.dim, k = order_of(a.m);
-  if (dim == 3 && k == 1) launch_t<3, 1>(a, parity, gws, st);
-  else if (dim == 2 && k == 1) launch_t<2, 1>(a, parity, gws, st);
-  else if (dim == 2 && k == 2) launch_t<2, 2>(a, parity, gws, st);
-  else if (dim == 2 && k == 3) launch_t<2, 3>(a, parity, gws, st);
+  if (dim == 3 && k == 1) launch_t<3, 1>(a, parity, gws, pre, st);
+  else if (dim == 2 && k == 1) launch_t<2, 1>(a, parity, gws, nullptr, st);
+  else if (dim == 2 && k == 2) launch_t<2, 2>(a, parity, gws, nullptr, st);
+  else if (dim == 2 && k == 3) launch_t<2, 3>(a, parity, gws, nullptr, st);
   count_launch();
 }
 

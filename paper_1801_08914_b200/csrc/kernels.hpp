@@ -72,7 +72,8 @@ void launch_hybridize_rt0_rows(const HybArgs& a, const double* host_consts, doub
 // k >= 1 with nF + 1 <= 32 (RT1 hexes, RT1..RT3 quads): one warp per cell (kern_warp.cu)
 bool hybridize_warp_supported(int dim, int k);
 int64_t hybridize_warp_scratch_doubles(const HybArgs& a);
-void launch_hybridize_warp(const HybArgs& a, int parity, double* gws, cudaStream_t st);
+// pre (3D RT1): (N + R) x ncells column-major [N0 f_e ; X^T f_e] (launch_gemm_f64_nn), else nullptr
+void launch_hybridize_warp(const HybArgs& a, int parity, double* gws, const double* pre, cudaStream_t st);
 // RT2 / RT3 hexahedra: one CTA per cell (kern_cta.cu)
 bool hybridize_big_supported(int dim, int k);
 int64_t hybridize_big_scratch_doubles(const HybArgs& a, int k);
