@@ -254,6 +254,15 @@ __device__ __forceinline__ void two_prod(double a, double b, double& p, double& 
   p = __dmul_rn(a, b);
   e = __fma_rn(a, b, -p);
 }
+// the same exact (s, e) as two_sum with 3 floating-point operations instead of 6:
+// Fast2Sum on the operands ordered by magnitude (the order costs a compare and
+// two selects, off the fp64 pipe's critical ops)
+__device__ __forceinline__ void two_sum_fast(double a, double b, double& s, double& e) {
+  s = __dadd_rn(a, b);
+  const bool sw = fabs(b) > fabs(a);
+  const double hi = sw ? b : a, lo = sw ? a : b;
+  e = __dsub_rn(lo, __dsub_rn(s, hi));
+}
 __device__ __forceinline__ void two_sum(double a, double b, double& s, double& e) {
   s = __dadd_rn(a, b);
   const double bb = __dsub_rn(s, a);

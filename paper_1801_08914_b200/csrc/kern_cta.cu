@@ -275,7 +275,7 @@ __device__ void correction_tc(BigSmem<K>& sm, const Fixed& fx, double a, double 
         double p1, e1, p2, e2, sm_, e3;
         two_prod(a, dm[i].x, p1, e1);
         two_prod(b, dm[i].y, p2, e2);
-        two_sum(p1, p2, sm_, e3);
+        two_sum_fast(p1, p2, sm_, e3);
         const float x = fmaf(af, em[i].x, fmaf(bf32, em[i].y, static_cast<float>(-((e1 + e2) + e3))));
         const uint32_t off = umma::kmajor_offset(m, k, NY) >> 2;
         tf32_split(x, T.bhi[off], T.blo[off]);

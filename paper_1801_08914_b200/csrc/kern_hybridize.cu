@@ -449,7 +449,7 @@ __device__ __forceinline__ float rt0_fast_correction(const Rt0Const<2 * DIM>& c,
       if ((k >> 1) == (l >> 1)) {
         double p2, e2, s_, e3;
         two_prod(b, c.M[k * N + l], p2, e2);
-        two_sum(p1, p2, s_, e3);
+        two_sum_fast(p1, p2, s_, e3);
         dl[sym_idx(k, l, N)] = static_cast<float>(-((e1 + e2) + e3));
       } else {
         dl[sym_idx(k, l, N)] = static_cast<float>(-e1);  // M_kl = 0: A_kl = fl(alpha D_kl)

@@ -479,7 +479,7 @@ __device__ __forceinline__ void warp_cell(const HybArgs& A, int e, int parity, i
       double p1, e1, p2, e2, s_, e3;
       two_prod(a, dm.x, p1, e1);
       two_prod(b, dm.y, p2, e2);
-      two_sum(p1, p2, s_, e3);
+      two_sum_fast(p1, p2, s_, e3);
       const int l = idx / N, i = idx - l * N;  // entry (i, l), stored transposed
       dst[l * ld + i] = fmaf(af, em.x, fmaf(bfl, em.y, static_cast<float>(-((e1 + e2) + e3))));
     }
