@@ -336,9 +336,22 @@ constexpr int64_t scratch_doubles_per_warp() {
   return (WarpSmem<DIM, K>::NR * NCP + S::N * S::N + 1) / 2 + 8;  // T, then a Delta32 copy for orders >= 2
 }
 
+// the next cell's coefficients and [N0 f ; X^T f] entry, loaded while the current cell runs
+struct CellPrefetch {
+  double a = 1.0, b = 1.0, p = 0.0;
+};
+template <int N, int R>
+__device__ __forceinline__ void prefetch_cell(const HybArgs& A, const double* pre, int e, int lane, CellPrefetch& q) {
+  if (e < 0) return;
+  q.a = A.alpha[e];
+  q.b = A.beta[e];
+  if (pre && lane < N + R) q.p = pre[static_cast<int64_t>(e) * (N + R) + lane];
+}
+
 template <int DIM, int K>
 __device__ __forceinline__ void warp_cell(const HybArgs& A, int e, int parity, int lane, WarpSmem<DIM, K>& sm,
-                                          const CtaShared<DIM, K>& cs, double* scratch, const double* pre) {
+                                          const CtaShared<DIM, K>& cs, double* scratch, const double* pre,
+                                          CellPrefetch& pf, int e_next) {
   constexpr int GT = Group<DIM, K>::GT;  // "lane" is the thread index within the cell's group
   using S = Shape<DIM, K>;
   using SM = WarpSmem<DIM, K>;
@@ -346,7 +359,7 @@ __device__ __forceinline__ void warp_cell(const HybArgs& A, int e, int parity, i
   constexpr int N = S::N, NF = S::NF, NC = S::NC, R = S::R, NINT = S::NINT, DPF = S::DPF, NCP = SM::NCP;
   const Fixed& fx = A.fx;
   float* tbuf = reinterpret_cast<float*>(scratch);  // N x NCP
-  const double a = A.alpha[e], b = A.beta[e];
+  const double a = pf.a, b = pf.b, pv = pf.p;
   const double ib = 1.0 / b;
   constexpr int NS = 2 * DIM;
   int cc[3];
@@ -391,17 +404,23 @@ __device__ __forceinline__ void warp_cell(const HybArgs& A, int e, int parity, i
     }
   }
   for (int j = lane; j < R; j += GT) sm.s[j] = b / fma(a, __ldg(fx.lam + j), b);
-  if (pre) {
-    // [N0 f ; X^T f] of every cell from one batched fp64 GEMM before the launch
-    const double* pe = pre + static_cast<int64_t>(e) * (N + R);
-    for (int i = lane; i < N; i += GT) sm.nf[i] = pe[i];
+  if (GT >= N + R && pre) {
+    // [N0 f ; X^T f] of every cell from one batched fp64 GEMM before the launch,
+    // entry `lane` prefetched during the previous cell (GT >= N + R)
+    if (lane < N) {
+      sm.nf[lane] = pv;
+    } else if (lane < N + R) {
+      const int j = lane - N;
+      sm.z[j * NC + NF] = (b / fma(a, __ldg(fx.lam + j), b)) * pv;  // = s_j (X^T f)_j
+    }
+    prefetch_cell<N, R>(A, pre, e_next, lane, pf);
     gsync<GT>();
     for (int idx = lane; idx < R * NF; idx += GT) {
       const int j = idx / NF, c = idx - j * NF;
       sm.z[j * NC + c] = sm.s[j] * cs.xt[j * N + NINT + c];
     }
-    for (int j = lane; j < R; j += GT) sm.z[j * NC + NF] = sm.s[j] * pe[N + j];
   } else {
+    prefetch_cell<N, R>(A, pre, e_next, lane, pf);
     const double* fe = A.f + static_cast<int64_t>(e) * N;
     for (int i = lane; i < N; i += GT) sm.f[i] = fe[i];
     gsync<GT>();
@@ -638,16 +657,20 @@ __global__ void __launch_bounds__(32 * kWarps, (DIM == 3 && K == 1) ? 8 : 1) k_h
   double* scratch = gws + (static_cast<int64_t>(blockIdx.x) * CPB + grp) * scratch_doubles_per_warp<DIM, K>();
   const uint32_t cnt = static_cast<uint32_t>(parity_count(A.m));
   // the loop bound is uniform over each group (a group never splits on it)
-  for (uint32_t t0 = blockIdx.x * CPB; t0 < cnt; t0 += gridDim.x * CPB) {
+  auto cell_at = [&](uint32_t t0) -> int {
     const uint32_t t = t0 + grp;
     int cc[3];
-    const int e = t < cnt ? parity_cell32(A.m, parity, t, cc) : -1;
-    if (GT > 32) {  // one cell per CTA: skip together
-      if (e < 0) continue;
-    } else if (e < 0) {
-      continue;
-    }
-    warp_cell<DIM, K>(A, e, parity, tid, *sm, *cs, scratch, pre);
+    return t < cnt ? parity_cell32(A.m, parity, t, cc) : -1;
+  };
+  const uint32_t stride = gridDim.x * CPB;
+  CellPrefetch pf;
+  int e = cell_at(blockIdx.x * CPB);
+  prefetch_cell<S::N, S::R>(A, pre, e, tid, pf);
+  for (uint32_t t0 = blockIdx.x * CPB; t0 < cnt; t0 += stride) {
+    const int e_next = t0 + stride < cnt ? cell_at(t0 + stride) : -1;
+    if (e >= 0) warp_cell<DIM, K>(A, e, parity, tid, *sm, *cs, scratch, pre, pf, e_next);
+    else prefetch_cell<S::N, S::R>(A, pre, e_next, tid, pf);
+    e = e_next;
   }
 }
 
