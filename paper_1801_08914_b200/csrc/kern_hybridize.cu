@@ -767,9 +767,18 @@ __global__ void __launch_bounds__(kCT, HDR_CELL_MINB) k_rt0_cell(HybArgs A, Rt0C
 // fl(h_minus + h_plus), the reference's two-term sum.
 // brick shapes: BX cells along x (64 when the mesh is at least 48 cells wide,
 // else 32) by 2 x 2 (3D) / 4 (2D); 512 threads per SM either way
+#ifndef HDR_BRICK_Y3
+#define HDR_BRICK_Y3 2
+#endif
+#ifndef HDR_BRICK_Z3
+#define HDR_BRICK_Z3 2
+#endif
+#ifndef HDR_BRICK_XW
+#define HDR_BRICK_XW 64  // BX of wide meshes
+#endif
 template <int DIM, int BX>
 struct Brick {
-  static constexpr int X = BX, Y = DIM == 3 ? 2 : 4, Z = DIM == 3 ? 2 : 1;
+  static constexpr int X = BX, Y = DIM == 3 ? HDR_BRICK_Y3 : 4, Z = DIM == 3 ? HDR_BRICK_Z3 : 1;
 };
 
 template <int DIM, int BX>
@@ -1396,7 +1405,7 @@ void launch_hybridize_rt0_rows(const HybArgs& a, const double* hc, double* stage
     Rt0Const<6> c;
     fill(c, 6);
     if (!rows && !cell) {
-      if (wide) brick(std::integral_constant<int, 3>{}, std::integral_constant<int, 64>{}, c, f3);
+      if (wide) brick(std::integral_constant<int, 3>{}, std::integral_constant<int, HDR_BRICK_XW>{}, c, f3);
       else brick(std::integral_constant<int, 3>{}, std::integral_constant<int, 32>{}, c, f3);
     } else if (rows) {
       const unsigned nb = static_cast<unsigned>((cnt + 4 * 5 - 1) / (4 * 5));
