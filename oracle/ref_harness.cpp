@@ -247,7 +247,10 @@ int cmd_dump(const std::map<std::string, std::string>& kv) {
   // (rtol, maxit of RunConfig) with each preconditioner
   if (kv.count("amg") && kv.at("amg") == "1" && hyb.h_mat.nrows > 0) {
     const double rtol = kv.count("rtol") ? std::stod(kv.at("rtol")) : 1e-12;
+    const double ts0 = now();
     const AmgHierarchy ah = amg_setup(hyb.h_mat);
+    const double ts1 = now();
+    std::fprintf(stderr, "{\"amg_setup_s\": %.4f}\n", ts1 - ts0);
     w.q("amg.levels", {static_cast<index_t>(ah.levels.size())});
     for (std::size_t l = 0; l < ah.levels.size(); ++l) {
       w.csr("amg.A" + std::to_string(l), ah.levels[l].matrix);
@@ -263,6 +266,8 @@ int cmd_dump(const std::map<std::string, std::string>& kv) {
         {"amg", amg_preconditioner(hyb.h_mat)}, {"sgs", ssgs_setup(hyb.h_mat)}, {"jacobi", jacobi_setup(hyb.h_mat)}};
     for (const auto& [name, pc] : pcs) {
       auto [sol, rep] = pcg(hyb.h_mat, pc.get(), g, rtol, 2000);
+      std::fprintf(stderr, "{\"pcg\": \"%s\", \"iterations\": %lld, \"wall_s\": %.4f}\n", name,
+                   static_cast<long long>(rep.iterations), rep.wall_time);
       w.q(std::string("pcg.") + name + ".iterations", {rep.iterations});
       w.d(std::string("pcg.") + name + ".residuals", rep.relative_residuals);
       w.d(std::string("pcg.") + name + ".x", sol);

@@ -3,6 +3,7 @@
 #pragma once
 
 #include <cstdint>
+#include <vector>
 
 #include "capi_util.hpp"
 
@@ -16,6 +17,21 @@ struct DCsr {  // device CSR: int64 row offsets, int32 columns
 };
 
 struct AmgHier;  // hierarchy + sweep state (kern_amg.cu)
+
+// Gauss-Seidel sweep state of one matrix: ready flags and the level orders
+// (rows sorted by their dependency depth in the forward / backward sweep),
+// built on first use
+struct SweepState {
+  DBuf<int> flags, fwd, bwd, lvl_fwd, lvl_bwd;  // orders and level offsets
+  DBuf<int64_t> eoff_fwd, eoff_bwd;              // entry offsets of the rows in level order
+  int64_t max_level_nnz = 0, max_level_rows = 0, max_row_len = 0;
+  std::vector<int64_t> h_eo_fwd, h_eo_bwd;  // host copies for the one-CTA batch plan
+  std::vector<int> h_off_fwd, h_off_bwd;
+  DBuf<int> bat_fwd, bat_bwd;  // one-CTA sweeps: batch starts (rows of one level)
+  int nbat_fwd = 0, nbat_bwd = 0;
+  int levels_fwd = 0, levels_bwd = 0;
+  bool ready = false;
+};
 
 // copy of a device CSR matrix (int32 or int64 columns) into a DCsr
 void dcsr_from_device(int64_t n, int64_t ncols, const int64_t* ro, const int32_t* ci32, const int64_t* ci64,
@@ -34,8 +50,8 @@ void amg_apply_device(AmgHier* h, const double* r, double* z);
 // the sweep machinery alone (SGS): context + forward scratch
 AmgHier* sweep_context(int64_t n, cudaStream_t st);
 double* sweep_scratch(AmgHier* h);
-// symmetric Gauss-Seidel apply of A (flags: n ints, zeroed once)
-void sgs_apply_device(AmgHier* h, const DCsr& A, DBuf<int>& flags, double* zf, const double* r, double* z);
+// symmetric Gauss-Seidel apply of A
+void sgs_apply_device(AmgHier* h, const DCsr& A, SweepState& sw, double* zf, const double* r, double* z);
 // sticky device status of the sweeps (ZeroDiagonal)
 hdr_status amg_status(AmgHier* h);
 // check_symmetric (src/solvers.cpp:25-30): max|A - A^T| and max|A| on the device

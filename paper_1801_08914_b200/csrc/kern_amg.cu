@@ -28,10 +28,14 @@
 // The one serial step, aggregate() (amg.cpp:48-83: a greedy pass whose result
 // depends on visiting the nodes in index order), runs on the host in C++ over
 // the device-built strength graph.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <cmath>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -45,9 +49,12 @@
 
 namespace hdr {
 
+namespace cg = cooperative_groups;
+
 namespace {
 
 constexpr int kT = 256;
+constexpr size_t kCtaSweepSmem = 200 * 1024;  // one-CTA sweeps: new iterate + the widest level's products
 
 inline unsigned nblk(int64_t n, int t = kT) { return static_cast<unsigned>(std::max<int64_t>(1, (n + t - 1) / t)); }
 
@@ -156,11 +163,28 @@ __global__ void k_div_into(int64_t n, const double* w, double norm, double* v) {
   const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (i < n) v[i] = w[i] / norm;
 }
-// sequential sum of squares (the reference's loop order) and its square root
-__global__ void k_seq_norm(int64_t n, const double* w, double* out) {
+// sequential sum of squares (the reference's loop order) and its square root:
+// the CTA stages chunks of squares in shared memory (coalesced loads, the
+// products in parallel), one thread adds them in order
+__global__ void __launch_bounds__(1024) k_seq_norm(int64_t n, const double* w, double* out) {
+  constexpr int CH = 2048;
+  __shared__ double sq[2][CH];
   double s = 0.0;
-  for (int64_t i = 0; i < n; ++i) s = __dadd_rn(s, __dmul_rn(w[i], w[i]));
-  out[0] = sqrt(s);
+  int buf = 0;
+  for (int64_t i = threadIdx.x; i < CH && i < n; i += blockDim.x) sq[0][i] = __dmul_rn(w[i], w[i]);
+  __syncthreads();
+  for (int64_t c0 = 0; c0 < n; c0 += CH, buf ^= 1) {
+    const int64_t c1 = c0 + CH;  // next chunk staged by the other threads while thread 0 adds this one
+    if (threadIdx.x == 0) {
+      const int m = static_cast<int>(n - c0 < CH ? n - c0 : CH);
+      for (int j = 0; j < m; ++j) s = __dadd_rn(s, sq[buf][j]);
+    } else {
+      for (int64_t i = c1 + threadIdx.x - 1; i < c1 + CH && i < n; i += blockDim.x - 1)
+        sq[buf ^ 1][i - c1] = __dmul_rn(w[i], w[i]);
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[0] = sqrt(s);
 }
 
 // smooth_prolongator (amg.cpp:146-157): P = P_tent - omega D^-1 AP on AP's
@@ -330,14 +354,14 @@ __global__ void k_tp_numeric(int64_t nr, const int64_t* rro, const int32_t* rci,
 template <bool FWD>
 __global__ void __launch_bounds__(kT) k_gs_sweep(int64_t n, const int64_t* ro, const int32_t* ci, const double* v,
                                                  const double* r, const double* zin, double* zout, int* flags,
-                                                 int epoch, unsigned long long* ticket, int* status) {
+                                                 int epoch, unsigned long long* ticket, int* status, const int* order) {
   const int lane = threadIdx.x & 31;
   while (true) {
     unsigned long long t = 0;
     if (lane == 0) t = atomicAdd(ticket, 1ull);
     t = __shfl_sync(0xffffffffu, t, 0);
     if (t >= static_cast<unsigned long long>(n)) return;
-    const int64_t i = FWD ? static_cast<int64_t>(t) : n - 1 - static_cast<int64_t>(t);
+    const int64_t i = order[t];  // rows in level order: every dependency has a smaller ticket
     const int64_t a = ro[i], b = ro[i + 1];
     double s = r[i], diag = 0.0;
     for (int64_t base = a; base < b; base += 32) {
@@ -349,8 +373,7 @@ __global__ void __launch_bounds__(kT) k_gs_sweep(int64_t n, const int64_t* ro, c
         vk = v[k];
         const bool dep = FWD ? c < i : c > i;  // already updated in this sweep
         if (dep) {
-          while (ld_acquire(flags + c) != epoch) {
-          }
+          while (ld_acquire(flags + c) != epoch) __nanosleep(64);
           zk = __ldcg(zout + c);
         } else if (c != i) {
           zk = zin ? zin[c] : 0.0;
@@ -372,6 +395,125 @@ __global__ void __launch_bounds__(kT) k_gs_sweep(int64_t n, const int64_t* ro, c
     }
     __syncwarp();
   }
+}
+
+// one row of a Gauss-Seidel sweep by one warp: lanes load 32 entries at a time
+// and form the products (dependencies from znew, the rest from zold or 0),
+// lane 0 subtracts them in storage order (the reference's roundings)
+template <bool FWD, class ZNEW>
+__device__ __forceinline__ void gs_row(int i, const int64_t* ro, const int32_t* ci, const double* v, const double* r,
+                                       const double* zold, ZNEW znew_at, double* zdst, int* status) {
+  const int lane = threadIdx.x & 31;
+  const int64_t a = ro[i], b = ro[i + 1];
+  double s = r[i], diag = 0.0;
+  for (int64_t base = a; base < b; base += 32) {
+    const int64_t k = base + lane;
+    int c = -1;
+    double p = 0.0;
+    if (k < b) {
+      c = ci[k];
+      const double vk = v[k];
+      if (c == i) {
+        p = vk;  // the diagonal travels in p
+      } else {
+        const bool dep = FWD ? c < i : c > i;
+        p = __dmul_rn(vk, dep ? znew_at(c) : (zold ? zold[c] : 0.0));
+      }
+    }
+    const int m = static_cast<int>(b - base < 32 ? b - base : 32);
+    for (int q = 0; q < m; ++q) {
+      const int cq = __shfl_sync(0xffffffffu, c, q);
+      const double pq = __shfl_sync(0xffffffffu, p, q);
+      if (cq == i) diag = pq;
+      else s = __dsub_rn(s, pq);
+    }
+  }
+  if (lane == 0) {
+    if (diag == 0.0) atomicOr(status, 1);
+    *zdst = s / diag;
+  }
+}
+
+// sweep of a small matrix in one CTA: the new iterate in shared memory, rows in
+// level order, per level (1) every product of the level's rows formed in
+// parallel into a shared buffer (the diagonal's slot holds +0: subtracting it
+// leaves every sum unchanged, so the fold equals the reference's, which skips
+// it), (2) one thread per row subtracts its products in storage order
+template <bool FWD>
+__global__ void __launch_bounds__(512) k_gs_cta(int n, const int64_t* ro, const int32_t* ci, const double* v,
+                                                const double* r, const double* zin, double* zout, const int* order,
+                                                const int* bat, int nbat, const int64_t* eoff, int* status) {
+  extern __shared__ double zs[];  // n new values, then the products of one batch of rows
+  double* pb = zs + ((n + 1) & ~1);
+  __shared__ double dg[512];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  // batches: rows [bat[j], bat[j + 1]) of one level, at most 512 rows and the buffer's entries
+  for (int j = 0; j < nbat; ++j) {
+    const int t0 = __ldg(bat + j), t1 = __ldg(bat + j + 1);
+    const int64_t e0 = __ldg(eoff + t0);
+    for (int t = t0 + warp; t < t1; t += nw) {  // products, warp per row
+      const int i = order[t];
+      const int64_t a = ro[i], b = ro[i + 1], dst = eoff[t] - e0 - a;
+      for (int64_t k = a + lane; k < b; k += 32) {
+        const int c = ci[k];
+        double p = 0.0;
+        if (c != i) {
+          const bool dep = FWD ? c < i : c > i;
+          p = __dmul_rn(v[k], dep ? zs[c] : (zin ? zin[c] : 0.0));
+        } else {
+          dg[t - t0] = v[k];
+        }
+        pb[dst + k] = p;
+      }
+    }
+    __syncthreads();
+    for (int t = t0 + threadIdx.x; t < t1; t += blockDim.x) {  // folds, thread per row
+      const int i = order[t];
+      const int64_t q0 = eoff[t] - e0, q1 = eoff[t + 1] - e0;
+      double sacc = r[i];
+#pragma unroll 8
+      for (int64_t q = q0; q < q1; ++q) sacc = __dsub_rn(sacc, pb[q]);
+      const double d = dg[t - t0];
+      if (d == 0.0) atomicOr(status, 1);
+      zs[i] = sacc / d;
+    }
+    __syncthreads();
+  }
+  for (int i = threadIdx.x; i < n; i += blockDim.x) zout[i] = zs[i];
+}
+
+// sweep of a larger matrix: a cooperative grid, warp per row, a grid barrier
+// between levels (the new iterate in global memory, read through L2)
+template <bool FWD>
+__global__ void __launch_bounds__(512) k_gs_coop(int n, const int64_t* ro, const int32_t* ci, const double* v,
+                                                 const double* r, const double* zin, double* zout,
+                                                 const int* order, const int* lvl, int nlev, int* status) {
+  cg::grid_group grid = cg::this_grid();
+  const int gw = static_cast<int>((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  const int nw = static_cast<int>((gridDim.x * blockDim.x) >> 5);
+  for (int L = 0; L < nlev; ++L) {
+    for (int t = lvl[L] + gw; t < lvl[L + 1]; t += nw) {
+      const int i = order[t];
+      gs_row<FWD>(i, ro, ci, v, r, zin, [&](int c) { return __ldcg(zout + c); }, zout + i, status);
+    }
+    grid.sync();
+  }
+}
+
+// dependency depth of every row in a forward (j < i) / backward (j > i) sweep:
+// one Jacobi step of lev_i = max over dependencies of lev_j + 1 (monotone from
+// zero; converged after as many steps as the longest chain)
+template <bool FWD>
+__global__ void k_level_iter(int64_t n, const int64_t* ro, const int32_t* ci, const int* lin, int* lout, int* changed) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= n) return;
+  int lv = 0;
+  for (int64_t k = ro[i]; k < ro[i + 1]; ++k) {
+    const int c = ci[k];
+    if (FWD ? c < i : c > i) lv = max(lv, lin[c] + 1);
+  }
+  lout[i] = lv;
+  if (lv != lin[i]) *changed = 1;
 }
 
 // residual = r - A z (v_cycle: spmv, then r_i - residual_i)
@@ -413,27 +555,44 @@ __global__ void __launch_bounds__(256) k_coarse_factor(int64_t n, const int64_t*
   __syncthreads();
   if (!cta_lu_factor(lu, nn, piv, red, ired) && threadIdx.x == 0) status[0] = 1;
 }
-__global__ void k_coarse_solve(int n, const double* lu, const int* piv, const double* r, double* z) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  for (int i = 0; i < n; ++i) z[i] = r[i];
-  for (int k = 0; k < n; ++k) {
-    const int p = piv[k];
-    if (p != k) {
-      const double t = z[k];
-      z[k] = z[p];
-      z[p] = t;
+// lu_solve (dense.cpp:99-120) with one CTA, z in shared memory: the forward
+// sweep parallel over the rows below each pivot (each entry sees the serial
+// sequence of updates), the back substitution row by row with the row's
+// products formed in parallel and summed by one thread in the serial order
+__global__ void __launch_bounds__(1024) k_coarse_solve(int n, const double* lu, const int* piv, const double* r,
+                                                       double* z) {
+  extern __shared__ double zs[];  // n, then n products
+  double* pr = zs + n;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) zs[i] = r[i];
+  __syncthreads();
+  if (threadIdx.x == 0)
+    for (int k = 0; k < n; ++k) {
+      const int p = piv[k];
+      if (p != k) {
+        const double t = zs[k];
+        zs[k] = zs[p];
+        zs[p] = t;
+      }
     }
-  }
+  __syncthreads();
   for (int k = 0; k < n; ++k) {
-    const double xk = z[k];
-    if (xk == 0.0) continue;
-    for (int i = k + 1; i < n; ++i) z[i] = __dsub_rn(z[i], __dmul_rn(lu[i * n + k], xk));
+    const double xk = zs[k];
+    if (xk != 0.0)
+      for (int i = k + 1 + threadIdx.x; i < n; i += blockDim.x)
+        zs[i] = __dsub_rn(zs[i], __dmul_rn(lu[static_cast<int64_t>(i) * n + k], xk));
+    __syncthreads();
   }
   for (int i = n - 1; i >= 0; --i) {
-    double s = z[i];
-    for (int j = i + 1; j < n; ++j) s = __dsub_rn(s, __dmul_rn(lu[i * n + j], z[j]));
-    z[i] = s / lu[i * n + i];
+    for (int j = i + 1 + threadIdx.x; j < n; j += blockDim.x) pr[j] = __dmul_rn(lu[static_cast<int64_t>(i) * n + j], zs[j]);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double sacc = zs[i];
+      for (int j = i + 1; j < n; ++j) sacc = __dsub_rn(sacc, pr[j]);
+      zs[i] = sacc / lu[static_cast<int64_t>(i) * n + i];
+    }
+    __syncthreads();
   }
+  for (int i = threadIdx.x; i < n; i += blockDim.x) z[i] = zs[i];
 }
 
 __global__ void k_fill_i64(int64_t n, int64_t* a, int64_t start) {
@@ -584,7 +743,7 @@ double spectral_bound(const DCsr& a, const double* inv_diag, int iterations, cud
   for (int it = 0; it < iterations; ++it) {
     k_spmv<<<nblk(n), kT, 0, st>>>(n, a.ro.p, a.ci.p, a.v.p, v.p, w.p);
     k_scale_inplace<<<nblk(n), kT, 0, st>>>(n, w.p, inv_diag);
-    k_seq_norm<<<1, 1, 0, st>>>(n, w.p, nrm.p);
+    k_seq_norm<<<1, 1024, 0, st>>>(n, w.p, nrm.p);
     count_launch(3);
     double norm = 0.0;
     CK(cudaMemcpyAsync(&norm, nrm.p, 8, cudaMemcpyDeviceToHost, st));
@@ -628,7 +787,7 @@ int64_t inv_diag_checked(const DCsr& a, DBuf<double>& d, cudaStream_t st) {
 struct AmgLevel {
   DCsr A, P, R;
   DBuf<double> r, z, res, cr;  // per-level vectors of the V-cycle
-  DBuf<int> flags;             // GS ready flags
+  SweepState sw;               // GS flags and level orders
 };
 
 struct AmgHier {
@@ -665,13 +824,31 @@ static void level_vectors(AmgLevel& L) {
   L.z.alloc(L.A.n);
   L.res.alloc(L.A.n);
   L.cr.alloc(L.P.ncols);
-  L.flags.alloc(L.A.n);
-  CK(cudaMemset(L.flags.p, 0, L.A.n * sizeof(int)));
+
 }
 
 // amg_setup (amg.cpp:189-244); takes ownership of A's buffers
+// HDR_AMG_PROFILE=1: phase times of the setup and the cycles on stderr (diagnostics)
+static bool amg_profile() {
+  static const bool on = getenv("HDR_AMG_PROFILE") != nullptr;
+  return on;
+}
+struct PhaseClock {
+  cudaStream_t st;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void lap(const char* what, int64_t level) {
+    if (!amg_profile()) return;
+    cudaStreamSynchronize(st);
+    const auto now = std::chrono::steady_clock::now();
+    fprintf(stderr, "[amg] level %lld %-12s %9.3f ms\n", static_cast<long long>(level), what,
+            std::chrono::duration<double, std::milli>(now - t).count());
+    t = now;
+  }
+};
+
 AmgHier* amg_setup_device(DCsr&& fine, const hdr_amg_options& o, cudaStream_t st) {
   if (fine.n != fine.ncols) throw StatusError(HDR_SETUP_FAILED, "amg_setup: matrix not square");
+  PhaseClock pc{st};
   std::unique_ptr<AmgHier> h(new AmgHier);
   h->st = st;
   DCsr current = std::move(fine);
@@ -704,6 +881,7 @@ AmgHier* amg_setup_device(DCsr&& fine, const hdr_amg_options& o, cudaStream_t st
       if (nc > 0 && static_cast<double>(nc) <= o.stall_ratio * static_cast<double>(n)) break;
       theta *= 0.25;
     }
+    pc.lap("aggregate", level);
     if (nc == 0) throw StatusError(HDR_SETUP_FAILED, "amg_setup: empty coarse level");
     if (static_cast<double>(nc) > o.stall_ratio * static_cast<double>(n)) break;  // coarsening stalled
     if (nc >= n) throw StatusError(HDR_SETUP_FAILED, "amg_setup: non-decreasing coarse size");
@@ -746,7 +924,9 @@ AmgHier* amg_setup_device(DCsr&& fine, const hdr_amg_options& o, cudaStream_t st
     DBuf<double> finv;
     const int64_t fbad = inv_diag_checked(F, finv, st);
     if (fbad >= 0) throw StatusError(HDR_SETUP_FAILED, "amg_setup: non-positive diagonal at row " + std::to_string(fbad));
+    pc.lap("filter", level);
     const double rho = spectral_bound(F, finv.p, o.power_iterations, st);
+    pc.lap("power", level);
     const double omega = o.omega_factor / rho;
     // P = (I - omega D_F^-1 F) P_tent on the pattern of AP = triple_product(I, F, P_tent)
     DCsr I;
@@ -767,9 +947,11 @@ AmgHier* amg_setup_device(DCsr&& fine, const hdr_amg_options& o, cudaStream_t st
     dev_triple(I, F, pt, L->P, st);
     k_smooth<<<nblk(n), kT, 0, st>>>(n, L->P.ro.p, L->P.ci.p, L->P.v.p, pt.ci.p, pt.v.p, finv.p, omega, L->P.v.p);
     count_launch();
+    pc.lap("smooth P", level);
     dev_transpose(L->P, L->R, st);
     DCsr coarse;
     dev_triple(L->R, current, L->P, coarse, st);
+    pc.lap("RAP", level);
     L->A = std::move(current);
     current = std::move(coarse);
     level_vectors(*L);
@@ -809,19 +991,171 @@ const DCsr& amg_matrix(const AmgHier* h, int64_t level, int which) {
   return which == 0 ? L.A : (which == 1 ? L.P : L.R);
 }
 
-// one sync-free Gauss-Seidel sweep of A on (r, zin) -> zout
-void gs_sweep(AmgHier* h, const DCsr& A, DBuf<int>& flags, bool fwd, const double* r, const double* zin, double* zout) {
+// level orders of A's forward and backward sweeps (rows sorted by dependency
+// depth, stable: rows of one level ascending) and the ready flags
+static void sweep_prepare(const DCsr& A, SweepState& sw, cudaStream_t st) {
+  const int64_t n = A.n;
+  sw.flags.alloc(std::max<int64_t>(1, n));
+  CK(cudaMemsetAsync(sw.flags.p, 0, std::max<int64_t>(1, n) * sizeof(int), st));
+  DBuf<int> la, lb, chg, iota, keys_out;
+  la.alloc(std::max<int64_t>(1, n));
+  lb.alloc(std::max<int64_t>(1, n));
+  chg.alloc(1);
+  iota.alloc(std::max<int64_t>(1, n));
+  keys_out.alloc(std::max<int64_t>(1, n));
+  {
+    std::vector<int> h(static_cast<size_t>(n));
+    for (int64_t i = 0; i < n; ++i) h[i] = static_cast<int>(i);
+    if (n) CK(cudaMemcpyAsync(iota.p, h.data(), n * sizeof(int), cudaMemcpyHostToDevice, st));
+    CK(cudaStreamSynchronize(st));
+  }
+  for (int dir = 0; dir < 2; ++dir) {
+    DBuf<int>& order = dir == 0 ? sw.fwd : sw.bwd;
+    order.alloc(std::max<int64_t>(1, n));
+    CK(cudaMemsetAsync(la.p, 0, std::max<int64_t>(1, n) * sizeof(int), st));
+    int* cur = la.p;
+    int* nxt = lb.p;
+    int64_t steps = 0;
+    while (n > 0) {  // blocks of 16 steps; converged when a block changes nothing
+      CK(cudaMemsetAsync(chg.p, 0, sizeof(int), st));
+      for (int q = 0; q < 16; ++q, ++steps) {
+        if (dir == 0) k_level_iter<true><<<nblk(n), kT, 0, st>>>(n, A.ro.p, A.ci.p, cur, nxt, chg.p);
+        else k_level_iter<false><<<nblk(n), kT, 0, st>>>(n, A.ro.p, A.ci.p, cur, nxt, chg.p);
+        std::swap(cur, nxt);
+      }
+      count_launch(16);
+      int hc = 0;
+      CK(cudaMemcpyAsync(&hc, chg.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      if (!hc || steps > n + 16) break;
+    }
+    int maxlev = 0;
+    if (n > 0) {  // levels + 1 from the last block's changes bound: find the maximum on the host
+      std::vector<int> hl(static_cast<size_t>(n));
+      CK(cudaMemcpyAsync(hl.data(), cur, n * sizeof(int), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      for (int x : hl) maxlev = std::max(maxlev, x);
+      std::vector<int> off(static_cast<size_t>(maxlev) + 2, 0);  // level offsets in the sorted order
+      for (int x : hl) ++off[static_cast<size_t>(x) + 1];
+      for (int L = 0; L <= maxlev; ++L) off[L + 1] += off[L];
+      (dir == 0 ? sw.lvl_fwd : sw.lvl_bwd).upload(off);
+      int bits = 1;
+      while (bits < 31 && (maxlev >> bits) != 0) ++bits;
+      size_t bytes = 0;
+      CK(cub::DeviceRadixSort::SortPairs(nullptr, bytes, cur, keys_out.p, iota.p, order.p, static_cast<int>(n), 0, bits, st));
+      DBuf<unsigned char> tmp;
+      tmp.alloc(bytes);
+      CK(cub::DeviceRadixSort::SortPairs(tmp.p, bytes, cur, keys_out.p, iota.p, order.p, static_cast<int>(n), 0, bits, st));
+      // entry offsets of the rows in level order, and the widest level's entries / rows
+      std::vector<int64_t> hro(static_cast<size_t>(n) + 1);
+      std::vector<int> hord(static_cast<size_t>(n));
+      CK(cudaMemcpyAsync(hro.data(), A.ro.p, (n + 1) * 8, cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(hord.data(), order.p, n * sizeof(int), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      std::vector<int64_t> eo(static_cast<size_t>(n) + 1, 0);
+      for (int64_t t = 0; t < n; ++t) eo[t + 1] = eo[t] + (hro[hord[t] + 1] - hro[hord[t]]);
+      int64_t wide = 0, rows = 0;
+      for (int64_t i = 0; i < n; ++i) sw.max_row_len = std::max(sw.max_row_len, hro[i + 1] - hro[i]);
+      for (int L = 0; L <= maxlev; ++L) {
+        wide = std::max(wide, eo[off[L + 1]] - eo[off[L]]);
+        rows = std::max<int64_t>(rows, off[L + 1] - off[L]);
+      }
+      (dir == 0 ? sw.eoff_fwd : sw.eoff_bwd).upload(eo);
+      (dir == 0 ? sw.h_eo_fwd : sw.h_eo_bwd) = eo;
+      (dir == 0 ? sw.h_off_fwd : sw.h_off_bwd) = off;
+      sw.max_level_nnz = std::max(sw.max_level_nnz, wide);
+      sw.max_level_rows = std::max(sw.max_level_rows, rows);
+    }
+    (dir == 0 ? sw.levels_fwd : sw.levels_bwd) = maxlev + 1;
+  }
+  CK(cudaStreamSynchronize(st));
+  sw.ready = true;
+}
+
+// one sync-free Gauss-Seidel sweep of A on (r, zin) -> zout, rows in level order
+void gs_sweep(AmgHier* h, const DCsr& A, SweepState& sw, bool fwd, const double* r, const double* zin, double* zout) {
   cudaStream_t st = h->st;
   if (A.n == 0) return;
+  if (!sw.ready) {
+    PhaseClock pc{st};
+    sweep_prepare(A, sw, st);
+    if (amg_profile())
+      fprintf(stderr, "[amg] matrix n %lld nnz %lld: %d forward / %d backward levels\n", static_cast<long long>(A.n),
+              static_cast<long long>(A.nnz), sw.levels_fwd, sw.levels_bwd);
+    pc.lap("levels", A.n);
+  }
+  // small (coarse) matrices: one CTA, a barrier per batch of rows within a level
+  const int64_t zbytes = static_cast<int64_t>((A.n + 1) & ~1) * 8;
+  const int64_t cap = (static_cast<int64_t>(kCtaSweepSmem) - zbytes) / 8;
+  if (cap >= std::max<int64_t>(2048, sw.max_row_len)) {
+    const int64_t capu = std::min(cap, sw.max_level_nnz);
+    const size_t cta_smem = static_cast<size_t>(zbytes) + static_cast<size_t>(capu) * 8;
+    if (!sw.bat_fwd.p) {  // batches: split every level into runs of <= 512 rows and <= capu entries
+      for (int dir = 0; dir < 2; ++dir) {
+        const std::vector<int64_t>& eo = dir == 0 ? sw.h_eo_fwd : sw.h_eo_bwd;
+        const std::vector<int>& off = dir == 0 ? sw.h_off_fwd : sw.h_off_bwd;
+        std::vector<int> bt{0};
+        for (size_t L = 0; L + 1 < off.size(); ++L) {
+          int t0 = off[L];
+          while (t0 < off[L + 1]) {
+            int te = t0 + 1;
+            while (te < off[L + 1] && te - t0 < 512 && eo[te + 1] - eo[t0] <= capu) ++te;
+            bt.push_back(te);
+            t0 = te;
+          }
+        }
+        (dir == 0 ? sw.bat_fwd : sw.bat_bwd).upload(bt);
+        (dir == 0 ? sw.nbat_fwd : sw.nbat_bwd) = static_cast<int>(bt.size()) - 1;
+      }
+    }
+    static bool attr = false;
+    if (!attr) {
+      CK(cudaFuncSetAttribute(k_gs_cta<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kCtaSweepSmem)));
+      CK(cudaFuncSetAttribute(k_gs_cta<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kCtaSweepSmem)));
+      attr = true;
+    }
+    if (fwd)
+      k_gs_cta<true><<<1, 512, cta_smem, st>>>(static_cast<int>(A.n), A.ro.p, A.ci.p, A.v.p, r, zin, zout, sw.fwd.p,
+                                               sw.bat_fwd.p, sw.nbat_fwd, sw.eoff_fwd.p, h->status.p);
+    else
+      k_gs_cta<false><<<1, 512, cta_smem, st>>>(static_cast<int>(A.n), A.ro.p, A.ci.p, A.v.p, r, zin, zout, sw.bwd.p,
+                                                sw.bat_bwd.p, sw.nbat_bwd, sw.eoff_bwd.p, h->status.p);
+    count_launch();
+    return;
+  }
+  if (!getenv("HDR_GS_FLAGS")) {  // level-synchronous cooperative grid (default)
+    static int coop_grid = 0;
+    if (!coop_grid) {
+      int dev = 0, sms = 148, per = 1;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_gs_coop<true>, 512, 0);
+      coop_grid = sms * std::max(1, std::min(per, 2));
+    }
+    int nn = static_cast<int>(A.n);
+    const int64_t* aro = A.ro.p;
+    const int32_t* aci = A.ci.p;
+    const double* av = A.v.p;
+    const int* ord = fwd ? sw.fwd.p : sw.bwd.p;
+    const int* lv = fwd ? sw.lvl_fwd.p : sw.lvl_bwd.p;
+    int nlev = fwd ? sw.levels_fwd : sw.levels_bwd;
+    int* stp = h->status.p;
+    void* args[] = {&nn, &aro, &aci, &av, &r, &zin, &zout, &ord, &lv, &nlev, &stp};
+    CK(cudaLaunchCooperativeKernel(fwd ? reinterpret_cast<void*>(k_gs_coop<true>) : reinterpret_cast<void*>(k_gs_coop<false>),
+                                   dim3(coop_grid), dim3(512), args, 0, st));
+    count_launch();
+    return;
+  }
   ++h->epoch;
   CK(cudaMemsetAsync(h->ticket.p, 0, 8, st));
-  const unsigned grid = static_cast<unsigned>(std::min<int64_t>(nblk(A.n * 32), 148 * 8));
+  // enough warps for the widest levels, few enough that waiting warps do not crowd the flags
+  const unsigned grid = static_cast<unsigned>(std::min<int64_t>(nblk(A.n * 32), 148 * 2));
   if (fwd)
-    k_gs_sweep<true><<<grid, kT, 0, st>>>(A.n, A.ro.p, A.ci.p, A.v.p, r, zin, zout, flags.p, h->epoch, h->ticket.p,
-                                          h->status.p);
+    k_gs_sweep<true><<<grid, kT, 0, st>>>(A.n, A.ro.p, A.ci.p, A.v.p, r, zin, zout, sw.flags.p, h->epoch, h->ticket.p,
+                                          h->status.p, sw.fwd.p);
   else
-    k_gs_sweep<false><<<grid, kT, 0, st>>>(A.n, A.ro.p, A.ci.p, A.v.p, r, zin, zout, flags.p, h->epoch, h->ticket.p,
-                                           h->status.p);
+    k_gs_sweep<false><<<grid, kT, 0, st>>>(A.n, A.ro.p, A.ci.p, A.v.p, r, zin, zout, sw.flags.p, h->epoch, h->ticket.p,
+                                           h->status.p, sw.bwd.p);
   count_launch();
 }
 
@@ -830,14 +1164,18 @@ static void v_cycle(AmgHier* h, size_t level, const double* r, double* z) {
   cudaStream_t st = h->st;
   if (level == h->levels.size()) {
     if (h->coarse.n > 0) {
-      k_coarse_solve<<<1, 32, 0, st>>>(static_cast<int>(h->coarse.n), h->coarse_lu.p, h->coarse_piv.p, r, z);
+      const size_t sm = static_cast<size_t>(h->coarse.n) * 16;
+      if (sm > 48 * 1024) CK(cudaFuncSetAttribute(k_coarse_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
+      k_coarse_solve<<<1, 1024, sm, st>>>(static_cast<int>(h->coarse.n), h->coarse_lu.p, h->coarse_piv.p, r, z);
       count_launch();
     }
     return;
   }
   AmgLevel& L = *h->levels[level];
   const int64_t n = L.A.n;
-  gs_sweep(h, L.A, L.flags, true, r, nullptr, L.z.p);  // z = 0, forward sweep
+  PhaseClock pc{st};
+  gs_sweep(h, L.A, L.sw, true, r, nullptr, L.z.p);  // z = 0, forward sweep
+  pc.lap("fwd sweep", static_cast<int64_t>(level));
   k_resid<<<nblk(n), kT, 0, st>>>(n, L.A.ro.p, L.A.ci.p, L.A.v.p, L.z.p, r, L.res.p);
   k_spmv<<<nblk(L.R.n), kT, 0, st>>>(L.R.n, L.R.ro.p, L.R.ci.p, L.R.v.p, L.res.p, L.cr.p);
   count_launch(2);
@@ -846,17 +1184,21 @@ static void v_cycle(AmgHier* h, size_t level, const double* r, double* z) {
   v_cycle(h, level + 1, L.cr.p, cz);
   k_prolong_add<<<nblk(n), kT, 0, st>>>(n, L.P.ro.p, L.P.ci.p, L.P.v.p, cz, L.z.p);
   count_launch();
-  gs_sweep(h, L.A, L.flags, false, r, L.z.p, z);  // backward sweep from z
+  pc.lap("coarser", static_cast<int64_t>(level));
+  gs_sweep(h, L.A, L.sw, false, r, L.z.p, z);  // backward sweep from z
+  pc.lap("bwd sweep", static_cast<int64_t>(level));
 }
 
 void amg_apply_device(AmgHier* h, const double* r, double* z) {
+  PhaseClock pc{h->st};
   v_cycle(h, 0, r, z);
+  pc.lap("v-cycle", 0);
 }
 
 // symmetric Gauss-Seidel (ssgs_setup's apply, solvers.cpp:60-72)
-void sgs_apply_device(AmgHier* h, const DCsr& A, DBuf<int>& flags, double* zf, const double* r, double* z) {
-  gs_sweep(h, A, flags, true, r, nullptr, zf);
-  gs_sweep(h, A, flags, false, r, zf, z);
+void sgs_apply_device(AmgHier* h, const DCsr& A, SweepState& sw, double* zf, const double* r, double* z) {
+  gs_sweep(h, A, sw, true, r, nullptr, zf);
+  gs_sweep(h, A, sw, false, r, zf, z);
 }
 
 hdr_status amg_status(AmgHier* h) {
@@ -1071,10 +1413,8 @@ hdr_status hdr_csr_precond_apply_host(int64_t n, const int64_t* ro, const int64_
       return HDR_OK;
     }
     std::unique_ptr<hdr::AmgHier, void (*)(hdr::AmgHier*)> ctx(hdr::sweep_context(n, nullptr), hdr::amg_destroy);
-    hdr::DBuf<int> flags;
-    flags.alloc(std::max<int64_t>(1, n));
-    CK(cudaMemset(flags.p, 0, std::max<int64_t>(1, n) * sizeof(int)));
-    hdr::sgs_apply_device(ctx.get(), a, flags, hdr::sweep_scratch(ctx.get()), dr.p, dz.p);
+    hdr::SweepState sw;
+    hdr::sgs_apply_device(ctx.get(), a, sw, hdr::sweep_scratch(ctx.get()), dr.p, dz.p);
     const hdr_status s = hdr::amg_status(ctx.get());
     if (s != HDR_OK) return s;
     if (n) CK(cudaMemcpy(z, dz.p, n * 8, cudaMemcpyDeviceToHost));

@@ -139,7 +139,7 @@ hdr_status pcg_device(int64_t n, const int64_t* ro, const int32_t* ci32, const i
   two.alloc(2);
   const double* dv = nullptr;
   std::unique_ptr<AmgHier, void (*)(AmgHier*)> hier(nullptr, amg_destroy);
-  DBuf<int> flags;
+  SweepState sw;
   if (precond == 1 || precond == 2) {  // jacobi_setup / ssgs_setup: positive_inv_diag
     const int64_t bad = positive_inv_diag(A, dinv, st);
     if (bad >= 0) return fail(HDR_VALIDATION, "ZeroDiagonal: non-positive diagonal entry at row " + std::to_string(bad));
@@ -147,8 +147,7 @@ hdr_status pcg_device(int64_t n, const int64_t* ro, const int32_t* ci32, const i
   }
   if (precond == 2) {
     hier.reset(sweep_context(n, st));
-    flags.alloc(std::max<int64_t>(1, n));
-    CK(cudaMemsetAsync(flags.p, 0, std::max<int64_t>(1, n) * sizeof(int), st));
+
   } else if (precond == 3) {  // amg_preconditioner with default AmgOptions
     hdr_amg_options o;
     hdr_amg_default_options(&o);
@@ -158,7 +157,7 @@ hdr_status pcg_device(int64_t n, const int64_t* ro, const int32_t* ci32, const i
   }
   const bool general = precond >= 2;  // z = M^-1 r is not fused into the update
   auto apply = [&](const double* in, double* out) -> hdr_status {
-    if (precond == 2) sgs_apply_device(hier.get(), A, flags, sweep_scratch(hier.get()), in, out);
+    if (precond == 2) sgs_apply_device(hier.get(), A, sw, sweep_scratch(hier.get()), in, out);
     else amg_apply_device(hier.get(), in, out);
     return amg_status(hier.get());
   };
