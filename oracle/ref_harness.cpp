@@ -247,8 +247,13 @@ int cmd_dump(const std::map<std::string, std::string>& kv) {
   // (rtol, maxit of RunConfig) with each preconditioner
   if (kv.count("amg") && kv.at("amg") == "1" && hyb.h_mat.nrows > 0) {
     const double rtol = kv.count("rtol") ? std::stod(kv.at("rtol")) : 1e-12;
+    AmgOptions aopt;  // amg_theta / amg_cap / amg_levels / amg_omega: non-default AmgOptions
+    if (kv.count("amg_theta")) aopt.strength_threshold = std::stod(kv.at("amg_theta"));
+    if (kv.count("amg_cap")) aopt.coarse_cap = std::stoll(kv.at("amg_cap"));
+    if (kv.count("amg_levels")) aopt.max_levels = std::stoi(kv.at("amg_levels"));
+    if (kv.count("amg_omega")) aopt.omega_factor = std::stod(kv.at("amg_omega"));
     const double ts0 = now();
-    const AmgHierarchy ah = amg_setup(hyb.h_mat);
+    const AmgHierarchy ah = amg_setup(hyb.h_mat, aopt);
     const double ts1 = now();
     std::fprintf(stderr, "{\"amg_setup_s\": %.4f}\n", ts1 - ts0);
     w.q("amg.levels", {static_cast<index_t>(ah.levels.size())});

@@ -194,7 +194,7 @@ def read_dump(path) -> dict:
 
 
 def run_ref_dump(out_path, dim, cells, k, coef, seed, weighted=False, blocks=True, essential=False,
-                 nullspace=False, amg=False) -> dict:
+                 nullspace=False, amg=False, amg_options=None) -> dict:
     """Runs the reference (oracle/_ref/ref_harness) and reads its dump (essential:
     every boundary face eliminated first, eliminate_essential)."""
     if not REF_HARNESS.exists():
@@ -202,6 +202,8 @@ def run_ref_dump(out_path, dim, cells, k, coef, seed, weighted=False, blocks=Tru
     args = [str(REF_HARNESS), "dump", f"out={out_path}", f"dim={dim}", "cells=" + ",".join(map(str, cells)),
             f"k={k}", f"coef={coef}", f"seed={seed}", f"weighted={int(weighted)}", f"blocks={int(blocks)}",
             f"essential={int(essential)}", f"nullspace={int(nullspace)}", f"amg={int(amg)}"]
+    for key, val in (amg_options or {}).items():  # amg_theta, amg_cap, amg_levels, amg_omega
+        args.append(f"{key}={val}")
     subprocess.run(args, check=True, env={**os.environ, "HDIVRED_NUM_THREADS": "1"})
     return read_dump(out_path)
 

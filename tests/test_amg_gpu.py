@@ -136,3 +136,33 @@ def test_amg_setup_failed_on_nonpositive_diagonal():
     ro = np.searchsorted(np.array(rows), np.arange(n + 1))
     with pytest.raises(hd.SetupFailed):
         hd.AmgHierarchy((n, n, ro, np.array(cols), np.array(vals)))
+
+
+@pytest.mark.parametrize("opts", [
+    {"amg_theta": 0.25, "amg_cap": 200},
+    {"amg_theta": 0.02, "amg_levels": 2},
+    {"amg_omega": 0.5, "amg_cap": 16},
+])
+def test_nondefault_options_bit_identical(opts):
+    """AmgOptions (amg.hpp:12-19) other than the defaults: the same hierarchy and cycle."""
+    with tempfile.TemporaryDirectory() as td:
+        d = run_ref_dump(Path(td) / "d.bin", 3, (8, 8, 8), 1, "softhard:4", 5, blocks=False, amg=True,
+                         amg_options=opts)
+    names = {"amg_theta": "strength_threshold", "amg_cap": "coarse_cap", "amg_levels": "max_levels",
+             "amg_omega": "omega_factor"}
+    amg = hd.AmgHierarchy(csr(d, "H"), **{names[k_]: v for k_, v in opts.items()})
+    assert amg.nlevels == int(d["amg.levels"][0])
+    for lvl in range(amg.nlevels):
+        for w in ("A", "P", "R"):
+            for a, b in zip(amg.matrix(lvl, w)[2:], csr(d, f"amg.{w}{lvl}")[2:]):
+                assert np.array_equal(a, b)
+    assert np.array_equal(amg.apply(d["g"]), d["amg.z"])
+
+
+def test_pcg_zero_rhs_and_zero_diagonal():
+    ro = np.array([0, 2, 4])
+    ci = np.array([0, 1, 0, 1])
+    x, rep = hd.pcg((2, 2, ro, ci, np.array([2.0, 1.0, 1.0, 2.0])), np.zeros(2), precond="amg")
+    assert rep["converged"] and rep["iterations"] == 0 and np.all(x == 0)
+    with pytest.raises(hd.ValidationError):  # ZeroDiagonal (solvers.cpp:32-44)
+        hd.pcg((2, 2, ro, ci, np.array([0.0, 1.0, 1.0, 2.0])), np.ones(2), precond="sgs")
