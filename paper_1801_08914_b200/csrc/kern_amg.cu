@@ -446,7 +446,27 @@ __global__ void __launch_bounds__(512) k_gs_cta(int n, const int64_t* ro, const 
   extern __shared__ double zs[];  // n new values, then the products of one batch of rows
   double* pb = zs + ((n + 1) & ~1);
   __shared__ double dg[512];
+  __shared__ int dpos[512];  // the row's split point: entries before it, resp. from it, are folded
+  __shared__ int ntail[512];  // forward sweep from zero: some skipped term is -0 (v has its sign bit set)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  // Only the terms of the dependencies need the level order.  Forward sweep from
+  // zero (zin == nullptr): the terms after the diagonal are v * 0 = +-0, which
+  // leave every running sum unchanged except -0 - (-0) = +0: they reduce to a
+  // sign fix-up.  Backward sweep: the terms before the diagonal use zin only, so
+  // their part of the ordered fold runs for every row up front, in parallel.
+  const bool fwd_zero = FWD && zin == nullptr;
+  if (!FWD) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      double sacc = r[i];
+      for (int64_t k = ro[i]; k < ro[i + 1]; ++k) {
+        const int c = ci[k];
+        if (c >= i) break;  // columns ascending: the rest are the diagonal and the dependencies
+        sacc = __dsub_rn(sacc, __dmul_rn(v[k], zin ? zin[c] : 0.0));
+      }
+      zs[i] = sacc;  // the row's partial sum until the row itself is swept
+    }
+    __syncthreads();
+  }
   // batches: rows [bat[j], bat[j + 1]) of one level, at most 512 rows and the buffer's entries
   for (int j = 0; j < nbat; ++j) {
     const int t0 = __ldg(bat + j), t1 = __ldg(bat + j + 1);
@@ -454,25 +474,42 @@ __global__ void __launch_bounds__(512) k_gs_cta(int n, const int64_t* ro, const 
     for (int t = t0 + warp; t < t1; t += nw) {  // products, warp per row
       const int i = order[t];
       const int64_t a = ro[i], b = ro[i + 1], dst = eoff[t] - e0 - a;
+      bool neg = false;
       for (int64_t k = a + lane; k < b; k += 32) {
         const int c = ci[k];
+        const double vk = v[k];
         double p = 0.0;
-        if (c != i) {
-          const bool dep = FWD ? c < i : c > i;
-          p = __dmul_rn(v[k], dep ? zs[c] : (zin ? zin[c] : 0.0));
+        if (c == i) {
+          dg[t - t0] = vk;
+          dpos[t - t0] = static_cast<int>(k - a);
+        } else if (FWD ? c < i : c > i) {
+          p = __dmul_rn(vk, zs[c]);
+        } else if (fwd_zero) {
+          neg = neg || signbit(vk);
         } else {
-          dg[t - t0] = v[k];
+          p = __dmul_rn(vk, zin ? zin[c] : 0.0);
         }
         pb[dst + k] = p;
       }
+      neg = __any_sync(0xffffffffu, neg);
+      if (lane == 0) ntail[t - t0] = neg ? 1 : 0;
     }
     __syncthreads();
     for (int t = t0 + threadIdx.x; t < t1; t += blockDim.x) {  // folds, thread per row
       const int i = order[t];
-      const int64_t q0 = eoff[t] - e0, q1 = eoff[t + 1] - e0;
-      double sacc = r[i];
+      const int64_t q0 = eoff[t] - e0, q1 = eoff[t + 1] - e0, qd = q0 + dpos[t - t0];
+      double sacc;
+      if (FWD) {
+        sacc = r[i];
+        const int64_t qe = fwd_zero ? qd : q1;  // the diagonal's slot holds +0: stopping there is exact
 #pragma unroll 8
-      for (int64_t q = q0; q < q1; ++q) sacc = __dsub_rn(sacc, pb[q]);
+        for (int64_t q = q0; q < qe; ++q) sacc = __dsub_rn(sacc, pb[q]);
+        if (fwd_zero && ntail[t - t0] && sacc == 0.0) sacc = 0.0;  // -0 - (-0) = +0
+      } else {
+        sacc = zs[i];  // r_i minus the terms before the diagonal
+#pragma unroll 8
+        for (int64_t q = qd + 1; q < q1; ++q) sacc = __dsub_rn(sacc, pb[q]);
+      }
       const double d = dg[t - t0];
       if (d == 0.0) atomicOr(status, 1);
       zs[i] = sacc / d;
@@ -1080,8 +1117,9 @@ void gs_sweep(AmgHier* h, const DCsr& A, SweepState& sw, bool fwd, const double*
     PhaseClock pc{st};
     sweep_prepare(A, sw, st);
     if (amg_profile())
-      fprintf(stderr, "[amg] matrix n %lld nnz %lld: %d forward / %d backward levels\n", static_cast<long long>(A.n),
-              static_cast<long long>(A.nnz), sw.levels_fwd, sw.levels_bwd);
+      fprintf(stderr, "[amg] matrix n %lld nnz %lld: %d forward / %d backward levels, longest row %lld, widest level %lld entries\n",
+              static_cast<long long>(A.n), static_cast<long long>(A.nnz), sw.levels_fwd, sw.levels_bwd,
+              static_cast<long long>(sw.max_row_len), static_cast<long long>(sw.max_level_nnz));
     pc.lap("levels", A.n);
   }
   // small (coarse) matrices: one CTA, a barrier per batch of rows within a level
@@ -1106,6 +1144,8 @@ void gs_sweep(AmgHier* h, const DCsr& A, SweepState& sw, bool fwd, const double*
         }
         (dir == 0 ? sw.bat_fwd : sw.bat_bwd).upload(bt);
         (dir == 0 ? sw.nbat_fwd : sw.nbat_bwd) = static_cast<int>(bt.size()) - 1;
+        if (amg_profile()) fprintf(stderr, "[amg] n %lld: one-CTA sweep, %d batches (%s)\n", static_cast<long long>(A.n),
+                                   static_cast<int>(bt.size()) - 1, dir == 0 ? "fwd" : "bwd");
       }
     }
     static bool attr = false;
