@@ -150,6 +150,18 @@ int main(int argc, char** argv) {
   const std::unique_ptr<Preconditioner> pc_ref = amg_preconditioner(ref.h_mat);
   const auto ref_solve = pcg(ref.h_mat, pc_ref.get(), g_ref, 1e-12, 2000);
   const auto dev_solve = hdivred_b200::pcg(ref.h_mat, PrecondKind::amg, g_ref, 1e-12, 2000);
+  // every PrecondKind through the shim's pcg on the reference's H: the same iteration counts
+  bool all_kinds = true;
+  for (const auto kind : {PrecondKind::none, PrecondKind::jacobi, PrecondKind::sgs, PrecondKind::amg}) {
+    const std::unique_ptr<Preconditioner> pk = kind == PrecondKind::none  ? nullptr
+                                               : kind == PrecondKind::jacobi ? jacobi_setup(ref.h_mat)
+                                               : kind == PrecondKind::sgs    ? ssgs_setup(ref.h_mat)
+                                                                             : amg_preconditioner(ref.h_mat);
+    const auto rs = pcg(ref.h_mat, pk.get(), g_ref, 1e-12, 5000);
+    const auto ds = hdivred_b200::pcg(ref.h_mat, kind, g_ref, 1e-12, 5000);
+    all_kinds = all_kinds && std::llabs(static_cast<long long>(rs.second.iterations - ds.second.iterations)) <= 1 &&
+                ds.second.converged == rs.second.converged;
+  }
   // near_nullspace_check, bit-identical (small meshes: dense m x m)
   bool ns_identical = true;
   if (ref.h_mat.nrows <= 600) ns_identical = near_nullspace_check(sp, co) == hdivred_b200::near_nullspace_check(sp, co);
@@ -163,7 +175,7 @@ int main(int argc, char** argv) {
               "\"fe_x_cond_rel\": %.3e, \"solve_hyb_alg_rel\": %.3e, \"solve_hyb_fe_rel\": %.3e, "
               "\"solve_cond_alg_rel\": %.3e, \"solve_cond_fe_rel\": %.3e, \"pcg_iterations\": [%lld, %lld, %lld, %lld, %lld, %lld], "
               "\"amg_iterations\": [%lld, %lld], \"solve_amg_fe_rel\": %.3e, \"amg_ref_matrix_iterations\": [%lld, %lld], "
-              "\"amg_ref_matrix_x_rel\": %.3e, \"nullspace_identical\": %s}\n",
+              "\"amg_ref_matrix_x_rel\": %.3e, \"nullspace_identical\": %s, \"all_precond_iterations_match\": %s}\n",
               n, k, pattern ? "true" : "false", dh / mh, dg / (mg > 0 ? mg : 1), spat ? "true" : "false", ds / ms,
               y_ref == y_gpu ? "true" : "false", apat ? "true" : "false", asym ? "true" : "false",
               rel(ref.h_mat.values, ahyb.h_mat.values), rel(g_ref, g_alg), rel(xh_ref, xh_alg), rel(x_ref, x_alg),
@@ -174,6 +186,6 @@ int main(int argc, char** argv) {
               static_cast<long long>(itc_alg), static_cast<long long>(itc_fe), static_cast<long long>(ita_ref),
               static_cast<long long>(ita_fe), rel(xa_ref, xa_fe), static_cast<long long>(ref_solve.second.iterations),
               static_cast<long long>(dev_solve.second.iterations), rel(ref_solve.first, dev_solve.first),
-              ns_identical ? "true" : "false");
-  return (pattern && spat && y_ref == y_gpu && apat && asym && acpat && ns_identical) ? 0 : 1;
+              ns_identical ? "true" : "false", all_kinds ? "true" : "false");
+  return (pattern && spat && y_ref == y_gpu && apat && asym && acpat && ns_identical && all_kinds) ? 0 : 1;
 }

@@ -47,4 +47,5 @@ def test_dropin_against_reference(n, k):
     ir_ref, ir_dev = line["amg_ref_matrix_iterations"]
     assert abs(ir_ref - ir_dev) <= 1 and line["amg_ref_matrix_x_rel"] < 1e-8, line
     assert line["nullspace_identical"], line
+    assert line["all_precond_iterations_match"], line  # none / jacobi / sgs / amg through the shim's pcg
     print(line)
