@@ -101,6 +101,28 @@ def test_hybridize_moderate_meshes_vs_dd(dim, cells, k, coef):
     assert rel_err(gv, o.get("g_dd")) <= TOL
 
 
+@pytest.mark.parametrize("cells,coef", [
+    ((1, 1, 5), "logu:1e-2:1e2"), ((7, 1, 1), "logu:1e-3:1e3"), ((2, 3, 1), "softhard:4"), ((1, 4, 3), "logu:1e-2:1e2"),
+    ((9, 2, 2), "checker:1e-2:1e2"), ((3, 3, 3), "uniform:2:0.5"),
+])
+def test_rt1_tensor_core_correction_thin_meshes_vs_dd(cells, coef):
+    """RT1 hexes (the mma.sync 3xTF32 correction, the prefetched [N0 f ; X^T f]):
+    one-cell-thick meshes, so cells with every count of interior faces, incl. none;
+    H, g and the recovery against the double-double oracle, no cell rejected."""
+    o = Oracle(3, cells, 1)
+    o.gen_inputs(coef, 31)
+    o.run("port_hybridize")
+    o.run("dd_hybridize")
+    o.run("dd_recover")
+    sp = hd.Space(3, cells, 1)
+    op = sp.hybridize(o.get("alpha"), o.get("beta"), o.get("f_hat"))
+    hv, gv = op.values()
+    assert op.exact_cells() == 0
+    assert rel_err(hv, o.get("H.values_dd")) <= TOL and rel_err(gv, o.get("g_dd")) <= TOL
+    x_hat, _ = op.recover(o.get("lambda"), o.get("f_hat"))
+    assert rel_err(x_hat, o.get("x_hat_dd")) <= TOL
+
+
 @pytest.mark.parametrize("dim,cells,coef", [
     (3, (8, 8, 8), "logu:1e-2:1e2"), (3, (37, 5, 7), "logu:1e-3:1e3"), (3, (70, 3, 2), "checker:1e-2:1e2"),
     (3, (1, 1, 9), "logu:1e-2:1e2"), (2, (64, 64), "uniform:1:1"), (2, (75, 9), "logu:1e-2:1e2"), (2, (1, 13), "logu:1e-2:1e2"),
