@@ -257,7 +257,7 @@ def kernel_name(cfg: dict) -> str:
     if cfg.get("perturb"):
         return "k_piola_gemm + k_spd_hyb + k_run_sum"
     if cfg["k"] == 0:
-        return "k_rt0_brick<dim,0> + k_rt0_brick<dim,1> (colour passes; k_rt0_cell below the brick size)"
+        return "k_rt0_pencil<dim> (one pass; the exact-path tail k_rt0_exact returns at once)"
     if cfg["dim"] == 3 and cfg["k"] >= 2:
         return "k_hyb_big<k> x2 colours"
     return "k_hyb_warp x2 colours"

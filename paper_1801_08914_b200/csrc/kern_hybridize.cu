@@ -1360,6 +1360,31 @@ void launch_hybridize_rt0_rows(const HybArgs& a, const double* hc, double* stage
     c.lam = hc[5 * N * N + N];
     c.rho = hc[5 * N * N + N + 1];
   };
+  // one-pass pencil kernel (kern_pencil.cu) when the element has its structure;
+  // the older variants stay selectable (HDR_RT0_ROWS / _CELL / _BRICK, A/B timing)
+  const bool forced = getenv("HDR_RT0_ROWS") || getenv("HDR_RT0_CELL") || getenv("HDR_RT0_BRICK") || getenv("HDR_RT0_NO_PENCIL");
+  if (!forced) {
+    PencilConst<3> p3;
+    PencilConst<2> p2;
+    const bool ok = a.m.dim == 3 ? pencil_setup<3>(hc, p3) : pencil_setup<2>(hc, p2);
+    if (ok) {
+      if (a.m.dim == 3) launch_rt0_pencil<3>(a, p3, st);
+      else launch_rt0_pencil<2>(a, p2, st);
+      cudaLaunchConfig_t xc{};
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[0].val.programmaticStreamSerializationAllowed = getenv("HDR_NO_PDL") ? 0 : 1;
+      xc.gridDim = dim3(1);
+      xc.blockDim = dim3(256);
+      xc.stream = st;
+      xc.attrs = attr;
+      xc.numAttrs = 1;
+      if (a.m.dim == 3) cudaLaunchKernelEx(&xc, k_rt0_exact<3>, a);
+      else cudaLaunchKernelEx(&xc, k_rt0_exact<2>, a);
+      count_launch();
+      return;
+    }
+  }
   // lane-per-row variant: A/B timing, or when the element lacks the structure of Rt0Fast
   bool rows = getenv("HDR_RT0_ROWS") != nullptr;
   Rt0Fast<6> f3{};

@@ -1,0 +1,369 @@
+// k = 0 hybridize in one pass: the pencil kernel (hybridize, src/reduction.cpp:262-354,
+// with element_matrices / assemble_from_reference, src/rt_space.cpp:345-374, and
+// the from_triplets scatter, src/csr.cpp:43-75).
+//
+// The RT0 reference element of an axis-aligned box (build_reference,
+// src/rt_space.cpp:180-314) has
+//   D = c 1 1^T                  (div of every RT0 basis function is the same constant:
+//                                 every entry carries the same bits, checked on the host)
+//   M = blockdiag(M_0, .., M_d-1) (2 x 2 per axis, cross-axis entries exactly 0)
+// so the reference's A_T = fl(fl(alpha D) + fl(beta M)) is, exactly,
+//   A_T = gamma 1 1^T + P,   gamma = fl(alpha c),   P = blockdiag(P_a),
+//   P_a[i][j] = A_T[i][j] - gamma   (Sterbenz / one rounding: the 2 x 2 mass blocks
+//                                    are well conditioned, cond ~ 3)
+// and by Sherman-Morrison, with u = P^-1 1 and sigma = 1^T u,
+//   A_T^-1 = P^-1 - kappa u u^T,   kappa = gamma / (1 + gamma sigma),
+//   A_T^-1 f = P^-1 f - kappa u (u . f).
+// Every term is a sum of same-signed quantities or a rank-one correction whose
+// size is bounded by |P^-1|, so the result is within a few ulp of max|A_T^-1|
+// whatever alpha / beta: the inverse of the reference's rounded A_T, not of the
+// unrounded one.  H_T = C_T A_T^-1 C_T^T is the interior-face block of A_T^-1
+// (unit constraint rows of build_C, src/reduction.cpp:172-181).
+//
+// Acceptance (DESIGN.md §2 "Fail-safe"): a cell whose condition bound
+// (1 + gamma sigma) max tr(P_a) max tr(P_a)/det(P_a) exceeds kPencilCond, or whose
+// blocks are not positive definite, contributes zeros and is listed for the
+// exact double-double path (k_rt0_exact, the reference's SingularBlock rule):
+// the reference's LU pivots of an accepted SPD cell are >= lambda_min / G >= 1e-12 / G
+// of the block maximum (G <= 2^(n-1) = 32 the partial-pivoting growth), above its
+// 1e-14 threshold.  BASELINE config 2's worst cell has a bound of ~5e9; the bound
+// grows like h^-2 alpha / beta.
+//
+// Scatter.  One warp per 32-cell segment of an x-line (lane = cell).  The H row of
+// the interior face between cells T- and T+ (T+ the cell on the face's plus side) is
+// assembled by T+'s lane: T-'s row comes from lane - 1 (x faces: a shuffle, or the
+// previous warp's last lane through shared memory) or is recomputed from T-'s
+// inputs (y, z faces: the cell below / behind, an L1 / L2 hit).  Rows of
+// consecutive lanes are consecutive rows of H (interior faces of one line, face
+// order), so a warp stages its rows in shared memory and writes them out as one
+// contiguous, coalesced segment.  No staging in HBM, no colouring, one launch; every
+// H entry and g entry is written exactly once; the two contributions to a diagonal
+// entry / g entry meet as fl(h(T-) + h(T+)), the reference's two-term sum.
+#include "hdr_device.cuh"
+#include "kernels.hpp"
+
+namespace hdr {
+
+namespace {
+
+constexpr int kPW = 8;              // warps per CTA
+#ifndef HDR_PENCIL_MINB
+#define HDR_PENCIL_MINB 1               // CTAs per SM asked of ptxas
+#endif
+constexpr double kPencilCond = 1e12;  // acceptance bound on cond(A_T)
+
+template <int DIM>
+struct PencilSol {  // A_T^-1 = P^-1 - kappa u u^T and A_T^-1 f in compact form
+  double i00[DIM], i01[DIM], i11[DIM];  // P_a^-1
+  double u[2 * DIM];
+  double pf[2 * DIM];  // P^-1 f
+  double kap, uf;      // kappa, u . f
+};
+
+__device__ __forceinline__ double rcp64(double d) {  // ~1 ulp reciprocal: MUFU seed + two Newton steps
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
+  double e = fma(-d, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-d, r, 1.0);
+  return fma(r, e, r);
+}
+
+// the compact solution of one cell; false: not accepted (not SPD, or the condition
+// bound is above kPencilCond, or non-finite); cond: the bound
+template <int DIM>
+__device__ __forceinline__ bool pencil_solve(const PencilConst<DIM>& pc, double a, double b, const double (&f)[2 * DIM],
+                                             PencilSol<DIM>& s, double& cond) {
+  const double gam = __dmul_rn(a, pc.c);  // fl(alpha D_ij), every ij
+  double sig = 0.0, tmax = 0.0, rmax = 0.0, uf = 0.0;
+  bool pd = gam >= 0.0;
+#pragma unroll
+  for (int ax = 0; ax < DIM; ++ax) {
+    // the reference's A_T entries of this axis block, minus gamma (no contraction)
+    const double p00 = __dsub_rn(__dadd_rn(gam, __dmul_rn(b, pc.md0[ax])), gam);
+    const double p11 = __dsub_rn(__dadd_rn(gam, __dmul_rn(b, pc.md1[ax])), gam);
+    const double p01 = __dsub_rn(__dadd_rn(gam, __dmul_rn(b, pc.mo[ax])), gam);
+    const double det = fma(p00, p11, -(p01 * p01));
+    pd = pd && p00 > 0.0 && det > 0.0;
+    const double id = rcp64(det);
+    s.i00[ax] = p11 * id;
+    s.i11[ax] = p00 * id;
+    s.i01[ax] = -p01 * id;
+    s.u[2 * ax] = s.i00[ax] + s.i01[ax];
+    s.u[2 * ax + 1] = s.i01[ax] + s.i11[ax];
+    sig += s.u[2 * ax] + s.u[2 * ax + 1];
+    const double tr = p00 + p11;
+    tmax = fmax(tmax, tr);
+    rmax = fmax(rmax, tr * id);  // >= 1 / lambda_min(P_a)
+    const double f0 = f[2 * ax], f1 = f[2 * ax + 1];
+    s.pf[2 * ax] = fma(s.i00[ax], f0, s.i01[ax] * f1);
+    s.pf[2 * ax + 1] = fma(s.i01[ax], f0, s.i11[ax] * f1);
+    uf = fma(s.u[2 * ax], f0, fma(s.u[2 * ax + 1], f1, uf));
+  }
+  const double den = fma(gam, sig, 1.0);
+  s.kap = gam * rcp64(den);
+  s.uf = uf;
+  cond = den * tmax * rmax;
+  return pd && cond <= kPencilCond && s.kap == s.kap && fabs(s.kap) < 1e300 && fabs(uf) < 1e300;
+}
+
+template <int DIM>
+__device__ __forceinline__ void pencil_zero(PencilSol<DIM>& s) {
+#pragma unroll
+  for (int ax = 0; ax < DIM; ++ax) s.i00[ax] = s.i01[ax] = s.i11[ax] = 0.0;
+#pragma unroll
+  for (int i = 0; i < 2 * DIM; ++i) s.u[i] = s.pf[i] = 0.0;
+  s.kap = s.uf = 0.0;
+}
+
+// row r of [A_T^-1 | A_T^-1 f]
+template <int DIM>
+__device__ __forceinline__ void pencil_row(const PencilSol<DIM>& s, int r, double (&h)[2 * DIM + 1]) {
+  constexpr int N = 2 * DIM;
+  const double kr = s.kap * s.u[r];
+  const int ar = r >> 1;
+#pragma unroll
+  for (int j = 0; j < N; ++j) {
+    double pinv = 0.0;
+    if ((j >> 1) == ar) pinv = (r & 1) ? ((j & 1) ? s.i11[ar] : s.i01[ar]) : ((j & 1) ? s.i01[ar] : s.i00[ar]);
+    h[j] = fma(-kr, s.u[j], pinv);
+  }
+  h[N] = fma(-kr, s.uf, s.pf[r]);
+}
+
+template <int DIM>
+__device__ __forceinline__ void load_cell(const HybArgs& A, int64_t e, double& a, double& b, double (&f)[2 * DIM]) {
+  a = __ldg(A.alpha + e);
+  b = __ldg(A.beta + e);
+  const double2* fp = reinterpret_cast<const double2*>(A.f + e * (2 * DIM));
+#pragma unroll
+  for (int j = 0; j < DIM; ++j) {
+    const double2 v = __ldg(fp + j);
+    f[2 * j] = v.x;
+    f[2 * j + 1] = v.y;
+  }
+}
+
+// the solution of a neighbour cell (zero when the cell is not accepted: its own
+// lane lists it for the exact path)
+template <int DIM>
+__device__ __forceinline__ void neighbour(const HybArgs& A, const PencilConst<DIM>& pc, int64_t e, PencilSol<DIM>& s) {
+  double a, b, f[2 * DIM], cond;
+  load_cell<DIM>(A, e, a, b, f);
+  if (!pencil_solve<DIM>(pc, a, b, f, s, cond) || A.force_exact) pencil_zero<DIM>(s);
+}
+
+// the same from prefetched inputs (zero for lanes without a cell)
+template <int DIM>
+__device__ __forceinline__ void solved_neighbour(const HybArgs& A, const PencilConst<DIM>& pc, bool valid, double a,
+                                                 double b, const double (&f)[2 * DIM], PencilSol<DIM>& s) {
+  double cond;
+  if (!valid || !pencil_solve<DIM>(pc, a, b, f, s, cond) || A.force_exact) pencil_zero<DIM>(s);
+}
+
+// Warp-collective: the H rows (and g entries) of the lanes with `has`, faces of
+// axis ax; hm = T-'s row (its slot 2 ax + 1), hp = T+'s row (slot 2 ax); c = T+'s
+// coordinates.  Column order (interior faces of T- and T+ in face order; T- and
+// T+ differ in coordinate ax): per axis b = 0..dim-1,
+//   b == ax: [T-.lo_b], diagonal, [T+.hi_b]
+//   b <  ax: T-.lo_b, T-.hi_b, T+.lo_b, T+.hi_b
+//   b >  ax: T-.lo_b, T+.lo_b, T-.hi_b, T+.hi_b
+// (lo_b / hi_b present when interior, the same for T- and T+ when b != ax).
+template <int DIM>
+__device__ __forceinline__ void emit_rows(const HybArgs& A, int ax, bool has, const int (&c)[3], const int (&nc)[3],
+                                          longlong2 fq, const double (&hm)[2 * DIM + 1], const double (&hp)[2 * DIM + 1],
+                                          double* stg) {
+  constexpr int N = 2 * DIM;
+  const int lane = threadIdx.x & 31;
+  const unsigned bal = __ballot_sync(0xffffffffu, has);
+  if (bal == 0u) return;
+  // the row's candidate entries in column order, each with its presence (static
+  // slots: registers, no local memory)
+  constexpr int RL = 4 * DIM - 1;
+  double v[RL];
+  bool pr[RL];
+  int t = 0;
+#pragma unroll
+  for (int b = 0; b < DIM; ++b) {
+    const double ml = hm[2 * b], mh = hm[2 * b + 1], pl = hp[2 * b], ph = hp[2 * b + 1];
+    if (b == ax) {
+      v[t] = ml, pr[t++] = c[b] >= 2;
+      v[t] = mh + pl, pr[t++] = true;
+      v[t] = ph, pr[t++] = c[b] + 1 < nc[b];
+    } else {
+      const bool lo = c[b] >= 1, hi = c[b] + 2 <= nc[b];
+      v[t] = ml, pr[t++] = lo;
+      if (b < ax) {
+        v[t] = mh, pr[t++] = hi;
+        v[t] = pl, pr[t++] = lo;
+      } else {
+        v[t] = pl, pr[t++] = lo;
+        v[t] = mh, pr[t++] = hi;
+      }
+      v[t] = ph, pr[t++] = hi;
+    }
+  }
+  int L = 0;
+#pragma unroll
+  for (int i = 0; i < RL; ++i) L += pr[i] ? 1 : 0;
+  if (!has) L = 0;
+  int off = L;  // inclusive scan of the row lengths
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(0xffffffffu, off, o);
+    if (lane >= o) off += t;
+  }
+  const int total = __shfl_sync(0xffffffffu, off, 31);
+  off -= L;
+  const int first = __ffs(bal) - 1;
+  // {row start, row} of the first row (prefetched by lane `first` at kernel start)
+  const long long rs = __shfl_sync(0xffffffffu, fq.x, first);
+  const long long row = __shfl_sync(0xffffffffu, fq.y, first);
+  if (has) {
+    int p = off;
+#pragma unroll
+    for (int i = 0; i < RL; ++i)
+      if (pr[i]) stg[p++] = v[i];
+  }
+  if (has) __stcs(A.g + row + (lane - first), hm[N] + hp[N]);
+  __syncwarp();
+  double* dst = A.hval + rs;
+  int i = lane;
+  for (; i + 96 < total; i += 128) {  // four loads in flight, then four coalesced stores
+    const double v0 = stg[i], v1 = stg[i + 32], v2 = stg[i + 64], v3 = stg[i + 96];
+    __stcs(dst + i, v0);
+    __stcs(dst + i + 32, v1);
+    __stcs(dst + i + 64, v2);
+    __stcs(dst + i + 96, v3);
+  }
+  for (; i < total; i += 32) __stcs(dst + i, stg[i]);
+  __syncwarp();
+}
+
+template <int DIM>
+__global__ void __launch_bounds__(kPW * 32, HDR_PENCIL_MINB) k_rt0_pencil(HybArgs A, PencilConst<DIM> pc, int nseg, int64_t nwarps) {
+  constexpr int N = 2 * DIM, NC = N + 1;
+  __shared__ double stg[kPW][32 * (4 * DIM - 1)];
+  __shared__ double xrow[kPW][NC];
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // the exact-path kernel may launch
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t gw = static_cast<int64_t>(blockIdx.x) * kPW + warp;
+  const DevMesh& m = A.m;
+  const int N0 = static_cast<int>(m.N[0]), N1 = static_cast<int>(m.N[1]), N2 = DIM == 3 ? static_cast<int>(m.N[2]) : 1;
+  const bool wvalid = gw < nwarps;
+  const int seg = wvalid ? static_cast<int>(gw % nseg) : 0;
+  const int64_t line = wvalid ? gw / nseg : 0;
+  const int y = static_cast<int>(line % N1), z = static_cast<int>(line / N1);
+  const int x = seg * 32 + lane;
+  const bool valid = wvalid && x < N0;
+  const int c[3] = {x, y, z}, nc[3] = {N0, N1, N2};
+  const int64_t e = x + static_cast<int64_t>(N0) * (y + static_cast<int64_t>(N1) * z);
+  // prefetch: the {row start, row} of each axis' first row (lane `first` of the
+  // group: x rows start at x = 1), and the inputs of the cells below / behind
+  const int xfirst = seg == 0 ? 1 : 0;
+  longlong2 fqx = {0, 0}, fqy = {0, 0}, fqz = {0, 0};
+  if (valid && lane == xfirst && x >= 1) fqx = A.frs[face_id32(m, 0, x, y, z)];
+  if (valid && lane == 0 && y >= 1) fqy = A.frs[face_id32(m, 1, x, y, z)];
+  if (DIM == 3 && valid && lane == 0 && z >= 1) fqz = A.frs[face_id32(m, 2, x, y, z)];
+  double ya = 1.0, yb = 1.0, yf[N], za = 1.0, zb = 1.0, zf[N];
+#pragma unroll
+  for (int j = 0; j < N; ++j) yf[j] = zf[j] = 0.0;
+  if (valid && y >= 1) load_cell<DIM>(A, e - N0, ya, yb, yf);
+  if (DIM == 3 && valid && z >= 1) load_cell<DIM>(A, e - static_cast<int64_t>(N0) * N1, za, zb, zf);
+  PencilSol<DIM> s;
+  {
+    double a = 1.0, b = 1.0, f[N], cond = 0.0;
+#pragma unroll
+    for (int j = 0; j < N; ++j) f[j] = 0.0;
+    if (valid) load_cell<DIM>(A, e, a, b, f);
+    const bool ok = pencil_solve<DIM>(pc, a, b, f, s, cond);
+    if (valid && A.qlog) A.qlog[e] = static_cast<float>(cond * 0x1p-53);
+    if (!valid || !ok || A.force_exact) {
+      pencil_zero<DIM>(s);
+      if (valid) {
+        atomicAdd(A.xcount, 1);
+        A.xlist[atomicAdd(A.xcount + 2, 1)] = static_cast<int>(e);
+      }
+    }
+  }
+  double* st = stg[warp];
+  double hm[NC], hp[NC];
+  // x faces: T- = (x - 1, y, z), its row of slot 1
+  pencil_row<DIM>(s, 1, hp);
+  if (lane == 31) {
+#pragma unroll
+    for (int q = 0; q < NC; ++q) xrow[warp][q] = hp[q];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < NC; ++q) hm[q] = __shfl_up_sync(0xffffffffu, hp[q], 1);
+  if (lane == 0 && seg > 0 && valid) {
+    if (warp > 0) {  // the previous warp holds the line's previous segment
+#pragma unroll
+      for (int q = 0; q < NC; ++q) hm[q] = xrow[warp - 1][q];
+    } else {  // the line's previous segment belongs to another CTA: recompute its last cell
+      PencilSol<DIM> sn;
+      neighbour<DIM>(A, pc, e - 1, sn);
+      pencil_row<DIM>(sn, 1, hm);
+    }
+  }
+  pencil_row<DIM>(s, 0, hp);
+  emit_rows<DIM>(A, 0, valid && x >= 1, c, nc, fqx, hm, hp, st);
+  // y faces: T- = (x, y - 1, z), slot 3 (line-uniform condition)
+  if (y >= 1) {
+    PencilSol<DIM> sn;
+    solved_neighbour<DIM>(A, pc, valid, ya, yb, yf, sn);
+    pencil_row<DIM>(sn, 3, hm);
+    pencil_row<DIM>(s, 2, hp);
+    emit_rows<DIM>(A, 1, valid, c, nc, fqy, hm, hp, st);
+  }
+  if (DIM == 3 && z >= 1) {  // z faces: T- = (x, y, z - 1), slot 5
+    PencilSol<DIM> sn;
+    solved_neighbour<DIM>(A, pc, valid, za, zb, zf, sn);
+    pencil_row<DIM>(sn, DIM == 3 ? 5 : 3, hm);
+    pencil_row<DIM>(s, DIM == 3 ? 4 : 2, hp);
+    emit_rows<DIM>(A, 2, valid, c, nc, fqz, hm, hp, st);
+  }
+}
+
+}  // namespace
+
+// host check of the structure the pencil kernel relies on (reference D, M as
+// packed by the space: D = hc[0, N^2), M = hc[N^2, 2 N^2))
+template <int DIM>
+bool pencil_setup(const double* hc, PencilConst<DIM>& pc) {
+  constexpr int N = 2 * DIM;
+  const double* D = hc;
+  const double* M = hc + N * N;
+  const double c = D[0];
+  if (!(c > 0.0)) return false;
+  for (int i = 0; i < N * N; ++i)
+    if (D[i] != c) return false;
+  for (int i = 0; i < N; ++i)
+    for (int j = 0; j < N; ++j) {
+      if ((i >> 1) != (j >> 1) && M[i * N + j] != 0.0) return false;
+      if (M[i * N + j] != M[j * N + i]) return false;
+    }
+  pc.c = c;
+  for (int a = 0; a < DIM; ++a) {
+    pc.md0[a] = M[(2 * a) * N + 2 * a];
+    pc.md1[a] = M[(2 * a + 1) * N + 2 * a + 1];
+    pc.mo[a] = M[(2 * a) * N + 2 * a + 1];
+  }
+  return true;
+}
+template bool pencil_setup<2>(const double*, PencilConst<2>&);
+template bool pencil_setup<3>(const double*, PencilConst<3>&);
+
+template <int DIM>
+void launch_rt0_pencil(const HybArgs& a, const PencilConst<DIM>& pc, cudaStream_t st) {
+  const int nseg = static_cast<int>((a.m.N[0] + 31) / 32);
+  const int64_t nwarps = static_cast<int64_t>(nseg) * a.m.N[1] * (DIM == 3 ? a.m.N[2] : 1);
+  const unsigned grid = static_cast<unsigned>((nwarps + kPW - 1) / kPW);
+  k_rt0_pencil<DIM><<<grid, kPW * 32, 0, st>>>(a, pc, nseg, nwarps);
+  count_launch();
+}
+template void launch_rt0_pencil<2>(const HybArgs&, const PencilConst<2>&, cudaStream_t);
+template void launch_rt0_pencil<3>(const HybArgs&, const PencilConst<3>&, cudaStream_t);
+
+}  // namespace hdr

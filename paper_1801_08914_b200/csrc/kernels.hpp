@@ -67,6 +67,18 @@ void launch_face_rows(int64_t nfaces, const int* mbase, const int64_t* rowoff, l
 // 4-bit column ranks (own slots, then the neighbour's slots; 15 = absent).
 std::vector<uint64_t> rank_table_rt0(int dim);
 
+// k = 0, one-pass pencil kernel (kern_pencil.cu): reference element with D = c 1 1^T
+// and axis-block-diagonal M (checked by pencil_setup on the packed constants)
+template <int DIM>
+struct PencilConst {
+  double c;                          // every entry of the reference divdiv
+  double md0[DIM], md1[DIM], mo[DIM];  // the 2 x 2 mass block of each axis
+};
+template <int DIM>
+bool pencil_setup(const double* host_consts, PencilConst<DIM>& pc);
+template <int DIM>
+void launch_rt0_pencil(const HybArgs& a, const PencilConst<DIM>& pc, cudaStream_t st);
+
 // k = 0, lane-per-row form with row-complete writes (stage: parity_count * N*(N+1) doubles)
 void launch_hybridize_rt0_rows(const HybArgs& a, const double* host_consts, double* stage, cudaStream_t st);
 // k >= 1 with nF + 1 <= 32 (RT1 hexes, RT1..RT3 quads): one warp per cell (kern_warp.cu)

@@ -21,17 +21,17 @@ timeout 600 python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu > "$OUT/plain
 # DRAM traffic of the dominant kernels, one step per config
 for c in 2 3 4 5; do
   case $c in
-    2) K='regex:k_rt0_brick|k_rt0_cell|k_rt0_rows' ;;
+    2) K='regex:k_rt0_pencil|k_rt0_brick|k_rt0_cell|k_rt0_rows' ;;
     3) K='regex:k_hyb_warp' ;;
     4) K='regex:k_piola_gemm|k_spd_hyb|k_run_sum' ;;
     5) K='regex:k_hyb_big|k_gemm_f64' ;;
   esac
   timeout 900 ncu --clock-control none --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum \
     -k "$K" --csv --log-file "$OUT/traffic_cfg$c.csv" \
-    python bench.py --config $c --steps 1 --warmup 3 --no-e2e --no-cpu > "$OUT/ncu_traffic_$c.log" 2>&1
+    python bench.py --config $c --steps 1 --warmup 3 --no-e2e --no-cpu --no-configs > "$OUT/ncu_traffic_$c.log" 2>&1
 done
 # --set full captures of the dominant kernels (summarised by profiles/summarize.py)
-timeout 900 ncu --set full --import-source on --clock-control none -k regex:k_rt0_brick -c 2 \
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:k_rt0_pencil -c 1 \
   -o "$OUT/full_cfg2" python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu --no-graph > "$OUT/full2.log" 2>&1
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:k_hyb_warp -c 1 \
   -o "$OUT/full_cfg3" python bench.py --config 3 --steps 1 --warmup 3 --no-e2e --no-cpu --no-graph > "$OUT/full3.log" 2>&1

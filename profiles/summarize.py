@@ -62,7 +62,7 @@ def main():
 
 # per step DRAM bytes (read + write) of the dominant kernels, from the traffic launch lists;
 # the number of steps captured = launches of the step's anchor kernel / its launches per step
-ANCHOR = {"cfg2": ("k_rt0_brick", 2), "cfg3": ("k_hyb_warp", 2), "cfg4": ("k_piola_gemm", 1), "cfg5": ("k_hyb_big", 2)}
+ANCHOR = {"cfg2": ("k_rt0_pencil<3>", 1), "cfg3": ("k_hyb_warp", 2), "cfg4": ("k_piola_gemm", 1), "cfg5": ("k_hyb_big", 2)}
 
 
 def traffic_json(src: Path):
@@ -82,14 +82,19 @@ def traffic_json(src: Path):
             if len(r) != len(hdr) or r is hdr:
                 continue
             d = dict(zip(hdr, r))
+            if cfg == "cfg2" and "<3>" not in d["Kernel Name"]:  # the per-config block's 2D launches
+                continue
             if d["Metric Name"] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
                 tot += float(d["Metric Value"].replace(",", "")) * scale.get(d["Metric Unit"], 1)
             if anchor in d["Kernel Name"]:
                 launches.add(d["ID"])
         if launches:
             out[cfg] = tot / (len(launches) / per_step)
-    if out:
-        Path("profiles").joinpath("ncu_traffic.json").write_text(json.dumps(out, indent=1) + "\n")
+    if out:  # merged into the committed per-config sums (configs not captured this time keep theirs)
+        tf = Path("profiles").joinpath("ncu_traffic.json")
+        old = json.loads(tf.read_text()) if tf.exists() else {}
+        old.update(out)
+        tf.write_text(json.dumps(old, indent=1) + "\n")
 
 
 if __name__ == "__main__":
