@@ -64,6 +64,7 @@ struct hdr_space_s {
   DBuf<float> etab;                // k >= 2 (3D): {E, Ma} (fp32) likewise
   DBuf<double> tdm;                // warp-kernel spaces: {D, M} transposed ((i, l) at l * n + i)
   DBuf<float> tem;                 // warp-kernel spaces: {E, Ma} (fp32) transposed
+  DBuf<int> tix;                   // warp-kernel spaces: (l << 16) | i of each table entry
   Fixed fx{};
   GeomState* geom = nullptr;  // mapped (trilinear) cells: hdr_space_set_vertices
   struct BatchCtx* batch = nullptr;  // hdr_hybridize_fe_batch: streams, events, two operators
@@ -436,20 +437,41 @@ hdr_status hdr_space_create(int dim, const int64_t cells[3], const double h[3], 
       CK(cudaStreamSynchronize(st));
     }
     if ((dim == 3 && order == 1) || (dim == 2 && order >= 1)) {  // transposed Delta inputs (kern_warp.cu)
-      std::vector<double> td(2 * nn);
-      std::vector<float> te(2 * nn);
-      for (int i = 0; i < n; ++i)
-        for (int l = 0; l < n; ++l) {
-          const size_t q = static_cast<size_t>(l) * n + i, o = static_cast<size_t>(i) * n + l;
-          td[2 * q] = sp->re.divdiv[o];
-          td[2 * q + 1] = sp->re.mass[o];
-          te[2 * q] = static_cast<float>(sp->st.E[o]);
-          te[2 * q + 1] = static_cast<float>(sp->st.Ma[o]);
+      std::vector<double> td;
+      std::vector<float> te;
+      std::vector<int> tx;
+      auto section = [&](bool zero_mass) {
+        const size_t start = tx.size();
+        for (int l = 0; l < n; ++l)
+          for (int i = 0; i < n; ++i) {
+            const size_t o = static_cast<size_t>(i) * n + l;
+            const float ma = static_cast<float>(sp->st.Ma[o]);
+            if ((sp->re.mass[o] == 0.0 && ma == 0.f) != zero_mass) continue;
+            td.push_back(sp->re.divdiv[o]);
+            td.push_back(sp->re.mass[o]);
+            te.push_back(static_cast<float>(sp->st.E[o]));
+            te.push_back(ma);
+            tx.push_back((l << 16) | i);
+          }
+        while (tx.size() > start && tx.size() % 128 != 0) {  // benign duplicates of the last entry
+          const size_t q = tx.size() - 1;
+          td.push_back(td[2 * q]);
+          td.push_back(td[2 * q + 1]);
+          te.push_back(te[2 * q]);
+          te.push_back(te[2 * q + 1]);
+          tx.push_back(tx[q]);
         }
+      };
+      section(true);
+      fx.tz = static_cast<int>(tx.size());
+      section(false);
+      fx.tn = static_cast<int>(tx.size());
       sp->tdm.upload(td);
       sp->tem.upload(te);
+      sp->tix.upload(tx);
       fx.tdm = reinterpret_cast<const double2*>(sp->tdm.p);
       fx.tem = reinterpret_cast<const float2*>(sp->tem.p);
+      fx.tix = sp->tix.p;
     }
     if (order == 0) {  // constant block for the register kernel: D, M, E, Ma, N0, X, lam, rho
       sp->rt0_consts.assign(pack.begin(), pack.begin() + 5 * nn + n + 1);

@@ -46,9 +46,15 @@ namespace hdr {
 
 namespace {
 
-constexpr int kPW = 8;              // warps per CTA
+#ifndef HDR_PENCIL_PW
+#define HDR_PENCIL_PW 4
+#endif
+constexpr int kPW = HDR_PENCIL_PW;  // warps per CTA
 #ifndef HDR_PENCIL_MINB
-#define HDR_PENCIL_MINB 1               // CTAs per SM asked of ptxas
+#define HDR_PENCIL_MINB 5               // CTAs per SM asked of ptxas: 96 registers, no spills, 20 warps per SM
+#endif
+#ifndef HDR_PENCIL_STAGE
+#define HDR_PENCIL_STAGE 1              // neighbour inputs wait in shared memory (cp.async) instead of registers
 #endif
 constexpr double kPencilCond = 1e12;  // acceptance bound on cond(A_T)
 
@@ -144,6 +150,41 @@ __device__ __forceinline__ void load_cell(const HybArgs& A, int64_t e, double& a
   }
 }
 
+// Neighbour inputs staged by cp.async: slot [0] = {alpha, beta}, [1 + j] = {f_2j, f_2j+1},
+// each slot 32 double2 (one per lane: conflict-free 16-byte accesses); the copies are
+// issued at kernel start and cost no registers while the own cell is solved.
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(dst))), "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(dst))), "l"(src)
+               : "memory");
+}
+template <int DIM>
+__device__ __forceinline__ void stage_cell(const HybArgs& A, int64_t e, double2* slot) {
+  cp_async8(&slot[0].x, A.alpha + e);
+  cp_async8(&slot[0].y, A.beta + e);
+  const double2* fp = reinterpret_cast<const double2*>(A.f + e * (2 * DIM));
+#pragma unroll
+  for (int j = 0; j < DIM; ++j) cp_async16(slot + 32 * (1 + j), fp + j);
+}
+template <int DIM>
+__device__ __forceinline__ void staged_cell(const double2* slot, bool ok, double& a, double& b, double (&f)[2 * DIM]) {
+  a = b = 1.0;
+#pragma unroll
+  for (int j = 0; j < 2 * DIM; ++j) f[j] = 0.0;
+  if (ok) {
+    const double2 ab = slot[0];
+    a = ab.x, b = ab.y;
+#pragma unroll
+    for (int j = 0; j < DIM; ++j) {
+      const double2 v = slot[32 * (1 + j)];
+      f[2 * j] = v.x, f[2 * j + 1] = v.y;
+    }
+  }
+}
+
 // the solution of a neighbour cell (zero when the cell is not accepted: its own
 // lane lists it for the exact path)
 template <int DIM>
@@ -171,7 +212,7 @@ __device__ __forceinline__ void solved_neighbour(const HybArgs& A, const PencilC
 // (lo_b / hi_b present when interior, the same for T- and T+ when b != ax).
 template <int DIM>
 __device__ __forceinline__ void emit_rows(const HybArgs& A, int ax, bool has, const int (&c)[3], const int (&nc)[3],
-                                          longlong2 fq, const double (&hm)[2 * DIM + 1], const double (&hp)[2 * DIM + 1],
+                                          const longlong2* fq, const double (&hm)[2 * DIM + 1], const double (&hp)[2 * DIM + 1],
                                           double* stg) {
   constexpr int N = 2 * DIM;
   const int lane = threadIdx.x & 31;
@@ -217,8 +258,13 @@ __device__ __forceinline__ void emit_rows(const HybArgs& A, int ax, bool has, co
   off -= L;
   const int first = __ffs(bal) - 1;
   // {row start, row} of the first row (prefetched by lane `first` at kernel start)
-  const long long rs = __shfl_sync(0xffffffffu, fq.x, first);
-  const long long row = __shfl_sync(0xffffffffu, fq.y, first);
+#if HDR_PENCIL_STAGE
+  const longlong2 fqv = *fq;  // broadcast read of the staged pair
+  const long long rs = fqv.x, row = fqv.y;
+#else
+  const long long rs = __shfl_sync(0xffffffffu, fq->x, first);
+  const long long row = __shfl_sync(0xffffffffu, fq->y, first);
+#endif
   if (has) {
     int p = off;
 #pragma unroll
@@ -241,10 +287,24 @@ __device__ __forceinline__ void emit_rows(const HybArgs& A, int ax, bool has, co
 }
 
 template <int DIM>
+struct PencilSmem {
+#if HDR_PENCIL_STAGE
+  double2 nbr[kPW][DIM - 1][DIM + 1][32];  // staged inputs of the cells below / behind
+  longlong2 fq[kPW][3];                     // {row start, row} of each axis' first row
+#endif
+  double stg[kPW][32 * (4 * DIM - 1)];      // a warp's H rows before the coalesced write-out
+  double xrow[kPW][2 * DIM + 1];            // last lane's x row for the next segment's first lane
+};
+
+template <int DIM>
 __global__ void __launch_bounds__(kPW * 32, HDR_PENCIL_MINB) k_rt0_pencil(HybArgs A, PencilConst<DIM> pc, int nseg, int64_t nwarps) {
   constexpr int N = 2 * DIM, NC = N + 1;
-  __shared__ double stg[kPW][32 * (4 * DIM - 1)];
-  __shared__ double xrow[kPW][NC];
+  // dynamic shared memory (above the 48 KB static limit with the neighbour slots)
+  extern __shared__ __align__(16) unsigned char pencil_smem[];
+  using Sm = PencilSmem<DIM>;
+  Sm& sm = *reinterpret_cast<Sm*>(pencil_smem);
+  auto& stg = sm.stg;
+  auto& xrow = sm.xrow;
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // the exact-path kernel may launch
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t gw = static_cast<int64_t>(blockIdx.x) * kPW + warp;
@@ -261,15 +321,32 @@ __global__ void __launch_bounds__(kPW * 32, HDR_PENCIL_MINB) k_rt0_pencil(HybArg
   // prefetch: the {row start, row} of each axis' first row (lane `first` of the
   // group: x rows start at x = 1), and the inputs of the cells below / behind
   const int xfirst = seg == 0 ? 1 : 0;
-  longlong2 fqx = {0, 0}, fqy = {0, 0}, fqz = {0, 0};
-  if (valid && lane == xfirst && x >= 1) fqx = A.frs[face_id32(m, 0, x, y, z)];
-  if (valid && lane == 0 && y >= 1) fqy = A.frs[face_id32(m, 1, x, y, z)];
-  if (DIM == 3 && valid && lane == 0 && z >= 1) fqz = A.frs[face_id32(m, 2, x, y, z)];
+#if HDR_PENCIL_STAGE
+  longlong2* const fqx = &sm.fq[warp][0];
+  longlong2* const fqy = &sm.fq[warp][1];
+  longlong2* const fqz = &sm.fq[warp][2];
+  if (valid && lane == xfirst && x >= 1) cp_async16(fqx, A.frs + face_id32(m, 0, x, y, z));
+  if (valid && lane == 0 && y >= 1) cp_async16(fqy, A.frs + face_id32(m, 1, x, y, z));
+  if (DIM == 3 && valid && lane == 0 && z >= 1) cp_async16(fqz, A.frs + face_id32(m, 2, x, y, z));
+#else
+  longlong2 fqxv = {0, 0}, fqyv = {0, 0}, fqzv = {0, 0};
+  if (valid && lane == xfirst && x >= 1) fqxv = A.frs[face_id32(m, 0, x, y, z)];
+  if (valid && lane == 0 && y >= 1) fqyv = A.frs[face_id32(m, 1, x, y, z)];
+  if (DIM == 3 && valid && lane == 0 && z >= 1) fqzv = A.frs[face_id32(m, 2, x, y, z)];
+  const longlong2 *fqx = &fqxv, *fqy = &fqyv, *fqz = &fqzv;
+#endif
+#if HDR_PENCIL_STAGE
+  auto& nbr = sm.nbr;
+  if (valid && y >= 1) stage_cell<DIM>(A, e - N0, &nbr[warp][0][0][lane]);
+  if (DIM == 3 && valid && z >= 1) stage_cell<DIM>(A, e - static_cast<int64_t>(N0) * N1, &nbr[warp][DIM - 2][0][lane]);
+  asm volatile("cp.async.commit_group;" ::: "memory");
+#else
   double ya = 1.0, yb = 1.0, yf[N], za = 1.0, zb = 1.0, zf[N];
 #pragma unroll
   for (int j = 0; j < N; ++j) yf[j] = zf[j] = 0.0;
   if (valid && y >= 1) load_cell<DIM>(A, e - N0, ya, yb, yf);
   if (DIM == 3 && valid && z >= 1) load_cell<DIM>(A, e - static_cast<int64_t>(N0) * N1, za, zb, zf);
+#endif
   PencilSol<DIM> s;
   {
     double a = 1.0, b = 1.0, f[N], cond = 0.0;
@@ -308,10 +385,18 @@ __global__ void __launch_bounds__(kPW * 32, HDR_PENCIL_MINB) k_rt0_pencil(HybArg
     }
   }
   pencil_row<DIM>(s, 0, hp);
+#if HDR_PENCIL_STAGE
+  asm volatile("cp.async.wait_group 0;" ::: "memory");  // neighbour inputs: own copies; row starts: another lane's
+  __syncwarp();
+#endif
   emit_rows<DIM>(A, 0, valid && x >= 1, c, nc, fqx, hm, hp, st);
   // y faces: T- = (x, y - 1, z), slot 3 (line-uniform condition)
   if (y >= 1) {
     PencilSol<DIM> sn;
+#if HDR_PENCIL_STAGE
+    double ya, yb, yf[N];
+    staged_cell<DIM>(&nbr[warp][0][0][lane], valid, ya, yb, yf);
+#endif
     solved_neighbour<DIM>(A, pc, valid, ya, yb, yf, sn);
     pencil_row<DIM>(sn, 3, hm);
     pencil_row<DIM>(s, 2, hp);
@@ -319,6 +404,10 @@ __global__ void __launch_bounds__(kPW * 32, HDR_PENCIL_MINB) k_rt0_pencil(HybArg
   }
   if (DIM == 3 && z >= 1) {  // z faces: T- = (x, y, z - 1), slot 5
     PencilSol<DIM> sn;
+#if HDR_PENCIL_STAGE
+    double za, zb, zf[N];
+    staged_cell<DIM>(&nbr[warp][DIM - 2][0][lane], valid, za, zb, zf);
+#endif
     solved_neighbour<DIM>(A, pc, valid, za, zb, zf, sn);
     pencil_row<DIM>(sn, DIM == 3 ? 5 : 3, hm);
     pencil_row<DIM>(s, DIM == 3 ? 4 : 2, hp);
@@ -360,7 +449,12 @@ void launch_rt0_pencil(const HybArgs& a, const PencilConst<DIM>& pc, cudaStream_
   const int nseg = static_cast<int>((a.m.N[0] + 31) / 32);
   const int64_t nwarps = static_cast<int64_t>(nseg) * a.m.N[1] * (DIM == 3 ? a.m.N[2] : 1);
   const unsigned grid = static_cast<unsigned>((nwarps + kPW - 1) / kPW);
-  k_rt0_pencil<DIM><<<grid, kPW * 32, 0, st>>>(a, pc, nseg, nwarps);
+  static const bool attr_set = [] {  // once per instantiation
+    return cudaFuncSetAttribute(k_rt0_pencil<DIM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(sizeof(PencilSmem<DIM>))) == cudaSuccess;
+  }();
+  (void)attr_set;
+  k_rt0_pencil<DIM><<<grid, kPW * 32, sizeof(PencilSmem<DIM>), st>>>(a, pc, nseg, nwarps);
   count_launch();
 }
 template void launch_rt0_pencil<2>(const HybArgs&, const PencilConst<2>&, cudaStream_t);

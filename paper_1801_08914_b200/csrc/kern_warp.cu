@@ -492,15 +492,24 @@ __device__ __forceinline__ void warp_cell(const HybArgs& A, int e, int parity, i
   // (transposed input tables: contiguous loads and stores; alpha E + beta Ma in fp32)
   const float af = static_cast<float>(a), bfl = static_cast<float>(b);
   auto fill_delta = [&](float* dst, int ld) {
-    for (int idx = lane; idx < N * N; idx += GT) {
+    const int tz = fx.tz, tn = fx.tn;
+    for (int idx = lane; idx < tz; idx += GT) {  // M = Ma = 0: delta = fl(alpha D) - alpha D (the same bits)
+      const double d = __ldg(&fx.tdm[idx].x);
+      const float e = __ldg(&fx.tem[idx].x);
+      const int li = __ldg(fx.tix + idx);
+      double p1, e1;
+      two_prod(a, d, p1, e1);
+      dst[(li >> 16) * ld + (li & 0xffff)] = fmaf(af, e, static_cast<float>(-e1));
+    }
+    for (int idx = tz + lane; idx < tn; idx += GT) {
       const double2 dm = __ldg(fx.tdm + idx);
       const float2 em = __ldg(fx.tem + idx);
+      const int li = __ldg(fx.tix + idx);
       double p1, e1, p2, e2, s_, e3;
       two_prod(a, dm.x, p1, e1);
       two_prod(b, dm.y, p2, e2);
       two_sum_fast(p1, p2, s_, e3);
-      const int l = idx / N, i = idx - l * N;  // entry (i, l), stored transposed
-      dst[l * ld + i] = fmaf(af, em.x, fmaf(bfl, em.y, static_cast<float>(-((e1 + e2) + e3))));
+      dst[(li >> 16) * ld + (li & 0xffff)] = fmaf(af, em.x, fmaf(bfl, em.y, static_cast<float>(-((e1 + e2) + e3))));
     }
   };
   fill_delta(sm.d32t, SM::DT);

@@ -29,10 +29,15 @@ struct Fixed {  // device pointers to the per-space fixed factors (see hdr_inter
   // kern_cta.cu (chunk c, row m < MP, k < 16 -> column 16 c + k; zero padded)
   const double2* dtab;  // {D, M}
   const float2* etab;   // {E, Ma} (tiny: fp32 carries them to 6e-8 relative)
-  // warp-kernel spaces (RT1 hexes, RT1-3 quads): the same inputs transposed,
-  // entry l * n + i = (i, l), so Delta^T is generated with contiguous loads and stores
+  // warp-kernel spaces (RT1 hexes, RT1-3 quads): the same inputs as two sections of
+  // entries, each padded to a multiple of 128 with copies of its last entry: first
+  // the entries whose M and Ma are exactly zero (the mass matrix couples one vector
+  // component only: delta is then the rounding error of fl(alpha D) alone), then the
+  // rest; tix = (l << 16) | i of the entry (i, l), which Delta^T stores at l * ld + i
   const double2* tdm;   // {D, M}
   const float2* tem;    // {E, Ma}
+  const int* tix;
+  int tz, tn;           // padded length of the zero-mass section, of both sections
   int r;
   double rho;
 };
