@@ -21,7 +21,8 @@
 // (unit constraint rows of build_C, src/reduction.cpp:172-181).
 //
 // Acceptance (DESIGN.md §2 "Fail-safe"): a cell whose condition bound
-// (1 + gamma sigma) max tr(P_a) max tr(P_a)/det(P_a) exceeds kPencilCond, or whose
+// (1 + gamma sigma) sum_a tr(P_a) sum_a tr(P_a)/det(P_a) (at most dim^2 times the
+// bound with maxima) exceeds kPencilCond, or whose
 // blocks are not positive definite, contributes zeros and is listed for the
 // exact double-double path (k_rt0_exact, the reference's SingularBlock rule):
 // the reference's LU pivots of an accepted SPD cell are >= lambda_min / G >= 1e-12 / G
@@ -81,7 +82,7 @@ template <int DIM>
 __device__ __forceinline__ bool pencil_solve(const PencilConst<DIM>& pc, double a, double b, const double (&f)[2 * DIM],
                                              PencilSol<DIM>& s, double& cond) {
   const double gam = __dmul_rn(a, pc.c);  // fl(alpha D_ij), every ij
-  double sig = 0.0, tmax = 0.0, rmax = 0.0, uf = 0.0;
+  double sig = 0.0, tsum = 0.0, rsum = 0.0, uf = 0.0;
   bool pd = gam >= 0.0;
 #pragma unroll
   for (int ax = 0; ax < DIM; ++ax) {
@@ -99,8 +100,8 @@ __device__ __forceinline__ bool pencil_solve(const PencilConst<DIM>& pc, double 
     s.u[2 * ax + 1] = s.i01[ax] + s.i11[ax];
     sig += s.u[2 * ax] + s.u[2 * ax + 1];
     const double tr = p00 + p11;
-    tmax = fmax(tmax, tr);
-    rmax = fmax(rmax, tr * id);  // >= 1 / lambda_min(P_a)
+    tsum += tr;                  // >= max_a tr(P_a)  (sums: an fp64 max is several instructions)
+    rsum = fma(tr, id, rsum);    // >= max_a tr(P_a) / det(P_a) >= 1 / lambda_min(P)
     const double f0 = f[2 * ax], f1 = f[2 * ax + 1];
     s.pf[2 * ax] = fma(s.i00[ax], f0, s.i01[ax] * f1);
     s.pf[2 * ax + 1] = fma(s.i01[ax], f0, s.i11[ax] * f1);
@@ -109,7 +110,7 @@ __device__ __forceinline__ bool pencil_solve(const PencilConst<DIM>& pc, double 
   const double den = fma(gam, sig, 1.0);
   s.kap = gam * rcp64(den);
   s.uf = uf;
-  cond = den * tmax * rmax;
+  cond = den * tsum * rsum;
   return pd && cond <= kPencilCond && s.kap == s.kap && fabs(s.kap) < 1e300 && fabs(uf) < 1e300;
 }
 
@@ -212,25 +213,27 @@ __device__ __forceinline__ void solved_neighbour(const HybArgs& A, const PencilC
 // (lo_b / hi_b present when interior, the same for T- and T+ when b != ax).
 template <int DIM>
 __device__ __forceinline__ void emit_rows(const HybArgs& A, int ax, bool has, const int (&c)[3], const int (&nc)[3],
-                                          const longlong2* fq, const double (&hm)[2 * DIM + 1], const double (&hp)[2 * DIM + 1],
-                                          double* stg) {
+                                          int x0, const longlong2* fq, const double (&hm)[2 * DIM + 1],
+                                          const double (&hp)[2 * DIM + 1], double* stg) {
   constexpr int N = 2 * DIM;
   const int lane = threadIdx.x & 31;
-  const unsigned bal = __ballot_sync(0xffffffffu, has);
-  if (bal == 0u) return;
+  if (__ballot_sync(0xffffffffu, has) == 0u) return;
   // the row's candidate entries in column order, each with its presence (static
   // slots: registers, no local memory)
   constexpr int RL = 4 * DIM - 1;
   double v[RL];
   bool pr[RL];
   int t = 0;
+  int lfull = 0;  // entries of a row whose cell is interior along x (warp-uniform)
 #pragma unroll
   for (int b = 0; b < DIM; ++b) {
     const double ml = hm[2 * b], mh = hm[2 * b + 1], pl = hp[2 * b], ph = hp[2 * b + 1];
     if (b == ax) {
-      v[t] = ml, pr[t++] = c[b] >= 2;
+      const bool far_lo = c[b] >= 2, far_hi = c[b] + 1 < nc[b];
+      v[t] = ml, pr[t++] = far_lo;
       v[t] = mh + pl, pr[t++] = true;
-      v[t] = ph, pr[t++] = c[b] + 1 < nc[b];
+      v[t] = ph, pr[t++] = far_hi;
+      lfull += b == 0 ? 3 : 1 + (far_lo ? 1 : 0) + (far_hi ? 1 : 0);
     } else {
       const bool lo = c[b] >= 1, hi = c[b] + 2 <= nc[b];
       v[t] = ml, pr[t++] = lo;
@@ -242,22 +245,27 @@ __device__ __forceinline__ void emit_rows(const HybArgs& A, int ax, bool has, co
         v[t] = mh, pr[t++] = hi;
       }
       v[t] = ph, pr[t++] = hi;
+      lfull += b == 0 ? 4 : 2 * ((lo ? 1 : 0) + (hi ? 1 : 0));
     }
   }
-  int L = 0;
-#pragma unroll
-  for (int i = 0; i < RL; ++i) L += pr[i] ? 1 : 0;
-  if (!has) L = 0;
-  int off = L;  // inclusive scan of the row lengths
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int t = __shfl_up_sync(0xffffffffu, off, o);
-    if (lane >= o) off += t;
+  // Row offsets in closed form (no scan): along the segment only the cells next to
+  // the x boundary have shorter rows.  x faces (rows of x >= 1): the row of x = 1
+  // lacks T-'s far face, the row of x = N0 - 1 T+'s; y / z faces: the rows of
+  // x = 0 and x = N0 - 1 lack the two x faces beyond the boundary.
+  const int n0 = nc[0], x = c[0];
+  const int x1 = min(x0 + 32, n0);            // one past the segment's last cell
+  const int xs = ax == 0 ? max(x0, 1) : x0;   // first cell with a row
+  if (x1 <= xs) return;                       // (warp-uniform)
+  const int first = xs - x0;
+  int off, total;
+  if (ax == 0) {
+    off = (x - xs) * lfull - ((xs <= 1 && x > 1) ? 1 : 0);
+    total = (x1 - xs) * lfull - ((xs <= 1 && x1 > 1) ? 1 : 0) - (x1 == n0 ? 1 : 0);
+  } else {
+    off = (x - xs) * lfull - ((xs == 0 && x > 0) ? 2 : 0);
+    total = (x1 - xs) * lfull - (xs == 0 ? 2 : 0) - (x1 == n0 ? 2 : 0);
   }
-  const int total = __shfl_sync(0xffffffffu, off, 31);
-  off -= L;
-  const int first = __ffs(bal) - 1;
-  // {row start, row} of the first row (prefetched by lane `first` at kernel start)
+  // {row start, row} of the first row (staged by lane `first` at kernel start)
 #if HDR_PENCIL_STAGE
   const longlong2 fqv = *fq;  // broadcast read of the staged pair
   const long long rs = fqv.x, row = fqv.y;
@@ -265,24 +273,31 @@ __device__ __forceinline__ void emit_rows(const HybArgs& A, int ax, bool has, co
   const long long rs = __shfl_sync(0xffffffffu, fq->x, first);
   const long long row = __shfl_sync(0xffffffffu, fq->y, first);
 #endif
+  // staged at the parity of the global position, so that the write-out moves
+  // aligned 16-byte pairs: stg[q] <-> hval[rs - pad + q] (pad: the 8-byte misalignment)
+  const int pad = static_cast<int>((reinterpret_cast<uintptr_t>(A.hval + rs) >> 3) & 1);  // any 8-byte aligned hval
   if (has) {
-    int p = off;
+    int p = off + pad;
 #pragma unroll
     for (int i = 0; i < RL; ++i)
       if (pr[i]) stg[p++] = v[i];
   }
   if (has) __stcs(A.g + row + (lane - first), hm[N] + hp[N]);
   __syncwarp();
-  double* dst = A.hval + rs;
-  int i = lane;
-  for (; i + 96 < total; i += 128) {  // four loads in flight, then four coalesced stores
-    const double v0 = stg[i], v1 = stg[i + 32], v2 = stg[i + 64], v3 = stg[i + 96];
-    __stcs(dst + i, v0);
-    __stcs(dst + i + 32, v1);
-    __stcs(dst + i + 64, v2);
-    __stcs(dst + i + 96, v3);
+  double* dst = A.hval + (rs - pad);
+  const int qe = pad + total;
+  if (pad && lane == 0) __stcs(dst + 1, stg[1]);
+  if ((qe & 1) && lane == 31 && qe - 1 >= 2 * pad) __stcs(dst + qe - 1, stg[qe - 1]);
+  const double2* s2 = reinterpret_cast<const double2*>(stg);
+  double2* d2 = reinterpret_cast<double2*>(dst);
+  const int je = qe >> 1;
+  int j = pad + lane;
+  for (; j + 32 < je; j += 64) {  // two loads in flight, then two coalesced 16-byte stores
+    const double2 v0 = s2[j], v1 = s2[j + 32];
+    __stcs(d2 + j, v0);
+    __stcs(d2 + j + 32, v1);
   }
-  for (; i < total; i += 32) __stcs(dst + i, stg[i]);
+  if (j < je) __stcs(d2 + j, s2[j]);
   __syncwarp();
 }
 
@@ -292,12 +307,12 @@ struct PencilSmem {
   double2 nbr[kPW][DIM - 1][DIM + 1][32];  // staged inputs of the cells below / behind
   longlong2 fq[kPW][3];                     // {row start, row} of each axis' first row
 #endif
-  double stg[kPW][32 * (4 * DIM - 1)];      // a warp's H rows before the coalesced write-out
+  double stg[kPW][32 * (4 * DIM - 1) + 2];  // a warp's H rows before the coalesced write-out (+ parity pad)
   double xrow[kPW][2 * DIM + 1];            // last lane's x row for the next segment's first lane
 };
 
 template <int DIM>
-__global__ void __launch_bounds__(kPW * 32, HDR_PENCIL_MINB) k_rt0_pencil(HybArgs A, PencilConst<DIM> pc, int nseg, int64_t nwarps) {
+__global__ void __launch_bounds__(kPW * 32, HDR_PENCIL_MINB) k_rt0_pencil(HybArgs A, PencilConst<DIM> pc, FastDiv dseg, uint32_t nwarps) {
   constexpr int N = 2 * DIM, NC = N + 1;
   // dynamic shared memory (above the 48 KB static limit with the neighbour slots)
   extern __shared__ __align__(16) unsigned char pencil_smem[];
@@ -307,13 +322,14 @@ __global__ void __launch_bounds__(kPW * 32, HDR_PENCIL_MINB) k_rt0_pencil(HybArg
   auto& xrow = sm.xrow;
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // the exact-path kernel may launch
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t gw = static_cast<int64_t>(blockIdx.x) * kPW + warp;
+  const uint32_t gw = blockIdx.x * kPW + warp;
   const DevMesh& m = A.m;
   const int N0 = static_cast<int>(m.N[0]), N1 = static_cast<int>(m.N[1]), N2 = DIM == 3 ? static_cast<int>(m.N[2]) : 1;
   const bool wvalid = gw < nwarps;
-  const int seg = wvalid ? static_cast<int>(gw % nseg) : 0;
-  const int64_t line = wvalid ? gw / nseg : 0;
-  const int y = static_cast<int>(line % N1), z = static_cast<int>(line / N1);
+  const uint32_t line = wvalid ? dseg.div(gw) : 0;  // multiply-shift divisions (32-bit: < 2^31 cells)
+  const int seg = wvalid ? static_cast<int>(gw - line * dseg.d) : 0;
+  const uint32_t zq = m.div_n1.div(line);
+  const int y = static_cast<int>(line - zq * static_cast<uint32_t>(N1)), z = static_cast<int>(zq);
   const int x = seg * 32 + lane;
   const bool valid = wvalid && x < N0;
   const int c[3] = {x, y, z}, nc[3] = {N0, N1, N2};
@@ -389,7 +405,7 @@ __global__ void __launch_bounds__(kPW * 32, HDR_PENCIL_MINB) k_rt0_pencil(HybArg
   asm volatile("cp.async.wait_group 0;" ::: "memory");  // neighbour inputs: own copies; row starts: another lane's
   __syncwarp();
 #endif
-  emit_rows<DIM>(A, 0, valid && x >= 1, c, nc, fqx, hm, hp, st);
+  emit_rows<DIM>(A, 0, valid && x >= 1, c, nc, seg * 32, fqx, hm, hp, st);
   // y faces: T- = (x, y - 1, z), slot 3 (line-uniform condition)
   if (y >= 1) {
     PencilSol<DIM> sn;
@@ -400,7 +416,7 @@ __global__ void __launch_bounds__(kPW * 32, HDR_PENCIL_MINB) k_rt0_pencil(HybArg
     solved_neighbour<DIM>(A, pc, valid, ya, yb, yf, sn);
     pencil_row<DIM>(sn, 3, hm);
     pencil_row<DIM>(s, 2, hp);
-    emit_rows<DIM>(A, 1, valid, c, nc, fqy, hm, hp, st);
+    emit_rows<DIM>(A, 1, valid, c, nc, seg * 32, fqy, hm, hp, st);
   }
   if (DIM == 3 && z >= 1) {  // z faces: T- = (x, y, z - 1), slot 5
     PencilSol<DIM> sn;
@@ -411,7 +427,7 @@ __global__ void __launch_bounds__(kPW * 32, HDR_PENCIL_MINB) k_rt0_pencil(HybArg
     solved_neighbour<DIM>(A, pc, valid, za, zb, zf, sn);
     pencil_row<DIM>(sn, DIM == 3 ? 5 : 3, hm);
     pencil_row<DIM>(s, DIM == 3 ? 4 : 2, hp);
-    emit_rows<DIM>(A, 2, valid, c, nc, fqz, hm, hp, st);
+    emit_rows<DIM>(A, 2, valid, c, nc, seg * 32, fqz, hm, hp, st);
   }
 }
 
@@ -454,7 +470,8 @@ void launch_rt0_pencil(const HybArgs& a, const PencilConst<DIM>& pc, cudaStream_
                                 static_cast<int>(sizeof(PencilSmem<DIM>))) == cudaSuccess;
   }();
   (void)attr_set;
-  k_rt0_pencil<DIM><<<grid, kPW * 32, sizeof(PencilSmem<DIM>), st>>>(a, pc, nseg, nwarps);
+  k_rt0_pencil<DIM><<<grid, kPW * 32, sizeof(PencilSmem<DIM>), st>>>(a, pc, FastDiv(static_cast<uint32_t>(nseg)),
+                                                                    static_cast<uint32_t>(nwarps));
   count_launch();
 }
 template void launch_rt0_pencil<2>(const HybArgs&, const PencilConst<2>&, cudaStream_t);
