@@ -16,6 +16,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 
 #include "hdr_device.cuh"
 #include "kernels.hpp"
@@ -286,6 +287,222 @@ __global__ void __launch_bounds__(kNT) k_sc_small(CondArgs C, int parity, double
     __syncthreads();
   }
   (void)ns;
+}
+
+// ------------------------------------------------------------------ small interior blocks, one warp per cell
+//
+// NI <= 12 interior dofs and NF <= 24 face dofs (RT1 hexahedra, RT1 / RT2
+// quadrilaterals): the whole cell fits one warp, so nothing waits on a CTA
+// barrier or on a single thread:
+//   * Cholesky of A_ii with lane i holding row i in registers, the pivot row
+//     broadcast by shuffles (right-looking, fully unrolled);
+//   * W = A_ii^-1 [A_iF | f_i]: lane c owns column c in registers, the factor read
+//     as shared-memory broadcasts, right-looking substitution (independent updates);
+//   * x = A_ii^-1 f_i refined to double-double (3 steps): lane i forms row i of the
+//     residual with exact products, the correction L^-T L^-1 r runs lane-per-row with
+//     shuffles, the factor read from shared memory;
+//   * S_pq = A_Fq,p - sum_i A_Fi[p][i] W[i][q]: lane q owns column q of W in registers,
+//     the row p of A_Fi is a broadcast; f_S,p by lane p with error-free accumulation;
+//   * scatter by the red-black scheme with per-cell tables (row starts, block ranks).
+// The arithmetic per entry is the CTA kernel's (same summation order).
+template <int DIM, int NI, int NF>
+struct ScWarpSm {
+  static constexpr int NC = NF + 1, NS = 2 * DIM;
+  double aii[NI * NI];  // A_ii as assembled (residuals)
+  double l[NI * NI];    // its Cholesky factor, row-major lower
+  double w[NI * NC];    // [A_iF | f_i] -> [W | x]
+  double afi[NF * NI];  // A_Fi
+  double ff[NF];        // f_F
+  double xh[NI], xl[NI];
+  double invd[NI];       // 1 / L_kk
+  long long rstart[NF];  // start of the S row of face dof p
+  int frow[NF];          // its row
+  int rank[NS * NS];     // column-block rank of face slot qs in the rows of slot ps
+};
+
+template <int DIM, int NI, int NF>
+__global__ void __launch_bounds__(128, 4) k_sc_warp(CondArgs C, int parity) {
+  using SM = ScWarpSm<DIM, NI, NF>;
+  constexpr int N = NI + NF, NC = SM::NC, NS = SM::NS, DPF = NF / NS;
+  constexpr unsigned FULL = 0xffffffffu;
+  extern __shared__ __align__(16) unsigned char sc_smem[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  SM& sm = reinterpret_cast<SM*>(sc_smem)[warp];
+  const DevMesh& m = C.m;
+  const double* __restrict__ Dg = C.fx.D;
+  const double* __restrict__ Mg = C.fx.M;
+  const uint32_t cnt = static_cast<uint32_t>(parity_count(m));
+  const int il = lane < NI ? lane : NI - 1;  // lanes beyond the block repeat its last row
+  for (uint32_t t = blockIdx.x * 4 + warp; t < cnt; t += gridDim.x * 4) {
+    int cc[3];
+    const int e = parity_cell32(m, parity, t, cc);
+    if (e < 0) continue;  // (warp-uniform)
+    if (DIM == 2) cc[2] = 0;
+    const double a = __ldg(C.alpha + e), b = __ldg(C.beta + e);
+    unsigned lo = 0, hi = 0;
+#pragma unroll
+    for (int x = 0; x < DIM; ++x) {
+      const int cx = x == 0 ? cc[0] : (x == 1 ? cc[1] : cc[2]);
+      const int Nx = static_cast<int>(x == 0 ? m.N[0] : (x == 1 ? m.N[1] : m.N[2]));
+      lo |= static_cast<unsigned>(cx > 0) << x;
+      hi |= static_cast<unsigned>(cx + 1 < Nx) << x;
+    }
+    // scatter tables (their loads are in flight during the assembly)
+    if (lane < NF) {
+      const int ps = lane / DPF, sub = lane - ps * DPF, ax = ps >> 1, side = ps & 1;
+      const int face = face_id32(m, ax, cc[0] + (ax == 0 ? side : 0), cc[1] + (ax == 1 ? side : 0),
+                                 cc[2] + (ax == 2 ? side : 0));
+      const int row = face * DPF + sub;
+      sm.frow[lane] = row;
+      sm.rstart[lane] = C.rowoff[row];
+    }
+    for (int idx = lane; idx < NS * NS; idx += 32) {
+      const int ps = idx / NS, qs = idx - ps * NS, ax = ps >> 1;
+      const int ca = ax == 0 ? cc[0] : (ax == 1 ? cc[1] : cc[2]);
+      const int na = static_cast<int>(ax == 0 ? m.N[0] : (ax == 1 ? m.N[1] : m.N[2]));
+      sm.rank[idx] = col_rank_fast(DIM, ps, qs, lo, hi, ca, na, true);
+    }
+    // assembly: A_ii, [A_iF | f_i], A_Fi, f_F
+    const double* fe = C.f + static_cast<int64_t>(e) * N;
+    for (int idx = lane; idx < NI * NI; idx += 32) {
+      const int i = idx / NI, j = idx - i * NI;
+      sm.aii[idx] = assemble_entry(a, b, __ldg(Dg + i * N + j), __ldg(Mg + i * N + j));
+    }
+    for (int idx = lane; idx < NI * NF; idx += 32) {
+      const int i = idx / NF, c = idx - i * NF;
+      sm.w[i * NC + c] = assemble_entry(a, b, __ldg(Dg + i * N + NI + c), __ldg(Mg + i * N + NI + c));
+    }
+    for (int idx = lane; idx < NF * NI; idx += 32) {
+      const int p = idx / NI, i = idx - p * NI;
+      sm.afi[idx] = assemble_entry(a, b, __ldg(Dg + (NI + p) * N + i), __ldg(Mg + (NI + p) * N + i));
+    }
+    if (lane < NI) sm.w[lane * NC + NF] = fe[lane];
+    if (lane < NF) sm.ff[lane] = fe[NI + lane];
+    __syncwarp();
+    // ---- Cholesky, lane il = row il
+    {
+      double row[NI];
+#pragma unroll
+      for (int j = 0; j < NI; ++j) row[j] = sm.aii[il * NI + j];
+      bool bad = false;
+#pragma unroll
+      for (int k = 0; k < NI; ++k) {
+        const double dkk = __shfl_sync(FULL, row[k], k);
+        bad = bad || !(dkk > 0.0);
+        const double lkk = sqrt(fmax(dkk, 0.0));
+        const double inv = lkk > 0.0 ? 1.0 / lkk : 0.0;
+        if (lane == 0) sm.invd[k] = inv;
+        const double lik = il == k ? lkk : row[k] * inv;
+        row[k] = lik;
+#pragma unroll
+        for (int j = k + 1; j < NI; ++j) row[j] = fma(-lik, __shfl_sync(FULL, lik, j), row[j]);
+      }
+      if (bad && lane == 0) atomicOr(C.status, 2);
+      if (lane < NI) {
+#pragma unroll
+        for (int j = 0; j < NI; ++j) sm.l[lane * NI + j] = row[j];
+      }
+    }
+    __syncwarp();
+    // ---- [W | x] = A_ii^-1 [A_iF | f_i], lane c = column c
+    if (lane < NC) {
+      double v[NI];
+#pragma unroll
+      for (int i = 0; i < NI; ++i) v[i] = sm.w[i * NC + lane];
+#pragma unroll
+      for (int j = 0; j < NI; ++j) {
+        v[j] *= sm.invd[j];
+#pragma unroll
+        for (int i = j + 1; i < NI; ++i) v[i] = fma(-sm.l[i * NI + j], v[j], v[i]);
+      }
+#pragma unroll
+      for (int j = NI - 1; j >= 0; --j) {
+        v[j] *= sm.invd[j];
+#pragma unroll
+        for (int i = 0; i < j; ++i) v[i] = fma(-sm.l[j * NI + i], v[j], v[i]);
+      }
+#pragma unroll
+      for (int i = 0; i < NI; ++i) sm.w[i * NC + lane] = v[i];
+    }
+    __syncwarp();
+    // ---- x = A_ii^-1 f_i to double-double, lane il = entry il
+    {
+      double xh = sm.w[il * NC + NF], xl = 0.0;
+      const double fi = fe[il];
+#pragma unroll 1
+      for (int step = 0; step < 3; ++step) {
+        ddv acc = {fi, 0.0};
+#pragma unroll
+        for (int j = 0; j < NI; ++j) {
+          const double aij = sm.aii[il * NI + j];
+          acc = dd_fma_sub(acc, aij, __shfl_sync(FULL, xh, j));
+          acc.lo = fma(-aij, __shfl_sync(FULL, xl, j), acc.lo);
+        }
+        double r = acc.hi + acc.lo;
+#pragma unroll
+        for (int j = 0; j < NI; ++j) {  // L y = r
+          const double vj = __shfl_sync(FULL, r, j) * sm.invd[j];
+          r = il == j ? vj : (il > j ? fma(-sm.l[il * NI + j], vj, r) : r);
+        }
+#pragma unroll
+        for (int j = NI - 1; j >= 0; --j) {  // L^T d = y
+          const double vj = __shfl_sync(FULL, r, j) * sm.invd[j];
+          r = il == j ? vj : (il < j ? fma(-sm.l[j * NI + il], vj, r) : r);
+        }
+        const ddv v = dd_add_d({xh, xl}, r);
+        xh = v.hi, xl = v.lo;
+      }
+      if (lane < NI) sm.xh[lane] = xh, sm.xl[lane] = xl;
+    }
+    __syncwarp();
+    // ---- S and f_S
+    if (lane < NF) {
+      const int q = lane, qs = q / DPF, sj = q - qs * DPF;
+      const double sq = (qs & 1) ? 1.0 : -1.0;
+      double wq[NI];
+#pragma unroll
+      for (int i = 0; i < NI; ++i) wq[i] = sm.w[i * NC + q];
+#pragma unroll 2
+      for (int p = 0; p < NF; ++p) {
+        const int ps = p / DPF, ax = ps >> 1, side = ps & 1;
+        const bool pin = ((side ? hi : lo) >> ax) & 1u;
+        double s_ = assemble_entry(a, b, __ldg(Dg + (NI + p) * N + NI + q), __ldg(Mg + (NI + p) * N + NI + q));
+#pragma unroll
+        for (int i = 0; i < NI; ++i) s_ = fma(-sm.afi[p * NI + i], wq[i], s_);
+        double* dst = C.sval + sm.rstart[p] + static_cast<int64_t>(sm.rank[ps * NS + qs]) * DPF + sj;
+        const double v = (side ? sq : -sq) * s_;
+        *dst = (parity == 1 && pin && ps == qs) ? *dst + v : v;
+      }
+      // f_S,p = f_F,p - A_Fi x  (x in double-double), p = lane
+      const int ps = lane / DPF, ax = ps >> 1, side = ps & 1;
+      const bool pin = ((side ? hi : lo) >> ax) & 1u;
+      ddv acc = {sm.ff[lane], 0.0};
+#pragma unroll
+      for (int i = 0; i < NI; ++i) {
+        const double api = sm.afi[lane * NI + i];
+        acc = dd_fma_sub(acc, api, sm.xh[i]);
+        acc.lo = fma(-api, sm.xl[i], acc.lo);
+      }
+      const double v = (side ? 1.0 : -1.0) * (acc.hi + acc.lo);
+      const int row_ = sm.frow[lane];
+      C.fs[row_] = (parity == 1 && pin) ? C.fs[row_] + v : v;
+    }
+    __syncwarp();
+  }
+}
+
+template <int DIM, int NI, int NF>
+void launch_sc_warp(const CondArgs& c, int parity, cudaStream_t st) {
+  using SM = ScWarpSm<DIM, NI, NF>;
+  const size_t smem = 4 * sizeof(SM);
+  static const bool attr_set = [] {
+    return cudaFuncSetAttribute(k_sc_warp<DIM, NI, NF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(4 * sizeof(SM))) == cudaSuccess;
+  }();
+  (void)attr_set;
+  const int64_t cnt = parity_count(c.m);
+  const unsigned grid = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>((cnt + 3) / 4, 148 * 8)));
+  k_sc_warp<DIM, NI, NF><<<grid, 128, smem, st>>>(c, parity);
 }
 
 // One warp: y <- L^-T L^-1 y for CPW columns y_c (stride ys) with the
@@ -594,6 +811,18 @@ void launch_condense(const CondArgs& c, int parity, double* gws, int64_t ws_doub
       k_sc_rt0<2><<<nb, 128, 0, st>>>(c, parity);
     count_launch();
     return;
+  }
+  if (!getenv("HDR_SC_NO_WARP")) {  // one warp per cell where the whole block fits a warp
+    const int dim = c.m.dim, ni = c.m.nint, nf = c.nF;
+    bool done = true;
+    if (dim == 3 && ni == 12 && nf == 24) launch_sc_warp<3, 12, 24>(c, parity, st);       // RT1 hexahedra
+    else if (dim == 2 && ni == 4 && nf == 8) launch_sc_warp<2, 4, 8>(c, parity, st);      // RT1 quadrilaterals
+    else if (dim == 2 && ni == 12 && nf == 12) launch_sc_warp<2, 12, 12>(c, parity, st);  // RT2 quadrilaterals
+    else done = false;
+    if (done) {
+      count_launch();
+      return;
+    }
   }
   if (c.m.nint <= 32) {  // small interior blocks: the 128-thread shared-memory kernel
     const ScLayout Ls = sc_layout(c.m.nint, c.nF, c.m.n);
