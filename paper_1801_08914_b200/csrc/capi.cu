@@ -1073,6 +1073,7 @@ static hdr_status run_condense(hdr_condensed_t op, const double* alpha, const do
     C.sval = op->sval.p;
     C.fs = op->fs.p;
     C.status = op->status.p;
+    C.host_consts = (sp->k == 0 && !sp->rt0_consts.empty()) ? sp->rt0_consts.data() : nullptr;
     for (int parity = 0; parity < 2; ++parity) launch_condense(C, parity, op->ws.p, op->ws_doubles, st);
     CK(cudaGetLastError());
     return check_cond_status(op->status.p, st);

@@ -804,6 +804,17 @@ __global__ void k_copy_masters(const double* xb, double* x, int64_t nmaster) {
 
 void launch_condense(const CondArgs& c, int parity, double* gws, int64_t ws_doubles, cudaStream_t st) {
   if (c.m.nint == 0) {
+    if (c.host_consts && !getenv("HDR_SC_NO_PENCIL")) {  // one pass over all cells (no colours), coalesced rows
+      PencilConst<3> p3;
+      PencilConst<2> p2;
+      if (c.m.dim == 3 ? pencil_setup<3>(c.host_consts, p3) : pencil_setup<2>(c.host_consts, p2)) {
+        if (parity == 0) {
+          if (c.m.dim == 3) launch_sc_pencil<3>(c, p3, st);
+          else launch_sc_pencil<2>(c, p2, st);
+        }
+        return;
+      }
+    }
     const unsigned nb = static_cast<unsigned>((parity_count(c.m) + 127) / 128);
     if (c.m.dim == 3)
       k_sc_rt0<3><<<nb, 128, 0, st>>>(c, parity);

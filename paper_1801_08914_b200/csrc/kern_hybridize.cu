@@ -1097,13 +1097,19 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
+__device__ __forceinline__ double quad_sum(double v) {  // over the 4 lanes of a row
+  v += __shfl_xor_sync(0xffffffffu, v, 1);
+  return v + __shfl_xor_sync(0xffffffffu, v, 2);
+}
+
 __global__ void __launch_bounds__(kNT) k_recover_cta(RecArgs R, double* gws, int64_t ws_stride, int use_smem) {
   extern __shared__ double smem[];
   double* ws = use_smem ? smem : gws + blockIdx.x * ws_stride;
   const DevMesh& m = R.m;
   const int n = m.n, r = R.fx.r, dpf = m.dpf, nint = m.nint;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const bool wide = n > 64;       // long rows: warp per row; short rows: thread per row
+  const bool wide = n > 64;       // long rows: warp per row; short rows: four lanes per row
+  const int row4 = threadIdx.x >> 2, part = threadIdx.x & 3, rows4 = blockDim.x >> 2;
   double* s = ws;                 // r
   double* y = ws + 64;            // n: current rhs
   double* t = y + kMaxN;          // n: current term
@@ -1141,11 +1147,14 @@ __global__ void __launch_bounds__(kNT) k_recover_cta(RecArgs R, double* gws, int
           u = warp_sum(u);
           if (lane == 0) xty[j] = u * s[j];
         }
-      } else {  // small elements: thread per row
-        for (int j = threadIdx.x; j < r; j += blockDim.x) {
+      } else {  // small elements: four lanes per row (launched with >= 4 n threads)
+        for (int j0 = 0; j0 < r; j0 += rows4) {
+          const int j = j0 + row4;
           double u = 0.0;
-          for (int l = 0; l < n; ++l) u = fma(__ldg(R.fx.X + static_cast<int64_t>(l) * r + j), y[l], u);
-          xty[j] = u * s[j];
+          if (j < r)
+            for (int l = part; l < n; l += 4) u = fma(__ldg(R.fx.X + static_cast<int64_t>(l) * r + j), y[l], u);
+          u = quad_sum(u);
+          if (j < r && part == 0) xty[j] = u * s[j];
         }
       }
       __syncthreads();
@@ -1163,13 +1172,19 @@ __global__ void __launch_bounds__(kNT) k_recover_cta(RecArgs R, double* gws, int
           }
         }
       } else {
-        for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        for (int i0 = 0; i0 < n; i0 += rows4) {
+          const int i = i0 + row4;
           double u = 0.0;
-          for (int l = 0; l < n; ++l) u = fma(__ldg(R.fx.N0 + static_cast<int64_t>(i) * n + l), y[l], u);
-          for (int j = 0; j < r; ++j) u = fma(__ldg(R.fx.X + static_cast<int64_t>(i) * r + j), xty[j], u);
-          u *= ib;
-          t[i] = u;
-          acc[i] = (p == 0) ? u : ((p & 1) ? acc[i] - u : acc[i] + u);
+          if (i < n) {
+            for (int l = part; l < n; l += 4) u = fma(__ldg(R.fx.N0 + static_cast<int64_t>(i) * n + l), y[l], u);
+            for (int j = part; j < r; j += 4) u = fma(__ldg(R.fx.X + static_cast<int64_t>(i) * r + j), xty[j], u);
+          }
+          u = quad_sum(u);
+          if (i < n && part == 0) {
+            u *= ib;
+            t[i] = u;
+            acc[i] = (p == 0) ? u : ((p & 1) ? acc[i] - u : acc[i] + u);
+          }
         }
       }
       __syncthreads();
@@ -1186,13 +1201,16 @@ __global__ void __launch_bounds__(kNT) k_recover_cta(RecArgs R, double* gws, int
           if (lane == 0) y[i] = u;
         }
       } else {
-        for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        for (int i0 = 0; i0 < n; i0 += rows4) {
+          const int i = i0 + row4;
           double u = 0.0;
-          for (int l = 0; l < n; ++l) {
-            const int64_t o = static_cast<int64_t>(i) * n + l;
-            u = fma(delta_entry(a, b, __ldg(R.fx.D + o), __ldg(R.fx.M + o), __ldg(R.fx.E + o), __ldg(R.fx.Ma + o)), t[l], u);
-          }
-          y[i] = u;
+          if (i < n)
+            for (int l = part; l < n; l += 4) {
+              const int64_t o = static_cast<int64_t>(i) * n + l;
+              u = fma(delta_entry(a, b, __ldg(R.fx.D + o), __ldg(R.fx.M + o), __ldg(R.fx.E + o), __ldg(R.fx.Ma + o)), t[l], u);
+            }
+          u = quad_sum(u);
+          if (i < n && part == 0) y[i] = u;
         }
       }
       __syncthreads();
@@ -1489,7 +1507,9 @@ void launch_recover_hybrid(const RecArgs& a, double* gws, int64_t ws_doubles, cu
   (void)ws_doubles;
   const size_t smem = static_cast<size_t>(64 + 3 * kMaxN + 64) * 8;
   const int64_t grid = std::min<int64_t>(a.m.ncells, 1 << 20);
-  k_recover_cta<<<static_cast<unsigned>(grid), 128, smem, st>>>(a, nullptr, 0, 1);
+  // long rows: 128 threads (warp per row); short rows: four lanes per row in one pass
+  const int threads = a.m.n > 64 ? 128 : std::min(256, ((4 * a.m.n + 31) / 32) * 32);
+  k_recover_cta<<<static_cast<unsigned>(grid), threads, smem, st>>>(a, nullptr, 0, 1);
   count_launch();
 }
 

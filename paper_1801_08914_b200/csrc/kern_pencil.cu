@@ -139,10 +139,11 @@ __device__ __forceinline__ void pencil_row(const PencilSol<DIM>& s, int r, doubl
 }
 
 template <int DIM>
-__device__ __forceinline__ void load_cell(const HybArgs& A, int64_t e, double& a, double& b, double (&f)[2 * DIM]) {
-  a = __ldg(A.alpha + e);
-  b = __ldg(A.beta + e);
-  const double2* fp = reinterpret_cast<const double2*>(A.f + e * (2 * DIM));
+__device__ __forceinline__ void load_cell(const double* alpha, const double* beta, const double* fh, int64_t e, double& a,
+                                          double& b, double (&f)[2 * DIM]) {
+  a = __ldg(alpha + e);
+  b = __ldg(beta + e);
+  const double2* fp = reinterpret_cast<const double2*>(fh + e * (2 * DIM));
 #pragma unroll
   for (int j = 0; j < DIM; ++j) {
     const double2 v = __ldg(fp + j);
@@ -191,7 +192,7 @@ __device__ __forceinline__ void staged_cell(const double2* slot, bool ok, double
 template <int DIM>
 __device__ __forceinline__ void neighbour(const HybArgs& A, const PencilConst<DIM>& pc, int64_t e, PencilSol<DIM>& s) {
   double a, b, f[2 * DIM], cond;
-  load_cell<DIM>(A, e, a, b, f);
+  load_cell<DIM>(A.alpha, A.beta, A.f, e, a, b, f);
   if (!pencil_solve<DIM>(pc, a, b, f, s, cond) || A.force_exact) pencil_zero<DIM>(s);
 }
 
@@ -201,6 +202,26 @@ __device__ __forceinline__ void solved_neighbour(const HybArgs& A, const PencilC
                                                  double b, const double (&f)[2 * DIM], PencilSol<DIM>& s) {
   double cond;
   if (!valid || !pencil_solve<DIM>(pc, a, b, f, s, cond) || A.force_exact) pencil_zero<DIM>(s);
+}
+
+// Warp-collective write-out of a staged segment: stg[q] -> dst[q] for q in
+// [pad, pad + total), dst 16-byte aligned (pad = the segment's 8-byte misalignment):
+// aligned 16-byte streaming stores, a scalar head / tail where the ends are odd.
+__device__ __forceinline__ void segment_write(double* dst, const double* stg, int pad, int total, int lane) {
+  const int qe = pad + total;
+  if (pad && lane == 0) __stcs(dst + 1, stg[1]);
+  if ((qe & 1) && lane == 31 && qe - 1 >= 2 * pad) __stcs(dst + qe - 1, stg[qe - 1]);
+  const double2* s2 = reinterpret_cast<const double2*>(stg);
+  double2* d2 = reinterpret_cast<double2*>(dst);
+  const int je = qe >> 1;
+  int j = pad + lane;
+  for (; j + 32 < je; j += 64) {  // two loads in flight, then two coalesced 16-byte stores
+    const double2 v0 = s2[j], v1 = s2[j + 32];
+    __stcs(d2 + j, v0);
+    __stcs(d2 + j + 32, v1);
+  }
+  if (j < je) __stcs(d2 + j, s2[j]);
+  __syncwarp();
 }
 
 // Warp-collective: the H rows (and g entries) of the lanes with `has`, faces of
@@ -284,21 +305,7 @@ __device__ __forceinline__ void emit_rows(const HybArgs& A, int ax, bool has, co
   }
   if (has) __stcs(A.g + row + (lane - first), hm[N] + hp[N]);
   __syncwarp();
-  double* dst = A.hval + (rs - pad);
-  const int qe = pad + total;
-  if (pad && lane == 0) __stcs(dst + 1, stg[1]);
-  if ((qe & 1) && lane == 31 && qe - 1 >= 2 * pad) __stcs(dst + qe - 1, stg[qe - 1]);
-  const double2* s2 = reinterpret_cast<const double2*>(stg);
-  double2* d2 = reinterpret_cast<double2*>(dst);
-  const int je = qe >> 1;
-  int j = pad + lane;
-  for (; j + 32 < je; j += 64) {  // two loads in flight, then two coalesced 16-byte stores
-    const double2 v0 = s2[j], v1 = s2[j + 32];
-    __stcs(d2 + j, v0);
-    __stcs(d2 + j + 32, v1);
-  }
-  if (j < je) __stcs(d2 + j, s2[j]);
-  __syncwarp();
+  segment_write(A.hval + (rs - pad), stg, pad, total, lane);
 }
 
 template <int DIM>
@@ -360,15 +367,15 @@ __global__ void __launch_bounds__(kPW * 32, HDR_PENCIL_MINB) k_rt0_pencil(HybArg
   double ya = 1.0, yb = 1.0, yf[N], za = 1.0, zb = 1.0, zf[N];
 #pragma unroll
   for (int j = 0; j < N; ++j) yf[j] = zf[j] = 0.0;
-  if (valid && y >= 1) load_cell<DIM>(A, e - N0, ya, yb, yf);
-  if (DIM == 3 && valid && z >= 1) load_cell<DIM>(A, e - static_cast<int64_t>(N0) * N1, za, zb, zf);
+  if (valid && y >= 1) load_cell<DIM>(A.alpha, A.beta, A.f, e - N0, ya, yb, yf);
+  if (DIM == 3 && valid && z >= 1) load_cell<DIM>(A.alpha, A.beta, A.f, e - static_cast<int64_t>(N0) * N1, za, zb, zf);
 #endif
   PencilSol<DIM> s;
   {
     double a = 1.0, b = 1.0, f[N], cond = 0.0;
 #pragma unroll
     for (int j = 0; j < N; ++j) f[j] = 0.0;
-    if (valid) load_cell<DIM>(A, e, a, b, f);
+    if (valid) load_cell<DIM>(A.alpha, A.beta, A.f, e, a, b, f);
     const bool ok = pencil_solve<DIM>(pc, a, b, f, s, cond);
     if (valid && A.qlog) A.qlog[e] = static_cast<float>(cond * 0x1p-53);
     if (!valid || !ok || A.force_exact) {
@@ -431,6 +438,165 @@ __global__ void __launch_bounds__(kPW * 32, HDR_PENCIL_MINB) k_rt0_pencil(HybArg
   }
 }
 
+// ------------------------------------------------------------------ k = 0 static condensation, one pass
+//
+// Without bubbles S = P^T A_hat P and f_S = P^T f_hat (static_condense,
+// src/reduction.cpp:448-557): the row of face F holds sp sq A_T[p][q] of its
+// one or two cells over all their faces, the diagonal and f_S entry the
+// two-term sums of the reference's from_triplets.  Same layout as the hybridize
+// pencil kernel: one warp per 32-cell segment of an x-line, the row of a face
+// assembled by the lane of its plus-side cell (T- by shuffle / from its inputs),
+// the rows of the faces on the far boundary (x = N0, y = N1, z = N2) by the last
+// cell / line / plane, every segment staged and written once with coalesced
+// 16-byte stores.  A_T[p][q] = fl(fl(alpha c) + fl(beta M_pq)) is assemble_entry
+// on the element's constants (M_pq = 0 across axes): bit-identical to the reference.
+template <int DIM>
+struct ScCell {  // what a row needs of a cell: gamma = fl(alpha c), beta, and the load entry of the slot
+  double gam, b;
+};
+
+// row of slot p of a cell over its own slots q, signed: h[q] = sp sq A[p][q]
+template <int DIM>
+__device__ __forceinline__ void sc_row(const PencilConst<DIM>& pc, double gam, double b, int p, double (&h)[2 * DIM]) {
+  const double sp = (p & 1) ? 1.0 : -1.0;
+#pragma unroll
+  for (int q = 0; q < 2 * DIM; ++q) {
+    double mpq = 0.0;
+    if ((q >> 1) == (p >> 1)) mpq = (p == q) ? ((p & 1) ? pc.md1[p >> 1] : pc.md0[p >> 1]) : pc.mo[p >> 1];
+    const double apq = __dadd_rn(gam, __dmul_rn(b, mpq));
+    h[q] = ((q & 1) ? sp : -sp) * apq;
+  }
+}
+
+// Warp-collective: the S rows of one x-line of faces of axis ax.  Lane = plus-side
+// cell x (hasp) with minus-side row hm (hasm); rows of lanes x0 <= x < x1; when
+// `tail` the lane of x = x1 - 1 appends the row of the far x face (its own slot-1 row
+// ht, T+ absent).  fm / fp: the signed load entries.  rs, frow: row start and row of the first face.
+template <int DIM>
+__device__ __forceinline__ void sc_emit(const CondArgs& C, int ax, bool valid, bool hasm, bool hasp, int x, int x0,
+                                        int x1, bool tail, const double (&hm)[2 * DIM], const double (&hp)[2 * DIM],
+                                        const double (&ht)[2 * DIM], double fm, double fp, double ft, long long rs,
+                                        int frow, double* stg) {
+  const int lane = threadIdx.x & 31;
+  const int lm = hasm ? 2 * DIM : 0, lp = hasp ? 2 * DIM : 0;
+  const int L = lm + lp - ((hasm && hasp) ? 1 : 0);
+  int off, total;
+  if (ax == 0) {  // only the row of x = 0 is short (no minus-side cell)
+    off = (4 * DIM - 1) * (x - x0) - ((x0 == 0 && x > 0) ? 2 * DIM - 1 : 0);
+    total = (4 * DIM - 1) * (x1 - x0) - (x0 == 0 ? 2 * DIM - 1 : 0);
+  } else {
+    off = L * (x - x0);
+    total = L * (x1 - x0);
+  }
+  const int pad = static_cast<int>((reinterpret_cast<uintptr_t>(C.sval + rs) >> 3) & 1);
+  if (valid) {
+    int p = off + pad;
+#pragma unroll
+    for (int b = 0; b < DIM; ++b) {
+      const double ml = hm[2 * b], mh = hm[2 * b + 1], pl = hp[2 * b], ph = hp[2 * b + 1];
+      if (b == ax) {
+        if (hasm) stg[p++] = ml;
+        stg[p++] = (hasm && hasp) ? mh + pl : (hasm ? mh : pl);
+        if (hasp) stg[p++] = ph;
+      } else if (b < ax) {
+        if (hasm) stg[p++] = ml, stg[p++] = mh;
+        if (hasp) stg[p++] = pl, stg[p++] = ph;
+      } else {
+        if (hasm) stg[p++] = ml;
+        if (hasp) stg[p++] = pl;
+        if (hasm) stg[p++] = mh;
+        if (hasp) stg[p++] = ph;
+      }
+    }
+    __stcs(C.fs + frow + (x - x0), (hasm && hasp) ? fm + fp : (hasm ? fm : fp));
+    if (tail && x == x1 - 1) {  // the far x face: this cell's slot-1 row alone
+      int q = total + pad;
+#pragma unroll
+      for (int j = 0; j < 2 * DIM; ++j) stg[q++] = ht[j];
+      __stcs(C.fs + frow + (x1 - x0), ft);
+    }
+  }
+  if (tail) total += 2 * DIM;
+  __syncwarp();
+  segment_write(C.sval + (rs - pad), stg, pad, total, lane);
+}
+
+template <int DIM>
+__global__ void __launch_bounds__(128, 5) k_sc_pencil(CondArgs C, PencilConst<DIM> pc, FastDiv dseg, uint32_t nwarps) {
+  constexpr int N = 2 * DIM;
+  __shared__ __align__(16) double stg_all[4][32 * (4 * DIM - 1) + 2 * DIM + 2];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t gw = blockIdx.x * 4 + warp;
+  if (gw >= nwarps) return;
+  const DevMesh& m = C.m;
+  const int N0 = static_cast<int>(m.N[0]), N1 = static_cast<int>(m.N[1]), N2 = DIM == 3 ? static_cast<int>(m.N[2]) : 1;
+  const uint32_t line = dseg.div(gw);
+  const int seg = static_cast<int>(gw - line * dseg.d);
+  const uint32_t zq = m.div_n1.div(line);
+  const int y = static_cast<int>(line - zq * static_cast<uint32_t>(N1)), z = static_cast<int>(zq);
+  const int x0 = seg * 32, x1 = min(x0 + 32, N0), x = x0 + lane;
+  const bool valid = x < N0;
+  const int64_t e = x + static_cast<int64_t>(N0) * (y + static_cast<int64_t>(N1) * z);
+  double* stg = stg_all[warp];
+  // own cell, and the entries needed of the cells before / below / behind
+  double a = 1.0, b = 1.0, f[N];
+#pragma unroll
+  for (int j = 0; j < N; ++j) f[j] = 0.0;
+  if (valid) load_cell<DIM>(C.alpha, C.beta, C.f, e, a, b, f);
+  double ya = 1.0, yb = 1.0, yf = 0.0, za = 1.0, zb = 1.0, zf = 0.0;
+  if (valid && y >= 1) {
+    const int64_t en = e - N0;
+    ya = __ldg(C.alpha + en), yb = __ldg(C.beta + en), yf = __ldg(C.f + en * N + 3);
+  }
+  if (DIM == 3 && valid && z >= 1) {
+    const int64_t en = e - static_cast<int64_t>(N0) * N1;
+    za = __ldg(C.alpha + en), zb = __ldg(C.beta + en), zf = __ldg(C.f + en * N + (N - 1));
+  }
+  double xa = __shfl_up_sync(0xffffffffu, a, 1), xb = __shfl_up_sync(0xffffffffu, b, 1);
+  double xf = __shfl_up_sync(0xffffffffu, f[1], 1);
+  if (lane == 0 && seg > 0 && valid) {
+    xa = __ldg(C.alpha + e - 1), xb = __ldg(C.beta + e - 1), xf = __ldg(C.f + (e - 1) * N + 1);
+  }
+  const double gam = __dmul_rn(a, pc.c);
+  double hm[N], hp[N], ht[N];
+  // x faces
+  {
+    sc_row<DIM>(pc, __dmul_rn(xa, pc.c), xb, 1, hm);
+    sc_row<DIM>(pc, gam, b, 0, hp);
+    sc_row<DIM>(pc, gam, b, 1, ht);
+    const int face0 = face_id32(m, 0, x0, y, z);
+    sc_emit<DIM>(C, 0, valid, x >= 1, true, x, x0, x1, x1 == N0, hm, hp, ht, xf, -f[0], f[1],
+                 __ldg(C.rowoff + face0), face0, stg);
+  }
+  // y faces (and the far y boundary from the last line)
+  {
+    sc_row<DIM>(pc, __dmul_rn(ya, pc.c), yb, 3, hm);
+    sc_row<DIM>(pc, gam, b, 2, hp);
+    const int face0 = face_id32(m, 1, x0, y, z);
+    sc_emit<DIM>(C, 1, valid, y >= 1, true, x, x0, x1, false, hm, hp, ht, yf, -f[2], 0.0, __ldg(C.rowoff + face0),
+                 face0, stg);
+    if (y == N1 - 1) {
+      sc_row<DIM>(pc, gam, b, 3, hm);
+      const int facet = face_id32(m, 1, x0, y + 1, z);
+      sc_emit<DIM>(C, 1, valid, true, false, x, x0, x1, false, hm, hp, ht, f[3], 0.0, 0.0, __ldg(C.rowoff + facet),
+                   facet, stg);
+    }
+  }
+  if (DIM == 3) {
+    sc_row<DIM>(pc, __dmul_rn(za, pc.c), zb, N - 1, hm);
+    sc_row<DIM>(pc, gam, b, N - 2, hp);
+    const int face0 = face_id32(m, 2, x0, y, z);
+    sc_emit<DIM>(C, 2, valid, z >= 1, true, x, x0, x1, false, hm, hp, ht, zf, -f[N - 2], 0.0, __ldg(C.rowoff + face0),
+                 face0, stg);
+    if (z == N2 - 1) {
+      sc_row<DIM>(pc, gam, b, N - 1, hm);
+      const int facet = face_id32(m, 2, x0, y, z + 1);
+      sc_emit<DIM>(C, 2, valid, true, false, x, x0, x1, false, hm, hp, ht, f[N - 1], 0.0, 0.0, __ldg(C.rowoff + facet),
+                   facet, stg);
+    }
+  }
+}
+
 }  // namespace
 
 // host check of the structure the pencil kernel relies on (reference D, M as
@@ -476,5 +642,16 @@ void launch_rt0_pencil(const HybArgs& a, const PencilConst<DIM>& pc, cudaStream_
 }
 template void launch_rt0_pencil<2>(const HybArgs&, const PencilConst<2>&, cudaStream_t);
 template void launch_rt0_pencil<3>(const HybArgs&, const PencilConst<3>&, cudaStream_t);
+
+template <int DIM>
+void launch_sc_pencil(const CondArgs& c, const PencilConst<DIM>& pc, cudaStream_t st) {
+  const int nseg = static_cast<int>((c.m.N[0] + 31) / 32);
+  const int64_t nwarps = static_cast<int64_t>(nseg) * c.m.N[1] * (DIM == 3 ? c.m.N[2] : 1);
+  const unsigned grid = static_cast<unsigned>((nwarps + 3) / 4);
+  k_sc_pencil<DIM><<<grid, 128, 0, st>>>(c, pc, FastDiv(static_cast<uint32_t>(nseg)), static_cast<uint32_t>(nwarps));
+  count_launch();
+}
+template void launch_sc_pencil<2>(const CondArgs&, const PencilConst<2>&, cudaStream_t);
+template void launch_sc_pencil<3>(const CondArgs&, const PencilConst<3>&, cudaStream_t);
 
 }  // namespace hdr

@@ -153,7 +153,11 @@ struct CondArgs {
   const double* xb;  // recover_condensed input (nS)
   double* x;         // recover_condensed output (ndofs)
   int* status;       // bit 1: A_ii not SPD
+  const double* host_consts = nullptr;  // k = 0: the packed host constants (pencil_setup), else null
 };
+// k = 0 static condensation in one pass (kern_pencil.cu), for elements with the pencil structure
+template <int DIM>
+void launch_sc_pencil(const CondArgs& c, const PencilConst<DIM>& pc, cudaStream_t st);
 void launch_condense(const CondArgs& c, int parity, double* gws, int64_t ws_doubles, cudaStream_t st);
 int64_t condense_ws_doubles(const DevMesh& m, int nF);
 void launch_recover_condensed(const CondArgs& c, double* gws, int64_t ws_doubles, cudaStream_t st);
