@@ -130,3 +130,26 @@ def test_anisotropic_cells_take_the_structured_kernels(dim, cells):
     sp = hd.Space(dim, cells, 0)
     hv, gv = sp.hybridize(o.get("alpha"), o.get("beta"), o.get("f_hat")).values()
     assert rel_err(hv, o.get("H.values_dd")) <= TOL and rel_err(gv, o.get("g_dd")) <= TOL
+
+
+@pytest.mark.parametrize("dim,cells", MESHES)
+def test_condense_pencil_bit_identical(dim, cells, monkeypatch):
+    """k = 0 static condensation in one pass (k_sc_pencil): S and f_S carry the
+    reference's bits (the oracle's port is pinned bit-exact to the reference) on
+    every boundary configuration, and equal the two-colour kernel's"""
+    h = [1.0 / max(cells)] * dim
+    o = Oracle(dim, cells, 0)
+    o.set_h(h + [1.0] * (3 - dim))
+    o.gen_inputs("logu:1e-2:1e2", 99)
+    o.run("port_condense")
+    a, b, f = o.get("alpha"), o.get("beta"), o.get("f_hat")
+    sp = hd.Space(dim, cells, 0, sizes=h)
+    ro, ci = sp.pattern("S")
+    assert np.array_equal(ro, o.getq("S.row_offsets")) and np.array_equal(ci, o.getq("S.col_indices"))
+    n0 = hd.launch_count()
+    sv, fs = sp.static_condense(a, b, f).values()
+    assert hd.launch_count() - n0 <= 1  # one pass, no colours
+    assert np.array_equal(sv, o.get("S.values")) and np.array_equal(fs, o.get("f_s"))
+    monkeypatch.setenv("HDR_SC_NO_PENCIL", "1")
+    sv2, fs2 = sp.static_condense(a, b, f).values()
+    assert np.array_equal(sv, sv2) and np.array_equal(fs, fs2)
