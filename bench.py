@@ -597,21 +597,19 @@ def stage_bench(args):
         flops = 2 * nnz
         byts = 12 * nnz + 8 * (m + 1) + 16 * m
         metric = "rows/s of SpMV with H (reference row-sum order)"
-    for _ in range(args.warmup):
-        run()
+    # timed like the headline: L2 flushed before each step, CUDA events on the library's
+    # stream, the step replayed from a CUDA graph when it captures (else launched directly)
+    run()
     torch.cuda.synchronize()
-    ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     l0 = hd.launch_count()
+    run()
+    torch.cuda.synchronize()
+    per_step = hd.launch_count() - l0
+    timer = Timer(torch, stream, flush, not args.no_graph)
     with ClockSampler(torch.cuda.current_device()) as clk:
-        for i in range(args.steps):
-            flush.fill_(float(i))
-            ev0[i].record(stream)
-            run()
-            ev1[i].record(stream)
-        torch.cuda.synchronize()
-    launches = hd.launch_count() - l0
-    ms = float(np.mean([a.elapsed_time(b) for a, b in zip(ev0, ev1)]))
+        ms_list, graphed = timer.run(run, lambda: None, args.steps, args.warmup)
+    launches = per_step * args.steps
+    ms = float(np.mean(ms_list))
     units = m if args.stage == "spmv" else nc
     peak, kind = load_peaks()
     tfl, _ = hd.measure_fp64_peak()
@@ -626,7 +624,7 @@ def stage_bench(args):
                       "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
                       "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
                       "data": "synthetic", "config": {"workload": cfg["desc"], "stage": args.stage,
-                                                      "l2": "flushed between steps"},
+                                                      "l2": "flushed between steps", "cuda_graph": graphed},
                       "roofline": roof, "gpu_launches": launches, "clocks": clk.summary()}))
     return 0
 

@@ -1174,9 +1174,9 @@ static hdr_status spmv_common(hdr_space_t sp, int which, const double* vals, con
       py = dy.p;
     }
     if (which == 0)
-      launch_spmv32(nr, sp->row_h.p, sp->col_h.p, vals, px, py, st);
+      launch_spmv32(nr, sp->row_h.p, sp->col_h.p, vals, px, py, st, sp->nnz_h);
     else
-      launch_spmv32(nr, sp->row_s.p, sp->col_s.p, vals, px, py, st);
+      launch_spmv32(nr, sp->row_s.p, sp->col_s.p, vals, px, py, st, sp->nnz_s);
     CK(cudaGetLastError());
     if (!on_device) CK(cudaMemcpyAsync(y, py, static_cast<size_t>(nr) * 8, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
@@ -1274,7 +1274,7 @@ hdr_status hdr_csr_spmv_host(int64_t nrows, int64_t ncols, const int64_t* row_of
       CK(cudaMemcpy(v.p, values, static_cast<size_t>(nnz) * 8, cudaMemcpyHostToDevice));
     }
     if (ncols) CK(cudaMemcpy(dx.p, x, static_cast<size_t>(ncols) * 8, cudaMemcpyHostToDevice));
-    launch_spmv64(nrows, ro.p, ci.p, v.p, dx.p, dy.p, nullptr);
+    launch_spmv64(nrows, ro.p, ci.p, v.p, dx.p, dy.p, nullptr, nnz);
     CK(cudaGetLastError());
     if (nrows) CK(cudaMemcpy(y, dy.p, static_cast<size_t>(nrows) * 8, cudaMemcpyDeviceToHost));
     return HDR_OK;

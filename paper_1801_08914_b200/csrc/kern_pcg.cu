@@ -169,7 +169,7 @@ hdr_status pcg_device(int64_t n, const int64_t* ro, const int32_t* ci32, const i
     CK(cudaMemcpyAsync(h2, two.p, 16, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
   };
-  auto spmv = [&](const double* in, double* out) { launch_spmv32(n, A.ro.p, A.ci.p, A.v.p, in, out, st); };
+  auto spmv = [&](const double* in, double* out) { launch_spmv32(n, A.ro.p, A.ci.p, A.v.p, in, out, st, A.nnz); };
   // x = 0, r = b, z = M^-1 r, p = z
   k_pcg_init<<<kRB, kRT, 0, st>>>(n, b, x, r.p, dv, z.p, p.p);
   count_launch();

@@ -163,10 +163,12 @@ int64_t condense_ws_doubles(const DevMesh& m, int nF);
 void launch_recover_condensed(const CondArgs& c, double* gws, int64_t ws_doubles, cudaStream_t st);
 
 // ---- spmv (kern_spmv.cu)
+// nnz (when known) selects the form: long rows (>= 32 entries on average) go through the
+// coalesced warp-tile kernel, short rows through thread-per-row; both give the same bits
 void launch_spmv32(int64_t nrows, const int64_t* ro, const int32_t* ci, const double* v, const double* x, double* y,
-                   cudaStream_t st);
+                   cudaStream_t st, int64_t nnz = -1);
 void launch_spmv64(int64_t nrows, const int64_t* ro, const int64_t* ci, const double* v, const double* x, double* y,
-                   cudaStream_t st);
+                   cudaStream_t st, int64_t nnz = -1);
 
 
 // ---- algebraic batch path (kern_alg.cu): general ReductionInputs
