@@ -376,6 +376,55 @@ def roofline_for(cfg: dict, ms: float, hbm_peak: float, fp64: tuple) -> dict:
     return f64
 
 
+# the stages each BASELINE config names beside hybridization (BASELINE.json configs)
+CONFIG_STAGES = {1: ("recover", "spmv"), 2: ("condense", "spmv"), 3: ("condense", "recover", "spmv"), 4: ("spmv",),
+                 5: ("recover", "spmv")}
+
+
+def stage_case(hd, torch, sp, stage: str, a_d, b_d, f_d):
+    """One call of a stage on device-resident inputs and its SURVEY.md §8(d) cost model:
+    (run, flops, bytes, units, metric, objects to keep alive)."""
+    n, nc, m = sp.n, sp.ncells, sp.m
+    nint = sp.info["interior_dofs_per_cell"]
+    nb = n - nint
+    lib = hd._lib()
+    if stage == "condense":
+        cop = sp.static_condense(a_d, b_d, f_d)
+
+        def run():
+            st = lib.hdr_static_condense_fe_into(cop._h, a_d.data_ptr(), b_d.data_ptr(), f_d.data_ptr(), 1)
+            assert st == 0, hd._capi.last_error()
+        flops = nc * (2 * (nint ** 3 / 3 + nint ** 2 * nb + nint * nb ** 2) + 2 * (nint ** 2 + nint * nb) + 3 * n ** 2)
+        byts = nc * (16 + 8 * n) + 8 * (sp.info["nnz_s"] + sp.info["n_s"])
+        return run, flops, byts, nc, "elements/s of static condensation (assemble+condense+scatter)", (cop,)
+    op = sp.hybridize(a_d, b_d, f_d)
+    if stage == "recover":
+        lam = torch.from_numpy(np.random.default_rng(3).uniform(-1, 1, m)).cuda()
+
+        def run():
+            op.recover(lam, f_d)
+        flops = nc * (2 * n ** 3 / 3 + 4 * n ** 2)
+        byts = nc * (16 + 16 * n) + 8 * m
+        return run, flops, byts, nc, "elements/s of hybrid recovery (x_hat = A^-1 (f - C^T lambda), averaged x)", (op, lam)
+    x = torch.from_numpy(np.random.default_rng(4).uniform(-1, 1, m)).cuda()
+    nnz = sp.info["nnz_h"]
+
+    def run():
+        op.spmv(x)
+    return run, 2 * nnz, 12 * nnz + 8 * (m + 1) + 16 * m, m, "rows/s of SpMV with H (reference row-sum order)", (op, x)
+
+
+def stage_roofline(stage: str, ms: float, flops: float, byts: float, hbm_peak: float, fp64_peak: float) -> dict:
+    bw = byts / (ms * 1e-3) / 1e9
+    fl = flops / (ms * 1e-3) / 1e12
+    hbm_frac, fp_frac = bw / hbm_peak, fl / fp64_peak
+    roof = ({"bound": "hbm", "achieved": bw, "peak": hbm_peak, "unit": "GB/s", "frac": hbm_frac, "traffic": None}
+            if hbm_frac >= fp_frac or stage == "spmv" else
+            {"bound": "fp64", "achieved": fl, "peak": fp64_peak, "unit": "TFLOP/s", "frac": fp_frac, "traffic": None})
+    roof.update({"algorithmic_bytes_per_step": byts, "algorithmic_flops_per_step": flops})
+    return roof
+
+
 def measure_config(hd, torch, timer, cfg_id: int, steps: int, warmup: int, hbm_peak: float, fp64: tuple,
                    seed=None) -> dict:
     """One BASELINE config timed like the headline (device-resident inputs)."""
@@ -397,6 +446,18 @@ def measure_config(hd, torch, timer, cfg_id: int, steps: int, warmup: int, hbm_p
     rec = {"workload": cfg["desc"], "value": sp.ncells / (ms * 1e-3), "unit": UNIT, "ms_per_step": ms,
            "roofline": roofline_for(cfg, ms, hbm_peak, fp64), "exact_cells": exact,
            "gpu_launches_per_step": per_step, "cuda_graph": graphed}
+    # the other stages BASELINE names for this config, timed the same way (fewer steps)
+    rec["stages"] = {}
+    for stage in CONFIG_STAGES.get(cfg_id, ()):
+        run, flops, byts, units, _metric, keep = stage_case(hd, torch, sp, stage, a_d, b_d, f_d)
+        # the stage calls return a status (they synchronise): launched directly, not graph-captured
+        s_ms, s_graph = Timer(torch, timer.stream, timer.flush, False).run(run, lambda: None, max(3, steps // 2), 2)
+        s_ms = float(np.mean(s_ms))
+        rec["stages"][stage] = {"ms_per_step": s_ms, "value": units / (s_ms * 1e-3),
+                                "unit": "rows/s" if stage == "spmv" else UNIT,
+                                "roofline": stage_roofline(stage, s_ms, flops, byts, hbm_peak, fp64[0]),
+                                "cuda_graph": s_graph}
+        del run, keep
     del op, sp
     torch.cuda.synchronize()
     return rec
@@ -564,62 +625,24 @@ def stage_bench(args):
     sp.set_stream(stream.cuda_stream)
     a_d, b_d, f_d = (torch.from_numpy(x).cuda() for x in (alpha, beta, f_hat))
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float64, device="cuda")
-    n, nc, m = sp.n, sp.ncells, sp.m
-    dpf = sp.info["dofs_per_face"]
-    nint = sp.info["interior_dofs_per_cell"]
-    nb = n - nint
-    lib = hd._lib()
-    if args.stage == "condense":
-        cop = sp.static_condense(a_d, b_d, f_d)
-
-        def run():
-            st = lib.hdr_static_condense_fe_into(cop._h, a_d.data_ptr(), b_d.data_ptr(), f_d.data_ptr(), 1)
-            assert st == 0, hd._capi.last_error()
-        flops = nc * (2 * (nint ** 3 / 3 + nint ** 2 * nb + nint * nb ** 2) + 2 * (nint ** 2 + nint * nb) + 3 * n ** 2)
-        byts = nc * (16 + 8 * n) + 8 * (sp.info["nnz_s"] + sp.info["n_s"])
-        metric = "elements/s of static condensation (assemble+condense+scatter)"
-    elif args.stage == "recover":
-        op = sp.hybridize(a_d, b_d, f_d)
-        lam = torch.from_numpy(np.random.default_rng(3).uniform(-1, 1, m)).cuda()
-
-        def run():
-            op.recover(lam, f_d)
-        flops = nc * (2 * n ** 3 / 3 + 4 * n ** 2)
-        byts = nc * (16 + 16 * n) + 8 * m
-        metric = "elements/s of hybrid recovery (x_hat = A^-1 (f - C^T lambda), averaged x)"
-    else:  # spmv
-        op = sp.hybridize(a_d, b_d, f_d)
-        x = torch.from_numpy(np.random.default_rng(4).uniform(-1, 1, m)).cuda()
-        nnz = sp.info["nnz_h"]
-
-        def run():
-            op.spmv(x)
-        flops = 2 * nnz
-        byts = 12 * nnz + 8 * (m + 1) + 16 * m
-        metric = "rows/s of SpMV with H (reference row-sum order)"
-    # timed like the headline: L2 flushed before each step, CUDA events on the library's
-    # stream, the step replayed from a CUDA graph when it captures (else launched directly)
+    run, flops, byts, units, metric, _keep = stage_case(hd, torch, sp, args.stage, a_d, b_d, f_d)
+    nc, m = sp.ncells, sp.m
+    # timed like the headline (L2 flushed before each step, CUDA events on the library's
+    # stream), launched directly through the public call
     run()
     torch.cuda.synchronize()
     l0 = hd.launch_count()
     run()
     torch.cuda.synchronize()
     per_step = hd.launch_count() - l0
-    timer = Timer(torch, stream, flush, not args.no_graph)
+    timer = Timer(torch, stream, flush, False)  # the stage calls return a status (they synchronise): no graph
     with ClockSampler(torch.cuda.current_device()) as clk:
         ms_list, graphed = timer.run(run, lambda: None, args.steps, args.warmup)
     launches = per_step * args.steps
     ms = float(np.mean(ms_list))
-    units = m if args.stage == "spmv" else nc
     peak, kind = load_peaks()
     tfl, _ = hd.measure_fp64_peak()
-    bw = byts / (ms * 1e-3) / 1e9
-    fl = flops / (ms * 1e-3) / 1e12
-    hbm_frac, fp_frac = bw / peak, fl / tfl
-    roof = ({"bound": "hbm", "achieved": bw, "peak": peak, "unit": "GB/s", "frac": hbm_frac, "traffic": None}
-            if hbm_frac >= fp_frac or args.stage == "spmv" else
-            {"bound": "fp64", "achieved": fl, "peak": tfl, "unit": "TFLOP/s", "frac": fp_frac, "traffic": None})
-    roof.update({"algorithmic_bytes_per_step": byts, "algorithmic_flops_per_step": flops})
+    roof = stage_roofline(args.stage, ms, flops, byts, peak, tfl)
     print(json.dumps({"metric": metric, "value": units / (ms * 1e-3), "unit": "rows/s" if args.stage == "spmv" else UNIT,
                       "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
                       "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
