@@ -58,7 +58,7 @@ struct hdr_space_s {
   DBuf<double> fixed;  // D, M, E, Ma, N0 (n*n each), X (n*r), lam (r)
   std::vector<double> rt0_consts;  // packed constant block of the k = 0 kernel
   DBuf<uint64_t> rank_tab;         // k = 0 row-rank table
-  DBuf<longlong2> frs;             // k = 0 per-face {row start, row}
+  DBuf<longlong2> frs;             // per-face {row start, row} (k = 0 kernels, warp kernels)
   DBuf<double> premat;             // k >= 2 (3D): [N0 ; X^T] column-major ((n + r) x n)
   DBuf<double> dtab;               // k >= 2 (3D): {D, M} in the tensor-core chunk order
   DBuf<float> etab;                // k >= 2 (3D): {E, Ma} (fp32) likewise
@@ -480,6 +480,8 @@ hdr_status hdr_space_create(int dim, const int64_t cells[3], const double h[3], 
       const std::vector<uint64_t> tab = rank_table_rt0(dim);
       sp->rank_tab.alloc(tab.size());
       CK(cudaMemcpyAsync(sp->rank_tab.p, tab.data(), tab.size() * 8, cudaMemcpyHostToDevice, st));
+    }
+    {  // per-face {row start, row}: the k = 0 kernels and the warp kernels reach a row with one load
       sp->frs.alloc(static_cast<size_t>(sp->nfaces));
       launch_face_rows(sp->nfaces, sp->mbase.p, sp->row_h.p, sp->frs.p, st);
     }

@@ -77,9 +77,11 @@ struct WarpSmem {
   double f[S::N];              // f_T
   double nf[S::N];             // N0 f
   double s[S::R];
-  long long rstart[2 * DIM];  // H row offset of the first row of each interior face slot (-1: boundary)
-  int rlen[2 * DIM];          // H row length of that face's rows
-  int grow[2 * DIM];          // multiplier index of the face's first row
+  // {H row offset, multiplier index} of the first row of each interior face slot ({-1, -1}:
+  // boundary), copied by cp.async from the per-face table at cell start: no thread waits on
+  // the load before the scatter at the end of the cell
+  alignas(16) longlong2 frs[2 * DIM];
+  int rlen[2 * DIM];          // H row length of that face's rows (closed form)
   int rank[4 * DIM * DIM];    // column-block rank of own slot t in the rows of slot s (-1: boundary)
   float red[8];               // cross-warp reduction scratch
 };
@@ -393,16 +395,19 @@ __device__ __forceinline__ void warp_cell(const HybArgs& A, int e, int parity, i
       if (pin) {
         const int face = face_id32(A.m, a_, cc[0] + (a_ == 0 ? side : 0), cc[1] + (a_ == 1 ? side : 0),
                                    cc[2] + (a_ == 2 ? side : 0));
-        const int row = A.mbase[face];
-        const int64_t r0s = A.rowoff[row];
-        sm.rstart[ps] = r0s;
-        sm.rlen[ps] = static_cast<int>(A.rowoff[row + 1] - r0s);
-        sm.grow[ps] = row;
+        cp_async16(&sm.frs[ps], A.frs + face);
+        // row length: the multipliers of the interior faces of the cell and of its
+        // neighbour across the face, the shared face once
+        const int cn = ca + (side ? 1 : -1);
+        const int nif_own = __popc(lo) + __popc(hi);
+        const int nif_nb = nif_own - ((lo >> a_) & 1) - ((hi >> a_) & 1) + (cn > 0) + (cn + 1 < na);
+        sm.rlen[ps] = DPF * (nif_own + nif_nb - 1);
       } else {
-        sm.rstart[ps] = -1;
+        sm.frs[ps] = make_longlong2(-1, -1);
       }
     }
   }
+  asm volatile("cp.async.commit_group;" ::: "memory");
   for (int j = lane; j < R; j += GT) sm.s[j] = b / fma(a, __ldg(fx.lam + j), b);
   if (GT >= N + R && pre) {
     // [N0 f ; X^T f] of every cell from one batched fp64 GEMM before the launch,
@@ -594,6 +599,8 @@ __device__ __forceinline__ void warp_cell(const HybArgs& A, int e, int parity, i
   }
   // scatter: H_pc = V_F(p, c) (fp64) - C_pc ; g_p = w_F(p) - C_p,NF, through the
   // per-cell tables built at the start; consecutive lanes write consecutive columns.
+  asm volatile("cp.async.wait_group 0;" ::: "memory");  // the row starts copied at cell start
+  gsync<GT>();
   if constexpr (DPF % 2 == 0) {
     // one (row, face block) run of DPF consecutive doubles per work item, stored
     // as double2 (H rows start at multiples of DPF doubles, cudaMalloc'd base);
@@ -601,7 +608,7 @@ __device__ __forceinline__ void warp_cell(const HybArgs& A, int e, int parity, i
     for (int idx = lane; idx < NF * NS; idx += GT) {
       const int p = idx / NS, qs = idx - p * NS;
       const int ps = p / DPF, sub = p - ps * DPF;
-      const int64_t rs = sm.rstart[ps];
+      const int64_t rs = sm.frs[ps].x;
       const int rk = sm.rank[ps * NS + qs];
       if (rs < 0 || rk < 0) continue;
       double2* hp = reinterpret_cast<double2*>(A.hval + rs + static_cast<int64_t>(sub) * sm.rlen[ps] + rk * DPF);
@@ -622,20 +629,20 @@ __device__ __forceinline__ void warp_cell(const HybArgs& A, int e, int parity, i
     }
     for (int p = lane; p < NF; p += GT) {
       const int ps = p / DPF, sub = p - ps * DPF;
-      if (sm.rstart[ps] < 0) continue;
+      if (sm.frs[ps].x < 0) continue;
       const double v = exact ? 0.0 : sm.vf[p * NC + NF] - static_cast<double>(corr[p * NCP + NF]);
-      double* gp = A.g + sm.grow[ps] + sub;
+      double* gp = A.g + sm.frs[ps].y + sub;
       *gp = parity ? *gp + v : v;
     }
   } else {
     for (int idx = lane; idx < NF * NC; idx += GT) {
       const int p = idx / NC, c = idx - p * NC;
       const int ps = p / DPF, sub = p - ps * DPF;
-      const int64_t rs = sm.rstart[ps];
+      const int64_t rs = sm.frs[ps].x;
       if (rs < 0) continue;
       const double v = exact ? 0.0 : sm.vf[p * NC + c] - static_cast<double>(corr[p * NCP + c]);
       if (c == NF) {
-        double* gp = A.g + sm.grow[ps] + sub;
+        double* gp = A.g + sm.frs[ps].y + sub;
         *gp = parity ? *gp + v : v;
         continue;
       }
