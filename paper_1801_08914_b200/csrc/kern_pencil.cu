@@ -22,13 +22,15 @@
 //
 // Acceptance (DESIGN.md §2 "Fail-safe"): a cell whose condition bound
 // (1 + gamma sigma) sum_a tr(P_a) sum_a tr(P_a)/det(P_a) (at most dim^2 times the
-// bound with maxima) exceeds kPencilCond, or whose
-// blocks are not positive definite, contributes zeros and is listed for the
-// exact double-double path (k_rt0_exact, the reference's SingularBlock rule):
-// the reference's LU pivots of an accepted SPD cell are >= lambda_min / G >= 1e-12 / G
-// of the block maximum (G <= 2^(n-1) = 32 the partial-pivoting growth), above its
-// 1e-14 threshold.  BASELINE config 2's worst cell has a bound of ~5e9; the bound
-// grows like h^-2 alpha / beta.
+// bound with maxima) exceeds kPencilCond, or whose blocks are not positive definite,
+// contributes zeros in the fast pass; a warp with such a cell in any of its rows
+// (its own cells or the cells below / behind / before them) then runs the segment
+// again, out of line, with the exact double-double rows of those cells (rt0_exact,
+// the reference's SingularBlock rule) and rewrites its rows: no list, no second
+// launch, no ordering between CTAs.  The reference's LU pivots of an accepted SPD
+// cell are >= lambda_min / G >= 1e-12 / G of the block maximum (G <= 2^(n-1) = 32 the
+// partial-pivoting growth), above its 1e-14 threshold.  BASELINE config 2's worst cell
+// has a bound of ~5e9; the bound grows like h^-2 alpha / beta.
 //
 // Scatter.  One warp per 32-cell segment of an x-line (lane = cell).  The H row of
 // the interior face between cells T- and T+ (T+ the cell on the face's plus side) is
@@ -42,6 +44,7 @@
 // entry / g entry meet as fl(h(T-) + h(T+)), the reference's two-term sum.
 #include "hdr_device.cuh"
 #include "kernels.hpp"
+#include "rt0_exact.cuh"
 
 namespace hdr {
 
@@ -53,9 +56,6 @@ namespace {
 constexpr int kPW = HDR_PENCIL_PW;  // warps per CTA
 #ifndef HDR_PENCIL_MINB
 #define HDR_PENCIL_MINB 5               // CTAs per SM asked of ptxas: 96 registers, no spills, 20 warps per SM
-#endif
-#ifndef HDR_PENCIL_STAGE
-#define HDR_PENCIL_STAGE 1              // neighbour inputs wait in shared memory (cp.async) instead of registers
 #endif
 constexpr double kPencilCond = 1e12;  // acceptance bound on cond(A_T)
 
@@ -187,21 +187,45 @@ __device__ __forceinline__ void staged_cell(const double2* slot, bool ok, double
   }
 }
 
+// Row r of [A_T^-1 | A_T^-1 f] of a cell the closed form does not accept: the exact
+// double-double path (rt0_exact, the reference's SingularBlock rule), out of line
+// and through shared memory so that the fast path keeps its registers.  Every lane
+// that needs a row of such a cell (its own lane, the lanes above / behind it)
+// computes it itself: no list, no second launch, no ordering between CTAs.
+template <int DIM>
+__device__ __noinline__ void pencil_exact_row(const double* D, const double* M, double a, double b, unsigned bmask,
+                                              const double* f, int r, int* status, double* out) {
+  constexpr int N = 2 * DIM, NC = N + 1;
+  double hx[N * NC];
+  for (int i = 0; i < N * NC; ++i) hx[i] = 0.0;  // a singular cell raises through status; its rows stay zero
+  rt0_exact<N, NC, true>(D, M, a, b, bmask, f, nullptr, hx, status);
+  for (int q = 0; q < NC; ++q) out[q] = hx[r * NC + q];
+}
+
 // the solution of a neighbour cell (zero when the cell is not accepted: its own
 // lane lists it for the exact path)
+// (returns the kind of the cell: 0 none, 1 closed form, 2 exact path)
 template <int DIM>
-__device__ __forceinline__ void neighbour(const HybArgs& A, const PencilConst<DIM>& pc, int64_t e, PencilSol<DIM>& s) {
+__device__ __forceinline__ int neighbour(const HybArgs& A, const PencilConst<DIM>& pc, int64_t e, PencilSol<DIM>& s) {
   double a, b, f[2 * DIM], cond;
   load_cell<DIM>(A.alpha, A.beta, A.f, e, a, b, f);
-  if (!pencil_solve<DIM>(pc, a, b, f, s, cond) || A.force_exact) pencil_zero<DIM>(s);
+  if (!pencil_solve<DIM>(pc, a, b, f, s, cond) || A.force_exact) {
+    pencil_zero<DIM>(s);
+    return 2;
+  }
+  return 1;
 }
 
 // the same from prefetched inputs (zero for lanes without a cell)
 template <int DIM>
-__device__ __forceinline__ void solved_neighbour(const HybArgs& A, const PencilConst<DIM>& pc, bool valid, double a,
-                                                 double b, const double (&f)[2 * DIM], PencilSol<DIM>& s) {
+__device__ __forceinline__ int solved_neighbour(const HybArgs& A, const PencilConst<DIM>& pc, bool valid, double a,
+                                                double b, const double (&f)[2 * DIM], PencilSol<DIM>& s) {
   double cond;
-  if (!valid || !pencil_solve<DIM>(pc, a, b, f, s, cond) || A.force_exact) pencil_zero<DIM>(s);
+  if (!valid || !pencil_solve<DIM>(pc, a, b, f, s, cond) || A.force_exact) {
+    pencil_zero<DIM>(s);
+    return valid ? 2 : 0;
+  }
+  return 1;
 }
 
 // Warp-collective write-out of a staged segment: stg[q] -> dst[q] for q in
@@ -287,13 +311,8 @@ __device__ __forceinline__ void emit_rows(const HybArgs& A, int ax, bool has, co
     total = (x1 - xs) * lfull - (xs == 0 ? 2 : 0) - (x1 == n0 ? 2 : 0);
   }
   // {row start, row} of the first row (staged by lane `first` at kernel start)
-#if HDR_PENCIL_STAGE
   const longlong2 fqv = *fq;  // broadcast read of the staged pair
   const long long rs = fqv.x, row = fqv.y;
-#else
-  const long long rs = __shfl_sync(0xffffffffu, fq->x, first);
-  const long long row = __shfl_sync(0xffffffffu, fq->y, first);
-#endif
   // staged at the parity of the global position, so that the write-out moves
   // aligned 16-byte pairs: stg[q] <-> hval[rs - pad + q] (pad: the 8-byte misalignment)
   const int pad = static_cast<int>((reinterpret_cast<uintptr_t>(A.hval + rs) >> 3) & 1);  // any 8-byte aligned hval
@@ -310,29 +329,32 @@ __device__ __forceinline__ void emit_rows(const HybArgs& A, int ax, bool has, co
 
 template <int DIM>
 struct PencilSmem {
-#if HDR_PENCIL_STAGE
+  struct Args {  // the kernel arguments for the out-of-line exact pass (written only when it runs)
+    HybArgs A;
+    PencilConst<DIM> pc;
+    FastDiv dseg;
+  };
   double2 nbr[kPW][DIM - 1][DIM + 1][32];  // staged inputs of the cells below / behind
   longlong2 fq[kPW][3];                     // {row start, row} of each axis' first row
-#endif
   double stg[kPW][32 * (4 * DIM - 1) + 2];  // a warp's H rows before the coalesced write-out (+ parity pad)
   double xrow[kPW][2 * DIM + 1];            // last lane's x row for the next segment's first lane
+  double xr[kPW][32][2 * DIM + 1];          // exact-path rows (rare), one slot per lane
+  int xkind[kPW];                           // kind of the last lane's cell
+  alignas(16) unsigned char args_raw[kPW][sizeof(Args)];
+  __device__ Args* args_ptr() { return reinterpret_cast<Args*>(args_raw); }
 };
 
-template <int DIM>
-__global__ void __launch_bounds__(kPW * 32, HDR_PENCIL_MINB) k_rt0_pencil(HybArgs A, PencilConst<DIM> pc, FastDiv dseg, uint32_t nwarps) {
+// One warp's segment.  EXACT = false: the fast pass (closed form; a cell that is not
+// accepted contributes zeros and the return value tells that some row of this warp
+// involves such a cell).  EXACT = true: the same segment again with the exact rows of
+// those cells (rare, out of line): it rewrites the warp's rows, now complete.
+template <int DIM, bool EXACT>
+__device__ __forceinline__ bool pencil_warp(const HybArgs& A, const PencilConst<DIM>& pc, FastDiv dseg, uint32_t gw,
+                                            bool wvalid, PencilSmem<DIM>& sm) {
   constexpr int N = 2 * DIM, NC = N + 1;
-  // dynamic shared memory (above the 48 KB static limit with the neighbour slots)
-  extern __shared__ __align__(16) unsigned char pencil_smem[];
-  using Sm = PencilSmem<DIM>;
-  Sm& sm = *reinterpret_cast<Sm*>(pencil_smem);
-  auto& stg = sm.stg;
-  auto& xrow = sm.xrow;
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // the exact-path kernel may launch
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const uint32_t gw = blockIdx.x * kPW + warp;
   const DevMesh& m = A.m;
   const int N0 = static_cast<int>(m.N[0]), N1 = static_cast<int>(m.N[1]), N2 = DIM == 3 ? static_cast<int>(m.N[2]) : 1;
-  const bool wvalid = gw < nwarps;
   const uint32_t line = wvalid ? dseg.div(gw) : 0;  // multiply-shift divisions (32-bit: < 2^31 cells)
   const int seg = wvalid ? static_cast<int>(gw - line * dseg.d) : 0;
   const uint32_t zq = m.div_n1.div(line);
@@ -341,100 +363,129 @@ __global__ void __launch_bounds__(kPW * 32, HDR_PENCIL_MINB) k_rt0_pencil(HybArg
   const bool valid = wvalid && x < N0;
   const int c[3] = {x, y, z}, nc[3] = {N0, N1, N2};
   const int64_t e = x + static_cast<int64_t>(N0) * (y + static_cast<int64_t>(N1) * z);
-  // prefetch: the {row start, row} of each axis' first row (lane `first` of the
-  // group: x rows start at x = 1), and the inputs of the cells below / behind
+  // staged by cp.async (no registers held while the own cell is solved): the {row
+  // start, row} of each axis' first row (by the lane that owns it: x rows start at
+  // x = 1) and the inputs of the cells below / behind
   const int xfirst = seg == 0 ? 1 : 0;
-#if HDR_PENCIL_STAGE
   longlong2* const fqx = &sm.fq[warp][0];
   longlong2* const fqy = &sm.fq[warp][1];
   longlong2* const fqz = &sm.fq[warp][2];
   if (valid && lane == xfirst && x >= 1) cp_async16(fqx, A.frs + face_id32(m, 0, x, y, z));
   if (valid && lane == 0 && y >= 1) cp_async16(fqy, A.frs + face_id32(m, 1, x, y, z));
   if (DIM == 3 && valid && lane == 0 && z >= 1) cp_async16(fqz, A.frs + face_id32(m, 2, x, y, z));
-#else
-  longlong2 fqxv = {0, 0}, fqyv = {0, 0}, fqzv = {0, 0};
-  if (valid && lane == xfirst && x >= 1) fqxv = A.frs[face_id32(m, 0, x, y, z)];
-  if (valid && lane == 0 && y >= 1) fqyv = A.frs[face_id32(m, 1, x, y, z)];
-  if (DIM == 3 && valid && lane == 0 && z >= 1) fqzv = A.frs[face_id32(m, 2, x, y, z)];
-  const longlong2 *fqx = &fqxv, *fqy = &fqyv, *fqz = &fqzv;
-#endif
-#if HDR_PENCIL_STAGE
   auto& nbr = sm.nbr;
   if (valid && y >= 1) stage_cell<DIM>(A, e - N0, &nbr[warp][0][0][lane]);
   if (DIM == 3 && valid && z >= 1) stage_cell<DIM>(A, e - static_cast<int64_t>(N0) * N1, &nbr[warp][DIM - 2][0][lane]);
   asm volatile("cp.async.commit_group;" ::: "memory");
-#else
-  double ya = 1.0, yb = 1.0, yf[N], za = 1.0, zb = 1.0, zf[N];
+  // row r of the cell ec = (ex, ey, ez) of kind `kind` (0 none, 1 closed form, 2 not accepted)
+  auto cell_row = [&](const PencilSol<DIM>& sol, int kind, int64_t ec, int ex, int ey, int ez, int r, double (&h)[NC]) {
+    pencil_row<DIM>(sol, r, h);  // zeros unless kind == 1
+    if (EXACT && kind == 2) {
+      const int cc3[3] = {ex, ey, ez};
+      double* out = sm.xr[warp][lane];
+      pencil_exact_row<DIM>(A.fx.D, A.fx.M, __ldg(A.alpha + ec), __ldg(A.beta + ec), rt0_bmask<DIM>(m, cc3),
+                            A.f + ec * N, r, A.status, out);
 #pragma unroll
-  for (int j = 0; j < N; ++j) yf[j] = zf[j] = 0.0;
-  if (valid && y >= 1) load_cell<DIM>(A.alpha, A.beta, A.f, e - N0, ya, yb, yf);
-  if (DIM == 3 && valid && z >= 1) load_cell<DIM>(A.alpha, A.beta, A.f, e - static_cast<int64_t>(N0) * N1, za, zb, zf);
-#endif
+      for (int q = 0; q < NC; ++q) h[q] = out[q];
+    }
+  };
   PencilSol<DIM> s;
+  int own = 1;
   {
     double a = 1.0, b = 1.0, f[N], cond = 0.0;
 #pragma unroll
     for (int j = 0; j < N; ++j) f[j] = 0.0;
     if (valid) load_cell<DIM>(A.alpha, A.beta, A.f, e, a, b, f);
     const bool ok = pencil_solve<DIM>(pc, a, b, f, s, cond);
-    if (valid && A.qlog) A.qlog[e] = static_cast<float>(cond * 0x1p-53);
+    if (!EXACT && valid && A.qlog) A.qlog[e] = static_cast<float>(cond * 0x1p-53);
     if (!valid || !ok || A.force_exact) {
       pencil_zero<DIM>(s);
-      if (valid) {
-        atomicAdd(A.xcount, 1);
-        A.xlist[atomicAdd(A.xcount + 2, 1)] = static_cast<int>(e);
-      }
+      own = valid ? 2 : 0;
+      if (!EXACT && valid) atomicAdd(A.xcount, 1);  // the count hdr_hybrid_exact_cells reports
     }
   }
-  double* st = stg[warp];
+  bool need = own == 2;
+  double* st = sm.stg[warp];
   double hm[NC], hp[NC];
   // x faces: T- = (x - 1, y, z), its row of slot 1
-  pencil_row<DIM>(s, 1, hp);
-  if (lane == 31) {
+  cell_row(s, own, e, x, y, z, 1, hp);
+  if (!EXACT) {  // the next segment's first lane takes this warp's last row through shared memory
+    if (lane == 31) {
 #pragma unroll
-    for (int q = 0; q < NC; ++q) xrow[warp][q] = hp[q];
+      for (int q = 0; q < NC; ++q) sm.xrow[warp][q] = hp[q];
+      sm.xkind[warp] = own;
+    }
+    __syncthreads();
   }
-  __syncthreads();
 #pragma unroll
   for (int q = 0; q < NC; ++q) hm[q] = __shfl_up_sync(0xffffffffu, hp[q], 1);
+  int kx = __shfl_up_sync(0xffffffffu, own, 1);
   if (lane == 0 && seg > 0 && valid) {
-    if (warp > 0) {  // the previous warp holds the line's previous segment
+    if (!EXACT && warp > 0) {  // the previous warp holds the line's previous segment
 #pragma unroll
-      for (int q = 0; q < NC; ++q) hm[q] = xrow[warp - 1][q];
-    } else {  // the line's previous segment belongs to another CTA: recompute its last cell
+      for (int q = 0; q < NC; ++q) hm[q] = sm.xrow[warp - 1][q];
+      kx = sm.xkind[warp - 1];
+    } else {  // another CTA's (or, in the exact pass, any previous) segment: recompute its last cell
       PencilSol<DIM> sn;
-      neighbour<DIM>(A, pc, e - 1, sn);
-      pencil_row<DIM>(sn, 1, hm);
+      kx = neighbour<DIM>(A, pc, e - 1, sn);
+      cell_row(sn, kx, e - 1, x - 1, y, z, 1, hm);
     }
   }
-  pencil_row<DIM>(s, 0, hp);
-#if HDR_PENCIL_STAGE
+  need = need || (valid && x >= 1 && kx == 2);
+  cell_row(s, own, e, x, y, z, 0, hp);
   asm volatile("cp.async.wait_group 0;" ::: "memory");  // neighbour inputs: own copies; row starts: another lane's
   __syncwarp();
-#endif
   emit_rows<DIM>(A, 0, valid && x >= 1, c, nc, seg * 32, fqx, hm, hp, st);
   // y faces: T- = (x, y - 1, z), slot 3 (line-uniform condition)
   if (y >= 1) {
     PencilSol<DIM> sn;
-#if HDR_PENCIL_STAGE
     double ya, yb, yf[N];
     staged_cell<DIM>(&nbr[warp][0][0][lane], valid, ya, yb, yf);
-#endif
-    solved_neighbour<DIM>(A, pc, valid, ya, yb, yf, sn);
-    pencil_row<DIM>(sn, 3, hm);
-    pencil_row<DIM>(s, 2, hp);
+    const int kn = solved_neighbour<DIM>(A, pc, valid, ya, yb, yf, sn);
+    need = need || kn == 2;
+    cell_row(sn, kn, e - N0, x, y - 1, z, 3, hm);
+    cell_row(s, own, e, x, y, z, 2, hp);
     emit_rows<DIM>(A, 1, valid, c, nc, seg * 32, fqy, hm, hp, st);
   }
   if (DIM == 3 && z >= 1) {  // z faces: T- = (x, y, z - 1), slot 5
     PencilSol<DIM> sn;
-#if HDR_PENCIL_STAGE
     double za, zb, zf[N];
     staged_cell<DIM>(&nbr[warp][DIM - 2][0][lane], valid, za, zb, zf);
-#endif
-    solved_neighbour<DIM>(A, pc, valid, za, zb, zf, sn);
-    pencil_row<DIM>(sn, DIM == 3 ? 5 : 3, hm);
-    pencil_row<DIM>(s, DIM == 3 ? 4 : 2, hp);
+    const int kn = solved_neighbour<DIM>(A, pc, valid, za, zb, zf, sn);
+    need = need || kn == 2;
+    cell_row(sn, kn, e - static_cast<int64_t>(N0) * N1, x, y, z - 1, DIM == 3 ? 5 : 3, hm);
+    cell_row(s, own, e, x, y, z, DIM == 3 ? 4 : 2, hp);
     emit_rows<DIM>(A, 2, valid, c, nc, seg * 32, fqz, hm, hp, st);
+  }
+  return need;
+}
+
+// the exact pass of one warp, out of line: its arguments come through shared memory,
+// so the fast pass keeps its registers and the kernel parameters stay in the constant bank
+template <int DIM>
+__device__ __noinline__ void pencil_warp_exact(PencilSmem<DIM>* sm, uint32_t gw) {
+  const typename PencilSmem<DIM>::Args& ar = sm->args_ptr()[threadIdx.x >> 5];
+  pencil_warp<DIM, true>(ar.A, ar.pc, ar.dseg, gw, true, *sm);
+}
+
+template <int DIM>
+__global__ void __launch_bounds__(kPW * 32, HDR_PENCIL_MINB) k_rt0_pencil(HybArgs A, PencilConst<DIM> pc, FastDiv dseg, uint32_t nwarps) {
+  // dynamic shared memory (above the 48 KB static limit with the neighbour slots)
+  extern __shared__ __align__(16) unsigned char pencil_smem[];
+  using Sm = PencilSmem<DIM>;
+  Sm& sm = *reinterpret_cast<Sm*>(pencil_smem);
+  const int warp = threadIdx.x >> 5;
+  const uint32_t gw = blockIdx.x * kPW + warp;
+  const bool need = pencil_warp<DIM, false>(A, pc, dseg, gw, gw < nwarps, sm);
+  if (__any_sync(0xffffffffu, need)) {  // rare: a row of this warp involves a cell the closed form rejected
+    typename Sm::Args& ar = sm.args_ptr()[warp];
+    if ((threadIdx.x & 31) == 0) {
+      ar.A = A;
+      ar.pc = pc;
+      ar.dseg = dseg;
+    }
+    __syncwarp();
+    pencil_warp_exact<DIM>(&sm, gw);
   }
 }
 
