@@ -320,8 +320,11 @@ struct ScWarpSm {
   int rank[NS * NS];     // column-block rank of face slot qs in the rows of slot ps
 };
 
+#ifndef HDR_SC_MINB
+#define HDR_SC_MINB 4  // CTAs (of 4 warps) per SM asked of ptxas
+#endif
 template <int DIM, int NI, int NF>
-__global__ void __launch_bounds__(128, 4) k_sc_warp(CondArgs C, int parity) {
+__global__ void __launch_bounds__(128, HDR_SC_MINB) k_sc_warp(CondArgs C, int parity) {
   using SM = ScWarpSm<DIM, NI, NF>;
   constexpr int N = NI + NF, NC = SM::NC, NS = SM::NS, DPF = NF / NS;
   constexpr unsigned FULL = 0xffffffffu;
