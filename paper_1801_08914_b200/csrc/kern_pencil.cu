@@ -344,6 +344,24 @@ struct PencilSmem {
   __device__ Args* args_ptr() { return reinterpret_cast<Args*>(args_raw); }
 };
 
+// row R of the cell ec = (ex, ey, ez) of kind `kind` (0 none, 1 closed form, 2 not
+// accepted): the closed-form row (zeros unless kind == 1), or, in the exact pass, the
+// double-double row of a cell that was not accepted
+template <int DIM, bool EXACT, int R>
+__device__ __forceinline__ void cell_row(const HybArgs& A, PencilSmem<DIM>& sm, const PencilSol<DIM>& sol, int kind,
+                                         int64_t ec, int ex, int ey, int ez, double (&h)[2 * DIM + 1]) {
+  constexpr int N = 2 * DIM, NC = N + 1;
+  pencil_row<DIM>(sol, R, h);
+  if (EXACT && kind == 2) {
+    const int cc3[3] = {ex, ey, ez};
+    double* out = sm.xr[threadIdx.x >> 5][threadIdx.x & 31];
+    pencil_exact_row<DIM>(A.fx.D, A.fx.M, __ldg(A.alpha + ec), __ldg(A.beta + ec), rt0_bmask<DIM>(A.m, cc3),
+                          A.f + ec * N, R, A.status, out);
+#pragma unroll
+    for (int q = 0; q < NC; ++q) h[q] = out[q];
+  }
+}
+
 // One warp's segment.  EXACT = false: the fast pass (closed form; a cell that is not
 // accepted contributes zeros and the return value tells that some row of this warp
 // involves such a cell).  EXACT = true: the same segment again with the exact rows of
@@ -377,18 +395,6 @@ __device__ __forceinline__ bool pencil_warp(const HybArgs& A, const PencilConst<
   if (valid && y >= 1) stage_cell<DIM>(A, e - N0, &nbr[warp][0][0][lane]);
   if (DIM == 3 && valid && z >= 1) stage_cell<DIM>(A, e - static_cast<int64_t>(N0) * N1, &nbr[warp][DIM - 2][0][lane]);
   asm volatile("cp.async.commit_group;" ::: "memory");
-  // row r of the cell ec = (ex, ey, ez) of kind `kind` (0 none, 1 closed form, 2 not accepted)
-  auto cell_row = [&](const PencilSol<DIM>& sol, int kind, int64_t ec, int ex, int ey, int ez, int r, double (&h)[NC]) {
-    pencil_row<DIM>(sol, r, h);  // zeros unless kind == 1
-    if (EXACT && kind == 2) {
-      const int cc3[3] = {ex, ey, ez};
-      double* out = sm.xr[warp][lane];
-      pencil_exact_row<DIM>(A.fx.D, A.fx.M, __ldg(A.alpha + ec), __ldg(A.beta + ec), rt0_bmask<DIM>(m, cc3),
-                            A.f + ec * N, r, A.status, out);
-#pragma unroll
-      for (int q = 0; q < NC; ++q) h[q] = out[q];
-    }
-  };
   PencilSol<DIM> s;
   int own = 1;
   {
@@ -408,7 +414,7 @@ __device__ __forceinline__ bool pencil_warp(const HybArgs& A, const PencilConst<
   double* st = sm.stg[warp];
   double hm[NC], hp[NC];
   // x faces: T- = (x - 1, y, z), its row of slot 1
-  cell_row(s, own, e, x, y, z, 1, hp);
+  cell_row<DIM, EXACT, 1>(A, sm, s, own, e, x, y, z, hp);
   if (!EXACT) {  // the next segment's first lane takes this warp's last row through shared memory
     if (lane == 31) {
 #pragma unroll
@@ -428,11 +434,11 @@ __device__ __forceinline__ bool pencil_warp(const HybArgs& A, const PencilConst<
     } else {  // another CTA's (or, in the exact pass, any previous) segment: recompute its last cell
       PencilSol<DIM> sn;
       kx = neighbour<DIM>(A, pc, e - 1, sn);
-      cell_row(sn, kx, e - 1, x - 1, y, z, 1, hm);
+      cell_row<DIM, EXACT, 1>(A, sm, sn, kx, e - 1, x - 1, y, z, hm);
     }
   }
   need = need || (valid && x >= 1 && kx == 2);
-  cell_row(s, own, e, x, y, z, 0, hp);
+  cell_row<DIM, EXACT, 0>(A, sm, s, own, e, x, y, z, hp);
   asm volatile("cp.async.wait_group 0;" ::: "memory");  // neighbour inputs: own copies; row starts: another lane's
   __syncwarp();
   emit_rows<DIM>(A, 0, valid && x >= 1, c, nc, seg * 32, fqx, hm, hp, st);
@@ -443,8 +449,8 @@ __device__ __forceinline__ bool pencil_warp(const HybArgs& A, const PencilConst<
     staged_cell<DIM>(&nbr[warp][0][0][lane], valid, ya, yb, yf);
     const int kn = solved_neighbour<DIM>(A, pc, valid, ya, yb, yf, sn);
     need = need || kn == 2;
-    cell_row(sn, kn, e - N0, x, y - 1, z, 3, hm);
-    cell_row(s, own, e, x, y, z, 2, hp);
+    cell_row<DIM, EXACT, 3>(A, sm, sn, kn, e - N0, x, y - 1, z, hm);
+    cell_row<DIM, EXACT, 2>(A, sm, s, own, e, x, y, z, hp);
     emit_rows<DIM>(A, 1, valid, c, nc, seg * 32, fqy, hm, hp, st);
   }
   if (DIM == 3 && z >= 1) {  // z faces: T- = (x, y, z - 1), slot 5
@@ -453,8 +459,8 @@ __device__ __forceinline__ bool pencil_warp(const HybArgs& A, const PencilConst<
     staged_cell<DIM>(&nbr[warp][DIM - 2][0][lane], valid, za, zb, zf);
     const int kn = solved_neighbour<DIM>(A, pc, valid, za, zb, zf, sn);
     need = need || kn == 2;
-    cell_row(sn, kn, e - static_cast<int64_t>(N0) * N1, x, y, z - 1, DIM == 3 ? 5 : 3, hm);
-    cell_row(s, own, e, x, y, z, DIM == 3 ? 4 : 2, hp);
+    cell_row<DIM, EXACT, DIM == 3 ? 5 : 3>(A, sm, sn, kn, e - static_cast<int64_t>(N0) * N1, x, y, z - 1, hm);
+    cell_row<DIM, EXACT, DIM == 3 ? 4 : 2>(A, sm, s, own, e, x, y, z, hp);
     emit_rows<DIM>(A, 2, valid, c, nc, seg * 32, fqz, hm, hp, st);
   }
   return need;
