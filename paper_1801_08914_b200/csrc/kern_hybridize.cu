@@ -1129,6 +1129,149 @@ __global__ void __launch_bounds__(kNT) k_recover_cta(RecArgs R, double* gws, int
   }
 }
 
+// Long rows (RT2 / RT3 hexahedra): CB cells per CTA.  The fixed factors (N0, X and the
+// Delta inputs D, M, E, Ma: 1.8 MB for RT3, far beyond L1) are streamed from L2 once per
+// CTA pass and applied to all CB cells (each cell its own alpha, beta, order), which
+// divides the L2 traffic that bounds the one-cell form by CB.  Per cell the arithmetic
+// and the summation order are those of k_recover_cta (warp per row, lanes along the row).
+template <int CB>
+__global__ void __launch_bounds__(kNT) k_recover_wide(RecArgs R) {
+  extern __shared__ double smem[];
+  constexpr int CELL = 64 + 3 * kMaxN + 64;  // s, y, t, acc, xty of one cell
+  const DevMesh& m = R.m;
+  const int n = m.n, r = R.fx.r, dpf = m.dpf, nint = m.nint;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  __shared__ double sa[CB], sb[CB], sib[CB];
+  __shared__ int sP[CB];  // the cell's Neumann order, -1: no cell / sent to the exact path
+  auto S = [&](int c) { return smem + c * CELL; };
+  auto Y = [&](int c) { return smem + c * CELL + 64; };
+  auto T = [&](int c) { return smem + c * CELL + 64 + kMaxN; };
+  auto ACC = [&](int c) { return smem + c * CELL + 64 + 2 * kMaxN; };
+  auto XTY = [&](int c) { return smem + c * CELL + 64 + 3 * kMaxN; };
+  const int64_t ncb = (m.ncells + CB - 1) / CB;
+  for (int64_t cb = blockIdx.x; cb < ncb; cb += gridDim.x) {
+    if (threadIdx.x < CB) {
+      const int c = threadIdx.x;
+      const int64_t e = cb * CB + c;
+      int P = -1;
+      double a = 1.0, b = 1.0;
+      if (e < m.ncells) {
+        a = R.alpha[e], b = R.beta[e];
+        bool exact = false;
+        P = struct_order_apriori(R.fx.rho * a / b, R.p_max, exact);
+        if (exact || R.force_exact) {  // x_hat of this cell from the exact path (kern_exact.cu)
+          exact_push(R.xlist, R.xcount, static_cast<int>(e));
+          P = -1;
+        }
+      }
+      sa[c] = a, sb[c] = b, sib[c] = 1.0 / b, sP[c] = P;
+    }
+    __syncthreads();
+    int Pm = -1;
+#pragma unroll
+    for (int c = 0; c < CB; ++c) Pm = max(Pm, sP[c]);
+    if (Pm < 0) {
+      __syncthreads();
+      continue;
+    }
+    for (int c = 0; c < CB; ++c) {
+      const int64_t e = cb * CB + c;
+      const bool live = e < m.ncells;
+      const double a = sa[c], b = sb[c];
+      int64_t cc[3] = {0, 0, 0};
+      if (live) cell_coords(m, e, cc);
+      for (int j = threadIdx.x; j < r; j += blockDim.x) S(c)[j] = b / fma(a, __ldg(R.fx.lam + j), b);
+      for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        double v = 0.0;
+        if (live) {
+          v = R.f[e * n + i];
+          if (i >= nint) {
+            const int p = (i - nint) / dpf, sub = (i - nint) - p * dpf;
+            bool in;
+            const int64_t f = slot_face(m, cc, p, &in);
+            if (in) v -= R.lambda[R.mbase[f] + sub];  // unit constraint rows: C_T^T lambda
+          }
+        }
+        Y(c)[i] = v;
+      }
+    }
+    __syncthreads();
+    for (int p = 0; p <= Pm; ++p) {
+      // t = A0^-1 y = (N0 y + X diag(s) X^T y) / beta
+      for (int j = warp; j < r; j += nw) {
+        double u[CB];
+#pragma unroll
+        for (int c = 0; c < CB; ++c) u[c] = 0.0;
+        for (int l = lane; l < n; l += 32) {
+          const double xv = __ldg(R.fx.X + static_cast<int64_t>(l) * r + j);
+#pragma unroll
+          for (int c = 0; c < CB; ++c) u[c] = fma(xv, Y(c)[l], u[c]);
+        }
+#pragma unroll
+        for (int c = 0; c < CB; ++c) {
+          const double w = warp_sum(u[c]);
+          if (lane == 0) XTY(c)[j] = w * S(c)[j];
+        }
+      }
+      __syncthreads();
+      for (int i = warp; i < n; i += nw) {
+        const double* row = R.fx.N0 + static_cast<int64_t>(i) * n;
+        double u[CB];
+#pragma unroll
+        for (int c = 0; c < CB; ++c) u[c] = 0.0;
+        for (int l = lane; l < n; l += 32) {
+          const double nv = __ldg(row + l);
+#pragma unroll
+          for (int c = 0; c < CB; ++c) u[c] = fma(nv, Y(c)[l], u[c]);
+        }
+        for (int j = lane; j < r; j += 32) {
+          const double xv = __ldg(R.fx.X + static_cast<int64_t>(i) * r + j);
+#pragma unroll
+          for (int c = 0; c < CB; ++c) u[c] = fma(xv, XTY(c)[j], u[c]);
+        }
+#pragma unroll
+        for (int c = 0; c < CB; ++c) {
+          double w = warp_sum(u[c]);
+          if (lane == 0 && p <= sP[c]) {
+            w *= sib[c];
+            T(c)[i] = w;
+            ACC(c)[i] = (p == 0) ? w : ((p & 1) ? ACC(c)[i] - w : ACC(c)[i] + w);
+          }
+        }
+      }
+      __syncthreads();
+      if (p == Pm) break;
+      // y = Delta t (Delta's inputs loaded once for the CB cells)
+      double ca[CB], cbeta[CB];
+#pragma unroll
+      for (int c = 0; c < CB; ++c) ca[c] = sa[c], cbeta[c] = sb[c];
+      for (int i = warp; i < n; i += nw) {
+        double u[CB];
+#pragma unroll
+        for (int c = 0; c < CB; ++c) u[c] = 0.0;
+        for (int l = lane; l < n; l += 32) {
+          const int64_t o = static_cast<int64_t>(i) * n + l;
+          const double d = __ldg(R.fx.D + o), mm = __ldg(R.fx.M + o), ee = __ldg(R.fx.E + o), ma = __ldg(R.fx.Ma + o);
+#pragma unroll
+          for (int c = 0; c < CB; ++c) u[c] = fma(delta_entry(ca[c], cbeta[c], d, mm, ee, ma), T(c)[l], u[c]);
+        }
+#pragma unroll
+        for (int c = 0; c < CB; ++c) {
+          const double w = warp_sum(u[c]);
+          if (lane == 0) Y(c)[i] = w;
+        }
+      }
+      __syncthreads();
+    }
+    for (int c = 0; c < CB; ++c) {
+      if (sP[c] < 0) continue;
+      const int64_t e = cb * CB + c;
+      for (int i = threadIdx.x; i < n; i += blockDim.x) R.x_hat[e * n + i] = ACC(c)[i];
+    }
+    __syncthreads();
+  }
+}
+
 // k = 0 recovery, one thread per cell: x_hat = A_T^-1 r, r = f - C_T^T lambda,
 // by the structured solve in fp64 (A0^-1 = (N0 + s X X^T) / beta, Neumann
 // terms with the exact rounding errors Delta; order from the a-priori bound
@@ -1408,6 +1551,20 @@ void launch_recover_hybrid(const RecArgs& a, double* gws, int64_t ws_doubles, cu
   // long rows: 128 threads (warp per row); short rows: four lanes per row, two thirds of the
   // rows per pass (measured on 48^3 RT1, n = 36: 32 / 64 / 96 / 128 / 160 threads ->
   // 1.22 / 0.92 / 0.89 / 1.00 / 0.99 ms)
+  if (a.m.n > 64 && !getenv("HDR_REC_ONE_CELL")) {  // long rows: CB cells per CTA share each pass over the factors
+    auto go = [&](auto cbc) {
+      constexpr int CB = decltype(cbc)::value;
+      const size_t smem_w = static_cast<size_t>(CB) * (64 + 3 * kMaxN + 64) * 8;
+      cudaFuncSetAttribute(k_recover_wide<CB>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_w));
+      const int64_t ncb = (a.m.ncells + CB - 1) / CB;
+      k_recover_wide<CB><<<static_cast<unsigned>(std::min<int64_t>(ncb, 148 * 8)), kNT, smem_w, st>>>(a);
+    };
+    // measured on 32^3 RT3 (cfg5): one cell per CTA 22.7 ms, four 12.8 ms, eight 11.2 ms
+    if (getenv("HDR_REC_CB4")) go(std::integral_constant<int, 4>{});
+    else go(std::integral_constant<int, 8>{});
+    count_launch();
+    return;
+  }
   int threads = a.m.n > 64 ? 128 : std::min(256, ((8 * a.m.n / 3 + 31) / 32) * 32);
   if (const char* ev = getenv("HDR_REC_THREADS")) threads = atoi(ev);  // A/B timing
   k_recover_cta<<<static_cast<unsigned>(grid), threads, smem, st>>>(a, nullptr, 0, 1);
