@@ -28,7 +28,14 @@ __global__ void k_spmv_rows(int64_t nrows, const int64_t* __restrict__ ro, const
 // adds the products of row i that fall in the tile, sequentially in storage order
 // (the reference's sum, starting from 0.0).  HBM sees full sectors once instead of
 // 32 strided streams; x is gathered through L1 / L2.
-constexpr int kSpmvTile = 1024;  // products per warp tile (8 KB)
+#ifndef HDR_SPMV_TILE
+#define HDR_SPMV_TILE 256   // measured (cfg3 / cfg5 ms): 1024x4 0.229 / 1.194, 512x8 0.288 / 1.182, 256x8 0.206 / 1.171, 1024x8 0.212 / 1.166
+#endif
+#ifndef HDR_SPMV_UNROLL
+#define HDR_SPMV_UNROLL 8
+#endif
+constexpr int kSpmvTile = HDR_SPMV_TILE;  // products per warp tile (8 bytes each; tile x unroll of the load loop)
+constexpr int kSpmvUnroll = HDR_SPMV_UNROLL;
 
 template <class Col>
 __global__ void __launch_bounds__(128) k_spmv_tiled(int64_t nrows, const int64_t* __restrict__ ro,
@@ -50,7 +57,7 @@ __global__ void __launch_bounds__(128) k_spmv_tiled(int64_t nrows, const int64_t
   double s = 0.0;
   for (int t0 = 0; t0 < span; t0 += kSpmvTile) {
     const int t1 = min(t0 + kSpmvTile, span);
-#pragma unroll 4
+#pragma unroll kSpmvUnroll
     for (int q = t0 + lane; q < t1; q += 32) P[q - t0] = __dmul_rn(vs[q], x[cs[q]]);
     __syncwarp();
     const int a = max(rb, t0), b = min(re, t1);
