@@ -40,7 +40,8 @@
 // consecutive lanes are consecutive rows of H (interior faces of one line, face
 // order), so a warp stages its rows in shared memory and writes them out as one
 // contiguous, coalesced segment.  No staging in HBM, no colouring, one launch; every
-// H entry and g entry is written exactly once; the two contributions to a diagonal
+// H entry and g entry is written exactly once (once more, complete, by the exact pass
+// of a warp whose rows involve a rejected cell); the two contributions to a diagonal
 // entry / g entry meet as fl(h(T-) + h(T+)), the reference's two-term sum.
 #include "hdr_device.cuh"
 #include "kernels.hpp"
