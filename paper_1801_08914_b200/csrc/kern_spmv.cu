@@ -17,7 +17,18 @@ __global__ void k_spmv_rows(int64_t nrows, const int64_t* __restrict__ ro, const
   if (i >= nrows) return;
   double s = 0.0;
   const int64_t end = ro[i + 1];
+#ifdef HDR_SPMV_ROWS_PLAIN
   for (int64_t k = ro[i]; k < end; ++k) s = __dadd_rn(s, __dmul_rn(v[k], x[ci[k]]));
+#else
+  // four products in flight (independent loads), added in storage order
+  int64_t k = ro[i];
+  for (; k + 4 <= end; k += 4) {
+    const double p0 = __dmul_rn(v[k], x[ci[k]]), p1 = __dmul_rn(v[k + 1], x[ci[k + 1]]);
+    const double p2 = __dmul_rn(v[k + 2], x[ci[k + 2]]), p3 = __dmul_rn(v[k + 3], x[ci[k + 3]]);
+    s = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(s, p0), p1), p2), p3);
+  }
+  for (; k < end; ++k) s = __dadd_rn(s, __dmul_rn(v[k], x[ci[k]]));
+#endif
   y[i] = s;
 }
 
@@ -69,8 +80,8 @@ __global__ void __launch_bounds__(128) k_spmv_tiled(int64_t nrows, const int64_t
 
 }  // namespace
 
-// measured on the B200 (10 steps, L2 flushed): 11 entries per row 64 vs 49 us (tile vs rows),
-// 44 per row 229 vs 244 us, ~550 per row 1.23 vs 1.71 ms
+// measured on the B200 (10 steps, L2 flushed; tiles vs thread per row): 11 entries per row
+// 64 vs 49 us, 44 per row 0.207 vs 0.244 ms, ~550 per row 1.17 vs 1.71 ms
 static bool use_tiles(int64_t nrows, int64_t nnz) {
   if (getenv("HDR_SPMV_ROWS")) return false;
   if (getenv("HDR_SPMV_TILES")) return true;
